@@ -1,0 +1,264 @@
+"""Pins of the CPU oracle to things other than itself (no GPU).
+
+Each pin cites the passage that fixes the value: SPEC.md hand values (relabelled
+to the 20-letter alphabet where SPEC used B/X), the SURVEY worked example
+(tests/golden), closed forms of sum-min, invariants of the method, and a Python
+brute force (tests/bruteforce.py: Counter + Fraction) on small random inputs.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import gen
+from tests import bruteforce as bf
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ---------------------------------------------------------------- counts (O2)
+
+def test_counts_hand_values():
+    # SPEC.md:153 "AAAA", k=2 -> {AA: 3}
+    assert oracle.count("AAAA", 2) == {"AA": 3}
+    # SPEC.md:154 "ACGT", k=4 -> {ACGT: 1}
+    assert oracle.count("ACGT", 4) == {"ACGT": 1}
+    # SPEC.md:155 "ABCAB", k=2 -> {AB:2, BC:1, CA:1}; relabelled B->D (SURVEY §8(c) pins)
+    assert oracle.count("ADCAD", 2) == {"AD": 2, "DC": 1, "CA": 1}
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 6])
+def test_counts_vs_bruteforce_and_total(k):
+    rng = np.random.default_rng(10 + k)
+    for _ in range(40):
+        L = int(rng.integers(k, 60))
+        x = "".join(rng.choice(list("ACDEFGHIKLMNPQRSTVWY"), L))
+        c = oracle.count(x, k)
+        assert c == dict(bf.kmers(x, k))
+        assert sum(c.values()) == L - k + 1          # SPEC.md:136 invariant: sum of counts == L-k+1
+
+
+# ---------------------------------------------------------------- similarity (O4)
+
+def test_similarity_hand_values():
+    # SPEC.md:162 x == y == "ACGTACGT", k=3 -> 1.0
+    S, d = oracle.pair("ACGTACGT", "ACGTACGT", 3)
+    assert S == d == 6
+    # SPEC.md:163 "AAAA" vs "CCCC", k=2 -> 0
+    assert oracle.pair("AAAA", "CCCC", 2) == (0, 3)
+    # SPEC.md:164 "ABCAB" vs "BCABX" -> 3/4 (relabelled B->D, X->W)
+    assert oracle.pair("ADCAD", "DCADW", 2) == (3, 4)
+    # SURVEY §8(c) brute-forced values: repeated k-mers, F = 1 without identity, DNA k=6
+    assert oracle.pair("ACACAC", "CACACA", 2) == (4, 5)
+    assert oracle.pair("AAAAC", "AAC", 2) == (2, 2)
+    assert oracle.pair("ACGTACGTAC", "TTACGTACGG", 6) == (3, 5)
+
+
+def test_fixed_point_values():
+    # q = floor(2^32 S / den) (reading A5); closed forms: 3/4 = 3*2^30, etc.
+    assert oracle.q(3, 4) == 3 * 2 ** 30 == 3221225472
+    assert oracle.q(4, 5) == 3435973836
+    assert oracle.q(3, 5) == 2576980377
+    assert oracle.q(2, 5) == 1717986918
+    assert oracle.q(1, 3) == 1431655765
+    assert oracle.q(3, 5) + oracle.q(2, 5) == 2 ** 32 - 1      # floors truncate each term
+    assert oracle.q(7, 7) == 2 ** 32 and oracle.q(0, 9) == 0
+    # exact over a grid: q*den <= S*2^32 < (q+1)*den
+    for den in (1, 2, 3, 7, 255, 256, 4097, 7995, 65535):
+        for S in sorted({0, 1, den // 3, den // 2, den - 1, den}):
+            qq = oracle.q(S, den)
+            assert qq * den <= S << 32 < (qq + 1) * den
+
+
+def test_rank_R_values():
+    # ln(0.1+0.9) = 0, ln 0.1, ln 1.1 (natural log, reading A4)
+    assert oracle.rank_R(0.9) == pytest.approx(0.0, abs=1e-15)
+    assert oracle.rank_R(0.0) == pytest.approx(math.log(0.1))
+    assert oracle.rank_R(1.0) == pytest.approx(0.0953101798, abs=1e-10)
+
+
+def test_similarity_closed_forms_and_invariants():
+    """sum_tau min(a,b) == sum_t [a>=t][b>=t] (A.1) == (sum a + sum b - sum|a-b|)/2 (A.2),
+    computed from the oracle's COUNT output and compared with its PAIR output."""
+    rng = np.random.default_rng(7)
+    for alpha, letters in (("protein", "ACDEFGHIKLMNPQRSTVWY"), ("dna", "ACGT")):
+        for k in (2, 3, 6):
+            for _ in range(25):
+                x = "".join(rng.choice(list(letters), int(rng.integers(k, 60))))
+                y = "".join(rng.choice(list(letters), int(rng.integers(k, 60))))
+                if rng.random() < 0.3:          # related pair
+                    y = x[int(rng.integers(0, 5)):] + y[:5]
+                    if len(y) < k:
+                        y = x
+                cx, cy = oracle.count(x, k), oracle.count(y, k)
+                S, den = oracle.pair(x, y, k)
+                keys = set(cx) | set(cy)
+                a1 = sum(1 for t in keys for l in range(1, 70)
+                         if cx.get(t, 0) >= l and cy.get(t, 0) >= l)
+                a2 = (sum(cx.values()) + sum(cy.values()) - sum(abs(cx.get(t, 0) - cy.get(t, 0)) for t in keys))
+                assert a2 % 2 == 0
+                assert S == a1 == a2 // 2
+                assert den == min(len(x), len(y)) - k + 1
+                assert 0 <= S <= den                               # 0 <= F <= 1
+                assert oracle.pair(y, x, k) == (S, den)           # symmetry
+                assert oracle.pair(x, x, k) == (len(x) - k + 1,) * 2   # F(x,x) = 1
+                assert S == bf.S(x, y, k)
+
+
+# ---------------------------------------------------------------- the worked example
+
+def _golden(name):
+    seqs, kv, buckets = [], {}, []
+    with open(os.path.join(GOLDEN, name)) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            tok = line.split()
+            if tok[0] == "seq":
+                seqs.append(tok[2])
+            elif tok[0] == "bucket":
+                buckets.append([int(t) for t in tok[2:]])
+            else:
+                kv[tok[0]] = tok[1:]
+    return seqs, kv, buckets
+
+
+def test_worked_example():
+    seqs, kv, buckets = _golden("worked_example_k2_dna.txt")
+    k, p = int(kv["k"][0]), int(kv["p"][0])
+    a, o = gen.from_strings(seqs)
+    r = oracle.run(a, o, kv["alphabet"][0], k, p)
+    assert [int(t) - 2 ** 32 for t in r.T] == [int(v) for v in kv["T_minus_2p32"]]
+    assert r.anc.tolist() == [int(v) for v in kv["ancestors"]]
+    assert r.ga == int(kv["ga"][0])
+    assert r.S.tolist() == [int(v) for v in kv["rank_S"]]
+    assert r.den.tolist() == [int(v) for v in kv["rank_den"]]
+    assert r.sorted.tolist() == [int(v) for v in kv["sorted"]]
+    assert r.samples.tolist() == [int(v) for v in kv["samples"]]
+    assert r.pivots.tolist() == [int(v) for v in kv["pivots"]]
+    assert r.buckets() == buckets
+    # and the brute force agrees
+    b = bf.pipeline(seqs, k, p)
+    assert b["buckets"] == buckets and b["ga"] == r.ga
+
+
+# ---------------------------------------------------------------- whole pipeline vs brute force
+
+@pytest.mark.parametrize("alpha,k", [("protein", 2), ("protein", 3), ("dna", 2), ("dna", 6), ("dna", 3)])
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+def test_pipeline_vs_bruteforce(alpha, k, p):
+    rng = np.random.default_rng(1000 * p + 10 * k + len(alpha))
+    for trial in range(3):
+        n = int(rng.integers(p * p, max(p * p + 1, 64) + 1))
+        if trial == 0:
+            a, o = gen.random_set(rng, n, alpha, k, 60)
+        else:   # related families (more ties, more repeated k-mers)
+            spec = gen.Spec("t", n, alpha, k, p, 2, "equal", 0.0, ("normal", 30, 10, max(k, 8), 60),
+                            (0.05, 0.3), 0.05, int(rng.integers(1 << 30)))
+            a, o = gen.generate(spec)
+        seqs = gen.to_strings(a, o)
+        r = oracle.run(a, o, alpha, k, p)
+        b = bf.pipeline(seqs, k, p)
+        assert [int(t) for t in r.T] == b["T"]
+        assert r.anc.tolist() == b["anc"]
+        assert r.ga == b["ga"]
+        assert [oracle.q(int(s), int(d)) for s, d in zip(r.S, r.den)] == [bf.fixed(f) for f in b["f"]]
+        assert all(int(s) * f.denominator == f.numerator * int(d) for s, d, f in zip(r.S, r.den, b["f"]))
+        assert r.sorted.tolist() == b["sorted"]
+        assert r.samples.tolist() == b["samples"]
+        assert r.pivots.tolist() == b["pivots"]
+        assert r.bucket.tolist() == b["bucket"]
+        assert r.buckets() == b["buckets"]
+
+
+# ---------------------------------------------------------------- invariants (north star)
+
+def _check_invariants(r, n, p):
+    flat = [i for bk in r.buckets() for i in bk]
+    assert sorted(flat) == list(range(n))                         # permutation of the input
+    assert int(r.bsize.sum()) == n
+    key = lambda i: (int(r.S[i]), int(r.den[i]), i)
+    less = lambda a, b: (a[0] * b[1], a[2]) < (b[0] * a[1], b[2])
+    for bk in r.buckets():
+        for u, v in zip(bk, bk[1:]):
+            assert less(key(u), key(v))                           # each bucket sorted
+    nonempty = [bk for bk in r.buckets() if bk]
+    for b1, b2 in zip(nonempty, nonempty[1:]):
+        assert less(key(b1[-1]), key(b2[0]))                      # max(b) < min(b+1)
+
+
+def test_invariants_configs_1_2():
+    for c in (1, 2):
+        spec = gen.SPECS[c]
+        a, o = gen.generate(c)
+        r = oracle.run(a, o, spec.alphabet, spec.k, spec.p)
+        n = len(o) - 1
+        _check_invariants(r, n, spec.p)
+        w = n // spec.p
+        assert r.bsize.max() <= 2 * w + spec.p
+
+
+def test_p1_single_bucket_is_sorted_input():
+    a, o = gen.generate(1)
+    r = oracle.run(a, o, "protein", 3, 1)
+    assert r.pivots.size == 0 and r.bsize.tolist() == [64]
+    assert r.buckets()[0] == r.sorted.tolist()
+    assert r.anc[0] == r.ga
+
+
+def test_adversarial_inputs():
+    # poly-A (counts far above any cap), L == k, identical sequences (all ties -> index order),
+    # containment (F = 1 without identity)
+    seqs = ["A" * 300, "A" * 3, "ACD", "ACDEFGHIK" * 10, "ACDEFGHIK" * 10, "ACDEFGHIK" * 10,
+            "AAAAAAAAAC", "AAC", "W" * 40, "ACDEFGHIK" * 3, "KIHGFEDCA" * 4, "MMMMMMMMMMMMMM"]
+    a, o = gen.from_strings(seqs)
+    for p in (1, 2, 3):
+        r = oracle.run(a, o, "protein", 3, p)
+        b = bf.pipeline(seqs, 3, p)
+        assert r.buckets() == b["buckets"] and [int(t) for t in r.T] == b["T"]
+        _check_invariants(r, len(seqs), p)
+    same = ["ACDEFGHIKL"] * 16
+    a, o = gen.from_strings(same)
+    r = oracle.run(a, o, "protein", 3, 4)
+    assert r.ga == 0 and r.anc.tolist() == [0, 4, 8, 12]
+    assert [i for bk in r.buckets() for i in bk] == list(range(16))
+
+
+def test_errors():
+    a, o = gen.from_strings(["ACDX", "ACDE"])                     # X rejected (reading A18)
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.run(a, o, "protein", 3, 1)
+    assert e.value.name == "SYMBOL" and (e.value.idx, e.value.pos) == (0, 3)
+    a, o = gen.from_strings(["ACDE", "AC"])                       # L < k (reading A19)
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.run(a, o, "protein", 3, 1)
+    assert e.value.name == "TOO_SHORT" and e.value.idx == 1
+    a, o = gen.from_strings(["ACDE"] * 5)                         # w < p (reading A16)
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.run(a, o, "protein", 3, 3)
+    assert e.value.name == "INSUFFICIENT"
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.run(np.zeros(0, np.uint8), np.zeros(1, np.int64), "protein", 3, 1)
+    assert e.value.name == "EMPTY"
+
+
+# ---------------------------------------------------------------- PSRS load bound
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_psrs_load_bound_trials(p):
+    """n = 4 p^3 short random DNA sequences (heavy rank ties), 70 seeded rounds per p
+    (210 in total, SPEC.md:733 asks >= 200): every bucket <= 2w + p, and < 2w when
+    p | w (the paper's "always less than 2w", PAPER.md:188,
+    is read as reading A23)."""
+    n = 4 * p ** 3
+    w = n // p
+    rng = np.random.default_rng(p)
+    for _ in range(70):
+        a, o = gen.random_set(rng, n, "dna", 2, 9)
+        r = oracle.run(a, o, "dna", 2, p)
+        assert r.bsize.sum() == n
+        assert r.bsize.max() <= 2 * w + p
+        assert r.bsize.max() < 2 * w                                # p | w here
