@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""bench.py — one step = the whole hot path over one batch.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--kernel tc|alu]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+    python bench.py --impl reference ...      # the CPU oracle arm (rank 0 only)
+
+Workload (N=1): BASELINE.json configs[3] ("config 4": N = 100,000 synthetic protein
+sequences, k = 3, p = 8 shards/buckets), the largest config the metric is quoted on
+that fits one GPU; at N > 1 the same 8 shards are spread over N GPUs (strong scaling,
+p = 8 fixed, bit-identical output).
+
+Prints ONE JSON line on rank 0 (see the bench contract in DESIGN.md §7).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pairwise k-mer similarities/s (whole rank+partition step)"
+UNIT = "pairs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--p", type=int, default=None)
+    ap.add_argument("--kernel", default="tc", choices=["tc", "alu"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def workload_name(spec, p):
+    return (f"{spec.name}: N={spec.n} {spec.alphabet} k={spec.k} p={p}, {spec.n_families} families "
+            f"({spec.family_sizes}), roots {spec.root_len}, sub U{spec.sub}, indel {spec.indel}, seed {spec.seed}")
+
+
+def total_pairs(n, p):
+    from synth import gen
+    sb = gen.shard_bounds(n, p)
+    return sum((sb[s + 1] - sb[s]) * (sb[s + 1] - sb[s] - 1) // 2 for s in range(p))
+
+
+# ----------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg and --impl reference)
+# ----------------------------------------------------------------------------------------
+
+def oracle_sample(a, o, spec, p, seconds):
+    """Time the oracle (as it stands, all host threads) on the first n_sub sequences of the
+    workload with the same p, n_sub sized for about `seconds` of CPU work."""
+    import oracle
+    cores = oracle.threads(0)
+    n_sub = min(len(o) - 1, max(p * p, 800))
+    sub = lambda m: (a[: o[m]], o[: m + 1])
+    t0 = time.perf_counter()
+    oracle.run(*sub(n_sub), spec.alphabet, spec.k, p)
+    dt = time.perf_counter() - t0
+    # all-pairs cost grows ~ n^2; scale to the time budget
+    scale = (seconds / max(dt, 1e-3)) ** 0.5
+    n_sub = int(min(len(o) - 1, max(n_sub, n_sub * scale)))
+    return n_sub, cores
+
+
+def run_oracle(a, o, spec, p, n_sub):
+    import oracle
+    t0 = time.perf_counter()
+    oracle.run(a[: o[n_sub]], o[: n_sub + 1], spec.alphabet, spec.k, p)
+    return time.perf_counter() - t0
+
+
+# ----------------------------------------------------------------------------------------
+# clocks during the timed region
+# ----------------------------------------------------------------------------------------
+
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, device: int):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_dev{device}.csv") if os.path.isdir(
+            os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_dev{device}_{os.getpid()}.csv"
+        self.device = device
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                r = int(parts[2], 16)
+            except ValueError:
+                continue
+            sm.append(s)
+            mx.append(m)
+            for bit, name in REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    from synth import gen
+    spec = gen.SPECS[args.config]
+    p = args.p or (8 if args.config in (2, 3, 4) else spec.p)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return reference_arm(args, spec, p, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_0901_2742_b200.runtime import Context
+
+    a, o = gen.generate(spec)
+    n = len(o) - 1
+    if p % world:
+        raise SystemExit(f"p={p} must be a multiple of the GPU count {world}")
+    pl = p // world
+    sb = gen.shard_bounds(n, p)
+    lo, hi = sb[rank * pl], sb[(rank + 1) * pl]
+    a_loc = np.ascontiguousarray(a[o[lo]: o[hi]])
+    o_loc = np.ascontiguousarray(o[lo: hi + 1] - o[lo])
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    d_a = torch.from_numpy(a_loc).to(dev)
+    d_o = torch.from_numpy(o_loc).to(dev)
+    h_a = torch.from_numpy(a_loc).pin_memory()
+    h_o = torch.from_numpy(o_loc).pin_memory()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)       # 256 MB > 126 MB L2
+
+    ctx = Context(spec.alphabet, spec.k, p, world=world, rank=rank, device=local_rank, stream=stream,
+                  kernel=args.kernel, group=group)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def step_device():
+        ctx.load(d_a, d_o, n, lo)
+        ctx.run()
+
+    def step_e2e():
+        ctx.load(h_a.numpy(), h_o.numpy(), n, lo)                   # H2D from pinned host memory
+        sizes = ctx.run()
+        keys = ctx.out_keys().cpu()                                  # D2H of the step's result
+        return keys, sizes
+
+    def timed(fn, steps):
+        ev = []
+        for _ in range(steps):
+            barrier()
+            flush.fill_(1)                                          # L2 flush between timed steps (untimed)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            s.record(stream)
+            fn()
+            e.record(stream)
+            ev.append((s, e))
+        barrier()
+        ms = sum(s.elapsed_time(e) for s, e in ev)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(args.warmup):
+        step_device()
+    ctx.reset_stats()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    ms_dev = timed(step_device, args.steps)
+    clk = clocks.stop()
+    st = ctx.stats()
+    launches = st["launches"]
+    ap_ms = st["allpairs_ms_total"] / max(st["calls"], 1)
+    op_ms = st["operand_ms_total"] / max(st["calls"], 1)
+    # e2e through the public API with host buffers
+    for _ in range(max(1, args.warmup // 2)):
+        step_e2e()
+    e2e_h2d = int(h_a.numel() + h_o.numel() * 8)
+    keys, _ = step_e2e()
+    e2e_d2h = int(keys.numel() * 8 + p * 8)
+    ms_e2e = timed(step_e2e, args.steps)
+
+    pairs_job = total_pairs(n, p)
+    ms_step = ms_dev / args.steps
+    value = pairs_job / (ms_step / 1e3)
+    e2e_value = pairs_job / (ms_e2e / args.steps / 1e3)
+
+    # roofline of the dominant kernel (the all-pairs kernel, K5 / K5')
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    _, _, kcols = ctx.profile_info()
+    w_loc = [sb[rank * pl + s + 1] - sb[rank * pl + s] for s in range(pl)]
+    if args.kernel == "tc":
+        # algorithmic dense work of the threshold-indicator SYRK: 2 * K_s ops per pair i <= j
+        ops = sum(2 * (w * (w + 1) // 2) * int(k) for w, k in zip(w_loc, kcols))
+        bf16 = peaks.get("bf16_tflops_sustained", 1373.2 if peaks else 1400.0)
+        peak = 2.0 * bf16            # int8 dense = 2 x bf16 dense (nominal ratio 4.5 / 2.25)
+        roof = {"bound": "tensor", "achieved": ops / (ap_ms / 1e3) / 1e12, "peak": peak, "unit": "TOPS",
+                "frac": None, "traffic": None,
+                "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops_sustained (int8:bf16 nominal ratio)"
+                if peaks else "2 x fallback 1.4 PFLOP/s sustained bf16"}
+    else:
+        vpad = ((ctx_V(spec) + 63) // 64) * 64
+        ops = sum((w * (w + 1) // 2) * vpad for w in w_loc)   # one VIMNMX.U16x2 + one VIADD.U16x2 per 2 k-mers
+        peak = 148 * 128 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
+        roof = {"bound": "alu", "achieved": ops / (ap_ms / 1e3) / 1e12, "peak": peak, "unit": "Tops",
+                "frac": None, "traffic": None,
+                "peak_source": "148 SMs x 128 int32 lanes x sm_max_mhz (DESIGN.md §5)"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["kernel_ms"] = ap_ms
+    roof["operand_build_ms"] = op_ms
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_sub, cores = oracle_sample(a, o, spec, p, args.cpu_seconds)
+        dt = run_oracle(a, o, spec, p, n_sub)
+        cpu = {"value": total_pairs(n_sub, p) / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"oracle.run (full pipeline, p={p}) on the first {n_sub} sequences of the workload, "
+                         f"{dt:.1f} s; value = that subset's within-shard pairs / time"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "i8" if args.kernel == "tc" else "u16", "data": "synthetic",
+            "config": {"workload": workload_name(spec, p), "p": p, "kernel": args.kernel,
+                       "pairs_per_step": pairs_job,
+                       "l2": "L2 flushed (256 MB write) before every timed step; operand working set > L2"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,
+                    "ms_per_step": ms_e2e / args.steps},
+            "allpairs_pairs_per_s": pairs_job / world / (ap_ms / 1e3) * world if ap_ms > 0 else None,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": int(launches) * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ctx_V(spec):
+    return (20 if spec.alphabet == "protein" else 4) ** spec.k
+
+
+def reference_arm(args, spec, p, world, rank):
+    """The oracle timed as it stands on the host cores, on this arm's config/metric."""
+    if rank != 0:
+        return 0
+    from synth import gen
+    a, o = gen.generate(spec)
+    per_step = max(2.0, min(8.0, 120.0 / max(args.steps + args.warmup, 1)))
+    n_sub, cores = oracle_sample(a, o, spec, p, per_step)
+    for _ in range(args.warmup):
+        run_oracle(a, o, spec, p, n_sub)
+    t = sum(run_oracle(a, o, spec, p, n_sub) for _ in range(args.steps))
+    value = total_pairs(n_sub, p) / (t / args.steps)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_name(spec, p), "p": p},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"each step: oracle.run on the first {n_sub} sequences of the workload"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main() or 0)

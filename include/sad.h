@@ -1,0 +1,275 @@
+/*
+ * sad.h — C ABI of libsad.so: the data-parallel hot path of Sample-Align-D
+ * (Saeed & Khokhar, arXiv 0901.2742), the k-mer-rank domain decomposition, on
+ * B200 (sm_100a).
+ *
+ * Citations: "P:n" = PAPER.md line n (the paper text), "S:n" = SPEC.md line n,
+ * "reading Ann" = the interpretation table of SURVEY.md §8(c) / DESIGN.md §3.
+ *
+ * The calls follow the paper's problem statement:
+ *   "Input <- N sequences"                       -> sad_load
+ *   "Locally compute k-mer rank ..." (counts)     -> sad_build_profiles
+ *   "... k-mer rank ... in each processor",
+ *   local ancestor                                -> sad_rank_local
+ *   "Send the k samples ... to all processors",
+ *   "Compute the k-mer rank of each sequence ...",
+ *   "Sort the sequences locally ...",
+ *   "Using regular sampling, choose p-1 ..."      -> sad_rank_global
+ *   "Sort all the p*(p-1) ranks ... p buckets",
+ *   bucket boundaries                             -> sad_partition_plan
+ *   "Redistributed sequences among processors"    -> sad_pack (send side) + sad_finish (receive side)
+ * Between those calls the caller moves the small exchange buffers between ranks
+ * (all-gather of ancestor records, of sample keys and of the count matrix, and
+ * the variable all-to-all of sequences); every byte of arithmetic of the method
+ * runs inside this library's CUDA kernels.
+ *
+ * CONVENTIONS (all calls)
+ *  - Return 0 on success or a negative SAD_E_* code. No exception crosses the ABI.
+ *  - Errors are sticky: after a failure every call except sad_last_error /
+ *    sad_destroy returns SAD_E_STATE.
+ *  - All device work is enqueued on cfg.stream (a cudaStream_t, may be NULL = legacy
+ *    default stream). Calls return after enqueueing, except where "syncs" is stated.
+ *  - Device pointers passed in ("d_" prefix) are owned by the caller, must stay valid
+ *    until the stream has consumed them, and are never freed by the library. Host
+ *    pointers ("h_" prefix) are read/written synchronously within the call.
+ *  - Layouts are dense, row-major, little-endian; no padding unless stated.
+ *  - The context is not thread-safe; one context per (process, GPU).
+ */
+#ifndef SAD_H_
+#define SAD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAD_ABI_VERSION 1u
+
+/* alphabets ("sequences of amino acids"; DNA per BASELINE.json configs[4]).
+ * Protein codes follow "ACDEFGHIKLMNPQRSTVWY", DNA "ACGT"; any other byte is an
+ * illegal symbol (reading A18). */
+#define SAD_PROTEIN20 0
+#define SAD_DNA4 1
+
+/* flags */
+#define SAD_F_KEEP_SIM 1u     /* keep the w x w similarity numerators S_ij (uint16) of every shard */
+#define SAD_F_KERNEL_ALU 2u   /* all-pairs on the CUDA-core min-sum (K5', dense uint16 count tiles) */
+#define SAD_F_KERNEL_TC 4u    /* all-pairs on tcgen05 tensor cores (K5, threshold-indicator GEMM); default */
+
+/* memory kinds of sad_load inputs */
+#define SAD_MEM_HOST 0
+#define SAD_MEM_DEVICE 1
+
+/* error codes */
+#define SAD_OK 0
+#define SAD_E_ARG (-1)           /* bad k/p/alphabet/world/rank, p % world != 0, A^k > 65536, NULL pointer */
+#define SAD_E_STATE (-2)         /* call order, or a sticky earlier error */
+#define SAD_E_SYMBOL (-3)        /* illegal residue; first offender via sad_last_error / sad_error_location */
+#define SAD_E_TOO_SHORT (-4)     /* a sequence with L < k (reading A19) */
+#define SAD_E_TOO_LONG (-5)      /* a sequence with L - k + 1 > 65535 (the fixed-point proof) */
+#define SAD_E_INSUFFICIENT (-6)  /* a shard with w < p (reading A16) */
+#define SAD_E_EMPTY (-7)         /* n_global == 0 or a rank with no shard rows */
+#define SAD_E_CAPACITY (-8)      /* a caller buffer is too small */
+#define SAD_E_CUDA (-9)          /* CUDA runtime error (message in sad_last_error) */
+#define SAD_E_OOM (-11)          /* workspace too small / host allocation failed */
+
+typedef struct sad_config {
+    int32_t alphabet;   /* SAD_PROTEIN20 | SAD_DNA4 */
+    int32_t k;          /* k-mer length, >= 1, alphabet^k <= 65536 */
+    int32_t p;          /* logical processors = shards = buckets (reading A21), >= 1 */
+    int32_t world;      /* G: number of ranks (GPUs); p % world == 0 */
+    int32_t rank;       /* this rank, 0..world-1; it owns shards rank*(p/world) .. (rank+1)*(p/world)-1
+                           and buckets with the same indices */
+    int32_t device;     /* CUDA device ordinal */
+    void *stream;       /* cudaStream_t used for all work */
+    uint32_t flags;     /* SAD_F_* */
+} sad_config;
+
+typedef struct sad_ctx sad_ctx;
+
+/* Version of this header the library was built from. */
+uint32_t sad_abi_version(void);
+
+/* Create a context. Does not allocate device memory. */
+int sad_create(const sad_config *cfg, sad_ctx **out);
+
+/* Destroy a context (waits for its stream). NULL is a no-op. */
+void sad_destroy(sad_ctx *ctx);
+
+/* Human-readable description of the last error ("" if none). Valid until the next call. */
+const char *sad_last_error(const sad_ctx *ctx);
+
+/* For SAD_E_SYMBOL / SAD_E_TOO_SHORT / SAD_E_TOO_LONG: global source index of the first
+ * offending sequence and (SYMBOL only) the 0-based residue position; -1 otherwise. */
+int sad_error_location(const sad_ctx *ctx, int64_t *source_index, int64_t *position);
+
+/* Bytes of device workspace sad_load needs for n_local sequences holding
+ * residues_local residues on this rank. */
+int sad_workspace_size(const sad_ctx *ctx, int64_t n_local, int64_t residues_local, size_t *bytes);
+
+/*
+ * sad_load — "Input <- N sequences ... Assume N/p sequences on each of the p processors"
+ * (P:60). This rank's contiguous slice: sequences first_source_index ..
+ * first_source_index + n_local - 1 of the global input, which must be exactly the rows of
+ * this rank's p/world shards under the block split of reading A15 (the first N mod p shards
+ * hold ceil(N/p) sequences, the rest floor(N/p)).
+ *   ascii    [offsets[n_local]] residue bytes (host or device per mem)
+ *   offsets  [n_local+1] int64, offsets[0] == 0, nondecreasing (host or device per mem)
+ *   mem      SAD_MEM_HOST (copied with cudaMemcpyAsync; synchronous w.r.t. the inputs) or
+ *            SAD_MEM_DEVICE (copied device-to-device on the stream)
+ *   d_ws     device workspace of at least sad_workspace_size(n_local, offsets[n_local]) bytes,
+ *            256-byte aligned, owned by the caller, kept until the next sad_load or sad_destroy.
+ * Inputs are copied; no input pointer is retained. Syncs (so host inputs may be reused on
+ * return).
+ */
+int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t n_local,
+             int64_t first_source_index, int64_t n_global, int32_t mem, void *d_ws, size_t ws_bytes);
+
+/*
+ * sad_build_profiles — k-mer count profiles n_x(tau) of every local sequence,
+ * tau = sum_m c_m A^(k-1-m) over residue codes c. Validates symbols and lengths, builds the
+ * per-sequence sorted (tau, count) lists and each shard's column map for the all-pairs
+ * stage. Syncs once (to report input errors and size the all-pairs operand).
+ */
+int sad_build_profiles(sad_ctx *ctx);
+
+/* Bytes of the all-pairs operand buffer sad_rank_local needs (valid after sad_build_profiles). */
+int sad_operand_size(const sad_ctx *ctx, size_t *bytes);
+
+/* Bytes of one ancestor record: { int64 source_index; int32 L; int32 pad; uint16 counts[A^k] }
+ * padded to 16 bytes. */
+size_t sad_ancestor_record_bytes(const sad_ctx *ctx);
+
+/*
+ * sad_rank_local — "Locally compute k-mer rank of all the sequences in each processor"
+ * and the local ancestor (reading A6):
+ *   S_ij = sum_tau min(n_i(tau), n_j(tau)),  den_ij = min(L_i, L_j) - k + 1   (reading A1)
+ *   q_ij = floor(2^32 S_ij / den_ij),  T_i = sum_{j in shard} q_ij            (readings A3, A5)
+ *   a_s  = argmax_{i in s} T_i, ties -> smaller source index                  (reading A6)
+ *   d_operand  device buffer of >= sad_operand_size bytes (scratch, caller-owned)
+ *   d_anc_out  device buffer of (p/world) ancestor records, this rank's shards in order
+ */
+int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_anc_out);
+
+/*
+ * sad_rank_global — global ancestor and rank against it (readings A7, A8, A9):
+ *   d_anc_all   p ancestor records of ALL shards in shard order (the all-gather of every
+ *               rank's d_anc_out; for world == 1 simply this rank's d_anc_out)
+ *   GA = argmax_a U_a, U_a = sum_b q(a, b) over the p ancestors, ties -> smaller index
+ *   S_i = S(x_i, GA), den_i = min(L_i, L_GA) - k + 1,
+ *   key_i = (floor(2^32 S_i / den_i) << 31) + source_index_i  (uint64; SURVEY A.3 — orders
+ *           exactly as "S_a den_b < S_b den_a, then smaller index")
+ *   local sort of each shard by key, and p-1 regular samples per shard at 1-based
+ *   positions floor(j w / p), j = 1..p-1 (reading A10)
+ *   d_samples_out  (p/world)*(p-1) uint64 keys, shard-major
+ */
+int sad_rank_global(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out);
+
+/*
+ * sad_partition_plan — pivots and bucket ranges (readings A11-A13):
+ *   d_samples_all  p*(p-1) uint64 sample keys of ALL shards (the all-gather of every rank's
+ *                  d_samples_out; for world == 1 this rank's d_samples_out)
+ *   pivots = sorted samples at 1-based positions floor(p/2) + i p, i = 0..p-2
+ *   bucket(x) = smallest b with key(x) <= pivot_b, else p-1
+ *   d_counts_out   int64 [p/world][p][2]: for each local shard s and bucket b, the number of
+ *                  sequences and of residues that shard s sends to bucket b
+ */
+int sad_partition_plan(sad_ctx *ctx, const uint64_t *d_samples_all, int64_t *d_counts_out);
+
+/* Send/receive sizes of the all-to-all (pure host function, needs no GPU and no context),
+ * derived from the counts of ALL ranks (h_counts_all = int64 [p][p][2], shard-major, the
+ * all-gather of every rank's d_counts_out): for every peer rank r, the sequences and residue
+ * bytes `rank` sends to r and receives from r. Rank r owns shards and buckets
+ * r*(p/world) .. (r+1)*(p/world)-1. Returns SAD_E_ARG on bad p/world/rank. */
+int sad_exchange_sizes(int32_t p, int32_t world, int32_t rank, const int64_t *h_counts_all,
+                       int64_t *h_send_seqs, int64_t *h_send_res, int64_t *h_recv_seqs, int64_t *h_recv_res);
+
+/* Send-buffer layout of `rank` (pure host function): h_seg = int64 [p/world][p][2], for each
+ * local shard s and bucket b the sequence offset and the residue-byte offset of slice (s, b)
+ * in the send buffers. Slices are grouped by destination rank, then ordered by (s, b). */
+int sad_pack_plan(int32_t p, int32_t world, int32_t rank, const int64_t *h_counts_all, int64_t *h_seg);
+
+/*
+ * sad_pack — send side of "Redistributed sequences among processors":
+ * writes this rank's sequences grouped by destination rank (rank r owns buckets
+ * r*(p/world) .. (r+1)*(p/world)-1), each group ordered by (source shard, bucket, key).
+ *   d_send_meta  [sum h_send_seqs][2] uint64: { key, L }
+ *   d_send_res   [sum h_send_res] residue bytes (ASCII, as loaded)
+ */
+int sad_pack(sad_ctx *ctx, const int64_t *h_counts_all, uint64_t *d_send_meta, uint8_t *d_send_res);
+
+/* Bytes of the output buffer sad_finish needs on this rank (host only): the received
+ * sequences' keys, offsets and residues plus merge scratch. */
+int sad_output_size(const sad_ctx *ctx, const int64_t *h_counts_all, size_t *bytes);
+
+/* Where sad_finish puts its results inside d_out: h_layout[0] = sequences n_out, [1] =
+ * residues r_out, [2] = byte offset of uint64 keys[n_out], [3] = byte offset of int64
+ * offsets[n_out+1], [4] = byte offset of residues[r_out], [5] = total bytes. Rows are the
+ * owned buckets back to back in bucket order, each in key order. Host only. */
+int sad_output_layout(const sad_ctx *ctx, const int64_t *h_counts_all, int64_t *h_layout);
+
+/*
+ * sad_finish — receive side: merges the received runs into this rank's buckets, each in key
+ * order (SPEC D-P4 ordering), and reports all bucket sizes (load bound of P:188,
+ * reading A23).
+ *   d_recv_meta / d_recv_res  the all-to-all output laid out by source rank (sizes from
+ *   sad_exchange_sizes). For world == 1 pass NULL for both: the local data is used in place.
+ *   d_out / out_bytes  caller buffer of >= sad_output_size bytes, 256-byte aligned; it must
+ *   stay valid while the getters below are used.
+ *   h_bucket_sizes  [p] int64 out: sizes of ALL buckets (host, from h_counts_all)
+ * Does not sync.
+ */
+int sad_finish(sad_ctx *ctx, const int64_t *h_counts_all, const uint64_t *d_recv_meta,
+               const uint8_t *d_recv_res, void *d_out, size_t out_bytes, int64_t *h_bucket_sizes);
+
+/* ---- getters (sync; copy device results into caller host buffers) ---- */
+
+/* T_i (uint64) of every sequence of local shard s (0 <= s < p/world), in input order. */
+int sad_get_local_rank(sad_ctx *ctx, int shard, uint64_t *h_T, int64_t cap);
+
+/* Local ancestors of ALL p shards and the GA, as global source indices (after sad_rank_global). */
+int sad_get_ancestors(sad_ctx *ctx, int64_t *h_local, int64_t *h_ga);
+
+/* S_i, den_i and key_i of every sequence of local shard s, in input order (after sad_rank_global). */
+int sad_get_ranks(sad_ctx *ctx, int shard, uint32_t *h_S, uint32_t *h_den, uint64_t *h_key, int64_t cap);
+
+/* Source indices of local shard s in its local sort order (after sad_rank_global). */
+int sad_get_sorted(sad_ctx *ctx, int shard, int64_t *h_idx, int64_t cap);
+
+/* The p-1 pivot keys (after sad_partition_plan). */
+int sad_get_pivots(sad_ctx *ctx, uint64_t *h_pivots);
+
+/* One bucket owned by this rank (after sad_finish): source indices, keys, residues (ASCII)
+ * and offsets[n+1] (relative to the bucket's first residue). Returns SAD_E_CAPACITY if a
+ * cap is too small; *n_out / *res_out receive the sizes in any case. Any output may be NULL. */
+int sad_get_bucket(sad_ctx *ctx, int bucket, int64_t *h_idx, uint64_t *h_key, uint8_t *h_res,
+                   int64_t *h_offsets, int64_t cap_seqs, int64_t cap_res, int64_t *n_out, int64_t *res_out);
+
+/* The w x w similarity numerators S_ij of local shard s (uint16, row-major, input order);
+ * only with SAD_F_KEEP_SIM. */
+int sad_get_similarity(sad_ctx *ctx, int shard, uint16_t *h_S, int64_t cap);
+
+/* Per-shard profile facts (after sad_build_profiles): total k-mer windows, distinct k-mers
+ * and the operand column count K_s of every local shard (int64 [p/world] each; any may be NULL). */
+int sad_get_profile_info(sad_ctx *ctx, int64_t *h_windows, int64_t *h_distinct, int64_t *h_kcols);
+
+/* Device times of the all-pairs kernel (K5/K5') summed over all sad_rank_local calls since the
+ * last reset, and the number of such calls; h_ms[0] = all-pairs kernel ms, h_ms[1] = operand
+ * build ms, h_counts[0] = calls, h_counts[1] = unordered pairs i<j per call, h_counts[2] =
+ * dense operand MACs per call (sum_s w_s(w_s+1)/2 * K_s), h_counts[3] = kernel launches of the
+ * last full step (load..finish). Syncs. */
+int sad_get_stats(sad_ctx *ctx, double *h_ms, int64_t *h_counts);
+int sad_reset_stats(sad_ctx *ctx);
+
+/* Exhaustive self-test of the device fixed-point division q = floor(2^32 S / den)
+ * (SURVEY A.3 / reading A5) for every den in [1, max_den] and S in [0, den], against
+ * 64-bit integer division on the device. Returns the number of mismatches in *h_bad. Syncs. */
+int sad_selftest_fixed_point(sad_ctx *ctx, int32_t max_den, int64_t *h_bad);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SAD_H_ */

@@ -1,0 +1,397 @@
+// k_rank.cu — K7 (local ancestors), K8 (GA), K9 (rank vs GA), K11 (samples, pivots),
+// K12 (bucket ranges), K13 (pack), K14 helpers (receive-side merge), fixed-point self-test.
+#include <cub/block/block_scan.cuh>
+
+#include "sad_internal.cuh"
+
+namespace sad {
+
+static inline unsigned grid1d(int64_t n) {
+    const int64_t g = (n + 255) / 256;
+    return (unsigned)(g < 4096 ? g : 4096);
+}
+
+// record layout: { int64 source_index; int32 L; uint32 tw; uint16 counts[V] }
+__device__ __forceinline__ int64_t rec_idx(const uint8_t *r) { return *reinterpret_cast<const int64_t *>(r); }
+__device__ __forceinline__ uint32_t rec_tw(const uint8_t *r) { return *reinterpret_cast<const uint32_t *>(r + 12); }
+__device__ __forceinline__ const uint16_t *rec_cnt(const uint8_t *r) { return reinterpret_cast<const uint16_t *>(r + 16); }
+
+__device__ __forceinline__ uint64_t q_den(uint32_t S, uint32_t d) {
+    return fixed_q(S, d, 0xFFFFFFFFu / d, 0xFFFFFFFFu % d + 1u);
+}
+
+// ---------------------------------------------------------------------------------------
+// K7: a_s = argmax_{i in s} T_i, ties -> smaller index (reading A6: the shard medoid under
+// distance 1 - F stands in for the alignment-derived "Local Ancestor" of PAPER.md:79),
+// then the ancestor record (dense counts) that the all-gather of PAPER.md:71/79 ships.
+// ---------------------------------------------------------------------------------------
+constexpr int kAncThreads = 1024;
+__global__ void __launch_bounds__(kAncThreads) k_local_anc(AncArgs a) {
+    __shared__ unsigned long long bT[32];
+    __shared__ long long bI[32];
+    const int s = blockIdx.x;
+    const int64_t b0 = a.shard_base[s], b1 = a.shard_base[s + 1];
+    unsigned long long best = 0;
+    long long bi = -1;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += kAncThreads) {
+        const unsigned long long t = a.T[i];
+        if (bi < 0 || t > best) { best = t; bi = i; }     // rows visited in increasing order
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long ot = __shfl_xor_sync(0xffffffffu, best, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (oi >= 0 && (bi < 0 || ot > best || (ot == best && oi < bi))) { best = ot; bi = oi; }
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) { bT[wid] = best; bI[wid] = bi; }
+    __syncthreads();
+    if (wid == 0) {
+        best = bT[lane];
+        bi = bI[lane];
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long ot = __shfl_xor_sync(0xffffffffu, best, o);
+            const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (oi >= 0 && (bi < 0 || ot > best || (ot == best && oi < bi))) { best = ot; bi = oi; }
+        }
+        if (lane == 0) { bI[0] = bi; }
+    }
+    __syncthreads();
+    const int64_t row = bI[0];
+    uint8_t *rec = a.rec_out + (size_t)s * a.rec_bytes;
+    uint16_t *cnt = reinterpret_cast<uint16_t *>(rec + 16);
+    for (size_t t = threadIdx.x; t < (a.rec_bytes - 16) / 2; t += kAncThreads) cnt[t] = 0;
+    __syncthreads();
+    const uint32_t *ent = a.csr + (a.off[row] - row * (int64_t)(a.k - 1));
+    for (int e = threadIdx.x; e < a.dcnt[row]; e += kAncThreads) cnt[ent[e] >> 16] = (uint16_t)(ent[e] & 0xFFFFu);
+    if (threadIdx.x == 0) {
+        *reinterpret_cast<int64_t *>(rec) = a.first_idx + row;
+        *reinterpret_cast<int32_t *>(rec + 8) = (int32_t)(a.rowinfo[row].tw + a.k - 1);
+        *reinterpret_cast<uint32_t *>(rec + 12) = a.rowinfo[row].tw;
+        a.anc_local[s] = row;
+    }
+}
+
+void launch_local_ancestors(const AncArgs &a, cudaStream_t st) {
+    k_local_anc<<<a.pl, kAncThreads, 0, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------------------
+// K8: S(a, b) between all gathered ancestors ("Determine 'Global' Ancestor GA
+// ... by aligning 'local' ancestors", reading A7: medoid of the ancestors).
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_ga_pairs(RankArgs a) {
+    __shared__ uint32_t red[8];
+    const int x = blockIdx.x / a.p, y = blockIdx.x % a.p;
+    const uint32_t *ca = reinterpret_cast<const uint32_t *>(rec_cnt(a.anc_all + (size_t)x * a.rec_bytes));
+    const uint32_t *cb = reinterpret_cast<const uint32_t *>(rec_cnt(a.anc_all + (size_t)y * a.rec_bytes));
+    uint32_t s = 0;
+    const int words = (a.V + 1) / 2;
+    for (int t = threadIdx.x; t < words; t += 256) {
+        const uint32_t m = __vminu2(ca[t], cb[t]);
+        s += (m & 0xFFFFu) + (m >> 16);
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        a.Sab[blockIdx.x] = t;
+    }
+}
+
+void launch_ga_pairs(const RankArgs &a, cudaStream_t st) {
+    k_ga_pairs<<<a.p * a.p, 256, 0, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------------------
+// K9: GA = argmax_a U_a, U_a = sum_b q(a,b) (ties -> smaller source index), recomputed by
+// every block from the p x p numerators; then, one warp per sequence, the rank against the
+// GA (reading A8): S_i = sum_tau min(n_i, n_GA), den_i = min(L_i, L_GA) - k + 1,
+// key_i = (floor(2^32 S_i/den_i) << 31) + source_index (the key order is the
+// exact rational order with index tie-break, reading A9).
+// ---------------------------------------------------------------------------------------
+constexpr int kRankThreads = 256;
+__global__ void __launch_bounds__(kRankThreads) k_rank_vs_ga(RankArgs a) {
+    extern __shared__ uint16_t ga_cnt[];
+    __shared__ unsigned long long U[256];
+    __shared__ int g_sh;
+    for (int x = threadIdx.x; x < a.p; x += kRankThreads) {
+        const uint32_t twx = rec_tw(a.anc_all + (size_t)x * a.rec_bytes);
+        unsigned long long u = 0;
+        for (int y = 0; y < a.p; ++y) {
+            const uint32_t twy = rec_tw(a.anc_all + (size_t)y * a.rec_bytes);
+            u += q_den(a.Sab[x * a.p + y], min(twx, twy));
+        }
+        U[x] = u;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int g = 0;
+        for (int x = 1; x < a.p; ++x) {
+            const int64_t ix = rec_idx(a.anc_all + (size_t)x * a.rec_bytes);
+            const int64_t ig = rec_idx(a.anc_all + (size_t)g * a.rec_bytes);
+            if (U[x] > U[g] || (U[x] == U[g] && ix < ig)) g = x;
+        }
+        g_sh = g;
+        if (blockIdx.x == 0) {
+            a.ga_info[0] = g;
+            a.ga_info[1] = rec_idx(a.anc_all + (size_t)g * a.rec_bytes);
+            for (int x = 0; x < a.p; ++x) a.ga_info[2 + x] = rec_idx(a.anc_all + (size_t)x * a.rec_bytes);
+        }
+    }
+    __syncthreads();
+    const uint8_t *grec = a.anc_all + (size_t)g_sh * a.rec_bytes;
+    const uint16_t *gc = rec_cnt(grec);
+    for (int t = threadIdx.x; t < a.V; t += kRankThreads) ga_cnt[t] = gc[t];
+    const uint32_t twg = rec_tw(grec);
+    const uint32_t qdg = 0xFFFFFFFFu / twg, rpg = 0xFFFFFFFFu % twg + 1u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (kRankThreads / 32);
+    for (int64_t i = (int64_t)blockIdx.x * (kRankThreads / 32) + (threadIdx.x >> 5); i < a.n; i += nwarps) {
+        const uint32_t *ent = a.csr + (a.off[i] - i * (int64_t)(a.k - 1));
+        const int d = a.dcnt[i];
+        uint32_t s = 0;
+        for (int e = lane; e < d; e += 32) {
+            const uint32_t v = ent[e];
+            s += min(v & 0xFFFFu, (uint32_t)ga_cnt[v >> 16]);
+        }
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            const RowInfo ri = a.rowinfo[i];
+            const uint32_t den = min(ri.tw, twg);
+            const uint64_t q = ri.tw <= twg ? fixed_q(s, ri.tw, ri.qd, ri.rp) : fixed_q(s, twg, qdg, rpg);
+            a.S_ga[i] = s;
+            a.den_ga[i] = den;
+            a.key[i] = (q << 31) + (uint64_t)(a.first_idx + i);
+            a.perm_in[i] = (int32_t)i;
+        }
+    }
+}
+
+void launch_rank_vs_ga(const RankArgs &a, cudaStream_t st) {
+    const size_t smem = (size_t)a.V * 2;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(k_rank_vs_ga, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t grid = (a.n + 7) / 8;
+    if (grid > (int64_t)sms * 4) grid = (int64_t)sms * 4;
+    if (grid < 1) grid = 1;
+    k_rank_vs_ga<<<(unsigned)grid, kRankThreads, smem, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------------------
+// K11a: p-1 regular samples per sorted shard at 1-based positions floor(j w / p)
+// ("k = (p-1) evenly spaced samples"; reading A10).
+// ---------------------------------------------------------------------------------------
+__global__ void k_samples(const unsigned long long *ks, const int64_t *sb, int pl, int p, unsigned long long *out) {
+    const int n = pl * (p - 1);
+    for (int t = threadIdx.x + blockIdx.x * blockDim.x; t < n; t += blockDim.x * gridDim.x) {
+        const int s = t / (p - 1), j = t % (p - 1) + 1;
+        const int64_t w = sb[s + 1] - sb[s];
+        out[t] = ks[sb[s] + (j * w) / p - 1];
+    }
+}
+
+void launch_samples(const unsigned long long *key_sorted, const int64_t *shard_base, int pl, int p,
+                    unsigned long long *samples_out, cudaStream_t st) {
+    if (p > 1) k_samples<<<1, 256, 0, st>>>(key_sorted, shard_base, pl, p, samples_out);
+}
+
+// ---------------------------------------------------------------------------------------
+// K11b + K12: sort the p(p-1) gathered samples, pivots at 1-based floor(p/2) + i p
+// (reading A11); bucket(x) = smallest b with key <= pivot_b (PAPER.md:188
+// "must be <= y1"; reading A13), found per shard by binary search on the sorted keys; and
+// the per-shard exclusive prefix of L over the sorted order (residue bytes per slice).
+// ---------------------------------------------------------------------------------------
+constexpr int kPlanThreads = 256;
+__global__ void __launch_bounds__(kPlanThreads) k_plan(PlanArgs a) {
+    extern __shared__ unsigned long long Y[];        // [p(p-1)] sorted samples, then pivots
+    typedef cub::BlockScan<long long, kPlanThreads> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    const int p = a.p, m = p * (p - 1);
+    unsigned long long *piv = Y + m;
+    for (int t = threadIdx.x; t < m; t += kPlanThreads) {
+        const unsigned long long v = a.samples_all[t];
+        int r = 0;
+        for (int u = 0; u < m; ++u) r += a.samples_all[u] < v;   // keys are unique
+        Y[r] = v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < p - 1; i += kPlanThreads) {
+        piv[i] = Y[p / 2 + i * p - 1];
+        if (blockIdx.x == 0) a.pivots[i] = piv[i];
+    }
+    __syncthreads();
+    const int s = blockIdx.x;
+    const int64_t base = a.shard_base[s], w = a.shard_base[s + 1] - base;
+    const unsigned long long *ks = a.key_sorted + base;
+    int64_t *bnd = a.bnd + (size_t)s * p;
+    for (int b = threadIdx.x; b < p; b += kPlanThreads) {
+        int64_t lo = 0, hi = w;                      // number of keys <= pivot_b
+        if (b == p - 1) {
+            lo = w;
+        } else {
+            const unsigned long long pv = piv[b];
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (ks[mid] <= pv) lo = mid + 1; else hi = mid;
+            }
+        }
+        bnd[b] = lo;
+    }
+    // exclusive prefix of L in sorted order: lpre[base + s + t], t = 0..w
+    int64_t *lp = a.lpre + base + s;
+    const int64_t per = (w + kPlanThreads - 1) / kPlanThreads;
+    const int64_t t0 = min(w, (int64_t)threadIdx.x * per), t1 = min(w, t0 + per);
+    long long sum = 0;
+    for (int64_t t = t0; t < t1; ++t) sum += a.rowinfo[a.perm_sorted[base + t]].tw + a.k - 1;
+    long long pre, total;
+    Scan(tmp).ExclusiveSum(sum, pre, total);
+    for (int64_t t = t0; t < t1; ++t) {
+        lp[t] = pre;
+        pre += a.rowinfo[a.perm_sorted[base + t]].tw + a.k - 1;
+    }
+    if (threadIdx.x == 0) lp[w] = total;
+    __syncthreads();
+    for (int b = threadIdx.x; b < p; b += kPlanThreads) {
+        const int64_t lo = b ? bnd[b - 1] : 0, hi = bnd[b];
+        a.counts[((size_t)s * p + b) * 2 + 0] = hi - lo;
+        a.counts[((size_t)s * p + b) * 2 + 1] = lp[hi] - lp[lo];
+    }
+}
+
+void launch_plan(const PlanArgs &a, cudaStream_t st) {
+    const size_t smem = (size_t)(a.p * (a.p - 1) + a.p) * 8;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    k_plan<<<a.pl, kPlanThreads, smem, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------------------
+// K13: pack — sequences grouped by destination, each slice (shard s, bucket b) a
+// contiguous run of s's sorted order ("Each processor partition its blocks into
+// p sub-blocks, one for each processor, using pivots as bucket boundaries").
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_pack(PackArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    for (int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); t < a.n; t += nw) {
+        int s = 0;
+        while (s + 1 < a.pl && t >= a.shard_base[s + 1]) ++s;
+        const int64_t tt = t - a.shard_base[s];
+        const int64_t *bnd = a.bnd + (size_t)s * a.p;
+        int b = 0;
+        while (tt >= bnd[b]) ++b;
+        const int64_t start = b ? bnd[b - 1] : 0;
+        const int64_t *lp = a.lpre + a.shard_base[s] + s;
+        const int64_t so = a.seg[((size_t)s * a.p + b) * 2 + 0] + (tt - start);
+        const int64_t ro = a.seg[((size_t)s * a.p + b) * 2 + 1] + (lp[tt] - lp[start]);
+        const int32_t row = a.perm_sorted[t];
+        const int64_t L = (int64_t)a.rowinfo[row].tw + a.k - 1;
+        if (lane == 0) {
+            a.send_meta[so * 2 + 0] = a.key_sorted[t];
+            a.send_meta[so * 2 + 1] = (unsigned long long)L;
+        }
+        const uint8_t *src = a.ascii + a.off[row];
+        uint8_t *dst = a.send_res + ro;
+        for (int64_t c = lane; c < L; c += 32) dst[c] = src[c];
+    }
+}
+
+void launch_pack(const PackArgs &a, cudaStream_t st) {
+    int64_t grid = (a.n + 7) / 8;
+    if (grid > 148 * 16) grid = 148 * 16;
+    if (grid > 0) k_pack<<<(unsigned)grid, 256, 0, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------------------
+// K14 helpers: the receiving rank sorts everything it received by key (the keys of its
+// buckets are contiguous key ranges, so one sort yields every owned bucket in key order)
+// and gathers the residues into that order.
+// ---------------------------------------------------------------------------------------
+__global__ void k_meta_local(const unsigned long long *key, const RowInfo *ri, int k, int64_t n,
+                             unsigned long long *keys_in, int32_t *vals_in, int64_t *len_in) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        keys_in[i] = key[i];
+        vals_in[i] = (int32_t)i;
+        len_in[i] = (int64_t)ri[i].tw + k - 1;
+    }
+}
+
+void launch_meta_from_local(const unsigned long long *key, const RowInfo *rowinfo, int k, int64_t n,
+                            unsigned long long *keys_in, int32_t *vals_in, int64_t *len_in, cudaStream_t st) {
+    if (n > 0) k_meta_local<<<grid1d(n), 256, 0, st>>>(key, rowinfo, k, n, keys_in, vals_in, len_in);
+}
+
+__global__ void k_meta_recv(const unsigned long long *m, int64_t n, unsigned long long *keys_in, int32_t *vals_in,
+                            int64_t *len_in) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        keys_in[i] = m[2 * i];
+        vals_in[i] = (int32_t)i;
+        len_in[i] = (int64_t)m[2 * i + 1];
+    }
+}
+
+void launch_meta_from_recv(const unsigned long long *recv_meta, int64_t n, unsigned long long *keys_in,
+                           int32_t *vals_in, int64_t *len_in, cudaStream_t st) {
+    if (n > 0) k_meta_recv<<<grid1d(n), 256, 0, st>>>(recv_meta, n, keys_in, vals_in, len_in);
+}
+
+__global__ void k_gather_len(const int32_t *perm, const int64_t *len_in, int64_t n, int64_t *len_sorted) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        len_sorted[i] = len_in[perm[i]];
+}
+
+void launch_gather_len(const int32_t *perm, const int64_t *len_in, int64_t n, int64_t *len_sorted, cudaStream_t st) {
+    if (n > 0) k_gather_len<<<grid1d(n), 256, 0, st>>>(perm, len_in, n, len_sorted);
+}
+
+__global__ void __launch_bounds__(256) k_gather_out(const int32_t *perm, int64_t n, const int64_t *src_off,
+                                                    const uint8_t *src_res, const int64_t *dst_off, uint8_t *dst_res) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    for (int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); t < n; t += nw) {
+        const uint8_t *src = src_res + src_off[perm[t]];
+        uint8_t *dst = dst_res + dst_off[t];
+        const int64_t L = dst_off[t + 1] - dst_off[t];
+        for (int64_t c = lane; c < L; c += 32) dst[c] = src[c];
+    }
+}
+
+void launch_gather_out(const int32_t *perm, int64_t n, const int64_t *src_off, const uint8_t *src_res,
+                       const int64_t *dst_off, uint8_t *dst_res, cudaStream_t st) {
+    int64_t grid = (n + 7) / 8;
+    if (grid > 148 * 16) grid = 148 * 16;
+    if (grid > 0) k_gather_out<<<(unsigned)grid, 256, 0, st>>>(perm, n, src_off, src_res, dst_off, dst_res);
+}
+
+// ---------------------------------------------------------------------------------------
+// exhaustive check of fixed_q against 64-bit division
+// ---------------------------------------------------------------------------------------
+__global__ void k_selftest_fixed(int max_den, unsigned long long *bad) {
+    const uint32_t d = blockIdx.x + 1;
+    if ((int)d > max_den) return;
+    const uint32_t qd = 0xFFFFFFFFu / d, rp = 0xFFFFFFFFu % d + 1u;
+    unsigned long long nbad = 0;
+    for (uint32_t S = threadIdx.x; S <= d; S += blockDim.x) {
+        const unsigned long long ref = ((unsigned long long)S << 32) / d;
+        nbad += fixed_q(S, d, qd, rp) != ref;
+    }
+    if (nbad) atomicAdd(bad, nbad);
+}
+
+void launch_selftest_fixed(int max_den, unsigned long long *bad, cudaStream_t st) {
+    if (max_den > 0) k_selftest_fixed<<<max_den, 256, 0, st>>>(max_den, bad);
+}
+
+}  // namespace sad

@@ -1,0 +1,263 @@
+// sad_internal.cuh — private declarations of libsad.so (not part of the ABI).
+//
+// Data layout in HBM (per rank; n = local sequences, R = local residues, pl = p/world
+// local shards, V = A^k):
+//   ascii   u8  [R]          residues as loaded (the redistribution payload)
+//   off     i64 [n+1]        residue offsets
+//   rowinfo u32x4 [n]        {Tw = L-k+1, Qd = floor((2^32-1)/Tw), Rp = (2^32-1) mod Tw + 1, shard}
+//   csr     u32 [sum Tw]     per sequence, distinct k-mers sorted by tau: (tau << 16) | count;
+//                            sequence i starts at off[i] - i*(k-1)
+//   dcnt    i32 [n]          distinct k-mers per sequence
+//   M/col0  u32 [pl][V]      per shard max count of tau / first operand column of tau
+//   T       u64 [n]          within-shard fixed-point rank sums (reading A5)
+//   key     u64 [n]          (floor(2^32 S/den) << 31) + source_index
+// The all-pairs operand (caller buffer) is either the binary threshold-indicator matrix
+// u8 [rows_pad][K_stride] (tensor-core path) or dense counts u16 [rows_pad][V_pad] (ALU path).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sad.h"
+
+namespace sad {
+
+constexpr int kMaxLocalShards = 256;
+constexpr int kRowPad = 128;        // operand rows per shard padded to this (tensor-core M tile)
+constexpr int kColPad = 128;        // operand columns padded to this (one 128-byte K block)
+
+struct RowInfo {                    // per local sequence, 16 bytes
+    uint32_t tw;                    // L - k + 1 (the den candidate of this row)
+    uint32_t qd;                    // floor((2^32 - 1) / tw)
+    uint32_t rp;                    // (2^32 - 1) mod tw + 1
+    uint32_t shard;                 // local shard index
+};
+
+// ------------------------------------------------------------------------------------
+// Exact fixed point q = floor(2^32 * S / d) for 0 <= S <= d <= 65535, d = min(tw_i, tw_j)
+// (reading A5). With 2^32 - 1 = Qd*d + (Rp-1):
+//   2^32 S = S*Qd*d + S*Rp  =>  q = S*Qd + floor(x/d),  x = S*Rp < 2^32.
+//   t0 = umulhi(x, Qd) = floor(x*Qd/2^32) and x*Qd/2^32 = x/d - x*Rp/(d*2^32) in (x/d - 1, x/d],
+//   so t0 is floor(x/d) or floor(x/d) - 1 and one remainder test fixes it.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t fixed_q(uint32_t S, uint32_t d, uint32_t qd, uint32_t rp) {
+    uint32_t x = S * rp;
+    uint32_t t = __umulhi(x, qd);
+    uint32_t r = x - t * d;
+    t += (r >= d) ? 1u : 0u;
+    return (uint64_t)S * qd + t;
+}
+
+__device__ __forceinline__ uint64_t pair_q(uint32_t S, const RowInfo &a, const RowInfo &b) {
+    return a.tw <= b.tw ? fixed_q(S, a.tw, a.qd, a.rp) : fixed_q(S, b.tw, b.qd, b.rp);
+}
+
+// ------------------------------------------------------------------------------------
+// kernels (defined in k_*.cu)
+// ------------------------------------------------------------------------------------
+struct ProfileArgs {
+    const uint8_t *ascii;
+    const int64_t *off;
+    int64_t n;
+    int64_t first_idx;
+    int k, A, V, alphabet, pl;
+    const int64_t *shard_base;       // device [pl+1]
+    RowInfo *rowinfo;
+    uint32_t *csr;
+    int32_t *dcnt;
+    uint32_t *M;                     // [pl][V]
+    unsigned long long *err;         // [4]: first bad symbol (idx<<32|pos), first short idx, first long idx, pad
+    unsigned long long *kinfo;       // [pl][4]: windows, distinct, K, pad
+};
+void launch_profile(const ProfileArgs &a, cudaStream_t st);
+void launch_colmap(const uint32_t *M, uint32_t *col0, unsigned long long *kinfo, int pl, int V, cudaStream_t st);
+
+struct OperandArgs {
+    const uint32_t *csr;
+    const int64_t *off;
+    const int32_t *dcnt;
+    const uint32_t *col0;            // [pl][V]
+    const int64_t *shard_base;       // device [pl+1] local row bases
+    const int64_t *shard_rowpad;     // device [pl+1] padded operand row bases
+    int64_t rows_pad;
+    int64_t stride;                  // bytes per operand row
+    int k, V, pl;
+    void *op;
+};
+void launch_indicator(const OperandArgs &a, cudaStream_t st);
+void launch_dense_counts(const OperandArgs &a, cudaStream_t st);
+
+struct AllPairsArgs {
+    const void *op;                  // operand
+    int64_t stride;                  // bytes per operand row
+    const RowInfo *rowinfo;          // [n] local rows
+    const int64_t *shard_base;       // device [pl+1]
+    const int64_t *shard_rowpad;     // device [pl+1]
+    const int64_t *shard_kblocks;    // device [pl]: 128-col K blocks of each shard (TC path)
+    int pl;
+    int64_t max_w;
+    unsigned long long *T;           // [n]
+    uint16_t *sim;                   // optional [sum w_s^2]
+    const int64_t *sim_base;         // device [pl] offsets into sim
+    int vwords;                      // ALU: u32 words per row (V_pad/2)
+    int num_sms;
+    const int64_t *tile_base;        // ALU: device [pl+1] prefix of 64x64 upper-triangle tiles
+    int64_t n_tiles;
+    const void *tmap;                // TC: CUtensorMap (64 B, host copy passed as __grid_constant__)
+    const int64_t *h_shard_base;     // host copies (launch configuration)
+    const int64_t *h_shard_rowpad;
+    const int64_t *h_kblocks;
+};
+void launch_allpairs_alu(const AllPairsArgs &a, cudaStream_t st);
+int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err);
+bool tc_supported(std::string &why);
+
+struct AncArgs {
+    const unsigned long long *T;
+    const int64_t *shard_base;
+    const uint32_t *csr;
+    const int64_t *off;
+    const int32_t *dcnt;
+    const RowInfo *rowinfo;
+    int64_t first_idx;
+    int k, V, pl;
+    size_t rec_bytes;
+    int64_t *anc_local;              // [pl] local row of each shard's ancestor
+    uint8_t *rec_out;                // [pl] records
+};
+void launch_local_ancestors(const AncArgs &a, cudaStream_t st);
+
+struct RankArgs {
+    const uint8_t *anc_all;          // [p] records
+    size_t rec_bytes;
+    int p, k, V;
+    uint32_t *Sab;                   // [p][p] scratch
+    long long *ga_info;              // [2 + p]: GA record index, GA source index, ancestors' source idx
+    const uint32_t *csr;
+    const int64_t *off;
+    const int32_t *dcnt;
+    const RowInfo *rowinfo;
+    int64_t n, first_idx;
+    uint32_t *S_ga, *den_ga;
+    unsigned long long *key;
+    int32_t *perm_in;
+};
+void launch_ga_pairs(const RankArgs &a, cudaStream_t st);
+void launch_rank_vs_ga(const RankArgs &a, cudaStream_t st);
+
+void launch_samples(const unsigned long long *key_sorted, const int64_t *shard_base, int pl, int p,
+                    unsigned long long *samples_out, cudaStream_t st);
+
+struct PlanArgs {
+    const unsigned long long *samples_all;   // [p(p-1)]
+    int p, pl;
+    const unsigned long long *key_sorted;    // [n] per shard sorted keys
+    const int32_t *perm_sorted;              // [n] local rows in sorted order
+    const int64_t *shard_base;
+    const RowInfo *rowinfo;
+    int k;
+    unsigned long long *pivots;              // [p-1] out
+    int64_t *bnd;                            // [pl][p] out: sorted-position end of each bucket slice
+    int64_t *lpre;                           // [n + pl] out: per shard exclusive prefix of L in sorted order (w+1 each)
+    int64_t *counts;                         // [pl][p][2] out
+};
+void launch_plan(const PlanArgs &a, cudaStream_t st);
+
+struct PackArgs {
+    const unsigned long long *key_sorted;
+    const int32_t *perm_sorted;
+    const int64_t *shard_base;
+    const int64_t *bnd;                      // [pl][p]
+    const int64_t *lpre;                     // [n + pl]
+    const int64_t *seg;                      // [pl][p][2]: send seq offset, send residue offset of each slice
+    const RowInfo *rowinfo;
+    const uint8_t *ascii;
+    const int64_t *off;
+    int p, pl, k;
+    int64_t n;
+    unsigned long long *send_meta;           // [.][2]
+    uint8_t *send_res;
+};
+void launch_pack(const PackArgs &a, cudaStream_t st);
+
+// receive side
+void launch_meta_from_local(const unsigned long long *key, const RowInfo *rowinfo, int k, int64_t n,
+                            unsigned long long *keys_in, int32_t *vals_in, int64_t *len_in, cudaStream_t st);
+void launch_meta_from_recv(const unsigned long long *recv_meta, int64_t n, unsigned long long *keys_in,
+                           int32_t *vals_in, int64_t *len_in, cudaStream_t st);
+void launch_gather_len(const int32_t *perm, const int64_t *len_in, int64_t n, int64_t *len_sorted, cudaStream_t st);
+void launch_gather_out(const int32_t *perm, int64_t n, const int64_t *src_off, const uint8_t *src_res,
+                       const int64_t *dst_off, uint8_t *dst_res, cudaStream_t st);
+
+void launch_selftest_fixed(int max_den, unsigned long long *bad, cudaStream_t st);
+
+}  // namespace sad
+
+// ------------------------------------------------------------------------------------
+// the context
+// ------------------------------------------------------------------------------------
+struct sad_ctx {
+    sad_config cfg{};
+    cudaStream_t st = nullptr;
+    int A = 0, V = 0, pl = 0, shard0 = 0;
+    int num_sms = 148;
+    std::string err;
+    int sticky = 0;
+    int64_t err_idx = -1, err_pos = -1;
+    int stage = 0;                   // 0 created, 1 loaded, 2 profiles, 3 rank_local, 4 rank_global, 5 plan, 6 finished
+
+    // sizes
+    int64_t n = 0, n_global = 0, first_idx = 0, R = 0;
+    std::vector<int64_t> shard_base, shard_rowpad;   // [pl+1]
+    int64_t rows_pad = 0, max_w = 0;
+    std::vector<int64_t> h_windows, h_distinct, h_K; // [pl]
+    int64_t K_stride = 0, V_pad = 0;
+    bool use_tc = false;
+
+    // device pointers carved from the caller workspace
+    uint8_t *ws = nullptr;
+    size_t ws_bytes = 0;
+    uint8_t *d_ascii = nullptr;
+    int64_t *d_off = nullptr;
+    sad::RowInfo *d_rowinfo = nullptr;
+    uint32_t *d_csr = nullptr;
+    int32_t *d_dcnt = nullptr;
+    uint32_t *d_M = nullptr, *d_col0 = nullptr;
+    unsigned long long *d_err = nullptr, *d_kinfo = nullptr;
+    int64_t *d_shard_base = nullptr, *d_shard_rowpad = nullptr, *d_kblocks = nullptr, *d_sim_base = nullptr;
+    int64_t *d_tile_base = nullptr;
+    int64_t alu_tiles = 0;
+    unsigned long long *d_T = nullptr;
+    int64_t *d_anc_local = nullptr;
+    uint32_t *d_Sab = nullptr;
+    long long *d_ga_info = nullptr;
+    uint32_t *d_S_ga = nullptr, *d_den_ga = nullptr;
+    unsigned long long *d_key = nullptr, *d_key_sorted = nullptr;
+    int32_t *d_perm_in = nullptr, *d_perm_sorted = nullptr;
+    unsigned long long *d_pivots = nullptr;
+    int64_t *d_bnd = nullptr, *d_lpre = nullptr, *d_seg = nullptr;
+    void *d_tmap = nullptr;
+    void *d_cub = nullptr;
+    size_t cub_bytes = 0;
+    uint16_t *d_sim = nullptr;       // optional (SAD_F_KEEP_SIM), inside the workspace
+    int64_t sim_elems = 0;
+
+    // last operand / output
+    void *d_operand = nullptr;
+    uint8_t *d_out = nullptr;
+    size_t out_bytes = 0;
+    int64_t out_n = 0, out_r = 0;
+    std::vector<int64_t> bucket_sizes, bucket_first;  // [p] sizes, first row of owned buckets in out
+    std::vector<int64_t> h_counts_all;                  // [p][p][2]
+
+    // pinned host staging
+    unsigned long long *h_small = nullptr;              // pinned, 4096 u64
+
+    // stats
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pairs_ap, ev_pairs_op, ev_free;
+    double ms_ap = 0, ms_op = 0;
+    int64_t calls = 0, pairs = 0, macs = 0, launches_last = 0, launches_step = 0;
+};

@@ -1,0 +1,299 @@
+"""Python driver of libsad.so: argument marshalling, torch-owned device memory, and the
+rank-to-rank exchange steps over torch.distributed.
+
+The method's arithmetic runs in the library's CUDA kernels. This module only
+  * allocates the device buffers the library asks for (grow-only torch tensors),
+  * passes the caller's CUDA stream,
+  * moves the exchange buffers between ranks ("Send the k samples from each
+    processor to all the processors", :74-76 gather/broadcast of the sample ranks, :77
+    "Redistributed sequences among processors") with torch.distributed collectives
+    (NCCL over NVLink on the GPU box; the same functions run on gloo/CPU in tests).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+
+ALPHABETS = {"protein": L.SAD_PROTEIN20, "dna": L.SAD_DNA4}
+
+
+def _vp(t) -> ctypes.c_void_p:
+    if t is None:
+        return ctypes.c_void_p(None)
+    if isinstance(t, int):
+        return ctypes.c_void_p(t)
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data_as(ctypes.c_void_p)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+# ----------------------------------------------------------------------------------------
+# exchange steps (device-agnostic: CUDA tensors on NCCL, CPU tensors on gloo)
+# ----------------------------------------------------------------------------------------
+
+def all_gather_rows(local: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """Concatenate every rank's `local` (same shape everywhere) in rank order."""
+    local = local.contiguous()
+    if world == 1:
+        return local
+    out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    if local.is_cuda:
+        dist.all_gather_into_tensor(out, local, group=group)
+    else:
+        dist.all_gather(list(out.chunk(world)), local, group=group)
+    return out
+
+
+def exchange_sizes(p: int, world: int, rank: int, counts_all: np.ndarray):
+    """Per-peer send/recv sequence and residue counts (host logic of libsad.so)."""
+    c = np.ascontiguousarray(counts_all, dtype=np.int64)
+    ss, sr, rs, rr = (np.zeros(world, np.int64) for _ in range(4))
+    L.call("sad_exchange_sizes", p, world, rank, _vp(c), _vp(ss), _vp(sr), _vp(rs), _vp(rr))
+    return ss, sr, rs, rr
+
+
+def pack_plan(p: int, world: int, rank: int, counts_all: np.ndarray) -> np.ndarray:
+    c = np.ascontiguousarray(counts_all, dtype=np.int64)
+    seg = np.zeros((p // world, p, 2), np.int64)
+    L.call("sad_pack_plan", p, world, rank, _vp(c), _vp(seg))
+    return seg
+
+
+def all_to_all_v(send: torch.Tensor, send_sizes, recv_sizes, group=None) -> torch.Tensor:
+    """Variable all-to-all of a flat tensor (rows of any width), split by rank."""
+    recv = torch.empty((int(np.sum(recv_sizes)),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
+    dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=[int(x) for x in recv_sizes],
+                           input_split_sizes=[int(x) for x in send_sizes], group=group)
+    return recv
+
+
+# ----------------------------------------------------------------------------------------
+# the context
+# ----------------------------------------------------------------------------------------
+
+class Context:
+    """One rank's view of the k-mer-rank domain decomposition (include/sad.h).
+
+    kernel: "tc" (tcgen05 threshold-indicator GEMM, default) or "alu" (CUDA-core min-sum).
+    """
+
+    def __init__(self, alphabet: str, k: int, p: int, *, world: int = 1, rank: int = 0, device: int | None = None,
+                 stream: torch.cuda.Stream | None = None, kernel: str = "tc", keep_sim: bool = False, group=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("the k-mer-rank path needs a CUDA device (no CPU fallback)")
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.alphabet, self.k, self.p, self.world, self.rank, self.group = alphabet, k, p, world, rank, group
+        self.pl = p // world
+        flags = (L.SAD_F_KEEP_SIM if keep_sim else 0) | (L.SAD_F_KERNEL_ALU if kernel == "alu" else L.SAD_F_KERNEL_TC)
+        self.kernel = kernel
+        cfg = L.SadConfig(ALPHABETS[alphabet], k, p, world, rank, device, self.stream.cuda_stream, flags)
+        h = ctypes.c_void_p()
+        L.call("sad_create", ctypes.byref(cfg), ctypes.byref(h))
+        self._h = h
+        self._bufs: dict[str, torch.Tensor] = {}
+        self.rec_bytes = int(L.lib().sad_ancestor_record_bytes(h))
+        self.counts_all = None
+        self.bucket_sizes = None
+        self.layout = None
+
+    # -- memory ------------------------------------------------------------------------
+    def _buf(self, name: str, nbytes: int, align: int = 1024) -> int:
+        """Device pointer to a grow-only torch buffer of >= nbytes, aligned to `align`."""
+        t = self._bufs.get(name)
+        if t is None or t.numel() < nbytes + align:
+            t = torch.empty(int(nbytes * 1.1) + align + 256, dtype=torch.uint8, device=self.device)
+            self._bufs[name] = t
+        base = t.data_ptr()
+        return (base + align - 1) // align * align
+
+    def _tensor(self, name: str, shape, dtype) -> torch.Tensor:
+        n = int(np.prod(shape)) if len(shape) else 1
+        key = f"t:{name}"
+        t = self._bufs.get(key)
+        if t is None or t.dtype != dtype or t.numel() < n:
+            t = torch.empty(max(n, 1), dtype=dtype, device=self.device)
+            self._bufs[key] = t
+        return t[:n].view(*shape) if len(shape) else t[:1]
+
+    def _call(self, name, *args):
+        return L.call(name, self._h, *args, ctx=self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.lib().sad_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- pipeline ------------------------------------------------------------------------
+    def load(self, ascii_, offsets, n_global: int, first_index: int = 0):
+        """This rank's contiguous slice (numpy host arrays or CUDA tensors)."""
+        on_dev = isinstance(ascii_, torch.Tensor) and ascii_.is_cuda
+        if on_dev:
+            n_local = int(offsets.numel()) - 1
+            R = int(offsets[-1].item()) if n_local >= 0 else 0
+            mem = L.SAD_MEM_DEVICE
+        else:
+            ascii_ = np.ascontiguousarray(ascii_, dtype=np.uint8)
+            offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+            n_local = len(offsets) - 1
+            R = int(offsets[-1])
+            mem = L.SAD_MEM_HOST
+            if ascii_.size == 0:
+                ascii_ = np.zeros(1, np.uint8)
+        self.n_local, self.n_global, self.first_index, self.R = n_local, n_global, first_index, R
+        ws = ctypes.c_size_t()
+        self._call("sad_workspace_size", n_local, R, ctypes.byref(ws))
+        p_ws = self._buf("ws", ws.value)
+        self._call("sad_load", _vp(ascii_), _vp(offsets), n_local, first_index, n_global, mem, ctypes.c_void_p(p_ws),
+                   ws.value)
+        return self
+
+    def build_profiles(self):
+        self._call("sad_build_profiles")
+
+    def rank_local(self) -> torch.Tensor:
+        ob = ctypes.c_size_t()
+        self._call("sad_operand_size", ctypes.byref(ob))
+        p_op = self._buf("operand", ob.value, align=1024)
+        anc = self._tensor("anc", (self.pl, self.rec_bytes), torch.uint8)
+        self._call("sad_rank_local", ctypes.c_void_p(p_op), ob.value, _vp(anc))
+        return anc
+
+    def rank_global(self, anc_all: torch.Tensor) -> torch.Tensor:
+        samples = self._tensor("samples", (max(self.pl * (self.p - 1), 1),), torch.int64)
+        self._call("sad_rank_global", _vp(anc_all), _vp(samples))
+        return samples[: self.pl * (self.p - 1)]
+
+    def partition_plan(self, samples_all: torch.Tensor) -> torch.Tensor:
+        counts = self._tensor("counts", (self.pl, self.p, 2), torch.int64)
+        self._call("sad_partition_plan", _vp(samples_all if self.p > 1 else None), _vp(counts))
+        return counts
+
+    def redistribute(self, counts_all: np.ndarray):
+        """All-to-all of the sequences (world > 1) and the receive-side merge."""
+        c = np.ascontiguousarray(counts_all, dtype=np.int64)
+        self.counts_all = c
+        recv_meta = recv_res = None
+        if self.world > 1:
+            ss, sr, rs, rr = exchange_sizes(self.p, self.world, self.rank, c)
+            send_meta = self._tensor("send_meta", (int(ss.sum()), 2), torch.int64)
+            send_res = self._tensor("send_res", (max(int(sr.sum()), 1),), torch.uint8)
+            self._call("sad_pack", _vp(c), _vp(send_meta), _vp(send_res))
+            recv_meta = all_to_all_v(send_meta, ss, rs, self.group)
+            recv_res = all_to_all_v(send_res[: int(sr.sum())], sr, rr, self.group)
+            if recv_res.numel() == 0:
+                recv_res = torch.zeros(1, dtype=torch.uint8, device=self.device)
+        ob = ctypes.c_size_t()
+        self._call("sad_output_size", _vp(c), ctypes.byref(ob))
+        p_out = self._buf("out", ob.value, align=256)
+        sizes = np.zeros(self.p, np.int64)
+        self._call("sad_finish", _vp(c), _vp(recv_meta), _vp(recv_res), ctypes.c_void_p(p_out), ob.value, _vp(sizes))
+        lay = np.zeros(6, np.int64)
+        self._call("sad_output_layout", _vp(c), _vp(lay))
+        self._out_ptr = p_out
+        self.layout = lay
+        self._keep = (recv_meta, recv_res)
+        self.bucket_sizes = sizes
+        return sizes
+
+    def run(self) -> np.ndarray:
+        """One full step: profiles -> local rank -> GA rank -> plan -> redistribution.
+        Returns the sizes of all p buckets (host)."""
+        self.build_profiles()
+        anc = self.rank_local()
+        anc_all = all_gather_rows(anc, self.world, self.group)
+        samples = self.rank_global(anc_all)
+        samples_all = all_gather_rows(samples, self.world, self.group) if self.p > 1 else samples
+        counts = self.partition_plan(samples_all)
+        counts_all = all_gather_rows(counts, self.world, self.group).cpu().numpy()   # the one D2H of the plan
+        return self.redistribute(counts_all.reshape(self.p, self.p, 2))
+
+    # -- results -------------------------------------------------------------------------
+    def out_keys(self) -> torch.Tensor:
+        """uint64 keys (as int64) of all owned buckets, back to back, each in key order (device view)."""
+        n = int(self.layout[0])
+        t = self._bufs["out"]
+        off = self._out_ptr - t.data_ptr() + int(self.layout[2])
+        return t[off: off + 8 * n].view(torch.int64)
+
+    def local_rank(self, shard: int) -> np.ndarray:
+        w = self.shard_size(shard)
+        out = np.zeros(w, np.uint64)
+        self._call("sad_get_local_rank", shard, _vp(out), w)
+        return out
+
+    def shard_size(self, shard: int) -> int:
+        base, extra = divmod(self.n_global, self.p)
+        s = self.rank * self.pl + shard
+        return base + (1 if s < extra else 0)
+
+    def ancestors(self):
+        loc = np.zeros(self.p, np.int64)
+        ga = ctypes.c_int64()
+        self._call("sad_get_ancestors", _vp(loc), ctypes.byref(ga))
+        return loc, ga.value
+
+    def ranks(self, shard: int):
+        w = self.shard_size(shard)
+        S, d, key = np.zeros(w, np.uint32), np.zeros(w, np.uint32), np.zeros(w, np.uint64)
+        self._call("sad_get_ranks", shard, _vp(S), _vp(d), _vp(key), w)
+        return S, d, key
+
+    def sorted(self, shard: int) -> np.ndarray:
+        w = self.shard_size(shard)
+        out = np.zeros(w, np.int64)
+        self._call("sad_get_sorted", shard, _vp(out), w)
+        return out
+
+    def pivots(self) -> np.ndarray:
+        out = np.zeros(max(self.p - 1, 1), np.uint64)
+        self._call("sad_get_pivots", _vp(out))
+        return out[: self.p - 1]
+
+    def bucket(self, b: int):
+        n, r = ctypes.c_int64(), ctypes.c_int64()
+        self._call("sad_get_bucket", b, None, None, None, None, 0, 0, ctypes.byref(n), ctypes.byref(r))
+        idx, key = np.zeros(max(n.value, 1), np.int64), np.zeros(max(n.value, 1), np.uint64)
+        res, off = np.zeros(max(r.value, 1), np.uint8), np.zeros(n.value + 1, np.int64)
+        self._call("sad_get_bucket", b, _vp(idx), _vp(key), _vp(res), _vp(off), n.value, r.value, ctypes.byref(n),
+                   ctypes.byref(r))
+        return idx[: n.value], key[: n.value], res[: r.value], off
+
+    def similarity(self, shard: int) -> np.ndarray:
+        w = self.shard_size(shard)
+        out = np.zeros(w * w, np.uint16)
+        self._call("sad_get_similarity", shard, _vp(out), w * w)
+        return out.reshape(w, w)
+
+    def profile_info(self):
+        a, b, c = (np.zeros(self.pl, np.int64) for _ in range(3))
+        self._call("sad_get_profile_info", _vp(a), _vp(b), _vp(c))
+        return a, b, c
+
+    def stats(self):
+        ms = np.zeros(2, np.float64)
+        cnt = np.zeros(4, np.int64)
+        self._call("sad_get_stats", _vp(ms), _vp(cnt))
+        return {"allpairs_ms_total": float(ms[0]), "operand_ms_total": float(ms[1]), "calls": int(cnt[0]),
+                "pairs": int(cnt[1]), "dense_macs": int(cnt[2]), "launches": int(cnt[3])}
+
+    def reset_stats(self):
+        self._call("sad_reset_stats")
+
+    def selftest_fixed_point(self, max_den: int = 8000) -> int:
+        bad = ctypes.c_int64()
+        self._call("sad_selftest_fixed_point", max_den, ctypes.byref(bad))
+        return bad.value

@@ -1,0 +1,209 @@
+"""GPU path (libsad.so through the C ABI) vs the CPU oracle, bit for bit.
+
+All arithmetic on the path is integer, so every comparison is
+exact: T_i, local ancestors, GA, S_i/den_i, keys, local sort order, samples,
+pivots, bucket membership and order, and the redistributed residues.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth import gen
+
+pytestmark = pytest.mark.gpu
+
+def _kernels():
+    # the tensor-core kernel is mandatory once built (tc_supported() in k_allpairs_tc.cu)
+    import os
+    return ["tc", "alu"] if os.environ.get("SAD_TEST_TC", "1") == "1" else ["alu"]
+
+
+KERNELS = _kernels()
+
+
+def _ctx(alpha, k, p, kernel, keep_sim=False):
+    from paper_0901_2742_b200.runtime import Context
+    return Context(alpha, k, p, kernel=kernel, keep_sim=keep_sim)
+
+
+def _run_gpu(a, o, alpha, k, p, kernel, keep_sim=False):
+    ctx = _ctx(alpha, k, p, kernel, keep_sim)
+    n = len(o) - 1
+    ctx.load(a, o, n, 0)
+    sizes = ctx.run()
+    return ctx, sizes
+
+
+def _compare_full(ctx, sizes, r, a, o, p):
+    n = len(o) - 1
+    sb = gen.shard_bounds(n, p)
+    # T per shard (O4)
+    T = np.concatenate([ctx.local_rank(s) for s in range(p)])
+    assert np.array_equal(T, r.T), "T_i differs"
+    # ancestors and GA (O5, O6)
+    loc, ga = ctx.ancestors()
+    assert loc.tolist() == r.anc.tolist()
+    assert ga == r.ga
+    # ranks vs GA (O7) and keys
+    S = np.concatenate([ctx.ranks(s)[0] for s in range(p)]).astype(np.int64)
+    D = np.concatenate([ctx.ranks(s)[1] for s in range(p)]).astype(np.int64)
+    K = np.concatenate([ctx.ranks(s)[2] for s in range(p)])
+    assert np.array_equal(S, r.S) and np.array_equal(D, r.den)
+    q = np.array([oracle.q(int(s), int(d)) for s, d in zip(r.S, r.den)], dtype=object)
+    assert [int(x) for x in K] == [(int(qq) << 31) + i for i, qq in enumerate(q)]
+    # local sort (O8)
+    srt = np.concatenate([ctx.sorted(s) for s in range(p)])
+    assert np.array_equal(srt, r.sorted)
+    # pivots (O9): keys of the oracle's pivot sequences
+    piv = ctx.pivots()
+    assert [int(x) & 0x7FFFFFFF for x in piv] == r.pivots.tolist()
+    # buckets (O10, O11)
+    assert sizes.tolist() == r.bsize.tolist()
+    seqs = gen.to_strings(a, o)
+    for b, ref in enumerate(r.buckets()):
+        idx, key, res, off = ctx.bucket(b)
+        assert idx.tolist() == ref
+        got = [bytes(res[off[i]: off[i + 1]]).decode() for i in range(len(idx))]
+        assert got == [seqs[i] for i in ref]
+    assert sb[-1] == n
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_fixed_point_selftest(kernel):
+    if kernel == "tc":
+        pytest.skip("self-test is kernel independent")
+    ctx = _ctx("protein", 3, 1, kernel)
+    assert ctx.selftest_fixed_point(65535) == 0
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_worked_example(kernel):
+    seqs = ["ACGTAC", "ACGTTT", "CGTAAA", "TTTTGG", "ACGG", "TTTGGA"]
+    a, o = gen.from_strings(seqs)
+    ctx, sizes = _run_gpu(a, o, "dna", 2, 2, kernel)
+    r = oracle.run(a, o, "dna", 2, 2)
+    _compare_full(ctx, sizes, r, a, o, 2)
+    assert [ctx.bucket(b)[0].tolist() for b in range(2)] == [[3], [5, 1, 2, 4, 0]]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_configs_1_2_full(kernel, cfg):
+    spec = gen.SPECS[cfg]
+    a, o = gen.generate(cfg)
+    ctx, sizes = _run_gpu(a, o, spec.alphabet, spec.k, spec.p, kernel, keep_sim=(cfg == 1))
+    r = oracle.run(a, o, spec.alphabet, spec.k, spec.p)
+    _compare_full(ctx, sizes, r, a, o, spec.p)
+    if cfg == 1:      # full similarity matrices of config 1
+        n = len(o) - 1
+        sb = gen.shard_bounds(n, spec.p)
+        for s in range(spec.p):
+            Sm = ctx.similarity(s)
+            ii, jj = np.meshgrid(np.arange(sb[s], sb[s + 1]), np.arange(sb[s], sb[s + 1]), indexing="ij")
+            Sref, _ = oracle.pairs_S(a, o, spec.k, ii.ravel(), jj.ravel())
+            assert np.array_equal(Sm.ravel().astype(np.int64), Sref)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("case", ["cfg3_small", "cfg4_small", "cfg5_small_p1", "cfg5_small_p4", "ragged_p3"])
+def test_scaled_configs(kernel, case):
+    """Oracle-sized versions of configs 3-5 (same recipe, fewer sequences) that still span
+    several 128-row tiles, ragged shard tails and p not dividing N."""
+    if case == "cfg3_small":
+        spec, n, p = gen.SPECS[3], 1500, 8
+    elif case == "cfg4_small":
+        spec, n, p = gen.SPECS[4], 2100, 8
+    elif case == "cfg5_small_p1":
+        spec, n, p = gen.SPECS[5], 700, 1
+    elif case == "cfg5_small_p4":
+        spec, n, p = gen.SPECS[5], 903, 4
+    else:
+        spec, n, p = gen.SPECS[2], 1001, 3
+    a, o = gen.generate(spec, n=n)
+    ctx, sizes = _run_gpu(a, o, spec.alphabet, spec.k, p, kernel)
+    r = oracle.run(a, o, spec.alphabet, spec.k, p)
+    _compare_full(ctx, sizes, r, a, o, p)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_adversarial(kernel):
+    """poly-A (counts far above any cap, K columns grow), L == k, identical sequences (all
+    rank ties -> index order), containment (F = 1 without identity), w = p."""
+    rng = np.random.default_rng(5)
+    seqs = ["A" * 3000, "A" * 3, "ACD", "W" * 700, "AAAAAAAAAC", "AAC", "MMMMMMMMMMMMMM"]
+    seqs += ["ACDEFGHIK" * 10] * 9
+    seqs += ["".join(rng.choice(list("ACDEFGHIKLMNPQRSTVWY"), int(rng.integers(3, 400)))) for _ in range(200)]
+    a, o = gen.from_strings(seqs)
+    for p in (1, 4):
+        ctx, sizes = _run_gpu(a, o, "protein", 3, p, kernel)
+        r = oracle.run(a, o, "protein", 3, p)
+        _compare_full(ctx, sizes, r, a, o, p)
+    same = ["ACDEFGHIKL"] * 16                                    # w == p == 4
+    a, o = gen.from_strings(same)
+    ctx, sizes = _run_gpu(a, o, "protein", 3, 4, kernel)
+    r = oracle.run(a, o, "protein", 3, 4)
+    _compare_full(ctx, sizes, r, a, o, 4)
+
+
+def test_errors():
+    from paper_0901_2742_b200 import SadError
+    a, o = gen.from_strings(["ACDE", "ACDX", "ACDE", "ACDE"])
+    ctx = _ctx("protein", 3, 1, "alu")
+    ctx.load(a, o, 4, 0)
+    with pytest.raises(SadError) as e:
+        ctx.run()
+    assert e.value.name == "SAD_E_SYMBOL" and e.value.location == (1, 3)
+    a, o = gen.from_strings(["ACDE", "AC", "ACDE", "ACDE"])
+    ctx = _ctx("protein", 3, 1, "alu")
+    ctx.load(a, o, 4, 0)
+    with pytest.raises(SadError) as e:
+        ctx.run()
+    assert e.value.name == "SAD_E_TOO_SHORT" and e.value.location[0] == 1
+    a, o = gen.from_strings(["ACDE"] * 5)
+    ctx = _ctx("protein", 3, 3, "alu")
+    with pytest.raises(SadError) as e:
+        ctx.load(a, o, 5, 0)
+    assert e.value.name == "SAD_E_INSUFFICIENT"
+
+
+@pytest.mark.parametrize("kernel", KERNELS[:1])
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_full_size_sampled(kernel, cfg):
+    """BASELINE sizes in the bench's launch configuration (config 4: N = 100k, p = 8 on one
+    GPU; config 5: N = 10k DNA, p = 1): sampled T rows and GA ranks against the oracle one
+    by one, and the properties that hold at any size."""
+    spec = gen.SPECS[cfg]
+    p = spec.p
+    a, o = gen.generate(cfg)
+    n = len(o) - 1
+    ctx, sizes = _run_gpu(a, o, spec.alphabet, spec.k, p, kernel)
+    sb = gen.shard_bounds(n, p)
+    rng = np.random.default_rng(cfg)
+    T = np.concatenate([ctx.local_rank(s) for s in range(p)])
+    rows = np.concatenate([rng.choice(np.arange(sb[s], sb[s + 1]), 6, replace=False) for s in range(p)])
+    assert np.array_equal(oracle.rows_T(a, o, spec.k, p, rows), T[rows])
+    loc, ga = ctx.ancestors()
+    for s in range(p):                                           # a_s = argmax T (ties -> smaller index)
+        seg = T[sb[s]: sb[s + 1]]
+        assert loc[s] == sb[s] + int(np.flatnonzero(seg == seg.max())[0])
+    assert ga in loc.tolist()
+    S = np.concatenate([ctx.ranks(s)[0] for s in range(p)]).astype(np.int64)
+    D = np.concatenate([ctx.ranks(s)[1] for s in range(p)]).astype(np.int64)
+    K = np.concatenate([ctx.ranks(s)[2] for s in range(p)])
+    samp = rng.choice(n, 400, replace=False)
+    Sref, Dref = oracle.pairs_S(a, o, spec.k, samp, np.full(len(samp), ga))
+    assert np.array_equal(S[samp], Sref) and np.array_equal(D[samp], Dref)
+    assert all(int(K[i]) == (oracle.q(int(S[i]), int(D[i])) << 31) + int(i) for i in samp)
+    # buckets: a permutation, each in key order, bucket ranges increasing, <= 2w + p
+    assert int(sizes.sum()) == n and int(sizes.max()) <= 2 * (n // p) + p
+    keys = ctx.out_keys().cpu().numpy().view(np.uint64)
+    assert np.all(keys[1:] > keys[:-1])
+    assert np.array_equal(np.sort((keys & np.uint64(0x7FFFFFFF)).astype(np.int64)), np.arange(n))
+    assert np.array_equal(np.sort(K), keys)
+    piv = ctx.pivots()
+    first = np.concatenate([[0], np.cumsum(sizes)])
+    for b in range(p - 1):
+        if sizes[b]:
+            assert keys[first[b + 1] - 1] <= piv[b]
+        if first[b + 1] < n:
+            assert keys[first[b + 1]] > piv[b]
