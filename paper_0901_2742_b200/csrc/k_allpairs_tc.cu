@@ -1,13 +1,420 @@
-// k_allpairs_tc.cu — K5: all-pairs on tcgen05 tensor cores (placeholder until the kernel lands).
+// k_allpairs_tc.cu — K5: all-pairs within each shard on the 5th-generation tensor cores.
+//
+// By the split identity min(a, b) = sum_{t >= 1} [a >= t][b >= t],
+//   S_ij = sum_tau min(n_i(tau), n_j(tau)) = (A_s A_s^T)_ij
+// for the binary threshold-indicator matrix A_s built by K4 (k_profile.cu), one column per
+// (k-mer tau, layer t <= max_i n_i(tau)). The product is an exact integer contraction:
+// uint8 operands, int32 accumulation in TMEM (tcgen05.mma.kind::i8).
+//
+// Persistent kernel, one CTA (256 threads) per SM, 128 x 256 output tiles of the upper
+// triangle of every shard:
+//   warp 0      TMA producer: 128-byte K slices of A_I (128 rows) and A_J (256 rows),
+//               128B-swizzled, into a 4-stage shared-memory ring (mbarrier full/empty)
+//   warp 1      MMA issuer: 4 x tcgen05.mma (M=128, N=256, K=32) per stage into one of two
+//               TMEM accumulators (2 x 256 columns), tcgen05.commit to release stages
+//   warp 2      TMEM allocator (512 columns)
+//   warps 4-7   fused epilogue, overlapped with the next tile's MMAs: tcgen05.ld of S,
+//               exact fixed point q = floor(2^32 S / den) (reading A5), row sums and
+//               column sums (warp transpose-reduce + per-warp shared slots) into T (u64 atomics,
+//               order independent: SURVEY A.5)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+
 #include "sad_internal.cuh"
 
 namespace sad {
+
+namespace tc {
+constexpr int BM = 128, BN = 256, BK = 128;
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK;                  // 16 KB
+constexpr int B_BYTES = BN * BK;                  // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int THREADS = 256;
+constexpr int ACC_COLS = BN;                       // TMEM columns per accumulator
+constexpr int TMEM_COLS = 2 * ACC_COLS;            // double-buffered accumulator
+constexpr int OFF_BAR = STAGES * STAGE_BYTES;      // barriers after the ring
+constexpr int OFF_COLINFO = OFF_BAR + 256;
+constexpr int OFF_COLSUM = OFF_COLINFO + BN * 16;
+constexpr int SMEM_BYTES = OFF_COLSUM + 4 * BN * 8 + 1024;   // + alignment slack
+// instruction descriptor: D = S32 (bits 4-5 = 2), A = B = uint8 (0), K-major A and B,
+// N >> 3 at bits 17-22, M >> 4 at bits 24-28
+constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}  // namespace tc
+
+struct TcTile {
+    int32_t s, I, J, pad;
+};
+
+struct TcParams {
+    const TcTile *tiles;
+    int64_t n_tiles;
+    const RowInfo *rowinfo;
+    const int64_t *shard_base;
+    const int64_t *shard_rowpad;
+    const int64_t *kblocks;
+    unsigned long long *T;
+    uint16_t *sim;
+    const int64_t *sim_base;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *bar, void *dst, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+// K-major operand, 128-byte swizzle: start >> 4, LBO = 1 (unused), SBO = 1024 B (8-row groups),
+// version 1 (sm_100), layout SWIZZLE_128B (2).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constant__ CUtensorMap tmap, TcParams P) {
+    using namespace tc;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + STAGES * A_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    RowInfo *colinfo = reinterpret_cast<RowInfo *>(smem + OFF_COLINFO);
+    unsigned long long *colsum = reinterpret_cast<unsigned long long *>(smem + OFF_COLSUM);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== TMA producer =====
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+                const TcTile tl = P.tiles[t];
+                const int rowA = (int)(P.shard_rowpad[tl.s] + (int64_t)tl.I * BM);
+                const int rowB = (int)(P.shard_rowpad[tl.s] + (int64_t)tl.J * BN);
+                const int nkb = (int)P.kblocks[tl.s];
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], STAGE_BYTES);
+                    tma_load_2d(&tmap, &full[stage], sA + stage * A_BYTES, kb * BK, rowA);
+                    tma_load_2d(&tmap, &full[stage], sB + stage * B_BYTES, kb * BK, rowB);
+                    tma_load_2d(&tmap, &full[stage], sB + stage * B_BYTES + B_BYTES / 2, kb * BK, rowB + BN / 2);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===== MMA issuer =====
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+                const TcTile tl = P.tiles[t];
+                const int nkb = (int)P.kblocks[tl.s];
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + (uint32_t)(acc * ACC_COLS);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 32; ++kk)
+                        mma_i8(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), IDESC, (kb | kk) != 0);
+                    tc_commit(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                tc_commit(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue =====
+        const int ew = warp - 4;                  // TMEM lanes 32*ew .. 32*ew+31
+        const int e = threadIdx.x - 128;          // 0..127
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+            const TcTile tl = P.tiles[t];
+            const int64_t rbase = P.shard_base[tl.s];
+            const int64_t w = P.shard_base[tl.s + 1] - rbase;
+            const int64_t col0 = (int64_t)tl.J * BN;
+            epi_bar();                            // previous tile's colinfo/colsum fully consumed
+            for (int c = e; c < BN; c += 128) {
+                const int64_t col = col0 + c;
+                colinfo[c] = col < w ? P.rowinfo[rbase + col] : RowInfo{1u, 0xFFFFFFFFu, 1u, 0u};
+            }
+            epi_bar();
+            const int64_t row = (int64_t)tl.I * BM + ew * 32 + lane;
+            const bool vrow = row < w;
+            const RowInfo ri = vrow ? P.rowinfo[rbase + row] : RowInfo{1u, 0xFFFFFFFFu, 1u, 0u};
+            uint16_t *simr = (P.sim && vrow) ? P.sim + P.sim_base[tl.s] : nullptr;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            unsigned long long rowsum = 0;
+            const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * ACC_COLS);
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 16; ++ch) {
+                uint32_t v[16];
+                tmem_ld16(tbase + ch * 16, v);
+                unsigned long long cv[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int64_t col = col0 + ch * 16 + j;
+                    const bool ok = vrow && col < w && col >= row;
+                    const uint64_t q = ok ? pair_q(v[j], ri, colinfo[ch * 16 + j]) : 0ull;
+                    rowsum += q;
+                    cv[j] = (ok && col != row) ? q : 0ull;
+                    if (simr && ok) {
+                        simr[row * w + col] = (uint16_t)v[j];
+                        simr[col * w + row] = (uint16_t)v[j];
+                    }
+                }
+                // warp transpose-reduce: after offsets 16, 8, 4, 2 lane l holds column (l >> 1) & 15
+                // summed over the 16 lanes sharing bit 0; offset 1 completes the 32-lane sum.
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const bool up = lane & 16;
+                    const unsigned long long snd = up ? cv[j] : cv[j + 8];
+                    const unsigned long long kp = up ? cv[j + 8] : cv[j];
+                    cv[j] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const bool up = lane & 8;
+                    const unsigned long long snd = up ? cv[j] : cv[j + 4];
+                    const unsigned long long kp = up ? cv[j + 4] : cv[j];
+                    cv[j] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+                }
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const bool up = lane & 4;
+                    const unsigned long long snd = up ? cv[j] : cv[j + 2];
+                    const unsigned long long kp = up ? cv[j + 2] : cv[j];
+                    cv[j] = kp + __shfl_xor_sync(0xffffffffu, snd, 4);
+                }
+                {
+                    const bool up = lane & 2;
+                    const unsigned long long snd = up ? cv[0] : cv[1];
+                    const unsigned long long kp = up ? cv[1] : cv[0];
+                    cv[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 2);
+                }
+                cv[0] += __shfl_xor_sync(0xffffffffu, cv[0], 1);
+                if (!(lane & 1)) colsum[ew * BN + ch * 16 + ((lane >> 1) & 15)] = cv[0];   // per-warp slot
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            if (vrow && rowsum) atomicAdd(&P.T[rbase + row], rowsum);
+            epi_bar();
+            for (int c = e; c < BN; c += 128) {
+                const int64_t col = col0 + c;
+                const unsigned long long cs = colsum[c] + colsum[BN + c] + colsum[2 * BN + c] + colsum[3 * BN + c];
+                if (col < w && cs) atomicAdd(&P.T[rbase + col], cs);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                     : "memory");
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
 bool tc_supported(std::string &why) {
-    why = "tcgen05 all-pairs kernel not built yet";
-    return false;
+    static std::once_flag once;
+    static bool ok = false;
+    static std::string reason;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceProp prop{};
+        if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+            reason = "no CUDA device";
+            return;
+        }
+        if (prop.major != 10) {
+            reason = "needs sm_100 (B200)";
+            return;
+        }
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+            reason = "cuTensorMapEncodeTiled unavailable";
+            return;
+        }
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        if (cudaFuncSetAttribute(k_syrk_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES) != cudaSuccess) {
+            reason = "cannot reserve shared memory";
+            return;
+        }
+        ok = true;
+    });
+    why = reason;
+    return ok;
 }
-int launch_allpairs_tc(const AllPairsArgs &, cudaStream_t, std::string &err) {
-    err = "not built";
-    return -1;
+
+// tiles of the upper triangle of every shard: (I, J) with J >= floor(I / 2) (the tile holds some
+// j >= i), in groups of kGroupJ column blocks so that the ~148 tiles in flight share a few
+// A_J blocks and walk the A_I blocks (L2 reuse).
+static void build_tiles(int pl, const int64_t *h_shard_base, std::vector<TcTile> &out) {
+    constexpr int kGroupJ = 8;
+    out.clear();
+    for (int s = 0; s < pl; ++s) {
+        const int64_t w = h_shard_base[s + 1] - h_shard_base[s];
+        const int nI = (int)((w + tc::BM - 1) / tc::BM), nJ = (int)((w + tc::BN - 1) / tc::BN);
+        for (int j0 = 0; j0 < nJ; j0 += kGroupJ)
+            for (int I = 0; I < nI; ++I)
+                for (int J = std::max(j0, I / 2); J < std::min(nJ, j0 + kGroupJ); ++J) out.push_back(TcTile{s, I, J, 0});
+    }
 }
+
+int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base) {
+    std::vector<TcTile> t;
+    build_tiles(pl, h_shard_base, t);
+    return (int64_t)t.size() * (int64_t)sizeof(TcTile);
+}
+
+int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err) {
+    std::string why;
+    if (!tc_supported(why)) {
+        err = why;
+        return -1;
+    }
+    // tile table, appended after the operand matrix (caller buffer, sized by sad_operand_size)
+    static thread_local std::vector<TcTile> tiles;
+    build_tiles(a.pl, a.h_shard_base, tiles);
+    if (tiles.empty()) return 0;
+    const int64_t rows_pad = a.h_shard_rowpad[a.pl];
+    uint8_t *tile_dev = reinterpret_cast<uint8_t *>(const_cast<void *>(a.op)) + rows_pad * a.stride;
+    tile_dev = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tile_dev) + 255) & ~uintptr_t(255));
+    static thread_local TcTile *pinned = nullptr;
+    static thread_local size_t pinned_n = 0;
+    if (pinned_n < tiles.size()) {
+        if (pinned) { cudaStreamSynchronize(st); cudaFreeHost(pinned); }
+        pinned_n = tiles.size() * 2;
+        if (cudaMallocHost(&pinned, pinned_n * sizeof(TcTile)) != cudaSuccess) {
+            err = "pinned allocation failed";
+            pinned = nullptr;
+            pinned_n = 0;
+            return -1;
+        }
+    }
+    // the previous call's copy has been consumed: every step synchronizes in sad_build_profiles
+    std::memcpy(pinned, tiles.data(), tiles.size() * sizeof(TcTile));
+    if (cudaMemcpyAsync(tile_dev, pinned, tiles.size() * sizeof(TcTile), cudaMemcpyHostToDevice, st) != cudaSuccess) {
+        err = "tile table upload failed";
+        return -1;
+    }
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof map);
+    const cuuint64_t dims[2] = {(cuuint64_t)a.stride, (cuuint64_t)rows_pad};
+    const cuuint64_t strides[1] = {(cuuint64_t)a.stride};
+    const cuuint32_t box[2] = {(cuuint32_t)tc::BK, 128u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    CUresult r = g_encode(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(a.op), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+        return -1;
+    }
+    TcParams P{};
+    P.tiles = reinterpret_cast<const TcTile *>(tile_dev);
+    P.n_tiles = (int64_t)tiles.size();
+    P.rowinfo = a.rowinfo;
+    P.shard_base = a.shard_base;
+    P.shard_rowpad = a.shard_rowpad;
+    P.kblocks = a.shard_kblocks;
+    P.T = a.T;
+    P.sim = a.sim;
+    P.sim_base = a.sim_base;
+    const int grid = (int)std::min<int64_t>(a.num_sms, P.n_tiles);
+    k_syrk_tc<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(map, P);
+    return 0;
+}
+
 }  // namespace sad

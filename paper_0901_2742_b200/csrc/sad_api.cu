@@ -410,7 +410,8 @@ int sad_operand_size(const sad_ctx *cctx, size_t *bytes) {
     sad_ctx *ctx = const_cast<sad_ctx *>(cctx);
     GUARD(2);
     if (!bytes) return SAD_E_ARG;
-    *bytes = ctx->use_tc ? (size_t)ctx->rows_pad * (size_t)ctx->K_stride
+    *bytes = ctx->use_tc ? (size_t)ctx->rows_pad * (size_t)ctx->K_stride + 256 +
+                               (size_t)tc_tiles_bytes(ctx->pl, ctx->shard_base.data())
                          : (size_t)ctx->rows_pad * (size_t)ctx->V_pad * 2;
     return SAD_OK;
 }

@@ -114,6 +114,7 @@ struct AllPairsArgs {
 void launch_allpairs_alu(const AllPairsArgs &a, cudaStream_t st);
 int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err);
 bool tc_supported(std::string &why);
+int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base);
 
 struct AncArgs {
     const unsigned long long *T;
