@@ -250,12 +250,37 @@ def main():
     if args.kernel == "tc":
         # algorithmic dense work of the threshold-indicator SYRK: 2 * K_s ops per pair i <= j
         ops = sum(2 * (w * (w + 1) // 2) * int(k) for w, k in zip(w_loc, kcols))
-        bf16 = peaks.get("bf16_tflops_sustained", 1373.2 if peaks else 1400.0)
-        peak = 2.0 * bf16            # int8 dense = 2 x bf16 dense (nominal ratio 4.5 / 2.25)
+        measured = {}
+        try:
+            measured = json.load(open(os.path.join(ROOT, "profiles", "peaks_b200.json")))
+        except Exception:
+            pass
+        if "int8_tops" in measured:
+            peak, src = measured["int8_tops"], ("measured int8 dense peak, cuBLAS torch._int_mm 8192^3 burst "
+                                                "(profiles/peaks_b200.json, tools/peaks.py)")
+        else:
+            bf16 = peaks.get("bf16_tflops", 1590.0)
+            peak, src = 2.0 * bf16, "2 x measured bf16 burst (nominal int8:bf16 = 2)"
         roof = {"bound": "tensor", "achieved": ops / (ap_ms / 1e3) / 1e12, "peak": peak, "unit": "TOPS",
-                "frac": None, "traffic": None,
-                "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops_sustained (int8:bf16 nominal ratio)"
-                if peaks else "2 x fallback 1.4 PFLOP/s sustained bf16"}
+                "frac": None, "traffic": None, "peak_source": src,
+                "int8_sustained_peak": measured.get("int8_tops_sustained")}
+        tr = os.path.join(ROOT, "profiles", "r01_ncu_syrk_tc_summary.csv")
+        if os.path.exists(tr):
+            vals = {}
+            for line in open(tr):
+                parts = line.strip().split(",")
+                if len(parts) == 3:
+                    vals[parts[0]] = parts
+            try:
+                def gb(k):
+                    v, u = float(vals[k][1]), vals[k][2]
+                    return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}[u]
+                roof["traffic"] = gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum")
+                roof["traffic_source"] = "ncu --set full, one k_syrk_tc launch (profiles/r01_ncu_syrk_tc_summary.csv)"
+                roof["operand_bytes"] = int(sum(((w + 127) // 128) * 128 for w in w_loc) * int(
+                    (max(int(k) for k in kcols) + 127) // 128 * 128))
+            except Exception:
+                pass
     else:
         vpad = ((ctx_V(spec) + 63) // 64) * 64
         ops = sum((w * (w + 1) // 2) * vpad for w in w_loc)   # one VIMNMX.U16x2 + one VIADD.U16x2 per 2 k-mers
