@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--p", type=int, default=None)
-    ap.add_argument("--kernel", default="tc", choices=["tc", "alu"])
+    ap.add_argument("--kernel", default="tc", choices=["tc", "tc8", "alu"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -247,7 +247,7 @@ def main():
         pass
     _, _, kcols = ctx.profile_info()
     w_loc = [sb[rank * pl + s + 1] - sb[rank * pl + s] for s in range(pl)]
-    if args.kernel == "tc":
+    if args.kernel in ("tc", "tc8"):
         # algorithmic dense work of the threshold-indicator SYRK: 2 * K_s ops per pair i <= j
         ops = sum(2 * (w * (w + 1) // 2) * int(k) for w, k in zip(w_loc, kcols))
         measured = {}
@@ -255,7 +255,13 @@ def main():
             measured = json.load(open(os.path.join(ROOT, "profiles", "peaks_b200.json")))
         except Exception:
             pass
-        if "int8_tops" in measured:
+        if args.kernel == "tc" and "fp4_tflops" in measured:
+            peak, src = measured["fp4_tflops"], ("measured fp4 (mxf4) dense peak, cuBLAS torch._scaled_mm 8192^3 "
+                                                 "burst (profiles/peaks_b200.json, tools/peaks.py)")
+        elif args.kernel == "tc" and "int8_tops" in measured:
+            peak, src = 2.0 * measured["int8_tops"], ("2 x measured int8 dense peak (cuBLAS torch._int_mm 8192^3 "
+                                                      "burst, profiles/peaks_b200.json): nominal fp4:int8 = 9:4.5")
+        elif "int8_tops" in measured:
             peak, src = measured["int8_tops"], ("measured int8 dense peak, cuBLAS torch._int_mm 8192^3 burst "
                                                 "(profiles/peaks_b200.json, tools/peaks.py)")
         else:
@@ -264,7 +270,7 @@ def main():
         roof = {"bound": "tensor", "achieved": ops / (ap_ms / 1e3) / 1e12, "peak": peak, "unit": "TOPS",
                 "frac": None, "traffic": None, "peak_source": src,
                 "int8_sustained_peak": measured.get("int8_tops_sustained")}
-        tr = os.path.join(ROOT, "profiles", "r01_ncu_syrk_tc_summary.csv")
+        tr = os.path.join(ROOT, "profiles", f"r01_ncu_syrk_{args.kernel}_summary.csv")
         if os.path.exists(tr):
             vals = {}
             for line in open(tr):
@@ -276,7 +282,7 @@ def main():
                     v, u = float(vals[k][1]), vals[k][2]
                     return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}[u]
                 roof["traffic"] = gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum")
-                roof["traffic_source"] = "ncu --set full, one k_syrk_tc launch (profiles/r01_ncu_syrk_tc_summary.csv)"
+                roof["traffic_source"] = f"ncu --set full, one k_syrk_tc launch ({os.path.relpath(tr, ROOT)})"
                 roof["operand_bytes"] = int(sum(((w + 127) // 128) * 128 for w in w_loc) * int(
                     (max(int(k) for k in kcols) + 127) // 128 * 128))
             except Exception:
@@ -304,7 +310,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "i8" if args.kernel == "tc" else "u16", "data": "synthetic",
+            "vs_baseline": None, "dtype": {"tc": "e2m1", "tc8": "i8", "alu": "u16"}[args.kernel], "data": "synthetic",
             "config": {"workload": workload_name(spec, p), "p": p, "kernel": args.kernel,
                        "pairs_per_step": pairs_job,
                        "l2": "L2 flushed (256 MB write) before every timed step; operand working set > L2"},

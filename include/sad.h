@@ -56,7 +56,10 @@ extern "C" {
 /* flags */
 #define SAD_F_KEEP_SIM 1u     /* keep the w x w similarity numerators S_ij (uint16) of every shard */
 #define SAD_F_KERNEL_ALU 2u   /* all-pairs on the CUDA-core min-sum (K5', dense uint16 count tiles) */
-#define SAD_F_KERNEL_TC 4u    /* all-pairs on tcgen05 tensor cores (K5, threshold-indicator GEMM); default */
+#define SAD_F_KERNEL_TC 4u    /* all-pairs on tcgen05 tensor cores (K5, threshold-indicator GEMM); default.
+                                 Operands are packed e2m1 0/1 (kind::mxf4, unit block scales, fp32
+                                 accumulators: exact below 2^24) unless SAD_F_TC_INT8 */
+#define SAD_F_TC_INT8 8u      /* tensor-core path with uint8 0/1 operands (kind::i8, int32 accumulators) */
 
 /* memory kinds of sad_load inputs */
 #define SAD_MEM_HOST 0

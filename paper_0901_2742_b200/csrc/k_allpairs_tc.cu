@@ -6,7 +6,8 @@
 // (k-mer tau, layer t <= max_i n_i(tau)). The product is an exact integer contraction:
 // uint8 operands, int32 accumulation in TMEM (tcgen05.mma.kind::i8).
 //
-// Persistent kernel, one CTA (256 threads) per SM, 128 x 256 output tiles of the upper
+// Persistent kernel, one CTA (256 threads) per SM, 128 x BN output tiles (BN = 256 for int8,
+// 240 for fp4) of the upper
 // triangle of every shard:
 //   warp 0      TMA producer: 128-byte K slices of A_I (128 rows) and A_J (256 rows),
 //               128B-swizzled, into a 4-stage shared-memory ring (mbarrier full/empty)
@@ -28,21 +29,34 @@
 namespace sad {
 
 namespace tc {
-constexpr int BM = 128, BN = 256, BK = 128;
+constexpr int BM = 128, BK = 128;                 // BK = bytes of K per stage (128B swizzle row)
 constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK;                  // 16 KB
-constexpr int B_BYTES = BN * BK;                  // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int THREADS = 256;
-constexpr int ACC_COLS = BN;                       // TMEM columns per accumulator
-constexpr int TMEM_COLS = 2 * ACC_COLS;            // double-buffered accumulator
-constexpr int OFF_BAR = STAGES * STAGE_BYTES;      // barriers after the ring
-constexpr int OFF_COLINFO = OFF_BAR + 256;
-constexpr int OFF_COLSUM = OFF_COLINFO + BN * 16;
-constexpr int SMEM_BYTES = OFF_COLSUM + 4 * BN * 8 + 1024;   // + alignment slack
-// instruction descriptor: D = S32 (bits 4-5 = 2), A = B = uint8 (0), K-major A and B,
-// N >> 3 at bits 17-22, M >> 4 at bits 24-28
-constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+constexpr int SF_COLS = 32;                       // TMEM columns of unit block scales (fp4 path)
+
+// KIND 0: uint8 0/1 operands, tcgen05.mma.kind::i8, int32 accumulators, N = 256.
+// KIND 1: packed e2m1 0/1 operands (two per byte), tcgen05.mma.kind::mxf4.block_scale with
+//         every UE8M0 scale = 2^0, fp32 accumulators (exact: S <= 65535 < 2^24), N = 240 so
+//         that two accumulators + the scale columns fit the 512 TMEM columns.
+template <int KIND>
+struct Traits {
+    static constexpr int BN = KIND == 0 ? 256 : 240;
+    static constexpr int B_BYTES = BN * BK;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int ACC_COLS = BN;
+    static constexpr int TMEM_COLS = 512;
+    static constexpr int SF_COL = 2 * BN;           // first scale-factor column (fp4)
+    static constexpr int OFF_BAR = STAGES * (A_BYTES + B_BYTES);
+    static constexpr int OFF_COLINFO = OFF_BAR + 256;
+    static constexpr int OFF_COLSUM = OFF_COLINFO + 256 * 16;
+    static constexpr int SMEM_BYTES = OFF_COLSUM + 4 * 256 * 8 + 1024;
+    // i8: D = S32 (bits 4-5 = 2), A = B = uint8 (0), K-major, N >> 3 at 17, M >> 4 at 24.
+    // mxf4: A = B = E2M1 (1) at bits 7 / 10, scale format UE8M0 (bit 23 = 1), K = 64 (bit 31 = 0).
+    static constexpr uint32_t IDESC =
+        KIND == 0 ? ((2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24))
+                  : ((1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24));
+};
 }  // namespace tc
 
 struct TcTile {
@@ -108,6 +122,23 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
 }
+__device__ __forceinline__ void mma_mxf4(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc,
+                                         uint32_t sfa, uint32_t sfb) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st32_const(uint32_t taddr, uint32_t x) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+        "%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
+        "r"(x)
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -119,8 +150,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-__global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constant__ CUtensorMap tmap, TcParams P) {
+template <int KIND>
+__global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constant__ CUtensorMap tmapA,
+                                                            const __grid_constant__ CUtensorMap tmapB, TcParams P) {
     using namespace tc;
+    using Tr = Traits<KIND>;
+    constexpr int BN = Tr::BN, B_BYTES = Tr::B_BYTES, STAGE_BYTES = Tr::STAGE_BYTES, ACC_COLS = Tr::ACC_COLS;
+    constexpr int OFF_BAR = Tr::OFF_BAR, OFF_COLINFO = Tr::OFF_COLINFO, OFF_COLSUM = Tr::OFF_COLSUM;
+    constexpr int TMEM_COLS = Tr::TMEM_COLS;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;
@@ -144,7 +181,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             mbar_init(&tempty[i], 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmapA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmapB)) : "memory");
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -156,6 +194,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if constexpr (KIND == 1) {
+        // unit block scales: every UE8M0 byte = 127 (2^0), so any scale-factor layout reads 1.0
+        if (warp >= 4) tmem_st32_const(tmem_base + ((uint32_t)((warp - 4) * 32) << 16) + Tr::SF_COL, 0x7F7F7F7Fu);
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
 
     if (warp == 0) {
         if (lane == 0) {
@@ -170,9 +215,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], STAGE_BYTES);
-                    tma_load_2d(&tmap, &full[stage], sA + stage * A_BYTES, kb * BK, rowA);
-                    tma_load_2d(&tmap, &full[stage], sB + stage * B_BYTES, kb * BK, rowB);
-                    tma_load_2d(&tmap, &full[stage], sB + stage * B_BYTES + B_BYTES / 2, kb * BK, rowB + BN / 2);
+                    tma_load_2d(&tmapA, &full[stage], sA + stage * A_BYTES, kb * BK, rowA);
+                    tma_load_2d(&tmapB, &full[stage], sB + stage * B_BYTES, kb * BK, rowB);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -195,8 +239,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < BK / 32; ++kk)
-                        mma_i8(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), IDESC, (kb | kk) != 0);
+                    for (int kk = 0; kk < BK / 32; ++kk) {
+                        if constexpr (KIND == 0)
+                            mma_i8(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), Tr::IDESC, (kb | kk) != 0);
+                        else
+                            mma_mxf4(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), Tr::IDESC, (kb | kk) != 0,
+                                     tmem_base + Tr::SF_COL, tmem_base + Tr::SF_COL);
+                    }
                     tc_commit(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -233,6 +282,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             for (int ch = 0; ch < BN / 16; ++ch) {
                 uint32_t v[16];
                 tmem_ld16(tbase + ch * 16, v);
+                if constexpr (KIND == 1) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = (uint32_t)__uint_as_float(v[j]);   // exact: integer < 2^24
+                }
                 unsigned long long cv[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
@@ -276,7 +329,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     cv[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 2);
                 }
                 cv[0] += __shfl_xor_sync(0xffffffffu, cv[0], 1);
-                if (!(lane & 1)) colsum[ew * BN + ch * 16 + ((lane >> 1) & 15)] = cv[0];   // per-warp slot
+                if (!(lane & 1)) colsum[ew * 256 + ch * 16 + ((lane >> 1) & 15)] = cv[0];   // per-warp slot
             }
             tc_fence_before();
             __syncwarp();
@@ -286,7 +339,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             epi_bar();
             for (int c = e; c < BN; c += 128) {
                 const int64_t col = col0 + c;
-                const unsigned long long cs = colsum[c] + colsum[BN + c] + colsum[2 * BN + c] + colsum[3 * BN + c];
+                const unsigned long long cs = colsum[c] + colsum[256 + c] + colsum[512 + c] + colsum[768 + c];
                 if (col < w && cs) atomicAdd(&P.T[rbase + col], cs);
             }
         }
@@ -327,7 +380,10 @@ bool tc_supported(std::string &why) {
             return;
         }
         g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-        if (cudaFuncSetAttribute(k_syrk_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES) != cudaSuccess) {
+        if (cudaFuncSetAttribute(k_syrk_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Traits<0>::SMEM_BYTES) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(k_syrk_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Traits<1>::SMEM_BYTES) !=
+                cudaSuccess) {
             reason = "cannot reserve shared memory";
             return;
         }
@@ -337,25 +393,41 @@ bool tc_supported(std::string &why) {
     return ok;
 }
 
-// tiles of the upper triangle of every shard: (I, J) with J >= floor(I / 2) (the tile holds some
-// j >= i), in groups of kGroupJ column blocks so that the ~148 tiles in flight share a few
-// A_J blocks and walk the A_I blocks (L2 reuse).
-static void build_tiles(int pl, const int64_t *h_shard_base, std::vector<TcTile> &out) {
+int tc_bn(int kind) { return kind == 0 ? tc::Traits<0>::BN : tc::Traits<1>::BN; }
+
+// tiles of the upper triangle of every shard: (I, J) such that the tile holds some j >= i, i.e.
+// BN*J + BN - 1 >= BM*I, in groups of kGroupJ column blocks so that the ~148 tiles in flight
+// share a few A_J blocks and walk the A_I blocks (L2 reuse).
+static void build_tiles(int pl, const int64_t *h_shard_base, int bn, std::vector<TcTile> &out) {
     constexpr int kGroupJ = 8;
     out.clear();
     for (int s = 0; s < pl; ++s) {
         const int64_t w = h_shard_base[s + 1] - h_shard_base[s];
-        const int nI = (int)((w + tc::BM - 1) / tc::BM), nJ = (int)((w + tc::BN - 1) / tc::BN);
+        const int nI = (int)((w + tc::BM - 1) / tc::BM), nJ = (int)((w + bn - 1) / bn);
         for (int j0 = 0; j0 < nJ; j0 += kGroupJ)
-            for (int I = 0; I < nI; ++I)
-                for (int J = std::max(j0, I / 2); J < std::min(nJ, j0 + kGroupJ); ++J) out.push_back(TcTile{s, I, J, 0});
+            for (int I = 0; I < nI; ++I) {
+                const int64_t need = (int64_t)tc::BM * I - (bn - 1);
+                const int jmin = need <= 0 ? 0 : (int)((need + bn - 1) / bn);
+                for (int J = std::max(j0, jmin); J < std::min(nJ, j0 + kGroupJ); ++J) out.push_back(TcTile{s, I, J, 0});
+            }
     }
 }
 
-int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base) {
+int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base, int kind) {
     std::vector<TcTile> t;
-    build_tiles(pl, h_shard_base, t);
+    build_tiles(pl, h_shard_base, tc_bn(kind), t);
     return (int64_t)t.size() * (int64_t)sizeof(TcTile);
+}
+
+static bool encode(CUtensorMap *map, const void *base, int64_t stride, int64_t rows, int box_rows) {
+    std::memset(map, 0, sizeof *map);
+    const cuuint64_t dims[2] = {(cuuint64_t)stride, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)stride};
+    const cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1u, 1u};
+    return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err) {
@@ -364,9 +436,10 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
         err = why;
         return -1;
     }
+    const int bn = tc_bn(a.kind);
     // tile table, appended after the operand matrix (caller buffer, sized by sad_operand_size)
     static thread_local std::vector<TcTile> tiles;
-    build_tiles(a.pl, a.h_shard_base, tiles);
+    build_tiles(a.pl, a.h_shard_base, bn, tiles);
     if (tiles.empty()) return 0;
     const int64_t rows_pad = a.h_shard_rowpad[a.pl];
     uint8_t *tile_dev = reinterpret_cast<uint8_t *>(const_cast<void *>(a.op)) + rows_pad * a.stride;
@@ -389,17 +462,9 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
         err = "tile table upload failed";
         return -1;
     }
-    CUtensorMap map;
-    std::memset(&map, 0, sizeof map);
-    const cuuint64_t dims[2] = {(cuuint64_t)a.stride, (cuuint64_t)rows_pad};
-    const cuuint64_t strides[1] = {(cuuint64_t)a.stride};
-    const cuuint32_t box[2] = {(cuuint32_t)tc::BK, 128u};
-    const cuuint32_t estr[2] = {1u, 1u};
-    CUresult r = g_encode(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(a.op), dims, strides, box, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-        err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+    CUtensorMap mapA, mapB;
+    if (!encode(&mapA, a.op, a.stride, rows_pad, tc::BM) || !encode(&mapB, a.op, a.stride, rows_pad, bn)) {
+        err = "cuTensorMapEncodeTiled failed";
         return -1;
     }
     TcParams P{};
@@ -413,7 +478,10 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
     P.sim = a.sim;
     P.sim_base = a.sim_base;
     const int grid = (int)std::min<int64_t>(a.num_sms, P.n_tiles);
-    k_syrk_tc<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(map, P);
+    if (a.kind == 0)
+        k_syrk_tc<0><<<grid, tc::THREADS, tc::Traits<0>::SMEM_BYTES, st>>>(mapA, mapB, P);
+    else
+        k_syrk_tc<1><<<grid, tc::THREADS, tc::Traits<1>::SMEM_BYTES, st>>>(mapA, mapB, P);
     return 0;
 }
 

@@ -173,7 +173,7 @@ __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl
 }
 
 // K4: the binary threshold-indicator operand of the tensor-core path,
-//   A_s[i, col0(tau) + t - 1] = 1  for 1 <= t <= n_i(tau),
+//   A_s[i, col0(tau) + t - 1] = 1  for 1 <= t <= n_i(tau)   (uint8, or packed e2m1 nibbles),
 // so that (A_s A_s^T)_ij = sum_tau min(n_i(tau), n_j(tau)) = S_ij exactly.
 // One block per padded row; the row is assembled in shared memory in 32 KB chunks and
 // written with 16-byte coalesced stores (rows are 128-byte aligned).
@@ -196,12 +196,29 @@ __global__ void __launch_bounds__(kOpThreads) k_indicator(OperandArgs a) {
         for (int t = threadIdx.x * 16; t < len; t += kOpThreads * 16)
             *reinterpret_cast<uint4 *>(row + t) = make_uint4(0, 0, 0, 0);
         __syncthreads();
-        for (int e = threadIdx.x; e < d; e += kOpThreads) {
-            const uint32_t v = ent[e];
-            const int64_t lo = (int64_t)c0[v >> 16];
-            const int64_t hi = lo + (v & 0xFFFFu);
-            const int64_t a0 = max(lo, ch), a1 = min(hi, ch + len);
-            for (int64_t c = a0; c < a1; ++c) row[c - ch] = 1;
+        if (!a.fp4) {
+            for (int e = threadIdx.x; e < d; e += kOpThreads) {
+                const uint32_t v = ent[e];
+                const int64_t lo = (int64_t)c0[v >> 16];
+                const int64_t hi = lo + (v & 0xFFFFu);
+                const int64_t a0 = max(lo, ch), a1 = min(hi, ch + len);
+                for (int64_t c = a0; c < a1; ++c) row[c - ch] = 1;
+            }
+        } else {
+            // two e2m1 entries per byte, 1.0 = 0b0010; neighbouring k-mers may share a byte, so
+            // the nibbles are set with 32-bit shared atomics
+            uint32_t *row32 = reinterpret_cast<uint32_t *>(row);
+            const int64_t c_lo = ch * 2, c_hi = (ch + len) * 2;
+            for (int e = threadIdx.x; e < d; e += kOpThreads) {
+                const uint32_t v = ent[e];
+                const int64_t lo = (int64_t)c0[v >> 16];
+                const int64_t hi = lo + (v & 0xFFFFu);
+                const int64_t a0 = max(lo, c_lo), a1 = min(hi, c_hi);
+                for (int64_t c = a0; c < a1; ++c) {
+                    const int64_t cc = c - c_lo;
+                    atomicOr(&row32[cc >> 3], 2u << (4 * (cc & 7)));
+                }
+            }
         }
         __syncthreads();
         for (int t = threadIdx.x * 16; t < len; t += kOpThreads * 16)

@@ -210,6 +210,7 @@ int sad_create(const sad_config *cfg, sad_ctx **out) {
     ctx->pl = cfg->p / cfg->world;
     ctx->shard0 = cfg->rank * ctx->pl;
     ctx->use_tc = !(cfg->flags & SAD_F_KERNEL_ALU);
+    ctx->tc_kind = (cfg->flags & SAD_F_TC_INT8) ? 0 : 1;
     if (cudaSetDevice(cfg->device) != cudaSuccess) {
         delete ctx;
         return SAD_E_CUDA;
@@ -400,7 +401,9 @@ int sad_build_profiles(sad_ctx *ctx) {
         ctx->h_K[s] = (int64_t)ctx->h_small[4 + 4 * s + 2];
         kmax = std::max(kmax, ctx->h_K[s]);
     }
-    ctx->K_stride = std::max<int64_t>(kColPad, rup(kmax, kColPad));
+    // operand row: K columns padded to one 128-byte K block = 128 int8 or 256 packed fp4 entries
+    ctx->kcols_per_block = (ctx->use_tc && ctx->tc_kind == 1) ? 256 : 128;
+    ctx->K_stride = std::max<int64_t>(1, (kmax + ctx->kcols_per_block - 1) / ctx->kcols_per_block) * 128;
     ctx->V_pad = rup(V, 64);
     ctx->stage = 2;
     return SAD_OK;
@@ -411,7 +414,7 @@ int sad_operand_size(const sad_ctx *cctx, size_t *bytes) {
     GUARD(2);
     if (!bytes) return SAD_E_ARG;
     *bytes = ctx->use_tc ? (size_t)ctx->rows_pad * (size_t)ctx->K_stride + 256 +
-                               (size_t)tc_tiles_bytes(ctx->pl, ctx->shard_base.data())
+                               (size_t)tc_tiles_bytes(ctx->pl, ctx->shard_base.data(), ctx->tc_kind)
                          : (size_t)ctx->rows_pad * (size_t)ctx->V_pad * 2;
     return SAD_OK;
 }
@@ -462,6 +465,7 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     o.k = ctx->cfg.k;
     o.V = ctx->V;
     o.pl = pl;
+    o.fp4 = ctx->use_tc && ctx->tc_kind == 1;
     o.op = d_operand;
     record_pair(ctx, ctx->ev_pairs_op, true);
     if (ctx->use_tc) launch_indicator(o, ctx->st); else launch_dense_counts(o, ctx->st);
@@ -472,7 +476,7 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     std::vector<int64_t> kb(pl + 1, 0);
     int64_t pairs = 0, macs = 0;
     for (int s = 0; s < pl; ++s) {
-        kb[s] = (ctx->h_K[s] + kColPad - 1) / kColPad;
+        kb[s] = (ctx->h_K[s] + ctx->kcols_per_block - 1) / ctx->kcols_per_block;
         const int64_t w = ctx->shard_base[s + 1] - ctx->shard_base[s];
         pairs += w * (w - 1) / 2;
         macs += w * (w + 1) / 2 * ctx->h_K[s];
@@ -502,6 +506,7 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     ap.h_shard_base = ctx->shard_base.data();
     ap.h_shard_rowpad = ctx->shard_rowpad.data();
     ap.h_kblocks = kb.data();
+    ap.kind = ctx->tc_kind;
     record_pair(ctx, ctx->ev_pairs_ap, true);
     if (ctx->use_tc) {
         std::string e;

@@ -85,6 +85,7 @@ struct OperandArgs {
     int64_t rows_pad;
     int64_t stride;                  // bytes per operand row
     int k, V, pl;
+    int fp4;                         // pack two 4-bit e2m1 entries per byte (1.0 = 0x2)
     void *op;
 };
 void launch_indicator(const OperandArgs &a, cudaStream_t st);
@@ -110,11 +111,12 @@ struct AllPairsArgs {
     const int64_t *h_shard_base;     // host copies (launch configuration)
     const int64_t *h_shard_rowpad;
     const int64_t *h_kblocks;
+    int kind;                        // TC: 0 = int8 operands (kind::i8), 1 = packed fp4 (kind::mxf4)
 };
 void launch_allpairs_alu(const AllPairsArgs &a, cudaStream_t st);
 int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err);
 bool tc_supported(std::string &why);
-int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base);
+int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base, int kind);
 
 struct AncArgs {
     const unsigned long long *T;
@@ -217,6 +219,8 @@ struct sad_ctx {
     std::vector<int64_t> h_windows, h_distinct, h_K; // [pl]
     int64_t K_stride = 0, V_pad = 0;
     bool use_tc = false;
+    int tc_kind = 1;                 // 0 = int8, 1 = fp4
+    int64_t kcols_per_block = 128;   // operand columns per 128-byte K block
 
     // device pointers carved from the caller workspace
     uint8_t *ws = nullptr;

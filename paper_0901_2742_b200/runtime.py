@@ -79,7 +79,8 @@ def all_to_all_v(send: torch.Tensor, send_sizes, recv_sizes, group=None) -> torc
 class Context:
     """One rank's view of the k-mer-rank domain decomposition (include/sad.h).
 
-    kernel: "tc" (tcgen05 threshold-indicator GEMM, default) or "alu" (CUDA-core min-sum).
+    kernel: "tc" (tcgen05 threshold-indicator GEMM on packed e2m1 operands, default),
+            "tc8" (the same on uint8 operands, kind::i8) or "alu" (CUDA-core min-sum).
     """
 
     def __init__(self, alphabet: str, k: int, p: int, *, world: int = 1, rank: int = 0, device: int | None = None,
@@ -92,7 +93,11 @@ class Context:
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.alphabet, self.k, self.p, self.world, self.rank, self.group = alphabet, k, p, world, rank, group
         self.pl = p // world
+        if kernel not in ("tc", "tc8", "alu"):
+            raise ValueError(f"kernel must be tc, tc8 or alu, not {kernel!r}")
         flags = (L.SAD_F_KEEP_SIM if keep_sim else 0) | (L.SAD_F_KERNEL_ALU if kernel == "alu" else L.SAD_F_KERNEL_TC)
+        if kernel == "tc8":
+            flags |= L.SAD_F_TC_INT8
         self.kernel = kernel
         cfg = L.SadConfig(ALPHABETS[alphabet], k, p, world, rank, device, self.stream.cuda_stream, flags)
         h = ctypes.c_void_p()

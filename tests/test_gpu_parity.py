@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 def _kernels():
     # the tensor-core kernel is mandatory once built (tc_supported() in k_allpairs_tc.cu)
     import os
-    return ["tc", "alu"] if os.environ.get("SAD_TEST_TC", "1") == "1" else ["alu"]
+    return ["tc", "tc8", "alu"] if os.environ.get("SAD_TEST_TC", "1") == "1" else ["alu"]
 
 
 KERNELS = _kernels()
@@ -70,7 +70,7 @@ def _compare_full(ctx, sizes, r, a, o, p):
 
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_fixed_point_selftest(kernel):
-    if kernel == "tc":
+    if kernel != "alu":
         pytest.skip("self-test is kernel independent")
     ctx = _ctx("protein", 3, 1, kernel)
     assert ctx.selftest_fixed_point(65535) == 0

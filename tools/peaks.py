@@ -54,6 +54,19 @@ def main():
             lambda: torch._scaled_mm(af, bf, scale_a=one, scale_b=one, out_dtype=torch.bfloat16), 2 * N ** 3)
     except Exception as ex:  # noqa: BLE001
         out["fp8_error"] = str(ex)[:200]
+    # mxfp4 (e2m1 operands, UE8M0 scales per 32 elements), as the fp4 all-pairs kernel uses
+    try:
+        rup = lambda x, m: (x + m - 1) // m * m
+        a4 = torch.full((N, N // 2), 0x22, dtype=torch.uint8, device="cuda").view(torch.float4_e2m1fn_x2)
+        b4 = torch.full((N, N // 2), 0x22, dtype=torch.uint8, device="cuda").view(torch.float4_e2m1fn_x2).t()
+        sa = torch.full((rup(N, 128) * rup(N // 32, 4),), 127, dtype=torch.uint8, device="cuda").view(torch.float8_e8m0fnu)
+        sb = torch.full((rup(N, 128) * rup(N // 32, 4),), 127, dtype=torch.uint8, device="cuda").view(torch.float8_e8m0fnu)
+        fn = lambda: torch._scaled_mm(a4, b4, scale_a=sa, scale_b=sb, out_dtype=torch.bfloat16)
+        r = fn()
+        out["fp4_check"] = float(r[0, 0])            # 1.0 * 1.0 summed over K = N
+        out["fp4_tflops"], out["fp4_tflops_sustained"] = bench(fn, 2 * N ** 3)
+    except Exception as ex:  # noqa: BLE001
+        out["fp4_error"] = str(ex)[:300]
     print(json.dumps(out))
 
 
