@@ -14,7 +14,7 @@
 //   warp 1      MMA issuer: 4 x tcgen05.mma (M=128, N=256, K=32) per stage into one of two
 //               TMEM accumulators (2 x 256 columns), tcgen05.commit to release stages
 //   warp 2      TMEM allocator (512 columns)
-//   warps 4-7   fused epilogue, overlapped with the next tile's MMAs: tcgen05.ld of S,
+//   warps 4-11  fused epilogue (two warpgroups split the tile's columns), overlapped with the next tile's MMAs: tcgen05.ld of S,
 //               exact fixed point q = floor(2^32 S / den) (reading A5), row sums and
 //               column sums (warp transpose-reduce + per-warp shared slots) into T (u64 atomics,
 //               order independent: SURVEY A.5)
@@ -32,7 +32,7 @@ namespace tc {
 constexpr int BM = 128, BK = 128;                 // BK = bytes of K per stage (128B swizzle row)
 constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK;                  // 16 KB
-constexpr int THREADS = 256;
+constexpr int THREADS = 384;                   // warps 0-3: TMA, MMA, TMEM alloc, idle; 4-11: epilogue
 constexpr int SF_COLS = 32;                       // TMEM columns of unit block scales (fp4 path)
 
 // KIND 0: uint8 0/1 operands, tcgen05.mma.kind::i8, int32 accumulators, N = 256.
@@ -50,7 +50,8 @@ struct Traits {
     static constexpr int OFF_BAR = STAGES * (A_BYTES + B_BYTES);
     static constexpr int OFF_COLINFO = OFF_BAR + 256;
     static constexpr int OFF_COLSUM = OFF_COLINFO + 256 * 16;
-    static constexpr int SMEM_BYTES = OFF_COLSUM + 4 * 256 * 8 + 1024;
+    static constexpr int OFF_ROWPART = OFF_COLSUM + 4 * 256 * 8;
+    static constexpr int SMEM_BYTES = OFF_ROWPART + 128 * 8 + 1024;
     // i8: D = S32 (bits 4-5 = 2), A = B = uint8 (0), K-major, N >> 3 at 17, M >> 4 at 24.
     // mxf4: A = B = E2M1 (1) at bits 7 / 10, scale format UE8M0 (bit 23 = 1), K = 64 (bit 31 = 0).
     static constexpr uint32_t IDESC =
@@ -148,7 +149,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 template <int KIND>
 __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constant__ CUtensorMap tmapA,
@@ -158,8 +159,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
     constexpr int BN = Tr::BN, B_BYTES = Tr::B_BYTES, STAGE_BYTES = Tr::STAGE_BYTES, ACC_COLS = Tr::ACC_COLS;
     constexpr int OFF_BAR = Tr::OFF_BAR, OFF_COLINFO = Tr::OFF_COLINFO, OFF_COLSUM = Tr::OFF_COLSUM;
     constexpr int TMEM_COLS = Tr::TMEM_COLS;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment for the 128B-swizzled stages, kept as an offset from the __shared__
+    // array so that every access below compiles to LDS/STS
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *sA = smem;
     uint8_t *sB = smem + STAGES * A_BYTES;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
@@ -169,6 +172,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
     RowInfo *colinfo = reinterpret_cast<RowInfo *>(smem + OFF_COLINFO);
     unsigned long long *colsum = reinterpret_cast<unsigned long long *>(smem + OFF_COLSUM);
+    unsigned long long *rowpart = reinterpret_cast<unsigned long long *>(smem + Tr::OFF_ROWPART);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -178,7 +182,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], 8);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmapA)) : "memory");
@@ -196,7 +200,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
     const uint32_t tmem_base = *tmem_slot;
     if constexpr (KIND == 1) {
         // unit block scales: every UE8M0 byte = 127 (2^0), so any scale-factor layout reads 1.0
-        if (warp >= 4) tmem_st32_const(tmem_base + ((uint32_t)((warp - 4) * 32) << 16) + Tr::SF_COL, 0x7F7F7F7Fu);
+        if (warp >= 4 && warp < 8) tmem_st32_const(tmem_base + ((uint32_t)((warp - 4) * 32) << 16) + Tr::SF_COL, 0x7F7F7F7Fu);
         tc_fence_before();
         __syncthreads();
         tc_fence_after();
@@ -254,49 +258,62 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             }
         }
     } else if (warp >= 4) {
-        // ===== epilogue =====
-        const int ew = warp - 4;                  // TMEM lanes 32*ew .. 32*ew+31
-        const int e = threadIdx.x - 128;          // 0..127
+        // ===== epilogue: 8 warps = 2 warpgroups; warp%4 selects the TMEM lane quarter (rows),
+        // the warpgroup selects half of the tile's 16-column chunks =====
+        const int quarter = warp & 3;             // TMEM lanes 32*quarter .. +31
+        const int grp = (warp - 4) >> 2;          // 0 or 1
+        const int e = threadIdx.x - 128;          // 0..255
+        constexpr int NCH = BN / 16;
+        const int ch0 = grp ? (NCH + 1) / 2 : 0, ch1 = grp ? NCH : (NCH + 1) / 2;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
             const TcTile tl = P.tiles[t];
             const int64_t rbase = P.shard_base[tl.s];
             const int64_t w = P.shard_base[tl.s + 1] - rbase;
-            const int64_t col0 = (int64_t)tl.J * BN;
-            epi_bar();                            // previous tile's colinfo/colsum fully consumed
-            for (int c = e; c < BN; c += 128) {
-                const int64_t col = col0 + c;
-                colinfo[c] = col < w ? P.rowinfo[rbase + col] : RowInfo{1u, 0xFFFFFFFFu, 1u, 0u};
+            const int64_t col0 = (int64_t)tl.J * BN, row0 = (int64_t)tl.I * BM;
+            epi_bar();                            // previous tile's colinfo / colsum / rowpart consumed
+            if (e < BN) {
+                const int64_t col = col0 + e;
+                colinfo[e] = col < w ? P.rowinfo[rbase + col] : RowInfo{1u, 0xFFFFFFFFu, 1u, 0u};
             }
             epi_bar();
-            const int64_t row = (int64_t)tl.I * BM + ew * 32 + lane;
+            const int64_t row = row0 + quarter * 32 + lane;
             const bool vrow = row < w;
             const RowInfo ri = vrow ? P.rowinfo[rbase + row] : RowInfo{1u, 0xFFFFFFFFu, 1u, 0u};
+            // interior tile: every (row, col) is a real pair with col > row -> no masks
+            const bool interior = (row0 + BM <= w) && (col0 + BN <= w) && (col0 > row0 + BM - 1);
             uint16_t *simr = (P.sim && vrow) ? P.sim + P.sim_base[tl.s] : nullptr;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             unsigned long long rowsum = 0;
-            const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * ACC_COLS);
+            const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * ACC_COLS);
 #pragma unroll 1
-            for (int ch = 0; ch < BN / 16; ++ch) {
+            for (int ch = ch0; ch < ch1; ++ch) {
                 uint32_t v[16];
                 tmem_ld16(tbase + ch * 16, v);
-                if constexpr (KIND == 1) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = (uint32_t)__uint_as_float(v[j]);   // exact: integer < 2^24
-                }
                 unsigned long long cv[16];
+                if (interior && !P.sim) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int64_t col = col0 + ch * 16 + j;
-                    const bool ok = vrow && col < w && col >= row;
-                    const uint64_t q = ok ? pair_q(v[j], ri, colinfo[ch * 16 + j]) : 0ull;
-                    rowsum += q;
-                    cv[j] = (ok && col != row) ? q : 0ull;
-                    if (simr && ok) {
-                        simr[row * w + col] = (uint16_t)v[j];
-                        simr[col * w + row] = (uint16_t)v[j];
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t S = KIND == 1 ? (uint32_t)__uint_as_float(v[j]) : v[j];
+                        const uint64_t q = pair_q(S, ri, colinfo[ch * 16 + j]);
+                        rowsum += q;
+                        cv[j] = q;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t S = KIND == 1 ? (uint32_t)__uint_as_float(v[j]) : v[j];
+                        const int64_t col = col0 + ch * 16 + j;
+                        const bool ok = vrow && col < w && col >= row;
+                        const uint64_t q = pair_q(ok ? S : 0u, ri, colinfo[ch * 16 + j]);
+                        rowsum += q;
+                        cv[j] = (col != row) ? q : 0ull;
+                        if (simr && ok) {
+                            simr[row * w + col] = (uint16_t)S;
+                            simr[col * w + row] = (uint16_t)S;
+                        }
                     }
                 }
                 // warp transpose-reduce: after offsets 16, 8, 4, 2 lane l holds column (l >> 1) & 15
@@ -329,17 +346,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     cv[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 2);
                 }
                 cv[0] += __shfl_xor_sync(0xffffffffu, cv[0], 1);
-                if (!(lane & 1)) colsum[ew * 256 + ch * 16 + ((lane >> 1) & 15)] = cv[0];   // per-warp slot
+                if (!(lane & 1)) colsum[quarter * 256 + ch * 16 + ((lane >> 1) & 15)] = cv[0];
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-            if (vrow && rowsum) atomicAdd(&P.T[rbase + row], rowsum);
+            if (grp == 1) rowpart[quarter * 32 + lane] = rowsum;
             epi_bar();
-            for (int c = e; c < BN; c += 128) {
-                const int64_t col = col0 + c;
-                const unsigned long long cs = colsum[c] + colsum[256 + c] + colsum[512 + c] + colsum[768 + c];
+            if (grp == 0) {
+                rowsum += rowpart[quarter * 32 + lane];
+                if (vrow && rowsum) atomicAdd(&P.T[rbase + row], rowsum);
+            }
+            if (e < BN) {
+                const int64_t col = col0 + e;
+                const unsigned long long cs = colsum[e] + colsum[256 + e] + colsum[512 + e] + colsum[768 + e];
                 if (col < w && cs) atomicAdd(&P.T[rbase + col], cs);
             }
         }
