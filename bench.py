@@ -186,9 +186,11 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    R_loc = int(o_loc[-1])
+
     def step_device():
-        ctx.load(d_a, d_o, n, lo)
-        ctx.run()
+        ctx.load(d_a, d_o, n, lo, residues=R_loc)
+        ctx.run(sync=False)
 
     def step_e2e():
         ctx.load(h_a.numpy(), h_o.numpy(), n, lo)                   # H2D from pinned host memory

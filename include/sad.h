@@ -120,15 +120,19 @@ int sad_workspace_size(const sad_ctx *ctx, int64_t n_local, int64_t residues_loc
  * hold ceil(N/p) sequences, the rest floor(N/p)).
  *   ascii    [offsets[n_local]] residue bytes (host or device per mem)
  *   offsets  [n_local+1] int64, offsets[0] == 0, nondecreasing (host or device per mem)
+ *   residues_local  offsets[n_local] if known, else -1 (device offsets are then read back,
+ *            which costs a synchronization)
  *   mem      SAD_MEM_HOST (copied with cudaMemcpyAsync; synchronous w.r.t. the inputs) or
  *            SAD_MEM_DEVICE (copied device-to-device on the stream)
  *   d_ws     device workspace of at least sad_workspace_size(n_local, offsets[n_local]) bytes,
  *            256-byte aligned, owned by the caller, kept until the next sad_load or sad_destroy.
- * Inputs are copied; no input pointer is retained. Syncs (so host inputs may be reused on
- * return).
+ * Inputs are copied; no input pointer is retained. Syncs for host inputs (so they may be
+ * reused on return) and when the shard layout changed; device inputs of a known size and
+ * layout are copied asynchronously.
  */
 int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t n_local,
-             int64_t first_source_index, int64_t n_global, int32_t mem, void *d_ws, size_t ws_bytes);
+             int64_t first_source_index, int64_t n_global, int64_t residues_local, int32_t mem,
+             void *d_ws, size_t ws_bytes);
 
 /*
  * sad_build_profiles — k-mer count profiles n_x(tau) of every local sequence,
@@ -204,7 +208,8 @@ int sad_pack_plan(int32_t p, int32_t world, int32_t rank, const int64_t *h_count
 int sad_pack(sad_ctx *ctx, const int64_t *h_counts_all, uint64_t *d_send_meta, uint8_t *d_send_res);
 
 /* Bytes of the output buffer sad_finish needs on this rank (host only): the received
- * sequences' keys, offsets and residues plus merge scratch. */
+ * sequences' keys, offsets and residues plus merge scratch. h_counts_all may be NULL when
+ * world == 1 (the rank then receives exactly what it holds). */
 int sad_output_size(const sad_ctx *ctx, const int64_t *h_counts_all, size_t *bytes);
 
 /* Where sad_finish puts its results inside d_out: h_layout[0] = sequences n_out, [1] =
@@ -221,13 +226,19 @@ int sad_output_layout(const sad_ctx *ctx, const int64_t *h_counts_all, int64_t *
  *   sad_exchange_sizes). For world == 1 pass NULL for both: the local data is used in place.
  *   d_out / out_bytes  caller buffer of >= sad_output_size bytes, 256-byte aligned; it must
  *   stay valid while the getters below are used.
- *   h_bucket_sizes  [p] int64 out: sizes of ALL buckets (host, from h_counts_all)
- * Does not sync.
+ *   h_counts_all may be NULL when world == 1: the counts then stay on the device and are read
+ *   back lazily by the getters (no synchronization in the step).
+ *   h_bucket_sizes  [p] int64 out (may be NULL): sizes of ALL buckets; with h_counts_all == NULL
+ *   filling it synchronizes.
+ * Does not sync otherwise.
  */
 int sad_finish(sad_ctx *ctx, const int64_t *h_counts_all, const uint64_t *d_recv_meta,
                const uint8_t *d_recv_res, void *d_out, size_t out_bytes, int64_t *h_bucket_sizes);
 
 /* ---- getters (sync; copy device results into caller host buffers) ---- */
+
+/* Sizes of all p buckets (after sad_finish; P:188 load report). */
+int sad_get_bucket_sizes(sad_ctx *ctx, int64_t *h_sizes);
 
 /* T_i (uint64) of every sequence of local shard s (0 <= s < p/world), in input order. */
 int sad_get_local_rank(sad_ctx *ctx, int shard, uint64_t *h_T, int64_t cap);

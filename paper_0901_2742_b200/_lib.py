@@ -23,7 +23,7 @@ SYMBOLS = [
     "sad_load", "sad_build_profiles", "sad_operand_size", "sad_ancestor_record_bytes", "sad_rank_local",
     "sad_rank_global", "sad_partition_plan", "sad_exchange_sizes", "sad_pack_plan", "sad_pack", "sad_output_size",
     "sad_output_layout", "sad_finish", "sad_get_local_rank", "sad_get_ancestors", "sad_get_ranks", "sad_get_sorted",
-    "sad_get_pivots", "sad_get_bucket", "sad_get_similarity", "sad_get_profile_info", "sad_get_stats",
+    "sad_get_pivots", "sad_get_bucket", "sad_get_bucket_sizes", "sad_get_similarity", "sad_get_profile_info", "sad_get_stats",
     "sad_reset_stats", "sad_selftest_fixed_point",
 ]
 
@@ -60,7 +60,7 @@ def lib():
         "sad_last_error": (ctypes.c_char_p, [P]),
         "sad_error_location": (i32, [P, P, P]),
         "sad_workspace_size": (i32, [P, i64, i64, ctypes.POINTER(sz)]),
-        "sad_load": (i32, [P, P, P, i64, i64, i64, i32, P, sz]),
+        "sad_load": (i32, [P, P, P, i64, i64, i64, i64, i32, P, sz]),
         "sad_build_profiles": (i32, [P]),
         "sad_operand_size": (i32, [P, ctypes.POINTER(sz)]),
         "sad_ancestor_record_bytes": (sz, [P]),
@@ -79,6 +79,7 @@ def lib():
         "sad_get_sorted": (i32, [P, i32, P, i64]),
         "sad_get_pivots": (i32, [P, P]),
         "sad_get_bucket": (i32, [P, i32, P, P, P, P, i64, i64, P, P]),
+        "sad_get_bucket_sizes": (i32, [P, P]),
         "sad_get_similarity": (i32, [P, i32, P, i64]),
         "sad_get_profile_info": (i32, [P, P, P, P]),
         "sad_get_stats": (i32, [P, P, P]),

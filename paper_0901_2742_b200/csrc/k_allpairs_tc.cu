@@ -6,7 +6,7 @@
 // (k-mer tau, layer t <= max_i n_i(tau)). The product is an exact integer contraction:
 // uint8 operands, int32 accumulation in TMEM (tcgen05.mma.kind::i8).
 //
-// Persistent kernel, one CTA (256 threads) per SM, 128 x BN output tiles (BN = 256 for int8,
+// Persistent kernel, one CTA (384 threads) per SM, 128 x BN output tiles (BN = 256 for int8,
 // 240 for fp4) of the upper
 // triangle of every shard:
 //   warp 0      TMA producer: 128-byte K slices of A_I (128 rows) and A_J (256 rows),
@@ -440,6 +440,20 @@ int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base, int kind) {
     return (int64_t)t.size() * (int64_t)sizeof(TcTile);
 }
 
+// upper bound of the tile count for n rows in pl shards (workspace sizing before the layout is known)
+int64_t tc_tiles_bound(int64_t n, int pl) {
+    return (n / tc::BM + pl + 1) * (n / tc::Traits<1>::BN + pl + 1) + 1;
+}
+
+// the tile table of a layout, written to host memory (16 bytes per tile); returns the count
+int64_t tc_build_tiles(int pl, const int64_t *h_shard_base, int kind, void *host_out, int64_t cap) {
+    std::vector<TcTile> t;
+    build_tiles(pl, h_shard_base, tc_bn(kind), t);
+    if ((int64_t)t.size() > cap) return -1;
+    std::memcpy(host_out, t.data(), t.size() * sizeof(TcTile));
+    return (int64_t)t.size();
+}
+
 static bool encode(CUtensorMap *map, const void *base, int64_t stride, int64_t rows, int box_rows) {
     std::memset(map, 0, sizeof *map);
     const cuuint64_t dims[2] = {(cuuint64_t)stride, (cuuint64_t)rows};
@@ -458,39 +472,17 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
         return -1;
     }
     const int bn = tc_bn(a.kind);
-    // tile table, appended after the operand matrix (caller buffer, sized by sad_operand_size)
-    static thread_local std::vector<TcTile> tiles;
-    build_tiles(a.pl, a.h_shard_base, bn, tiles);
-    if (tiles.empty()) return 0;
+    (void)bn;
+    if (a.n_tiles_tc <= 0) return 0;
     const int64_t rows_pad = a.h_shard_rowpad[a.pl];
-    uint8_t *tile_dev = reinterpret_cast<uint8_t *>(const_cast<void *>(a.op)) + rows_pad * a.stride;
-    tile_dev = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tile_dev) + 255) & ~uintptr_t(255));
-    static thread_local TcTile *pinned = nullptr;
-    static thread_local size_t pinned_n = 0;
-    if (pinned_n < tiles.size()) {
-        if (pinned) { cudaStreamSynchronize(st); cudaFreeHost(pinned); }
-        pinned_n = tiles.size() * 2;
-        if (cudaMallocHost(&pinned, pinned_n * sizeof(TcTile)) != cudaSuccess) {
-            err = "pinned allocation failed";
-            pinned = nullptr;
-            pinned_n = 0;
-            return -1;
-        }
-    }
-    // the previous call's copy has been consumed: every step synchronizes in sad_build_profiles
-    std::memcpy(pinned, tiles.data(), tiles.size() * sizeof(TcTile));
-    if (cudaMemcpyAsync(tile_dev, pinned, tiles.size() * sizeof(TcTile), cudaMemcpyHostToDevice, st) != cudaSuccess) {
-        err = "tile table upload failed";
-        return -1;
-    }
     CUtensorMap mapA, mapB;
     if (!encode(&mapA, a.op, a.stride, rows_pad, tc::BM) || !encode(&mapB, a.op, a.stride, rows_pad, bn)) {
         err = "cuTensorMapEncodeTiled failed";
         return -1;
     }
     TcParams P{};
-    P.tiles = reinterpret_cast<const TcTile *>(tile_dev);
-    P.n_tiles = (int64_t)tiles.size();
+    P.tiles = reinterpret_cast<const TcTile *>(a.tiles);
+    P.n_tiles = a.n_tiles_tc;
     P.rowinfo = a.rowinfo;
     P.shard_base = a.shard_base;
     P.shard_rowpad = a.shard_rowpad;

@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kRankThreads) k_rank_vs_ga(RankArgs a) {
             a.den_ga[i] = den;
             a.key[i] = (q << 31) + (uint64_t)(a.first_idx + i);
             a.perm_in[i] = (int32_t)i;
+            if (a.ckey) a.ckey[i] = ((uint64_t)ri.shard << (33 + a.ib)) | (q << a.ib) | (uint64_t)i;
         }
     }
 }
@@ -373,6 +374,89 @@ void launch_gather_out(const int32_t *perm, int64_t n, const int64_t *src_off, c
     int64_t grid = (n + 7) / 8;
     if (grid > 148 * 16) grid = 148 * 16;
     if (grid > 0) k_gather_out<<<(unsigned)grid, 256, 0, st>>>(perm, n, src_off, src_res, dst_off, dst_res);
+}
+
+
+// unpack the sorted composite keys (shard | q | row) into the real keys and rows
+__global__ void k_unpack_sorted(const unsigned long long *ck, int64_t n, int ib, int64_t first_idx,
+                                unsigned long long *key_sorted, int32_t *perm_sorted) {
+    const unsigned long long rmask = (1ull << ib) - 1ull, qmask = (1ull << 33) - 1ull;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long c = ck[t];
+        const int64_t row = (int64_t)(c & rmask);
+        const unsigned long long q = (c >> ib) & qmask;
+        key_sorted[t] = (q << 31) + (unsigned long long)(first_idx + row);
+        perm_sorted[t] = (int32_t)row;
+    }
+}
+
+void launch_unpack_sorted(const unsigned long long *ckey_sorted, int64_t n, int ib, int64_t first_idx,
+                          unsigned long long *key_sorted, int32_t *perm_sorted, cudaStream_t st) {
+    if (n > 0) k_unpack_sorted<<<grid1d(n), 256, 0, st>>>(ckey_sorted, n, ib, first_idx, key_sorted, perm_sorted);
+}
+
+// K14: merge by ranking. Keys are unique, every run is sorted, so the output slot of an element is
+// the number of keys smaller than it: its position in its own run plus a lower_bound in every
+// other run.
+__global__ void __launch_bounds__(256) k_rank_merge(MergeArgs a) {
+    __shared__ int64_t rs[65];
+    for (int r = threadIdx.x; r <= a.nr; r += blockDim.x) rs[r] = a.run_start[r];
+    __syncthreads();
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < a.n; t += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long kt = a.keys[t * a.kstride];
+        int64_t pos = 0;
+        for (int r = 0; r < a.nr; ++r) {
+            int64_t lo = rs[r], hi = rs[r + 1];
+            if (t >= lo && t < hi) {
+                pos += t - lo;
+                continue;
+            }
+            const int64_t base = lo;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (a.keys[mid * a.kstride] < kt) lo = mid + 1; else hi = mid;
+            }
+            pos += lo - base;
+        }
+        const int64_t L = a.lens ? (int64_t)a.lens[t * a.lstride] : (int64_t)a.rowinfo[a.perm[t]].tw + a.k - 1;
+        a.out_key[pos] = kt;
+        a.out_len[pos] = L;
+        a.out_src[pos] = (int32_t)t;
+    }
+}
+
+void launch_rank_merge(const MergeArgs &a, cudaStream_t st) {
+    if (a.n > 0) k_rank_merge<<<grid1d(a.n), 256, 0, st>>>(a);
+}
+
+__global__ void __launch_bounds__(256) k_gather_res(const int32_t *out_src, const int32_t *perm, int64_t n,
+                                                    const int64_t *src_off, const uint8_t *src_res,
+                                                    const int64_t *dst_off, uint8_t *dst_res) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    for (int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); r < n; r += nw) {
+        const int32_t t = out_src[r];
+        const uint8_t *src = src_res + src_off[perm ? perm[t] : t];
+        uint8_t *dst = dst_res + dst_off[r];
+        const int64_t L = dst_off[r + 1] - dst_off[r];
+        for (int64_t c = lane; c < L; c += 32) dst[c] = src[c];
+    }
+}
+
+void launch_gather_res(const int32_t *out_src, const int32_t *perm, int64_t n, const int64_t *src_off,
+                       const uint8_t *src_res, const int64_t *dst_off, uint8_t *dst_res, cudaStream_t st) {
+    int64_t grid = (n + 7) / 8;
+    if (grid > 148 * 16) grid = 148 * 16;
+    if (grid > 0) k_gather_res<<<(unsigned)grid, 256, 0, st>>>(out_src, perm, n, src_off, src_res, dst_off, dst_res);
+}
+
+__global__ void k_lens_recv(const unsigned long long *m, int64_t n, int64_t *len) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        len[i] = (int64_t)m[2 * i + 1];
+}
+
+void launch_lens_recv(const unsigned long long *recv_meta, int64_t n, int64_t *len, cudaStream_t st) {
+    if (n > 0) k_lens_recv<<<grid1d(n), 256, 0, st>>>(recv_meta, n, len);
 }
 
 // ---------------------------------------------------------------------------------------

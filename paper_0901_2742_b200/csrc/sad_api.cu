@@ -91,8 +91,8 @@ size_t cub_bytes_needed(int64_t n, int pl) {
                                              (unsigned long long *)nullptr, (const int32_t *)nullptr,
                                              (int32_t *)nullptr, (int)std::max<int64_t>(n, 1), pl,
                                              (const int64_t *)nullptr, (const int64_t *)nullptr, 0, 64);
-    cub::DeviceRadixSort::SortPairs(nullptr, b, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
-                                    (const int32_t *)nullptr, (int32_t *)nullptr, (int)std::max<int64_t>(n, 1), 0, 64);
+    cub::DeviceRadixSort::SortKeys(nullptr, b, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                   (int)std::max<int64_t>(n, 1), 0, 64);
     return std::max(a, b) + 1024;
 }
 
@@ -122,12 +122,18 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_den_ga = b.take<uint32_t>((size_t)n);
     c->d_key = b.take<unsigned long long>((size_t)n);
     c->d_key_sorted = b.take<unsigned long long>((size_t)n);
+    c->d_ckey = b.take<unsigned long long>((size_t)n);
+    c->d_ckey_sorted = b.take<unsigned long long>((size_t)n);
+    c->d_runs = b.take<int64_t>((size_t)p + 1);
     c->d_perm_in = b.take<int32_t>((size_t)n);
     c->d_perm_sorted = b.take<int32_t>((size_t)n);
     c->d_pivots = b.take<unsigned long long>((size_t)p);
     c->d_bnd = b.take<int64_t>((size_t)pl * p);
     c->d_lpre = b.take<int64_t>((size_t)n + pl);
     c->d_seg = b.take<int64_t>((size_t)pl * p * 2);
+    c->d_counts = b.take<int64_t>((size_t)pl * p * 2);
+    c->tc_tiles_cap = tc_tiles_bound(n, pl);
+    c->d_tc_tiles = b.take<uint8_t>((size_t)c->tc_tiles_cap * 16);
     c->cub_bytes = cub_bytes_needed(n, pl);
     c->d_cub = b.take<uint8_t>(c->cub_bytes);
     if (c->cfg.flags & SAD_F_KEEP_SIM) {
@@ -174,6 +180,11 @@ OutLayout out_layout(uint8_t *base, int64_t n, int64_t r) {
 
 void sum_recv(const sad_ctx *c, const int64_t *h_counts_all, int64_t &n_out, int64_t &r_out) {
     const int p = c->cfg.p, bpr = c->pl;
+    if (!h_counts_all) {          // world == 1: this rank receives exactly what it holds
+        n_out = c->n;
+        r_out = c->R;
+        return;
+    }
     n_out = r_out = 0;
     for (int s = 0; s < p; ++s)
         for (int b = c->shard0; b < c->shard0 + bpr; ++b) {
@@ -185,6 +196,8 @@ void sum_recv(const sad_ctx *c, const int64_t *h_counts_all, int64_t &n_out, int
 }  // namespace
 
 extern "C" {
+
+static void bucket_sizes_from_counts(sad_ctx *ctx);
 
 uint32_t sad_abi_version(void) { return SAD_ABI_VERSION; }
 
@@ -239,6 +252,7 @@ void sad_destroy(sad_ctx *ctx) {
     for (auto &v : {&ctx->ev_pairs_ap, &ctx->ev_pairs_op, &ctx->ev_free})
         for (auto &e : *v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     if (ctx->h_small) cudaFreeHost(ctx->h_small);
+    if (ctx->h_tiles) cudaFreeHost(ctx->h_tiles);
     delete ctx;
 }
 
@@ -263,7 +277,7 @@ int sad_workspace_size(const sad_ctx *cctx, int64_t n_local, int64_t residues_lo
 }
 
 int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t n_local, int64_t first_source_index,
-             int64_t n_global, int32_t mem, void *d_ws, size_t ws_bytes) {
+             int64_t n_global, int64_t residues_local, int32_t mem, void *d_ws, size_t ws_bytes) {
     GUARD(0);
     if (!offsets || !d_ws || n_local < 0 || n_global < 0 || (mem != SAD_MEM_HOST && mem != SAD_MEM_DEVICE))
         return fail(ctx, SAD_E_ARG, "sad_load: bad arguments");
@@ -280,13 +294,16 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
                     (long long)(first_index_of_rank(ctx, n_global) + sb[ctx->pl]), (long long)n_local,
                     (long long)first_source_index);
     if (n_local == 0) return fail(ctx, SAD_E_EMPTY, "rank has no sequences");
-    int64_t R = 0;
+    int64_t R = residues_local;
+    bool need_sync = mem == SAD_MEM_HOST;     // host inputs may be reused by the caller on return
     if (mem == SAD_MEM_HOST) {
-        R = offsets[n_local];
         if (offsets[0] != 0) return fail(ctx, SAD_E_ARG, "offsets[0] != 0");
-    } else {
-        CK(cudaMemcpyAsync(&R, offsets + n_local, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->st));
+        if (R >= 0 && R != offsets[n_local]) return fail(ctx, SAD_E_ARG, "residues_local != offsets[n_local]");
+        R = offsets[n_local];
+    } else if (R < 0) {
+        CK(cudaMemcpyAsync(ctx->h_small + 40000, offsets + n_local, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
+        R = (int64_t)ctx->h_small[40000];
     }
     if (R > 0 && !ascii) return fail(ctx, SAD_E_ARG, "ascii is NULL");
     const size_t need = carve(ctx, nullptr, n_local, R);
@@ -313,32 +330,52 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
     const cudaMemcpyKind kind = mem == SAD_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     if (R > 0) CK(cudaMemcpyAsync(ctx->d_ascii, ascii, (size_t)R, kind, ctx->st));
     CK(cudaMemcpyAsync(ctx->d_off, offsets, sizeof(int64_t) * (size_t)(n_local + 1), kind, ctx->st));
-    // small per-shard tables
-    std::vector<int64_t> tbl(5 * (ctx->pl + 1), 0);
-    int64_t simb = 0, tiles = 0;
-    for (int s = 0; s <= ctx->pl; ++s) {
-        tbl[s] = sb[s];
-        tbl[(ctx->pl + 1) + s] = ctx->shard_rowpad[s];
-        tbl[3 * (ctx->pl + 1) + s] = simb;
-        tbl[4 * (ctx->pl + 1) + s] = tiles;
-        if (s < ctx->pl) {
-            const int64_t w = sb[s + 1] - sb[s];
-            simb += w * w;
-            const int64_t nt = (w + 63) / 64;
-            tiles += nt * (nt + 1) / 2;
+    // small per-shard tables (uploaded only when the layout changes)
+    const bool same = ctx->tbl_ws == base && ctx->tbl_n == n_local && ctx->tbl_ng == n_global &&
+                      ctx->tbl_first == first_source_index;
+    if (!same) {
+        int64_t *tbl = reinterpret_cast<int64_t *>(ctx->h_small + 32768);
+        int64_t simb = 0, tiles = 0;
+        for (int s = 0; s <= ctx->pl; ++s) {
+            tbl[s] = sb[s];
+            tbl[(ctx->pl + 1) + s] = ctx->shard_rowpad[s];
+            tbl[2 * (ctx->pl + 1) + s] = simb;
+            tbl[3 * (ctx->pl + 1) + s] = tiles;
+            if (s < ctx->pl) {
+                const int64_t w = sb[s + 1] - sb[s];
+                simb += w * w;
+                const int64_t nt = (w + 63) / 64;
+                tiles += nt * (nt + 1) / 2;
+            }
         }
+        ctx->alu_tiles = tiles;
+        if (ctx->use_tc) {           // the tensor-core tile table of this layout
+            const size_t need_b = (size_t)ctx->tc_tiles_cap * 16;
+            if (ctx->h_tiles_bytes < need_b) {
+                if (ctx->h_tiles) cudaFreeHost(ctx->h_tiles);
+                ctx->h_tiles = nullptr;
+                ctx->h_tiles_bytes = 0;
+                CK(cudaMallocHost(&ctx->h_tiles, need_b));
+                ctx->h_tiles_bytes = need_b;
+            }
+            ctx->tc_tiles_n = tc_build_tiles(ctx->pl, sb.data(), ctx->tc_kind, ctx->h_tiles, ctx->tc_tiles_cap);
+            if (ctx->tc_tiles_n < 0) return fail(ctx, SAD_E_OOM, "tile table exceeds its bound");
+            if (ctx->tc_tiles_n > 0)
+                CK(cudaMemcpyAsync(ctx->d_tc_tiles, ctx->h_tiles, (size_t)ctx->tc_tiles_n * 16, cudaMemcpyHostToDevice,
+                                   ctx->st));
+        }
+        const size_t tb = sizeof(int64_t) * (ctx->pl + 1);
+        CK(cudaMemcpyAsync(ctx->d_shard_base, tbl, tb, cudaMemcpyHostToDevice, ctx->st));
+        CK(cudaMemcpyAsync(ctx->d_shard_rowpad, tbl + (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
+        CK(cudaMemcpyAsync(ctx->d_sim_base, tbl + 2 * (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
+        CK(cudaMemcpyAsync(ctx->d_tile_base, tbl + 3 * (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
+        ctx->tbl_ws = base;
+        ctx->tbl_n = n_local;
+        ctx->tbl_ng = n_global;
+        ctx->tbl_first = first_source_index;
+        need_sync = true;
     }
-    ctx->alu_tiles = tiles;
-    std::memcpy(ctx->h_small, tbl.data(), tbl.size() * sizeof(int64_t));
-    CK(cudaMemcpyAsync(ctx->d_shard_base, ctx->h_small, sizeof(int64_t) * (ctx->pl + 1), cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaMemcpyAsync(ctx->d_shard_rowpad, ctx->h_small + (ctx->pl + 1), sizeof(int64_t) * (ctx->pl + 1),
-                       cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaMemcpyAsync(ctx->d_sim_base, ctx->h_small + 3 * (ctx->pl + 1), sizeof(int64_t) * (ctx->pl + 1),
-                       cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaMemcpyAsync(ctx->d_tile_base, ctx->h_small + 4 * (ctx->pl + 1), sizeof(int64_t) * (ctx->pl + 1),
-                       cudaMemcpyHostToDevice, ctx->st));
-    // the host inputs and the pinned staging may be reused on return
-    CK(cudaStreamSynchronize(ctx->st));
+    if (need_sync) CK(cudaStreamSynchronize(ctx->st));
     ctx->stage = 1;
     ctx->launches_step = 0;
     return SAD_OK;
@@ -413,8 +450,7 @@ int sad_operand_size(const sad_ctx *cctx, size_t *bytes) {
     sad_ctx *ctx = const_cast<sad_ctx *>(cctx);
     GUARD(2);
     if (!bytes) return SAD_E_ARG;
-    *bytes = ctx->use_tc ? (size_t)ctx->rows_pad * (size_t)ctx->K_stride + 256 +
-                               (size_t)tc_tiles_bytes(ctx->pl, ctx->shard_base.data(), ctx->tc_kind)
+    *bytes = ctx->use_tc ? (size_t)ctx->rows_pad * (size_t)ctx->K_stride
                          : (size_t)ctx->rows_pad * (size_t)ctx->V_pad * 2;
     return SAD_OK;
 }
@@ -507,6 +543,8 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     ap.h_shard_rowpad = ctx->shard_rowpad.data();
     ap.h_kblocks = kb.data();
     ap.kind = ctx->tc_kind;
+    ap.tiles = ctx->d_tc_tiles;
+    ap.n_tiles_tc = ctx->tc_tiles_n;
     record_pair(ctx, ctx->ev_pairs_ap, true);
     if (ctx->use_tc) {
         std::string e;
@@ -561,15 +599,32 @@ int sad_rank_global(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out
     r.den_ga = ctx->d_den_ga;
     r.key = ctx->d_key;
     r.perm_in = ctx->d_perm_in;
+    // a7: one radix sort of composite keys (shard | q | row) when they fit 64 bits, else a
+    // segmented sort of the real keys
+    int ib = 1, sbits = 0;
+    while ((int64_t(1) << ib) < ctx->n) ++ib;
+    while ((1 << sbits) < ctx->pl) ++sbits;
+    const int cbits = sbits + 33 + ib;
+    r.ib = ib;
+    r.ckey = cbits <= 64 ? ctx->d_ckey : nullptr;
     launch_ga_pairs(r, ctx->st);
     LAUNCHED();
     launch_rank_vs_ga(r, ctx->st);
     LAUNCHED();
     size_t tb = ctx->cub_bytes;
-    CK(cub::DeviceSegmentedRadixSort::SortPairs(ctx->d_cub, tb, ctx->d_key, ctx->d_key_sorted, ctx->d_perm_in,
-                                                ctx->d_perm_sorted, (int)ctx->n, ctx->pl, ctx->d_shard_base,
-                                                ctx->d_shard_base + 1, 0, 64, ctx->st));
-    LAUNCHED();
+    if (r.ckey) {
+        CK(cub::DeviceRadixSort::SortKeys(ctx->d_cub, tb, ctx->d_ckey, ctx->d_ckey_sorted, (int)ctx->n, 0, cbits,
+                                          ctx->st));
+        LAUNCHED();
+        launch_unpack_sorted(ctx->d_ckey_sorted, ctx->n, ib, ctx->first_idx, ctx->d_key_sorted, ctx->d_perm_sorted,
+                             ctx->st);
+        LAUNCHED();
+    } else {
+        CK(cub::DeviceSegmentedRadixSort::SortPairs(ctx->d_cub, tb, ctx->d_key, ctx->d_key_sorted, ctx->d_perm_in,
+                                                    ctx->d_perm_sorted, (int)ctx->n, ctx->pl, ctx->d_shard_base,
+                                                    ctx->d_shard_base + 1, 0, 64, ctx->st));
+        LAUNCHED();
+    }
     if (p > 1) {
         launch_samples(ctx->d_key_sorted, ctx->d_shard_base, ctx->pl, p,
                        reinterpret_cast<unsigned long long *>(d_samples_out), ctx->st);
@@ -598,6 +653,8 @@ int sad_partition_plan(sad_ctx *ctx, const uint64_t *d_samples_all, int64_t *d_c
     a.counts = d_counts_out;
     launch_plan(a, ctx->st);
     LAUNCHED();
+    CK(cudaMemcpyAsync(ctx->d_counts, d_counts_out, sizeof(int64_t) * (size_t)ctx->pl * p * 2,
+                       cudaMemcpyDeviceToDevice, ctx->st));
     ctx->stage = 5;
     return SAD_OK;
 }
@@ -676,7 +733,7 @@ int sad_pack(sad_ctx *ctx, const int64_t *h_counts_all, uint64_t *d_send_meta, u
 int sad_output_size(const sad_ctx *cctx, const int64_t *h_counts_all, size_t *bytes) {
     sad_ctx *ctx = const_cast<sad_ctx *>(cctx);
     GUARD(5);
-    if (!h_counts_all || !bytes) return SAD_E_ARG;
+    if ((!h_counts_all && ctx->cfg.world != 1) || !bytes) return SAD_E_ARG;
     int64_t n_out, r_out;
     sum_recv(ctx, h_counts_all, n_out, r_out);
     *bytes = out_layout(nullptr, n_out, r_out).total;
@@ -686,7 +743,7 @@ int sad_output_size(const sad_ctx *cctx, const int64_t *h_counts_all, size_t *by
 int sad_output_layout(const sad_ctx *cctx, const int64_t *h_counts_all, int64_t *h_layout) {
     sad_ctx *ctx = const_cast<sad_ctx *>(cctx);
     GUARD(5);
-    if (!h_counts_all || !h_layout) return SAD_E_ARG;
+    if ((!h_counts_all && ctx->cfg.world != 1) || !h_layout) return SAD_E_ARG;
     int64_t n_out, r_out;
     sum_recv(ctx, h_counts_all, n_out, r_out);
     OutLayout o = out_layout(nullptr, n_out, r_out);
@@ -703,67 +760,130 @@ int sad_finish(sad_ctx *ctx, const int64_t *h_counts_all, const uint64_t *d_recv
                void *d_out, size_t out_bytes, int64_t *h_bucket_sizes) {
     GUARD(5);
     const int p = ctx->cfg.p;
-    if (!h_counts_all || !d_out) return fail(ctx, SAD_E_ARG, "sad_finish: NULL buffer");
+    if ((!h_counts_all && ctx->cfg.world != 1) || !d_out) return fail(ctx, SAD_E_ARG, "sad_finish: NULL buffer");
     if ((reinterpret_cast<uintptr_t>(d_out) & 255) != 0) return fail(ctx, SAD_E_ARG, "output must be 256-byte aligned");
     const bool local = d_recv_meta == nullptr;
     if (local && ctx->cfg.world != 1) return fail(ctx, SAD_E_ARG, "NULL receive buffers need world == 1");
     int64_t n_out, r_out;
     sum_recv(ctx, h_counts_all, n_out, r_out);
-    if (local && (n_out != ctx->n || r_out != ctx->R)) return fail(ctx, SAD_E_STATE, "counts do not cover the input");
+    if (local && h_counts_all && (n_out != ctx->n || r_out != ctx->R))
+        return fail(ctx, SAD_E_STATE, "counts do not cover the input");
     OutLayout o = out_layout(reinterpret_cast<uint8_t *>(d_out), n_out, r_out);
     if (out_bytes < o.total) return fail(ctx, SAD_E_CAPACITY, "output %zu < %zu bytes", out_bytes, o.total);
     const int nn = (int)n_out;
+    // K14: merge the sorted runs by ranking (every owned bucket is a key range, so the merged
+    // order is the bucket order and each bucket is in key order), then move the residues
+    MergeArgs m{};
+    m.n = n_out;
+    m.k = ctx->cfg.k;
+    m.out_key = o.key;
+    m.out_len = o.len_in;
+    m.out_src = o.perm;
     const int64_t *src_off;
+    const int32_t *src_perm;
     const uint8_t *src_res;
-    if (local) {
-        launch_meta_from_local(ctx->d_key, ctx->d_rowinfo, ctx->cfg.k, n_out, o.keys_in, o.vals_in, o.len_in, ctx->st);
-        LAUNCHED();
+    if (local) {                          // runs = this rank's sorted shards
+        m.keys = ctx->d_key_sorted;
+        m.kstride = 1;
+        m.run_start = ctx->d_shard_base;
+        m.nr = ctx->pl;
+        m.perm = ctx->d_perm_sorted;
+        m.rowinfo = ctx->d_rowinfo;
         src_off = ctx->d_off;
+        src_perm = ctx->d_perm_sorted;
         src_res = ctx->d_ascii;
-    } else {
+    } else {                              // runs = the source shards, in rank (= shard) order
         if (n_out > 0 && (!d_recv_meta || (r_out > 0 && !d_recv_res)))
             return fail(ctx, SAD_E_ARG, "sad_finish: NULL receive buffer");
-        launch_meta_from_recv(reinterpret_cast<const unsigned long long *>(d_recv_meta), n_out, o.keys_in, o.vals_in,
-                              o.len_in, ctx->st);
+        int64_t *runs = reinterpret_cast<int64_t *>(ctx->h_small + 16384);
+        runs[0] = 0;
+        for (int s = 0; s < p; ++s) {
+            int64_t c = 0;
+            for (int b = ctx->shard0; b < ctx->shard0 + ctx->pl; ++b) c += h_counts_all[((size_t)s * p + b) * 2];
+            runs[s + 1] = runs[s] + c;
+        }
+        CK(cudaMemcpyAsync(ctx->d_runs, runs, sizeof(int64_t) * (p + 1), cudaMemcpyHostToDevice, ctx->st));
+        m.keys = reinterpret_cast<const unsigned long long *>(d_recv_meta);
+        m.kstride = 2;
+        m.lens = reinterpret_cast<const unsigned long long *>(d_recv_meta) + 1;
+        m.lstride = 2;
+        m.run_start = ctx->d_runs;
+        m.nr = p;
+        launch_lens_recv(reinterpret_cast<const unsigned long long *>(d_recv_meta), n_out, o.len_sorted, ctx->st);
         LAUNCHED();
         if (n_out > 0) {
             size_t tb = o.cub_bytes;
-            CK(cub::DeviceScan::ExclusiveSum(o.cub, tb, o.len_in, o.src_off, nn, ctx->st));
+            CK(cub::DeviceScan::ExclusiveSum(o.cub, tb, o.len_sorted, o.src_off, nn, ctx->st));
             LAUNCHED();
         }
         src_off = o.src_off;
+        src_perm = nullptr;
         src_res = d_recv_res;
     }
     CK(cudaMemsetAsync(o.off, 0, sizeof(int64_t), ctx->st));
     if (n_out > 0) {
+        launch_rank_merge(m, ctx->st);
+        LAUNCHED();
         size_t tb = o.cub_bytes;
-        CK(cub::DeviceRadixSort::SortPairs(o.cub, tb, o.keys_in, o.key, o.vals_in, o.perm, nn, 0, 64, ctx->st));
+        CK(cub::DeviceScan::InclusiveSum(o.cub, tb, o.len_in, o.off + 1, nn, ctx->st));
         LAUNCHED();
-        launch_gather_len(o.perm, o.len_in, n_out, o.len_sorted, ctx->st);
-        LAUNCHED();
-        tb = o.cub_bytes;
-        CK(cub::DeviceScan::InclusiveSum(o.cub, tb, o.len_sorted, o.off + 1, nn, ctx->st));
-        LAUNCHED();
-        launch_gather_out(o.perm, n_out, src_off, src_res, o.off, o.res, ctx->st);
+        launch_gather_res(o.perm, src_perm, n_out, src_off, src_res, o.off, o.res, ctx->st);
         LAUNCHED();
     }
     ctx->d_out = reinterpret_cast<uint8_t *>(d_out);
     ctx->out_bytes = out_bytes;
     ctx->out_n = n_out;
     ctx->out_r = r_out;
-    ctx->h_counts_all.assign(h_counts_all, h_counts_all + (size_t)p * p * 2);
-    ctx->bucket_sizes.assign(p, 0);
-    for (int s = 0; s < p; ++s)
-        for (int b = 0; b < p; ++b) ctx->bucket_sizes[b] += h_counts_all[((size_t)s * p + b) * 2];
-    ctx->bucket_first.assign(p + 1, 0);
-    for (int b = 0; b < p; ++b) ctx->bucket_first[b + 1] = ctx->bucket_first[b] + ctx->bucket_sizes[b];
-    if (h_bucket_sizes) std::memcpy(h_bucket_sizes, ctx->bucket_sizes.data(), sizeof(int64_t) * p);
+    ctx->stage = 6;
+    ctx->launches_last = ctx->launches_step;
+    if (h_counts_all) {
+        ctx->h_counts_all.assign(h_counts_all, h_counts_all + (size_t)p * p * 2);
+        ctx->counts_pending = false;
+        bucket_sizes_from_counts(ctx);
+        if (h_bucket_sizes) std::memcpy(h_bucket_sizes, ctx->bucket_sizes.data(), sizeof(int64_t) * p);
+    } else {
+        // world == 1: the counts stay on the device; they are read back lazily (getters sync)
+        CK(cudaMemcpyAsync(ctx->h_small + 45056, ctx->d_counts, sizeof(int64_t) * (size_t)p * p * 2,
+                           cudaMemcpyDeviceToHost, ctx->st));
+        ctx->counts_pending = true;
+        if (h_bucket_sizes) {
+            if (int rc = sad_get_bucket_sizes(ctx, h_bucket_sizes)) return rc;
+        }
+    }
     ctx->stage = 6;
     ctx->launches_last = ctx->launches_step;
     return SAD_OK;
 }
 
 // --------------------------------------------------------------------------- getters
+
+static void bucket_sizes_from_counts(sad_ctx *ctx) {
+    const int p = ctx->cfg.p;
+    ctx->bucket_sizes.assign(p, 0);
+    for (int s = 0; s < p; ++s)
+        for (int b = 0; b < p; ++b) ctx->bucket_sizes[b] += ctx->h_counts_all[((size_t)s * p + b) * 2];
+    ctx->bucket_first.assign(p + 1, 0);
+    for (int b = 0; b < p; ++b) ctx->bucket_first[b + 1] = ctx->bucket_first[b] + ctx->bucket_sizes[b];
+}
+
+static int resolve_counts(sad_ctx *ctx) {
+    if (!ctx->counts_pending) return SAD_OK;
+    CK(cudaStreamSynchronize(ctx->st));
+    const int p = ctx->cfg.p;
+    const int64_t *c = reinterpret_cast<const int64_t *>(ctx->h_small + 45056);
+    ctx->h_counts_all.assign(c, c + (size_t)p * p * 2);
+    ctx->counts_pending = false;
+    bucket_sizes_from_counts(ctx);
+    return SAD_OK;
+}
+
+int sad_get_bucket_sizes(sad_ctx *ctx, int64_t *h_sizes) {
+    GUARD(6);
+    if (!h_sizes) return SAD_E_ARG;
+    if (int rc = resolve_counts(ctx)) return rc;
+    std::memcpy(h_sizes, ctx->bucket_sizes.data(), sizeof(int64_t) * ctx->cfg.p);
+    return SAD_OK;
+}
 
 static int shard_check(sad_ctx *ctx, int shard, int64_t cap, int64_t &b0, int64_t &w) {
     if (shard < 0 || shard >= ctx->pl) return fail(ctx, SAD_E_ARG, "bad shard %d", shard);
@@ -829,6 +949,7 @@ int sad_get_bucket(sad_ctx *ctx, int bucket, int64_t *h_idx, uint64_t *h_key, ui
     GUARD(6);
     const int b0 = ctx->shard0, b1 = ctx->shard0 + ctx->pl;
     if (bucket < b0 || bucket >= b1) return fail(ctx, SAD_E_ARG, "bucket %d is not owned by rank %d", bucket, ctx->cfg.rank);
+    if (int rc = resolve_counts(ctx)) return rc;
     int64_t first = 0;
     for (int b = b0; b < bucket; ++b) first += ctx->bucket_sizes[b];
     const int64_t n = ctx->bucket_sizes[bucket];

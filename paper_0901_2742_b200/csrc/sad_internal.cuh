@@ -112,11 +112,15 @@ struct AllPairsArgs {
     const int64_t *h_shard_rowpad;
     const int64_t *h_kblocks;
     int kind;                        // TC: 0 = int8 operands (kind::i8), 1 = packed fp4 (kind::mxf4)
+    const void *tiles;               // TC: device tile table (16 B per tile) and its length
+    int64_t n_tiles_tc;
 };
 void launch_allpairs_alu(const AllPairsArgs &a, cudaStream_t st);
 int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err);
 bool tc_supported(std::string &why);
 int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base, int kind);
+int64_t tc_tiles_bound(int64_t n, int pl);
+int64_t tc_build_tiles(int pl, const int64_t *h_shard_base, int kind, void *host_out, int64_t cap);
 
 struct AncArgs {
     const unsigned long long *T;
@@ -147,12 +151,40 @@ struct RankArgs {
     uint32_t *S_ga, *den_ga;
     unsigned long long *key;
     int32_t *perm_in;
+    unsigned long long *ckey;        // composite sort key (shard << (33+ib)) | (q << ib) | row, or null
+    int ib;                          // index bits of the composite key
 };
 void launch_ga_pairs(const RankArgs &a, cudaStream_t st);
 void launch_rank_vs_ga(const RankArgs &a, cudaStream_t st);
 
 void launch_samples(const unsigned long long *key_sorted, const int64_t *shard_base, int pl, int p,
                     unsigned long long *samples_out, cudaStream_t st);
+void launch_unpack_sorted(const unsigned long long *ckey_sorted, int64_t n, int ib, int64_t first_idx,
+                          unsigned long long *key_sorted, int32_t *perm_sorted, cudaStream_t st);
+
+// K14: rank-merge of nr sorted runs of unique keys (keys at stride `kstride` u64 words):
+// out position of element t = sum over runs r of #{keys in r < key_t}.
+struct MergeArgs {
+    const unsigned long long *keys;  // element t's key at keys[t * kstride]
+    int kstride;
+    int64_t n;
+    const int64_t *run_start;        // device [nr + 1]
+    int nr;
+    // element length: lens[t * lstride] if lens, else rowinfo[perm[t]].tw + k - 1
+    const unsigned long long *lens;
+    int lstride;
+    const int32_t *perm;
+    const RowInfo *rowinfo;
+    int k;
+    unsigned long long *out_key;     // [n]
+    int64_t *out_len;                // [n]
+    int32_t *out_src;                // [n] element index t of each output slot
+};
+void launch_rank_merge(const MergeArgs &a, cudaStream_t st);
+// residues: dst_res[dst_off[r] ...] = src_res[src_off(out_src[r]) ...]; src_off(t) = src_off[perm ? perm[t] : t]
+void launch_gather_res(const int32_t *out_src, const int32_t *perm, int64_t n, const int64_t *src_off,
+                       const uint8_t *src_res, const int64_t *dst_off, uint8_t *dst_res, cudaStream_t st);
+void launch_lens_recv(const unsigned long long *recv_meta, int64_t n, int64_t *len, cudaStream_t st);
 
 struct PlanArgs {
     const unsigned long long *samples_all;   // [p(p-1)]
@@ -234,16 +266,22 @@ struct sad_ctx {
     unsigned long long *d_err = nullptr, *d_kinfo = nullptr;
     int64_t *d_shard_base = nullptr, *d_shard_rowpad = nullptr, *d_kblocks = nullptr, *d_sim_base = nullptr;
     int64_t *d_tile_base = nullptr;
+    void *d_tc_tiles = nullptr;      // TC tile table (workspace), built once per layout
+    int64_t tc_tiles_cap = 0, tc_tiles_n = 0;
+    void *h_tiles = nullptr;         // pinned staging of the tile table
+    size_t h_tiles_bytes = 0;
     int64_t alu_tiles = 0;
     unsigned long long *d_T = nullptr;
     int64_t *d_anc_local = nullptr;
     uint32_t *d_Sab = nullptr;
     long long *d_ga_info = nullptr;
     uint32_t *d_S_ga = nullptr, *d_den_ga = nullptr;
-    unsigned long long *d_key = nullptr, *d_key_sorted = nullptr;
+    unsigned long long *d_key = nullptr, *d_key_sorted = nullptr, *d_ckey = nullptr, *d_ckey_sorted = nullptr;
+    int64_t *d_runs = nullptr;
     int32_t *d_perm_in = nullptr, *d_perm_sorted = nullptr;
     unsigned long long *d_pivots = nullptr;
-    int64_t *d_bnd = nullptr, *d_lpre = nullptr, *d_seg = nullptr;
+    int64_t *d_bnd = nullptr, *d_lpre = nullptr, *d_seg = nullptr, *d_counts = nullptr;
+    bool counts_pending = false;
     void *d_tmap = nullptr;
     void *d_cub = nullptr;
     size_t cub_bytes = 0;
@@ -257,6 +295,10 @@ struct sad_ctx {
     int64_t out_n = 0, out_r = 0;
     std::vector<int64_t> bucket_sizes, bucket_first;  // [p] sizes, first row of owned buckets in out
     std::vector<int64_t> h_counts_all;                  // [p][p][2]
+
+    // layout of the last uploaded per-shard tables
+    uint8_t *tbl_ws = nullptr;
+    int64_t tbl_n = -1, tbl_ng = -1, tbl_first = -1;
 
     // pinned host staging
     unsigned long long *h_small = nullptr;              // pinned, 4096 u64

@@ -143,12 +143,13 @@ class Context:
             pass
 
     # -- pipeline ------------------------------------------------------------------------
-    def load(self, ascii_, offsets, n_global: int, first_index: int = 0):
-        """This rank's contiguous slice (numpy host arrays or CUDA tensors)."""
+    def load(self, ascii_, offsets, n_global: int, first_index: int = 0, residues: int | None = None):
+        """This rank's contiguous slice (numpy host arrays or CUDA tensors). For CUDA tensors pass
+        `residues` (= offsets[-1]) to avoid a device read-back."""
         on_dev = isinstance(ascii_, torch.Tensor) and ascii_.is_cuda
         if on_dev:
             n_local = int(offsets.numel()) - 1
-            R = int(offsets[-1].item()) if n_local >= 0 else 0
+            R = int(residues) if residues is not None else int(offsets[-1].item())
             mem = L.SAD_MEM_DEVICE
         else:
             ascii_ = np.ascontiguousarray(ascii_, dtype=np.uint8)
@@ -162,8 +163,8 @@ class Context:
         ws = ctypes.c_size_t()
         self._call("sad_workspace_size", n_local, R, ctypes.byref(ws))
         p_ws = self._buf("ws", ws.value)
-        self._call("sad_load", _vp(ascii_), _vp(offsets), n_local, first_index, n_global, mem, ctypes.c_void_p(p_ws),
-                   ws.value)
+        self._call("sad_load", _vp(ascii_), _vp(offsets), n_local, first_index, n_global, R, mem,
+                   ctypes.c_void_p(p_ws), ws.value)
         return self
 
     def build_profiles(self):
@@ -187,24 +188,28 @@ class Context:
         self._call("sad_partition_plan", _vp(samples_all if self.p > 1 else None), _vp(counts))
         return counts
 
-    def redistribute(self, counts_all: np.ndarray):
-        """All-to-all of the sequences (world > 1) and the receive-side merge."""
+    def pack(self, counts_all: np.ndarray):
+        """Send side of the redistribution (world > 1): this rank's sequences grouped by
+        destination. Returns (send_meta, send_res, send_seqs, send_res_bytes, recv_seqs, recv_res_bytes)."""
         c = np.ascontiguousarray(counts_all, dtype=np.int64)
+        ss, sr, rs, rr = exchange_sizes(self.p, self.world, self.rank, c)
+        send_meta = self._tensor("send_meta", (int(ss.sum()), 2), torch.int64)
+        send_res = self._tensor("send_res", (max(int(sr.sum()), 1),), torch.uint8)
+        self._call("sad_pack", _vp(c), _vp(send_meta), _vp(send_res))
+        return send_meta, send_res[: int(sr.sum())], ss, sr, rs, rr
+
+    def finish(self, counts_all, recv_meta=None, recv_res=None, sync: bool = True):
+        """Receive side: merge into this rank's buckets (recv_* None for world == 1). With
+        world == 1 counts_all may be None (the counts stay on the device); sync=False then
+        returns None instead of the bucket sizes (no host synchronization)."""
+        c = None if counts_all is None else np.ascontiguousarray(counts_all, dtype=np.int64)
         self.counts_all = c
-        recv_meta = recv_res = None
-        if self.world > 1:
-            ss, sr, rs, rr = exchange_sizes(self.p, self.world, self.rank, c)
-            send_meta = self._tensor("send_meta", (int(ss.sum()), 2), torch.int64)
-            send_res = self._tensor("send_res", (max(int(sr.sum()), 1),), torch.uint8)
-            self._call("sad_pack", _vp(c), _vp(send_meta), _vp(send_res))
-            recv_meta = all_to_all_v(send_meta, ss, rs, self.group)
-            recv_res = all_to_all_v(send_res[: int(sr.sum())], sr, rr, self.group)
-            if recv_res.numel() == 0:
-                recv_res = torch.zeros(1, dtype=torch.uint8, device=self.device)
+        if recv_res is not None and recv_res.numel() == 0:
+            recv_res = torch.zeros(1, dtype=torch.uint8, device=self.device)
         ob = ctypes.c_size_t()
         self._call("sad_output_size", _vp(c), ctypes.byref(ob))
         p_out = self._buf("out", ob.value, align=256)
-        sizes = np.zeros(self.p, np.int64)
+        sizes = np.zeros(self.p, np.int64) if (sync or c is not None) else None
         self._call("sad_finish", _vp(c), _vp(recv_meta), _vp(recv_res), ctypes.c_void_p(p_out), ob.value, _vp(sizes))
         lay = np.zeros(6, np.int64)
         self._call("sad_output_layout", _vp(c), _vp(lay))
@@ -214,17 +219,34 @@ class Context:
         self.bucket_sizes = sizes
         return sizes
 
-    def run(self) -> np.ndarray:
+    def redistribute(self, counts_all: np.ndarray):
+        """All-to-all of the sequences (world > 1) and the receive-side merge."""
+        if self.world == 1:
+            return self.finish(counts_all)
+        send_meta, send_res, ss, sr, rs, rr = self.pack(counts_all)
+        recv_meta = all_to_all_v(send_meta, ss, rs, self.group)
+        recv_res = all_to_all_v(send_res, sr, rr, self.group)
+        return self.finish(counts_all, recv_meta, recv_res)
+
+    def run(self, sync: bool = True):
         """One full step: profiles -> local rank -> GA rank -> plan -> redistribution.
-        Returns the sizes of all p buckets (host)."""
+        Returns the sizes of all p buckets (host); with world == 1 and sync=False nothing is
+        read back (the step is left enqueued on the stream) and None is returned."""
         self.build_profiles()
         anc = self.rank_local()
         anc_all = all_gather_rows(anc, self.world, self.group)
         samples = self.rank_global(anc_all)
         samples_all = all_gather_rows(samples, self.world, self.group) if self.p > 1 else samples
         counts = self.partition_plan(samples_all)
+        if self.world == 1:
+            return self.finish(None, sync=sync)
         counts_all = all_gather_rows(counts, self.world, self.group).cpu().numpy()   # the one D2H of the plan
         return self.redistribute(counts_all.reshape(self.p, self.p, 2))
+
+    def bucket_sizes_now(self) -> np.ndarray:
+        out = np.zeros(self.p, np.int64)
+        self._call("sad_get_bucket_sizes", _vp(out))
+        return out
 
     # -- results -------------------------------------------------------------------------
     def out_keys(self) -> torch.Tensor:
