@@ -61,18 +61,21 @@ def total_pairs(n, p):
 # ----------------------------------------------------------------------------------------
 
 def oracle_sample(a, o, spec, p, seconds):
-    """Time the oracle (as it stands, all host threads) on the first n_sub sequences of the
-    workload with the same p, n_sub sized for about `seconds` of CPU work."""
+    """Size a prefix of the workload (same p) so that one oracle run takes about `seconds` on
+    all host threads: grow the prefix until a probe run takes >= seconds/4, then scale by the
+    pairs' n^2 growth."""
     import oracle
     cores = oracle.threads(0)
-    n_sub = min(len(o) - 1, max(p * p, 800))
-    sub = lambda m: (a[: o[m]], o[: m + 1])
-    t0 = time.perf_counter()
-    oracle.run(*sub(n_sub), spec.alphabet, spec.k, p)
-    dt = time.perf_counter() - t0
-    # all-pairs cost grows ~ n^2; scale to the time budget
-    scale = (seconds / max(dt, 1e-3)) ** 0.5
-    n_sub = int(min(len(o) - 1, max(n_sub, n_sub * scale)))
+    N = len(o) - 1
+    n_sub = min(N, max(p * p, 800))
+    while True:
+        t0 = time.perf_counter()
+        oracle.run(a[: o[n_sub]], o[: n_sub + 1], spec.alphabet, spec.k, p)
+        dt = time.perf_counter() - t0
+        if dt >= seconds / 4 or n_sub >= N:
+            break
+        n_sub = min(N, int(n_sub * min(3.0, max(1.2, (seconds / 4 / max(dt, 1e-3)) ** 0.5))))
+    n_sub = int(min(N, max(p * p, n_sub * (seconds / max(dt, 1e-3)) ** 0.5)))
     return n_sub, cores
 
 
