@@ -60,6 +60,8 @@ extern "C" {
                                  Operands are packed e2m1 0/1 (kind::mxf4, unit block scales, fp32
                                  accumulators: exact below 2^24) unless SAD_F_TC_INT8 */
 #define SAD_F_TC_INT8 8u      /* tensor-core path with uint8 0/1 operands (kind::i8, int32 accumulators) */
+#define SAD_F_TC_1SM 16u      /* tensor-core path with one CTA per 128-row tile (default: CTA pairs,
+                                 tcgen05 cta_group::2, 256-row tiles) */
 
 /* memory kinds of sad_load inputs */
 #define SAD_MEM_HOST 0

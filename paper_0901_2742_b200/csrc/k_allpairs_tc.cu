@@ -28,9 +28,11 @@
 
 namespace sad {
 
+#ifndef SAD_FP4_BN
+#define SAD_FP4_BN 240
+#endif
 namespace tc {
 constexpr int BM = 128, BK = 128;                 // BK = bytes of K per stage (128B swizzle row)
-constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK;                  // 16 KB
 constexpr int THREADS = 384;                   // warps 0-3: TMA, MMA, TMEM alloc, idle; 4-11: epilogue
 constexpr int SF_COLS = 32;                       // TMEM columns of unit block scales (fp4 path)
@@ -39,10 +41,13 @@ constexpr int SF_COLS = 32;                       // TMEM columns of unit block 
 // KIND 1: packed e2m1 0/1 operands (two per byte), tcgen05.mma.kind::mxf4.block_scale with
 //         every UE8M0 scale = 2^0, fp32 accumulators (exact: S <= 65535 < 2^24), N = 240 so
 //         that two accumulators + the scale columns fit the 512 TMEM columns.
-template <int KIND>
+template <int KIND, int CG = 1>
 struct Traits {
-    static constexpr int BN = KIND == 0 ? 256 : 240;
-    static constexpr int B_BYTES = BN * BK;
+    static constexpr int BN = KIND == 0 ? 256 : SAD_FP4_BN;   // MMA N (tile columns)
+    static constexpr int BNC = BN / CG;                 // B rows held by each CTA of the pair
+    static constexpr int BMT = BM * CG;                 // tile rows (MMA M)
+    static constexpr int STAGES = CG == 1 ? 4 : 6;
+    static constexpr int B_BYTES = BNC * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int ACC_COLS = BN;
     static constexpr int TMEM_COLS = 512;
@@ -55,8 +60,8 @@ struct Traits {
     // i8: D = S32 (bits 4-5 = 2), A = B = uint8 (0), K-major, N >> 3 at 17, M >> 4 at 24.
     // mxf4: A = B = E2M1 (1) at bits 7 / 10, scale format UE8M0 (bit 23 = 1), K = 64 (bit 31 = 0).
     static constexpr uint32_t IDESC =
-        KIND == 0 ? ((2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24))
-                  : ((1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24));
+        KIND == 0 ? ((2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BMT >> 4) << 24))
+                  : ((1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BMT >> 4) << 24));
 };
 }  // namespace tc
 
@@ -103,6 +108,52 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *ba
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+// 2-CTA (cta_group::2) variants. A shared::cta address with the peer bit (24) cleared names the
+// same offset in the leader CTA (rank 0) of the pair.
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap *map, uint64_t *bar, void *dst, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(b) & kPeerMask) : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_mxf4_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc,
+                                              uint32_t sfa, uint32_t sfb) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb)
+        : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t *bar) {
@@ -151,12 +202,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-template <int KIND>
+template <int KIND, int CG>
 __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constant__ CUtensorMap tmapA,
                                                             const __grid_constant__ CUtensorMap tmapB, TcParams P) {
     using namespace tc;
-    using Tr = Traits<KIND>;
+    using Tr = Traits<KIND, CG>;
     constexpr int BN = Tr::BN, B_BYTES = Tr::B_BYTES, STAGE_BYTES = Tr::STAGE_BYTES, ACC_COLS = Tr::ACC_COLS;
+    constexpr int STAGES = Tr::STAGES, BNC = Tr::BNC, BMT = Tr::BMT;
     constexpr int OFF_BAR = Tr::OFF_BAR, OFF_COLINFO = Tr::OFF_COLINFO, OFF_COLSUM = Tr::OFF_COLSUM;
     constexpr int TMEM_COLS = Tr::TMEM_COLS;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -175,6 +227,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
     unsigned long long *rowpart = reinterpret_cast<unsigned long long *>(smem + Tr::OFF_ROWPART);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t crank = CG == 2 ? cluster_rank() : 0u;        // rank in the CTA pair
+    const bool leader = crank == 0;
+    // persistent schedule: the pair (or the single CTA) takes every (gridDim.x / CG)-th tile
+    const int64_t t0 = (int64_t)blockIdx.x / CG, tstep = (int64_t)gridDim.x / CG;
     if (threadIdx.x == 0) {
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&full[i], 1);
@@ -182,27 +238,34 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 8);
+            mbar_init(&tempty[i], 8 * CG);          // every epilogue warp of the pair releases
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmapA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmapB)) : "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if constexpr (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if constexpr (KIND == 1) {
         // unit block scales: every UE8M0 byte = 127 (2^0), so any scale-factor layout reads 1.0
         if (warp >= 4 && warp < 8) tmem_st32_const(tmem_base + ((uint32_t)((warp - 4) * 32) << 16) + Tr::SF_COL, 0x7F7F7F7Fu);
         tc_fence_before();
-        __syncthreads();
+        if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
         tc_fence_after();
     }
 
@@ -211,28 +274,35 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             // ===== TMA producer =====
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+            for (int64_t t = t0; t < P.n_tiles; t += tstep) {
                 const TcTile tl = P.tiles[t];
-                const int rowA = (int)(P.shard_rowpad[tl.s] + (int64_t)tl.I * BM);
-                const int rowB = (int)(P.shard_rowpad[tl.s] + (int64_t)tl.J * BN);
+                const int rowA = (int)(P.shard_rowpad[tl.s] + (int64_t)tl.I * BMT + (int64_t)crank * BM);
+                const int rowB = (int)(P.shard_rowpad[tl.s] + (int64_t)tl.J * BN + (int64_t)crank * BNC);
                 const int nkb = (int)P.kblocks[tl.s];
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], STAGE_BYTES);
-                    tma_load_2d(&tmapA, &full[stage], sA + stage * A_BYTES, kb * BK, rowA);
-                    tma_load_2d(&tmapB, &full[stage], sB + stage * B_BYTES, kb * BK, rowB);
+                    if constexpr (CG == 1) {
+                        mbar_expect_tx(&full[stage], STAGE_BYTES);
+                        tma_load_2d(&tmapA, &full[stage], sA + stage * A_BYTES, kb * BK, rowA);
+                        tma_load_2d(&tmapB, &full[stage], sB + stage * B_BYTES, kb * BK, rowB);
+                    } else {
+                        // the leader's full barrier counts the bytes of both CTAs
+                        if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+                        tma_load_2d_pair(&tmapA, &full[stage], sA + stage * A_BYTES, kb * BK, rowA);
+                        tma_load_2d_pair(&tmapB, &full[stage], sB + stage * B_BYTES, kb * BK, rowB);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && leader) {
             // ===== MMA issuer =====
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+            for (int64_t t = t0; t < P.n_tiles; t += tstep) {
                 const TcTile tl = P.tiles[t];
                 const int nkb = (int)P.kblocks[tl.s];
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -244,16 +314,20 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
                     for (int kk = 0; kk < BK / 32; ++kk) {
-                        if constexpr (KIND == 0)
-                            mma_i8(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), Tr::IDESC, (kb | kk) != 0);
-                        else
-                            mma_mxf4(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), Tr::IDESC, (kb | kk) != 0,
-                                     tmem_base + Tr::SF_COL, tmem_base + Tr::SF_COL);
+                        const uint64_t ad = sw128_desc(a0 + kk * 32), bd = sw128_desc(b0 + kk * 32);
+                        const uint32_t accf = (kb | kk) != 0;
+                        if constexpr (CG == 1) {
+                            if constexpr (KIND == 0) mma_i8(d, ad, bd, Tr::IDESC, accf);
+                            else mma_mxf4(d, ad, bd, Tr::IDESC, accf, tmem_base + Tr::SF_COL, tmem_base + Tr::SF_COL);
+                        } else {
+                            if constexpr (KIND == 0) mma_i8_pair(d, ad, bd, Tr::IDESC, accf);
+                            else mma_mxf4_pair(d, ad, bd, Tr::IDESC, accf, tmem_base + Tr::SF_COL, tmem_base + Tr::SF_COL);
+                        }
                     }
-                    tc_commit(&empty[stage]);
+                    if constexpr (CG == 1) tc_commit(&empty[stage]); else tc_commit_pair(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                tc_commit(&tfull[acc]);
+                if constexpr (CG == 1) tc_commit(&tfull[acc]); else tc_commit_pair(&tfull[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
@@ -267,11 +341,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         const int ch0 = grp ? (NCH + 1) / 2 : 0, ch1 = grp ? NCH : (NCH + 1) / 2;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+        for (int64_t t = t0; t < P.n_tiles; t += tstep) {
             const TcTile tl = P.tiles[t];
             const int64_t rbase = P.shard_base[tl.s];
             const int64_t w = P.shard_base[tl.s + 1] - rbase;
-            const int64_t col0 = (int64_t)tl.J * BN, row0 = (int64_t)tl.I * BM;
+            const int64_t col0 = (int64_t)tl.J * BN, row0 = (int64_t)tl.I * BMT + (int64_t)crank * BM;
             epi_bar();                            // previous tile's colinfo / colsum / rowpart consumed
             if (e < BN) {
                 const int64_t col = col0 + e;
@@ -350,7 +424,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if constexpr (CG == 1) mbar_arrive(&tempty[acc]); else mbar_arrive_leader(&tempty[acc]);
+            }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             if (grp == 1) rowpart[quarter * 32 + lane] = rowsum;
             epi_bar();
@@ -366,11 +442,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
-    if (warp == 2)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
-                     : "memory");
+    if (warp == 2) {
+        if constexpr (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                         : "memory");
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -401,10 +482,14 @@ bool tc_supported(std::string &why) {
             return;
         }
         g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-        if (cudaFuncSetAttribute(k_syrk_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Traits<0>::SMEM_BYTES) !=
-                cudaSuccess ||
-            cudaFuncSetAttribute(k_syrk_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Traits<1>::SMEM_BYTES) !=
-                cudaSuccess) {
+        if (cudaFuncSetAttribute(k_syrk_tc<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::Traits<0, 1>::SMEM_BYTES) != cudaSuccess ||
+            cudaFuncSetAttribute(k_syrk_tc<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::Traits<1, 1>::SMEM_BYTES) != cudaSuccess ||
+            cudaFuncSetAttribute(k_syrk_tc<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::Traits<0, 2>::SMEM_BYTES) != cudaSuccess ||
+            cudaFuncSetAttribute(k_syrk_tc<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::Traits<1, 2>::SMEM_BYTES) != cudaSuccess) {
             reason = "cannot reserve shared memory";
             return;
         }
@@ -419,24 +504,24 @@ int tc_bn(int kind) { return kind == 0 ? tc::Traits<0>::BN : tc::Traits<1>::BN; 
 // tiles of the upper triangle of every shard: (I, J) such that the tile holds some j >= i, i.e.
 // BN*J + BN - 1 >= BM*I, in groups of kGroupJ column blocks so that the ~148 tiles in flight
 // share a few A_J blocks and walk the A_I blocks (L2 reuse).
-static void build_tiles(int pl, const int64_t *h_shard_base, int bn, std::vector<TcTile> &out) {
+static void build_tiles(int pl, const int64_t *h_shard_base, int bn, int bm, std::vector<TcTile> &out) {
     constexpr int kGroupJ = 8;
     out.clear();
     for (int s = 0; s < pl; ++s) {
         const int64_t w = h_shard_base[s + 1] - h_shard_base[s];
-        const int nI = (int)((w + tc::BM - 1) / tc::BM), nJ = (int)((w + bn - 1) / bn);
+        const int nI = (int)((w + bm - 1) / bm), nJ = (int)((w + bn - 1) / bn);
         for (int j0 = 0; j0 < nJ; j0 += kGroupJ)
             for (int I = 0; I < nI; ++I) {
-                const int64_t need = (int64_t)tc::BM * I - (bn - 1);
+                const int64_t need = (int64_t)bm * I - (bn - 1);
                 const int jmin = need <= 0 ? 0 : (int)((need + bn - 1) / bn);
                 for (int J = std::max(j0, jmin); J < std::min(nJ, j0 + kGroupJ); ++J) out.push_back(TcTile{s, I, J, 0});
             }
     }
 }
 
-int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base, int kind) {
+int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base, int kind, int cg) {
     std::vector<TcTile> t;
-    build_tiles(pl, h_shard_base, tc_bn(kind), t);
+    build_tiles(pl, h_shard_base, tc_bn(kind), tc::BM * cg, t);
     return (int64_t)t.size() * (int64_t)sizeof(TcTile);
 }
 
@@ -446,9 +531,9 @@ int64_t tc_tiles_bound(int64_t n, int pl) {
 }
 
 // the tile table of a layout, written to host memory (16 bytes per tile); returns the count
-int64_t tc_build_tiles(int pl, const int64_t *h_shard_base, int kind, void *host_out, int64_t cap) {
+int64_t tc_build_tiles(int pl, const int64_t *h_shard_base, int kind, int cg, void *host_out, int64_t cap) {
     std::vector<TcTile> t;
-    build_tiles(pl, h_shard_base, tc_bn(kind), t);
+    build_tiles(pl, h_shard_base, tc_bn(kind), tc::BM * cg, t);
     if ((int64_t)t.size() > cap) return -1;
     std::memcpy(host_out, t.data(), t.size() * sizeof(TcTile));
     return (int64_t)t.size();
@@ -476,7 +561,7 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
     if (a.n_tiles_tc <= 0) return 0;
     const int64_t rows_pad = a.h_shard_rowpad[a.pl];
     CUtensorMap mapA, mapB;
-    if (!encode(&mapA, a.op, a.stride, rows_pad, tc::BM) || !encode(&mapB, a.op, a.stride, rows_pad, bn)) {
+    if (!encode(&mapA, a.op, a.stride, rows_pad, tc::BM) || !encode(&mapB, a.op, a.stride, rows_pad, bn / a.cg)) {
         err = "cuTensorMapEncodeTiled failed";
         return -1;
     }
@@ -490,11 +575,33 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
     P.T = a.T;
     P.sim = a.sim;
     P.sim_base = a.sim_base;
-    const int grid = (int)std::min<int64_t>(a.num_sms, P.n_tiles);
-    if (a.kind == 0)
-        k_syrk_tc<0><<<grid, tc::THREADS, tc::Traits<0>::SMEM_BYTES, st>>>(mapA, mapB, P);
-    else
-        k_syrk_tc<1><<<grid, tc::THREADS, tc::Traits<1>::SMEM_BYTES, st>>>(mapA, mapB, P);
+    if (a.cg == 1) {
+        const int grid = (int)std::min<int64_t>(a.num_sms, P.n_tiles);
+        if (a.kind == 0)
+            k_syrk_tc<0, 1><<<grid, tc::THREADS, tc::Traits<0, 1>::SMEM_BYTES, st>>>(mapA, mapB, P);
+        else
+            k_syrk_tc<1, 1><<<grid, tc::THREADS, tc::Traits<1, 1>::SMEM_BYTES, st>>>(mapA, mapB, P);
+    } else {
+        // CTA pairs (cluster of 2): one persistent pair per two SMs
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(a.num_sms / 2, P.n_tiles)));
+        cfg.blockDim = dim3(tc::THREADS);
+        cfg.dynamicSmemBytes = a.kind == 0 ? tc::Traits<0, 2>::SMEM_BYTES : tc::Traits<1, 2>::SMEM_BYTES;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t e = a.kind == 0 ? cudaLaunchKernelEx(&cfg, k_syrk_tc<0, 2>, mapA, mapB, P)
+                                    : cudaLaunchKernelEx(&cfg, k_syrk_tc<1, 2>, mapA, mapB, P);
+        if (e != cudaSuccess) {
+            err = std::string("cluster launch failed: ") + cudaGetErrorString(e);
+            return -1;
+        }
+    }
     return 0;
 }
 

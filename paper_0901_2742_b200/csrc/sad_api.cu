@@ -224,6 +224,7 @@ int sad_create(const sad_config *cfg, sad_ctx **out) {
     ctx->shard0 = cfg->rank * ctx->pl;
     ctx->use_tc = !(cfg->flags & SAD_F_KERNEL_ALU);
     ctx->tc_kind = (cfg->flags & SAD_F_TC_INT8) ? 0 : 1;
+    ctx->tc_cg = (cfg->flags & SAD_F_TC_1SM) ? 1 : 2;
     if (cudaSetDevice(cfg->device) != cudaSuccess) {
         delete ctx;
         return SAD_E_CUDA;
@@ -358,7 +359,7 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
                 CK(cudaMallocHost(&ctx->h_tiles, need_b));
                 ctx->h_tiles_bytes = need_b;
             }
-            ctx->tc_tiles_n = tc_build_tiles(ctx->pl, sb.data(), ctx->tc_kind, ctx->h_tiles, ctx->tc_tiles_cap);
+            ctx->tc_tiles_n = tc_build_tiles(ctx->pl, sb.data(), ctx->tc_kind, ctx->tc_cg, ctx->h_tiles, ctx->tc_tiles_cap);
             if (ctx->tc_tiles_n < 0) return fail(ctx, SAD_E_OOM, "tile table exceeds its bound");
             if (ctx->tc_tiles_n > 0)
                 CK(cudaMemcpyAsync(ctx->d_tc_tiles, ctx->h_tiles, (size_t)ctx->tc_tiles_n * 16, cudaMemcpyHostToDevice,
@@ -545,6 +546,7 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     ap.kind = ctx->tc_kind;
     ap.tiles = ctx->d_tc_tiles;
     ap.n_tiles_tc = ctx->tc_tiles_n;
+    ap.cg = ctx->tc_cg;
     record_pair(ctx, ctx->ev_pairs_ap, true);
     if (ctx->use_tc) {
         std::string e;

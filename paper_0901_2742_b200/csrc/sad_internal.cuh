@@ -114,13 +114,14 @@ struct AllPairsArgs {
     int kind;                        // TC: 0 = int8 operands (kind::i8), 1 = packed fp4 (kind::mxf4)
     const void *tiles;               // TC: device tile table (16 B per tile) and its length
     int64_t n_tiles_tc;
+    int cg;                          // TC: 1 = one CTA per tile, 2 = CTA pair (cta_group::2, M = 256)
 };
 void launch_allpairs_alu(const AllPairsArgs &a, cudaStream_t st);
 int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err);
 bool tc_supported(std::string &why);
-int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base, int kind);
+int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base, int kind, int cg);
 int64_t tc_tiles_bound(int64_t n, int pl);
-int64_t tc_build_tiles(int pl, const int64_t *h_shard_base, int kind, void *host_out, int64_t cap);
+int64_t tc_build_tiles(int pl, const int64_t *h_shard_base, int kind, int cg, void *host_out, int64_t cap);
 
 struct AncArgs {
     const unsigned long long *T;
@@ -252,6 +253,7 @@ struct sad_ctx {
     int64_t K_stride = 0, V_pad = 0;
     bool use_tc = false;
     int tc_kind = 1;                 // 0 = int8, 1 = fp4
+    int tc_cg = 2;                   // 1 or 2 CTAs per tensor-core tile
     int64_t kcols_per_block = 128;   // operand columns per 128-byte K block
 
     // device pointers carved from the caller workspace

@@ -20,6 +20,9 @@ import torch.distributed as dist
 from . import _lib as L
 
 ALPHABETS = {"protein": L.SAD_PROTEIN20, "dna": L.SAD_DNA4}
+KERNELS = {"tc": L.SAD_F_KERNEL_TC, "tc1": L.SAD_F_KERNEL_TC | L.SAD_F_TC_1SM,
+           "tc8": L.SAD_F_KERNEL_TC | L.SAD_F_TC_INT8, "tc81": L.SAD_F_KERNEL_TC | L.SAD_F_TC_INT8 | L.SAD_F_TC_1SM,
+           "alu": L.SAD_F_KERNEL_ALU}
 
 
 def _vp(t) -> ctypes.c_void_p:
@@ -79,8 +82,10 @@ def all_to_all_v(send: torch.Tensor, send_sizes, recv_sizes, group=None) -> torc
 class Context:
     """One rank's view of the k-mer-rank domain decomposition (include/sad.h).
 
-    kernel: "tc" (tcgen05 threshold-indicator GEMM on packed e2m1 operands, default),
-            "tc8" (the same on uint8 operands, kind::i8) or "alu" (CUDA-core min-sum).
+    kernel: "tc"  tcgen05 threshold-indicator GEMM, packed e2m1 operands, CTA pairs (default)
+            "tc1" the same with one CTA per 128-row tile
+            "tc8" uint8 operands (kind::i8), CTA pairs; "tc81" uint8, one CTA per tile
+            "alu" CUDA-core min-sum
     """
 
     def __init__(self, alphabet: str, k: int, p: int, *, world: int = 1, rank: int = 0, device: int | None = None,
@@ -93,11 +98,9 @@ class Context:
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.alphabet, self.k, self.p, self.world, self.rank, self.group = alphabet, k, p, world, rank, group
         self.pl = p // world
-        if kernel not in ("tc", "tc8", "alu"):
-            raise ValueError(f"kernel must be tc, tc8 or alu, not {kernel!r}")
-        flags = (L.SAD_F_KEEP_SIM if keep_sim else 0) | (L.SAD_F_KERNEL_ALU if kernel == "alu" else L.SAD_F_KERNEL_TC)
-        if kernel == "tc8":
-            flags |= L.SAD_F_TC_INT8
+        if kernel not in KERNELS:
+            raise ValueError(f"kernel must be one of {sorted(KERNELS)}, not {kernel!r}")
+        flags = (L.SAD_F_KEEP_SIM if keep_sim else 0) | KERNELS[kernel]
         self.kernel = kernel
         cfg = L.SadConfig(ALPHABETS[alphabet], k, p, world, rank, device, self.stream.cuda_stream, flags)
         h = ctypes.c_void_p()

@@ -35,7 +35,7 @@ def run_emulated(a, o, alpha, k, p, G, kernel):
     return ctxs, sizes
 
 
-@pytest.mark.parametrize("kernel", ["tc", "alu"])
+@pytest.mark.parametrize("kernel", ["tc", "tc1", "alu"])
 @pytest.mark.parametrize("G", [2, 4, 8])
 def test_g_invariance(kernel, G):
     spec = gen.SPECS[3]

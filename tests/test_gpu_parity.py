@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 def _kernels():
     # the tensor-core kernel is mandatory once built (tc_supported() in k_allpairs_tc.cu)
     import os
-    return ["tc", "tc8", "alu"] if os.environ.get("SAD_TEST_TC", "1") == "1" else ["alu"]
+    return ["tc", "tc1", "tc8", "tc81", "alu"] if os.environ.get("SAD_TEST_TC", "1") == "1" else ["alu"]
 
 
 KERNELS = _kernels()
