@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--p", type=int, default=None)
-    ap.add_argument("--kernel", default="tc", choices=["tc", "tc1", "tc8", "tc81", "alu"])
+    ap.add_argument("--kernel", default="tc", choices=["tc", "tc1", "tc8", "tc81", "tcfull", "tc8full", "alu"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -260,10 +260,11 @@ def main():
             measured = json.load(open(os.path.join(ROOT, "profiles", "peaks_b200.json")))
         except Exception:
             pass
-        if args.kernel in ("tc", "tc1") and "fp4_tflops" in measured:
+        fp4 = args.kernel in ("tc", "tc1", "tcfull")
+        if fp4 and "fp4_tflops" in measured:
             peak, src = measured["fp4_tflops"], ("measured fp4 (mxf4) dense peak, cuBLAS torch._scaled_mm 8192^3 "
                                                  "burst (profiles/peaks_b200.json, tools/peaks.py)")
-        elif args.kernel in ("tc", "tc1") and "int8_tops" in measured:
+        elif fp4 and "int8_tops" in measured:
             peak, src = 2.0 * measured["int8_tops"], ("2 x measured int8 dense peak (cuBLAS torch._int_mm 8192^3 "
                                                       "burst, profiles/peaks_b200.json): nominal fp4:int8 = 9:4.5")
         elif "int8_tops" in measured:
@@ -315,7 +316,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": {"tc": "e2m1", "tc1": "e2m1", "tc8": "i8", "tc81": "i8", "alu": "u16"}[args.kernel], "data": "synthetic",
+            "vs_baseline": None, "dtype": {"tc": "e2m1", "tc1": "e2m1", "tcfull": "e2m1", "tc8": "i8", "tc81": "i8", "tc8full": "i8",
+                                               "alu": "u16"}[args.kernel], "data": "synthetic",
             "config": {"workload": workload_name(spec, p), "p": p, "kernel": args.kernel,
                        "pairs_per_step": pairs_job,
                        "l2": "L2 flushed (256 MB write) before every timed step; operand working set > L2"},

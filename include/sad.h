@@ -62,6 +62,11 @@ extern "C" {
 #define SAD_F_TC_INT8 8u      /* tensor-core path with uint8 0/1 operands (kind::i8, int32 accumulators) */
 #define SAD_F_TC_1SM 16u      /* tensor-core path with one CTA per 128-row tile (default: CTA pairs,
                                  tcgen05 cta_group::2, 256-row tiles) */
+#define SAD_F_TC_ALL_LAYERS 32u /* tensor-core path with every threshold layer t <= max n(tau) dense in the
+                                 contraction. Default: the layers are capped per shard at the smallest
+                                 T in {1,2,4,8} with max_i sum_tau (n_i(tau) - T)+ <= 255, and the
+                                 remainder sum_tau min((n_i-T)+, (n_j-T)+) is added per pair from a
+                                 sparse scatter (exact either way) */
 
 /* memory kinds of sad_load inputs */
 #define SAD_MEM_HOST 0

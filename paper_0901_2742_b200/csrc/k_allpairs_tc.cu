@@ -14,6 +14,8 @@
 //   warp 1      MMA issuer: 4 x tcgen05.mma (M=128, N=256, K=32) per stage into one of two
 //               TMEM accumulators (2 x 256 columns), tcgen05.commit to release stages
 //   warp 2      TMEM allocator (512 columns)
+//   warp 3      K6 staging: the next tile's excess bytes e_ij of this CTA's rows, scattered from
+//               the k_xrows runs into a double-buffered shared [chunk][row][16] buffer
 //   warps 4-11  fused epilogue (two warpgroups split the tile's columns), overlapped with the next tile's MMAs: tcgen05.ld of S,
 //               exact fixed point q = floor(2^32 S / den) (reading A5), row sums and
 //               column sums (warp transpose-reduce + per-warp shared slots) into T (u64 atomics,
@@ -46,7 +48,7 @@ struct Traits {
     static constexpr int BN = KIND == 0 ? 256 : SAD_FP4_BN;   // MMA N (tile columns)
     static constexpr int BNC = BN / CG;                 // B rows held by each CTA of the pair
     static constexpr int BMT = BM * CG;                 // tile rows (MMA M)
-    static constexpr int STAGES = CG == 1 ? 4 : 6;
+    static constexpr int STAGES = CG == 1 ? 3 : 4;
     static constexpr int B_BYTES = BNC * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int ACC_COLS = BN;
@@ -56,7 +58,9 @@ struct Traits {
     static constexpr int OFF_COLINFO = OFF_BAR + 256;
     static constexpr int OFF_COLSUM = OFF_COLINFO + 256 * 16;
     static constexpr int OFF_ROWPART = OFF_COLSUM + 4 * 256 * 8;
-    static constexpr int SMEM_BYTES = OFF_ROWPART + 128 * 8 + 1024;
+    static constexpr int OFF_XBUF = OFF_ROWPART + 128 * 8;
+    static constexpr int XBUF_BYTES = BM * BN;         // one tile's K6 excess bytes of this CTA's rows
+    static constexpr int SMEM_BYTES = OFF_XBUF + 2 * XBUF_BYTES + 1024;
     // i8: D = S32 (bits 4-5 = 2), A = B = uint8 (0), K-major, N >> 3 at 17, M >> 4 at 24.
     // mxf4: A = B = E2M1 (1) at bits 7 / 10, scale format UE8M0 (bit 23 = 1), K = 64 (bit 31 = 0).
     static constexpr uint32_t IDESC =
@@ -79,6 +83,10 @@ struct TcParams {
     unsigned long long *T;
     uint16_t *sim;
     const int64_t *sim_base;
+    const uint2 *xrow;               // K6 runs {first, count} per local row, or NULL
+    const uint32_t *rl;              // K6 runs (j << 8) | e_ij, sorted by j
+    const uint32_t *xidx;            // K6 run index: [row][nJ] first entry at col >= J BN
+    const int64_t *xibase;           // [pl+1] per shard base of xidx
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -202,6 +210,28 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
+// global inputs of one tile's epilogue for one thread (row = its TMEM lane, column e < BN for the
+// shared colinfo row)
+struct EpiPre {
+    TcTile tl;                       // pad = -1: no tile
+    RowInfo ri, ci;
+};
+
+template <int BN, int BMT>
+__device__ __forceinline__ void epi_pre_rows(const TcParams &P, EpiPre &p, uint32_t crank, int quarter, int lane,
+                                             int e) {
+    const RowInfo none{1u, 0xFFFFFFFFu, 1u, 0u};
+    p.ri = none;
+    p.ci = none;
+    if (p.tl.pad != 0) return;
+    const int64_t rbase = P.shard_base[p.tl.s];
+    const int64_t w = P.shard_base[p.tl.s + 1] - rbase;
+    const int64_t row = (int64_t)p.tl.I * BMT + (int64_t)crank * tc::BM + quarter * 32 + lane;
+    const int64_t col = (int64_t)p.tl.J * BN + e;
+    if (e < BN && col < w) p.ci = P.rowinfo[rbase + col];
+    if (row < w) p.ri = P.rowinfo[rbase + row];
+}
+
 template <int KIND, int CG>
 __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constant__ CUtensorMap tmapA,
                                                             const __grid_constant__ CUtensorMap tmapB, TcParams P) {
@@ -221,7 +251,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *xfull = tempty + 2;          // K6 excess buffers: staged by warp 3 / released by the epilogue
+    uint64_t *xempty = xfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xempty + 2);
+    uint8_t *xbuf = smem + Tr::OFF_XBUF;    // [2][chunk][BM rows][16 bytes]
     RowInfo *colinfo = reinterpret_cast<RowInfo *>(smem + OFF_COLINFO);
     unsigned long long *colsum = reinterpret_cast<unsigned long long *>(smem + OFF_COLSUM);
     unsigned long long *rowpart = reinterpret_cast<unsigned long long *>(smem + Tr::OFF_ROWPART);
@@ -239,6 +272,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 8 * CG);          // every epilogue warp of the pair releases
+            mbar_init(&xfull[i], 32);               // every lane of the staging warp
+            mbar_init(&xempty[i], 8);               // every epilogue warp of this CTA
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmapA)) : "memory");
@@ -257,6 +292,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
         }
     }
+    if (P.xrow)                              // the K6 buffers start (and are left by the epilogue) zeroed
+        for (int t = threadIdx.x; t < 2 * Tr::XBUF_BYTES / 16; t += THREADS)
+            reinterpret_cast<uint4 *>(xbuf)[t] = make_uint4(0, 0, 0, 0);
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
@@ -331,6 +369,43 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
+    } else if (warp == 3) {
+        if (P.xrow) {
+            // ===== K6 staging: scatter this CTA's rows' excess e_ij of the next tile into a zeroed
+            // shared buffer [chunk][row][16] (the epilogue adds it to S and re-zeroes it) =====
+            int xb = 0;
+            uint32_t xph = 0;
+            for (int64_t t = t0; t < P.n_tiles; t += tstep) {
+                const TcTile tl = P.tiles[t];
+                const int64_t rbase = P.shard_base[tl.s];
+                const int64_t w = P.shard_base[tl.s + 1] - rbase;
+                const int64_t nJ = (w + BN - 1) / BN;
+                const int64_t col0 = (int64_t)tl.J * BN;
+                uint32_t st[4], en[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t row = (int64_t)tl.I * BMT + (int64_t)crank * BM + u * 32 + lane;
+                    st[u] = en[u] = 0;
+                    if (row < w) {
+                        const uint32_t *xi = P.xidx + P.xibase[tl.s] + row * nJ + tl.J;
+                        st[u] = xi[0];
+                        if (tl.J + 1 < nJ) en[u] = xi[1];
+                        else { const uint2 rr = P.xrow[rbase + row]; en[u] = rr.x + rr.y; }
+                    }
+                }
+                mbar_wait(&xempty[xb], xph ^ 1);
+                uint8_t *xd = xbuf + xb * Tr::XBUF_BYTES;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    for (uint32_t q = st[u]; q < en[u]; ++q) {
+                        const uint32_t v = P.rl[q];
+                        const uint32_t c = (v >> 8) - (uint32_t)col0;
+                        xd[(c >> 4) * (BM * 16) + (u * 32 + lane) * 16 + (c & 15u)] = (uint8_t)(v & 0xFFu);
+                    }
+                mbar_arrive(&xfull[xb]);
+                if (++xb == 2) { xb = 0; xph ^= 1; }
+            }
+        }
     } else if (warp >= 4) {
         // ===== epilogue: 8 warps = 2 warpgroups; warp%4 selects the TMEM lane quarter (rows),
         // the warpgroup selects half of the tile's 16-column chunks =====
@@ -339,25 +414,36 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         const int e = threadIdx.x - 128;          // 0..255
         constexpr int NCH = BN / 16;
         const int ch0 = grp ? (NCH + 1) / 2 : 0, ch1 = grp ? NCH : (NCH + 1) / 2;
-        int acc = 0;
-        uint32_t acc_phase = 0;
+        int acc = 0, xb = 0;
+        uint32_t acc_phase = 0, xph = 0;
+        // Everything a tile's epilogue reads from global memory is prefetched one tile ahead
+        // (the epilogue, not the MMA, bounds this kernel, so load latency must not sit on it):
+        // the tile descriptor two tiles ahead, the row/column RowInfo and the K6 run position
+        // while the previous tile's first chunk is processed, the K6 run window three chunks later.
+        const TcTile tnone{0, 0, 0, -1};
+        EpiPre cur, nxt;
+        cur.tl = t0 < P.n_tiles ? P.tiles[t0] : tnone;
+        nxt.tl = t0 + tstep < P.n_tiles ? P.tiles[t0 + tstep] : tnone;
+        epi_pre_rows<BN, BMT>(P, cur, crank, quarter, lane, e);
         for (int64_t t = t0; t < P.n_tiles; t += tstep) {
-            const TcTile tl = P.tiles[t];
+            const TcTile tl = cur.tl;
+            const TcTile tl2 = t + 2 * tstep < P.n_tiles ? P.tiles[t + 2 * tstep] : tnone;
+            const bool has_next = nxt.tl.pad == 0;
             const int64_t rbase = P.shard_base[tl.s];
             const int64_t w = P.shard_base[tl.s + 1] - rbase;
             const int64_t col0 = (int64_t)tl.J * BN, row0 = (int64_t)tl.I * BMT + (int64_t)crank * BM;
             epi_bar();                            // previous tile's colinfo / colsum / rowpart consumed
-            if (e < BN) {
-                const int64_t col = col0 + e;
-                colinfo[e] = col < w ? P.rowinfo[rbase + col] : RowInfo{1u, 0xFFFFFFFFu, 1u, 0u};
-            }
+            if (e < BN) colinfo[e] = cur.ci;
             epi_bar();
             const int64_t row = row0 + quarter * 32 + lane;
             const bool vrow = row < w;
-            const RowInfo ri = vrow ? P.rowinfo[rbase + row] : RowInfo{1u, 0xFFFFFFFFu, 1u, 0u};
+            const RowInfo ri = cur.ri;
             // interior tile: every (row, col) is a real pair with col > row -> no masks
             const bool interior = (row0 + BM <= w) && (col0 + BN <= w) && (col0 > row0 + BM - 1);
             uint16_t *simr = (P.sim && vrow) ? P.sim + P.sim_base[tl.s] : nullptr;
+            // K6: this tile's excess bytes, staged by warp 3
+            uint8_t *xrow_s = xbuf + xb * Tr::XBUF_BYTES + (quarter * 32 + lane) * 16;
+            if (P.xrow) mbar_wait(&xfull[xb], xph);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             unsigned long long rowsum = 0;
@@ -366,21 +452,37 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             for (int ch = ch0; ch < ch1; ++ch) {
                 uint32_t v[16];
                 tmem_ld16(tbase + ch * 16, v);
+                if (has_next && ch == ch0) epi_pre_rows<BN, BMT>(P, nxt, crank, quarter, lane, e);
+                if constexpr (KIND == 1) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = (uint32_t)__uint_as_float(v[j]);
+                }
+                // S = capped-layer contraction + excess e_ij, before the fixed point
+                if (P.xrow) {
+                    uint4 *xs = reinterpret_cast<uint4 *>(xrow_s + ch * (BM * 16));
+                    const uint4 ex = *xs;
+                    if (ex.x | ex.y | ex.z | ex.w) {
+                        *xs = make_uint4(0, 0, 0, 0);
+                        const uint32_t ew[4] = {ex.x, ex.y, ex.z, ex.w};
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] += (ew[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+                    }
+                }
                 unsigned long long cv[16];
                 if (interior && !P.sim) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        const uint32_t S = KIND == 1 ? (uint32_t)__uint_as_float(v[j]) : v[j];
-                        const uint64_t q = pair_q(S, ri, colinfo[ch * 16 + j]);
+                        const uint64_t q = pair_q(v[j], ri, colinfo[ch * 16 + j]);
                         rowsum += q;
                         cv[j] = q;
                     }
                 } else {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        const uint32_t S = KIND == 1 ? (uint32_t)__uint_as_float(v[j]) : v[j];
                         const int64_t col = col0 + ch * 16 + j;
                         const bool ok = vrow && col < w && col >= row;
+                        // the self term is exactly 2^32 (reading A3: S_ii = den_ii = L_i - k + 1)
+                        const uint32_t S = col == row ? ri.tw : v[j];
                         const uint64_t q = pair_q(ok ? S : 0u, ri, colinfo[ch * 16 + j]);
                         rowsum += q;
                         cv[j] = (col != row) ? q : 0ull;
@@ -426,7 +528,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             __syncwarp();
             if (lane == 0) {
                 if constexpr (CG == 1) mbar_arrive(&tempty[acc]); else mbar_arrive_leader(&tempty[acc]);
+                if (P.xrow) mbar_arrive(&xempty[xb]);
             }
+            if (++xb == 2) { xb = 0; xph ^= 1; }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             if (grp == 1) rowpart[quarter * 32 + lane] = rowsum;
             epi_bar();
@@ -439,6 +543,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                 const unsigned long long cs = colsum[e] + colsum[256 + e] + colsum[512 + e] + colsum[768 + e];
                 if (col < w && cs) atomicAdd(&P.T[rbase + col], cs);
             }
+            cur = nxt;
+            nxt.tl = tl2;
         }
     }
     tc_fence_before();
@@ -575,6 +681,10 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
     P.T = a.T;
     P.sim = a.sim;
     P.sim_base = a.sim_base;
+    P.xrow = a.xrow;
+    P.rl = a.rl;
+    P.xidx = a.xidx;
+    P.xibase = a.xibase;
     if (a.cg == 1) {
         const int grid = (int)std::min<int64_t>(a.num_sms, P.n_tiles);
         if (a.kind == 0)

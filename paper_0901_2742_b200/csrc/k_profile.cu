@@ -18,9 +18,10 @@ __constant__ char c_alpha[2][24] = {"ACDEFGHIKLMNPQRSTVWY", "ACGT"};
 // shared-memory histogram (two bins per u32 word; a bin never exceeds L-k+1 <= 65535, so the
 // halves never carry). Pass 2 revisits the windows: the first thread to clear a bin with
 // atomicAnd receives its count and emits the distinct entry (tau << 16 | count), so the
-// histogram is left zeroed for the next sequence. The per-sequence entry list is unordered:
-// no consumer needs tau order (operand rows, GA rank and ancestor records are all sums or
-// scatters over the entries).
+// histogram is left zeroed for the next sequence. The per-sequence entry list is unordered in
+// tau (no consumer needs tau order: operand rows, GA rank and ancestor records are all sums or
+// scatters over the entries) but grouped: the nhi[i] entries with count >= 2 come first, so
+// the K6 consumers (k_indicator's list fill, k_xrows) read only those.
 constexpr int kProfThreads = 128;
 constexpr int kCodeCap = 4096;           // residues staged in shared memory (longer sequences read global)
 __global__ void __launch_bounds__(kProfThreads) k_profile(ProfileArgs a) {
@@ -29,6 +30,8 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfileArgs a) {
     const int HW = (V + 1) >> 1;
     uint8_t *lut = reinterpret_cast<uint8_t *>(sm);          // 256 bytes
     uint32_t *nent = sm + 64;                                 // entry counter of the current sequence
+    uint32_t *exs = sm + 65;                                  // [j] sum_tau (count - 2^j)+ of the current sequence
+    uint32_t *nhi = sm + 69;                                  // entries with count >= 2 of the current sequence
     uint32_t *hist = sm + 72;
     uint8_t *cod = reinterpret_cast<uint8_t *>(hist + HW);    // residue codes of the current sequence
     for (int t = threadIdx.x; t < 72 + HW; t += kProfThreads) sm[t] = 0;
@@ -47,8 +50,8 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfileArgs a) {
     for (int64_t i = i0; i < i1; ++i) {
         if (i >= a.shard_base[s + 1]) {                        // shard change: flush the totals
             if (threadIdx.x == 0 && (acc_w | acc_d)) {
-                atomicAdd(&a.kinfo[s * 4 + 0], acc_w);
-                atomicAdd(&a.kinfo[s * 4 + 1], acc_d);
+                atomicAdd(&a.kinfo[s * kKinfo + 0], acc_w);
+                atomicAdd(&a.kinfo[s * kKinfo + 1], acc_d);
             }
             acc_w = acc_d = 0;
             while (s + 1 < a.pl && i >= a.shard_base[s + 1]) ++s;
@@ -74,6 +77,7 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfileArgs a) {
                 atomicMin(&a.err[L < k ? 1 : 2], gidx);
                 a.rowinfo[i] = RowInfo{1u, 0xFFFFFFFFu, 1u, (uint32_t)s};
                 a.dcnt[i] = 0;
+                a.nhi[i] = 0;
             }
             __syncthreads();
             continue;
@@ -102,14 +106,41 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfileArgs a) {
             const uint32_t old = atomicAnd(&hist[tau >> 1], ~mask);
             const uint32_t c = (tau & 1) ? (old >> 16) : (old & 0xFFFFu);
             if (c) {
-                out[atomicAdd(nent, 1u)] = (tau << 16) | c;
+                // entries with count >= 2 fill the row from the front, count-1 entries from the back
+                if (c >= 2) out[atomicAdd(nhi, 1u)] = (tau << 16) | c;
+                else out[Tw - 1 - atomicAdd(nent, 1u)] = (tau << 16) | c;
                 atomicMax(&Ms[tau], c);
+                if (c >= 2) {                                  // excess beyond the layer caps 1, 2, 4, 8
+#pragma unroll
+                    for (int j = 0; j < kNumCaps; ++j)
+                        if (c > (1u << j)) {
+                            atomicAdd(&exs[j], c - (1u << j));
+                            atomicAdd(&a.Xc[((size_t)s * kNumCaps + j) * V + tau], 1u);
+                        }
+                }
             }
         }
         __syncthreads();
+        // close the gap: [0, n_hi) count >= 2 (the K6 candidates), then [n_hi, d) count 1. Only the
+        // count-1 entries at [max(d, Tw - n_lo), Tw) move, into the gap [n_hi, Tw - n_lo) (disjoint).
+        const uint32_t n_hi = *nhi, n_lo = *nent;
+        {
+            const int64_t d = (int64_t)n_hi + n_lo, src0 = d > Tw - n_lo ? d : Tw - n_lo;
+            for (int64_t t = threadIdx.x; t < Tw - src0; t += kProfThreads) out[n_hi + t] = out[src0 + t];
+        }
+        __syncthreads();
         if (threadIdx.x == 0) {
-            const uint32_t total = *nent;
+            const uint32_t total = n_hi + n_lo;
             *nent = 0;
+            *nhi = 0;
+            a.nhi[i] = (int32_t)n_hi;
+            if (exs[0]) {                      // exs[j] <= exs[0]
+#pragma unroll
+                for (int j = 0; j < kNumCaps; ++j) {
+                    atomicMax(&a.kinfo[s * kKinfo + 4 + j], (unsigned long long)exs[j]);
+                    exs[j] = 0;
+                }
+            }
             a.dcnt[i] = (int32_t)total;
             const uint32_t tw = (uint32_t)Tw;
             a.rowinfo[i] = RowInfo{tw, 0xFFFFFFFFu / tw, 0xFFFFFFFFu % tw + 1u, (uint32_t)s};
@@ -118,8 +149,8 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfileArgs a) {
         }
     }
     if (threadIdx.x == 0 && (acc_w | acc_d)) {
-        atomicAdd(&a.kinfo[s * 4 + 0], acc_w);
-        atomicAdd(&a.kinfo[s * 4 + 1], acc_d);
+        atomicAdd(&a.kinfo[s * kKinfo + 0], acc_w);
+        atomicAdd(&a.kinfo[s * kKinfo + 1], acc_d);
     }
 }
 
@@ -142,32 +173,91 @@ void launch_profile(const ProfileArgs &a, cudaStream_t st) {
     k_profile<<<(unsigned)grid, kProfThreads, smem, st>>>(a);
 }
 
-// K3: per shard, col0(tau) = exclusive scan of M(tau) over tau, K_s = sum_tau M(tau).
-// Column block [col0(tau), col0(tau)+M(tau)) holds the threshold layers t = 1..M(tau)
-// of k-mer tau (SURVEY Appendix A.1 with T = infinity: min(a,b) = sum_t [a>=t][b>=t]).
+// K3: per shard, col0(tau) = exclusive scan over tau of min(M(tau), T_s) and
+// K_s = sum_tau min(M(tau), T_s). Column block [col0(tau), col0(tau) + min(M(tau), T_s)) holds
+// the threshold layers t = 1..min(M(tau), T_s) of k-mer tau (SURVEY Appendix A.1:
+// min(a,b) = min(min(a,T), min(b,T)) + min((a-T)+, (b-T)+), the first term being
+// sum_{t<=T} [a>=t][b>=t]); the second term is the sparse excess of K6 (k_excess.cu).
+// The same kernel (cap = NULL, sel = the chosen cap index per shard) scans the K6 list lengths
+// X_T(tau) = #{i : n_i(tau) > T_s} into per-shard list offsets.
 constexpr int kScanThreads = 1024;
-__global__ void __launch_bounds__(kScanThreads) k_colmap(const uint32_t *M, uint32_t *col0,
-                                                         unsigned long long *kinfo, int V) {
+__global__ void __launch_bounds__(kScanThreads) k_capscan(const uint32_t *in, int64_t in_stride, const uint32_t *sel,
+                                                          const uint32_t *cap, uint32_t *out,
+                                                          unsigned long long *total_out, int total_stride, int V) {
     typedef cub::BlockScan<unsigned long long, kScanThreads> Scan;
     __shared__ typename Scan::TempStorage tmp;
     const int s = blockIdx.x;
-    const uint32_t *m = M + (size_t)s * V;
-    uint32_t *c = col0 + (size_t)s * V;
+    const uint32_t T = cap ? cap[s] : 0xFFFFFFFFu;
+    if (sel && sel[s] >= (uint32_t)kNumCaps) {       // shard without excess lists
+        for (int t = threadIdx.x; t < V; t += kScanThreads) out[(size_t)s * V + t] = 0;
+        if (threadIdx.x == 0 && total_out) total_out[(size_t)s * total_stride] = 0;
+        return;
+    }
+    const uint32_t *m = in + (size_t)s * in_stride + (sel ? (size_t)sel[s] * V : 0);
+    uint32_t *c = out + (size_t)s * V;
     const int per = (V + kScanThreads - 1) / kScanThreads;
     const int t0 = min(V, (int)threadIdx.x * per), t1 = min(V, t0 + per);
     unsigned long long sum = 0;
-    for (int t = t0; t < t1; ++t) sum += m[t];
+    for (int t = t0; t < t1; ++t) sum += min(m[t], T);
     unsigned long long base, total;
     Scan(tmp).ExclusiveSum(sum, base, total);
     for (int t = t0; t < t1; ++t) {
         c[t] = (uint32_t)base;
-        base += m[t];
+        base += min(m[t], T);
     }
-    if (threadIdx.x == 0) kinfo[s * 4 + 2] = total;
+    if (threadIdx.x == 0 && total_out) total_out[(size_t)s * total_stride] = total;
 }
 
-void launch_colmap(const uint32_t *M, uint32_t *col0, unsigned long long *kinfo, int pl, int V, cudaStream_t st) {
-    k_colmap<<<pl, kScanThreads, 0, st>>>(M, col0, kinfo, V);
+void launch_capscan(const uint32_t *in, int64_t in_stride, const uint32_t *sel, const uint32_t *cap, uint32_t *out,
+                    unsigned long long *total_out, int total_stride, int pl, int V, cudaStream_t st) {
+    k_capscan<<<pl, kScanThreads, 0, st>>>(in, in_stride, sel, cap, out, total_out, total_stride, V);
+}
+
+// K3 statistics per shard, for every candidate cap T = 2^j (and no cap):
+//   K_s(T) = sum_tau min(M(tau), T)                        -> kinfo[s][2] (no cap), [8 + j]
+//   sum_tau C(X_T(tau), 2), X_T(tau) = #{i : n_i(tau) > T}  -> kinfo[s][12 + j] (bound of K6 pairs)
+//   sum_tau X_T(tau)                                       -> kinfo[s][16 + j] (K6 list entries)
+__global__ void __launch_bounds__(kScanThreads) k_kstats(const uint32_t *M, const uint32_t *Xc,
+                                                         unsigned long long *kinfo, int V) {
+    constexpr int NV = 3 * kNumCaps + 1;
+    __shared__ unsigned long long red[NV];
+    const int s = blockIdx.x;
+    if (threadIdx.x < NV) red[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t *m = M + (size_t)s * V;
+    const uint32_t *xc = Xc + (size_t)s * kNumCaps * V;
+    unsigned long long acc[NV] = {};
+    for (int t = threadIdx.x; t < V; t += kScanThreads) {
+        const uint32_t x = m[t];
+        acc[kNumCaps] += x;
+#pragma unroll
+        for (int j = 0; j < kNumCaps; ++j) {
+            acc[j] += min(x, 1u << j);
+            const unsigned long long c = xc[(size_t)j * V + t];
+            acc[kNumCaps + 1 + j] += c * (c - (c ? 1 : 0)) / 2;
+            acc[2 * kNumCaps + 1 + j] += c;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        unsigned long long v = acc[j];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&red[j], v);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long *ki = kinfo + (size_t)s * kKinfo;
+        ki[2] = red[kNumCaps];
+        for (int j = 0; j < kNumCaps; ++j) {
+            ki[8 + j] = red[j];
+            ki[12 + j] = red[kNumCaps + 1 + j];
+            ki[16 + j] = red[2 * kNumCaps + 1 + j];
+        }
+    }
+}
+
+void launch_kstats(const uint32_t *M, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V, cudaStream_t st) {
+    k_kstats<<<pl, kScanThreads, 0, st>>>(M, Xc, kinfo, V);
 }
 
 __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl, int64_t r) {
@@ -177,8 +267,10 @@ __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl
 }
 
 // K4: the binary threshold-indicator operand of the tensor-core path,
-//   A_s[i, col0(tau) + t - 1] = 1  for 1 <= t <= n_i(tau)   (uint8, or packed e2m1 nibbles),
-// so that (A_s A_s^T)_ij = sum_tau min(n_i(tau), n_j(tau)) = S_ij exactly. Persistent warps,
+//   A_s[i, col0(tau) + t - 1] = 1  for 1 <= t <= min(n_i(tau), T_s)   (uint8, or packed e2m1 nibbles),
+// so that (A_s A_s^T)_ij = sum_tau min(min(n_i, T_s), min(n_j, T_s)); with T_s unlimited this is
+// S_ij itself. Entries with n_i(tau) > T_s are also placed into the K6 list of (shard, tau)
+// as (row << 8) | (n_i(tau) - T_s) (offsets from k_capscan of the profile's X counts). Persistent warps,
 // one padded row at a time: the row (or a slice of at most kRowSlice bytes) is assembled in
 // the warp's own shared-memory slice and written with 16-byte coalesced stores (rows are
 // 128-byte aligned), so HBM sees exactly one streaming write of the operand.
@@ -187,6 +279,15 @@ constexpr int kOpWarps = 8;
 constexpr int kRowSlice = 16384;
 __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int slice) {
     extern __shared__ __align__(16) uint8_t opsm[];
+    __shared__ unsigned long long lbase[kMaxLocalShards + 1];   // per-shard base of the K6 lists
+    if (threadIdx.x == 0 && a.lists) {
+        unsigned long long acc = 0;
+        for (int s = 0; s < a.pl; ++s) {
+            lbase[s] = acc;
+            acc += a.xtot[s];
+        }
+    }
+    __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t *row = opsm + (size_t)wid * slice;
     uint32_t *row32 = reinterpret_cast<uint32_t *>(row);
@@ -202,6 +303,18 @@ __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int 
         const uint32_t *ent = real ? a.csr + (a.off[i] - i * (int64_t)(a.k - 1)) : nullptr;
         const int d = real ? a.dcnt[i] : 0;
         const uint32_t *c0 = a.col0 + (size_t)s * a.V;
+        const uint32_t T = a.cap ? a.cap[s] : 0xFFFFFFFFu;
+        if (a.lists && real && T != kNoCap) {  // K6 input: this row's entries above the cap
+            const int dh = a.nhi[i];
+            for (int e = lane; e < dh; e += 32) {
+                const uint32_t v = ent[e], n = v & 0xFFFFu;
+                if (n > T) {
+                    const uint32_t key = (uint32_t)s * (uint32_t)a.V + (v >> 16);
+                    const uint32_t pos = atomicAdd(&a.xcur[key], 1u);
+                    a.lists[lbase[s] + a.xoff[key] + pos] = ((uint32_t)local << 8) | (n - T);
+                }
+            }
+        }
         uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a.op) + r * a.stride);
         for (uint32_t ch = 0; ch < stride; ch += (uint32_t)slice) {
             const uint32_t len = min((uint32_t)slice, stride - ch);
@@ -210,7 +323,8 @@ __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int 
             const uint32_t c_lo = ch * per_byte, c_hi = (ch + len) * per_byte;
             for (int e = lane; e < d; e += 32) {
                 const uint32_t v = ent[e];
-                const uint32_t lo = max(c0[v >> 16], c_lo), hi = min(c0[v >> 16] + (v & 0xFFFFu), c_hi);
+                const uint32_t n = v & 0xFFFFu;
+                const uint32_t lo = max(c0[v >> 16], c_lo), hi = min(c0[v >> 16] + min(n, T), c_hi);
                 for (uint32_t c = lo; c < hi; ++c) {
                     const uint32_t cc = c - c_lo;
                     if (a.fp4)        // e2m1 1.0 = 0b0010; neighbouring k-mers may share a word

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -105,10 +106,19 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_rowinfo = b.take<RowInfo>((size_t)n);
     c->d_csr = b.take<uint32_t>((size_t)std::max<int64_t>(R, 1));
     c->d_dcnt = b.take<int32_t>((size_t)n);
+    c->d_nhi = b.take<int32_t>((size_t)n);
     c->d_M = b.take<uint32_t>((size_t)pl * V);
     c->d_col0 = b.take<uint32_t>((size_t)pl * V);
     c->d_err = b.take<unsigned long long>(4);
-    c->d_kinfo = b.take<unsigned long long>((size_t)pl * 4);
+    c->d_kinfo = b.take<unsigned long long>((size_t)pl * kKinfo);
+    c->d_cap = b.take<uint32_t>((size_t)pl);
+    c->d_xsel = b.take<uint32_t>((size_t)pl);
+    c->d_Xc = b.take<uint32_t>((size_t)pl * kNumCaps * V);
+    c->d_xoff = b.take<uint32_t>((size_t)pl * V + 2 * (size_t)pl + 2);
+    c->d_xcur = b.take<uint32_t>((size_t)pl * V);
+    c->d_rcount = b.take<unsigned long long>(1);
+    c->d_xrow = b.take<uint2>((size_t)n);
+    c->d_xibase = b.take<int64_t>((size_t)pl + 1);
     c->d_shard_base = b.take<int64_t>((size_t)pl + 1);
     c->d_shard_rowpad = b.take<int64_t>((size_t)pl + 1);
     c->d_kblocks = b.take<int64_t>((size_t)pl + 1);
@@ -350,6 +360,13 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
             }
         }
         ctx->alu_tiles = tiles;
+        // K6 run index bases: per shard w * ceil(w / BN) u32
+        ctx->h_xibase.assign(ctx->pl + 1, 0);
+        for (int s = 0; s < ctx->pl; ++s) {
+            const int64_t w = sb[s + 1] - sb[s], bn = tc_bn(ctx->tc_kind);
+            ctx->h_xibase[s + 1] = ctx->h_xibase[s] + w * ((w + bn - 1) / bn);
+        }
+        std::memcpy(tbl + 4 * (ctx->pl + 1), ctx->h_xibase.data(), sizeof(int64_t) * (ctx->pl + 1));
         if (ctx->use_tc) {           // the tensor-core tile table of this layout
             const size_t need_b = (size_t)ctx->tc_tiles_cap * 16;
             if (ctx->h_tiles_bytes < need_b) {
@@ -364,12 +381,14 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
             if (ctx->tc_tiles_n > 0)
                 CK(cudaMemcpyAsync(ctx->d_tc_tiles, ctx->h_tiles, (size_t)ctx->tc_tiles_n * 16, cudaMemcpyHostToDevice,
                                    ctx->st));
+
         }
         const size_t tb = sizeof(int64_t) * (ctx->pl + 1);
         CK(cudaMemcpyAsync(ctx->d_shard_base, tbl, tb, cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_shard_rowpad, tbl + (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_sim_base, tbl + 2 * (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_tile_base, tbl + 3 * (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
+        CK(cudaMemcpyAsync(ctx->d_xibase, tbl + 4 * (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
         ctx->tbl_ws = base;
         ctx->tbl_n = n_local;
         ctx->tbl_ng = n_global;
@@ -387,7 +406,8 @@ int sad_build_profiles(sad_ctx *ctx) {
     const int pl = ctx->pl, V = ctx->V;
     CK(cudaMemsetAsync(ctx->d_M, 0, sizeof(uint32_t) * (size_t)pl * V, ctx->st));
     CK(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long) * 4, ctx->st));
-    CK(cudaMemsetAsync(ctx->d_kinfo, 0, sizeof(unsigned long long) * 4 * (size_t)pl, ctx->st));
+    CK(cudaMemsetAsync(ctx->d_kinfo, 0, sizeof(unsigned long long) * kKinfo * (size_t)pl, ctx->st));
+    CK(cudaMemsetAsync(ctx->d_Xc, 0, sizeof(uint32_t) * kNumCaps * (size_t)pl * V, ctx->st));
     ProfileArgs a{};
     a.ascii = ctx->d_ascii;
     a.off = ctx->d_off;
@@ -405,13 +425,15 @@ int sad_build_profiles(sad_ctx *ctx) {
     a.M = ctx->d_M;
     a.err = ctx->d_err;
     a.kinfo = ctx->d_kinfo;
+    a.Xc = ctx->d_Xc;
+    a.nhi = ctx->d_nhi;
     launch_profile(a, ctx->st);
     LAUNCHED();
-    launch_colmap(ctx->d_M, ctx->d_col0, ctx->d_kinfo, pl, V, ctx->st);
+    launch_kstats(ctx->d_M, ctx->d_Xc, ctx->d_kinfo, pl, V, ctx->st);
     LAUNCHED();
+    unsigned long long *hk = ctx->h_small + 8192;
     CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, ctx->st));
-    CK(cudaMemcpyAsync(ctx->h_small + 4, ctx->d_kinfo, sizeof(unsigned long long) * 4 * pl, cudaMemcpyDeviceToHost,
-                       ctx->st));
+    CK(cudaMemcpyAsync(hk, ctx->d_kinfo, sizeof(unsigned long long) * kKinfo * pl, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     const unsigned long long NONE = ~0ull;
     if (ctx->h_small[0] != NONE) {
@@ -432,12 +454,44 @@ int sad_build_profiles(sad_ctx *ctx) {
     ctx->h_windows.assign(pl, 0);
     ctx->h_distinct.assign(pl, 0);
     ctx->h_K.assign(pl, 0);
+    ctx->h_cap.assign(pl, kNoCap);
+    std::vector<uint32_t> sel(pl, kNumCaps);
     int64_t kmax = 0;
+    ctx->n_x = ctx->n_xp = 0;
+    bool any_excess = false;
     for (int s = 0; s < pl; ++s) {
-        ctx->h_windows[s] = (int64_t)ctx->h_small[4 + 4 * s + 0];
-        ctx->h_distinct[s] = (int64_t)ctx->h_small[4 + 4 * s + 1];
-        ctx->h_K[s] = (int64_t)ctx->h_small[4 + 4 * s + 2];
+        const unsigned long long *ki = hk + (size_t)kKinfo * s;
+        ctx->h_windows[s] = (int64_t)ki[0];
+        ctx->h_distinct[s] = (int64_t)ki[1];
+        ctx->h_K[s] = (int64_t)ki[2];
+        // layer cap: the smallest T in {1, 2, 4, 8} whose per-row excess
+        // sum_tau (n_i - T)+ stays <= 255 for every row, so that every pair's excess fits one
+        // byte of the K6 matrix; otherwise all layers stay dense (no cap)
+        // (the K6 row accumulators hold max_w bytes per warp in shared memory)
+        if (ctx->use_tc && !(ctx->cfg.flags & SAD_F_TC_ALL_LAYERS) && rup(ctx->max_w, 16) <= kXrSmem)
+            for (int j = 0; j < kNumCaps; ++j)
+                if (ki[4 + j] <= 255) {
+                    ctx->h_cap[s] = 1u << j;
+                    ctx->h_K[s] = (int64_t)ki[8 + j];
+                    if (ki[4 + j] > 0) {
+                        any_excess = true;
+                        sel[s] = (uint32_t)j;
+                        ctx->n_xp += (int64_t)ki[12 + j];
+                        ctx->n_x += (int64_t)ki[16 + j];
+                    }
+                    break;
+                }
         kmax = std::max(kmax, ctx->h_K[s]);
+    }
+    ctx->use_excess = any_excess;
+    if (ctx->use_tc) {
+        uint32_t *hc = reinterpret_cast<uint32_t *>(ctx->h_small + 12288);
+        for (int s = 0; s < pl; ++s) {
+            hc[s] = ctx->h_cap[s];
+            hc[pl + s] = sel[s];
+        }
+        CK(cudaMemcpyAsync(ctx->d_cap, hc, sizeof(uint32_t) * pl, cudaMemcpyHostToDevice, ctx->st));
+        CK(cudaMemcpyAsync(ctx->d_xsel, hc + pl, sizeof(uint32_t) * pl, cudaMemcpyHostToDevice, ctx->st));
     }
     // operand row: K columns padded to one 128-byte K block = 128 int8 or 256 packed fp4 entries
     ctx->kcols_per_block = (ctx->use_tc && ctx->tc_kind == 1) ? 256 : 128;
@@ -447,12 +501,26 @@ int sad_build_profiles(sad_ctx *ctx) {
     return SAD_OK;
 }
 
+// the operand buffer: [indicator | counts operand][K6 lists L_tau u32][K6 row runs u32][K6 run index u32]
+static void operand_parts(const sad_ctx *ctx, size_t &op, size_t &xl, size_t &xr, size_t &xi) {
+    op = ctx->use_tc ? (size_t)ctx->rows_pad * (size_t)ctx->K_stride : (size_t)ctx->rows_pad * (size_t)ctx->V_pad * 2;
+    op = (size_t)rup((int64_t)op, 1024);
+    xl = xr = xi = 0;
+    if (ctx->use_tc && ctx->use_excess) {
+        xl = (size_t)rup(ctx->n_x * 4, 1024);
+        // runs: n_xp entries at most, plus the chunk allocator's slack (< n_xp + a chunk per warp)
+        xr = (size_t)rup((2 * ctx->n_xp + ((int64_t)ctx->num_sms * 64 + 1) * kRunChunk) * 4, 1024);
+        xi = (size_t)rup(ctx->h_xibase[ctx->pl] * 4 + 4, 1024);
+    }
+}
+
 int sad_operand_size(const sad_ctx *cctx, size_t *bytes) {
     sad_ctx *ctx = const_cast<sad_ctx *>(cctx);
     GUARD(2);
     if (!bytes) return SAD_E_ARG;
-    *bytes = ctx->use_tc ? (size_t)ctx->rows_pad * (size_t)ctx->K_stride
-                         : (size_t)ctx->rows_pad * (size_t)ctx->V_pad * 2;
+    size_t op = 0, xl = 0, xr = 0, xi = 0;
+    operand_parts(ctx, op, xl, xr, xi);
+    *bytes = op + xl + xr + xi;
     return SAD_OK;
 }
 
@@ -504,9 +572,62 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     o.pl = pl;
     o.fp4 = ctx->use_tc && ctx->tc_kind == 1;
     o.op = d_operand;
+    size_t op_b = 0, xl_b = 0, xr_b = 0, xi_b = 0;
+    operand_parts(ctx, op_b, xl_b, xr_b, xi_b);
+    uint32_t *xidx = xl_b ? reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_operand) + op_b + xl_b + xr_b)
+                          : nullptr;
+    uint32_t *lists = xl_b ? reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_operand) + op_b) : nullptr;
+    uint32_t *runs = xl_b ? reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_operand) + op_b + xl_b) : nullptr;
+    unsigned long long *xtot = reinterpret_cast<unsigned long long *>(ctx->d_xoff + (size_t)pl * ctx->V + 1) ;
+    xtot = reinterpret_cast<unsigned long long *>(rup(reinterpret_cast<int64_t>(xtot), 8));
     record_pair(ctx, ctx->ev_pairs_op, true);
-    if (ctx->use_tc) launch_indicator(o, ctx->st); else launch_dense_counts(o, ctx->st);
-    LAUNCHED();
+    if (ctx->use_tc) {
+        // K3 under the layer caps; K6 list offsets; K4 (+ the K6 lists); K6 row runs
+        launch_capscan(ctx->d_M, ctx->V, nullptr, ctx->d_cap, ctx->d_col0, nullptr, 0, pl, ctx->V, ctx->st);
+        LAUNCHED();
+        o.cap = ctx->d_cap;
+        if (lists) {
+            launch_capscan(ctx->d_Xc, (int64_t)kNumCaps * ctx->V, ctx->d_xsel, nullptr, ctx->d_xoff, xtot, 1, pl,
+                           ctx->V, ctx->st);
+            LAUNCHED();
+            CK(cudaMemsetAsync(ctx->d_xcur, 0, sizeof(uint32_t) * (size_t)pl * ctx->V, ctx->st));
+            CK(cudaMemsetAsync(ctx->d_rcount, 0, sizeof(unsigned long long), ctx->st));
+            o.xoff = ctx->d_xoff;
+            o.xtot = xtot;
+            o.nhi = ctx->d_nhi;
+            o.xcur = ctx->d_xcur;
+            o.lists = lists;
+        }
+        launch_indicator(o, ctx->st);
+        LAUNCHED();
+        if (lists) {
+            ExcessArgs x{};
+            x.csr = ctx->d_csr;
+            x.off = ctx->d_off;
+            x.nhi = ctx->d_nhi;
+            x.bn = tc_bn(ctx->tc_kind);
+            x.xibase = ctx->d_xibase;
+            x.xidx = xidx;
+            x.shard_base = ctx->d_shard_base;
+            x.n = ctx->n;
+            x.pl = pl;
+            x.V = ctx->V;
+            x.k = ctx->cfg.k;
+            x.cap = ctx->d_cap;
+            x.xoff = ctx->d_xoff;
+            x.xtot = xtot;
+            x.lists = lists;
+            x.accb = (int)rup(ctx->max_w, 16);
+            x.xrow = ctx->d_xrow;
+            x.rcount = ctx->d_rcount;
+            x.rl = runs;
+            if (launch_excess(x, ctx->st)) return fail(ctx, SAD_E_ARG, "K6: shard too wide for the row accumulators");
+            LAUNCHED();
+        }
+    } else {
+        launch_dense_counts(o, ctx->st);
+        LAUNCHED();
+    }
     record_pair(ctx, ctx->ev_pairs_op, false);
 
     // per shard K blocks (TC)
@@ -547,6 +668,11 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     ap.tiles = ctx->d_tc_tiles;
     ap.n_tiles_tc = ctx->tc_tiles_n;
     ap.cg = ctx->tc_cg;
+    ap.xrow = lists ? ctx->d_xrow : nullptr;
+    if (getenv("SAD_DEBUG_SKIP_EXCESS_EPI")) ap.xrow = nullptr;   // timing experiment only: wrong S
+    ap.rl = runs;
+    ap.xidx = xidx;
+    ap.xibase = ctx->d_xibase;
     record_pair(ctx, ctx->ev_pairs_ap, true);
     if (ctx->use_tc) {
         std::string e;

@@ -8,6 +8,7 @@
 //   csr     u32 [sum Tw]     per sequence, distinct k-mers sorted by tau: (tau << 16) | count;
 //                            sequence i starts at off[i] - i*(k-1)
 //   dcnt    i32 [n]          distinct k-mers per sequence
+//   nhi     i32 [n]          of which count >= 2; those lead the row's CSR entries
 //   M/col0  u32 [pl][V]      per shard max count of tau / first operand column of tau
 //   T       u64 [n]          within-shard fixed-point rank sums (reading A5)
 //   key     u64 [n]          (floor(2^32 S/den) << 31) + source_index
@@ -28,6 +29,14 @@ namespace sad {
 constexpr int kMaxLocalShards = 256;
 constexpr int kRowPad = 128;        // operand rows per shard padded to this (tensor-core M tile)
 constexpr int kColPad = 128;        // operand columns padded to this (one 128-byte K block)
+constexpr int kKinfo = 24;          // u64 per shard in kinfo: [0] windows, [1] distinct, [2] K (no cap),
+                                    // [4 + j] max_i sum_tau (n_i - 2^j)+, [8 + j] K under cap 2^j,
+                                    // [12 + j] sum_tau C(X_j(tau), 2), [16 + j] sum_tau X_j(tau) with
+                                    // X_j(tau) = #{i : n_i(tau) > 2^j}   (j < kNumCaps)
+constexpr int kNumCaps = 4;         // candidate layer caps T = 1, 2, 4, 8
+constexpr int kXrSmem = 200 * 1024; // K6 row accumulators (u8 per shard column) per block
+constexpr int kRunChunk = 1024;     // K6 run entries a warp reserves at a time
+constexpr uint32_t kNoCap = 0xFFFFFFFFu;
 
 struct RowInfo {                    // per local sequence, 16 bytes
     uint32_t tw;                    // L - k + 1 (the den candidate of this row)
@@ -70,10 +79,14 @@ struct ProfileArgs {
     int32_t *dcnt;
     uint32_t *M;                     // [pl][V]
     unsigned long long *err;         // [4]: first bad symbol (idx<<32|pos), first short idx, first long idx, pad
-    unsigned long long *kinfo;       // [pl][4]: windows, distinct, K, pad
+    unsigned long long *kinfo;       // [pl][kKinfo] (see kKinfo)
+    uint32_t *Xc;                    // [pl][kNumCaps][V]: #{i : n_i(tau) > 2^j} (zeroed)
+    int32_t *nhi;                    // [n] entries with count >= 2 (they lead each CSR row)
 };
 void launch_profile(const ProfileArgs &a, cudaStream_t st);
-void launch_colmap(const uint32_t *M, uint32_t *col0, unsigned long long *kinfo, int pl, int V, cudaStream_t st);
+void launch_capscan(const uint32_t *in, int64_t in_stride, const uint32_t *sel, const uint32_t *cap, uint32_t *out,
+                    unsigned long long *total_out, int total_stride, int pl, int V, cudaStream_t st);
+void launch_kstats(const uint32_t *M, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V, cudaStream_t st);
 
 struct OperandArgs {
     const uint32_t *csr;
@@ -87,8 +100,39 @@ struct OperandArgs {
     int k, V, pl;
     int fp4;                         // pack two 4-bit e2m1 entries per byte (1.0 = 0x2)
     void *op;
+    const uint32_t *cap;             // device [pl] layer cap T_s per shard (kNoCap: none), or NULL
+    const uint32_t *xoff;            // device [pl][V] K6 list offsets within the shard's lists
+    const unsigned long long *xtot;  // device [pl] K6 list entries per shard
+    const int32_t *nhi;              // device [n] leading count >= 2 entries per row
+    uint32_t *xcur;                  // device [pl][V] fill cursors (zeroed)
+    uint32_t *lists;                 // K6 lists L_tau: (row << 8) | (n - T_s), or NULL (no excess)
 };
 void launch_indicator(const OperandArgs &a, cudaStream_t st);
+
+// K6: the sparse excess of the capped layers (k_excess.cu),
+//   e_ij = sum_tau min((n_i(tau) - T_s)+, (n_j(tau) - T_s)+)   for i < j in shard s,
+// as one sorted run per row: rl[xrow[i].x ...] = (j << 8) | e_ij for the j > i with e_ij > 0.
+struct ExcessArgs {
+    const uint32_t *csr;
+    const int64_t *off;
+    const int32_t *nhi;              // [n] leading count >= 2 entries of each CSR row
+    const int64_t *shard_base;       // device [pl+1]
+    int64_t n;
+    int pl, V, k;
+    int bn;                          // K5 tile columns (the run index granularity)
+    const int64_t *xibase;           // device [pl+1]: per shard base of xidx
+    uint32_t *xidx;                  // per row [nJ_s]: run position of the first entry with
+                                     // column >= J * BN, nJ_s = ceil(w_s / BN)
+    const uint32_t *cap;             // device [pl]
+    const uint32_t *xoff;            // device [pl][V]
+    const unsigned long long *xtot;  // device [pl]
+    const uint32_t *lists;           // K6 lists L_tau (from K4)
+    int accb;                        // bytes of one row accumulator (max_w rounded up to 16)
+    uint2 *xrow;                     // [n] {first, count} of each row's run
+    unsigned long long *rcount;      // run allocation counter (zeroed)
+    uint32_t *rl;                    // runs
+};
+int launch_excess(const ExcessArgs &a, cudaStream_t st);
 void launch_dense_counts(const OperandArgs &a, cudaStream_t st);
 
 struct AllPairsArgs {
@@ -115,6 +159,10 @@ struct AllPairsArgs {
     const void *tiles;               // TC: device tile table (16 B per tile) and its length
     int64_t n_tiles_tc;
     int cg;                          // TC: 1 = one CTA per tile, 2 = CTA pair (cta_group::2, M = 256)
+    const uint2 *xrow;               // TC: K6 runs {first, count} per local row, or NULL
+    const uint32_t *rl;              // TC: K6 runs (j << 8) | e_ij
+    const uint32_t *xidx;            // TC: K6 run index (see ExcessArgs)
+    const int64_t *xibase;
 };
 void launch_allpairs_alu(const AllPairsArgs &a, cudaStream_t st);
 int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err);
@@ -122,6 +170,7 @@ bool tc_supported(std::string &why);
 int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base, int kind, int cg);
 int64_t tc_tiles_bound(int64_t n, int pl);
 int64_t tc_build_tiles(int pl, const int64_t *h_shard_base, int kind, int cg, void *host_out, int64_t cap);
+int tc_bn(int kind);
 
 struct AncArgs {
     const unsigned long long *T;
@@ -250,6 +299,9 @@ struct sad_ctx {
     std::vector<int64_t> shard_base, shard_rowpad;   // [pl+1]
     int64_t rows_pad = 0, max_w = 0;
     std::vector<int64_t> h_windows, h_distinct, h_K; // [pl]
+    std::vector<uint32_t> h_cap;                      // [pl] layer cap T_s (kNoCap: all layers dense)
+    bool use_excess = false;                          // some shard has entries above its cap (K6 runs)
+    int64_t n_x = 0, n_xp = 0;                        // K6 list entries / bound of the K6 row-run entries
     int64_t K_stride = 0, V_pad = 0;
     bool use_tc = false;
     int tc_kind = 1;                 // 0 = int8, 1 = fp4
@@ -263,9 +315,16 @@ struct sad_ctx {
     int64_t *d_off = nullptr;
     sad::RowInfo *d_rowinfo = nullptr;
     uint32_t *d_csr = nullptr;
-    int32_t *d_dcnt = nullptr;
+    int32_t *d_dcnt = nullptr, *d_nhi = nullptr;
     uint32_t *d_M = nullptr, *d_col0 = nullptr;
     unsigned long long *d_err = nullptr, *d_kinfo = nullptr;
+    uint32_t *d_cap = nullptr, *d_xsel = nullptr;   // layer cap T_s and its index j_s per shard
+    uint32_t *d_Xc = nullptr;        // [pl][kNumCaps][V] entries above each candidate cap
+    uint32_t *d_xoff = nullptr, *d_xcur = nullptr;  // [pl][V] K6 list offsets (+ u64 [pl] totals) / cursors
+    unsigned long long *d_rcount = nullptr;
+    uint2 *d_xrow = nullptr;         // [n] K6 row runs
+    int64_t *d_xibase = nullptr;     // [pl+1] K6 run index bases (host copy below)
+    std::vector<int64_t> h_xibase;
     int64_t *d_shard_base = nullptr, *d_shard_rowpad = nullptr, *d_kblocks = nullptr, *d_sim_base = nullptr;
     int64_t *d_tile_base = nullptr;
     void *d_tc_tiles = nullptr;      // TC tile table (workspace), built once per layout

@@ -22,6 +22,8 @@ from . import _lib as L
 ALPHABETS = {"protein": L.SAD_PROTEIN20, "dna": L.SAD_DNA4}
 KERNELS = {"tc": L.SAD_F_KERNEL_TC, "tc1": L.SAD_F_KERNEL_TC | L.SAD_F_TC_1SM,
            "tc8": L.SAD_F_KERNEL_TC | L.SAD_F_TC_INT8, "tc81": L.SAD_F_KERNEL_TC | L.SAD_F_TC_INT8 | L.SAD_F_TC_1SM,
+           "tcfull": L.SAD_F_KERNEL_TC | L.SAD_F_TC_ALL_LAYERS,
+           "tc8full": L.SAD_F_KERNEL_TC | L.SAD_F_TC_INT8 | L.SAD_F_TC_ALL_LAYERS,
            "alu": L.SAD_F_KERNEL_ALU}
 
 
@@ -85,6 +87,7 @@ class Context:
     kernel: "tc"  tcgen05 threshold-indicator GEMM, packed e2m1 operands, CTA pairs (default)
             "tc1" the same with one CTA per 128-row tile
             "tc8" uint8 operands (kind::i8), CTA pairs; "tc81" uint8, one CTA per tile
+            "tcfull"/"tc8full" every threshold layer dense (no layer cap + sparse excess)
             "alu" CUDA-core min-sum
     """
 

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 def _kernels():
     # the tensor-core kernel is mandatory once built (tc_supported() in k_allpairs_tc.cu)
     import os
-    return ["tc", "tc1", "tc8", "tc81", "alu"] if os.environ.get("SAD_TEST_TC", "1") == "1" else ["alu"]
+    return ["tc", "tc1", "tc8", "tc81", "tcfull", "tc8full", "alu"] if os.environ.get("SAD_TEST_TC", "1") == "1" else ["alu"]
 
 
 KERNELS = _kernels()
@@ -143,6 +143,38 @@ def test_adversarial(kernel):
     ctx, sizes = _run_gpu(a, o, "protein", 3, 4, kernel)
     r = oracle.run(a, o, "protein", 3, 4)
     _compare_full(ctx, sizes, r, a, o, 4)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_excess_path(kernel):
+    """The capped layers + sparse excess: rows whose per-row excess
+    sum_tau (n - T)+ sits just below / above the 255 byte bound of each cap T in {1,2,4,8}
+    (periodic sequences), pairs whose excess is ~200, shards with and without excess, list
+    lengths above a warp, and a ragged tail across several 256 x 240 tiles."""
+    rng = np.random.default_rng(11)
+    alpha = list("ACDEFGHIKLMNPQRSTVWY")
+    seqs = []
+    for _ in range(40):                                         # ~10 3-mers x 21 repeats: excess 200 at T=1
+        seqs.append("ACDEFGHIKL" * 21 + "".join(rng.choice(alpha, int(rng.integers(0, 30)))))
+    seqs += ["ACDEFG" * 50, "MNPQRS" * 43, "ACDEFGHIKLMN" * 23]  # excess > 255 at T=1 (T=2, 4, 8 or none)
+    for _ in range(560):                                        # families with shared repeats
+        base = "".join(rng.choice(alpha, int(rng.integers(40, 500))))
+        rep = "".join(rng.choice(alpha, 4)) * int(rng.integers(1, 12))
+        cut = int(rng.integers(0, len(base)))
+        seqs.append(base[:cut] + rep + base[cut:])
+    order = rng.permutation(len(seqs))
+    seqs = [seqs[i] for i in order]
+    a, o = gen.from_strings(seqs)
+    for p in (1, 3):
+        ctx, sizes = _run_gpu(a, o, "protein", 3, p, kernel)
+        r = oracle.run(a, o, "protein", 3, p)
+        _compare_full(ctx, sizes, r, a, o, p)
+    # one shard with a row far above every cap next to shards with none
+    seqs2 = ["A" * 5000] + ["".join(rng.choice(alpha, int(rng.integers(50, 300)))) for _ in range(299)]
+    a, o = gen.from_strings(seqs2)
+    ctx, sizes = _run_gpu(a, o, "protein", 3, 3, kernel)
+    r = oracle.run(a, o, "protein", 3, 3)
+    _compare_full(ctx, sizes, r, a, o, 3)
 
 
 def test_errors():
