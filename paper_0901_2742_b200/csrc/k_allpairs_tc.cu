@@ -14,8 +14,8 @@
 //   warp 1      MMA issuer: 4 x tcgen05.mma (M=128, N=256, K=32) per stage into one of two
 //               TMEM accumulators (2 x 256 columns), tcgen05.commit to release stages
 //   warp 2      TMEM allocator (512 columns)
-//   warp 3      K6 staging: the next tile's excess bytes e_ij of this CTA's rows, scattered from
-//               the k_xrows runs into a double-buffered shared [chunk][row][16] buffer
+//   warp 3      K6 staging: bulk copies of the next tile's dense excess rows e_ij of this CTA's
+//               rows into a double-buffered shared [row][XSTRIDE] buffer
 //   warps 4-11  fused epilogue (two warpgroups split the tile's columns), overlapped with the next tile's MMAs: tcgen05.ld of S,
 //               exact fixed point q = floor(2^32 S / den) (reading A5), row sums and
 //               column sums (warp transpose-reduce + per-warp shared slots) into T (u64 atomics,
@@ -59,7 +59,8 @@ struct Traits {
     static constexpr int OFF_COLSUM = OFF_COLINFO + 256 * 16;
     static constexpr int OFF_ROWPART = OFF_COLSUM + 4 * 256 * 8;
     static constexpr int OFF_XBUF = OFF_ROWPART + 128 * 8;
-    static constexpr int XBUF_BYTES = BM * BN;         // one tile's K6 excess bytes of this CTA's rows
+    static constexpr int XSTRIDE = BN % 32 == 0 ? BN + 16 : BN;   // odd multiple of 16 B: conflict-free LDS.128
+    static constexpr int XBUF_BYTES = BM * XSTRIDE;    // one tile's K6 excess bytes of this CTA's rows
     static constexpr int SMEM_BYTES = OFF_XBUF + 2 * XBUF_BYTES + 1024;
     // i8: D = S32 (bits 4-5 = 2), A = B = uint8 (0), K-major, N >> 3 at 17, M >> 4 at 24.
     // mxf4: A = B = E2M1 (1) at bits 7 / 10, scale format UE8M0 (bit 23 = 1), K = 64 (bit 31 = 0).
@@ -84,9 +85,9 @@ struct TcParams {
     uint16_t *sim;
     const int64_t *sim_base;
     const uint2 *xrow;               // K6 runs {first, count} per local row, or NULL
-    const uint32_t *rl;              // K6 runs (j << 8) | e_ij, sorted by j
-    const uint32_t *xidx;            // K6 run index: [row][nJ] first entry at col >= J BN
-    const int64_t *xibase;           // [pl+1] per shard base of xidx
+    const uint8_t *E;                // K6 dense excess rows E_s[i][j], row pitch rup(w_s, 16)
+    const int64_t *ebase;            // [pl+1] per shard byte offset of E_s
+    const uint8_t *zero;             // 256 zero bytes
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -115,6 +116,13 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *ba
             smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
+}
+// contiguous global -> shared bulk copy (16-byte aligned, size a multiple of 16) completing `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 // 2-CTA (cta_group::2) variants. A shared::cta address with the peer bit (24) cleared names the
 // same offset in the leader CTA (rank 0) of the pair.
@@ -254,7 +262,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
     uint64_t *xfull = tempty + 2;          // K6 excess buffers: staged by warp 3 / released by the epilogue
     uint64_t *xempty = xfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xempty + 2);
-    uint8_t *xbuf = smem + Tr::OFF_XBUF;    // [2][chunk][BM rows][16 bytes]
+    uint8_t *xbuf = smem + Tr::OFF_XBUF;    // [2][BM rows][XSTRIDE bytes]
     RowInfo *colinfo = reinterpret_cast<RowInfo *>(smem + OFF_COLINFO);
     unsigned long long *colsum = reinterpret_cast<unsigned long long *>(smem + OFF_COLSUM);
     unsigned long long *rowpart = reinterpret_cast<unsigned long long *>(smem + Tr::OFF_ROWPART);
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 8 * CG);          // every epilogue warp of the pair releases
-            mbar_init(&xfull[i], 32);               // every lane of the staging warp
+            mbar_init(&xfull[i], 1);                // the staging warp's expect_tx (bulk copies complete it)
             mbar_init(&xempty[i], 8);               // every epilogue warp of this CTA
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -292,9 +300,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
         }
     }
-    if (P.xrow)                              // the K6 buffers start (and are left by the epilogue) zeroed
-        for (int t = threadIdx.x; t < 2 * Tr::XBUF_BYTES / 16; t += THREADS)
-            reinterpret_cast<uint4 *>(xbuf)[t] = make_uint4(0, 0, 0, 0);
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
@@ -371,38 +376,30 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         }
     } else if (warp == 3) {
         if (P.xrow) {
-            // ===== K6 staging: scatter this CTA's rows' excess e_ij of the next tile into a zeroed
-            // shared buffer [chunk][row][16] (the epilogue adds it to S and re-zeroes it) =====
+            // ===== K6 staging: bulk-copy the tile's 240-byte segments E_s[row][col0 ..] of this CTA's
+            // rows (rows without excess copy a zero segment) into a double-buffered shared
+            // [row][XSTRIDE] buffer; the copies complete the buffer's mbarrier =====
             int xb = 0;
             uint32_t xph = 0;
             for (int64_t t = t0; t < P.n_tiles; t += tstep) {
                 const TcTile tl = P.tiles[t];
                 const int64_t rbase = P.shard_base[tl.s];
                 const int64_t w = P.shard_base[tl.s + 1] - rbase;
-                const int64_t nJ = (w + BN - 1) / BN;
+                const int64_t wp = (w + 15) & ~int64_t(15);
                 const int64_t col0 = (int64_t)tl.J * BN;
-                uint32_t st[4], en[4];
+                const uint32_t nbytes = (uint32_t)min((int64_t)BN, wp - col0);
+                const uint8_t *src[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int64_t row = (int64_t)tl.I * BMT + (int64_t)crank * BM + u * 32 + lane;
-                    st[u] = en[u] = 0;
-                    if (row < w) {
-                        const uint32_t *xi = P.xidx + P.xibase[tl.s] + row * nJ + tl.J;
-                        st[u] = xi[0];
-                        if (tl.J + 1 < nJ) en[u] = xi[1];
-                        else { const uint2 rr = P.xrow[rbase + row]; en[u] = rr.x + rr.y; }
-                    }
+                    src[u] = (row < w && P.xrow[rbase + row].x) ? P.E + P.ebase[tl.s] + row * wp + col0 : P.zero;
                 }
                 mbar_wait(&xempty[xb], xph ^ 1);
+                if (lane == 0) mbar_expect_tx(&xfull[xb], (uint32_t)BM * nbytes);
+                __syncwarp();
                 uint8_t *xd = xbuf + xb * Tr::XBUF_BYTES;
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    for (uint32_t q = st[u]; q < en[u]; ++q) {
-                        const uint32_t v = P.rl[q];
-                        const uint32_t c = (v >> 8) - (uint32_t)col0;
-                        xd[(c >> 4) * (BM * 16) + (u * 32 + lane) * 16 + (c & 15u)] = (uint8_t)(v & 0xFFu);
-                    }
-                mbar_arrive(&xfull[xb]);
+                for (int u = 0; u < 4; ++u) bulk_g2s(xd + (u * 32 + lane) * Tr::XSTRIDE, src[u], nbytes, &xfull[xb]);
                 if (++xb == 2) { xb = 0; xph ^= 1; }
             }
         }
@@ -441,8 +438,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             // interior tile: every (row, col) is a real pair with col > row -> no masks
             const bool interior = (row0 + BM <= w) && (col0 + BN <= w) && (col0 > row0 + BM - 1);
             uint16_t *simr = (P.sim && vrow) ? P.sim + P.sim_base[tl.s] : nullptr;
-            // K6: this tile's excess bytes, staged by warp 3
-            uint8_t *xrow_s = xbuf + xb * Tr::XBUF_BYTES + (quarter * 32 + lane) * 16;
+            // K6: this tile's excess bytes of this row, staged by warp 3
+            const uint8_t *xrow_s = xbuf + xb * Tr::XBUF_BYTES + (quarter * 32 + lane) * Tr::XSTRIDE;
             if (P.xrow) mbar_wait(&xfull[xb], xph);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -459,10 +456,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                 }
                 // S = capped-layer contraction + excess e_ij, before the fixed point
                 if (P.xrow) {
-                    uint4 *xs = reinterpret_cast<uint4 *>(xrow_s + ch * (BM * 16));
-                    const uint4 ex = *xs;
+                    const uint4 ex = *reinterpret_cast<const uint4 *>(xrow_s + ch * 16);
                     if (ex.x | ex.y | ex.z | ex.w) {
-                        *xs = make_uint4(0, 0, 0, 0);
                         const uint32_t ew[4] = {ex.x, ex.y, ex.z, ex.w};
 #pragma unroll
                         for (int j = 0; j < 16; ++j) v[j] += (ew[j >> 2] >> (8 * (j & 3))) & 0xFFu;
@@ -682,9 +677,9 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
     P.sim = a.sim;
     P.sim_base = a.sim_base;
     P.xrow = a.xrow;
-    P.rl = a.rl;
-    P.xidx = a.xidx;
-    P.xibase = a.xibase;
+    P.E = a.E;
+    P.ebase = a.ebase;
+    P.zero = a.zero;
     if (a.cg == 1) {
         const int grid = (int)std::min<int64_t>(a.num_sms, P.n_tiles);
         if (a.kind == 0)

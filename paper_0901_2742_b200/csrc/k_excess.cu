@@ -6,17 +6,20 @@
 // (exact for every integer T >= 0). With the cap T_s = 1 of config 4 the
 // dense contraction shrinks from K = sum_tau max_i n_i(tau) ~ 16.7k to <= V = 8000 columns,
 // while only ~1 % of (row, tau) entries exceed the cap (9.6 per row); they form short per-k-mer
-// lists L_tau (K4 fills them), and a row's excess partners are the union of its lists.
+// lists L_tau (k_xfill), and a row's excess partners are the union of its lists.
 //
 // k_xrows (Gustavson's row-by-row sparse product, one warp per row i of a capped shard):
 //   acc[j] += min(x_i(tau), x_j(tau))  for every tau with x_i(tau) = (n_i(tau) - T)+ > 0 and
 //                                      every j > i in L_tau        (u8 lanes in shared memory)
-//   then the nonzero acc[j] are emitted in increasing j as (j << 8) | e_ij into the row's own
-//   run of `rl` and acc is cleared again. xrow[i] = {first, count} of the run.
-// The K5 epilogue adds e_ij to the tensor-core S before the fixed point (it binary-searches the
-// run for the tile's first column). The host picks T_s so that max_i sum_tau x_i(tau) <= 255:
-// every e_ij then fits its byte and the packed 32-bit shared-memory adds never carry into a
-// neighbour. Integer addition is associative, so the result is independent of the atomic order.
+//   then the row's upper part acc[(i+1) & ~15 ..] is copied with 16-byte stores to the dense
+//   excess matrix E_s[i][.] (u8, row pitch w rounded up to 16) and acc is cleared again;
+//   xrow[i].x = 1 if the row has any excess (rows without it are never read).
+// The K5 kernel's staging warp bulk-copies each tile's 240-byte row segments of E into shared
+// memory, and the epilogue adds e_ij to the tensor-core S before the fixed point (entries at
+// j <= i are never written and never used: the epilogue masks those pairs). The host picks T_s
+// so that max_i sum_tau x_i(tau) <= 255: every e_ij then fits its byte and the packed 32-bit
+// shared-memory adds never carry into a neighbour. Integer addition is associative, so the
+// result is independent of the atomic order.
 #include <algorithm>
 
 #include "sad_internal.cuh"
@@ -25,7 +28,47 @@ namespace sad {
 
 constexpr int kXrWarps = 8;
 
-template <int NCHB>   // K5 tile columns / 16
+// K6 lists: every entry above its shard's cap goes to L_tau as (row << 8) | (n - T_s), one warp
+// per row over the row's leading count >= 2 entries (positions from per-(shard, tau) cursors)
+__global__ void __launch_bounds__(256) k_xfill(ExcessArgs a, uint32_t *xcur) {
+    __shared__ unsigned long long lbase[kMaxLocalShards + 1];
+    if (threadIdx.x == 0) {
+        unsigned long long acc = 0;
+        for (int s = 0; s < a.pl; ++s) {
+            lbase[s] = acc;
+            acc += a.xtot[s];
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    for (int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); r < a.n; r += nw) {
+        int s = 0;
+        while (s + 1 < a.pl && r >= a.shard_base[s + 1]) ++s;
+        const uint32_t T = a.cap[s];
+        if (T == kNoCap) continue;
+        const int dh = a.nhi[r];
+        const uint32_t *ent = a.csr + (a.off[r] - r * (int64_t)(a.k - 1));
+        const uint32_t local = (uint32_t)(r - a.shard_base[s]);
+        for (int e = lane; e < dh; e += 32) {
+            const uint32_t v = ent[e], n = v & 0xFFFFu;
+            if (n > T) {
+                const uint32_t key = (uint32_t)s * (uint32_t)a.V + (v >> 16);
+                const uint32_t pos = atomicAdd(&xcur[key], 1u);
+                const_cast<uint32_t *>(a.lists)[lbase[s] + a.xoff[key] + pos] = (local << 8) | (n - T);
+            }
+        }
+    }
+}
+
+void launch_xfill(const ExcessArgs &a, uint32_t *xcur, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = std::min<int64_t>((int64_t)sms * 8, (a.n + 7) / 8);
+    if (grid > 0) k_xfill<<<(unsigned)grid, 256, 0, st>>>(a, xcur);
+}
+
 __global__ void __launch_bounds__(kXrWarps * 32) k_xrows(ExcessArgs a, int warps) {
     extern __shared__ __align__(16) uint8_t xsm[];
     __shared__ unsigned long long lbase[kMaxLocalShards + 1];
@@ -46,8 +89,6 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows(ExcessArgs a, int warps
     for (int t = lane; t < a.accb / 16; t += 32) acc4[t] = make_uint4(0, 0, 0, 0);
     __syncwarp();
     const int64_t nw = (int64_t)gridDim.x * warps;
-    unsigned long long cpos = 0;                 // the warp's run chunk: next free entry, entries left
-    uint32_t left = 0;
     for (int64_t r = (int64_t)blockIdx.x * warps + wid; r < a.n; r += nw) {
         int s = 0;
         while (s + 1 < a.pl && r >= a.shard_base[s + 1]) ++s;
@@ -105,99 +146,24 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows(ExcessArgs a, int warps
                         const uint32_t b = vb[u] >> 8;
                         if (xa[u] && b > local) {
                             const uint32_t sh = 8u * (b & 3u);
-                            const uint32_t old = atomicAdd(&acc32[b >> 2], min(xa[u], vb[u] & 0xFFu) << sh);
-                            distinct += ((old >> sh) & 0xFFu) == 0u;
+                            atomicAdd(&acc32[b >> 2], min(xa[u], vb[u] & 0xFFu) << sh);
+                            distinct = 1u;
                         }
                     }
                 }
                 __syncwarp();
             }
         }
-        uint32_t total = distinct;
-        for (int o = 16; o; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-        // the row's run: from the warp's current chunk of kRunChunk entries (one global atomic per
-        // chunk, not per row); a row that does not fit the chunk's rest opens a new chunk, a row
-        // above half a chunk gets an exact reservation
-        unsigned long long base = 0;
-        if (total) {
-            if (total <= left) {
-                base = cpos;
-                cpos += total;
-                left -= total;
-            } else {
-                const bool big = total > (uint32_t)(kRunChunk / 2);
-                unsigned long long got = 0;
-                if (lane == 0) got = atomicAdd(a.rcount, big ? (unsigned long long)total : (unsigned long long)kRunChunk);
-                base = __shfl_sync(0xffffffffu, got, 0);
-                if (!big) {
-                    cpos = base + total;
-                    left = (uint32_t)kRunChunk - total;
-                }
+        const bool any = __any_sync(0xffffffffu, distinct != 0u);
+        if (lane == 0) a.xrow[r] = make_uint2(any ? 1u : 0u, 0u);
+        if (any) {                              // the row's upper part -> E_s[i], acc cleared
+            const int nch = (int)((w + 15) >> 4);
+            uint4 *dst = reinterpret_cast<uint4 *>(a.E + a.ebase[s] + (int64_t)local * (nch * 16));
+            for (int c = (int)((local + 1) >> 4) + lane; c < nch; c += 32) {
+                dst[c] = acc4[c];
+                acc4[c] = make_uint4(0, 0, 0, 0);
             }
         }
-        if (lane == 0) a.xrow[r] = make_uint2((uint32_t)base, total);
-        // run index: xi[J] = position of the first entry at column >= J * BN (the K5 tile column
-        // blocks): base before the scanned range, base + total after it
-        const int nJ = (int)((w + NCHB * 16 - 1) / (NCHB * 16));
-        uint32_t *xi = a.xidx + a.xibase[s] + (int64_t)local * nJ;
-        const int c_first = (int)((local + 1) >> 4);
-        for (int J = lane; J < nJ; J += 32)
-            if (J * NCHB <= c_first) xi[J] = (uint32_t)base;
-        __syncwarp();
-        const int nch = (int)((w + 15) >> 4);
-        int c_end = c_first;                    // first chunk not scanned
-        if (total) {                            // emit the nonzero acc[j], j > i, in increasing j
-            uint32_t done = 0;
-            // each lane takes 4 consecutive 16-byte chunks per pass
-            for (int c0 = c_first; c0 < nch && done < total; c0 += 128) {
-                const int cl = c0 + 4 * lane;
-                uint32_t wd[16], m[4], nz[4], nzl = 0;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint4 x = cl + k < nch ? acc4[cl + k] : make_uint4(0, 0, 0, 0);
-                    wd[4 * k + 0] = x.x;
-                    wd[4 * k + 1] = x.y;
-                    wd[4 * k + 2] = x.z;
-                    wd[4 * k + 3] = x.w;
-                    m[k] = 0;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t b = __vcmpne4(wd[4 * k + q], 0u) & 0x01010101u;   // 1 per nonzero byte
-                        m[k] |= ((b * 0x01020408u) >> 24) << (4 * q);
-                    }
-                    nz[k] = __popc(m[k]);
-                    nzl += nz[k];
-                }
-                uint32_t incl = nzl;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                uint32_t pos = (uint32_t)base + done + (incl - nzl);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int c = cl + k;
-                    if (c < nch && c > c_first && c % NCHB == 0) xi[c / NCHB] = pos;   // index boundary
-                    if (nz[k]) {
-                        uint32_t mk = m[k];
-                        const unsigned long long lo = ((unsigned long long)wd[4 * k + 1] << 32) | wd[4 * k + 0];
-                        const unsigned long long hi = ((unsigned long long)wd[4 * k + 3] << 32) | wd[4 * k + 2];
-                        while (mk) {
-                            const int q = __ffs(mk) - 1;
-                            mk &= mk - 1;
-                            const uint32_t byte = (uint32_t)(((q < 8 ? lo : hi) >> (8 * (q & 7))) & 0xFFu);
-                            a.rl[pos++] = ((uint32_t)(c * 16 + q) << 8) | byte;
-                        }
-                        acc4[c] = make_uint4(0, 0, 0, 0);
-                    }
-                }
-                done += __shfl_sync(0xffffffffu, incl, 31);
-                c_end = c0 + 128;
-            }
-        }
-        for (int J = lane; J < nJ; J += 32)      // boundaries past the scanned range
-            if (J * NCHB > c_first && (J * NCHB >= c_end || J * NCHB >= nch)) xi[J] = (uint32_t)(base + total);
         __syncwarp();
     }
 }
@@ -206,22 +172,19 @@ int launch_excess(const ExcessArgs &a, cudaStream_t st) {
     const int warps = (int)std::min<int64_t>(kXrWarps, (int64_t)kXrSmem / a.accb);
     if (warps < 1) return -1;
     const size_t smem = (size_t)warps * a.accb;
-    if (a.bn != 240 && a.bn != 256) return -1;
-    auto kern = a.bn == 240 ? k_xrows<15> : k_xrows<16>;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_xrows<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kXrSmem);
-        cudaFuncSetAttribute(k_xrows<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kXrSmem);
+        cudaFuncSetAttribute(k_xrows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kXrSmem);
         configured = true;
     }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kXrWarps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_xrows, kXrWarps * 32, smem);
     int64_t grid = (int64_t)sms * std::max(per_sm, 1);
     grid = std::min<int64_t>(grid, (a.n + warps - 1) / warps);
-    if (grid > 0) kern<<<(unsigned)grid, kXrWarps * 32, smem, st>>>(a, warps);
+    if (grid > 0) k_xrows<<<(unsigned)grid, kXrWarps * 32, smem, st>>>(a, warps);
     return 0;
 }
 

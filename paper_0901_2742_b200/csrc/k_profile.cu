@@ -269,74 +269,79 @@ __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl
 // K4: the binary threshold-indicator operand of the tensor-core path,
 //   A_s[i, col0(tau) + t - 1] = 1  for 1 <= t <= min(n_i(tau), T_s)   (uint8, or packed e2m1 nibbles),
 // so that (A_s A_s^T)_ij = sum_tau min(min(n_i, T_s), min(n_j, T_s)); with T_s unlimited this is
-// S_ij itself. Entries with n_i(tau) > T_s are also placed into the K6 list of (shard, tau)
-// as (row << 8) | (n_i(tau) - T_s) (offsets from k_capscan of the profile's X counts). Persistent warps,
-// one padded row at a time: the row (or a slice of at most kRowSlice bytes) is assembled in
-// the warp's own shared-memory slice and written with 16-byte coalesced stores (rows are
-// 128-byte aligned), so HBM sees exactly one streaming write of the operand.
+// S_ij itself (the remainder above the cap is K6, k_excess.cu). Persistent warps, one padded row
+// at a time: the row (or a slice of at most kRowSlice bytes) is assembled in the warp's own
+// shared-memory slice and written with 16-byte coalesced stores (rows are 128-byte aligned), so
+// HBM sees exactly one streaming write of the operand. The entry and column-map loads are
+// issued kOpBatch per lane at a time, and the next row's CSR position is fetched one row ahead.
 constexpr int kOpThreads = 256;
 constexpr int kOpWarps = 8;
 constexpr int kRowSlice = 16384;
+constexpr int kOpBatch = 4;
 __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int slice) {
     extern __shared__ __align__(16) uint8_t opsm[];
-    __shared__ unsigned long long lbase[kMaxLocalShards + 1];   // per-shard base of the K6 lists
-    if (threadIdx.x == 0 && a.lists) {
-        unsigned long long acc = 0;
-        for (int s = 0; s < a.pl; ++s) {
-            lbase[s] = acc;
-            acc += a.xtot[s];
-        }
-    }
-    __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t *row = opsm + (size_t)wid * slice;
     uint32_t *row32 = reinterpret_cast<uint32_t *>(row);
     const int64_t nw = (int64_t)gridDim.x * kOpWarps;
     const uint32_t stride = (uint32_t)a.stride;
     const uint32_t per_byte = a.fp4 ? 2u : 1u;               // operand columns per byte
-    for (int64_t r = (int64_t)blockIdx.x * kOpWarps + wid; r < a.rows_pad; r += nw) {
-        const int s = shard_of_padded_row(a.shard_rowpad, a.pl, r);
+    // CSR position (entry offset, entry count) of padded row r; count 0 for padding rows
+    auto locate = [&](int64_t r, int &s, int64_t &eo, int &d) {
+        s = shard_of_padded_row(a.shard_rowpad, a.pl, r);
         const int64_t local = r - a.shard_rowpad[s];
-        const int64_t w = a.shard_base[s + 1] - a.shard_base[s];
-        const bool real = local < w;
+        const bool real = local < a.shard_base[s + 1] - a.shard_base[s];
         const int64_t i = a.shard_base[s] + local;
-        const uint32_t *ent = real ? a.csr + (a.off[i] - i * (int64_t)(a.k - 1)) : nullptr;
-        const int d = real ? a.dcnt[i] : 0;
+        eo = real ? a.off[i] - i * (int64_t)(a.k - 1) : 0;
+        d = real ? a.dcnt[i] : 0;
+    };
+    int64_t r = (int64_t)blockIdx.x * kOpWarps + wid;
+    int s = 0, d = 0;
+    int64_t eo = 0;
+    if (r < a.rows_pad) locate(r, s, eo, d);
+    for (; r < a.rows_pad; r += nw) {
+        const uint32_t *ent = a.csr + eo;
         const uint32_t *c0 = a.col0 + (size_t)s * a.V;
         const uint32_t T = a.cap ? a.cap[s] : 0xFFFFFFFFu;
-        if (a.lists && real && T != kNoCap) {  // K6 input: this row's entries above the cap
-            const int dh = a.nhi[i];
-            for (int e = lane; e < dh; e += 32) {
-                const uint32_t v = ent[e], n = v & 0xFFFFu;
-                if (n > T) {
-                    const uint32_t key = (uint32_t)s * (uint32_t)a.V + (v >> 16);
-                    const uint32_t pos = atomicAdd(&a.xcur[key], 1u);
-                    a.lists[lbase[s] + a.xoff[key] + pos] = ((uint32_t)local << 8) | (n - T);
-                }
-            }
-        }
+        const int dcur = d;
+        int sn = 0, dn = 0;                  // next row of this warp, fetched ahead
+        int64_t eon = 0;
+        if (r + nw < a.rows_pad) locate(r + nw, sn, eon, dn);
         uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a.op) + r * a.stride);
         for (uint32_t ch = 0; ch < stride; ch += (uint32_t)slice) {
             const uint32_t len = min((uint32_t)slice, stride - ch);
             for (uint32_t t = lane; t < len / 16; t += 32) reinterpret_cast<uint4 *>(row)[t] = make_uint4(0, 0, 0, 0);
             __syncwarp();
             const uint32_t c_lo = ch * per_byte, c_hi = (ch + len) * per_byte;
-            for (int e = lane; e < d; e += 32) {
-                const uint32_t v = ent[e];
-                const uint32_t n = v & 0xFFFFu;
-                const uint32_t lo = max(c0[v >> 16], c_lo), hi = min(c0[v >> 16] + min(n, T), c_hi);
-                for (uint32_t c = lo; c < hi; ++c) {
-                    const uint32_t cc = c - c_lo;
-                    if (a.fp4)        // e2m1 1.0 = 0b0010; neighbouring k-mers may share a word
-                        atomicOr(&row32[cc >> 3], 2u << (4 * (cc & 7)));
-                    else
-                        row[cc] = 1;
+            for (int e0 = 0; e0 < dcur; e0 += 32 * kOpBatch) {
+                uint32_t v[kOpBatch], cb[kOpBatch];
+#pragma unroll
+                for (int b = 0; b < kOpBatch; ++b) {
+                    const int e = e0 + b * 32 + lane;
+                    v[b] = e < dcur ? ent[e] : 0u;
+                }
+#pragma unroll
+                for (int b = 0; b < kOpBatch; ++b) cb[b] = (v[b] & 0xFFFFu) ? c0[v[b] >> 16] : 0u;
+#pragma unroll
+                for (int b = 0; b < kOpBatch; ++b) {
+                    const uint32_t n = v[b] & 0xFFFFu;     // 0 for lanes past the row's entries
+                    const uint32_t lo = max(cb[b], c_lo), hi = min(cb[b] + min(n, T), c_hi);
+                    for (uint32_t c = lo; c < hi; ++c) {
+                        const uint32_t cc = c - c_lo;
+                        if (a.fp4)        // e2m1 1.0 = 0b0010; neighbouring k-mers may share a word
+                            atomicOr(&row32[cc >> 3], 2u << (4 * (cc & 7)));
+                        else
+                            row[cc] = 1;
+                    }
                 }
             }
             __syncwarp();
             for (uint32_t t = lane; t < len / 16; t += 32) dst[ch / 16 + t] = reinterpret_cast<const uint4 *>(row)[t];
             __syncwarp();
         }
+        s = sn;
+        eo = eon;
+        d = dn;
     }
 }
 

@@ -116,9 +116,8 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_Xc = b.take<uint32_t>((size_t)pl * kNumCaps * V);
     c->d_xoff = b.take<uint32_t>((size_t)pl * V + 2 * (size_t)pl + 2);
     c->d_xcur = b.take<uint32_t>((size_t)pl * V);
-    c->d_rcount = b.take<unsigned long long>(1);
     c->d_xrow = b.take<uint2>((size_t)n);
-    c->d_xibase = b.take<int64_t>((size_t)pl + 1);
+    c->d_ebase = b.take<int64_t>((size_t)pl + 1);
     c->d_shard_base = b.take<int64_t>((size_t)pl + 1);
     c->d_shard_rowpad = b.take<int64_t>((size_t)pl + 1);
     c->d_kblocks = b.take<int64_t>((size_t)pl + 1);
@@ -244,12 +243,17 @@ int sad_create(const sad_config *cfg, sad_ctx **out) {
         delete ctx;
         return SAD_E_CUDA;
     }
+    if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaFreeHost(ctx->h_small);
+        delete ctx;
+        return SAD_E_CUDA;
+    }
     if (ctx->use_tc) {
         std::string why;
         if (!tc_supported(why)) {
-            fail(ctx, SAD_E_ARG, "tensor-core all-pairs unavailable: %s", why.c_str());
-            cudaFreeHost(ctx->h_small);
-            delete ctx;
+            sad_destroy(ctx);
             return SAD_E_ARG;
         }
     }
@@ -262,6 +266,12 @@ void sad_destroy(sad_ctx *ctx) {
     if (ctx->st) cudaStreamSynchronize(ctx->st); else cudaDeviceSynchronize();
     for (auto &v : {&ctx->ev_pairs_ap, &ctx->ev_pairs_op, &ctx->ev_free})
         for (auto &e : *v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+    }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->h_small) cudaFreeHost(ctx->h_small);
     if (ctx->h_tiles) cudaFreeHost(ctx->h_tiles);
     delete ctx;
@@ -360,13 +370,13 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
             }
         }
         ctx->alu_tiles = tiles;
-        // K6 run index bases: per shard w * ceil(w / BN) u32
-        ctx->h_xibase.assign(ctx->pl + 1, 0);
+        // K6 dense excess matrices: per shard w x rup(w, 16) bytes
+        ctx->h_ebase.assign(ctx->pl + 1, 0);
         for (int s = 0; s < ctx->pl; ++s) {
-            const int64_t w = sb[s + 1] - sb[s], bn = tc_bn(ctx->tc_kind);
-            ctx->h_xibase[s + 1] = ctx->h_xibase[s] + w * ((w + bn - 1) / bn);
+            const int64_t w = sb[s + 1] - sb[s];
+            ctx->h_ebase[s + 1] = ctx->h_ebase[s] + w * rup(w, 16);
         }
-        std::memcpy(tbl + 4 * (ctx->pl + 1), ctx->h_xibase.data(), sizeof(int64_t) * (ctx->pl + 1));
+        std::memcpy(tbl + 4 * (ctx->pl + 1), ctx->h_ebase.data(), sizeof(int64_t) * (ctx->pl + 1));
         if (ctx->use_tc) {           // the tensor-core tile table of this layout
             const size_t need_b = (size_t)ctx->tc_tiles_cap * 16;
             if (ctx->h_tiles_bytes < need_b) {
@@ -388,7 +398,7 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
         CK(cudaMemcpyAsync(ctx->d_shard_rowpad, tbl + (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_sim_base, tbl + 2 * (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_tile_base, tbl + 3 * (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
-        CK(cudaMemcpyAsync(ctx->d_xibase, tbl + 4 * (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
+        CK(cudaMemcpyAsync(ctx->d_ebase, tbl + 4 * (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
         ctx->tbl_ws = base;
         ctx->tbl_n = n_local;
         ctx->tbl_ng = n_global;
@@ -457,7 +467,7 @@ int sad_build_profiles(sad_ctx *ctx) {
     ctx->h_cap.assign(pl, kNoCap);
     std::vector<uint32_t> sel(pl, kNumCaps);
     int64_t kmax = 0;
-    ctx->n_x = ctx->n_xp = 0;
+    ctx->n_x = 0;
     bool any_excess = false;
     for (int s = 0; s < pl; ++s) {
         const unsigned long long *ki = hk + (size_t)kKinfo * s;
@@ -468,7 +478,8 @@ int sad_build_profiles(sad_ctx *ctx) {
         // sum_tau (n_i - T)+ stays <= 255 for every row, so that every pair's excess fits one
         // byte of the K6 matrix; otherwise all layers stay dense (no cap)
         // (the K6 row accumulators hold max_w bytes per warp in shared memory)
-        if (ctx->use_tc && !(ctx->cfg.flags & SAD_F_TC_ALL_LAYERS) && rup(ctx->max_w, 16) <= kXrSmem)
+        if (ctx->use_tc && !(ctx->cfg.flags & SAD_F_TC_ALL_LAYERS) && rup(ctx->max_w, 16) <= kXrSmem &&
+            ctx->h_ebase[pl] <= kMaxExcessBytes)
             for (int j = 0; j < kNumCaps; ++j)
                 if (ki[4 + j] <= 255) {
                     ctx->h_cap[s] = 1u << j;
@@ -476,7 +487,6 @@ int sad_build_profiles(sad_ctx *ctx) {
                     if (ki[4 + j] > 0) {
                         any_excess = true;
                         sel[s] = (uint32_t)j;
-                        ctx->n_xp += (int64_t)ki[12 + j];
                         ctx->n_x += (int64_t)ki[16 + j];
                     }
                     break;
@@ -501,16 +511,14 @@ int sad_build_profiles(sad_ctx *ctx) {
     return SAD_OK;
 }
 
-// the operand buffer: [indicator | counts operand][K6 lists L_tau u32][K6 row runs u32][K6 run index u32]
-static void operand_parts(const sad_ctx *ctx, size_t &op, size_t &xl, size_t &xr, size_t &xi) {
+// the operand buffer: [indicator | counts operand][K6 lists L_tau u32][K6 dense excess E u8 + 256 zero bytes]
+static void operand_parts(const sad_ctx *ctx, size_t &op, size_t &xl, size_t &xe) {
     op = ctx->use_tc ? (size_t)ctx->rows_pad * (size_t)ctx->K_stride : (size_t)ctx->rows_pad * (size_t)ctx->V_pad * 2;
     op = (size_t)rup((int64_t)op, 1024);
-    xl = xr = xi = 0;
+    xl = xe = 0;
     if (ctx->use_tc && ctx->use_excess) {
         xl = (size_t)rup(ctx->n_x * 4, 1024);
-        // runs: n_xp entries at most, plus the chunk allocator's slack (< n_xp + a chunk per warp)
-        xr = (size_t)rup((2 * ctx->n_xp + ((int64_t)ctx->num_sms * 64 + 1) * kRunChunk) * 4, 1024);
-        xi = (size_t)rup(ctx->h_xibase[ctx->pl] * 4 + 4, 1024);
+        xe = (size_t)rup(ctx->h_ebase[ctx->pl] + 256, 1024);
     }
 }
 
@@ -518,9 +526,9 @@ int sad_operand_size(const sad_ctx *cctx, size_t *bytes) {
     sad_ctx *ctx = const_cast<sad_ctx *>(cctx);
     GUARD(2);
     if (!bytes) return SAD_E_ARG;
-    size_t op = 0, xl = 0, xr = 0, xi = 0;
-    operand_parts(ctx, op, xl, xr, xi);
-    *bytes = op + xl + xr + xi;
+    size_t op = 0, xl = 0, xe = 0;
+    operand_parts(ctx, op, xl, xe);
+    *bytes = op + xl + xe;
     return SAD_OK;
 }
 
@@ -572,17 +580,15 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     o.pl = pl;
     o.fp4 = ctx->use_tc && ctx->tc_kind == 1;
     o.op = d_operand;
-    size_t op_b = 0, xl_b = 0, xr_b = 0, xi_b = 0;
-    operand_parts(ctx, op_b, xl_b, xr_b, xi_b);
-    uint32_t *xidx = xl_b ? reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_operand) + op_b + xl_b + xr_b)
-                          : nullptr;
+    size_t op_b = 0, xl_b = 0, xe_b = 0;
+    operand_parts(ctx, op_b, xl_b, xe_b);
     uint32_t *lists = xl_b ? reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_operand) + op_b) : nullptr;
-    uint32_t *runs = xl_b ? reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_operand) + op_b + xl_b) : nullptr;
+    uint8_t *E = xl_b ? reinterpret_cast<uint8_t *>(d_operand) + op_b + xl_b : nullptr;
     unsigned long long *xtot = reinterpret_cast<unsigned long long *>(ctx->d_xoff + (size_t)pl * ctx->V + 1) ;
     xtot = reinterpret_cast<unsigned long long *>(rup(reinterpret_cast<int64_t>(xtot), 8));
     record_pair(ctx, ctx->ev_pairs_op, true);
     if (ctx->use_tc) {
-        // K3 under the layer caps; K6 list offsets; K4 (+ the K6 lists); K6 row runs
+        // K3 under the layer caps; K6 list offsets and lists; K4 beside K6 rows (side stream)
         launch_capscan(ctx->d_M, ctx->V, nullptr, ctx->d_cap, ctx->d_col0, nullptr, 0, pl, ctx->V, ctx->st);
         LAUNCHED();
         o.cap = ctx->d_cap;
@@ -591,23 +597,11 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
                            ctx->V, ctx->st);
             LAUNCHED();
             CK(cudaMemsetAsync(ctx->d_xcur, 0, sizeof(uint32_t) * (size_t)pl * ctx->V, ctx->st));
-            CK(cudaMemsetAsync(ctx->d_rcount, 0, sizeof(unsigned long long), ctx->st));
-            o.xoff = ctx->d_xoff;
-            o.xtot = xtot;
-            o.nhi = ctx->d_nhi;
-            o.xcur = ctx->d_xcur;
-            o.lists = lists;
-        }
-        launch_indicator(o, ctx->st);
-        LAUNCHED();
-        if (lists) {
+            CK(cudaMemsetAsync(E + ctx->h_ebase[pl], 0, 256, ctx->st));   // the zero row segment
             ExcessArgs x{};
             x.csr = ctx->d_csr;
             x.off = ctx->d_off;
             x.nhi = ctx->d_nhi;
-            x.bn = tc_bn(ctx->tc_kind);
-            x.xibase = ctx->d_xibase;
-            x.xidx = xidx;
             x.shard_base = ctx->d_shard_base;
             x.n = ctx->n;
             x.pl = pl;
@@ -619,11 +613,20 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
             x.lists = lists;
             x.accb = (int)rup(ctx->max_w, 16);
             x.xrow = ctx->d_xrow;
-            x.rcount = ctx->d_rcount;
-            x.rl = runs;
-            if (launch_excess(x, ctx->st)) return fail(ctx, SAD_E_ARG, "K6: shard too wide for the row accumulators");
+            x.E = E;
+            x.ebase = ctx->d_ebase;
+            launch_xfill(x, ctx->d_xcur, ctx->st);
             LAUNCHED();
+            // K6 rows on the side stream, concurrently with K4 (both only read the CSR / lists)
+            CK(cudaEventRecord(ctx->ev_fork, ctx->st));
+            CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+            if (launch_excess(x, ctx->side)) return fail(ctx, SAD_E_ARG, "K6: shard too wide for the row accumulators");
+            LAUNCHED();
+            CK(cudaEventRecord(ctx->ev_join, ctx->side));
         }
+        launch_indicator(o, ctx->st);
+        LAUNCHED();
+        if (lists) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_join, 0));
     } else {
         launch_dense_counts(o, ctx->st);
         LAUNCHED();
@@ -670,9 +673,9 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     ap.cg = ctx->tc_cg;
     ap.xrow = lists ? ctx->d_xrow : nullptr;
     if (getenv("SAD_DEBUG_SKIP_EXCESS_EPI")) ap.xrow = nullptr;   // timing experiment only: wrong S
-    ap.rl = runs;
-    ap.xidx = xidx;
-    ap.xibase = ctx->d_xibase;
+    ap.E = E;
+    ap.ebase = ctx->d_ebase;
+    ap.zero = E ? E + ctx->h_ebase[pl] : nullptr;
     record_pair(ctx, ctx->ev_pairs_ap, true);
     if (ctx->use_tc) {
         std::string e;

@@ -35,7 +35,7 @@ constexpr int kKinfo = 24;          // u64 per shard in kinfo: [0] windows, [1] 
                                     // X_j(tau) = #{i : n_i(tau) > 2^j}   (j < kNumCaps)
 constexpr int kNumCaps = 4;         // candidate layer caps T = 1, 2, 4, 8
 constexpr int kXrSmem = 200 * 1024; // K6 row accumulators (u8 per shard column) per block
-constexpr int kRunChunk = 1024;     // K6 run entries a warp reserves at a time
+constexpr int64_t kMaxExcessBytes = int64_t(32) << 30;   // K6 dense excess matrices above this: no layer cap
 constexpr uint32_t kNoCap = 0xFFFFFFFFu;
 
 struct RowInfo {                    // per local sequence, 16 bytes
@@ -101,17 +101,12 @@ struct OperandArgs {
     int fp4;                         // pack two 4-bit e2m1 entries per byte (1.0 = 0x2)
     void *op;
     const uint32_t *cap;             // device [pl] layer cap T_s per shard (kNoCap: none), or NULL
-    const uint32_t *xoff;            // device [pl][V] K6 list offsets within the shard's lists
-    const unsigned long long *xtot;  // device [pl] K6 list entries per shard
-    const int32_t *nhi;              // device [n] leading count >= 2 entries per row
-    uint32_t *xcur;                  // device [pl][V] fill cursors (zeroed)
-    uint32_t *lists;                 // K6 lists L_tau: (row << 8) | (n - T_s), or NULL (no excess)
 };
 void launch_indicator(const OperandArgs &a, cudaStream_t st);
 
 // K6: the sparse excess of the capped layers (k_excess.cu),
 //   e_ij = sum_tau min((n_i(tau) - T_s)+, (n_j(tau) - T_s)+)   for i < j in shard s,
-// as one sorted run per row: rl[xrow[i].x ...] = (j << 8) | e_ij for the j > i with e_ij > 0.
+// as a dense u8 matrix E_s[i][j] (row pitch rup(w_s, 16); only j > i is written).
 struct ExcessArgs {
     const uint32_t *csr;
     const int64_t *off;
@@ -119,20 +114,17 @@ struct ExcessArgs {
     const int64_t *shard_base;       // device [pl+1]
     int64_t n;
     int pl, V, k;
-    int bn;                          // K5 tile columns (the run index granularity)
-    const int64_t *xibase;           // device [pl+1]: per shard base of xidx
-    uint32_t *xidx;                  // per row [nJ_s]: run position of the first entry with
-                                     // column >= J * BN, nJ_s = ceil(w_s / BN)
     const uint32_t *cap;             // device [pl]
     const uint32_t *xoff;            // device [pl][V]
     const unsigned long long *xtot;  // device [pl]
-    const uint32_t *lists;           // K6 lists L_tau (from K4)
+    const uint32_t *lists;           // K6 lists L_tau (from k_xfill)
     int accb;                        // bytes of one row accumulator (max_w rounded up to 16)
-    uint2 *xrow;                     // [n] {first, count} of each row's run
-    unsigned long long *rcount;      // run allocation counter (zeroed)
-    uint32_t *rl;                    // runs
+    uint2 *xrow;                     // [n] .x = 1 if the row has excess
+    uint8_t *E;                      // dense excess rows
+    const int64_t *ebase;            // device [pl+1] per shard byte offset of E_s
 };
 int launch_excess(const ExcessArgs &a, cudaStream_t st);
+void launch_xfill(const ExcessArgs &a, uint32_t *xcur, cudaStream_t st);   // K6 lists (before launch_excess)
 void launch_dense_counts(const OperandArgs &a, cudaStream_t st);
 
 struct AllPairsArgs {
@@ -159,10 +151,10 @@ struct AllPairsArgs {
     const void *tiles;               // TC: device tile table (16 B per tile) and its length
     int64_t n_tiles_tc;
     int cg;                          // TC: 1 = one CTA per tile, 2 = CTA pair (cta_group::2, M = 256)
-    const uint2 *xrow;               // TC: K6 runs {first, count} per local row, or NULL
-    const uint32_t *rl;              // TC: K6 runs (j << 8) | e_ij
-    const uint32_t *xidx;            // TC: K6 run index (see ExcessArgs)
-    const int64_t *xibase;
+    const uint2 *xrow;               // TC: K6 row flags (.x = 1: the row has excess), or NULL
+    const uint8_t *E;                // TC: K6 dense excess rows (see ExcessArgs)
+    const int64_t *ebase;            // TC: device [pl+1] per shard byte offset of E_s
+    const uint8_t *zero;             // TC: 256 zero bytes (the staging source of rows without excess)
 };
 void launch_allpairs_alu(const AllPairsArgs &a, cudaStream_t st);
 int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err);
@@ -287,6 +279,8 @@ void launch_selftest_fixed(int max_den, unsigned long long *bad, cudaStream_t st
 struct sad_ctx {
     sad_config cfg{};
     cudaStream_t st = nullptr;
+    cudaStream_t side = nullptr;     // internal stream: K6 rows run beside K4 (fork/join by events)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int A = 0, V = 0, pl = 0, shard0 = 0;
     int num_sms = 148;
     std::string err;
@@ -301,7 +295,7 @@ struct sad_ctx {
     std::vector<int64_t> h_windows, h_distinct, h_K; // [pl]
     std::vector<uint32_t> h_cap;                      // [pl] layer cap T_s (kNoCap: all layers dense)
     bool use_excess = false;                          // some shard has entries above its cap (K6 runs)
-    int64_t n_x = 0, n_xp = 0;                        // K6 list entries / bound of the K6 row-run entries
+    int64_t n_x = 0;                                  // K6 list entries
     int64_t K_stride = 0, V_pad = 0;
     bool use_tc = false;
     int tc_kind = 1;                 // 0 = int8, 1 = fp4
@@ -321,10 +315,9 @@ struct sad_ctx {
     uint32_t *d_cap = nullptr, *d_xsel = nullptr;   // layer cap T_s and its index j_s per shard
     uint32_t *d_Xc = nullptr;        // [pl][kNumCaps][V] entries above each candidate cap
     uint32_t *d_xoff = nullptr, *d_xcur = nullptr;  // [pl][V] K6 list offsets (+ u64 [pl] totals) / cursors
-    unsigned long long *d_rcount = nullptr;
-    uint2 *d_xrow = nullptr;         // [n] K6 row runs
-    int64_t *d_xibase = nullptr;     // [pl+1] K6 run index bases (host copy below)
-    std::vector<int64_t> h_xibase;
+    uint2 *d_xrow = nullptr;         // [n] K6 row flags
+    int64_t *d_ebase = nullptr;      // [pl+1] K6 dense excess matrix bases (host copy below)
+    std::vector<int64_t> h_ebase;
     int64_t *d_shard_base = nullptr, *d_shard_rowpad = nullptr, *d_kblocks = nullptr, *d_sim_base = nullptr;
     int64_t *d_tile_base = nullptr;
     void *d_tc_tiles = nullptr;      // TC tile table (workspace), built once per layout
