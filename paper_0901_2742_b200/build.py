@@ -43,7 +43,8 @@ def up_to_date() -> bool:
 
 def _compile(src: str) -> tuple[str, str]:
     obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    extra = os.environ.get("SAD_NVCC_EXTRA", "").split()      # experiments only (e.g. -DSAD_TC_STAGES2=6)
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

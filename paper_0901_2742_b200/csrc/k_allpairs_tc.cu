@@ -36,7 +36,9 @@ namespace sad {
 namespace tc {
 constexpr int BM = 128, BK = 128;                 // BK = bytes of K per stage (128B swizzle row)
 constexpr int A_BYTES = BM * BK;                  // 16 KB
-constexpr int THREADS = 384;                   // warps 0-3: TMA, MMA, TMEM alloc, idle; 4-11: epilogue
+constexpr int THREADS = 512;                   // warps 0-3: TMA, MMA, TMEM alloc, K6 staging; 4-15: epilogue
+constexpr int EPI_WARPS = 12;                  // three warpgroups, each covering the tile's 128 TMEM lanes
+constexpr int REG_PRODUCER = 56, REG_EPILOGUE = 152;   // setmaxnreg split: 4*56 + 12*152 = 512*128
 constexpr int SF_COLS = 32;                       // TMEM columns of unit block scales (fp4 path)
 
 // KIND 0: uint8 0/1 operands, tcgen05.mma.kind::i8, int32 accumulators, N = 256.
@@ -48,7 +50,14 @@ struct Traits {
     static constexpr int BN = KIND == 0 ? 256 : SAD_FP4_BN;   // MMA N (tile columns)
     static constexpr int BNC = BN / CG;                 // B rows held by each CTA of the pair
     static constexpr int BMT = BM * CG;                 // tile rows (MMA M)
-    static constexpr int STAGES = CG == 1 ? 3 : 4;
+#ifndef SAD_TC_STAGES2
+#define SAD_TC_STAGES2 4
+#endif
+#ifndef SAD_TC_XBUFS
+#define SAD_TC_XBUFS 2
+#endif
+    static constexpr int STAGES = CG == 1 ? (KIND == 0 ? 2 : 3) : SAD_TC_STAGES2;   // (one-CTA tiles: reference variants)
+    static constexpr int XBUFS = SAD_TC_XBUFS;          // K6 staging buffers
     static constexpr int B_BYTES = BNC * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int ACC_COLS = BN;
@@ -58,10 +67,10 @@ struct Traits {
     static constexpr int OFF_COLINFO = OFF_BAR + 256;
     static constexpr int OFF_COLSUM = OFF_COLINFO + 256 * 16;
     static constexpr int OFF_ROWPART = OFF_COLSUM + 4 * 256 * 8;
-    static constexpr int OFF_XBUF = OFF_ROWPART + 128 * 8;
+    static constexpr int OFF_XBUF = OFF_ROWPART + 2 * 128 * 8;
     static constexpr int XSTRIDE = BN % 32 == 0 ? BN + 16 : BN;   // odd multiple of 16 B: conflict-free LDS.128
     static constexpr int XBUF_BYTES = BM * XSTRIDE;    // one tile's K6 excess bytes of this CTA's rows
-    static constexpr int SMEM_BYTES = OFF_XBUF + 2 * XBUF_BYTES + 1024;
+    static constexpr int SMEM_BYTES = OFF_XBUF + XBUFS * XBUF_BYTES + 1024;
     // i8: D = S32 (bits 4-5 = 2), A = B = uint8 (0), K-major, N >> 3 at 17, M >> 4 at 24.
     // mxf4: A = B = E2M1 (1) at bits 7 / 10, scale format UE8M0 (bit 23 = 1), K = 64 (bit 31 = 0).
     static constexpr uint32_t IDESC =
@@ -216,7 +225,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 384;" ::: "memory"); }
 
 // global inputs of one tile's epilogue for one thread (row = its TMEM lane, column e < BN for the
 // shared colinfo row)
@@ -279,9 +288,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 8 * CG);          // every epilogue warp of the pair releases
+            mbar_init(&tempty[i], EPI_WARPS * CG);  // every epilogue warp of the pair releases
             mbar_init(&xfull[i], 1);                // the staging warp's expect_tx (bulk copies complete it)
-            mbar_init(&xempty[i], 8);               // every epilogue warp of this CTA
+            mbar_init(&xempty[i], EPI_WARPS);       // every epilogue warp of this CTA
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmapA)) : "memory");
@@ -311,6 +320,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
         tc_fence_after();
     }
+    // registers move from the producer warpgroup (TMA, MMA, allocator, K6 staging) to the three
+    // epilogue warpgroups
+    if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REG_PRODUCER));
 
     if (warp == 0) {
         if (lane == 0) {
@@ -329,6 +341,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                         tma_load_2d(&tmapA, &full[stage], sA + stage * A_BYTES, kb * BK, rowA);
                         tma_load_2d(&tmapB, &full[stage], sB + stage * B_BYTES, kb * BK, rowB);
                     } else {
+#ifdef SAD_TC_DBG_NOTMA
+                        if (leader) mbar_arrive(&full[stage]);   // timing experiment: no loads (wrong results)
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        continue;
+#endif
                         // the leader's full barrier counts the bytes of both CTAs
                         if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
                         tma_load_2d_pair(&tmapA, &full[stage], sA + stage * A_BYTES, kb * BK, rowA);
@@ -359,6 +376,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     for (int kk = 0; kk < BK / 32; ++kk) {
                         const uint64_t ad = sw128_desc(a0 + kk * 32), bd = sw128_desc(b0 + kk * 32);
                         const uint32_t accf = (kb | kk) != 0;
+#ifdef SAD_TC_DBG_NOMMA
+                        if (kb >= 0) continue;       // timing experiment: no MMAs (wrong results)
+#endif
                         if constexpr (CG == 1) {
                             if constexpr (KIND == 0) mma_i8(d, ad, bd, Tr::IDESC, accf);
                             else mma_mxf4(d, ad, bd, Tr::IDESC, accf, tmem_base + Tr::SF_COL, tmem_base + Tr::SF_COL);
@@ -400,17 +420,18 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                 uint8_t *xd = xbuf + xb * Tr::XBUF_BYTES;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) bulk_g2s(xd + (u * 32 + lane) * Tr::XSTRIDE, src[u], nbytes, &xfull[xb]);
-                if (++xb == 2) { xb = 0; xph ^= 1; }
+                if (++xb == Tr::XBUFS) { xb = 0; xph ^= 1; }
             }
         }
     } else if (warp >= 4) {
-        // ===== epilogue: 8 warps = 2 warpgroups; warp%4 selects the TMEM lane quarter (rows),
-        // the warpgroup selects half of the tile's 16-column chunks =====
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REG_EPILOGUE));
+        // ===== epilogue: 12 warps = 3 warpgroups; warp%4 selects the TMEM lane quarter (rows),
+        // the warpgroup selects a third of the tile's 16-column chunks =====
         const int quarter = warp & 3;             // TMEM lanes 32*quarter .. +31
-        const int grp = (warp - 4) >> 2;          // 0 or 1
-        const int e = threadIdx.x - 128;          // 0..255
+        const int grp = (warp - 4) >> 2;          // 0, 1 or 2
+        const int e = threadIdx.x - 128;          // 0..383
         constexpr int NCH = BN / 16;
-        const int ch0 = grp ? (NCH + 1) / 2 : 0, ch1 = grp ? NCH : (NCH + 1) / 2;
+        const int ch0 = grp * NCH / 3, ch1 = (grp + 1) * NCH / 3;
         int acc = 0, xb = 0;
         uint32_t acc_phase = 0, xph = 0;
         // Everything a tile's epilogue reads from global memory is prefetched one tile ahead
@@ -446,15 +467,30 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             unsigned long long rowsum = 0;
             const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * ACC_COLS);
 #pragma unroll 1
+#ifdef SAD_TC_DBG_NOEPI
+            for (int ch = ch0; ch < ch0; ++ch) {     // timing experiment: no epilogue work (wrong results)
+#else
             for (int ch = ch0; ch < ch1; ++ch) {
+#endif
                 uint32_t v[16];
+#ifdef SAD_TC_DBG_NOTLD
+                for (int j = 0; j < 16; ++j) v[j] = (uint32_t)(ch * 16 + j + lane);   // timing experiment: no TMEM loads
+#else
                 tmem_ld16(tbase + ch * 16, v);
+#endif
+#ifdef SAD_TC_DBG_TLDONLY
+                if (v[0] == 0xFFFFFFFFu && v[15] == 0xFFFFFFFEu) rowsum += v[3];        // timing experiment: TMEM loads only
+                continue;
+#endif
                 if (has_next && ch == ch0) epi_pre_rows<BN, BMT>(P, nxt, crank, quarter, lane, e);
                 if constexpr (KIND == 1) {
+                    // fp32 accumulators hold exact integers < 2^23: adding 2^23 puts the value in the
+                    // mantissa bits (two ALU ops instead of a float-to-int conversion)
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = (uint32_t)__uint_as_float(v[j]);
+                    for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + 8388608.0f) - 0x4B000000u;
                 }
                 // S = capped-layer contraction + excess e_ij, before the fixed point
+#ifndef SAD_TC_DBG_NOXADD
                 if (P.xrow) {
                     const uint4 ex = *reinterpret_cast<const uint4 *>(xrow_s + ch * 16);
                     if (ex.x | ex.y | ex.z | ex.w) {
@@ -463,11 +499,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                         for (int j = 0; j < 16; ++j) v[j] += (ew[j >> 2] >> (8 * (j & 3))) & 0xFFu;
                     }
                 }
+#endif
                 unsigned long long cv[16];
                 if (interior && !P.sim) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        const uint64_t q = pair_q(v[j], ri, colinfo[ch * 16 + j]);
+                        // length order: every column of a tile strictly above the diagonal is at
+                        // least as long as the row, so the pair's denominator is the row's
+                        const uint64_t q = fixed_q(v[j], ri.tw, ri.qd, ri.rp);
                         rowsum += q;
                         cv[j] = q;
                     }
@@ -482,11 +521,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                         rowsum += q;
                         cv[j] = (col != row) ? q : 0ull;
                         if (simr && ok) {
-                            simr[row * w + col] = (uint16_t)S;
-                            simr[col * w + row] = (uint16_t)S;
+                            const int64_t oi = ri.shard, oj = colinfo[ch * 16 + j].shard;   // local indices
+                            simr[oi * w + oj] = (uint16_t)S;
+                            simr[oj * w + oi] = (uint16_t)S;
                         }
                     }
                 }
+#ifdef SAD_TC_DBG_NOSHFL
+                if (!(lane & 1)) colsum[quarter * 256 + ch * 16 + ((lane >> 1) & 15)] = cv[lane & 15];
+                continue;                    // timing experiment: no column reduction (wrong results)
+#endif
                 // warp transpose-reduce: after offsets 16, 8, 4, 2 lane l holds column (l >> 1) & 15
                 // summed over the 16 lanes sharing bit 0; offset 1 completes the 32-lane sum.
 #pragma unroll
@@ -525,18 +569,18 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                 if constexpr (CG == 1) mbar_arrive(&tempty[acc]); else mbar_arrive_leader(&tempty[acc]);
                 if (P.xrow) mbar_arrive(&xempty[xb]);
             }
-            if (++xb == 2) { xb = 0; xph ^= 1; }
+            if (++xb == Tr::XBUFS) { xb = 0; xph ^= 1; }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-            if (grp == 1) rowpart[quarter * 32 + lane] = rowsum;
+            if (grp) rowpart[(grp - 1) * 128 + quarter * 32 + lane] = rowsum;
             epi_bar();
             if (grp == 0) {
-                rowsum += rowpart[quarter * 32 + lane];
-                if (vrow && rowsum) atomicAdd(&P.T[rbase + row], rowsum);
+                rowsum += rowpart[quarter * 32 + lane] + rowpart[128 + quarter * 32 + lane];
+                if (vrow && rowsum) atomicAdd(&P.T[rbase + ri.shard], rowsum);   // .shard: local index
             }
             if (e < BN) {
                 const int64_t col = col0 + e;
                 const unsigned long long cs = colsum[e] + colsum[256 + e] + colsum[512 + e] + colsum[768 + e];
-                if (col < w && cs) atomicAdd(&P.T[rbase + col], cs);
+                if (col < w && cs) atomicAdd(&P.T[rbase + colinfo[e].shard], cs);
             }
             cur = nxt;
             nxt.tl = tl2;

@@ -8,6 +8,7 @@
 // while only ~1 % of (row, tau) entries exceed the cap (9.6 per row); they form short per-k-mer
 // lists L_tau (k_xfill), and a row's excess partners are the union of its lists.
 //
+// Rows and columns are positions in the shard's length order (sigma); the lists hold positions.
 // k_xrows (Gustavson's row-by-row sparse product, one warp per row i of a capped shard):
 //   acc[j] += min(x_i(tau), x_j(tau))  for every tau with x_i(tau) = (n_i(tau) - T)+ > 0 and
 //                                      every j > i in L_tau        (u8 lanes in shared memory)
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(256) k_xfill(ExcessArgs a, uint32_t *xcur) {
         if (T == kNoCap) continue;
         const int dh = a.nhi[r];
         const uint32_t *ent = a.csr + (a.off[r] - r * (int64_t)(a.k - 1));
-        const uint32_t local = (uint32_t)(r - a.shard_base[s]);
+        const uint32_t local = (uint32_t)a.sigma_inv[r];      // the row's position in length order
         for (int e = lane; e < dh; e += 32) {
             const uint32_t v = ent[e], n = v & 0xFFFFu;
             if (n > T) {
@@ -93,12 +94,13 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows(ExcessArgs a, int warps
         int s = 0;
         while (s + 1 < a.pl && r >= a.shard_base[s + 1]) ++s;
         const uint32_t T = a.cap[s];
-        const uint32_t local = (uint32_t)(r - a.shard_base[s]);
+        const uint32_t local = (uint32_t)(r - a.shard_base[s]);          // sorted position (length order)
+        const int64_t i = a.shard_base[s] + a.sigma[r];                  // the sequence there
         const int64_t w = a.shard_base[s + 1] - a.shard_base[s];
         uint32_t distinct = 0;
         if (T != kNoCap) {
-            const uint32_t *ent = a.csr + (a.off[r] - r * (int64_t)(a.k - 1));
-            const int d = a.nhi[r];               // the row's count >= 2 entries lead its CSR
+            const uint32_t *ent = a.csr + (a.off[i] - i * (int64_t)(a.k - 1));
+            const int d = a.nhi[i];               // the row's count >= 2 entries lead its CSR
             for (int e0 = 0; e0 < d; e0 += 32) {
                 // the batch's excess k-mers: lane-parallel list lookups, then one flattened walk
                 // over the concatenated lists (4 independent loads in flight per lane)

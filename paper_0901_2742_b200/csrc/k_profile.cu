@@ -13,47 +13,74 @@ namespace sad {
 
 __constant__ char c_alpha[2][24] = {"ACDEFGHIKLMNPQRSTVWY", "ACGT"};
 
-// K1+K2. One block of 128 threads per sequence (persistent blocks over contiguous runs of
-// sequences). Pass 1 validates every residue and counts every window in a packed u16
-// shared-memory histogram (two bins per u32 word; a bin never exceeds L-k+1 <= 65535, so the
-// halves never carry). Pass 2 revisits the windows: the first thread to clear a bin with
-// atomicAnd receives its count and emits the distinct entry (tau << 16 | count), so the
-// histogram is left zeroed for the next sequence. The per-sequence entry list is unordered in
-// tau (no consumer needs tau order: operand rows, GA rank and ancestor records are all sums or
-// scatters over the entries) but grouped: the nhi[i] entries with count >= 2 come first, so
-// the K6 consumers (k_indicator's list fill, k_xrows) read only those.
-constexpr int kProfThreads = 128;
-constexpr int kCodeCap = 4096;           // residues staged in shared memory (longer sequences read global)
-__global__ void __launch_bounds__(kProfThreads) k_profile(ProfileArgs a) {
-    extern __shared__ uint32_t sm[];
-    const int V = a.V;
-    const int HW = (V + 1) >> 1;
-    uint8_t *lut = reinterpret_cast<uint8_t *>(sm);          // 256 bytes
-    uint32_t *nent = sm + 64;                                 // entry counter of the current sequence
-    uint32_t *exs = sm + 65;                                  // [j] sum_tau (count - 2^j)+ of the current sequence
-    uint32_t *nhi = sm + 69;                                  // entries with count >= 2 of the current sequence
-    uint32_t *hist = sm + 72;
-    uint8_t *cod = reinterpret_cast<uint8_t *>(hist + HW);    // residue codes of the current sequence
-    for (int t = threadIdx.x; t < 72 + HW; t += kProfThreads) sm[t] = 0;
-    __syncthreads();
-    if (threadIdx.x < 64) sm[threadIdx.x] = 0xFFFFFFFFu;
+// K1+K2. One warp per sequence (persistent warps over contiguous runs of sequences, no block
+// barriers), each with its own packed u16 shared-memory histogram (two bins per u32 word; a bin
+// never exceeds L-k+1 <= 65535, so the halves never carry) and a staging buffer of residue codes.
+// Pass 1 validates every residue (K1) and counts every window tau = sum_m c_m A^(k-1-m) (K2).
+// Pass 2 revisits the windows: the first lane to clear a bin with atomicAnd receives its count
+// and emits the distinct entry (tau << 16 | count), so the histogram is left zeroed for the next
+// sequence. The entry list is unordered in tau (no consumer needs tau order: operand rows, GA
+// rank and ancestor records are all sums or scatters over the entries) but grouped: the nhi[i]
+// entries with count >= 2 come first (warp-aggregated appends from the front, count-1 entries
+// from the back, then the gap is closed), so the K6 consumers read only those. Sequences longer
+// than the staging buffer are processed in segments of windows.
+constexpr int kProfWarps = 12;
+constexpr int kCodeSeg = 2048;           // residue codes staged per warp
+
+template <int KT>
+__device__ __forceinline__ uint32_t window_tau(const uint8_t *c, int k, uint32_t A) {
+    uint32_t tau = 0;
+    if constexpr (KT > 0) {
+#pragma unroll
+        for (int m = 0; m < KT; ++m) tau = tau * A + c[m];
+    } else {
+        for (int m = 0; m < k; ++m) tau = tau * A + c[m];
+    }
+    return tau;
+}
+
+template <int KT>
+__global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int warps, int hw) {
+    extern __shared__ __align__(16) uint32_t psm[];
+    __shared__ uint8_t lut[256];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = threadIdx.x; t < 256; t += blockDim.x) lut[t] = 255;
     __syncthreads();
     if (threadIdx.x < a.A) lut[(uint8_t)c_alpha[a.alphabet][threadIdx.x]] = (uint8_t)threadIdx.x;
     __syncthreads();
+    if (wid >= warps) return;
+    uint32_t *hist = psm + (size_t)wid * (hw + kCodeSeg / 4);
+    uint8_t *cod = reinterpret_cast<uint8_t *>(hist + hw);
+    for (int t = lane; t < hw; t += 32) hist[t] = 0;
+    __syncwarp();
 
-    const int k = a.k;
+    const int k = KT > 0 ? KT : a.k;
     const uint32_t A = (uint32_t)a.A;
-    const int64_t i0 = (int64_t)blockIdx.x * a.n / gridDim.x, i1 = (int64_t)(blockIdx.x + 1) * a.n / gridDim.x;
+    const int V = a.V;
+    const int64_t W = (int64_t)gridDim.x * warps, gw = (int64_t)blockIdx.x * warps + wid;
+    const int64_t i0 = gw * a.n / W, i1 = (gw + 1) * a.n / W;
     int s = 0;
     while (s + 1 < a.pl && i0 >= a.shard_base[s + 1]) ++s;
     unsigned long long acc_w = 0, acc_d = 0;
-    for (int64_t i = i0; i < i1; ++i) {
-        if (i >= a.shard_base[s + 1]) {                        // shard change: flush the totals
-            if (threadIdx.x == 0 && (acc_w | acc_d)) {
+    uint32_t exm[kNumCaps] = {};
+    auto flush = [&]() {
+        if (lane == 0) {
+            if (acc_w | acc_d) {
                 atomicAdd(&a.kinfo[s * kKinfo + 0], acc_w);
                 atomicAdd(&a.kinfo[s * kKinfo + 1], acc_d);
             }
-            acc_w = acc_d = 0;
+#pragma unroll
+            for (int j = 0; j < kNumCaps; ++j)
+                if (exm[j]) atomicMax(&a.kinfo[s * kKinfo + 4 + j], (unsigned long long)exm[j]);
+        }
+        acc_w = acc_d = 0;
+#pragma unroll
+        for (int j = 0; j < kNumCaps; ++j) exm[j] = 0;
+    };
+    const int SW = kCodeSeg - (k - 1);   // windows per segment
+    for (int64_t i = i0; i < i1; ++i) {
+        if (i >= a.shard_base[s + 1]) {                        // shard change: flush the totals
+            flush();
             while (s + 1 < a.pl && i >= a.shard_base[s + 1]) ++s;
         }
         const int64_t off0 = a.off[i];
@@ -61,116 +88,178 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfileArgs a) {
         const uint8_t *x = a.ascii + off0;
         const unsigned long long gidx = (unsigned long long)(a.first_idx + i);
         const int64_t Tw = L - k + 1;
-        const bool bad_len = L < k || Tw > 65535;              // readings A19 / SURVEY A.3 precondition
-        const bool staged = L <= kCodeCap;
-        // pass 0: K1 — every residue must be a letter of the alphabet (reading A18); codes to smem
-        for (int64_t t = threadIdx.x; t < L; t += kProfThreads) {
-            uint32_t c = lut[x[t]];
-            if (c == 255) {
-                atomicMin(&a.err[0], (gidx << 32) | (unsigned long long)t);
-                c = 0;
-            }
-            if (staged) cod[t] = (uint8_t)c;
-        }
-        if (bad_len) {
-            if (threadIdx.x == 0) {
+        if (L < k || Tw > 65535) {                             // readings A19 / SURVEY A.3 precondition
+            for (int64_t t = lane; t < L; t += 32)
+                if (lut[x[t]] == 255) atomicMin(&a.err[0], (gidx << 32) | (unsigned long long)t);
+            if (lane == 0) {
                 atomicMin(&a.err[L < k ? 1 : 2], gidx);
                 a.rowinfo[i] = RowInfo{1u, 0xFFFFFFFFu, 1u, (uint32_t)s};
                 a.dcnt[i] = 0;
                 a.nhi[i] = 0;
             }
-            __syncthreads();
             continue;
         }
-        __syncthreads();
-        // pass 1: K2 — count every window (overlaps included)
-        for (int64_t t = threadIdx.x; t < Tw; t += kProfThreads) {
-            uint32_t tau = 0;
-            for (int m = 0; m < k; ++m) {
-                const uint32_t c = staged ? (uint32_t)cod[t + m] : (uint32_t)lut[x[t + m]];
-                tau = tau * A + (c == 255 ? 0u : c);
+        const int nseg = (int)((Tw + SW - 1) / SW);
+        // stage the codes of segment g: residues [g SW, min(L, (g + 1) SW + k - 1)); K1 on the first pass
+        // (16-byte aligned vector loads: the residue buffer is padded by 16 bytes past its end)
+        auto stage = [&](int g, bool check) {
+            const int64_t r0 = (int64_t)g * SW, r1 = min(L, r0 + SW + k - 1);
+            const int64_t b0 = (off0 + r0) & ~int64_t(15), b1 = off0 + r1;
+            for (int64_t b = b0 + 16 * lane; b < b1; b += 512) {
+                const uint4 q = *reinterpret_cast<const uint4 *>(a.ascii + b);
+                const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int64_t t = b + j - off0;          // residue position in the sequence
+                    if (t >= r0 && t < r1) {
+                        uint32_t c = lut[(qw[j >> 2] >> (8 * (j & 3))) & 0xFFu];
+                        if (c == 255) {
+                            if (check) atomicMin(&a.err[0], (gidx << 32) | (unsigned long long)t);
+                            c = 0;
+                        }
+                        cod[t - r0] = (uint8_t)c;
+                    }
+                }
             }
-            atomicAdd(&hist[tau >> 1], (tau & 1) ? 0x10000u : 1u);
+            __syncwarp();
+        };
+        // pass 1: count every window (overlaps included)
+        for (int g = 0; g < nseg; ++g) {
+            stage(g, true);
+            const int w1 = (int)min((int64_t)SW, Tw - (int64_t)g * SW);
+            for (int t = lane; t < w1; t += 32) {
+                const uint32_t tau = window_tau<KT>(cod + t, k, A);
+                atomicAdd(&hist[tau >> 1], (tau & 1) ? 0x10000u : 1u);
+            }
+            __syncwarp();
         }
-        __syncthreads();
         // pass 2: claim every bin once, emit (tau, count), update the shard's column maxima
         uint32_t *out = a.csr + (off0 - i * (int64_t)(k - 1));
         uint32_t *Ms = a.M + (size_t)s * V;
-        for (int64_t t = threadIdx.x; t < Tw; t += kProfThreads) {
-            uint32_t tau = 0;
-            for (int m = 0; m < k; ++m) {
-                const uint32_t c = staged ? (uint32_t)cod[t + m] : (uint32_t)lut[x[t + m]];
-                tau = tau * A + (c == 255 ? 0u : c);
-            }
-            const uint32_t mask = (tau & 1) ? 0xFFFF0000u : 0x0000FFFFu;
-            const uint32_t old = atomicAnd(&hist[tau >> 1], ~mask);
-            const uint32_t c = (tau & 1) ? (old >> 16) : (old & 0xFFFFu);
-            if (c) {
-                // entries with count >= 2 fill the row from the front, count-1 entries from the back
-                if (c >= 2) out[atomicAdd(nhi, 1u)] = (tau << 16) | c;
-                else out[Tw - 1 - atomicAdd(nent, 1u)] = (tau << 16) | c;
-                atomicMax(&Ms[tau], c);
-                if (c >= 2) {                                  // excess beyond the layer caps 1, 2, 4, 8
+        uint32_t n_hi = 0, n_lo = 0, ex[kNumCaps] = {};
+        for (int g = nseg - 1; g >= 0; --g) {                  // the last staged segment first
+            if (g != nseg - 1) stage(g, false);
+            const int w1 = (int)min((int64_t)SW, Tw - (int64_t)g * SW);
+            for (int t0 = 0; t0 < w1; t0 += 32) {
+                const int t = t0 + lane;
+                uint32_t c = 0, tau = 0;
+                if (t < w1) {
+                    tau = window_tau<KT>(cod + t, k, A);
+                    const uint32_t mask = (tau & 1) ? 0xFFFF0000u : 0x0000FFFFu;
+                    const uint32_t old = atomicAnd(&hist[tau >> 1], ~mask);
+                    c = (tau & 1) ? (old >> 16) : (old & 0xFFFFu);
+                }
+                const uint32_t mh = __ballot_sync(0xffffffffu, c >= 2), ml = __ballot_sync(0xffffffffu, c == 1);
+                const uint32_t lt = (1u << lane) - 1u;
+                if (c >= 2) out[n_hi + __popc(mh & lt)] = (tau << 16) | c;
+                else if (c == 1) out[Tw - 1 - (n_lo + __popc(ml & lt))] = (tau << 16) | 1u;
+                n_hi += __popc(mh);
+                n_lo += __popc(ml);
+                if (c) {
+                    atomicMax(&Ms[tau], c);
+                    if (c >= 2) {                              // excess beyond the layer caps 1, 2, 4, 8
 #pragma unroll
-                    for (int j = 0; j < kNumCaps; ++j)
-                        if (c > (1u << j)) {
-                            atomicAdd(&exs[j], c - (1u << j));
-                            atomicAdd(&a.Xc[((size_t)s * kNumCaps + j) * V + tau], 1u);
-                        }
+                        for (int j = 0; j < kNumCaps; ++j)
+                            if (c > (1u << j)) {
+                                ex[j] += c - (1u << j);
+                                atomicAdd(&a.Xc[((size_t)s * kNumCaps + j) * V + tau], 1u);
+                            }
+                    }
                 }
             }
         }
-        __syncthreads();
+        __syncwarp();
         // close the gap: [0, n_hi) count >= 2 (the K6 candidates), then [n_hi, d) count 1. Only the
         // count-1 entries at [max(d, Tw - n_lo), Tw) move, into the gap [n_hi, Tw - n_lo) (disjoint).
-        const uint32_t n_hi = *nhi, n_lo = *nent;
         {
             const int64_t d = (int64_t)n_hi + n_lo, src0 = d > Tw - n_lo ? d : Tw - n_lo;
-            for (int64_t t = threadIdx.x; t < Tw - src0; t += kProfThreads) out[n_hi + t] = out[src0 + t];
+            for (int64_t t = lane; t < Tw - src0; t += 32) out[n_hi + t] = out[src0 + t];
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const uint32_t total = n_hi + n_lo;
-            *nent = 0;
-            *nhi = 0;
-            a.nhi[i] = (int32_t)n_hi;
-            if (exs[0]) {                      // exs[j] <= exs[0]
 #pragma unroll
-                for (int j = 0; j < kNumCaps; ++j) {
-                    atomicMax(&a.kinfo[s * kKinfo + 4 + j], (unsigned long long)exs[j]);
-                    exs[j] = 0;
-                }
-            }
-            a.dcnt[i] = (int32_t)total;
+        for (int j = 0; j < kNumCaps; ++j) {
+            uint32_t v = ex[j];
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            exm[j] = max(exm[j], v);
+        }
+        if (lane == 0) {
+            a.nhi[i] = (int32_t)n_hi;
+            a.dcnt[i] = (int32_t)(n_hi + n_lo);
             const uint32_t tw = (uint32_t)Tw;
             a.rowinfo[i] = RowInfo{tw, 0xFFFFFFFFu / tw, 0xFFFFFFFFu % tw + 1u, (uint32_t)s};
-            acc_w += (unsigned long long)Tw;
-            acc_d += total;
         }
+        acc_w += (unsigned long long)Tw;
+        acc_d += n_hi + n_lo;
+        __syncwarp();
     }
-    if (threadIdx.x == 0 && (acc_w | acc_d)) {
-        atomicAdd(&a.kinfo[s * kKinfo + 0], acc_w);
-        atomicAdd(&a.kinfo[s * kKinfo + 1], acc_d);
-    }
+    flush();
 }
 
 void launch_profile(const ProfileArgs &a, cudaStream_t st) {
-    const int HW = (a.V + 1) / 2;
-    const size_t smem = (size_t)(72 + HW) * 4 + kCodeCap;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(k_profile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
+    const int hw = (a.V + 1) / 2;
+    const size_t per_warp = (size_t)hw * 4 + kCodeSeg;
+    const int warps = (int)std::max<size_t>(1, std::min<size_t>(kProfWarps, (size_t)(110 * 1024) / per_warp));
+    const size_t smem = per_warp * warps;
+    auto kern = a.k == 3 ? k_profile<3> : a.k == 6 ? k_profile<6> : k_profile<0>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_profile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_profile<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_profile<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
     }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_profile, kProfThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kProfWarps * 32, smem);
     int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-    if (grid > a.n) grid = a.n;
+    grid = std::min<int64_t>(grid, (a.n + warps - 1) / warps);
     if (grid < 1) grid = 1;
-    k_profile<<<(unsigned)grid, kProfThreads, smem, st>>>(a);
+    kern<<<(unsigned)grid, kProfWarps * 32, smem, st>>>(a, warps, hw);
+}
+
+// Length order of every shard (the all-pairs kernel works on rows sorted by L - k + 1, so that
+// in a tile strictly above the diagonal every pair's denominator min(L_i, L_j) - k + 1 is the
+// row's own; T and S are permutation invariant): keys (shard, Tw) with the local index as the
+// value of one stable radix sort, then sigma (sorted position -> local index), its inverse, and the sorted RowInfo with
+// .shard replaced by the local index.
+__global__ void k_lenkeys(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *keys,
+                          int32_t *vals) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int s = 0;
+        while (s + 1 < pl && i >= shard_base[s + 1]) ++s;
+        keys[i] = ((uint32_t)s << 16) | rowinfo[i].tw;          // stable sort: ties keep index order
+        vals[i] = (int32_t)(i - shard_base[s]);
+    }
+}
+
+__global__ void k_lenperm(const uint32_t *keys_sorted, const int32_t *vals_sorted, const RowInfo *rowinfo,
+                          const int64_t *shard_base, int64_t n, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(keys_sorted[p] >> 16);
+        const int32_t local = vals_sorted[p];
+        const int64_t b = shard_base[s];
+        sigma[p] = local;
+        sigma_inv[b + local] = (int32_t)(p - b);
+        RowInfo r = rowinfo[b + local];
+        r.shard = (uint32_t)local;
+        rinfo_s[p] = r;
+    }
+}
+
+void launch_lenkeys(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *keys,
+                    int32_t *vals, cudaStream_t st) {
+    const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
+    if (g > 0) k_lenkeys<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, keys, vals);
+}
+
+void launch_lenperm(const uint32_t *keys_sorted, const int32_t *vals_sorted, const RowInfo *rowinfo,
+                    const int64_t *shard_base, int64_t n, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s,
+                    cudaStream_t st) {
+    const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
+    if (g > 0)
+        k_lenperm<<<(unsigned)g, 256, 0, st>>>(keys_sorted, vals_sorted, rowinfo, shard_base, n, sigma, sigma_inv,
+                                                rinfo_s);
 }
 
 // K3: per shard, col0(tau) = exclusive scan over tau of min(M(tau), T_s) and
@@ -269,8 +358,8 @@ __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl
 // K4: the binary threshold-indicator operand of the tensor-core path,
 //   A_s[i, col0(tau) + t - 1] = 1  for 1 <= t <= min(n_i(tau), T_s)   (uint8, or packed e2m1 nibbles),
 // so that (A_s A_s^T)_ij = sum_tau min(min(n_i, T_s), min(n_j, T_s)); with T_s unlimited this is
-// S_ij itself (the remainder above the cap is K6, k_excess.cu). Persistent warps, one padded row
-// at a time: the row (or a slice of at most kRowSlice bytes) is assembled in the warp's own
+// S_ij itself (the remainder above the cap is K6, k_excess.cu). Operand row r of shard s is the
+// sequence sigma_s(r) (length order). Persistent warps, one padded row at a time: the row (or a slice of at most kRowSlice bytes) is assembled in the warp's own
 // shared-memory slice and written with 16-byte coalesced stores (rows are 128-byte aligned), so
 // HBM sees exactly one streaming write of the operand. The entry and column-map loads are
 // issued kOpBatch per lane at a time, and the next row's CSR position is fetched one row ahead.
@@ -291,7 +380,7 @@ __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int 
         s = shard_of_padded_row(a.shard_rowpad, a.pl, r);
         const int64_t local = r - a.shard_rowpad[s];
         const bool real = local < a.shard_base[s + 1] - a.shard_base[s];
-        const int64_t i = a.shard_base[s] + local;
+        const int64_t i = a.shard_base[s] + (real && a.sigma ? a.sigma[a.shard_base[s] + local] : local);
         eo = real ? a.off[i] - i * (int64_t)(a.k - 1) : 0;
         d = real ? a.dcnt[i] : 0;
     };

@@ -94,7 +94,10 @@ size_t cub_bytes_needed(int64_t n, int pl) {
                                              (const int64_t *)nullptr, (const int64_t *)nullptr, 0, 64);
     cub::DeviceRadixSort::SortKeys(nullptr, b, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
                                    (int)std::max<int64_t>(n, 1), 0, 64);
-    return std::max(a, b) + 1024;
+    size_t c = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint32_t *)nullptr, (uint32_t *)nullptr, (const int32_t *)nullptr,
+                                    (int32_t *)nullptr, (int)std::max<int64_t>(n, 1), 0, 32);
+    return std::max(std::max(a, b), c) + 1024;
 }
 
 // carve the workspace; with base == nullptr only the size is computed
@@ -107,6 +110,9 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_csr = b.take<uint32_t>((size_t)std::max<int64_t>(R, 1));
     c->d_dcnt = b.take<int32_t>((size_t)n);
     c->d_nhi = b.take<int32_t>((size_t)n);
+    c->d_sigma = b.take<int32_t>((size_t)n);
+    c->d_sigma_inv = b.take<int32_t>((size_t)n);
+    c->d_rinfo_s = b.take<RowInfo>((size_t)n);
     c->d_M = b.take<uint32_t>((size_t)pl * V);
     c->d_col0 = b.take<uint32_t>((size_t)pl * V);
     c->d_err = b.take<unsigned long long>(4);
@@ -315,6 +321,7 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
                     (long long)(first_index_of_rank(ctx, n_global) + sb[ctx->pl]), (long long)n_local,
                     (long long)first_source_index);
     if (n_local == 0) return fail(ctx, SAD_E_EMPTY, "rank has no sequences");
+    if (n_global / p + 1 >= (int64_t(1) << 24)) return fail(ctx, SAD_E_ARG, "shards of 2^24 or more sequences");
     int64_t R = residues_local;
     bool need_sync = mem == SAD_MEM_HOST;     // host inputs may be reused by the caller on return
     if (mem == SAD_MEM_HOST) {
@@ -588,7 +595,23 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     xtot = reinterpret_cast<unsigned long long *>(rup(reinterpret_cast<int64_t>(xtot), 8));
     record_pair(ctx, ctx->ev_pairs_op, true);
     if (ctx->use_tc) {
-        // K3 under the layer caps; K6 list offsets and lists; K4 beside K6 rows (side stream)
+        // length order of every shard (sigma), then K3 under the layer caps; K6 list offsets and
+        // lists; K4 beside K6 rows (side stream)
+        {
+            uint32_t *k_in = reinterpret_cast<uint32_t *>(ctx->d_ckey), *k_out = reinterpret_cast<uint32_t *>(ctx->d_ckey_sorted);
+            launch_lenkeys(ctx->d_rowinfo, ctx->d_shard_base, pl, ctx->n, k_in, ctx->d_perm_in, ctx->st);
+            LAUNCHED();
+            size_t tb = ctx->cub_bytes;
+            int sbits = 0;
+            while ((1 << sbits) < pl) ++sbits;
+            CK(cub::DeviceRadixSort::SortPairs(ctx->d_cub, tb, k_in, k_out, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
+                                               0, 16 + sbits, ctx->st));
+            LAUNCHED();
+            launch_lenperm(k_out, ctx->d_perm_sorted, ctx->d_rowinfo, ctx->d_shard_base, ctx->n, ctx->d_sigma,
+                           ctx->d_sigma_inv, ctx->d_rinfo_s, ctx->st);
+        }
+        LAUNCHED();
+        o.sigma = ctx->d_sigma;
         launch_capscan(ctx->d_M, ctx->V, nullptr, ctx->d_cap, ctx->d_col0, nullptr, 0, pl, ctx->V, ctx->st);
         LAUNCHED();
         o.cap = ctx->d_cap;
@@ -615,6 +638,8 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
             x.xrow = ctx->d_xrow;
             x.E = E;
             x.ebase = ctx->d_ebase;
+            x.sigma = ctx->d_sigma;
+            x.sigma_inv = ctx->d_sigma_inv;
             launch_xfill(x, ctx->d_xcur, ctx->st);
             LAUNCHED();
             // K6 rows on the side stream, concurrently with K4 (both only read the CSR / lists)
@@ -651,7 +676,7 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     AllPairsArgs ap{};
     ap.op = d_operand;
     ap.stride = o.stride;
-    ap.rowinfo = ctx->d_rowinfo;
+    ap.rowinfo = ctx->use_tc ? ctx->d_rinfo_s : ctx->d_rowinfo;   // TC: length order
     ap.shard_base = ctx->d_shard_base;
     ap.shard_rowpad = ctx->d_shard_rowpad;
     ap.shard_kblocks = ctx->d_kblocks;

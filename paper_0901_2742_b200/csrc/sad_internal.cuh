@@ -101,12 +101,19 @@ struct OperandArgs {
     int fp4;                         // pack two 4-bit e2m1 entries per byte (1.0 = 0x2)
     void *op;
     const uint32_t *cap;             // device [pl] layer cap T_s per shard (kNoCap: none), or NULL
+    const int32_t *sigma;            // device [n] length order (sorted position -> local index), or NULL
 };
 void launch_indicator(const OperandArgs &a, cudaStream_t st);
+void launch_lenkeys(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *keys,
+                    int32_t *vals, cudaStream_t st);
+void launch_lenperm(const uint32_t *keys_sorted, const int32_t *vals_sorted, const RowInfo *rowinfo,
+                    const int64_t *shard_base, int64_t n, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s,
+                    cudaStream_t st);
 
 // K6: the sparse excess of the capped layers (k_excess.cu),
 //   e_ij = sum_tau min((n_i(tau) - T_s)+, (n_j(tau) - T_s)+)   for i < j in shard s,
-// as a dense u8 matrix E_s[i][j] (row pitch rup(w_s, 16); only j > i is written).
+// as a dense u8 matrix E_s[r][c] over sorted positions (length order; row pitch rup(w_s, 16);
+// only c > r is written).
 struct ExcessArgs {
     const uint32_t *csr;
     const int64_t *off;
@@ -119,7 +126,9 @@ struct ExcessArgs {
     const unsigned long long *xtot;  // device [pl]
     const uint32_t *lists;           // K6 lists L_tau (from k_xfill)
     int accb;                        // bytes of one row accumulator (max_w rounded up to 16)
-    uint2 *xrow;                     // [n] .x = 1 if the row has excess
+    const int32_t *sigma;            // [n] length order: sorted position -> local index
+    const int32_t *sigma_inv;        // [n] local index -> sorted position
+    uint2 *xrow;                     // [n] .x = 1 if the row (sorted position) has excess
     uint8_t *E;                      // dense excess rows
     const int64_t *ebase;            // device [pl+1] per shard byte offset of E_s
 };
@@ -130,7 +139,7 @@ void launch_dense_counts(const OperandArgs &a, cudaStream_t st);
 struct AllPairsArgs {
     const void *op;                  // operand
     int64_t stride;                  // bytes per operand row
-    const RowInfo *rowinfo;          // [n] local rows
+    const RowInfo *rowinfo;          // [n] local rows (TC path: in length order, .shard = local index)
     const int64_t *shard_base;       // device [pl+1]
     const int64_t *shard_rowpad;     // device [pl+1]
     const int64_t *shard_kblocks;    // device [pl]: 128-col K blocks of each shard (TC path)
@@ -310,6 +319,8 @@ struct sad_ctx {
     sad::RowInfo *d_rowinfo = nullptr;
     uint32_t *d_csr = nullptr;
     int32_t *d_dcnt = nullptr, *d_nhi = nullptr;
+    int32_t *d_sigma = nullptr, *d_sigma_inv = nullptr;   // length order of every shard (TC path)
+    sad::RowInfo *d_rinfo_s = nullptr;                    // RowInfo in length order, .shard = local index
     uint32_t *d_M = nullptr, *d_col0 = nullptr;
     unsigned long long *d_err = nullptr, *d_kinfo = nullptr;
     uint32_t *d_cap = nullptr, *d_xsel = nullptr;   // layer cap T_s and its index j_s per shard
