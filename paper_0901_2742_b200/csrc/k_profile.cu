@@ -14,8 +14,9 @@ namespace sad {
 __constant__ char c_alpha[2][24] = {"ACDEFGHIKLMNPQRSTVWY", "ACGT"};
 
 // K1+K2. One warp per sequence (persistent warps over contiguous runs of sequences, no block
-// barriers), each with its own packed u16 shared-memory histogram (two bins per u32 word; a bin
-// never exceeds L-k+1 <= 65535, so the halves never carry) and a staging buffer of residue codes.
+// barriers), each with its own shared-memory histogram of u8 bins (four per u32 word; a sequence
+// with a k-mer seen 256+ times is recounted with u16 bins over each half of the k-mers, which
+// cannot carry since L-k+1 <= 65535) and a staging buffer of residue codes.
 // Pass 1 validates every residue (K1) and counts every window tau = sum_m c_m A^(k-1-m) (K2).
 // Pass 2 revisits the windows: the first lane to clear a bin with atomicAnd receives its count
 // and emits the distinct entry (tau << 16 | count), so the histogram is left zeroed for the next
@@ -24,7 +25,7 @@ __constant__ char c_alpha[2][24] = {"ACDEFGHIKLMNPQRSTVWY", "ACGT"};
 // entries with count >= 2 come first (warp-aggregated appends from the front, count-1 entries
 // from the back, then the gap is closed), so the K6 consumers read only those. Sequences longer
 // than the staging buffer are processed in segments of windows.
-constexpr int kProfWarps = 12;
+constexpr int kProfWarps = 10;
 constexpr int kCodeSeg = 2048;           // residue codes staged per warp
 
 template <int KT>
@@ -40,7 +41,7 @@ __device__ __forceinline__ uint32_t window_tau(const uint8_t *c, int k, uint32_t
 }
 
 template <int KT>
-__global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int warps, int hw) {
+__global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int warps, int hbytes) {
     extern __shared__ __align__(16) uint32_t psm[];
     __shared__ uint8_t lut[256];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -49,6 +50,7 @@ __global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int 
     if (threadIdx.x < a.A) lut[(uint8_t)c_alpha[a.alphabet][threadIdx.x]] = (uint8_t)threadIdx.x;
     __syncthreads();
     if (wid >= warps) return;
+    const int hw = hbytes / 4;                  // histogram words (V bytes, rounded up to 16)
     uint32_t *hist = psm + (size_t)wid * (hw + kCodeSeg / 4);
     uint8_t *cod = reinterpret_cast<uint8_t *>(hist + hw);
     for (int t = lane; t < hw; t += 32) hist[t] = 0;
@@ -57,6 +59,7 @@ __global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int 
     const int k = KT > 0 ? KT : a.k;
     const uint32_t A = (uint32_t)a.A;
     const int V = a.V;
+    const uint32_t Vh = (uint32_t)(V + 1) / 2;  // u16 fallback: bins of half the k-mers per sub-pass
     const int64_t W = (int64_t)gridDim.x * warps, gw = (int64_t)blockIdx.x * warps + wid;
     const int64_t i0 = gw * a.n / W, i1 = (gw + 1) * a.n / W;
     int s = 0;
@@ -100,11 +103,15 @@ __global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int 
             continue;
         }
         const int nseg = (int)((Tw + SW - 1) / SW);
-        // stage the codes of segment g: residues [g SW, min(L, (g + 1) SW + k - 1)); K1 on the first pass
-        // (16-byte aligned vector loads: the residue buffer is padded by 16 bytes past its end)
-        auto stage = [&](int g, bool check) {
+        int staged = -1, checked = -1;          // segment now in `cod`, last segment validated (K1)
+        // stage the codes of segment g: residues [g SW, min(L, (g + 1) SW + k - 1)), validated (K1) the
+        // first time (16-byte aligned vector loads: the residue buffer is padded by 16 bytes past its end)
+        auto stage = [&](int g) {
+            if (g == staged) return;
+            const bool check = g > checked;
             const int64_t r0 = (int64_t)g * SW, r1 = min(L, r0 + SW + k - 1);
             const int64_t b0 = (off0 + r0) & ~int64_t(15), b1 = off0 + r1;
+            __syncwarp();
             for (int64_t b = b0 + 16 * lane; b < b1; b += 512) {
                 const uint4 q = *reinterpret_cast<const uint4 *>(a.ascii + b);
                 const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
@@ -122,53 +129,83 @@ __global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int 
                 }
             }
             __syncwarp();
+            staged = g;
+            checked = max(checked, g);
         };
-        // pass 1: count every window (overlaps included)
-        for (int g = 0; g < nseg; ++g) {
-            stage(g, true);
-            const int w1 = (int)min((int64_t)SW, Tw - (int64_t)g * SW);
-            for (int t = lane; t < w1; t += 32) {
-                const uint32_t tau = window_tau<KT>(cod + t, k, A);
-                atomicAdd(&hist[tau >> 1], (tau & 1) ? 0x10000u : 1u);
+        // pass 1: count every window (overlaps included). Normally u8 bins (V bytes); a bin that
+        // would pass 255 (the add carries into its neighbour) sends the sequence to the fallback:
+        // clear the bins and count with u16 bins over each half of the k-mers in turn.
+        auto count = [&](int bits, uint32_t lo, uint32_t hi) -> bool {
+            bool ovf = false;
+            for (int g = 0; g < nseg; ++g) {
+                stage(g);
+                const int w1 = (int)min((int64_t)SW, Tw - (int64_t)g * SW);
+                for (int t = lane; t < w1; t += 32) {
+                    const uint32_t tau = window_tau<KT>(cod + t, k, A);
+                    if (tau < lo || tau >= hi) continue;
+                    const uint32_t idx = tau - lo;
+                    const uint32_t sh = bits == 8 ? 8u * (idx & 3u) : 16u * (idx & 1u);
+                    const uint32_t old = atomicAdd(&hist[bits == 8 ? idx >> 2 : idx >> 1], 1u << sh);
+                    if (bits == 8 && ((old >> sh) & 0xFFu) == 0xFFu) ovf = true;
+                }
             }
             __syncwarp();
-        }
+            return __any_sync(0xffffffffu, ovf);
+        };
         // pass 2: claim every bin once, emit (tau, count), update the shard's column maxima
         uint32_t *out = a.csr + (off0 - i * (int64_t)(k - 1));
         uint32_t *Ms = a.M + (size_t)s * V;
         uint32_t n_hi = 0, n_lo = 0, ex[kNumCaps] = {};
-        for (int g = nseg - 1; g >= 0; --g) {                  // the last staged segment first
-            if (g != nseg - 1) stage(g, false);
-            const int w1 = (int)min((int64_t)SW, Tw - (int64_t)g * SW);
-            for (int t0 = 0; t0 < w1; t0 += 32) {
-                const int t = t0 + lane;
-                uint32_t c = 0, tau = 0;
-                if (t < w1) {
-                    tau = window_tau<KT>(cod + t, k, A);
-                    const uint32_t mask = (tau & 1) ? 0xFFFF0000u : 0x0000FFFFu;
-                    const uint32_t old = atomicAnd(&hist[tau >> 1], ~mask);
-                    c = (tau & 1) ? (old >> 16) : (old & 0xFFFFu);
-                }
-                const uint32_t mh = __ballot_sync(0xffffffffu, c >= 2), ml = __ballot_sync(0xffffffffu, c == 1);
-                const uint32_t lt = (1u << lane) - 1u;
-                if (c >= 2) out[n_hi + __popc(mh & lt)] = (tau << 16) | c;
-                else if (c == 1) out[Tw - 1 - (n_lo + __popc(ml & lt))] = (tau << 16) | 1u;
-                n_hi += __popc(mh);
-                n_lo += __popc(ml);
-                if (c) {
-                    atomicMax(&Ms[tau], c);
-                    if (c >= 2) {                              // excess beyond the layer caps 1, 2, 4, 8
+        auto claim = [&](int bits, uint32_t lo, uint32_t hi) {
+            for (int gg = 0; gg < nseg; ++gg) {
+                const int g = nseg - 1 - gg;                   // the last staged segment first
+                stage(g);
+                const int w1 = (int)min((int64_t)SW, Tw - (int64_t)g * SW);
+                for (int t0 = 0; t0 < w1; t0 += 32) {
+                    const int t = t0 + lane;
+                    uint32_t c = 0, tau = 0;
+                    if (t < w1) {
+                        tau = window_tau<KT>(cod + t, k, A);
+                        if (tau >= lo && tau < hi) {
+                            const uint32_t idx = tau - lo;
+                            const uint32_t sh = bits == 8 ? 8u * (idx & 3u) : 16u * (idx & 1u);
+                            const uint32_t mask = (bits == 8 ? 0xFFu : 0xFFFFu) << sh;
+                            const uint32_t old = atomicAnd(&hist[bits == 8 ? idx >> 2 : idx >> 1], ~mask);
+                            c = (old & mask) >> sh;
+                        }
+                    }
+                    const uint32_t mh = __ballot_sync(0xffffffffu, c >= 2), ml = __ballot_sync(0xffffffffu, c == 1);
+                    const uint32_t lt = (1u << lane) - 1u;
+                    if (c >= 2) out[n_hi + __popc(mh & lt)] = (tau << 16) | c;
+                    else if (c == 1) out[Tw - 1 - (n_lo + __popc(ml & lt))] = (tau << 16) | 1u;
+                    n_hi += __popc(mh);
+                    n_lo += __popc(ml);
+                    if (c) {
+                        atomicMax(&Ms[tau], c);
+                        if (c >= 2) {                          // excess beyond the layer caps 1, 2, 4, 8
 #pragma unroll
-                        for (int j = 0; j < kNumCaps; ++j)
-                            if (c > (1u << j)) {
-                                ex[j] += c - (1u << j);
-                                atomicAdd(&a.Xc[((size_t)s * kNumCaps + j) * V + tau], 1u);
-                            }
+                            for (int j = 0; j < kNumCaps; ++j)
+                                if (c > (1u << j)) {
+                                    ex[j] += c - (1u << j);
+                                    atomicAdd(&a.Xc[((size_t)s * kNumCaps + j) * V + tau], 1u);
+                                }
+                        }
                     }
                 }
             }
+            __syncwarp();
+        };
+        if (!count(8, 0u, (uint32_t)V)) {
+            claim(8, 0u, (uint32_t)V);
+        } else {
+            for (int t = lane; t < hw; t += 32) hist[t] = 0;
+            __syncwarp();
+            for (uint32_t h = 0; h < 2; ++h) {
+                const uint32_t lo = h * Vh, hi = min((uint32_t)V, lo + Vh);
+                count(16, lo, hi);
+                claim(16, lo, hi);
+            }
         }
-        __syncwarp();
         // close the gap: [0, n_hi) count >= 2 (the K6 candidates), then [n_hi, d) count 1. Only the
         // count-1 entries at [max(d, Tw - n_lo), Tw) move, into the gap [n_hi, Tw - n_lo) (disjoint).
         {
@@ -195,9 +232,9 @@ __global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int 
 }
 
 void launch_profile(const ProfileArgs &a, cudaStream_t st) {
-    const int hw = (a.V + 1) / 2;
-    const size_t per_warp = (size_t)hw * 4 + kCodeSeg;
-    const int warps = (int)std::max<size_t>(1, std::min<size_t>(kProfWarps, (size_t)(110 * 1024) / per_warp));
+    const int hbytes = (a.V + 15) / 16 * 16;     // u8 bins (or u16 bins over half the k-mers)
+    const size_t per_warp = (size_t)hbytes + kCodeSeg;
+    const int warps = (int)std::max<size_t>(1, std::min<size_t>(kProfWarps, (size_t)(100 * 1024) / per_warp));
     const size_t smem = per_warp * warps;
     auto kern = a.k == 3 ? k_profile<3> : a.k == 6 ? k_profile<6> : k_profile<0>;
     static bool configured = false;
@@ -215,7 +252,7 @@ void launch_profile(const ProfileArgs &a, cudaStream_t st) {
     int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     grid = std::min<int64_t>(grid, (a.n + warps - 1) / warps);
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kProfWarps * 32, smem, st>>>(a, warps, hw);
+    kern<<<(unsigned)grid, kProfWarps * 32, smem, st>>>(a, warps, hbytes);
 }
 
 // Length order of every shard (the all-pairs kernel works on rows sorted by L - k + 1, so that
