@@ -347,13 +347,13 @@ __global__ void __launch_bounds__(kScanThreads) k_kstats(const uint32_t *M, cons
                                                          unsigned long long *kinfo, int V) {
     constexpr int NV = 3 * kNumCaps + 1;
     __shared__ unsigned long long red[NV];
-    const int s = blockIdx.x;
+    const int s = blockIdx.y;                 // blocks of k-mers x shards (kinfo zeroed by the caller)
     if (threadIdx.x < NV) red[threadIdx.x] = 0;
     __syncthreads();
     const uint32_t *m = M + (size_t)s * V;
     const uint32_t *xc = Xc + (size_t)s * kNumCaps * V;
     unsigned long long acc[NV] = {};
-    for (int t = threadIdx.x; t < V; t += kScanThreads) {
+    for (int t = blockIdx.x * kScanThreads + threadIdx.x; t < V; t += gridDim.x * kScanThreads) {
         const uint32_t x = m[t];
         acc[kNumCaps] += x;
 #pragma unroll
@@ -373,17 +373,18 @@ __global__ void __launch_bounds__(kScanThreads) k_kstats(const uint32_t *M, cons
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long *ki = kinfo + (size_t)s * kKinfo;
-        ki[2] = red[kNumCaps];
+        atomicAdd(&ki[2], red[kNumCaps]);
         for (int j = 0; j < kNumCaps; ++j) {
-            ki[8 + j] = red[j];
-            ki[12 + j] = red[kNumCaps + 1 + j];
-            ki[16 + j] = red[2 * kNumCaps + 1 + j];
+            atomicAdd(&ki[8 + j], red[j]);
+            atomicAdd(&ki[12 + j], red[kNumCaps + 1 + j]);
+            atomicAdd(&ki[16 + j], red[2 * kNumCaps + 1 + j]);
         }
     }
 }
 
 void launch_kstats(const uint32_t *M, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V, cudaStream_t st) {
-    k_kstats<<<pl, kScanThreads, 0, st>>>(M, Xc, kinfo, V);
+    const int bx = std::max(1, std::min(16, V / 512));
+    k_kstats<<<dim3(bx, pl), kScanThreads, 0, st>>>(M, Xc, kinfo, V);
 }
 
 __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl, int64_t r) {

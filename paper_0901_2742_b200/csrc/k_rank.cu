@@ -211,7 +211,7 @@ void launch_samples(const unsigned long long *key_sorted, const int64_t *shard_b
 // "must be <= y1"; reading A13), found per shard by binary search on the sorted keys; and
 // the per-shard exclusive prefix of L over the sorted order (residue bytes per slice).
 // ---------------------------------------------------------------------------------------
-constexpr int kPlanThreads = 256;
+constexpr int kPlanThreads = 256;   // one block per local shard
 __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanArgs a) {
     extern __shared__ unsigned long long Y[];        // [p(p-1)] sorted samples, then pivots
     typedef cub::BlockScan<long long, kPlanThreads> Scan;
@@ -247,20 +247,10 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanArgs a) {
         }
         bnd[b] = lo;
     }
-    // exclusive prefix of L in sorted order: lpre[base + s + t], t = 0..w
-    int64_t *lp = a.lpre + base + s;
-    const int64_t per = (w + kPlanThreads - 1) / kPlanThreads;
-    const int64_t t0 = min(w, (int64_t)threadIdx.x * per), t1 = min(w, t0 + per);
-    long long sum = 0;
-    for (int64_t t = t0; t < t1; ++t) sum += a.rowinfo[a.perm_sorted[base + t]].tw + a.k - 1;
-    long long pre, total;
-    Scan(tmp).ExclusiveSum(sum, pre, total);
-    for (int64_t t = t0; t < t1; ++t) {
-        lp[t] = pre;
-        pre += a.rowinfo[a.perm_sorted[base + t]].tw + a.k - 1;
-    }
-    if (threadIdx.x == 0) lp[w] = total;
     __syncthreads();
+    // residues of every (shard, bucket) slice from the exclusive prefix G of L in sorted order
+    // (lpre[t], t = 0..n, computed by one device scan in sad_rank_global)
+    const int64_t *lp = a.lpre + base;
     for (int b = threadIdx.x; b < p; b += kPlanThreads) {
         const int64_t lo = b ? bnd[b - 1] : 0, hi = bnd[b];
         a.counts[((size_t)s * p + b) * 2 + 0] = hi - lo;
@@ -294,7 +284,7 @@ __global__ void __launch_bounds__(256) k_pack(PackArgs a) {
         int b = 0;
         while (tt >= bnd[b]) ++b;
         const int64_t start = b ? bnd[b - 1] : 0;
-        const int64_t *lp = a.lpre + a.shard_base[s] + s;
+        const int64_t *lp = a.lpre + a.shard_base[s];
         const int64_t so = a.seg[((size_t)s * a.p + b) * 2 + 0] + (tt - start);
         const int64_t ro = a.seg[((size_t)s * a.p + b) * 2 + 1] + (lp[tt] - lp[start]);
         const int32_t row = a.perm_sorted[t];
@@ -379,7 +369,8 @@ void launch_gather_out(const int32_t *perm, int64_t n, const int64_t *src_off, c
 
 // unpack the sorted composite keys (shard | q | row) into the real keys and rows
 __global__ void k_unpack_sorted(const unsigned long long *ck, int64_t n, int ib, int64_t first_idx,
-                                unsigned long long *key_sorted, int32_t *perm_sorted) {
+                                unsigned long long *key_sorted, int32_t *perm_sorted, const RowInfo *rowinfo, int k,
+                                int64_t *len_sorted) {
     const unsigned long long rmask = (1ull << ib) - 1ull, qmask = (1ull << 33) - 1ull;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long c = ck[t];
@@ -387,12 +378,27 @@ __global__ void k_unpack_sorted(const unsigned long long *ck, int64_t n, int ib,
         const unsigned long long q = (c >> ib) & qmask;
         key_sorted[t] = (q << 31) + (unsigned long long)(first_idx + row);
         perm_sorted[t] = (int32_t)row;
+        len_sorted[t] = (int64_t)rowinfo[row].tw + k - 1;
     }
 }
 
 void launch_unpack_sorted(const unsigned long long *ckey_sorted, int64_t n, int ib, int64_t first_idx,
-                          unsigned long long *key_sorted, int32_t *perm_sorted, cudaStream_t st) {
-    if (n > 0) k_unpack_sorted<<<grid1d(n), 256, 0, st>>>(ckey_sorted, n, ib, first_idx, key_sorted, perm_sorted);
+                          unsigned long long *key_sorted, int32_t *perm_sorted, const RowInfo *rowinfo, int k,
+                          int64_t *len_sorted, cudaStream_t st) {
+    if (n > 0)
+        k_unpack_sorted<<<grid1d(n), 256, 0, st>>>(ckey_sorted, n, ib, first_idx, key_sorted, perm_sorted, rowinfo, k,
+                                                   len_sorted);
+}
+
+__global__ void k_lens_sorted(const int32_t *perm_sorted, const RowInfo *rowinfo, int k, int64_t n,
+                              int64_t *len_sorted) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        len_sorted[t] = (int64_t)rowinfo[perm_sorted[t]].tw + k - 1;
+}
+
+void launch_lens_sorted(const int32_t *perm_sorted, const RowInfo *rowinfo, int k, int64_t n, int64_t *len_sorted,
+                        cudaStream_t st) {
+    if (n > 0) k_lens_sorted<<<grid1d(n), 256, 0, st>>>(perm_sorted, rowinfo, k, n, len_sorted);
 }
 
 // K14: merge by ranking. Keys are unique, every run is sorted, so the output slot of an element is

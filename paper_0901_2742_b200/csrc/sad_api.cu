@@ -94,10 +94,11 @@ size_t cub_bytes_needed(int64_t n, int pl) {
                                              (const int64_t *)nullptr, (const int64_t *)nullptr, 0, 64);
     cub::DeviceRadixSort::SortKeys(nullptr, b, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
                                    (int)std::max<int64_t>(n, 1), 0, 64);
-    size_t c = 0;
+    size_t c = 0, d = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint32_t *)nullptr, (uint32_t *)nullptr, (const int32_t *)nullptr,
                                     (int32_t *)nullptr, (int)std::max<int64_t>(n, 1), 0, 32);
-    return std::max(std::max(a, b), c) + 1024;
+    cub::DeviceScan::InclusiveSum(nullptr, d, (const int64_t *)nullptr, (int64_t *)nullptr, (int)std::max<int64_t>(n, 1));
+    return std::max(std::max(a, b), std::max(c, d)) + 1024;
 }
 
 // carve the workspace; with base == nullptr only the size is computed
@@ -144,7 +145,8 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_perm_sorted = b.take<int32_t>((size_t)n);
     c->d_pivots = b.take<unsigned long long>((size_t)p);
     c->d_bnd = b.take<int64_t>((size_t)pl * p);
-    c->d_lpre = b.take<int64_t>((size_t)n + pl);
+    c->d_lpre = b.take<int64_t>((size_t)n + pl + 1);
+    c->d_len_sorted = b.take<int64_t>((size_t)n);
     c->d_seg = b.take<int64_t>((size_t)pl * p * 2);
     c->d_counts = b.take<int64_t>((size_t)pl * p * 2);
     c->tc_tiles_cap = tc_tiles_bound(n, pl);
@@ -773,12 +775,21 @@ int sad_rank_global(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out
                                           ctx->st));
         LAUNCHED();
         launch_unpack_sorted(ctx->d_ckey_sorted, ctx->n, ib, ctx->first_idx, ctx->d_key_sorted, ctx->d_perm_sorted,
-                             ctx->st);
+                             ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, ctx->st);
         LAUNCHED();
     } else {
         CK(cub::DeviceSegmentedRadixSort::SortPairs(ctx->d_cub, tb, ctx->d_key, ctx->d_key_sorted, ctx->d_perm_in,
                                                     ctx->d_perm_sorted, (int)ctx->n, ctx->pl, ctx->d_shard_base,
                                                     ctx->d_shard_base + 1, 0, 64, ctx->st));
+        LAUNCHED();
+        launch_lens_sorted(ctx->d_perm_sorted, ctx->d_rowinfo, ctx->cfg.k, ctx->n, ctx->d_len_sorted, ctx->st);
+        LAUNCHED();
+    }
+    // exclusive prefix of L in sorted order (the residue offsets of every bucket slice, K12/K13)
+    CK(cudaMemsetAsync(ctx->d_lpre, 0, sizeof(int64_t), ctx->st));
+    {
+        size_t tb2 = ctx->cub_bytes;
+        CK(cub::DeviceScan::InclusiveSum(ctx->d_cub, tb2, ctx->d_len_sorted, ctx->d_lpre + 1, (int)ctx->n, ctx->st));
         LAUNCHED();
     }
     if (p > 1) {

@@ -211,7 +211,10 @@ void launch_rank_vs_ga(const RankArgs &a, cudaStream_t st);
 void launch_samples(const unsigned long long *key_sorted, const int64_t *shard_base, int pl, int p,
                     unsigned long long *samples_out, cudaStream_t st);
 void launch_unpack_sorted(const unsigned long long *ckey_sorted, int64_t n, int ib, int64_t first_idx,
-                          unsigned long long *key_sorted, int32_t *perm_sorted, cudaStream_t st);
+                          unsigned long long *key_sorted, int32_t *perm_sorted, const RowInfo *rowinfo, int k,
+                          int64_t *len_sorted, cudaStream_t st);
+void launch_lens_sorted(const int32_t *perm_sorted, const RowInfo *rowinfo, int k, int64_t n, int64_t *len_sorted,
+                        cudaStream_t st);
 
 // K14: rank-merge of nr sorted runs of unique keys (keys at stride `kstride` u64 words):
 // out position of element t = sum over runs r of #{keys in r < key_t}.
@@ -247,7 +250,7 @@ struct PlanArgs {
     int k;
     unsigned long long *pivots;              // [p-1] out
     int64_t *bnd;                            // [pl][p] out: sorted-position end of each bucket slice
-    int64_t *lpre;                           // [n + pl] out: per shard exclusive prefix of L in sorted order (w+1 each)
+    const int64_t *lpre;                     // [n + 1] exclusive prefix of L in sorted order (all shards)
     int64_t *counts;                         // [pl][p][2] out
 };
 void launch_plan(const PlanArgs &a, cudaStream_t st);
@@ -257,7 +260,7 @@ struct PackArgs {
     const int32_t *perm_sorted;
     const int64_t *shard_base;
     const int64_t *bnd;                      // [pl][p]
-    const int64_t *lpre;                     // [n + pl]
+    const int64_t *lpre;                     // [n + 1]
     const int64_t *seg;                      // [pl][p][2]: send seq offset, send residue offset of each slice
     const RowInfo *rowinfo;
     const uint8_t *ascii;
@@ -346,6 +349,7 @@ struct sad_ctx {
     int32_t *d_perm_in = nullptr, *d_perm_sorted = nullptr;
     unsigned long long *d_pivots = nullptr;
     int64_t *d_bnd = nullptr, *d_lpre = nullptr, *d_seg = nullptr, *d_counts = nullptr;
+    int64_t *d_len_sorted = nullptr;  // [n] L of each sequence in sorted order (scanned into d_lpre)
     bool counts_pending = false;
     void *d_tmap = nullptr;
     void *d_cub = nullptr;
