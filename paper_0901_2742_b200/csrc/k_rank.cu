@@ -166,7 +166,10 @@ __global__ void __launch_bounds__(kRankThreads) k_rank_vs_ga(RankArgs a) {
             a.den_ga[i] = den;
             a.key[i] = (q << 31) + (uint64_t)(a.first_idx + i);
             a.perm_in[i] = (int32_t)i;
-            if (a.ckey) a.ckey[i] = ((uint64_t)ri.shard << (33 + a.ib)) | (q << a.ib) | (uint64_t)i;
+            // sort key (shard, q) with q = 2^32 folded onto 2^32 - 1: for S < den <= 65535,
+            // q <= 2^32 - 65537, so the fold keeps the order; equal q are equal rationals (SURVEY
+            // A.3) and the stable sort keeps them in index order
+            a.ckey[i] = ((uint64_t)ri.shard << 32) | (q > 0xFFFFFFFFull ? 0xFFFFFFFFull : q);
         }
     }
 }
@@ -368,37 +371,23 @@ void launch_gather_out(const int32_t *perm, int64_t n, const int64_t *src_off, c
 
 
 // unpack the sorted composite keys (shard | q | row) into the real keys and rows
-__global__ void k_unpack_sorted(const unsigned long long *ck, int64_t n, int ib, int64_t first_idx,
-                                unsigned long long *key_sorted, int32_t *perm_sorted, const RowInfo *rowinfo, int k,
-                                int64_t *len_sorted) {
-    const unsigned long long rmask = (1ull << ib) - 1ull, qmask = (1ull << 33) - 1ull;
+__global__ void k_unpack_sorted(const unsigned long long *ck, const int32_t *perm_sorted, int64_t n, int64_t first_idx,
+                                unsigned long long *key_sorted, const RowInfo *rowinfo, int k, int64_t *len_sorted) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long c = ck[t];
-        const int64_t row = (int64_t)(c & rmask);
-        const unsigned long long q = (c >> ib) & qmask;
+        const unsigned long long q32 = ck[t] & 0xFFFFFFFFull;
+        const unsigned long long q = q32 == 0xFFFFFFFFull ? (1ull << 32) : q32;
+        const int32_t row = perm_sorted[t];
         key_sorted[t] = (q << 31) + (unsigned long long)(first_idx + row);
-        perm_sorted[t] = (int32_t)row;
         len_sorted[t] = (int64_t)rowinfo[row].tw + k - 1;
     }
 }
 
-void launch_unpack_sorted(const unsigned long long *ckey_sorted, int64_t n, int ib, int64_t first_idx,
-                          unsigned long long *key_sorted, int32_t *perm_sorted, const RowInfo *rowinfo, int k,
+void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, int64_t n,
+                          int64_t first_idx, unsigned long long *key_sorted, const RowInfo *rowinfo, int k,
                           int64_t *len_sorted, cudaStream_t st) {
     if (n > 0)
-        k_unpack_sorted<<<grid1d(n), 256, 0, st>>>(ckey_sorted, n, ib, first_idx, key_sorted, perm_sorted, rowinfo, k,
+        k_unpack_sorted<<<grid1d(n), 256, 0, st>>>(ckey_sorted, perm_sorted, n, first_idx, key_sorted, rowinfo, k,
                                                    len_sorted);
-}
-
-__global__ void k_lens_sorted(const int32_t *perm_sorted, const RowInfo *rowinfo, int k, int64_t n,
-                              int64_t *len_sorted) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
-        len_sorted[t] = (int64_t)rowinfo[perm_sorted[t]].tw + k - 1;
-}
-
-void launch_lens_sorted(const int32_t *perm_sorted, const RowInfo *rowinfo, int k, int64_t n, int64_t *len_sorted,
-                        cudaStream_t st) {
-    if (n > 0) k_lens_sorted<<<grid1d(n), 256, 0, st>>>(perm_sorted, rowinfo, k, n, len_sorted);
 }
 
 // K14: merge by ranking. Keys are unique, every run is sorted, so the output slot of an element is

@@ -94,7 +94,10 @@ size_t cub_bytes_needed(int64_t n, int pl) {
                                              (const int64_t *)nullptr, (const int64_t *)nullptr, 0, 64);
     cub::DeviceRadixSort::SortKeys(nullptr, b, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
                                    (int)std::max<int64_t>(n, 1), 0, 64);
-    size_t c = 0, d = 0;
+    size_t c = 0, d = 0, e = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, e, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, (int)std::max<int64_t>(n, 1), 0, 64);
+    a = std::max(a, e);
     cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint32_t *)nullptr, (uint32_t *)nullptr, (const int32_t *)nullptr,
                                     (int32_t *)nullptr, (int)std::max<int64_t>(n, 1), 0, 32);
     cub::DeviceScan::InclusiveSum(nullptr, d, (const int64_t *)nullptr, (int64_t *)nullptr, (int)std::max<int64_t>(n, 1));
@@ -757,34 +760,21 @@ int sad_rank_global(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out
     r.den_ga = ctx->d_den_ga;
     r.key = ctx->d_key;
     r.perm_in = ctx->d_perm_in;
-    // a7: one radix sort of composite keys (shard | q | row) when they fit 64 bits, else a
-    // segmented sort of the real keys
-    int ib = 1, sbits = 0;
-    while ((int64_t(1) << ib) < ctx->n) ++ib;
+    // a7: one stable radix sort of (shard, q) with the row as value: 32 + shard bits
+    int sbits = 0;
     while ((1 << sbits) < ctx->pl) ++sbits;
-    const int cbits = sbits + 33 + ib;
-    r.ib = ib;
-    r.ckey = cbits <= 64 ? ctx->d_ckey : nullptr;
+    r.ckey = ctx->d_ckey;
     launch_ga_pairs(r, ctx->st);
     LAUNCHED();
     launch_rank_vs_ga(r, ctx->st);
     LAUNCHED();
     size_t tb = ctx->cub_bytes;
-    if (r.ckey) {
-        CK(cub::DeviceRadixSort::SortKeys(ctx->d_cub, tb, ctx->d_ckey, ctx->d_ckey_sorted, (int)ctx->n, 0, cbits,
-                                          ctx->st));
-        LAUNCHED();
-        launch_unpack_sorted(ctx->d_ckey_sorted, ctx->n, ib, ctx->first_idx, ctx->d_key_sorted, ctx->d_perm_sorted,
-                             ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, ctx->st);
-        LAUNCHED();
-    } else {
-        CK(cub::DeviceSegmentedRadixSort::SortPairs(ctx->d_cub, tb, ctx->d_key, ctx->d_key_sorted, ctx->d_perm_in,
-                                                    ctx->d_perm_sorted, (int)ctx->n, ctx->pl, ctx->d_shard_base,
-                                                    ctx->d_shard_base + 1, 0, 64, ctx->st));
-        LAUNCHED();
-        launch_lens_sorted(ctx->d_perm_sorted, ctx->d_rowinfo, ctx->cfg.k, ctx->n, ctx->d_len_sorted, ctx->st);
-        LAUNCHED();
-    }
+    CK(cub::DeviceRadixSort::SortPairs(ctx->d_cub, tb, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in,
+                                       ctx->d_perm_sorted, (int)ctx->n, 0, 32 + sbits, ctx->st));
+    LAUNCHED();
+    launch_unpack_sorted(ctx->d_ckey_sorted, ctx->d_perm_sorted, ctx->n, ctx->first_idx, ctx->d_key_sorted,
+                         ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, ctx->st);
+    LAUNCHED();
     // exclusive prefix of L in sorted order (the residue offsets of every bucket slice, K12/K13)
     CK(cudaMemsetAsync(ctx->d_lpre, 0, sizeof(int64_t), ctx->st));
     {

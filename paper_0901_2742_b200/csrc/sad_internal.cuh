@@ -202,19 +202,16 @@ struct RankArgs {
     uint32_t *S_ga, *den_ga;
     unsigned long long *key;
     int32_t *perm_in;
-    unsigned long long *ckey;        // composite sort key (shard << (33+ib)) | (q << ib) | row, or null
-    int ib;                          // index bits of the composite key
+    unsigned long long *ckey;        // sort key (shard << 32) | min(q, 2^32 - 1), sorted with the row as value
 };
 void launch_ga_pairs(const RankArgs &a, cudaStream_t st);
 void launch_rank_vs_ga(const RankArgs &a, cudaStream_t st);
 
 void launch_samples(const unsigned long long *key_sorted, const int64_t *shard_base, int pl, int p,
                     unsigned long long *samples_out, cudaStream_t st);
-void launch_unpack_sorted(const unsigned long long *ckey_sorted, int64_t n, int ib, int64_t first_idx,
-                          unsigned long long *key_sorted, int32_t *perm_sorted, const RowInfo *rowinfo, int k,
+void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, int64_t n,
+                          int64_t first_idx, unsigned long long *key_sorted, const RowInfo *rowinfo, int k,
                           int64_t *len_sorted, cudaStream_t st);
-void launch_lens_sorted(const int32_t *perm_sorted, const RowInfo *rowinfo, int k, int64_t n, int64_t *len_sorted,
-                        cudaStream_t st);
 
 // K14: rank-merge of nr sorted runs of unique keys (keys at stride `kstride` u64 words):
 // out position of element t = sum over runs r of #{keys in r < key_t}.
