@@ -71,6 +71,8 @@ extern "C" {
 /* memory kinds of sad_load inputs */
 #define SAD_MEM_HOST 0
 #define SAD_MEM_DEVICE 1
+#define SAD_MEM_DEVICE_REBASE 2  /* device inputs whose offsets start at offsets[0] != 0 (ascii points
+                                    at residue offsets[0]); e.g. a bucket view of sad_get_bucket_view */
 
 /* error codes */
 #define SAD_OK 0
@@ -129,8 +131,9 @@ int sad_workspace_size(const sad_ctx *ctx, int64_t n_local, int64_t residues_loc
  *   offsets  [n_local+1] int64, offsets[0] == 0, nondecreasing (host or device per mem)
  *   residues_local  offsets[n_local] if known, else -1 (device offsets are then read back,
  *            which costs a synchronization)
- *   mem      SAD_MEM_HOST (copied with cudaMemcpyAsync; synchronous w.r.t. the inputs) or
- *            SAD_MEM_DEVICE (copied device-to-device on the stream)
+ *   mem      SAD_MEM_HOST (copied with cudaMemcpyAsync; synchronous w.r.t. the inputs),
+ *            SAD_MEM_DEVICE (copied device-to-device on the stream) or SAD_MEM_DEVICE_REBASE
+ *            (device, offsets[0] may be nonzero: offsets are taken relative to it)
  *   d_ws     device workspace of at least sad_workspace_size(n_local, offsets[n_local]) bytes,
  *            256-byte aligned, owned by the caller, kept until the next sad_load or sad_destroy.
  * Inputs are copied; no input pointer is retained. Syncs for host inputs (so they may be
@@ -271,6 +274,21 @@ int sad_get_bucket(sad_ctx *ctx, int bucket, int64_t *h_idx, uint64_t *h_key, ui
 /* The w x w similarity numerators S_ij of local shard s (uint16, row-major, input order);
  * only with SAD_F_KEEP_SIM. */
 int sad_get_similarity(sad_ctx *ctx, int shard, uint16_t *h_S, int64_t cap);
+
+/* Device view of one bucket owned by this rank (after sad_finish), for feeding it to another
+ * context with sad_load(..., SAD_MEM_DEVICE_REBASE): *d_res = its first residue, *d_offsets =
+ * its n+1 residue offsets (absolute inside this context's output; rebase by offsets[0]),
+ * *n = sequences, *res_bytes = residues. The pointers stay valid until the next sad_finish
+ * or sad_destroy of this context. Syncs (reads one offset). */
+int sad_get_bucket_view(sad_ctx *ctx, int bucket, const uint8_t **d_res, const int64_t **d_offsets, int64_t *n,
+                        int64_t *res_bytes);
+
+/* Distance matrix of local shard s (SPEC S:347-352 build_distance_matrix,
+ * PAPER.md:52 "k-mer distance can be used to rapidly construct phylogenetic trees"):
+ * d_D[i][j] = 1 - S_ij / (min(L_i, L_j) - k + 1) in IEEE float32 (fdiv_rn then fsub_rn), 0 on
+ * the diagonal, w x w row-major in input order, device memory of >= cap floats. Needs
+ * SAD_F_KEEP_SIM and sad_rank_local; enqueued on the stream. */
+int sad_get_distance(sad_ctx *ctx, int shard, float *d_D, int64_t cap);
 
 /* Per-shard profile facts (after sad_build_profiles): total k-mer windows, distinct k-mers
  * and the operand column count K_s of every local shard (int64 [p/world] each; any may be NULL). */

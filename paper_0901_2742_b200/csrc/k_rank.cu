@@ -473,4 +473,30 @@ void launch_selftest_fixed(int max_den, unsigned long long *bad, cudaStream_t st
     if (max_den > 0) k_selftest_fixed<<<max_den, 256, 0, st>>>(max_den, bad);
 }
 
+// device offsets with a nonzero base (SAD_MEM_DEVICE_REBASE): off[i] = src[i] - src[0]
+__global__ void k_rebase(const int64_t *src, int64_t n1, int64_t *off) {
+    const int64_t b = src[0];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n1; t += (int64_t)gridDim.x * blockDim.x)
+        off[t] = src[t] - b;
+}
+
+void launch_rebase(const int64_t *src, int64_t n1, int64_t *off, cudaStream_t st) {
+    if (n1 > 0) k_rebase<<<grid1d(n1), 256, 0, st>>>(src, n1, off);
+}
+
+// f3: distance matrix d = 1 - S/den of one shard (SPEC S:347 build_distance_matrix), from the kept
+// numerators (input order) and the denominators min(L_i, L_j) - k + 1
+__global__ void k_distance(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, float *D) {
+    const int64_t nn = w * w;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nn; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / w, j = t - i * w;
+        const uint32_t den = min(rowinfo[i].tw, rowinfo[j].tw);
+        D[t] = i == j ? 0.0f : __fsub_rn(1.0f, __fdiv_rn((float)sim[t], (float)den));
+    }
+}
+
+void launch_distance(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, float *D, cudaStream_t st) {
+    if (w > 0) k_distance<<<grid1d(w * w), 256, 0, st>>>(sim, rowinfo, w, D);
+}
+
 }  // namespace sad

@@ -311,7 +311,8 @@ int sad_workspace_size(const sad_ctx *cctx, int64_t n_local, int64_t residues_lo
 int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t n_local, int64_t first_source_index,
              int64_t n_global, int64_t residues_local, int32_t mem, void *d_ws, size_t ws_bytes) {
     GUARD(0);
-    if (!offsets || !d_ws || n_local < 0 || n_global < 0 || (mem != SAD_MEM_HOST && mem != SAD_MEM_DEVICE))
+    if (!offsets || !d_ws || n_local < 0 || n_global < 0 ||
+        (mem != SAD_MEM_HOST && mem != SAD_MEM_DEVICE && mem != SAD_MEM_DEVICE_REBASE))
         return fail(ctx, SAD_E_ARG, "sad_load: bad arguments");
     if (n_global == 0) return fail(ctx, SAD_E_EMPTY, "EmptyInput: no sequences");
     if (n_global > 0x7FFFFFFF) return fail(ctx, SAD_E_ARG, "n_global >= 2^31 (the key reserves 31 index bits)");
@@ -333,6 +334,8 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
         if (offsets[0] != 0) return fail(ctx, SAD_E_ARG, "offsets[0] != 0");
         if (R >= 0 && R != offsets[n_local]) return fail(ctx, SAD_E_ARG, "residues_local != offsets[n_local]");
         R = offsets[n_local];
+    } else if (R < 0 && mem == SAD_MEM_DEVICE_REBASE) {
+        return fail(ctx, SAD_E_ARG, "SAD_MEM_DEVICE_REBASE needs residues_local");
     } else if (R < 0) {
         CK(cudaMemcpyAsync(ctx->h_small + 40000, offsets + n_local, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
@@ -362,7 +365,12 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
     ctx->rows_pad = ctx->shard_rowpad[ctx->pl];
     const cudaMemcpyKind kind = mem == SAD_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     if (R > 0) CK(cudaMemcpyAsync(ctx->d_ascii, ascii, (size_t)R, kind, ctx->st));
-    CK(cudaMemcpyAsync(ctx->d_off, offsets, sizeof(int64_t) * (size_t)(n_local + 1), kind, ctx->st));
+    if (mem == SAD_MEM_DEVICE_REBASE) {
+        launch_rebase(offsets, n_local + 1, ctx->d_off, ctx->st);
+        LAUNCHED();
+    } else {
+        CK(cudaMemcpyAsync(ctx->d_off, offsets, sizeof(int64_t) * (size_t)(n_local + 1), kind, ctx->st));
+    }
     // small per-shard tables (uploaded only when the layout changes)
     const bool same = ctx->tbl_ws == base && ctx->tbl_n == n_local && ctx->tbl_ng == n_global &&
                       ctx->tbl_first == first_source_index;
@@ -1145,6 +1153,43 @@ int sad_get_similarity(sad_ctx *ctx, int shard, uint16_t *h_S, int64_t cap) {
     }
     CK(cudaMemcpyAsync(h_S, ctx->d_sim + sb, 2 * w * w, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
+    return SAD_OK;
+}
+
+int sad_get_bucket_view(sad_ctx *ctx, int bucket, const uint8_t **d_res, const int64_t **d_offsets, int64_t *n,
+                        int64_t *res_bytes) {
+    GUARD(6);
+    const int b0 = ctx->shard0, b1 = ctx->shard0 + ctx->pl;
+    if (bucket < b0 || bucket >= b1) return fail(ctx, SAD_E_ARG, "bucket %d is not owned by rank %d", bucket, ctx->cfg.rank);
+    if (int rc = resolve_counts(ctx)) return rc;
+    int64_t first = 0;
+    for (int b = b0; b < bucket; ++b) first += ctx->bucket_sizes[b];
+    const int64_t nb = ctx->bucket_sizes[bucket];
+    OutLayout o = out_layout(ctx->d_out, ctx->out_n, ctx->out_r);
+    int64_t r[2] = {0, 0};
+    CK(cudaMemcpyAsync(r, o.off + first, 8, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaMemcpyAsync(r + 1, o.off + first + nb, 8, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    if (d_res) *d_res = o.res + r[0];
+    if (d_offsets) *d_offsets = o.off + first;
+    if (n) *n = nb;
+    if (res_bytes) *res_bytes = r[1] - r[0];
+    return SAD_OK;
+}
+
+int sad_get_distance(sad_ctx *ctx, int shard, float *d_D, int64_t cap) {
+    GUARD(3);
+    if (!ctx->d_sim) return fail(ctx, SAD_E_STATE, "context created without SAD_F_KEEP_SIM");
+    int64_t b0, w;
+    if (int rc = shard_check(ctx, shard, INT64_MAX, b0, w)) return rc;
+    if (!d_D || cap < w * w) return fail(ctx, SAD_E_CAPACITY, "capacity %lld < %lld", (long long)cap, (long long)(w * w));
+    int64_t sb = 0;
+    for (int s = 0; s < shard; ++s) {
+        const int64_t ws = ctx->shard_base[s + 1] - ctx->shard_base[s];
+        sb += ws * ws;
+    }
+    launch_distance(ctx->d_sim + sb, ctx->d_rowinfo + b0, w, d_D, ctx->st);
+    LAUNCHED();
     return SAD_OK;
 }
 

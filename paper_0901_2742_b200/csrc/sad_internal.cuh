@@ -279,6 +279,8 @@ void launch_gather_out(const int32_t *perm, int64_t n, const int64_t *src_off, c
                        const int64_t *dst_off, uint8_t *dst_res, cudaStream_t st);
 
 void launch_selftest_fixed(int max_den, unsigned long long *bad, cudaStream_t st);
+void launch_rebase(const int64_t *src, int64_t n1, int64_t *off, cudaStream_t st);
+void launch_distance(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, float *D, cudaStream_t st);
 
 }  // namespace sad
 

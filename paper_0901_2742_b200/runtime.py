@@ -305,6 +305,41 @@ class Context:
                    ctypes.byref(r))
         return idx[: n.value], key[: n.value], res[: r.value], off
 
+    def bucket_view(self, b: int):
+        """Device view of owned bucket b: (residue pointer, absolute offsets pointer, n, residues)."""
+        res, off = ctypes.c_void_p(), ctypes.c_void_p()
+        n, r = ctypes.c_int64(), ctypes.c_int64()
+        self._call("sad_get_bucket_view", b, ctypes.byref(res), ctypes.byref(off), ctypes.byref(n), ctypes.byref(r))
+        return res.value, off.value, n.value, r.value
+
+    def bucket_distances(self, b: int, kernel: str | None = None):
+        """the k-mer distance matrix 1 - F of owned bucket b (the input of
+        the per-bucket aligner's guide tree), computed on this device by a child
+        context (one shard = the bucket, similarities kept). Returns (D float32 [n, n] CUDA tensor
+        in the bucket's order, S uint16 [n, n] host array)."""
+        res, off, n, r = self.bucket_view(b)
+        child = Context(self.alphabet, self.k, 1, device=self.device.index, stream=self.stream,
+                        kernel=kernel or self.kernel, keep_sim=True)
+        child.load_device_view(res, off, n, r)
+        child.build_profiles()
+        child.rank_local()
+        D = torch.empty((n, n), dtype=torch.float32, device=self.device)
+        child._call("sad_get_distance", 0, _vp(D), n * n)
+        S = child.similarity(0)
+        child.close()
+        return D, S
+
+    def load_device_view(self, res_ptr: int, off_ptr: int, n: int, residues: int):
+        """Load n sequences from device memory whose offsets start at an arbitrary base (a bucket
+        view of another context); source indices 0..n-1."""
+        self.n_local, self.n_global, self.first_index, self.R = n, n, 0, residues
+        ws = ctypes.c_size_t()
+        self._call("sad_workspace_size", n, residues, ctypes.byref(ws))
+        p_ws = self._buf("ws", ws.value)
+        self._call("sad_load", ctypes.c_void_p(res_ptr), ctypes.c_void_p(off_ptr), n, 0, n, residues,
+                   L.SAD_MEM_DEVICE_REBASE, ctypes.c_void_p(p_ws), ws.value)
+        return self
+
     def similarity(self, shard: int) -> np.ndarray:
         w = self.shard_size(shard)
         out = np.zeros(w * w, np.uint16)

@@ -239,3 +239,31 @@ def test_full_size_sampled(kernel, cfg):
             assert keys[first[b + 1] - 1] <= piv[b]
         if first[b + 1] < n:
             assert keys[first[b + 1]] > piv[b]
+
+
+@pytest.mark.parametrize("kernel", ["tc", "alu"])
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_bucket_distance_matrices(kernel, cfg):
+    """SURVEY §8(f) f3 (SPEC S:347 build_distance_matrix): after the redistribution, every bucket's
+    distance matrix d = 1 - S/den on the GPU equals the oracle: S exact (integers), d bit-exact to
+    the same IEEE float32 arithmetic (fdiv then fsub) and within 2^-23 of the fp64 value."""
+    spec = gen.SPECS[cfg]
+    a, o = gen.generate(cfg)
+    ctx, sizes = _run_gpu(a, o, spec.alphabet, spec.k, spec.p, kernel)
+    for b in range(spec.p):
+        idx = ctx.bucket(b)[0]
+        if len(idx) == 0:
+            continue
+        D, S = ctx.bucket_distances(b)
+        ii, jj = np.meshgrid(idx, idx, indexing="ij")
+        Sref, dref = oracle.pairs_S(a, o, spec.k, ii.ravel(), jj.ravel())
+        assert np.array_equal(S.ravel().astype(np.int64), Sref)
+        Dg = D.cpu().numpy().ravel()
+        d32 = np.float32(1) - np.float32(Sref) / np.float32(dref)
+        d32[np.flatnonzero(ii.ravel() == jj.ravel())] = 0
+        assert np.array_equal(Dg, d32)
+        d64 = 1.0 - Sref / dref
+        d64[ii.ravel() == jj.ravel()] = 0
+        assert np.max(np.abs(Dg - d64)) <= 2.0 ** -23
+        assert np.array_equal(D.cpu().numpy(), D.cpu().numpy().T)
+
