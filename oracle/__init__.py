@@ -54,6 +54,8 @@ def lib():
         L.or_pair.argtypes = [P, i64, P, i64, i32, P, P]
         L.or_run.restype = i32
         L.or_run.argtypes = [P, P, i64, i32, i32, i32, i32] + [P] * 14
+        L.or_run2.restype = i32
+        L.or_run2.argtypes = [P, P, i64, i32, i32, i32, i32, i32] + [P] * 15
         L.or_rows_T.restype = i32
         L.or_rows_T.argtypes = [P, P, i64, i32, i32, P, i64, i32, P]
         L.or_pairs_S.restype = i32
@@ -126,6 +128,7 @@ class Result:
     border: np.ndarray
     bsize: np.ndarray
     stage_ms: np.ndarray
+    rsamples: np.ndarray | None = None
 
     def buckets(self):
         out, o = [], 0
@@ -135,8 +138,10 @@ class Result:
         return out
 
 
-def run(ascii_, offsets, alphabet: str, k: int, p: int, nthreads: int = 0) -> Result:
-    """The whole oracle pipeline on one process."""
+def run(ascii_, offsets, alphabet: str, k: int, p: int, nthreads: int = 0, mode: str = "ga") -> Result:
+    """The whole oracle pipeline on one process. mode "ga": rank against
+    the global ancestor (readings A7, A8); "samples": the paper's literal rank against the k*p
+    gathered samples (S and den then hold (Dbar, 1))."""
     a = np.ascontiguousarray(ascii_, dtype=np.uint8)
     if a.size == 0:
         a = np.zeros(1, np.uint8)
@@ -147,13 +152,14 @@ def run(ascii_, offsets, alphabet: str, k: int, p: int, nthreads: int = 0) -> Re
     srt, smp, piv, bk, bo, bs = z(n), z(p * (p - 1)), z(p - 1), z(n), z(n), z(p)
     ms = np.zeros(4, np.float64)
     ei, ep = np.full(1, -1, np.int64), np.full(1, -1, np.int64)
-    rc = lib().or_run(_p(a), _p(o), n, ALPHABETS[alphabet], k, p, nthreads,
-                      _p(T), _p(anc), _p(ga), _p(Sg), _p(dg), _p(srt), _p(smp), _p(piv), _p(bk), _p(bo), _p(bs),
-                      _p(ms), _p(ei), _p(ep))
+    rs = z(p * (p - 1))
+    rc = lib().or_run2(_p(a), _p(o), n, ALPHABETS[alphabet], k, p, {"ga": 0, "samples": 1}[mode], nthreads,
+                       _p(T), _p(anc), _p(ga), _p(Sg), _p(dg), _p(srt), _p(smp), _p(piv), _p(bk), _p(bo), _p(bs),
+                       _p(rs), _p(ms), _p(ei), _p(ep))
     if rc:
         raise OracleError(rc, int(ei[0]), int(ep[0]))
     return Result(T[:n], anc[:p], int(ga[0]), Sg[:n], dg[:n], srt[:n], smp[: p * (p - 1)], piv[: p - 1],
-                  bk[:n], bo[:n], bs[:p], ms)
+                  bk[:n], bo[:n], bs[:p], ms, rs[: p * (p - 1)] if mode == "samples" else None)
 
 
 def rows_T(ascii_, offsets, k: int, p: int, rows, nthreads: int = 0) -> np.ndarray:

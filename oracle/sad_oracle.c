@@ -36,7 +36,7 @@
 #define OR_E_EMPTY (-7)
 #define OR_E_OOM (-11)
 
-int or_abi(void) { return 3; }
+int or_abi(void) { return 4; }
 
 /* ---------------------------------------------------------------------------
  * Input alphabet ("Input <- N sequences of amino acids x1 ... xN";
@@ -214,11 +214,42 @@ static double now_ms(void) {
  * Returns 0, or a negative error code; *err_idx / *err_pos locate the first
  * offending sequence / residue when not NULL.
  */
+/* Local order of reading f1 ("Sort the sequences locally in each processor based
+ * on k-mer rank"): ascending local rank T, ties by the smaller source index. */
+typedef struct { uint64_t T; int64_t idx; } tkey;
+
+static int cmp_tkey(const void *a, const void *b) {
+    const tkey *x = (const tkey *)a, *y = (const tkey *)b;
+    if (x->T != y->T) return x->T < y->T ? -1 : 1;
+    return x->idx < y->idx ? -1 : (x->idx > y->idx ? 1 : 0);
+}
+
+int or_run2(const uint8_t *ascii, const int64_t *offsets, int64_t n, int alphabet, int k, int p, int mode,
+            int nthreads, uint64_t *T, int64_t *anc, int64_t *ga, int64_t *Sg, int64_t *dg, int64_t *sorted,
+            int64_t *samples, int64_t *pivots, int64_t *bucket, int64_t *border, int64_t *bsize,
+            int64_t *rsamples, double *stage_ms, int64_t *err_idx, int64_t *err_pos);
+
 int or_run(const uint8_t *ascii, const int64_t *offsets, int64_t n, int alphabet, int k, int p, int nthreads,
            uint64_t *T, int64_t *anc, int64_t *ga, int64_t *Sg, int64_t *dg, int64_t *sorted,
            int64_t *samples, int64_t *pivots, int64_t *bucket, int64_t *border, int64_t *bsize,
            double *stage_ms, int64_t *err_idx, int64_t *err_pos) {
-    if (alphabet < 0 || alphabet > 1 || k < 1 || p < 1) return OR_E_ARG;
+    return or_run2(ascii, offsets, n, alphabet, k, p, 0, nthreads, T, anc, ga, Sg, dg, sorted, samples, pivots,
+                   bucket, border, bsize, NULL, stage_ms, err_idx, err_pos);
+}
+
+/* mode 0: rank against the global ancestor (readings A7, A8 — the north star's path).
+ * mode 1: the paper's literal listing: the
+ *   k = p-1 rank samples of every shard are the sequences at the evenly spaced positions of its
+ *   local order, and every sequence is ranked by its mean fixed-point similarity to the
+ *   m = p(p-1) gathered samples, Dbar_i = floor(sum_s q(x_i, s) / m) (reading A5 for the sum);
+ *   the rank order is (Dbar, index); Sg/dg report (Dbar, 1), ga = -1, and rsamples[m] the
+ *   rank samples (source indices). Needs p >= 2. */
+int or_run2(const uint8_t *ascii, const int64_t *offsets, int64_t n, int alphabet, int k, int p, int mode,
+            int nthreads, uint64_t *T, int64_t *anc, int64_t *ga, int64_t *Sg, int64_t *dg, int64_t *sorted,
+            int64_t *samples, int64_t *pivots, int64_t *bucket, int64_t *border, int64_t *bsize,
+            int64_t *rsamples, double *stage_ms, int64_t *err_idx, int64_t *err_pos) {
+    if (alphabet < 0 || alphabet > 1 || k < 1 || p < 1 || mode < 0 || mode > 1) return OR_E_ARG;
+    if (mode == 1 && p < 2) return OR_E_ARG;
     if (n <= 0) return OR_E_EMPTY;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -308,12 +339,45 @@ int or_run(const uint8_t *ascii, const int64_t *offsets, int64_t n, int alphabet
      * read as: against the global ancestor (reading A8):
      * S_i = S(x_i, GA), den_i = min(L_i, L_GA) - k + 1. */
     rkey *rk = (rkey *)malloc(sizeof(rkey) * (size_t)n);
-    int64_t Lg = offsets[g + 1] - offsets[g];
+    if (mode == 0) {
+        int64_t Lg = offsets[g + 1] - offsets[g];
 #pragma omp parallel for schedule(dynamic, 64)
-    for (int64_t i = 0; i < n; ++i) {
-        rk[i].S = min_sum(&kc[i], &kc[g], k);
-        rk[i].den = den_of(offsets[i + 1] - offsets[i], Lg, k);
-        rk[i].idx = i;
+        for (int64_t i = 0; i < n; ++i) {
+            rk[i].S = min_sum(&kc[i], &kc[g], k);
+            rk[i].den = den_of(offsets[i + 1] - offsets[i], Lg, k);
+            rk[i].idx = i;
+        }
+    } else {
+        /* f1, "Sort the sequences locally in each processor based on k-mer rank",
+         * :69 "Choose a sample set of k sequences in each processor" (k = p-1 at the evenly
+         * spaced 1-based positions floor(j*w/p), readings A10, A20), :70 "Send the k samples
+         * from each processor to all the processors", :72 "Compute the k-mer rank of each
+         * sequence against the k*p samples": Dbar_i = floor(sum_s q(x_i, s) / m). */
+        int64_t m = (int64_t)p * (p - 1);
+        int64_t *rs = (int64_t *)malloc(sizeof(int64_t) * (size_t)m);
+        tkey *tk = (tkey *)malloc(sizeof(tkey) * (size_t)n);
+        for (int64_t i = 0; i < n; ++i) { tk[i].T = Tl[i]; tk[i].idx = i; }
+        for (int s = 0; s < p; ++s) {
+            int64_t w = sb[s + 1] - sb[s];
+            qsort(tk + sb[s], (size_t)w, sizeof(tkey), cmp_tkey);
+            for (int j = 1; j <= p - 1; ++j) rs[(int64_t)s * (p - 1) + (j - 1)] = tk[sb[s] + (j * w) / p - 1].idx;
+        }
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int64_t i = 0; i < n; ++i) {
+            uint64_t acc = 0;
+            int64_t Li = offsets[i + 1] - offsets[i];
+            for (int64_t t = 0; t < m; ++t) {
+                int64_t j = rs[t], Lj = offsets[j + 1] - offsets[j];
+                acc += or_q((uint64_t)min_sum(&kc[i], &kc[j], k), (uint64_t)den_of(Li, Lj, k));
+            }
+            rk[i].S = (int64_t)(acc / (uint64_t)m);
+            rk[i].den = 1;
+            rk[i].idx = i;
+        }
+        if (rsamples) memcpy(rsamples, rs, sizeof(int64_t) * (size_t)m);
+        free(rs);
+        free(tk);
+        g = -1;
     }
     double t3 = now_ms();
 

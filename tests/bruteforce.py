@@ -38,7 +38,11 @@ def shards(n: int, p: int):
     return [list(range(b[s], b[s + 1])) for s in range(p)]
 
 
-def pipeline(seqs, k: int, p: int) -> dict:
+def pipeline(seqs, k: int, p: int, mode: str = "ga") -> dict:
+    """mode "ga": rank against the global ancestor (readings A7, A8); "samples": the paper's
+    listing PAPER.md:67-72 literally: local order by T (ties by index), the
+    p-1 sequences at positions floor(j w/p) of every shard as rank samples, and the rank
+    Dbar_i = floor(sum_s floor(2^32 F(x_i, s)) / (p(p-1))) with index tie-break."""
     n = len(seqs)
     sh = shards(n, p)
     T = [0] * n
@@ -48,7 +52,18 @@ def pipeline(seqs, k: int, p: int) -> dict:
     anc = [max(s, key=lambda i: (T[i], -i)) for s in sh]
     U = {a: sum(fixed(F(seqs[a], seqs[b], k)) for b in anc) for a in anc}
     ga = max(anc, key=lambda a: (U[a], -a))
-    f = [F(seqs[i], seqs[ga], k) for i in range(n)]
+    rsamples = None
+    if mode == "samples":
+        rsamples = []
+        for s in sh:
+            loc = sorted(s, key=lambda i: (T[i], i))
+            w = len(loc)
+            rsamples += [loc[(j * w) // p - 1] for j in range(1, p)]
+        m = len(rsamples)
+        f = [Fraction(sum(fixed(F(seqs[i], seqs[t], k)) for t in rsamples) // m) for i in range(n)]
+        ga = -1
+    else:
+        f = [F(seqs[i], seqs[ga], k) for i in range(n)]
     key = lambda i: (f[i], i)
     srt = [sorted(s, key=key) for s in sh]
     samples = []
@@ -67,4 +82,4 @@ def pipeline(seqs, k: int, p: int) -> dict:
         bucket.append(b)
     buckets = [sorted([i for i in range(n) if bucket[i] == b], key=key) for b in range(p)]
     return dict(T=T, anc=anc, ga=ga, f=f, sorted=[i for s in srt for i in s], samples=samples,
-                pivots=pivots, bucket=bucket, buckets=buckets)
+                pivots=pivots, bucket=bucket, buckets=buckets, rsamples=rsamples)

@@ -174,6 +174,55 @@ def test_pipeline_vs_bruteforce(alpha, k, p):
         assert r.buckets() == b["buckets"]
 
 
+@pytest.mark.parametrize("alpha,k", [("protein", 3), ("dna", 2), ("dna", 6)])
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_pipeline_samples_mode_vs_bruteforce(alpha, k, p):
+    """SURVEY §8(f) f1 (the rank against the k*p gathered samples): the oracle's
+    mode "samples" against the brute force (Counter + Fraction), every intermediate."""
+    rng = np.random.default_rng(7000 + 100 * p + k)
+    for trial in range(3):
+        n = int(rng.integers(p * p, max(p * p + 1, 48) + 1))
+        if trial == 0:
+            a, o = gen.random_set(rng, n, alpha, k, 50)
+        else:
+            spec = gen.Spec("t", n, alpha, k, p, 2, "equal", 0.0, ("normal", 30, 10, max(k, 8), 60),
+                            (0.05, 0.3), 0.05, int(rng.integers(1 << 30)))
+            a, o = gen.generate(spec)
+        seqs = gen.to_strings(a, o)
+        r = oracle.run(a, o, alpha, k, p, mode="samples")
+        b = bf.pipeline(seqs, k, p, mode="samples")
+        assert [int(t) for t in r.T] == b["T"]
+        assert r.rsamples.tolist() == b["rsamples"]
+        assert r.ga == -1 and set(r.den.tolist()) == {1}
+        assert [int(s) for s in r.S] == [int(f) for f in b["f"]]
+        assert r.sorted.tolist() == b["sorted"]
+        assert r.samples.tolist() == b["samples"]
+        assert r.pivots.tolist() == b["pivots"]
+        assert r.buckets() == b["buckets"]
+
+
+def test_samples_mode_hand_case():
+    """f1 by hand (PAPER.md:67-72): p = 2, four DNA sequences, k = 2. Shards {0,1}, {2,3};
+    T within each shard, one rank sample per shard at position floor(1*2/2) = 1 of its local order
+    (the smaller T), Dbar = floor((q(x, s0) + q(x, s1)) / 2)."""
+    seqs = ["ACGT", "ACGA", "TTTT", "TTTA"]
+    a, o = gen.from_strings(seqs)
+    r = oracle.run(a, o, "dna", 2, 2, mode="samples")
+    # shard 0: F(0,1) = |{AC,CG}| / 3 = 2/3 -> T0 = T1 = 2^32 + floor(2^32 * 2/3)
+    # shard 1: F(2,3) = |{TT, TT}| = min counts: TT 3 vs 2 -> 2/3 -> T2 = T3; ties -> smaller index
+    assert r.rsamples.tolist() == [0, 2]
+    q23 = (2 << 32) // 3
+    assert [int(t) for t in r.T] == [(1 << 32) + q23] * 4
+    # Dbar_0 = floor((2^32 + q(S(0,2)=0)) / 2), S(ACGT, TTTT) = 0
+    assert int(r.S[0]) == (1 << 32) // 2
+    # Dbar_1: F(ACGA, ACGT) = 2/3, F(ACGA, TTTT) = 0
+    assert int(r.S[1]) == q23 // 2
+    # Dbar_2: F(TTTT, ACGT) = 0, self = 2^32
+    assert int(r.S[2]) == (1 << 32) // 2
+    # Dbar_3: F(TTTA, ACGT) = 0 (TT, TA vs AC, CG, GT), F(TTTA, TTTT) = 2/3
+    assert int(r.S[3]) == q23 // 2
+
+
 # ---------------------------------------------------------------- invariants (SPEC.md:297-300, north star)
 
 def _check_invariants(r, n, p):
