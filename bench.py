@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--p", type=int, default=None)
     ap.add_argument("--kernel", default="tc", choices=["tc", "tc1", "tc8", "tc81", "tcfull", "tc8full", "alu"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rank-mode", default="ga", choices=["ga", "samples"],
+                    help="ga: rank vs the global ancestor (north star); samples: SURVEY f1, vs the k*p samples")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -182,7 +184,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)       # 256 MB > 126 MB L2
 
     ctx = Context(spec.alphabet, spec.k, p, world=world, rank=rank, device=local_rank, stream=stream,
-                  kernel=args.kernel, group=group)
+                  kernel=args.kernel, group=group, rank_mode=args.rank_mode)
 
     def barrier():
         if world > 1:
@@ -318,7 +320,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": {"tc": "e2m1", "tc1": "e2m1", "tcfull": "e2m1", "tc8": "i8", "tc81": "i8", "tc8full": "i8",
                                                "alu": "u16"}[args.kernel], "data": "synthetic",
-            "config": {"workload": workload_name(spec, p), "p": p, "kernel": args.kernel,
+            "config": {"workload": workload_name(spec, p), "p": p, "kernel": args.kernel, "rank_mode": args.rank_mode,
                        "pairs_per_step": pairs_job,
                        "l2": "L2 flushed (256 MB write) before every timed step; operand working set > L2"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,

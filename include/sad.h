@@ -62,6 +62,13 @@ extern "C" {
 #define SAD_F_TC_INT8 8u      /* tensor-core path with uint8 0/1 operands (kind::i8, int32 accumulators) */
 #define SAD_F_TC_1SM 16u      /* tensor-core path with one CTA per 128-row tile (default: CTA pairs,
                                  tcgen05 cta_group::2, 256-row tiles) */
+#define SAD_F_RANK_SAMPLES 64u /* SURVEY §8(f) row f1, the paper's literal listing: rank every
+                                 sequence by its mean fixed-point similarity to the k*p gathered samples
+                                 (k = p-1 per shard, evenly spaced in the local order by T) instead of by
+                                 its similarity to the global ancestor; key = (floor(sum_s q / (p(p-1)))
+                                 << 31) + index. Needs p >= 2 and A^k <= 25600. sad_rank_local then
+                                 writes p/world*(p-1) sample records instead of p/world ancestor records
+                                 (sad_exchange_records) and sad_rank_global takes all p(p-1) of them. */
 #define SAD_F_TC_ALL_LAYERS 32u /* tensor-core path with every threshold layer t <= max n(tau) dense in the
                                  contraction. Default: the layers are capped per shard at the smallest
                                  T in {1,2,4,8} with max_i sum_tau (n_i(tau) - T)+ <= 255, and the
@@ -158,6 +165,11 @@ int sad_operand_size(const sad_ctx *ctx, size_t *bytes);
 /* Bytes of one ancestor record: { int64 source_index; int32 L; int32 pad; uint16 counts[A^k] }
  * padded to 16 bytes. */
 size_t sad_ancestor_record_bytes(const sad_ctx *ctx);
+
+/* Records this rank contributes to the exchange after sad_rank_local (and that sad_rank_global
+ * expects world times): p/world ancestor records, or p/world*(p-1) rank-sample records with
+ * SAD_F_RANK_SAMPLES. Each record is sad_ancestor_record_bytes long. */
+int32_t sad_exchange_records(const sad_ctx *ctx);
 
 /*
  * sad_rank_local — "Locally compute k-mer rank of all the sequences in each processor"

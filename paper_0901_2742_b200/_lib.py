@@ -13,6 +13,7 @@ LIB_PATH = os.environ.get("SAD_LIB_PATH", os.path.join(HERE, "libsad.so"))   # o
 
 SAD_PROTEIN20, SAD_DNA4 = 0, 1
 SAD_F_KEEP_SIM, SAD_F_KERNEL_ALU, SAD_F_KERNEL_TC, SAD_F_TC_INT8, SAD_F_TC_1SM, SAD_F_TC_ALL_LAYERS = 1, 2, 4, 8, 16, 32
+SAD_F_RANK_SAMPLES = 64
 SAD_MEM_HOST, SAD_MEM_DEVICE, SAD_MEM_DEVICE_REBASE = 0, 1, 2
 ERRORS = {-1: "SAD_E_ARG", -2: "SAD_E_STATE", -3: "SAD_E_SYMBOL", -4: "SAD_E_TOO_SHORT", -5: "SAD_E_TOO_LONG",
           -6: "SAD_E_INSUFFICIENT", -7: "SAD_E_EMPTY", -8: "SAD_E_CAPACITY", -9: "SAD_E_CUDA", -11: "SAD_E_OOM"}
@@ -24,7 +25,7 @@ SYMBOLS = [
     "sad_rank_global", "sad_partition_plan", "sad_exchange_sizes", "sad_pack_plan", "sad_pack", "sad_output_size",
     "sad_output_layout", "sad_finish", "sad_get_local_rank", "sad_get_ancestors", "sad_get_ranks", "sad_get_sorted",
     "sad_get_pivots", "sad_get_bucket", "sad_get_bucket_sizes", "sad_get_similarity", "sad_get_profile_info", "sad_get_stats",
-    "sad_reset_stats", "sad_selftest_fixed_point", "sad_get_bucket_view", "sad_get_distance",
+    "sad_reset_stats", "sad_selftest_fixed_point", "sad_get_bucket_view", "sad_get_distance", "sad_exchange_records",
 ]
 
 
@@ -87,6 +88,7 @@ def lib():
         "sad_selftest_fixed_point": (i32, [P, i32, P]),
         "sad_get_bucket_view": (i32, [P, i32, P, P, P, P]),
         "sad_get_distance": (i32, [P, i32, P, i64]),
+        "sad_exchange_records": (i32, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

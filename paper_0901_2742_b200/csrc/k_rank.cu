@@ -2,6 +2,8 @@
 // K12 (bucket ranges), K13 (pack), K14 helpers (receive-side merge), fixed-point self-test.
 #include <cub/block/block_scan.cuh>
 
+#include <algorithm>
+
 #include "sad_internal.cuh"
 
 namespace sad {
@@ -57,6 +59,10 @@ __global__ void __launch_bounds__(kAncThreads) k_local_anc(AncArgs a) {
     }
     __syncthreads();
     const int64_t row = bI[0];
+    if (!a.rec_out) {                                // rank-against-samples mode: no ancestor records
+        if (threadIdx.x == 0) a.anc_local[s] = row;
+        return;
+    }
     uint8_t *rec = a.rec_out + (size_t)s * a.rec_bytes;
     uint16_t *cnt = reinterpret_cast<uint16_t *>(rec + 16);
     for (size_t t = threadIdx.x; t < (a.rec_bytes - 16) / 2; t += kAncThreads) cnt[t] = 0;
@@ -372,10 +378,11 @@ void launch_gather_out(const int32_t *perm, int64_t n, const int64_t *src_off, c
 
 // unpack the sorted composite keys (shard | q | row) into the real keys and rows
 __global__ void k_unpack_sorted(const unsigned long long *ck, const int32_t *perm_sorted, int64_t n, int64_t first_idx,
-                                unsigned long long *key_sorted, const RowInfo *rowinfo, int k, int64_t *len_sorted) {
+                                unsigned long long *key_sorted, const RowInfo *rowinfo, int k, int64_t *len_sorted,
+                                unsigned long long qmask) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long q32 = ck[t] & 0xFFFFFFFFull;
-        const unsigned long long q = q32 == 0xFFFFFFFFull ? (1ull << 32) : q32;
+        const unsigned long long q32 = ck[t] & qmask;
+        const unsigned long long q = (qmask == 0xFFFFFFFFull && q32 == 0xFFFFFFFFull) ? (1ull << 32) : q32;
         const int32_t row = perm_sorted[t];
         key_sorted[t] = (q << 31) + (unsigned long long)(first_idx + row);
         len_sorted[t] = (int64_t)rowinfo[row].tw + k - 1;
@@ -384,10 +391,10 @@ __global__ void k_unpack_sorted(const unsigned long long *ck, const int32_t *per
 
 void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, int64_t n,
                           int64_t first_idx, unsigned long long *key_sorted, const RowInfo *rowinfo, int k,
-                          int64_t *len_sorted, cudaStream_t st) {
+                          int64_t *len_sorted, int qbits, cudaStream_t st) {
     if (n > 0)
         k_unpack_sorted<<<grid1d(n), 256, 0, st>>>(ckey_sorted, perm_sorted, n, first_idx, key_sorted, rowinfo, k,
-                                                   len_sorted);
+                                                   len_sorted, (1ull << qbits) - 1ull);
 }
 
 // K14: merge by ranking. Keys are unique, every run is sorted, so the output slot of an element is
@@ -497,6 +504,191 @@ __global__ void k_distance(const uint16_t *sim, const RowInfo *rowinfo, int64_t 
 
 void launch_distance(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, float *D, cudaStream_t st) {
     if (w > 0) k_distance<<<grid1d(w * w), 256, 0, st>>>(sim, rowinfo, w, D);
+}
+
+// ---------------------------------------------------------------------------------------
+// f1: the paper's literal listing, PAPER.md:68-72 — "Sort the sequences locally
+// in each processor based on k-mer rank", "Choose a sample set of k sequences in each
+// processor", "Send the k samples from each processor to all the processors", "Compute the
+// k-mer rank of each sequence against the k*p samples". Local order: ascending T, ties by
+// index (one stable sort of (shard, T) with rows as values); k = p - 1 samples at the evenly
+// spaced 1-based positions floor(j w/p) (readings A10, A20), shipped as records.
+// ---------------------------------------------------------------------------------------
+__global__ void k_tkeys(const unsigned long long *T, const RowInfo *rowinfo, int64_t n, unsigned long long *keys,
+                        int32_t *rows) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = ((unsigned long long)rowinfo[i].shard << 56) | T[i];     // T < w 2^32 <= 2^56
+        rows[i] = (int32_t)i;
+    }
+}
+
+void launch_tkeys(const unsigned long long *T, const RowInfo *rowinfo, int64_t n, unsigned long long *keys,
+                  int32_t *rows, cudaStream_t st) {
+    if (n > 0) k_tkeys<<<grid1d(n), 256, 0, st>>>(T, rowinfo, n, keys, rows);
+}
+
+// one block per rank sample: record {source index, L, Tw, dense counts} of the sequence at local
+// position floor(j w/p) - 1 of shard s (block = s (p-1) + j - 1)
+__global__ void __launch_bounds__(256) k_sample_records(const int32_t *rows_sorted, const int64_t *shard_base, int p,
+                                                        const uint32_t *csr, const int64_t *off, const int32_t *dcnt,
+                                                        const RowInfo *rowinfo, int64_t first_idx, int k,
+                                                        size_t rec_bytes, uint8_t *rec_out) {
+    const int s = blockIdx.x / (p - 1), j = blockIdx.x % (p - 1) + 1;
+    const int64_t b0 = shard_base[s], w = shard_base[s + 1] - b0;
+    const int64_t row = rows_sorted[b0 + (j * w) / p - 1];
+    uint8_t *rec = rec_out + (size_t)blockIdx.x * rec_bytes;
+    uint16_t *cnt = reinterpret_cast<uint16_t *>(rec + 16);
+    for (size_t t = threadIdx.x; t < (rec_bytes - 16) / 2; t += blockDim.x) cnt[t] = 0;
+    __syncthreads();
+    const uint32_t *ent = csr + (off[row] - row * (int64_t)(k - 1));
+    for (int e = threadIdx.x; e < dcnt[row]; e += blockDim.x) cnt[ent[e] >> 16] = (uint16_t)(ent[e] & 0xFFFFu);
+    if (threadIdx.x == 0) {
+        *reinterpret_cast<int64_t *>(rec) = first_idx + row;
+        *reinterpret_cast<int32_t *>(rec + 8) = (int32_t)(rowinfo[row].tw + k - 1);
+        *reinterpret_cast<uint32_t *>(rec + 12) = rowinfo[row].tw;
+    }
+}
+
+void launch_sample_records(const int32_t *rows_sorted, const int64_t *shard_base, int pl, int p, const uint32_t *csr,
+                           const int64_t *off, const int32_t *dcnt, const RowInfo *rowinfo, int64_t first_idx, int k,
+                           size_t rec_bytes, uint8_t *rec_out, cudaStream_t st) {
+    if (p > 1) k_sample_records<<<pl * (p - 1), 256, 0, st>>>(rows_sorted, shard_base, p, csr, off, dcnt, rowinfo,
+                                                              first_idx, k, rec_bytes, rec_out);
+}
+
+// T'_i = sum over the m gathered samples of q(x_i, s) (reading A5 fixed point), 8 samples per
+// block y: their counts, clamped to 255, transposed to [tau][8] u8 in shared memory (V*8 bytes,
+// so several blocks share an SM); one warp per sequence walks its CSR entries (4 loads in flight
+// per lane) and takes 8 min-sums per entry with byte-SIMD minima widened into u16 pairs (every
+// partial sum is at most S <= 65535, so no lane carries). The clamp is exact unless both counts
+// exceed 255: such entries take min(n, count) from the record in global memory.
+constexpr int kSmpG = 8;
+__global__ void __launch_bounds__(256) k_rank_vs_samples(RankArgs a, int m, unsigned long long *Tp) {
+    extern __shared__ __align__(16) uint8_t cs8[];       // [V][8]
+    __shared__ RowInfo sri[kSmpG];
+    __shared__ int big_sh;
+    const int g0 = blockIdx.y * kSmpG;
+    if (threadIdx.x == 0) big_sh = 0;
+    __syncthreads();
+    int big = 0;
+    for (int u = 0; u < kSmpG; ++u) {                  // coalesced record reads, transposed into [tau][8]
+        const uint16_t *rc = g0 + u < m ? rec_cnt(a.anc_all + (size_t)(g0 + u) * a.rec_bytes) : nullptr;
+        for (int tau = threadIdx.x; tau < a.V; tau += blockDim.x) {
+            const uint32_t c = rc ? rc[tau] : 0u;
+            big |= c > 255u;
+            cs8[tau * kSmpG + u] = (uint8_t)min(c, 255u);
+        }
+    }
+    if (big) atomicOr(&big_sh, 1);
+    if (threadIdx.x < kSmpG) {
+        const uint32_t tw = g0 + (int)threadIdx.x < m ? rec_tw(a.anc_all + (size_t)(g0 + threadIdx.x) * a.rec_bytes) : 1u;
+        sri[threadIdx.x] = RowInfo{tw, 0xFFFFFFFFu / tw, 0xFFFFFFFFu % tw + 1u, 0u};
+    }
+    __syncthreads();
+    const bool any_big = big_sh != 0;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < a.n; i += nwarps) {
+        const uint32_t *ent = a.csr + (a.off[i] - i * (int64_t)(a.k - 1));
+        const int d = a.dcnt[i];
+        uint32_t acc[4] = {};                           // u16 pairs: samples (0,1) (2,3) (4,5) (6,7)
+        uint32_t corr[kSmpG] = {};                      // exact terms where both counts exceed 255
+        for (int e0 = 0; e0 < d; e0 += 128) {
+            uint32_t v[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int e = e0 + b * 32 + lane;
+                v[b] = e < d ? ent[e] : 0u;
+            }
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const uint32_t n = v[b] & 0xFFFFu;    // 0 past the row's entries: contributes 0
+                const uint32_t nc = min(n, 255u), n4 = nc * 0x01010101u;
+                const uint2 c = *reinterpret_cast<const uint2 *>(cs8 + (size_t)(v[b] >> 16) * kSmpG);
+                const uint32_t m0 = __vminu4(c.x, n4), m1 = __vminu4(c.y, n4);
+                acc[0] = __vadd2(acc[0], __byte_perm(m0, 0, 0x4140));   // bytes 0,1 -> u16 pair
+                acc[1] = __vadd2(acc[1], __byte_perm(m0, 0, 0x4342));
+                acc[2] = __vadd2(acc[2], __byte_perm(m1, 0, 0x4140));
+                acc[3] = __vadd2(acc[3], __byte_perm(m1, 0, 0x4342));
+                if (any_big && n > 255u) {
+                    for (int u = 0; u < kSmpG; ++u)
+                        if (g0 + u < m) {
+                            const uint32_t t = rec_cnt(a.anc_all + (size_t)(g0 + u) * a.rec_bytes)[v[b] >> 16];
+                            corr[u] += min(n, t) - min(nc, min(t, 255u));
+                        }
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            for (int o = 16; o; o >>= 1) acc[u] = __vadd2(acc[u], __shfl_xor_sync(0xffffffffu, acc[u], o));
+        if (any_big)
+#pragma unroll
+            for (int u = 0; u < kSmpG; ++u)
+                for (int o = 16; o; o >>= 1) corr[u] += __shfl_xor_sync(0xffffffffu, corr[u], o);
+        if (lane == 0) {
+            const RowInfo ri = a.rowinfo[i];
+            unsigned long long t = 0;
+#pragma unroll
+            for (int u = 0; u < kSmpG; ++u)
+                if (g0 + u < m) t += pair_q(((acc[u >> 1] >> (16 * (u & 1))) & 0xFFFFu) + corr[u], ri, sri[u]);
+            atomicAdd(&Tp[i], t);
+        }
+    }
+}
+
+int launch_rank_vs_samples(const RankArgs &a, int m, unsigned long long *Tp, int num_sms, cudaStream_t st) {
+    const size_t smem = (size_t)a.V * kSmpG;
+    if (smem > 200 * 1024) return -1;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_rank_vs_samples, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rank_vs_samples, 256, smem);
+    const int groups = (m + kSmpG - 1) / kSmpG;
+    // blocks per group: enough that all groups together fill the GPU once
+    const int64_t gx = std::min<int64_t>(std::max<int64_t>(1, (int64_t)num_sms * std::max(per_sm, 1) / groups + 1),
+                                         (a.n + 7) / 8);
+    dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)groups);
+    k_rank_vs_samples<<<grid, 256, smem, st>>>(a, m, Tp);
+    return 0;
+}
+
+// Dbar_i = floor(T'_i / m); key_i = (Dbar_i << 31) + source index; the a7 sort key (shard, Dbar)
+// takes 33 bits of Dbar (Dbar <= 2^32). S_ga reports the low 32 bits of Dbar, den_ga 0.
+__global__ void k_f1_keys(const unsigned long long *Tp, int64_t n, int m, int64_t first_idx, const RowInfo *rowinfo,
+                          unsigned long long *key, unsigned long long *ckey, int32_t *perm_in, uint32_t *S_ga,
+                          uint32_t *den_ga) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long db = Tp[i] / (unsigned long long)m;
+        key[i] = (db << 31) + (unsigned long long)(first_idx + i);
+        ckey[i] = ((unsigned long long)rowinfo[i].shard << 33) | db;
+        perm_in[i] = (int32_t)i;
+        S_ga[i] = (uint32_t)db;
+        den_ga[i] = 0u;
+    }
+}
+
+void launch_f1_keys(const unsigned long long *Tp, int64_t n, int m, int64_t first_idx, const RowInfo *rowinfo,
+                    unsigned long long *key, unsigned long long *ckey, int32_t *perm_in, uint32_t *S_ga,
+                    uint32_t *den_ga, cudaStream_t st) {
+    if (n > 0) k_f1_keys<<<grid1d(n), 256, 0, st>>>(Tp, n, m, first_idx, rowinfo, key, ckey, perm_in, S_ga, den_ga);
+}
+
+// f1 has no global ancestor: ga_info = {-1, -1, local ancestors of this rank's shards, -1 elsewhere}
+__global__ void k_f1_gainfo(const int64_t *anc_local, int pl, int shard0, int p, int64_t first_idx, long long *ga_info) {
+    for (int t = threadIdx.x; t < p + 2; t += blockDim.x) {
+        long long v = -1;
+        if (t >= 2 && t - 2 >= shard0 && t - 2 < shard0 + pl) v = first_idx + anc_local[t - 2 - shard0];
+        ga_info[t] = v;
+    }
+}
+
+void launch_f1_gainfo(const int64_t *anc_local, int pl, int shard0, int p, int64_t first_idx, long long *ga_info,
+                      cudaStream_t st) {
+    k_f1_gainfo<<<1, 256, 0, st>>>(anc_local, pl, shard0, p, first_idx, ga_info);
 }
 
 }  // namespace sad

@@ -228,12 +228,14 @@ int sad_create(const sad_config *cfg, sad_ctx **out) {
     if (cfg->k < 1 || cfg->p < 1 || cfg->p > 64 || cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world)
         return SAD_E_ARG;
     if (cfg->p % cfg->world != 0) return SAD_E_ARG;
+    if ((cfg->flags & SAD_F_RANK_SAMPLES) && cfg->p < 2) return SAD_E_ARG;   // f1 needs k = p-1 >= 1 samples
     const int A = cfg->alphabet == SAD_PROTEIN20 ? 20 : 4;
     int64_t V = 1;
     for (int i = 0; i < cfg->k; ++i) {
         V *= A;
         if (V > 65536) return SAD_E_ARG;
     }
+    if ((cfg->flags & SAD_F_RANK_SAMPLES) && V * 8 > 200 * 1024) return SAD_E_ARG;
     sad_ctx *ctx = new (std::nothrow) sad_ctx();
     if (!ctx) return SAD_E_OOM;
     ctx->cfg = *cfg;
@@ -552,6 +554,11 @@ int sad_operand_size(const sad_ctx *cctx, size_t *bytes) {
     return SAD_OK;
 }
 
+int32_t sad_exchange_records(const sad_ctx *ctx) {
+    if (!ctx) return SAD_E_ARG;
+    return (ctx->cfg.flags & SAD_F_RANK_SAMPLES) ? ctx->pl * (ctx->cfg.p - 1) : ctx->pl;
+}
+
 size_t sad_ancestor_record_bytes(const sad_ctx *ctx) {
     return ctx ? (size_t)rup(16 + 2 * (int64_t)ctx->V, 16) : 0;
 }
@@ -739,9 +746,25 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     an.pl = pl;
     an.rec_bytes = sad_ancestor_record_bytes(ctx);
     an.anc_local = ctx->d_anc_local;
-    an.rec_out = reinterpret_cast<uint8_t *>(d_anc_out);
+    const bool f1 = ctx->cfg.flags & SAD_F_RANK_SAMPLES;
+    an.rec_out = f1 ? nullptr : reinterpret_cast<uint8_t *>(d_anc_out);
     launch_local_ancestors(an, ctx->st);
     LAUNCHED();
+    if (f1) {
+        // f1: local order by T, the k = p-1 rank samples of every shard -> records
+        launch_tkeys(ctx->d_T, ctx->d_rowinfo, ctx->n, ctx->d_ckey, ctx->d_perm_in, ctx->st);
+        LAUNCHED();
+        int sbits = 0;
+        while ((1 << sbits) < pl) ++sbits;
+        size_t tb = ctx->cub_bytes;
+        CK(cub::DeviceRadixSort::SortPairs(ctx->d_cub, tb, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in,
+                                           ctx->d_perm_sorted, (int)ctx->n, 0, 56 + sbits, ctx->st));
+        LAUNCHED();
+        launch_sample_records(ctx->d_perm_sorted, ctx->d_shard_base, pl, ctx->cfg.p, ctx->d_csr, ctx->d_off,
+                              ctx->d_dcnt, ctx->d_rowinfo, ctx->first_idx, ctx->cfg.k, an.rec_bytes,
+                              reinterpret_cast<uint8_t *>(d_anc_out), ctx->st);
+        LAUNCHED();
+    }
     ctx->stage = 3;
     return SAD_OK;
 }
@@ -768,20 +791,37 @@ int sad_rank_global(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out
     r.den_ga = ctx->d_den_ga;
     r.key = ctx->d_key;
     r.perm_in = ctx->d_perm_in;
-    // a7: one stable radix sort of (shard, q) with the row as value: 32 + shard bits
+    // a7: one stable radix sort of (shard, q) with the row as value: 32 (GA) or 33 (f1) + shard bits
     int sbits = 0;
     while ((1 << sbits) < ctx->pl) ++sbits;
     r.ckey = ctx->d_ckey;
-    launch_ga_pairs(r, ctx->st);
-    LAUNCHED();
-    launch_rank_vs_ga(r, ctx->st);
-    LAUNCHED();
+    const bool f1 = ctx->cfg.flags & SAD_F_RANK_SAMPLES;
+    const int qbits = f1 ? 33 : 32;
+    if (!f1) {
+        launch_ga_pairs(r, ctx->st);
+        LAUNCHED();
+        launch_rank_vs_ga(r, ctx->st);
+        LAUNCHED();
+    } else {
+        // f1: T'_i = sum of q(x_i, s) over the m = p(p-1) gathered samples, then
+        // Dbar_i = floor(T'_i / m) and the keys (d_key doubles as the T' accumulator)
+        const int m = p * (p - 1);
+        CK(cudaMemsetAsync(ctx->d_key, 0, sizeof(unsigned long long) * (size_t)ctx->n, ctx->st));
+        if (launch_rank_vs_samples(r, m, ctx->d_key, ctx->num_sms, ctx->st))
+            return fail(ctx, SAD_E_ARG, "rank vs samples: V too large");
+        LAUNCHED();
+        launch_f1_keys(ctx->d_key, ctx->n, m, ctx->first_idx, ctx->d_rowinfo, ctx->d_key, ctx->d_ckey, ctx->d_perm_in,
+                       ctx->d_S_ga, ctx->d_den_ga, ctx->st);
+        LAUNCHED();
+        launch_f1_gainfo(ctx->d_anc_local, ctx->pl, ctx->shard0, p, ctx->first_idx, ctx->d_ga_info, ctx->st);
+        LAUNCHED();
+    }
     size_t tb = ctx->cub_bytes;
     CK(cub::DeviceRadixSort::SortPairs(ctx->d_cub, tb, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in,
-                                       ctx->d_perm_sorted, (int)ctx->n, 0, 32 + sbits, ctx->st));
+                                       ctx->d_perm_sorted, (int)ctx->n, 0, qbits + sbits, ctx->st));
     LAUNCHED();
     launch_unpack_sorted(ctx->d_ckey_sorted, ctx->d_perm_sorted, ctx->n, ctx->first_idx, ctx->d_key_sorted,
-                         ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, ctx->st);
+                         ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, qbits, ctx->st);
     LAUNCHED();
     // exclusive prefix of L in sorted order (the residue offsets of every bucket slice, K12/K13)
     CK(cudaMemsetAsync(ctx->d_lpre, 0, sizeof(int64_t), ctx->st));

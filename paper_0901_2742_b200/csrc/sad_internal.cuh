@@ -211,7 +211,19 @@ void launch_samples(const unsigned long long *key_sorted, const int64_t *shard_b
                     unsigned long long *samples_out, cudaStream_t st);
 void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, int64_t n,
                           int64_t first_idx, unsigned long long *key_sorted, const RowInfo *rowinfo, int k,
-                          int64_t *len_sorted, cudaStream_t st);
+                          int64_t *len_sorted, int qbits, cudaStream_t st);
+// f1: rank against the k*p gathered samples
+void launch_tkeys(const unsigned long long *T, const RowInfo *rowinfo, int64_t n, unsigned long long *keys,
+                  int32_t *rows, cudaStream_t st);
+void launch_sample_records(const int32_t *rows_sorted, const int64_t *shard_base, int pl, int p, const uint32_t *csr,
+                           const int64_t *off, const int32_t *dcnt, const RowInfo *rowinfo, int64_t first_idx, int k,
+                           size_t rec_bytes, uint8_t *rec_out, cudaStream_t st);
+int launch_rank_vs_samples(const RankArgs &a, int m, unsigned long long *Tp, int num_sms, cudaStream_t st);
+void launch_f1_keys(const unsigned long long *Tp, int64_t n, int m, int64_t first_idx, const RowInfo *rowinfo,
+                    unsigned long long *key, unsigned long long *ckey, int32_t *perm_in, uint32_t *S_ga,
+                    uint32_t *den_ga, cudaStream_t st);
+void launch_f1_gainfo(const int64_t *anc_local, int pl, int shard0, int p, int64_t first_idx, long long *ga_info,
+                      cudaStream_t st);
 
 // K14: rank-merge of nr sorted runs of unique keys (keys at stride `kstride` u64 words):
 // out position of element t = sum over runs r of #{keys in r < key_t}.

@@ -92,7 +92,8 @@ class Context:
     """
 
     def __init__(self, alphabet: str, k: int, p: int, *, world: int = 1, rank: int = 0, device: int | None = None,
-                 stream: torch.cuda.Stream | None = None, kernel: str = "tc", keep_sim: bool = False, group=None):
+                 stream: torch.cuda.Stream | None = None, kernel: str = "tc", keep_sim: bool = False, group=None,
+                 rank_mode: str = "ga"):
         if not torch.cuda.is_available():
             raise RuntimeError("the k-mer-rank path needs a CUDA device (no CPU fallback)")
         if device is None:
@@ -103,7 +104,11 @@ class Context:
         self.pl = p // world
         if kernel not in KERNELS:
             raise ValueError(f"kernel must be one of {sorted(KERNELS)}, not {kernel!r}")
-        flags = (L.SAD_F_KEEP_SIM if keep_sim else 0) | KERNELS[kernel]
+        if rank_mode not in ("ga", "samples"):
+            raise ValueError(f"rank_mode must be 'ga' or 'samples', not {rank_mode!r}")
+        flags = (L.SAD_F_KEEP_SIM if keep_sim else 0) | KERNELS[kernel] | (
+            L.SAD_F_RANK_SAMPLES if rank_mode == "samples" else 0)
+        self.rank_mode = rank_mode
         self.kernel = kernel
         cfg = L.SadConfig(ALPHABETS[alphabet], k, p, world, rank, device, self.stream.cuda_stream, flags)
         h = ctypes.c_void_p()
@@ -180,7 +185,8 @@ class Context:
         ob = ctypes.c_size_t()
         self._call("sad_operand_size", ctypes.byref(ob))
         p_op = self._buf("operand", ob.value, align=1024)
-        anc = self._tensor("anc", (self.pl, self.rec_bytes), torch.uint8)
+        nrec = int(L.lib().sad_exchange_records(self._h))
+        anc = self._tensor("anc", (nrec, self.rec_bytes), torch.uint8)
         self._call("sad_rank_local", ctypes.c_void_p(p_op), ob.value, _vp(anc))
         return anc
 

@@ -12,12 +12,12 @@ from synth import gen
 pytestmark = pytest.mark.gpu
 
 
-def run_emulated(a, o, alpha, k, p, G, kernel):
+def run_emulated(a, o, alpha, k, p, G, kernel, rank_mode="ga"):
     from paper_0901_2742_b200.runtime import Context
     n = len(o) - 1
     sb = gen.shard_bounds(n, p)
     pl = p // G
-    ctxs = [Context(alpha, k, p, world=G, rank=r, kernel=kernel) for r in range(G)]
+    ctxs = [Context(alpha, k, p, world=G, rank=r, kernel=kernel, rank_mode=rank_mode) for r in range(G)]
     for r, c in enumerate(ctxs):
         lo, hi = sb[r * pl], sb[(r + 1) * pl]
         c.load(a[o[lo]: o[hi]], o[lo: hi + 1] - o[lo], n, lo)
@@ -54,3 +54,19 @@ def test_g_invariance(kernel, G):
             idx, key, res, off = c.bucket(b)
             assert idx.tolist() == r.buckets()[b]
             assert [bytes(res[off[i]: off[i + 1]]).decode() for i in range(len(idx))] == [seqs[i] for i in idx]
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_g_invariance_samples_mode(G):
+    """SURVEY §8(f) f1 across emulated ranks: the rank-sample records are all-gathered like the
+    ancestor records; buckets identical to the oracle's mode "samples"."""
+    spec = gen.SPECS[2]
+    a, o = gen.generate(spec)
+    p = spec.p
+    ctxs, _ = run_emulated(a, o, spec.alphabet, spec.k, p, G, "tc", rank_mode="samples")
+    r = oracle.run(a, o, spec.alphabet, spec.k, p, mode="samples")
+    pl = p // G
+    for rk, c in enumerate(ctxs):
+        for b in range(rk * pl, (rk + 1) * pl):
+            assert c.bucket(b)[0].tolist() == r.buckets()[b]
+

@@ -267,3 +267,53 @@ def test_bucket_distance_matrices(kernel, cfg):
         assert np.max(np.abs(Dg - d64)) <= 2.0 ** -23
         assert np.array_equal(D.cpu().numpy(), D.cpu().numpy().T)
 
+
+def _compare_f1(ctx, sizes, r, a, o, p):
+    """rank against the k*p samples: keys, local order, PSRS pivots, buckets."""
+    n = len(o) - 1
+    T = np.concatenate([ctx.local_rank(s) for s in range(p)])
+    assert np.array_equal(T, r.T)
+    loc, ga = ctx.ancestors()
+    assert ga == -1 and loc.tolist() == r.anc.tolist()
+    K = np.concatenate([ctx.ranks(s)[2] for s in range(p)])
+    assert [int(x) for x in K] == [(int(d) << 31) + i for i, d in enumerate(r.S)]
+    assert np.array_equal(np.concatenate([ctx.sorted(s) for s in range(p)]), r.sorted)
+    assert [int(x) & 0x7FFFFFFF for x in ctx.pivots()] == r.pivots.tolist()
+    assert sizes.tolist() == r.bsize.tolist()
+    for b, ref in enumerate(r.buckets()):
+        assert ctx.bucket(b)[0].tolist() == ref
+    assert int(sizes.sum()) == n
+
+
+@pytest.mark.parametrize("kernel", ["tc", "tc8", "alu"])
+@pytest.mark.parametrize("case", ["cfg1", "cfg2", "cfg3_small_p4", "dna_p3", "adv"])
+def test_samples_mode(kernel, case):
+    """the GPU path in rank-against-samples mode is bit-identical
+    to the oracle's mode "samples"."""
+    from paper_0901_2742_b200.runtime import Context
+    if case in ("cfg1", "cfg2"):
+        spec = gen.SPECS[int(case[3])]
+        a, o = gen.generate(spec)
+        alpha, k, p = spec.alphabet, spec.k, spec.p
+    elif case == "cfg3_small_p4":
+        spec = gen.SPECS[3]
+        a, o = gen.generate(spec, n=3000, seed=17)
+        alpha, k, p = spec.alphabet, spec.k, 4
+    elif case == "dna_p3":
+        spec = gen.SPECS[5]
+        a, o = gen.generate(spec, n=600, seed=5)
+        alpha, k, p = spec.alphabet, spec.k, 3
+    else:   # k-mer counts above 255 on both sides of a (sequence, sample) pair: the exact fix-up
+        rng = np.random.default_rng(23)
+        seqs = ["A" * int(rng.integers(300, 3000)) for _ in range(12)] + ["A" * 40 + "C" * 400] * 3
+        seqs += ["".join(rng.choice(list("ACDEFGHIKLMNPQRSTVWY"), int(rng.integers(20, 300)))) for _ in range(45)]
+        seqs = [seqs[i] for i in rng.permutation(len(seqs))]
+        a, o = gen.from_strings(seqs)
+        alpha, k, p = "protein", 3, 3
+    n = len(o) - 1
+    ctx = Context(alpha, k, p, kernel=kernel, rank_mode="samples")
+    ctx.load(a, o, n, 0)
+    sizes = ctx.run()
+    r = oracle.run(a, o, alpha, k, p, mode="samples")
+    _compare_f1(ctx, sizes, r, a, o, p)
+
