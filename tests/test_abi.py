@@ -65,3 +65,17 @@ def test_bad_args(L):
     from paper_0901_2742_b200.runtime import exchange_sizes
     with pytest.raises(L.SadError):
         exchange_sizes(6, 4, 0, np.zeros((6, 6, 2), np.int64))
+
+
+def test_rank_stats_spec_examples():
+    """SPEC S:633-641 rank_stats examples (SURVEY §8(f) f2 reporting): a == b -> zero spread;
+    a = [0, 0], b = [1, 3] -> mean_b 2, diffs [1, 3], population variance 1, stddev 1."""
+    from paper_0901_2742_b200 import stats
+    r = stats.rank_stats([0.5, 0.25], [0.5, 0.25])
+    assert r["Variance w.r.t. Centralized"] == 0 and r["Standard Dev. w.r.t Centralized"] == 0
+    r = stats.rank_stats([0, 0], [1, 3])
+    assert r["Average Globalized"] == 2 and r["Variance w.r.t. Centralized"] == 1
+    assert r["Standard Dev. w.r.t Centralized"] == 1
+    assert r["(Maximum, Minimum) Globalized"] == (3, 1)
+    # R values of SPEC S:180-182 (PAPER.md:50, natural log)
+    assert abs(stats.rank_R([0.0])[0] + 2.302585093) < 1e-9 and abs(stats.rank_R([1.0])[0] - 0.0953101798) < 1e-9

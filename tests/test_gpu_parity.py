@@ -317,3 +317,20 @@ def test_samples_mode(kernel, case):
     r = oracle.run(a, o, alpha, k, p, mode="samples")
     _compare_f1(ctx, sizes, r, a, o, p)
 
+
+def test_centralized_full_size_sampled():
+    """the centralized rank (one shard of all N = 100 000 sequences of config 4,
+    the 5 x 10^9-pair all-pairs on the tensor cores): sampled T_i against the oracle row by row,
+    and the properties that hold at any size."""
+    spec = gen.SPECS[4]
+    a, o = gen.generate(spec)
+    n = len(o) - 1
+    ctx, sizes = _run_gpu(a, o, spec.alphabet, spec.k, 1, "tc")
+    T = ctx.local_rank(0)
+    rows = np.random.default_rng(44).choice(n, 12, replace=False)
+    assert np.array_equal(oracle.rows_T(a, o, spec.k, 1, rows), T[rows])
+    assert sizes.tolist() == [n]
+    keys = ctx.out_keys().cpu().numpy().view(np.uint64)
+    assert np.all(keys[1:] > keys[:-1])
+    assert np.array_equal(np.sort((keys & np.uint64(0x7FFFFFFF)).astype(np.int64)), np.arange(n))
+
