@@ -311,3 +311,47 @@ def test_psrs_load_bound_trials(p):
         assert r.bsize.sum() == n
         assert r.bsize.max() <= 2 * w + p
         assert r.bsize.max() < 2 * w                                # p | w here
+
+
+# ---------------------------------------------------------------- f4: UPGMA guide tree (oracle)
+
+def test_upgma_spec_examples():
+    """n = 2 -> one join at d(0,1)/2; n = 3 with d(0,1) = 0.2 < d(0,2) = 0.8,
+    d(1,2) = 0.9 -> {0,1} first, then with 2 at height (0.8 + 0.9)/4; n = 1 -> no join."""
+    from oracle import upgma as U
+    m, h, s = U.upgma(np.array([[0.0, 0.6], [0.6, 0.0]]))
+    assert m.tolist() == [[0, 1]] and h.tolist() == [0.3] and s.tolist() == [2]
+    D = np.array([[0.0, 0.2, 0.8], [0.2, 0.0, 0.9], [0.8, 0.9, 0.0]])
+    m, h, s = U.upgma(D)
+    assert m.tolist() == [[0, 1], [3, 2]]
+    assert h[0] == 0.1 and h[1] == (0.8 + 0.9) / 4 and s.tolist() == [2, 3]
+    m, h, s = U.upgma(np.zeros((1, 1)))
+    assert len(m) == 0
+
+
+def test_upgma_ties_lexicographic():
+    """D-M1: all distances equal -> (0,1) first, then the new cluster (position 0) with 2, ..."""
+    from oracle import upgma as U
+    n = 5
+    D = np.ones((n, n)) - np.eye(n)
+    m, h, s = U.upgma(D)
+    assert m.tolist() == [[0, 1], [5, 2], [6, 3], [7, 4]]
+    assert h.tolist() == [0.5] * 4
+
+
+def test_upgma_vs_scipy_average_linkage():
+    """Special case that reduces to a library routine: on tie-free random metrics, UPGMA equals
+    scipy.cluster.hierarchy.linkage(method='average') (same merge sets, heights = d/2)."""
+    from scipy.cluster.hierarchy import linkage
+    from scipy.spatial.distance import squareform
+    from oracle import upgma as U
+    rng = np.random.default_rng(3)
+    for n in (4, 9, 30, 64):
+        X = rng.random((n, 5))
+        D = np.sqrt(((X[:, None, :] - X[None, :, :]) ** 2).sum(-1))
+        m, h, s = U.upgma(D)
+        Z = linkage(squareform(D, checks=False), method="average")
+        assert np.allclose(h * 2, Z[:, 2], rtol=0, atol=1e-12)
+        assert [sorted(r) for r in m.tolist()] == [sorted(map(int, r)) for r in Z[:, :2]]
+        assert s.tolist() == Z[:, 3].astype(int).tolist()
+        assert np.all(np.diff(h) >= -1e-15)                       # ultrametric: heights never decrease
