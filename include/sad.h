@@ -302,6 +302,27 @@ int sad_get_bucket_view(sad_ctx *ctx, int bucket, const uint8_t **d_res, const i
  * SAD_F_KEEP_SIM and sad_rank_local; enqueued on the stream. */
 int sad_get_distance(sad_ctx *ctx, int shard, float *d_D, int64_t cap);
 
+/* The same distances in IEEE float64 (__ddiv_rn then __dsub_rn), the input of sad_upgma. */
+int sad_get_distance_f64(sad_ctx *ctx, int shard, double *d_D, int64_t cap);
+
+/*
+ * sad_upgma — SURVEY §8(f) row f4: the UPGMA guide tree of n sequences (the first
+ * stage of the per-bucket progressive aligner). Context-free, enqueued on `stream`.
+ *   d_D        n x n float64 distances (device); only the upper triangle is read; DESTROYED
+ *   d_merges   [n-1][2] int64 out: step t joins the clusters with these ids (leaves 0..n-1, the
+ *              cluster of step t is n + t); the first id is the cluster at the smaller position
+ *   d_heights  [n-1] float64 out: join height d/2
+ *   d_sizes    [n-1] int64 out: leaves under the new cluster
+ *   d_ws       >= sad_upgma_workspace(n) bytes, 256-byte aligned
+ * Rules: closest active pair (i < j) by position, ties -> smallest i then j (D-M1); a cluster lives
+ * at its smallest leaf's position; average linkage (n_i d(k,i) + n_j d(k,j)) / (n_i + n_j) with
+ * each IEEE float64 operation rounded once. n == 1: nothing to do. One thread block; O(n^2) work
+ * per merge in the worst case, O(n) typically.
+ */
+size_t sad_upgma_workspace(int64_t n);
+int sad_upgma(double *d_D, int64_t n, int64_t *d_merges, double *d_heights, int64_t *d_sizes, void *d_ws,
+              size_t ws_bytes, void *stream);
+
 /* Per-shard profile facts (after sad_build_profiles): total k-mer windows, distinct k-mers
  * and the operand column count K_s of every local shard (int64 [p/world] each; any may be NULL). */
 int sad_get_profile_info(sad_ctx *ctx, int64_t *h_windows, int64_t *h_distinct, int64_t *h_kcols);

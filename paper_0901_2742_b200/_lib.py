@@ -25,7 +25,8 @@ SYMBOLS = [
     "sad_rank_global", "sad_partition_plan", "sad_exchange_sizes", "sad_pack_plan", "sad_pack", "sad_output_size",
     "sad_output_layout", "sad_finish", "sad_get_local_rank", "sad_get_ancestors", "sad_get_ranks", "sad_get_sorted",
     "sad_get_pivots", "sad_get_bucket", "sad_get_bucket_sizes", "sad_get_similarity", "sad_get_profile_info", "sad_get_stats",
-    "sad_reset_stats", "sad_selftest_fixed_point", "sad_get_bucket_view", "sad_get_distance", "sad_exchange_records",
+    "sad_reset_stats", "sad_selftest_fixed_point", "sad_get_bucket_view", "sad_get_distance", "sad_exchange_records", "sad_get_distance_f64",
+    "sad_upgma_workspace", "sad_upgma",
 ]
 
 
@@ -89,6 +90,9 @@ def lib():
         "sad_get_bucket_view": (i32, [P, i32, P, P, P, P]),
         "sad_get_distance": (i32, [P, i32, P, i64]),
         "sad_exchange_records": (i32, [P]),
+        "sad_get_distance_f64": (i32, [P, i32, P, i64]),
+        "sad_upgma_workspace": (sz, [i64]),
+        "sad_upgma": (i32, [P, i64, P, P, P, P, sz, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -506,6 +506,20 @@ void launch_distance(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, flo
     if (w > 0) k_distance<<<grid1d(w * w), 256, 0, st>>>(sim, rowinfo, w, D);
 }
 
+// the same in float64 (the input of the f4 guide tree): __ddiv_rn then __dsub_rn
+__global__ void k_distance64(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, double *D) {
+    const int64_t nn = w * w;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nn; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / w, j = t - i * w;
+        const uint32_t den = min(rowinfo[i].tw, rowinfo[j].tw);
+        D[t] = i == j ? 0.0 : __dsub_rn(1.0, __ddiv_rn((double)sim[t], (double)den));
+    }
+}
+
+void launch_distance64(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, double *D, cudaStream_t st) {
+    if (w > 0) k_distance64<<<grid1d(w * w), 256, 0, st>>>(sim, rowinfo, w, D);
+}
+
 // ---------------------------------------------------------------------------------------
 // f1: the paper's literal listing, PAPER.md:68-72 — "Sort the sequences locally
 // in each processor based on k-mer rank", "Choose a sample set of k sequences in each

@@ -1233,6 +1233,34 @@ int sad_get_distance(sad_ctx *ctx, int shard, float *d_D, int64_t cap) {
     return SAD_OK;
 }
 
+int sad_get_distance_f64(sad_ctx *ctx, int shard, double *d_D, int64_t cap) {
+    GUARD(3);
+    if (!ctx->d_sim) return fail(ctx, SAD_E_STATE, "context created without SAD_F_KEEP_SIM");
+    int64_t b0, w;
+    if (int rc = shard_check(ctx, shard, INT64_MAX, b0, w)) return rc;
+    if (!d_D || cap < w * w) return fail(ctx, SAD_E_CAPACITY, "capacity %lld < %lld", (long long)cap, (long long)(w * w));
+    int64_t sb = 0;
+    for (int s = 0; s < shard; ++s) {
+        const int64_t ws = ctx->shard_base[s + 1] - ctx->shard_base[s];
+        sb += ws * ws;
+    }
+    launch_distance64(ctx->d_sim + sb, ctx->d_rowinfo + b0, w, d_D, ctx->st);
+    LAUNCHED();
+    return SAD_OK;
+}
+
+size_t sad_upgma_workspace(int64_t n) { return n > 0 ? upgma_workspace(n) : 0; }
+
+int sad_upgma(double *d_D, int64_t n, int64_t *d_merges, double *d_heights, int64_t *d_sizes, void *d_ws,
+              size_t ws_bytes, void *stream) {
+    if (n < 1 || !d_D || (n > 1 && (!d_merges || !d_heights || !d_sizes)) || n > 0x7FFFFFFF) return SAD_E_ARG;
+    if (n == 1) return SAD_OK;
+    if (!d_ws || ws_bytes < upgma_workspace(n) || (reinterpret_cast<uintptr_t>(d_ws) & 255)) return SAD_E_CAPACITY;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    launch_upgma(d_D, n, d_merges, d_heights, d_sizes, d_ws, st);
+    return cudaGetLastError() == cudaSuccess ? SAD_OK : SAD_E_CUDA;
+}
+
 int sad_get_profile_info(sad_ctx *ctx, int64_t *h_windows, int64_t *h_distinct, int64_t *h_kcols) {
     GUARD(2);
     for (int s = 0; s < ctx->pl; ++s) {

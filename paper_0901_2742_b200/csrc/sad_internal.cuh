@@ -293,6 +293,9 @@ void launch_gather_out(const int32_t *perm, int64_t n, const int64_t *src_off, c
 void launch_selftest_fixed(int max_den, unsigned long long *bad, cudaStream_t st);
 void launch_rebase(const int64_t *src, int64_t n1, int64_t *off, cudaStream_t st);
 void launch_distance(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, float *D, cudaStream_t st);
+void launch_distance64(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, double *D, cudaStream_t st);
+size_t upgma_workspace(int64_t n);
+void launch_upgma(double *D, int64_t n, int64_t *merges, double *heights, int64_t *sizes, void *ws, cudaStream_t st);
 
 }  // namespace sad
 

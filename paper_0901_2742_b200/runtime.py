@@ -77,6 +77,23 @@ def all_to_all_v(send: torch.Tensor, send_sizes, recv_sizes, group=None) -> torc
     return recv
 
 
+def upgma(D: torch.Tensor, stream: torch.cuda.Stream | None = None):
+    """UPGMA guide tree of a float64 CUDA distance matrix (include/sad.h sad_upgma; D is destroyed).
+    Returns host arrays (merges [n-1, 2], heights [n-1], sizes [n-1])."""
+    n = int(D.shape[0])
+    merges = torch.empty((max(n - 1, 1), 2), dtype=torch.int64, device=D.device)
+    heights = torch.empty(max(n - 1, 1), dtype=torch.float64, device=D.device)
+    sizes = torch.empty(max(n - 1, 1), dtype=torch.int64, device=D.device)
+    wsb = int(L.lib().sad_upgma_workspace(n))
+    ws = torch.empty(wsb + 256, dtype=torch.uint8, device=D.device)
+    p_ws = (ws.data_ptr() + 255) // 256 * 256
+    st = stream if stream is not None else torch.cuda.current_stream(D.device)
+    L.check(L.lib().sad_upgma(_vp(D), n, _vp(merges), _vp(heights), _vp(sizes), ctypes.c_void_p(p_ws), wsb,
+                              ctypes.c_void_p(st.cuda_stream)), "sad_upgma")
+    st.synchronize()
+    return merges[: n - 1].cpu().numpy(), heights[: n - 1].cpu().numpy(), sizes[: n - 1].cpu().numpy()
+
+
 # ----------------------------------------------------------------------------------------
 # the context
 # ----------------------------------------------------------------------------------------
@@ -334,6 +351,22 @@ class Context:
         S = child.similarity(0)
         child.close()
         return D, S
+
+    def bucket_guide_tree(self, b: int, kernel: str | None = None):
+        """the UPGMA guide tree of owned bucket b on this device (sad_upgma on
+        the bucket's float64 k-mer distances). Returns host arrays (merges [n-1, 2] cluster ids,
+        heights [n-1], sizes [n-1]); leaves are positions in the bucket's order."""
+        res, off, n, r = self.bucket_view(b)
+        child = Context(self.alphabet, self.k, 1, device=self.device.index, stream=self.stream,
+                        kernel=kernel or self.kernel, keep_sim=True)
+        child.load_device_view(res, off, n, r)
+        child.build_profiles()
+        child.rank_local()
+        D = torch.empty((n, n), dtype=torch.float64, device=self.device)
+        child._call("sad_get_distance_f64", 0, _vp(D), n * n)
+        out = upgma(D, self.stream)
+        child.close()
+        return out
 
     def load_device_view(self, res_ptr: int, off_ptr: int, n: int, residues: int):
         """Load n sequences from device memory whose offsets start at an arbitrary base (a bucket

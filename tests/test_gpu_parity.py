@@ -334,3 +334,45 @@ def test_centralized_full_size_sampled():
     assert np.all(keys[1:] > keys[:-1])
     assert np.array_equal(np.sort((keys & np.uint64(0x7FFFFFFF)).astype(np.int64)), np.arange(n))
 
+
+def test_upgma_random_and_tied_matrices():
+    """f4 kernel vs the oracle UPGMA on synthetic distance matrices: continuous (no ties), heavily
+    tied (values on a grid of 8 levels) and all-equal, n from 2 to 700: identical merges, heights
+    bit-equal (the same IEEE float64 operation sequence)."""
+    import torch
+    from oracle import upgma as U
+    from paper_0901_2742_b200.runtime import upgma
+    rng = np.random.default_rng(9)
+    for n, kind in [(2, "c"), (3, "c"), (17, "t"), (64, "c"), (200, "t"), (333, "e"), (700, "t")]:
+        if kind == "e":
+            D = np.ones((n, n)) - np.eye(n)
+        else:
+            A = rng.random((n, n))
+            if kind == "t":
+                A = np.floor(A * 8) / 8
+            D = np.triu(A, 1)
+            D = D + D.T
+        ref = U.upgma(D)
+        got = upgma(torch.from_numpy(D).cuda())
+        assert np.array_equal(got[0], ref[0]), (n, kind)
+        assert np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_bucket_guide_trees(cfg):
+    """f4 on the path's output: every bucket's UPGMA tree on the GPU (from its float64 k-mer
+    distances) equals the oracle's tree on the oracle's distances."""
+    from oracle import upgma as U
+    spec = gen.SPECS[cfg]
+    a, o = gen.generate(cfg)
+    ctx, sizes = _run_gpu(a, o, spec.alphabet, spec.k, spec.p, "tc")
+    for b in range(spec.p):
+        idx = ctx.bucket(b)[0]
+        if len(idx) < 2:
+            continue
+        ii, jj = np.meshgrid(idx, idx, indexing="ij")
+        Sref, dref = oracle.pairs_S(a, o, spec.k, ii.ravel(), jj.ravel())
+        ref = U.upgma(U.distance_f64(Sref.reshape(len(idx), -1), dref.reshape(len(idx), -1)))
+        got = ctx.bucket_guide_tree(b)
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
+
