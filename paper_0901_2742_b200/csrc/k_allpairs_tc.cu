@@ -56,6 +56,9 @@ struct Traits {
 #ifndef SAD_TC_XBUFS
 #define SAD_TC_XBUFS 2
 #endif
+#ifndef SAD_TC_NOBAR
+#define SAD_TC_NOBAR 0       // 1: epilogue warps add their row / column partials to T directly (no barriers)
+#endif
     static constexpr int STAGES = CG == 1 ? (KIND == 0 ? 2 : 3) : SAD_TC_STAGES2;   // (one-CTA tiles: reference variants)
     static constexpr int XBUFS = SAD_TC_XBUFS;          // K6 staging buffers
     static constexpr int B_BYTES = BNC * BK;
@@ -450,9 +453,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             const int64_t rbase = P.shard_base[tl.s];
             const int64_t w = P.shard_base[tl.s + 1] - rbase;
             const int64_t col0 = (int64_t)tl.J * BN, row0 = (int64_t)tl.I * BMT + (int64_t)crank * BM;
+#if !SAD_TC_NOBAR
             epi_bar();                            // previous tile's colinfo / colsum / rowpart consumed
             if (e < BN) colinfo[e] = cur.ci;
             epi_bar();
+#endif
             const int64_t row = row0 + quarter * 32 + lane;
             const bool vrow = row < w;
             const RowInfo ri = cur.ri;
@@ -517,11 +522,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                         const bool ok = vrow && col < w && col >= row;
                         // the self term is exactly 2^32 (reading A3: S_ii = den_ii = L_i - k + 1)
                         const uint32_t S = col == row ? ri.tw : v[j];
-                        const uint64_t q = pair_q(ok ? S : 0u, ri, colinfo[ch * 16 + j]);
+#if SAD_TC_NOBAR
+                        const RowInfo cj = col < w ? P.rowinfo[rbase + col] : RowInfo{1u, 0xFFFFFFFFu, 1u, 0u};
+#else
+                        const RowInfo cj = colinfo[ch * 16 + j];
+#endif
+                        const uint64_t q = pair_q(ok ? S : 0u, ri, cj);
                         rowsum += q;
                         cv[j] = (col != row) ? q : 0ull;
                         if (simr && ok) {
-                            const int64_t oi = ri.shard, oj = colinfo[ch * 16 + j].shard;   // local indices
+                            const int64_t oi = ri.shard, oj = cj.shard;   // local indices
                             simr[oi * w + oj] = (uint16_t)S;
                             simr[oj * w + oi] = (uint16_t)S;
                         }
@@ -561,7 +571,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     cv[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 2);
                 }
                 cv[0] += __shfl_xor_sync(0xffffffffu, cv[0], 1);
+#if SAD_TC_NOBAR
+                // this warp's 32-row partial of column (lane >> 1) & 15 straight into T (u64 RED; the
+                // four row quarters and the two CTAs add theirs independently: integer addition)
+                if (!(lane & 1)) {
+                    const int64_t col = col0 + ch * 16 + ((lane >> 1) & 15);
+                    if (col < w && cv[0]) atomicAdd(&P.T[rbase + P.rowinfo[rbase + col].shard], cv[0]);
+                }
+#else
                 if (!(lane & 1)) colsum[quarter * 256 + ch * 16 + ((lane >> 1) & 15)] = cv[0];
+#endif
             }
             tc_fence_before();
             __syncwarp();
@@ -571,6 +590,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             }
             if (++xb == Tr::XBUFS) { xb = 0; xph ^= 1; }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+#if SAD_TC_NOBAR
+            if (vrow && rowsum) atomicAdd(&P.T[rbase + ri.shard], rowsum);       // .shard: local index
+#else
             if (grp) rowpart[(grp - 1) * 128 + quarter * 32 + lane] = rowsum;
             epi_bar();
             if (grp == 0) {
@@ -582,6 +604,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                 const unsigned long long cs = colsum[e] + colsum[256 + e] + colsum[512 + e] + colsum[768 + e];
                 if (col < w && cs) atomicAdd(&P.T[rbase + colinfo[e].shard], cs);
             }
+#endif
             cur = nxt;
             nxt.tl = tl2;
         }

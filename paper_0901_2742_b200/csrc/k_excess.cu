@@ -28,6 +28,9 @@
 namespace sad {
 
 constexpr int kXrWarps = 8;
+#ifndef SAD_XROWS_GLOBAL
+#define SAD_XROWS_GLOBAL 1   // 1: accumulate each row's excess in place in E (global); 0: shared-memory rows
+#endif
 
 // K6 lists: every entry above its shard's cap goes to L_tau as (row << 8) | (n - T_s), one warp
 // per row over the row's leading count >= 2 entries (positions from per-(shard, tau) cursors)
@@ -170,7 +173,108 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows(ExcessArgs a, int warps
     }
 }
 
+// The same product with the row's dense excess bytes accumulated in place, in E (global memory,
+// L2-resident while the warp works on the row): the row's upper part is zeroed when its first
+// excess k-mer appears, then the partners' bytes are added with fire-and-forget 32-bit atomics
+// (no carry: every e_ij <= 255). No shared-memory accumulator, so occupancy is not bounded by w.
+__global__ void __launch_bounds__(kXrWarps * 32) k_xrows_g(ExcessArgs a) {
+    __shared__ unsigned long long lbase[kMaxLocalShards + 1];
+    __shared__ uint32_t sg_end[kXrWarps][32], sg_src[kXrWarps][32], sg_xa[kXrWarps][32];   // per-batch list segments
+    if (threadIdx.x == 0) {
+        unsigned long long acc = 0;
+        for (int s = 0; s < a.pl; ++s) {
+            lbase[s] = acc;
+            acc += a.xtot[s];
+        }
+    }
+    __syncthreads();
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * kXrWarps;
+    for (int64_t r = (int64_t)blockIdx.x * kXrWarps + wid; r < a.n; r += nw) {
+        int s = 0;
+        while (s + 1 < a.pl && r >= a.shard_base[s + 1]) ++s;
+        const uint32_t T = a.cap[s];
+        const uint32_t local = (uint32_t)(r - a.shard_base[s]);          // sorted position (length order)
+        const int64_t i = a.shard_base[s] + a.sigma[r];                  // the sequence there
+        const int64_t w = a.shard_base[s + 1] - a.shard_base[s];
+        const int nch = (int)((w + 15) >> 4);
+        uint8_t *erow = a.E + a.ebase[s] + (int64_t)local * (nch * 16);
+        bool zeroed = false;
+        if (T != kNoCap) {
+            const uint32_t *ent = a.csr + (a.off[i] - i * (int64_t)(a.k - 1));
+            const int d = a.nhi[i];               // the row's count >= 2 entries lead its CSR
+            for (int e0 = 0; e0 < d; e0 += 32) {
+                const int e = e0 + lane;
+                const uint32_t v = e < d ? ent[e] : 0u;
+                const bool hit = (v & 0xFFFFu) > T;
+                const uint32_t mask = __ballot_sync(0xffffffffu, hit);
+                if (!mask) continue;
+                if (!zeroed) {                    // the row's upper part, once
+                    for (int c = (int)((local + 1) >> 4) + lane; c < nch; c += 32)
+                        reinterpret_cast<uint4 *>(erow)[c] = make_uint4(0, 0, 0, 0);
+                    zeroed = true;
+                    __syncwarp();                 // orders the zeros before every lane's atomics
+                }
+                uint32_t len = 0;
+                if (hit) {
+                    const uint32_t key = (uint32_t)s * (uint32_t)a.V + (v >> 16);
+                    const uint32_t o0 = a.xoff[key];
+                    const uint32_t o1 = (v >> 16) + 1 < (uint32_t)a.V ? a.xoff[key + 1] : (uint32_t)a.xtot[s];
+                    len = o1 - o0;
+                    const int hrank = __popc(mask & ((1u << lane) - 1u));
+                    sg_src[wid][hrank] = (uint32_t)(lbase[s] + o0);
+                    sg_xa[wid][hrank] = (v & 0xFFFFu) - T;
+                }
+                uint32_t incl = len;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                if (hit) sg_end[wid][__popc(mask & ((1u << lane) - 1u))] = incl;
+                const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+                __syncwarp();
+                int g = 0;
+                for (uint32_t t0 = 0; t0 < tot; t0 += 128) {
+                    uint32_t vb[4], xa[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t t = t0 + (uint32_t)(u * 32 + lane);
+                        vb[u] = 0;
+                        xa[u] = 0;
+                        if (t < tot) {
+                            while (t >= sg_end[wid][g]) ++g;
+                            const uint32_t st = g ? sg_end[wid][g - 1] : 0u;
+                            vb[u] = a.lists[sg_src[wid][g] + (t - st)];
+                            xa[u] = sg_xa[wid][g];
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t b = vb[u] >> 8;
+                        if (xa[u] && b > local)
+                            atomicAdd(reinterpret_cast<uint32_t *>(erow + (b & ~3u)),
+                                      min(xa[u], vb[u] & 0xFFu) << (8u * (b & 3u)));
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        if (lane == 0) a.xrow[r] = make_uint2(zeroed ? 1u : 0u, 0u);
+    }
+}
+
 int launch_excess(const ExcessArgs &a, cudaStream_t st) {
+    if (SAD_XROWS_GLOBAL) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_xrows_g, kXrWarps * 32, 0);
+        const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), (a.n + kXrWarps - 1) / kXrWarps);
+        if (grid > 0) k_xrows_g<<<(unsigned)grid, kXrWarps * 32, 0, st>>>(a);
+        return 0;
+    }
     const int warps = (int)std::min<int64_t>(kXrWarps, (int64_t)kXrSmem / a.accb);
     if (warps < 1) return -1;
     const size_t smem = (size_t)warps * a.accb;
