@@ -426,10 +426,13 @@ __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int 
     int s = 0, d = 0;
     int64_t eo = 0;
     if (r < a.rows_pad) locate(r, s, eo, d);
+    uint32_t vpre[kOpBatch];                 // the row's first entry batch, loaded during the previous row
+    bool have_pre = false;
     for (; r < a.rows_pad; r += nw) {
         const uint32_t *ent = a.csr + eo;
         const uint32_t *c0 = a.col0 + (size_t)s * a.V;
         const uint32_t T = a.cap ? a.cap[s] : 0xFFFFFFFFu;
+        const bool ident = a.ident && a.ident[s];   // column of tau is tau itself (cap 1, every k-mer present)
         const int dcur = d;
         int sn = 0, dn = 0;                  // next row of this warp, fetched ahead
         int64_t eon = 0;
@@ -442,13 +445,19 @@ __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int 
             const uint32_t c_lo = ch * per_byte, c_hi = (ch + len) * per_byte;
             for (int e0 = 0; e0 < dcur; e0 += 32 * kOpBatch) {
                 uint32_t v[kOpBatch], cb[kOpBatch];
+                if (e0 == 0 && ch == 0 && have_pre) {
 #pragma unroll
-                for (int b = 0; b < kOpBatch; ++b) {
-                    const int e = e0 + b * 32 + lane;
-                    v[b] = e < dcur ? ent[e] : 0u;
+                    for (int b = 0; b < kOpBatch; ++b) v[b] = vpre[b];
+                } else {
+#pragma unroll
+                    for (int b = 0; b < kOpBatch; ++b) {
+                        const int e = e0 + b * 32 + lane;
+                        v[b] = e < dcur ? ent[e] : 0u;
+                    }
                 }
 #pragma unroll
-                for (int b = 0; b < kOpBatch; ++b) cb[b] = (v[b] & 0xFFFFu) ? c0[v[b] >> 16] : 0u;
+                for (int b = 0; b < kOpBatch; ++b)
+                    cb[b] = ident ? (v[b] >> 16) : ((v[b] & 0xFFFFu) ? c0[v[b] >> 16] : 0u);
 #pragma unroll
                 for (int b = 0; b < kOpBatch; ++b) {
                     const uint32_t n = v[b] & 0xFFFFu;     // 0 for lanes past the row's entries
@@ -461,6 +470,15 @@ __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int 
                             row[cc] = 1;
                     }
                 }
+            }
+            have_pre = false;
+            if (ch + (uint32_t)slice >= stride && r + nw < a.rows_pad) {   // the next row's first batch
+#pragma unroll
+                for (int b = 0; b < kOpBatch; ++b) {
+                    const int e = b * 32 + lane;
+                    vpre[b] = e < dn ? a.csr[eon + e] : 0u;
+                }
+                have_pre = true;
             }
             __syncwarp();
             for (uint32_t t = lane; t < len / 16; t += 32) dst[ch / 16 + t] = reinterpret_cast<const uint4 *>(row)[t];

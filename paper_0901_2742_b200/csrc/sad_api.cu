@@ -122,6 +122,7 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_err = b.take<unsigned long long>(4);
     c->d_kinfo = b.take<unsigned long long>((size_t)pl * kKinfo);
     c->d_cap = b.take<uint32_t>((size_t)pl);
+    c->d_ident = b.take<uint32_t>((size_t)pl);
     c->d_xsel = b.take<uint32_t>((size_t)pl);
     c->d_Xc = b.take<uint32_t>((size_t)pl * kNumCaps * V);
     c->d_xoff = b.take<uint32_t>((size_t)pl * V + 2 * (size_t)pl + 2);
@@ -521,7 +522,9 @@ int sad_build_profiles(sad_ctx *ctx) {
         for (int s = 0; s < pl; ++s) {
             hc[s] = ctx->h_cap[s];
             hc[pl + s] = sel[s];
+            hc[2 * pl + s] = (ctx->h_cap[s] == 1u && ctx->h_K[s] == V) ? 1u : 0u;   // col0(tau) = tau
         }
+        CK(cudaMemcpyAsync(ctx->d_ident, hc + 2 * pl, sizeof(uint32_t) * pl, cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_cap, hc, sizeof(uint32_t) * pl, cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_xsel, hc + pl, sizeof(uint32_t) * pl, cudaMemcpyHostToDevice, ctx->st));
     }
@@ -635,6 +638,7 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
         launch_capscan(ctx->d_M, ctx->V, nullptr, ctx->d_cap, ctx->d_col0, nullptr, 0, pl, ctx->V, ctx->st);
         LAUNCHED();
         o.cap = ctx->d_cap;
+        o.ident = ctx->d_ident;
         if (lists) {
             launch_capscan(ctx->d_Xc, (int64_t)kNumCaps * ctx->V, ctx->d_xsel, nullptr, ctx->d_xoff, xtot, 1, pl,
                            ctx->V, ctx->st);

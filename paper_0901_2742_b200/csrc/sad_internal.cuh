@@ -102,6 +102,7 @@ struct OperandArgs {
     void *op;
     const uint32_t *cap;             // device [pl] layer cap T_s per shard (kNoCap: none), or NULL
     const int32_t *sigma;            // device [n] length order (sorted position -> local index), or NULL
+    const uint32_t *ident;           // device [pl] 1: the column of tau is tau (cap 1, all V k-mers present), or NULL
 };
 void launch_indicator(const OperandArgs &a, cudaStream_t st);
 void launch_lenkeys(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *keys,
@@ -341,6 +342,7 @@ struct sad_ctx {
     uint32_t *d_M = nullptr, *d_col0 = nullptr;
     unsigned long long *d_err = nullptr, *d_kinfo = nullptr;
     uint32_t *d_cap = nullptr, *d_xsel = nullptr;   // layer cap T_s and its index j_s per shard
+    uint32_t *d_ident = nullptr;                    // per shard: identity column map (K4 skips col0)
     uint32_t *d_Xc = nullptr;        // [pl][kNumCaps][V] entries above each candidate cap
     uint32_t *d_xoff = nullptr, *d_xcur = nullptr;  // [pl][V] K6 list offsets (+ u64 [pl] totals) / cursors
     uint2 *d_xrow = nullptr;         // [n] K6 row flags
