@@ -190,22 +190,38 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows_g(ExcessArgs a) {
     __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * kXrWarps;
-    for (int64_t r = (int64_t)blockIdx.x * kXrWarps + wid; r < a.n; r += nw) {
+    // the next row's sequence index, CSR position and first entry batch are fetched during the
+    // current row (a three-step dependent chain: sigma -> off / nhi -> entries)
+    int64_t r = (int64_t)blockIdx.x * kXrWarps + wid;
+    int64_t i_c = r < a.n ? a.shard_base[0] + 0 : 0;
+    auto seq_of = [&](int64_t rr) {
+        int s = 0;
+        while (s + 1 < a.pl && rr >= a.shard_base[s + 1]) ++s;
+        return a.shard_base[s] + a.sigma[rr];
+    };
+    i_c = r < a.n ? seq_of(r) : 0;
+    int64_t eo_c = r < a.n ? a.off[i_c] - i_c * (int64_t)(a.k - 1) : 0;
+    int d_c = r < a.n ? a.nhi[i_c] : 0;
+    uint32_t v_c = lane < d_c ? a.csr[eo_c + lane] : 0u;
+    for (; r < a.n; r += nw) {
         int s = 0;
         while (s + 1 < a.pl && r >= a.shard_base[s + 1]) ++s;
         const uint32_t T = a.cap[s];
         const uint32_t local = (uint32_t)(r - a.shard_base[s]);          // sorted position (length order)
-        const int64_t i = a.shard_base[s] + a.sigma[r];                  // the sequence there
         const int64_t w = a.shard_base[s + 1] - a.shard_base[s];
         const int nch = (int)((w + 15) >> 4);
         uint8_t *erow = a.E + a.ebase[s] + (int64_t)local * (nch * 16);
+        const int64_t rn = r + nw;
+        const int64_t i_n = rn < a.n ? seq_of(rn) : 0;                   // step 1 of the next row
+        int64_t eo_n = 0;
+        int d_n = 0;
         bool zeroed = false;
         if (T != kNoCap) {
-            const uint32_t *ent = a.csr + (a.off[i] - i * (int64_t)(a.k - 1));
-            const int d = a.nhi[i];               // the row's count >= 2 entries lead its CSR
+            const uint32_t *ent = a.csr + eo_c;
+            const int d = d_c;                    // the row's count >= 2 entries lead its CSR
             for (int e0 = 0; e0 < d; e0 += 32) {
                 const int e = e0 + lane;
-                const uint32_t v = e < d ? ent[e] : 0u;
+                const uint32_t v = e0 == 0 ? v_c : (e < d ? ent[e] : 0u);
                 const bool hit = (v & 0xFFFFu) > T;
                 const uint32_t mask = __ballot_sync(0xffffffffu, hit);
                 if (!mask) continue;
@@ -234,6 +250,10 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows_g(ExcessArgs a) {
                 if (hit) sg_end[wid][__popc(mask & ((1u << lane) - 1u))] = incl;
                 const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
                 __syncwarp();
+                if (e0 == 0 && rn < a.n) {        // step 2 of the next row
+                    eo_n = a.off[i_n] - i_n * (int64_t)(a.k - 1);
+                    d_n = a.nhi[i_n];
+                }
                 int g = 0;
                 for (uint32_t t0 = 0; t0 < tot; t0 += 128) {
                     uint32_t vb[4], xa[4];
@@ -261,6 +281,15 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows_g(ExcessArgs a) {
             }
         }
         if (lane == 0) a.xrow[r] = make_uint2(zeroed ? 1u : 0u, 0u);
+        if (rn < a.n) {
+            if (!d_n && !eo_n) {                  // step 2 not issued above (no hit batch in this row)
+                eo_n = a.off[i_n] - i_n * (int64_t)(a.k - 1);
+                d_n = a.nhi[i_n];
+            }
+            v_c = lane < d_n ? a.csr[eo_n + lane] : 0u;                  // step 3
+        }
+        eo_c = eo_n;
+        d_c = d_n;
     }
 }
 
