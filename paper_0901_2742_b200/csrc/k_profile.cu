@@ -81,13 +81,23 @@ __global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int 
         for (int j = 0; j < kNumCaps; ++j) exm[j] = 0;
     };
     const int SW = kCodeSeg - (k - 1);   // windows per segment
+    // the next sequence's offsets and first 512 residue bytes are loaded during the current one
+    int64_t off_c = i0 < i1 ? a.off[i0] : 0, off_e = i0 < i1 ? a.off[i0 + 1] : 0;
+    uint4 qpre = i0 < i1 ? *reinterpret_cast<const uint4 *>(a.ascii + ((off_c & ~int64_t(15)) + 16 * lane))
+                         : make_uint4(0, 0, 0, 0);
     for (int64_t i = i0; i < i1; ++i) {
         if (i >= a.shard_base[s + 1]) {                        // shard change: flush the totals
             flush();
             while (s + 1 < a.pl && i >= a.shard_base[s + 1]) ++s;
         }
-        const int64_t off0 = a.off[i];
-        const int64_t L = a.off[i + 1] - off0;
+        const int64_t off0 = off_c;
+        const int64_t L = off_e - off0;
+        const uint4 qfirst = qpre;                             // residues [off0 & ~15, +512) of this lane
+        if (i + 1 < i1) {
+            off_c = off_e;
+            off_e = a.off[i + 2];
+            qpre = *reinterpret_cast<const uint4 *>(a.ascii + ((off_c & ~int64_t(15)) + 16 * lane));
+        }
         const uint8_t *x = a.ascii + off0;
         const unsigned long long gidx = (unsigned long long)(a.first_idx + i);
         const int64_t Tw = L - k + 1;
@@ -113,7 +123,7 @@ __global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int 
             const int64_t b0 = (off0 + r0) & ~int64_t(15), b1 = off0 + r1;
             __syncwarp();
             for (int64_t b = b0 + 16 * lane; b < b1; b += 512) {
-                const uint4 q = *reinterpret_cast<const uint4 *>(a.ascii + b);
+                const uint4 q = (g == 0 && b < b0 + 512) ? qfirst : *reinterpret_cast<const uint4 *>(a.ascii + b);
                 const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {

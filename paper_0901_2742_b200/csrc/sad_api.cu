@@ -108,7 +108,7 @@ size_t cub_bytes_needed(int64_t n, int pl) {
 size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     Bump b{base};
     const int pl = c->pl, p = c->cfg.p, V = c->V;
-    c->d_ascii = b.take<uint8_t>((size_t)R + 16);
+    c->d_ascii = b.take<uint8_t>((size_t)R + 528);     // + 512 + 16: vector reads past the last residue
     c->d_off = b.take<int64_t>((size_t)n + 1);
     c->d_rowinfo = b.take<RowInfo>((size_t)n);
     c->d_csr = b.take<uint32_t>((size_t)std::max<int64_t>(R, 1));
