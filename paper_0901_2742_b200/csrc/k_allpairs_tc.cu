@@ -461,6 +461,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             const int64_t row = row0 + quarter * 32 + lane;
             const bool vrow = row < w;
             const RowInfo ri = cur.ri;
+            const uint32_t nd = 0u - ri.tw;       // -den of the row (interior tiles: the pair's den)
             // interior tile: every (row, col) is a real pair with col > row -> no masks
             const bool interior = (row0 + BM <= w) && (col0 + BN <= w) && (col0 > row0 + BM - 1);
             uint16_t *simr = (P.sim && vrow) ? P.sim + P.sim_base[tl.s] : nullptr;
@@ -511,7 +512,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     for (int j = 0; j < 16; ++j) {
                         // length order: every column of a tile strictly above the diagonal is at
                         // least as long as the row, so the pair's denominator is the row's
-                        const uint64_t q = fixed_q(v[j], ri.tw, ri.qd, ri.rp);
+                        const uint64_t q = fixed_q_nd(v[j], ri.tw, nd, ri.qd, ri.rp);
                         rowsum += q;
                         cv[j] = q;
                     }

@@ -60,6 +60,15 @@ __device__ __forceinline__ uint64_t fixed_q(uint32_t S, uint32_t d, uint32_t qd,
     return (uint64_t)S * qd + t;
 }
 
+// the same with -d supplied (r = x + t*(-d): one IMAD) and the fix-up as a predicated add
+__device__ __forceinline__ uint64_t fixed_q_nd(uint32_t S, uint32_t d, uint32_t nd, uint32_t qd, uint32_t rp) {
+    const uint32_t x = S * rp;
+    uint32_t t = __umulhi(x, qd);
+    const uint32_t r = x + t * nd;
+    asm("{\n\t.reg .pred p;\n\tsetp.ge.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(t) : "r"(r), "r"(d));
+    return (uint64_t)S * qd + t;
+}
+
 __device__ __forceinline__ uint64_t pair_q(uint32_t S, const RowInfo &a, const RowInfo &b) {
     return a.tw <= b.tw ? fixed_q(S, a.tw, a.qd, a.rp) : fixed_q(S, b.tw, b.qd, b.rp);
 }
