@@ -216,6 +216,17 @@ void sum_recv(const sad_ctx *c, const int64_t *h_counts_all, int64_t &n_out, int
 
 }  // namespace
 
+
+// stable (key, row) radix sort: one block for small inputs, else cub::DeviceRadixSort
+template <typename K>
+static cudaError_t sort_pairs(sad_ctx *ctx, const K *ki, K *ko, const int32_t *vi, int32_t *vo, int n, int end_bit) {
+    // (one block wins for 32-bit keys; for 64-bit keys the device sort's passes are faster)
+    if (sizeof(K) == 4 && n <= kSmallSortMax && small_sort_pairs(ki, vi, n, ko, vo, 0, end_bit, ctx->st) == 0)
+        return cudaGetLastError();
+    size_t tb = ctx->cub_bytes;
+    return cub::DeviceRadixSort::SortPairs(ctx->d_cub, tb, ki, ko, vi, vo, n, 0, end_bit, ctx->st);
+}
+
 extern "C" {
 
 static void bucket_sizes_from_counts(sad_ctx *ctx);
@@ -624,11 +635,9 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
             uint32_t *k_in = reinterpret_cast<uint32_t *>(ctx->d_ckey), *k_out = reinterpret_cast<uint32_t *>(ctx->d_ckey_sorted);
             launch_lenkeys(ctx->d_rowinfo, ctx->d_shard_base, pl, ctx->n, k_in, ctx->d_perm_in, ctx->st);
             LAUNCHED();
-            size_t tb = ctx->cub_bytes;
             int sbits = 0;
             while ((1 << sbits) < pl) ++sbits;
-            CK(cub::DeviceRadixSort::SortPairs(ctx->d_cub, tb, k_in, k_out, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
-                                               0, 16 + sbits, ctx->st));
+            CK(sort_pairs(ctx, k_in, k_out, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n, 16 + sbits));
             LAUNCHED();
             launch_lenperm(k_out, ctx->d_perm_sorted, ctx->d_rowinfo, ctx->d_shard_base, ctx->n, ctx->d_sigma,
                            ctx->d_sigma_inv, ctx->d_rinfo_s, ctx->st);
@@ -760,9 +769,8 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
         LAUNCHED();
         int sbits = 0;
         while ((1 << sbits) < pl) ++sbits;
-        size_t tb = ctx->cub_bytes;
-        CK(cub::DeviceRadixSort::SortPairs(ctx->d_cub, tb, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in,
-                                           ctx->d_perm_sorted, (int)ctx->n, 0, 56 + sbits, ctx->st));
+        CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
+                      56 + sbits));
         LAUNCHED();
         launch_sample_records(ctx->d_perm_sorted, ctx->d_shard_base, pl, ctx->cfg.p, ctx->d_csr, ctx->d_off,
                               ctx->d_dcnt, ctx->d_rowinfo, ctx->first_idx, ctx->cfg.k, an.rec_bytes,
@@ -820,9 +828,8 @@ int sad_rank_global(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out
         launch_f1_gainfo(ctx->d_anc_local, ctx->pl, ctx->shard0, p, ctx->first_idx, ctx->d_ga_info, ctx->st);
         LAUNCHED();
     }
-    size_t tb = ctx->cub_bytes;
-    CK(cub::DeviceRadixSort::SortPairs(ctx->d_cub, tb, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in,
-                                       ctx->d_perm_sorted, (int)ctx->n, 0, qbits + sbits, ctx->st));
+    CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
+                  qbits + sbits));
     LAUNCHED();
     launch_unpack_sorted(ctx->d_ckey_sorted, ctx->d_perm_sorted, ctx->n, ctx->first_idx, ctx->d_key_sorted,
                          ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, qbits, ctx->st);

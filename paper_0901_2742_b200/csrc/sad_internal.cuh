@@ -301,6 +301,12 @@ void launch_gather_out(const int32_t *perm, int64_t n, const int64_t *src_off, c
                        const int64_t *dst_off, uint8_t *dst_res, cudaStream_t st);
 
 void launch_selftest_fixed(int max_den, unsigned long long *bad, cudaStream_t st);
+// one-block stable radix sort of n <= kSmallSortMax (key, value) pairs (k_sort.cu); 0 or -1
+constexpr int kSmallSortMax = 512 * 32;
+int small_sort_pairs(const uint32_t *ki, const int32_t *vi, int n, uint32_t *ko, int32_t *vo, int b0, int b1,
+                     cudaStream_t st);
+int small_sort_pairs(const unsigned long long *ki, const int32_t *vi, int n, unsigned long long *ko, int32_t *vo,
+                     int b0, int b1, cudaStream_t st);
 void launch_rebase(const int64_t *src, int64_t n1, int64_t *off, cudaStream_t st);
 void launch_distance(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, float *D, cudaStream_t st);
 void launch_distance64(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, double *D, cudaStream_t st);
