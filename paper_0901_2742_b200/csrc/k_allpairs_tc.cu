@@ -182,6 +182,58 @@ __device__ __forceinline__ void mma_mxf4_pair(uint32_t d, uint64_t a, uint64_t b
         : "memory");
 }
 
+// Warp-wide issue helpers (the whole warp runs the producer / issuer loops, so the descriptor and
+// coordinate arithmetic is warp-uniform and stays on the uniform datapath; one elected lane issues):
+// one stage = BK / 32 = 4 MMAs (K = 64 e2m1 each, descriptor start + 32 B = +2 per step), then the
+// multicast commit that releases the stage in both CTAs.
+#define SAD_MMA_STAGE_ASM(OP, SF)                                                                           \
+    "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t.reg .b16 m;\n\t"                        \
+    "setp.ne.b32 p, %4, 0;\n\t"                                                                          \
+    "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"                                  \
+    "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"                                  \
+    "mov.b16 m, 3;\n\t"                                                                                   \
+    "elect.sync _|e, 0xffffffff;\n\t"                                                                     \
+    "@e " OP " [%0], %1, %2, %3" SF ", p;\n\t"                                                             \
+    "@e " OP " [%0], a1, b1, %3" SF ", 1;\n\t"                                                             \
+    "@e " OP " [%0], a2, b2, %3" SF ", 1;\n\t"                                                             \
+    "@e " OP " [%0], a3, b3, %3" SF ", 1;\n\t"                                                             \
+    "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%6], m;\n}"
+template <int KIND>
+__device__ __forceinline__ void mma_stage_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accf,
+                                               uint32_t sf, uint64_t *bar) {
+    if constexpr (KIND == 1)
+        asm volatile(SAD_MMA_STAGE_ASM("tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32", ", [%5], [%5]")::"r"(d),
+                     "l"(a), "l"(b), "r"(idesc), "r"(accf), "r"(sf), "r"(smem_u32(bar))
+                     : "memory");
+    else
+        asm volatile(SAD_MMA_STAGE_ASM("tcgen05.mma.cta_group::2.kind::i8", "")::"r"(d), "l"(a), "l"(b), "r"(idesc),
+                     "r"(accf), "r"(sf), "r"(smem_u32(bar))
+                     : "memory");
+}
+#undef SAD_MMA_STAGE_ASM
+__device__ __forceinline__ void tc_commit_pair_elect(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+// one stage of 2-SM tensor loads (A and B slices) from an elected lane; the leader CTA's lane also
+// posts the expect_tx of both CTAs' bytes on its full barrier
+__device__ __forceinline__ void tma_stage_pair(const CUtensorMap *mA, const CUtensorMap *mB, uint64_t *bar, void *dA,
+                                               void *dB, int c0, int rA, int rB, uint32_t expect) {
+    asm volatile(
+        "{\n\t.reg .pred e, l;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.and.b32 l, %7, 0, e;\n\t"
+        "@l mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %7;\n\t"
+        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%3], [%0, {%5, %6}], [%9];\n\t"
+        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%4], [%1, {%5, %8}], [%9];\n}" ::"l"(
+            reinterpret_cast<uint64_t>(mA)),
+        "l"(reinterpret_cast<uint64_t>(mB)), "r"(smem_u32(bar)), "r"(smem_u32(dA)), "r"(smem_u32(dB)), "r"(c0), "r"(rA),
+        "r"(expect), "r"(rB), "r"(smem_u32(bar) & kPeerMask)
+        : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t *bar) {
@@ -229,6 +281,24 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 384;" ::: "memory"); }
+
+// SAD_TC_DBG_PROF (timing experiment): clock64 cycles each role spends waiting, printed by two
+// CTA pairs at the end of the launch
+#ifdef SAD_TC_DBG_PROF
+#define TC_TW(acc, stmt)                  \
+    {                                     \
+        const long long _c0 = clock64();  \
+        stmt;                             \
+        acc += clock64() - _c0;           \
+    }
+#define TC_PROF_PRINT(role, a, b, c)                                                                          \
+    if (blockIdx.x < 2 || blockIdx.x == gridDim.x - 1)                                                      \
+        printf("tcprof blk %d %s total %lld waitA %lld waitB %lld\n", (int)blockIdx.x, role, (long long)(a), \
+               (long long)(b), (long long)(c));
+#else
+#define TC_TW(acc, stmt) stmt
+#define TC_PROF_PRINT(role, a, b, c)
+#endif
 
 // global inputs of one tile's epilogue for one thread (row = its TMEM lane, column e < BN for the
 // shared colinfo row)
@@ -328,53 +398,67 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
     if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REG_PRODUCER));
 
     if (warp == 0) {
-        if (lane == 0) {
-            // ===== TMA producer =====
+        if (CG == 2 || lane == 0) {
+            // ===== TMA producer (pairs: the whole warp runs the loop, one elected lane issues) =====
             int stage = 0;
             uint32_t phase = 0;
+            long long pw0 = 0, pw1 = 0;
+            const long long pst = clock64();
             for (int64_t t = t0; t < P.n_tiles; t += tstep) {
                 const TcTile tl = P.tiles[t];
                 const int rowA = (int)(P.shard_rowpad[tl.s] + (int64_t)tl.I * BMT + (int64_t)crank * BM);
                 const int rowB = (int)(P.shard_rowpad[tl.s] + (int64_t)tl.J * BN + (int64_t)crank * BNC);
                 const int nkb = (int)P.kblocks[tl.s];
                 for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
+                    TC_TW(pw0, mbar_wait(&empty[stage], phase ^ 1));
                     if constexpr (CG == 1) {
                         mbar_expect_tx(&full[stage], STAGE_BYTES);
                         tma_load_2d(&tmapA, &full[stage], sA + stage * A_BYTES, kb * BK, rowA);
                         tma_load_2d(&tmapB, &full[stage], sB + stage * B_BYTES, kb * BK, rowB);
                     } else {
 #ifdef SAD_TC_DBG_NOTMA
-                        if (leader) mbar_arrive(&full[stage]);   // timing experiment: no loads (wrong results)
+                        if (leader && lane == 0) mbar_arrive(&full[stage]);   // timing experiment: no loads (wrong results)
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                         continue;
 #endif
                         // the leader's full barrier counts the bytes of both CTAs
-                        if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
-                        tma_load_2d_pair(&tmapA, &full[stage], sA + stage * A_BYTES, kb * BK, rowA);
-                        tma_load_2d_pair(&tmapB, &full[stage], sB + stage * B_BYTES, kb * BK, rowB);
+                        tma_stage_pair(&tmapA, &tmapB, &full[stage], sA + stage * A_BYTES, sB + stage * B_BYTES, kb * BK,
+                                       rowA, rowB, leader ? 2u * STAGE_BYTES : 0u);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
+            if (lane == 0) TC_PROF_PRINT("tma(empty)", clock64() - pst, pw0, pw1);
         }
     } else if (warp == 1) {
-        if (lane == 0 && leader) {
-            // ===== MMA issuer =====
+        if (leader && (CG == 2 || lane == 0)) {
+            // ===== MMA issuer (pairs: the whole warp runs the loop, one elected lane issues) =====
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
+            long long pw0 = 0, pw1 = 0;
+            const long long pst = clock64();
             for (int64_t t = t0; t < P.n_tiles; t += tstep) {
                 const TcTile tl = P.tiles[t];
                 const int nkb = (int)P.kblocks[tl.s];
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                TC_TW(pw0, mbar_wait(&tempty[acc], acc_phase ^ 1));
                 tc_fence_after();
                 const uint32_t d = tmem_base + (uint32_t)(acc * ACC_COLS);
                 for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(&full[stage], phase);
+                    TC_TW(pw1, mbar_wait(&full[stage], phase));
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
+                    if constexpr (CG == 2) {
+#ifdef SAD_TC_DBG_NOMMA
+                        tc_commit_pair_elect(&empty[stage]);       // timing experiment: no MMAs (wrong results)
+#else
+                        mma_stage_pair<KIND>(d, sw128_desc(a0), sw128_desc(b0), Tr::IDESC, kb != 0,
+                                             tmem_base + Tr::SF_COL, &empty[stage]);
+#endif
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
 #pragma unroll
                     for (int kk = 0; kk < BK / 32; ++kk) {
                         const uint64_t ad = sw128_desc(a0 + kk * 32), bd = sw128_desc(b0 + kk * 32);
@@ -393,9 +477,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     if constexpr (CG == 1) tc_commit(&empty[stage]); else tc_commit_pair(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                if constexpr (CG == 1) tc_commit(&tfull[acc]); else tc_commit_pair(&tfull[acc]);
+                if constexpr (CG == 1) tc_commit(&tfull[acc]); else tc_commit_pair_elect(&tfull[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
+            if (lane == 0) TC_PROF_PRINT("mma(tempty,full)", clock64() - pst, pw0, pw1);
         }
     } else if (warp == 3) {
         if (P.xrow) {
@@ -404,6 +489,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             // [row][XSTRIDE] buffer; the copies complete the buffer's mbarrier =====
             int xb = 0;
             uint32_t xph = 0;
+            long long pw0 = 0, pw1 = 0;
+            const long long pst = clock64();
             for (int64_t t = t0; t < P.n_tiles; t += tstep) {
                 const TcTile tl = P.tiles[t];
                 const int64_t rbase = P.shard_base[tl.s];
@@ -417,7 +504,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     const int64_t row = (int64_t)tl.I * BMT + (int64_t)crank * BM + u * 32 + lane;
                     src[u] = (row < w && P.xrow[rbase + row].x) ? P.E + P.ebase[tl.s] + row * wp + col0 : P.zero;
                 }
-                mbar_wait(&xempty[xb], xph ^ 1);
+                TC_TW(pw0, mbar_wait(&xempty[xb], xph ^ 1));
                 if (lane == 0) mbar_expect_tx(&xfull[xb], (uint32_t)BM * nbytes);
                 __syncwarp();
                 uint8_t *xd = xbuf + xb * Tr::XBUF_BYTES;
@@ -425,6 +512,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                 for (int u = 0; u < 4; ++u) bulk_g2s(xd + (u * 32 + lane) * Tr::XSTRIDE, src[u], nbytes, &xfull[xb]);
                 if (++xb == Tr::XBUFS) { xb = 0; xph ^= 1; }
             }
+            if (lane == 0) TC_PROF_PRINT("stage(xempty)", clock64() - pst, pw0, pw1);
         }
     } else if (warp >= 4) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REG_EPILOGUE));
@@ -446,6 +534,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         cur.tl = t0 < P.n_tiles ? P.tiles[t0] : tnone;
         nxt.tl = t0 + tstep < P.n_tiles ? P.tiles[t0 + tstep] : tnone;
         epi_pre_rows<BN, BMT>(P, cur, crank, quarter, lane, e);
+        long long pw0 = 0, pw1 = 0, pw2 = 0;
+        const long long pst = clock64();
         for (int64_t t = t0; t < P.n_tiles; t += tstep) {
             const TcTile tl = cur.tl;
             const TcTile tl2 = t + 2 * tstep < P.n_tiles ? P.tiles[t + 2 * tstep] : tnone;
@@ -454,9 +544,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             const int64_t w = P.shard_base[tl.s + 1] - rbase;
             const int64_t col0 = (int64_t)tl.J * BN, row0 = (int64_t)tl.I * BMT + (int64_t)crank * BM;
 #if !SAD_TC_NOBAR
-            epi_bar();                            // previous tile's colinfo / colsum / rowpart consumed
+            TC_TW(pw1, epi_bar());                // previous tile's colinfo / colsum / rowpart consumed
             if (e < BN) colinfo[e] = cur.ci;
-            epi_bar();
+            TC_TW(pw1, epi_bar());
 #endif
             const int64_t row = row0 + quarter * 32 + lane;
             const bool vrow = row < w;
@@ -467,11 +557,22 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             uint16_t *simr = (P.sim && vrow) ? P.sim + P.sim_base[tl.s] : nullptr;
             // K6: this tile's excess bytes of this row, staged by warp 3
             const uint8_t *xrow_s = xbuf + xb * Tr::XBUF_BYTES + (quarter * 32 + lane) * Tr::XSTRIDE;
-            if (P.xrow) mbar_wait(&xfull[xb], xph);
-            mbar_wait(&tfull[acc], acc_phase);
+            if (P.xrow) TC_TW(pw2, mbar_wait(&xfull[xb], xph));
+            TC_TW(pw0, mbar_wait(&tfull[acc], acc_phase));
             tc_fence_after();
             unsigned long long rowsum = 0;
             const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * ACC_COLS);
+#ifdef SAD_TC_DBG_SPIN
+            {   // timing experiment: SAD_TC_DBG_SPIN iterations of 4 independent integer chains per thread
+                uint32_t a0 = lane, a1 = lane + 1, a2 = lane + 2, a3 = lane + 3;
+#pragma unroll 4
+                for (int i = 0; i < SAD_TC_DBG_SPIN; ++i) {
+                    a0 = a0 * 0x9E3779B1u + 7u; a1 = a1 * 0x85EBCA77u + 5u;
+                    a2 = a2 * 0xC2B2AE3Du + 3u; a3 = a3 * 0x27D4EB2Fu + 1u;
+                }
+                if ((a0 ^ a1 ^ a2 ^ a3) == 0x12345u) rowsum += 1;
+            }
+#endif
 #pragma unroll 1
 #ifdef SAD_TC_DBG_NOEPI
             for (int ch = ch0; ch < ch0; ++ch) {     // timing experiment: no epilogue work (wrong results)
@@ -512,7 +613,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     for (int j = 0; j < 16; ++j) {
                         // length order: every column of a tile strictly above the diagonal is at
                         // least as long as the row, so the pair's denominator is the row's
+#ifdef SAD_TC_DBG_NOFQ
+                        const uint64_t q = v[j];    // timing experiment: no fixed point (wrong results)
+#else
                         const uint64_t q = fixed_q_nd(v[j], ri.tw, nd, ri.qd, ri.rp);
+#endif
                         rowsum += q;
                         cv[j] = q;
                     }
@@ -595,7 +700,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             if (vrow && rowsum) atomicAdd(&P.T[rbase + ri.shard], rowsum);       // .shard: local index
 #else
             if (grp) rowpart[(grp - 1) * 128 + quarter * 32 + lane] = rowsum;
-            epi_bar();
+            TC_TW(pw1, epi_bar());
             if (grp == 0) {
                 rowsum += rowpart[quarter * 32 + lane] + rowpart[128 + quarter * 32 + lane];
                 if (vrow && rowsum) atomicAdd(&P.T[rbase + ri.shard], rowsum);   // .shard: local index
@@ -608,6 +713,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
 #endif
             cur = nxt;
             nxt.tl = tl2;
+        }
+        if (lane == 0 && (warp == 4 || warp == 15)) {
+            TC_PROF_PRINT(warp == 4 ? "epi4(tfull,bar)" : "epi15(tfull,bar)", clock64() - pst, pw0, pw1);
+            TC_PROF_PRINT(warp == 4 ? "epi4(xfull)" : "epi15(xfull)", 0, pw2, 0);
         }
     }
     tc_fence_before();
