@@ -303,6 +303,14 @@ def main():
                 "frac": None, "traffic": None,
                 "peak_source": "148 SMs x 128 int32 lanes x sm_max_mhz (DESIGN.md §5)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    if args.kernel in ("tc", "tc1", "tcfull"):
+        # the same fraction against the other admissible denominators, for context: MEASURED_PEAKS.json's
+        # bf16 burst x the nominal fp4:bf16 ratio (9 : 2.25), and the nominal dense fp4 figure
+        bf16 = peaks.get("bf16_tflops")
+        if bf16:
+            roof["peak_bf16x4"] = 4.0 * bf16
+            roof["frac_bf16x4"] = roof["achieved"] / roof["peak_bf16x4"]
+        roof["frac_nominal_fp4_9000"] = roof["achieved"] / 9000.0
     roof["kernel_ms"] = ap_ms
     roof["operand_build_ms"] = op_ms
 

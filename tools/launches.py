@@ -18,10 +18,12 @@ def main(path, steps):
         tot[name] += v
         cnt[name] += 1
     allms = sum(tot.values())
+    if steps <= 0:   # auto: one all-pairs launch per step
+        steps = float(max(c for k, c in cnt.items() if "syrk" in k or "allpairs" in k))
     print(f"{len(rows) - hi - 1} launches, {allms / steps:.3f} ms of kernel time per step ({steps} steps)")
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         print(f"{v / steps:9.4f} ms/step {cnt[k] / steps:5.1f} launches/step {100 * v / allms:5.1f}%  {k}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 1.0)
+    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 0.0)
