@@ -14,9 +14,10 @@ namespace sad {
 __constant__ char c_alpha[2][24] = {"ACDEFGHIKLMNPQRSTVWY", "ACGT"};
 
 // K1+K2. One warp per sequence (persistent warps over contiguous runs of sequences, no block
-// barriers), each with its own shared-memory histogram of u8 bins (four per u32 word; a sequence
-// with a k-mer seen 256+ times is recounted with u16 bins over each half of the k-mers, which
-// cannot carry since L-k+1 <= 65535) and a staging buffer of residue codes.
+// barriers), each with its own shared-memory histogram of narrow bins (kBinBits = 4: eight per u32
+// word, so that 32 warps fit an SM; a sequence with a k-mer seen 2^kBinBits - 1 or more times is
+// recounted with u16 bins over 1/kWidePasses of the k-mers at a time, which cannot carry since
+// L-k+1 <= 65535) and a staging buffer of residue codes.
 // Pass 1 validates every residue (K1) and counts every window tau = sum_m c_m A^(k-1-m) (K2).
 // Pass 2 revisits the windows: the first lane to clear a bin with atomicAnd receives its count
 // and emits the distinct entry (tau << 16 | count), so the histogram is left zeroed for the next
@@ -25,8 +26,21 @@ __constant__ char c_alpha[2][24] = {"ACDEFGHIKLMNPQRSTVWY", "ACGT"};
 // entries with count >= 2 come first (warp-aggregated appends from the front, count-1 entries
 // from the back, then the gap is closed), so the K6 consumers read only those. Sequences longer
 // than the staging buffer are processed in segments of windows.
-constexpr int kProfWarps = 10;
+#ifndef SAD_PROF_BINBITS
+#define SAD_PROF_BINBITS 8               // bin width of the k-mer histogram (4 or 8 bits)
+#endif
+#ifndef SAD_PROF_WARPS
+#define SAD_PROF_WARPS 10
+#endif
+#ifndef SAD_PROF_MINB
+#define SAD_PROF_MINB 2                  // blocks per SM the register budget is sized for
+#endif
+constexpr int kProfWarps = SAD_PROF_WARPS;
+constexpr int kBinBits = SAD_PROF_BINBITS, kBinsPerWord = 32 / kBinBits;
+constexpr uint32_t kBinMax = (1u << kBinBits) - 1u;
+constexpr int kWidePasses = 16 / kBinBits;   // overflow fallback: u16 bins over 1/kWidePasses of the k-mers
 constexpr int kCodeSeg = 2048;           // residue codes staged per warp
+constexpr int kCodeBuf = kCodeSeg + 32;  // staged bytes keep the residues' 16-byte alignment (shift <= 15)
 
 template <int KT>
 __device__ __forceinline__ uint32_t window_tau(const uint8_t *c, int k, uint32_t A) {
@@ -41,7 +55,7 @@ __device__ __forceinline__ uint32_t window_tau(const uint8_t *c, int k, uint32_t
 }
 
 template <int KT>
-__global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int warps, int hbytes) {
+__global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(ProfileArgs a, int warps, int hbytes) {
     extern __shared__ __align__(16) uint32_t psm[];
     __shared__ uint8_t lut[256];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -50,23 +64,38 @@ __global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int 
     if (threadIdx.x < a.A) lut[(uint8_t)c_alpha[a.alphabet][threadIdx.x]] = (uint8_t)threadIdx.x;
     __syncthreads();
     if (wid >= warps) return;
-    const int hw = hbytes / 4;                  // histogram words (V bytes, rounded up to 16)
-    uint32_t *hist = psm + (size_t)wid * (hw + kCodeSeg / 4);
+    const int hw = hbytes / 4;                  // histogram words (V bins, rounded up to 16 bytes)
+    const int VW = (a.V + 31) / 32;             // presence words (one bit per k-mer)
+    uint32_t *hist = psm + (size_t)wid * (hw + kCodeBuf / 4 + ((VW + 3) & ~3));   // 16-byte aligned slices
     uint8_t *cod = reinterpret_cast<uint8_t *>(hist + hw);
+    uint32_t *pres = hist + hw + kCodeBuf / 4;  // k-mers seen by this warp in the current shard
     for (int t = lane; t < hw; t += 32) hist[t] = 0;
+    for (int t = lane; t < VW; t += 32) pres[t] = 0;
     __syncwarp();
 
     const int k = KT > 0 ? KT : a.k;
     const uint32_t A = (uint32_t)a.A;
     const int V = a.V;
-    const uint32_t Vh = (uint32_t)(V + 1) / 2;  // u16 fallback: bins of half the k-mers per sub-pass
+    const uint32_t Vh = (uint32_t)(V + kWidePasses - 1) / kWidePasses;   // u16 fallback: k-mers per sub-pass
     const int64_t W = (int64_t)gridDim.x * warps, gw = (int64_t)blockIdx.x * warps + wid;
-    const int64_t i0 = gw * a.n / W, i1 = (gw + 1) * a.n / W;
+    const int64_t nr = a.i_end - a.i_begin;
+    const int64_t i0 = a.i_begin + gw * nr / W, i1 = a.i_begin + (gw + 1) * nr / W;
     int s = 0;
     while (s + 1 < a.pl && i0 >= a.shard_base[s + 1]) ++s;
     unsigned long long acc_w = 0, acc_d = 0;
     uint32_t exm[kNumCaps] = {};
     auto flush = [&]() {
+        // M(tau) >= 1 for every k-mer present: the warp's presence bits, OR-ed once per word
+        // (counts >= 2 update M itself); k_kstats folds the bits into M
+        __syncwarp();
+        for (int t = lane; t < VW; t += 32) {
+            const uint32_t b = pres[t];
+            if (b) {
+                atomicOr(&a.Mb[(size_t)s * VW + t], b);
+                pres[t] = 0;
+            }
+        }
+        __syncwarp();
         if (lane == 0) {
             if (acc_w | acc_d) {
                 atomicAdd(&a.kinfo[s * kKinfo + 0], acc_w);
@@ -114,58 +143,116 @@ __global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int 
         }
         const int nseg = (int)((Tw + SW - 1) / SW);
         int staged = -1, checked = -1;          // segment now in `cod`, last segment validated (K1)
+        int sh = 0;                             // cod[sh + t - r0] = code of residue t of the staged segment
         // stage the codes of segment g: residues [g SW, min(L, (g + 1) SW + k - 1)), validated (K1) the
-        // first time (16-byte aligned vector loads: the residue buffer is padded by 16 bytes past its end)
+        // first time. Each lane translates one 16-byte aligned vector at a time and stores the 16 codes
+        // with one 16-byte store at the vector's own alignment (bytes outside the segment are never read
+        // as codes); a residue outside the alphabet (bit 7 of its LUT entry) takes the rare per-byte path.
         auto stage = [&](int g) {
             if (g == staged) return;
             const bool check = g > checked;
             const int64_t r0 = (int64_t)g * SW, r1 = min(L, r0 + SW + k - 1);
             const int64_t b0 = (off0 + r0) & ~int64_t(15), b1 = off0 + r1;
+            sh = (int)(off0 + r0 - b0);
+            const int nb = (int)(b1 - b0);      // staged bytes (<= kCodeSeg + 15)
             __syncwarp();
-            for (int64_t b = b0 + 16 * lane; b < b1; b += 512) {
-                const uint4 q = (g == 0 && b < b0 + 512) ? qfirst : *reinterpret_cast<const uint4 *>(a.ascii + b);
+            for (int u = 16 * lane; u < nb; u += 512) {
+                const uint4 q = (g == 0 && u < 512) ? qfirst : *reinterpret_cast<const uint4 *>(a.ascii + b0 + u);
                 const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+                uint32_t cw[4];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int64_t t = b + j - off0;          // residue position in the sequence
-                    if (t >= r0 && t < r1) {
-                        uint32_t c = lut[(qw[j >> 2] >> (8 * (j & 3))) & 0xFFu];
-                        if (c == 255) {
-                            if (check) atomicMin(&a.err[0], (gidx << 32) | (unsigned long long)t);
-                            c = 0;
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t c0 = lut[qw[i] & 0xFFu], c1 = lut[(qw[i] >> 8) & 0xFFu];
+                    const uint32_t c2 = lut[(qw[i] >> 16) & 0xFFu], c3 = lut[qw[i] >> 24];
+                    cw[i] = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+                }
+                // bytes [lo, hi) of this vector belong to the segment
+                const int lo = max(0, sh - u), hi = min(16, nb - u);
+                uint32_t bad = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int l = min(max(lo - 4 * i, 0), 4), h = min(max(hi - 4 * i, 0), 4);
+                    const uint32_t m = h > l ? ((0xFFFFFFFFu >> (32 - 8 * (h - l))) << (8 * l)) : 0u;
+                    bad |= cw[i] & m & 0x80808080u;
+                }
+                if (bad) {                                   // rare: report the first bad residue, code it 0
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t c = (cw[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+                        if (j >= lo && j < hi && c == 255u) {
+                            if (check) atomicMin(&a.err[0], (gidx << 32) | (unsigned long long)(b0 + u + j - off0));
+                            cw[j >> 2] &= ~(0xFFu << (8 * (j & 3)));
                         }
-                        cod[t - r0] = (uint8_t)c;
                     }
                 }
+                *reinterpret_cast<uint4 *>(cod + u) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
             }
             __syncwarp();
             staged = g;
             checked = max(checked, g);
         };
-        // pass 1: count every window (overlaps included). Normally u8 bins (V bytes); a bin that
-        // would pass 255 (the add carries into its neighbour) sends the sequence to the fallback:
-        // clear the bins and count with u16 bins over each half of the k-mers in turn.
-        auto count = [&](int bits, uint32_t lo, uint32_t hi) -> bool {
+        // pass 1: count every window (overlaps included). Normally narrow bins; a bin that reaches
+        // its maximum (the next add could carry into its neighbour) sends the sequence to the
+        // fallback: clear the bins and count with u16 bins over each part of the k-mers in turn. With `lst`,
+        // the first window of every k-mer (its bin was 0) appends the k-mer to the owner list.
+        int nl = 0;
+        auto count = [&](int bits, uint32_t lo, uint32_t hi, uint16_t *lst) -> bool {
             bool ovf = false;
             for (int g = 0; g < nseg; ++g) {
                 stage(g);
                 const int w1 = (int)min((int64_t)SW, Tw - (int64_t)g * SW);
-                for (int t = lane; t < w1; t += 32) {
-                    const uint32_t tau = window_tau<KT>(cod + t, k, A);
-                    if (tau < lo || tau >= hi) continue;
-                    const uint32_t idx = tau - lo;
-                    const uint32_t sh = bits == 8 ? 8u * (idx & 3u) : 16u * (idx & 1u);
-                    const uint32_t old = atomicAdd(&hist[bits == 8 ? idx >> 2 : idx >> 1], 1u << sh);
-                    if (bits == 8 && ((old >> sh) & 0xFFu) == 0xFFu) ovf = true;
+                for (int t0 = 0; t0 < w1; t0 += 32) {
+                    const int t = t0 + lane;
+                    bool first = false;
+                    uint32_t tau = 0;
+                    if (t < w1) {
+                        tau = window_tau<KT>(cod + sh + t, k, A);
+                        if (tau >= lo && tau < hi) {
+                            const uint32_t idx = tau - lo;
+                            const bool nb = bits != 16;
+                            const uint32_t sh8 = nb ? kBinBits * (idx % kBinsPerWord) : 16u * (idx & 1u);
+                            const uint32_t old = atomicAdd(&hist[nb ? idx / kBinsPerWord : idx >> 1], 1u << sh8);
+                            const uint32_t ob = (old >> sh8) & (nb ? kBinMax : 0xFFFFu);
+                            if (nb && ob == kBinMax) ovf = true;
+                            first = ob == 0;
+                        }
+                    }
+                    if (lst) {
+                        const uint32_t fm = __ballot_sync(0xffffffffu, first);
+                        if (first) lst[nl + __popc(fm & ((1u << lane) - 1u))] = (uint16_t)tau;
+                        nl += __popc(fm);
+                    }
                 }
             }
             __syncwarp();
             return __any_sync(0xffffffffu, ovf);
         };
-        // pass 2: claim every bin once, emit (tau, count), update the shard's column maxima
+        // pass 2: every k-mer once, emit (tau, count), update the shard's column maxima
         uint32_t *out = a.csr + (off0 - i * (int64_t)(k - 1));
         uint32_t *Ms = a.M + (size_t)s * V;
         uint32_t n_hi = 0, n_lo = 0, ex[kNumCaps] = {};
+        int64_t bk = Tw;                                  // count-1 entries fill [.., bk) from the back
+        auto emit = [&](uint32_t c, uint32_t tau) {       // warp-uniform call; c = 0: nothing
+            const uint32_t mh = __ballot_sync(0xffffffffu, c >= 2), ml = __ballot_sync(0xffffffffu, c == 1);
+            const uint32_t lt = (1u << lane) - 1u;
+            if (c >= 2) out[n_hi + __popc(mh & lt)] = (tau << 16) | c;
+            else if (c == 1) out[bk - 1 - (n_lo + __popc(ml & lt))] = (tau << 16) | 1u;
+            n_hi += __popc(mh);
+            n_lo += __popc(ml);
+            if (c) {
+                atomicOr(&pres[tau >> 5], 1u << (tau & 31));
+                if (c >= 2) {                          // excess beyond the layer caps 1, 2, 4, 8
+                    atomicMax(&Ms[tau], c);
+#pragma unroll
+                    for (int j = 0; j < kNumCaps; ++j)
+                        if (c > (1u << j)) {
+                            ex[j] += c - (1u << j);
+                            atomicAdd(&a.Xc[((size_t)s * kNumCaps + j) * V + tau], 1u);
+                        }
+                }
+            }
+        };
+        // claim by windows: every bin taken once by atomicAnd (the bins end cleared)
         auto claim = [&](int bits, uint32_t lo, uint32_t hi) {
             for (int gg = 0; gg < nseg; ++gg) {
                 const int g = nseg - 1 - gg;                   // the last staged segment first
@@ -175,52 +262,58 @@ __global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int 
                     const int t = t0 + lane;
                     uint32_t c = 0, tau = 0;
                     if (t < w1) {
-                        tau = window_tau<KT>(cod + t, k, A);
+                        tau = window_tau<KT>(cod + sh + t, k, A);
                         if (tau >= lo && tau < hi) {
                             const uint32_t idx = tau - lo;
-                            const uint32_t sh = bits == 8 ? 8u * (idx & 3u) : 16u * (idx & 1u);
-                            const uint32_t mask = (bits == 8 ? 0xFFu : 0xFFFFu) << sh;
-                            const uint32_t old = atomicAnd(&hist[bits == 8 ? idx >> 2 : idx >> 1], ~mask);
-                            c = (old & mask) >> sh;
+                            const bool nb = bits != 16;
+                            const uint32_t sh8 = nb ? kBinBits * (idx % kBinsPerWord) : 16u * (idx & 1u);
+                            const uint32_t mask = (nb ? kBinMax : 0xFFFFu) << sh8;
+                            const uint32_t old = atomicAnd(&hist[nb ? idx / kBinsPerWord : idx >> 1], ~mask);
+                            c = (old & mask) >> sh8;
                         }
                     }
-                    const uint32_t mh = __ballot_sync(0xffffffffu, c >= 2), ml = __ballot_sync(0xffffffffu, c == 1);
-                    const uint32_t lt = (1u << lane) - 1u;
-                    if (c >= 2) out[n_hi + __popc(mh & lt)] = (tau << 16) | c;
-                    else if (c == 1) out[Tw - 1 - (n_lo + __popc(ml & lt))] = (tau << 16) | 1u;
-                    n_hi += __popc(mh);
-                    n_lo += __popc(ml);
-                    if (c) {
-                        atomicMax(&Ms[tau], c);
-                        if (c >= 2) {                          // excess beyond the layer caps 1, 2, 4, 8
-#pragma unroll
-                            for (int j = 0; j < kNumCaps; ++j)
-                                if (c > (1u << j)) {
-                                    ex[j] += c - (1u << j);
-                                    atomicAdd(&a.Xc[((size_t)s * kNumCaps + j) * V + tau], 1u);
-                                }
-                        }
-                    }
+                    emit(c, tau);
                 }
             }
             __syncwarp();
         };
-        if (!count(8, 0u, (uint32_t)V)) {
-            claim(8, 0u, (uint32_t)V);
+        // one-segment sequences keep the owner list in the staging buffer past the codes (a k-mer
+        // list is at most Tw entries); the emission then walks d owners instead of Tw windows
+        stage(0);
+        const int lofs = (sh + (int)min(L, (int64_t)kCodeSeg) + 15) & ~15;
+        uint16_t *lst = (nseg == 1 && (kCodeBuf - lofs) / 2 >= Tw) ? reinterpret_cast<uint16_t *>(cod + lofs) : nullptr;
+        if (!count(kBinBits, 0u, (uint32_t)V, lst)) {
+            if (lst) {
+                bk = nl;                               // d is known: the two groups meet exactly
+                for (int e0 = 0; e0 < nl; e0 += 32) {
+                    const int e = e0 + lane;
+                    uint32_t c = 0, tau = 0;
+                    if (e < nl) {
+                        tau = lst[e];
+                        c = (hist[tau / kBinsPerWord] >> (kBinBits * (tau % kBinsPerWord))) & kBinMax;
+                    }
+                    emit(c, tau);
+                }
+                __syncwarp();
+                for (int t = lane; t < hw / 4; t += 32) reinterpret_cast<uint4 *>(hist)[t] = make_uint4(0, 0, 0, 0);
+                __syncwarp();
+            } else {
+                claim(kBinBits, 0u, (uint32_t)V);
+            }
         } else {
             for (int t = lane; t < hw; t += 32) hist[t] = 0;
             __syncwarp();
-            for (uint32_t h = 0; h < 2; ++h) {
+            for (uint32_t h = 0; h < (uint32_t)kWidePasses; ++h) {
                 const uint32_t lo = h * Vh, hi = min((uint32_t)V, lo + Vh);
-                count(16, lo, hi);
+                count(16, lo, hi, nullptr);
                 claim(16, lo, hi);
             }
         }
         // close the gap: [0, n_hi) count >= 2 (the K6 candidates), then [n_hi, d) count 1. Only the
         // count-1 entries at [max(d, Tw - n_lo), Tw) move, into the gap [n_hi, Tw - n_lo) (disjoint).
         {
-            const int64_t d = (int64_t)n_hi + n_lo, src0 = d > Tw - n_lo ? d : Tw - n_lo;
-            for (int64_t t = lane; t < Tw - src0; t += 32) out[n_hi + t] = out[src0 + t];
+            const int64_t d = (int64_t)n_hi + n_lo, src0 = d > bk - n_lo ? d : bk - n_lo;
+            for (int64_t t = lane; t < bk - src0; t += 32) out[n_hi + t] = out[src0 + t];
         }
 #pragma unroll
         for (int j = 0; j < kNumCaps; ++j) {
@@ -242,9 +335,12 @@ __global__ void __launch_bounds__(kProfWarps * 32) k_profile(ProfileArgs a, int 
 }
 
 void launch_profile(const ProfileArgs &a, cudaStream_t st) {
-    const int hbytes = (a.V + 15) / 16 * 16;     // u8 bins (or u16 bins over half the k-mers)
-    const size_t per_warp = (size_t)hbytes + kCodeSeg;
-    const int warps = (int)std::max<size_t>(1, std::min<size_t>(kProfWarps, (size_t)(100 * 1024) / per_warp));
+    // V narrow bins, or u16 bins over 1/kWidePasses of the k-mers (the overflow fallback)
+    const int narrow = (int)(((int64_t)a.V * kBinBits + 7) / 8);
+    const int wide = 2 * ((a.V + kWidePasses - 1) / kWidePasses);
+    const int hbytes = (std::max(narrow, wide) + 15) / 16 * 16;
+    const size_t per_warp = (size_t)hbytes + kCodeBuf + 4 * (size_t)((((a.V + 31) / 32) + 3) & ~3);
+    const int warps = (int)std::max<size_t>(1, std::min<size_t>(kProfWarps, (size_t)(220 * 1024 / SAD_PROF_MINB) / per_warp));
     const size_t smem = per_warp * warps;
     auto kern = a.k == 3 ? k_profile<3> : a.k == 6 ? k_profile<6> : k_profile<0>;
     static bool configured = false;
@@ -260,7 +356,7 @@ void launch_profile(const ProfileArgs &a, cudaStream_t st) {
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kProfWarps * 32, smem);
     int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-    grid = std::min<int64_t>(grid, (a.n + warps - 1) / warps);
+    grid = std::min<int64_t>(grid, (a.i_end - a.i_begin + warps - 1) / warps);
     if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, kProfWarps * 32, smem, st>>>(a, warps, hbytes);
 }
@@ -353,18 +449,23 @@ void launch_capscan(const uint32_t *in, int64_t in_stride, const uint32_t *sel, 
 //   K_s(T) = sum_tau min(M(tau), T)                        -> kinfo[s][2] (no cap), [8 + j]
 //   sum_tau C(X_T(tau), 2), X_T(tau) = #{i : n_i(tau) > T}  -> kinfo[s][12 + j] (bound of K6 pairs)
 //   sum_tau X_T(tau)                                       -> kinfo[s][16 + j] (K6 list entries)
-__global__ void __launch_bounds__(kScanThreads) k_kstats(const uint32_t *M, const uint32_t *Xc,
+__global__ void __launch_bounds__(kScanThreads) k_kstats(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc,
                                                          unsigned long long *kinfo, int V) {
     constexpr int NV = 3 * kNumCaps + 1;
     __shared__ unsigned long long red[NV];
     const int s = blockIdx.y;                 // blocks of k-mers x shards (kinfo zeroed by the caller)
     if (threadIdx.x < NV) red[threadIdx.x] = 0;
     __syncthreads();
-    const uint32_t *m = M + (size_t)s * V;
+    uint32_t *m = M + (size_t)s * V;
     const uint32_t *xc = Xc + (size_t)s * kNumCaps * V;
     unsigned long long acc[NV] = {};
+    const uint32_t *mb = Mb + (size_t)s * ((V + 31) / 32);
     for (int t = blockIdx.x * kScanThreads + threadIdx.x; t < V; t += gridDim.x * kScanThreads) {
-        const uint32_t x = m[t];
+        uint32_t x = m[t];
+        if (x == 0 && ((mb[t >> 5] >> (t & 31)) & 1u)) {   // present once at most per sequence: M = 1
+            x = 1;
+            m[t] = 1;
+        }
         acc[kNumCaps] += x;
 #pragma unroll
         for (int j = 0; j < kNumCaps; ++j) {
@@ -392,9 +493,10 @@ __global__ void __launch_bounds__(kScanThreads) k_kstats(const uint32_t *M, cons
     }
 }
 
-void launch_kstats(const uint32_t *M, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V, cudaStream_t st) {
+void launch_kstats(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,
+                   cudaStream_t st) {
     const int bx = std::max(1, std::min(16, V / 512));
-    k_kstats<<<dim3(bx, pl), kScanThreads, 0, st>>>(M, Xc, kinfo, V);
+    k_kstats<<<dim3(bx, pl), kScanThreads, 0, st>>>(M, Mb, Xc, kinfo, V);
 }
 
 __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl, int64_t r) {

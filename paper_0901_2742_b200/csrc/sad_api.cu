@@ -118,6 +118,7 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_sigma_inv = b.take<int32_t>((size_t)n);
     c->d_rinfo_s = b.take<RowInfo>((size_t)n);
     c->d_M = b.take<uint32_t>((size_t)pl * V);
+    c->d_Mb = b.take<uint32_t>((size_t)pl * ((V + 31) / 32));
     c->d_col0 = b.take<uint32_t>((size_t)pl * V);
     c->d_err = b.take<unsigned long long>(4);
     c->d_kinfo = b.take<unsigned long long>((size_t)pl * kKinfo);
@@ -270,7 +271,12 @@ int sad_create(const sad_config *cfg, sad_ctx **out) {
     }
     if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        [&] {
+            for (auto &e : ctx->ev_chunk)
+                if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return true;
+            return false;
+        }()) {
         cudaFreeHost(ctx->h_small);
         delete ctx;
         return SAD_E_CUDA;
@@ -297,6 +303,8 @@ void sad_destroy(sad_ctx *ctx) {
     }
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    for (auto &e : ctx->ev_chunk)
+        if (e) cudaEventDestroy(e);
     if (ctx->h_small) cudaFreeHost(ctx->h_small);
     if (ctx->h_tiles) cudaFreeHost(ctx->h_tiles);
     delete ctx;
@@ -321,6 +329,9 @@ int sad_workspace_size(const sad_ctx *cctx, int64_t n_local, int64_t residues_lo
     *bytes = carve(&tmp, nullptr, n_local, residues_local);
     return SAD_OK;
 }
+
+static int profile_reset(sad_ctx *ctx);
+static int profile_launch(sad_ctx *ctx, int64_t i0, int64_t i1);
 
 int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t n_local, int64_t first_source_index,
              int64_t n_global, int64_t residues_local, int32_t mem, void *d_ws, size_t ws_bytes) {
@@ -378,7 +389,16 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
     }
     ctx->rows_pad = ctx->shard_rowpad[ctx->pl];
     const cudaMemcpyKind kind = mem == SAD_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-    if (R > 0) CK(cudaMemcpyAsync(ctx->d_ascii, ascii, (size_t)R, kind, ctx->st));
+    // host inputs of a few MB or more: the residues are copied in chunks on the internal stream and
+    // each chunk's k-mer counts (K1/K2) start on ctx->st as soon as it has landed (below)
+    static const int nch_env = [] {        // SAD_LOAD_CHUNKS=0 disables the pipeline (experiments)
+        const char *e = getenv("SAD_LOAD_CHUNKS");
+        return e ? std::max(0, std::min(atoi(e), (int)sad_ctx::kLoadChunks)) : 4;
+    }();
+    const int nch = nch_env;
+    const bool pipelined = nch > 0 && mem == SAD_MEM_HOST && R >= (int64_t(4) << 20) && n_local >= 64 * nch;
+    ctx->profiled = false;
+    if (R > 0 && !pipelined) CK(cudaMemcpyAsync(ctx->d_ascii, ascii, (size_t)R, kind, ctx->st));
     if (mem == SAD_MEM_DEVICE_REBASE) {
         launch_rebase(offsets, n_local + 1, ctx->d_off, ctx->st);
         LAUNCHED();
@@ -439,19 +459,42 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
         ctx->tbl_first = first_source_index;
         need_sync = true;
     }
+    ctx->launches_step = 0;
+    if (pipelined) {
+        if (int rc = profile_reset(ctx)) return rc;
+        // the previous step's readers of d_ascii (on ctx->st) finish before the first chunk lands
+        CK(cudaEventRecord(ctx->ev_fork, ctx->st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        for (int c = 0; c < nch; ++c) {
+            const int64_t i0 = n_local * c / nch, i1 = n_local * (c + 1) / nch;
+            const int64_t b0 = offsets[i0], b1 = offsets[i1];
+            if (b1 > b0)
+                CK(cudaMemcpyAsync(ctx->d_ascii + b0, ascii + b0, (size_t)(b1 - b0), cudaMemcpyHostToDevice, ctx->side));
+            CK(cudaEventRecord(ctx->ev_chunk[c], ctx->side));
+            CK(cudaStreamWaitEvent(ctx->st, ctx->ev_chunk[c], 0));
+            if (int rc = profile_launch(ctx, i0, i1)) return rc;
+        }
+        ctx->profiled = true;
+    }
     if (need_sync) CK(cudaStreamSynchronize(ctx->st));
     ctx->stage = 1;
-    ctx->launches_step = 0;
     return SAD_OK;
 }
 
-int sad_build_profiles(sad_ctx *ctx) {
-    GUARD(1);
+// K1/K2 accumulators cleared, on ctx->st
+static int profile_reset(sad_ctx *ctx) {
     const int pl = ctx->pl, V = ctx->V;
     CK(cudaMemsetAsync(ctx->d_M, 0, sizeof(uint32_t) * (size_t)pl * V, ctx->st));
+    CK(cudaMemsetAsync(ctx->d_Mb, 0, sizeof(uint32_t) * (size_t)pl * ((V + 31) / 32), ctx->st));
     CK(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long) * 4, ctx->st));
     CK(cudaMemsetAsync(ctx->d_kinfo, 0, sizeof(unsigned long long) * kKinfo * (size_t)pl, ctx->st));
     CK(cudaMemsetAsync(ctx->d_Xc, 0, sizeof(uint32_t) * kNumCaps * (size_t)pl * V, ctx->st));
+    return SAD_OK;
+}
+
+// K1/K2 over sequences [i0, i1), on ctx->st
+static int profile_launch(sad_ctx *ctx, int64_t i0, int64_t i1) {
+    const int pl = ctx->pl, V = ctx->V;
     ProfileArgs a{};
     a.ascii = ctx->d_ascii;
     a.off = ctx->d_off;
@@ -470,10 +513,24 @@ int sad_build_profiles(sad_ctx *ctx) {
     a.err = ctx->d_err;
     a.kinfo = ctx->d_kinfo;
     a.Xc = ctx->d_Xc;
+    a.Mb = ctx->d_Mb;
     a.nhi = ctx->d_nhi;
+    a.i_begin = i0;
+    a.i_end = i1;
     launch_profile(a, ctx->st);
     LAUNCHED();
-    launch_kstats(ctx->d_M, ctx->d_Xc, ctx->d_kinfo, pl, V, ctx->st);
+    return SAD_OK;
+}
+
+int sad_build_profiles(sad_ctx *ctx) {
+    GUARD(1);
+    const int pl = ctx->pl, V = ctx->V;
+    if (!ctx->profiled) {
+        if (int rc = profile_reset(ctx)) return rc;
+        if (int rc = profile_launch(ctx, 0, ctx->n)) return rc;
+    }
+    ctx->profiled = false;
+    launch_kstats(ctx->d_M, ctx->d_Mb, ctx->d_Xc, ctx->d_kinfo, pl, V, ctx->st);
     LAUNCHED();
     unsigned long long *hk = ctx->h_small + 8192;
     CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, ctx->st));

@@ -80,6 +80,7 @@ struct ProfileArgs {
     const uint8_t *ascii;
     const int64_t *off;
     int64_t n;
+    int64_t i_begin, i_end;          // the sequences this launch profiles (a chunk of [0, n))
     int64_t first_idx;
     int k, A, V, alphabet, pl;
     const int64_t *shard_base;       // device [pl+1]
@@ -90,12 +91,14 @@ struct ProfileArgs {
     unsigned long long *err;         // [4]: first bad symbol (idx<<32|pos), first short idx, first long idx, pad
     unsigned long long *kinfo;       // [pl][kKinfo] (see kKinfo)
     uint32_t *Xc;                    // [pl][kNumCaps][V]: #{i : n_i(tau) > 2^j} (zeroed)
+    uint32_t *Mb;                    // [pl][ceil(V/32)]: k-mers present in the shard (zeroed; M >= 2 goes to M)
     int32_t *nhi;                    // [n] entries with count >= 2 (they lead each CSR row)
 };
 void launch_profile(const ProfileArgs &a, cudaStream_t st);
 void launch_capscan(const uint32_t *in, int64_t in_stride, const uint32_t *sel, const uint32_t *cap, uint32_t *out,
                     unsigned long long *total_out, int total_stride, int pl, int V, cudaStream_t st);
-void launch_kstats(const uint32_t *M, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V, cudaStream_t st);
+void launch_kstats(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,
+                   cudaStream_t st);
 
 struct OperandArgs {
     const uint32_t *csr;
@@ -323,6 +326,9 @@ struct sad_ctx {
     cudaStream_t st = nullptr;
     cudaStream_t side = nullptr;     // internal stream: K6 rows run beside K4 (fork/join by events)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    static constexpr int kLoadChunks = 16;     // host loads: chunked H2D copies on `side`, each chunk's
+    cudaEvent_t ev_chunk[kLoadChunks] = {};    // k-mer counts launched on `st` as soon as it lands
+    bool profiled = false;                     // K1/K2 already launched by sad_load
     int A = 0, V = 0, pl = 0, shard0 = 0;
     int num_sms = 148;
     std::string err;
@@ -354,7 +360,7 @@ struct sad_ctx {
     int32_t *d_dcnt = nullptr, *d_nhi = nullptr;
     int32_t *d_sigma = nullptr, *d_sigma_inv = nullptr;   // length order of every shard (TC path)
     sad::RowInfo *d_rinfo_s = nullptr;                    // RowInfo in length order, .shard = local index
-    uint32_t *d_M = nullptr, *d_col0 = nullptr;
+    uint32_t *d_M = nullptr, *d_Mb = nullptr, *d_col0 = nullptr;
     unsigned long long *d_err = nullptr, *d_kinfo = nullptr;
     uint32_t *d_cap = nullptr, *d_xsel = nullptr;   // layer cap T_s and its index j_s per shard
     uint32_t *d_ident = nullptr;                    // per shard: identity column map (K4 skips col0)

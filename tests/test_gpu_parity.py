@@ -376,3 +376,38 @@ def test_bucket_guide_trees(cfg):
         got = ctx.bucket_guide_tree(b)
         assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
 
+
+
+@pytest.mark.gpu
+def test_host_load_pipelined():
+    """Host inputs of 4 MB or more are copied in chunks with each chunk's k-mer counts started
+    as it lands (sad_load): the results equal those of a device-resident load, a bad symbol in the
+    last chunk is still reported with its position, and a reused context reloads correctly."""
+    import torch
+    from paper_0901_2742_b200 import SadError
+    spec = gen.SPECS[3]
+    a, o = gen.generate(3, n=16000)
+    n = len(o) - 1
+    assert int(o[-1]) >= 4 << 20
+    ctx_h = _ctx(spec.alphabet, spec.k, 8, KERNELS[0])
+    ctx_h.load(a, o, n, 0)
+    sizes_h = ctx_h.run()
+    ctx_d = _ctx(spec.alphabet, spec.k, 8, KERNELS[0])
+    ctx_d.load(torch.from_numpy(a).cuda(), torch.from_numpy(o).cuda(), n, 0, residues=int(o[-1]))
+    sizes_d = ctx_d.run()
+    assert np.array_equal(sizes_h, sizes_d)
+    for s in range(8):
+        assert np.array_equal(ctx_h.local_rank(s), ctx_d.local_rank(s))
+    assert np.array_equal(ctx_h.out_keys().cpu().numpy(), ctx_d.out_keys().cpu().numpy())
+    # the same context again (chunk events and the profile flag reset per load)
+    ctx_h.load(a, o, n, 0)
+    assert np.array_equal(ctx_h.run(), sizes_d)
+    assert np.array_equal(ctx_h.out_keys().cpu().numpy(), ctx_d.out_keys().cpu().numpy())
+    bad = a.copy()
+    pos = int(o[n - 1]) + 5
+    bad[pos] = ord("X")
+    ctx_e = _ctx(spec.alphabet, spec.k, 8, KERNELS[0])
+    ctx_e.load(bad, o, n, 0)
+    with pytest.raises(SadError) as e:
+        ctx_e.run()
+    assert e.value.name == "SAD_E_SYMBOL" and e.value.location == (n - 1, 5)
