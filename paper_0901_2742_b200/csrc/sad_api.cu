@@ -694,7 +694,10 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
             LAUNCHED();
             int sbits = 0;
             while ((1 << sbits) < pl) ++sbits;
-            CK(sort_pairs(ctx, k_in, k_out, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n, 16 + sbits));
+            if (!(pl > 1 && ctx->max_w <= kSmallSortMax &&
+                  seg_sort_pairs(k_in, ctx->d_perm_in, ctx->d_shard_base, pl, k_out, ctx->d_perm_sorted, 16,
+                                 ctx->st) == 0))
+                CK(sort_pairs(ctx, k_in, k_out, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n, 16 + sbits));
             LAUNCHED();
             launch_lenperm(k_out, ctx->d_perm_sorted, ctx->d_rowinfo, ctx->d_shard_base, ctx->n, ctx->d_sigma,
                            ctx->d_sigma_inv, ctx->d_rinfo_s, ctx->st);
@@ -885,8 +888,11 @@ int sad_rank_global(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out
         launch_f1_gainfo(ctx->d_anc_local, ctx->pl, ctx->shard0, p, ctx->first_idx, ctx->d_ga_info, ctx->st);
         LAUNCHED();
     }
-    CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
-                  qbits + sbits));
+    if (!(ctx->pl > 1 && qbits == 32 && ctx->max_w <= kSmallSortMax &&
+          seg_sort_pairs(ctx->d_ckey, ctx->d_perm_in, ctx->d_shard_base, ctx->pl, ctx->d_ckey_sorted, ctx->d_perm_sorted,
+                         32, ctx->st) == 0))
+        CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
+                      qbits + sbits));
     LAUNCHED();
     launch_unpack_sorted(ctx->d_ckey_sorted, ctx->d_perm_sorted, ctx->n, ctx->first_idx, ctx->d_key_sorted,
                          ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, qbits, ctx->st);

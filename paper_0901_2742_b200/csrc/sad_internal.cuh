@@ -310,6 +310,11 @@ int small_sort_pairs(const uint32_t *ki, const int32_t *vi, int n, uint32_t *ko,
                      cudaStream_t st);
 int small_sort_pairs(const unsigned long long *ki, const int32_t *vi, int n, unsigned long long *ko, int32_t *vo,
                      int b0, int b1, cudaStream_t st);
+// per-segment stable sort by key bits [0, end_bit <= 32), every segment <= kSmallSortMax pairs; 0 or -1
+int seg_sort_pairs(const uint32_t *ki, const int32_t *vi, const int64_t *seg, int nseg, uint32_t *ko, int32_t *vo,
+                   int end_bit, cudaStream_t st);
+int seg_sort_pairs(const unsigned long long *ki, const int32_t *vi, const int64_t *seg, int nseg,
+                   unsigned long long *ko, int32_t *vo, int end_bit, cudaStream_t st);
 void launch_rebase(const int64_t *src, int64_t n1, int64_t *off, cudaStream_t st);
 void launch_distance(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, float *D, cudaStream_t st);
 void launch_distance64(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, double *D, cudaStream_t st);
