@@ -155,17 +155,33 @@ __global__ void __launch_bounds__(kRankThreads) k_rank_vs_ga(RankArgs a) {
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)gridDim.x * (kRankThreads / 32);
-    for (int64_t i = (int64_t)blockIdx.x * (kRankThreads / 32) + (threadIdx.x >> 5); i < a.n; i += nwarps) {
-        const uint32_t *ent = a.csr + (a.off[i] - i * (int64_t)(a.k - 1));
-        const int d = a.dcnt[i];
+    // the next sequence's CSR position and entry count are loaded during the current one, and
+    // each lane issues its entry loads four at a time (one round trip per 128 entries)
+    int64_t i = (int64_t)blockIdx.x * (kRankThreads / 32) + (threadIdx.x >> 5);
+    int64_t off_n = i < a.n ? a.off[i] : 0;
+    int d_n = i < a.n ? a.dcnt[i] : 0;
+    for (; i < a.n; i += nwarps) {
+        const uint32_t *ent = a.csr + (off_n - i * (int64_t)(a.k - 1));
+        const int d = d_n;
+        const int64_t inext = i + nwarps;
+        if (inext < a.n) {
+            off_n = a.off[inext];
+            d_n = a.dcnt[inext];
+        }
+        const RowInfo ri = a.rowinfo[i];
         uint32_t s = 0;
-        for (int e = lane; e < d; e += 32) {
-            const uint32_t v = ent[e];
-            s += min(v & 0xFFFFu, (uint32_t)ga_cnt[v >> 16]);
+        for (int e0 = 0; e0 < d; e0 += 128) {
+            uint32_t v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * 32 + lane;
+                v[u] = e < d ? ent[e] : 0u;        // (tau 0, count 0) adds nothing
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s += min(v[u] & 0xFFFFu, (uint32_t)ga_cnt[v[u] >> 16]);
         }
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) {
-            const RowInfo ri = a.rowinfo[i];
             const uint32_t den = min(ri.tw, twg);
             const uint64_t q = ri.tw <= twg ? fixed_q(s, ri.tw, ri.qd, ri.rp) : fixed_q(s, twg, qdg, rpg);
             a.S_ga[i] = s;
@@ -191,7 +207,7 @@ void launch_rank_vs_ga(const RankArgs &a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = (a.n + 7) / 8;
-    if (grid > (int64_t)sms * 4) grid = (int64_t)sms * 4;
+    if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
     if (grid < 1) grid = 1;
     k_rank_vs_ga<<<(unsigned)grid, kRankThreads, smem, st>>>(a);
 }
@@ -438,10 +454,32 @@ __global__ void __launch_bounds__(256) k_gather_res(const int32_t *out_src, cons
     const int64_t nw = (int64_t)gridDim.x * 8;
     for (int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); r < n; r += nw) {
         const int32_t t = out_src[r];
-        const uint8_t *src = src_res + src_off[perm ? perm[t] : t];
-        uint8_t *dst = dst_res + dst_off[r];
-        const int64_t L = dst_off[r + 1] - dst_off[r];
-        for (int64_t c = lane; c < L; c += 32) dst[c] = src[c];
+        const int64_t so = src_off[perm ? perm[t] : t], d0 = dst_off[r];
+        const int64_t L = dst_off[r + 1] - d0;
+        // 8-byte destination words (8-byte aligned; both buffers are 256-byte aligned): each is
+        // assembled from the two aligned source words it straddles; partial words at the ends
+        // are written byte by byte
+        const int64_t w0 = d0 >> 3, w1 = (d0 + L + 7) >> 3;
+        for (int64_t w = w0 + lane; w < w1; w += 32) {
+            const int64_t db = w << 3;                     // destination byte of this word
+            const int64_t sb = so + (db - d0);             // its source byte (may precede the sequence)
+            if (db >= d0 && db + 8 <= d0 + L && sb >= 0) {
+                const int64_t sa = sb & ~int64_t(7);
+                const unsigned sh = (unsigned)(sb & 7) * 8u;
+                const unsigned long long lo = *reinterpret_cast<const unsigned long long *>(src_res + sa);
+                unsigned long long x = lo;
+                if (sh) {
+                    const unsigned long long hi = *reinterpret_cast<const unsigned long long *>(src_res + sa + 8);
+                    x = (lo >> sh) | (hi << (64u - sh));
+                }
+                *reinterpret_cast<unsigned long long *>(dst_res + db) = x;
+            } else {
+                for (int j = 0; j < 8; ++j) {
+                    const int64_t c = db + j - d0;
+                    if (c >= 0 && c < L) dst_res[db + j] = src_res[so + c];
+                }
+            }
+        }
     }
 }
 
