@@ -28,6 +28,9 @@
 namespace sad {
 
 constexpr int kXrWarps = 8;
+#ifndef SAD_XR_BATCH
+#define SAD_XR_BATCH 4                  // list entries per lane in flight (one round trip per 32 * batch)
+#endif
 #ifndef SAD_XROWS_GLOBAL
 #define SAD_XROWS_GLOBAL 1   // 1: accumulate each row's excess in place in E (global); 0: shared-memory rows
 #endif
@@ -132,10 +135,10 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows(ExcessArgs a, int warps
                 const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
                 __syncwarp();
                 int g = 0;
-                for (uint32_t t0 = 0; t0 < tot; t0 += 128) {
-                    uint32_t vb[4], xa[4];
+                for (uint32_t t0 = 0; t0 < tot; t0 += 32 * SAD_XR_BATCH) {
+                    uint32_t vb[SAD_XR_BATCH], xa[SAD_XR_BATCH];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < SAD_XR_BATCH; ++u) {
                         const uint32_t t = t0 + (uint32_t)(u * 32 + lane);
                         vb[u] = 0;
                         xa[u] = 0;
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows(ExcessArgs a, int warps
                         }
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < SAD_XR_BATCH; ++u) {
                         const uint32_t b = vb[u] >> 8;
                         if (xa[u] && b > local) {
                             const uint32_t sh = 8u * (b & 3u);
@@ -255,10 +258,10 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows_g(ExcessArgs a) {
                     d_n = a.nhi[i_n];
                 }
                 int g = 0;
-                for (uint32_t t0 = 0; t0 < tot; t0 += 128) {
-                    uint32_t vb[4], xa[4];
+                for (uint32_t t0 = 0; t0 < tot; t0 += 32 * SAD_XR_BATCH) {
+                    uint32_t vb[SAD_XR_BATCH], xa[SAD_XR_BATCH];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < SAD_XR_BATCH; ++u) {
                         const uint32_t t = t0 + (uint32_t)(u * 32 + lane);
                         vb[u] = 0;
                         xa[u] = 0;
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows_g(ExcessArgs a) {
                         }
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < SAD_XR_BATCH; ++u) {
                         const uint32_t b = vb[u] >> 8;
                         if (xa[u] && b > local)
                             atomicAdd(reinterpret_cast<uint32_t *>(erow + (b & ~3u)),
@@ -300,7 +303,11 @@ int launch_excess(const ExcessArgs &a, cudaStream_t st) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_xrows_g, kXrWarps * 32, 0);
-        const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), (a.n + kXrWarps - 1) / kXrWarps);
+#ifndef SAD_K6_DIV
+#define SAD_K6_DIV 1                      // K6 takes 1/SAD_K6_DIV of the resident blocks (K4 runs beside it)
+#endif
+        const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(per_sm / SAD_K6_DIV, 1),
+                                               (a.n + kXrWarps - 1) / kXrWarps);
         if (grid > 0) k_xrows_g<<<(unsigned)grid, kXrWarps * 32, 0, st>>>(a);
         return 0;
     }

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
     const int64_t i0 = a.i_begin + gw * nr / W, i1 = a.i_begin + (gw + 1) * nr / W;
     int s = 0;
     while (s + 1 < a.pl && i0 >= a.shard_base[s + 1]) ++s;
-    unsigned long long acc_w = 0, acc_d = 0;
+    unsigned long long acc_w = 0, acc_d = 0, max_tw = 0;
     uint32_t exm[kNumCaps] = {};
     auto flush = [&]() {
         // M(tau) >= 1 for every k-mer present: the warp's presence bits, OR-ed once per word
@@ -100,12 +100,13 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
             if (acc_w | acc_d) {
                 atomicAdd(&a.kinfo[s * kKinfo + 0], acc_w);
                 atomicAdd(&a.kinfo[s * kKinfo + 1], acc_d);
+                atomicMax(&a.kinfo[s * kKinfo + 3], max_tw);
             }
 #pragma unroll
             for (int j = 0; j < kNumCaps; ++j)
                 if (exm[j]) atomicMax(&a.kinfo[s * kKinfo + 4 + j], (unsigned long long)exm[j]);
         }
-        acc_w = acc_d = 0;
+        acc_w = acc_d = max_tw = 0;
 #pragma unroll
         for (int j = 0; j < kNumCaps; ++j) exm[j] = 0;
     };
@@ -328,6 +329,7 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
             a.rowinfo[i] = RowInfo{tw, 0xFFFFFFFFu / tw, 0xFFFFFFFFu % tw + 1u, (uint32_t)s};
         }
         acc_w += (unsigned long long)Tw;
+        max_tw = max(max_tw, (unsigned long long)Tw);
         acc_d += n_hi + n_lo;
         __syncwarp();
     }
@@ -363,47 +365,49 @@ void launch_profile(const ProfileArgs &a, cudaStream_t st) {
 
 // Length order of every shard (the all-pairs kernel works on rows sorted by L - k + 1, so that
 // in a tile strictly above the diagonal every pair's denominator min(L_i, L_j) - k + 1 is the
-// row's own; T and S are permutation invariant): keys (shard, Tw) with the local index as the
-// value of one stable radix sort, then sigma (sorted position -> local index), its inverse, and the sorted RowInfo with
-// .shard replaced by the local index.
-__global__ void k_lenkeys(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *keys,
-                          int32_t *vals) {
+// row's own), by counting: per-shard histogram of Tw, one exclusive scan over [shard][Tw] (which
+// gives global sorted positions directly: shards are contiguous), then every sequence takes the next
+// slot of its bin -> sigma (sorted position -> local index), its inverse, and the sorted RowInfo
+// with .shard replaced by the local index. Rows of equal Tw land in arbitrary order: nothing
+// downstream depends on it (T and S are permutation invariant; K5 only needs Tw non-decreasing
+// along every shard, K6 only a consistent order).
+__global__ void k_lenhist(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, int nb,
+                          uint32_t *cnt) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int s = 0;
         while (s + 1 < pl && i >= shard_base[s + 1]) ++s;
-        keys[i] = ((uint32_t)s << 16) | rowinfo[i].tw;          // stable sort: ties keep index order
-        vals[i] = (int32_t)(i - shard_base[s]);
+        atomicAdd(&cnt[(size_t)s * nb + min((int)rowinfo[i].tw, nb - 1)], 1u);
     }
 }
 
-__global__ void k_lenperm(const uint32_t *keys_sorted, const int32_t *vals_sorted, const RowInfo *rowinfo,
-                          const int64_t *shard_base, int64_t n, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-        const int s = (int)(keys_sorted[p] >> 16);
-        const int32_t local = vals_sorted[p];
+__global__ void k_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, int nb,
+                             uint32_t *pos, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int s = 0;
+        while (s + 1 < pl && i >= shard_base[s + 1]) ++s;
+        RowInfo r = rowinfo[i];
+        const int64_t p = atomicAdd(&pos[(size_t)s * nb + min((int)r.tw, nb - 1)], 1u);   // sorted position
         const int64_t b = shard_base[s];
+        const int32_t local = (int32_t)(i - b);
         sigma[p] = local;
-        sigma_inv[b + local] = (int32_t)(p - b);
-        RowInfo r = rowinfo[b + local];
+        sigma_inv[i] = (int32_t)(p - b);
         r.shard = (uint32_t)local;
         rinfo_s[p] = r;
     }
 }
 
-void launch_lenkeys(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *keys,
-                    int32_t *vals, cudaStream_t st) {
-    const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
-    if (g > 0) k_lenkeys<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, keys, vals);
-}
-
-void launch_lenperm(const uint32_t *keys_sorted, const int32_t *vals_sorted, const RowInfo *rowinfo,
-                    const int64_t *shard_base, int64_t n, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s,
+void launch_lenhist(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, int nb, uint32_t *cnt,
                     cudaStream_t st) {
     const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
-    if (g > 0)
-        k_lenperm<<<(unsigned)g, 256, 0, st>>>(keys_sorted, vals_sorted, rowinfo, shard_base, n, sigma, sigma_inv,
-                                                rinfo_s);
+    if (g > 0) k_lenhist<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, nb, cnt);
 }
+
+void launch_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, int nb, uint32_t *pos,
+                       int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s, cudaStream_t st) {
+    const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
+    if (g > 0) k_lenscatter<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, nb, pos, sigma, sigma_inv, rinfo_s);
+}
+
 
 // K3: per shard, col0(tau) = exclusive scan over tau of min(M(tau), T_s) and
 // K_s = sum_tau min(M(tau), T_s). Column block [col0(tau), col0(tau) + min(M(tau), T_s)) holds
@@ -615,7 +619,10 @@ void launch_indicator(const OperandArgs &a, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_indicator, kOpWarps * 32, smem);
-    int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+#ifndef SAD_K4_DIV
+#define SAD_K4_DIV 1
+#endif
+    int64_t grid = (int64_t)sms * std::max(per_sm / SAD_K4_DIV, 1);
     const int64_t need = (a.rows_pad + kOpWarps - 1) / kOpWarps;
     if (grid > need) grid = need;
     if (grid > 0) k_indicator<<<(unsigned)grid, kOpWarps * 32, smem, st>>>(a, slice);

@@ -53,11 +53,20 @@ static int block_sort(const K *ki, const int32_t *vi, int n, K *ko, int32_t *vo,
 // Segmented variant: block b sorts segment [seg[b], seg[b+1]) (at most kSmallSortMax pairs) by bits
 // [0, end_bit) of its keys, stably; the bits above end_bit are the same within a segment (the
 // shard) and are carried over from the segment's first key. One launch for every shard of a rank.
+#ifndef SAD_SEG_THREADS
+#define SAD_SEG_THREADS 512
+#endif
+#ifndef SAD_SEG_RADIX
+#define SAD_SEG_RADIX 4
+#endif
+constexpr int kSegThreads = SAD_SEG_THREADS, kSegItems = kSmallSortMax / SAD_SEG_THREADS;
+using SegSort = cub::BlockRadixSort<uint32_t, kSegThreads, kSegItems, int32_t, SAD_SEG_RADIX>;
+
 template <typename K>
-__global__ void __launch_bounds__(kSortThreads) k_seg_sort(const K *keys_in, const int32_t *vals_in,
+__global__ void __launch_bounds__(kSegThreads) k_seg_sort(const K *keys_in, const int32_t *vals_in,
                                                             const int64_t *seg, K *keys_out, int32_t *vals_out,
                                                             int end_bit) {
-    using BRS = cub::BlockRadixSort<uint32_t, kSortThreads, kSortItems, int32_t>;
+    using BRS = SegSort;
     extern __shared__ __align__(16) uint8_t sort_smem[];
     typename BRS::TempStorage &tmp = *reinterpret_cast<typename BRS::TempStorage *>(sort_smem);
     const int64_t b = seg[blockIdx.x];
@@ -65,18 +74,18 @@ __global__ void __launch_bounds__(kSortThreads) k_seg_sort(const K *keys_in, con
     if (n <= 0) return;
     const K low = end_bit >= (int)(8 * sizeof(K)) ? ~K(0) : ((K(1) << end_bit) - 1);
     const K high = keys_in[b] & ~low;
-    uint32_t k[kSortItems];
-    int32_t v[kSortItems];
+    uint32_t k[kSegItems];
+    int32_t v[kSegItems];
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
-        const int idx = threadIdx.x * kSortItems + i;
+    for (int i = 0; i < kSegItems; ++i) {
+        const int idx = threadIdx.x * kSegItems + i;
         k[i] = idx < n ? (uint32_t)(keys_in[b + idx] & low) : 0xFFFFFFFFu;   // padding sorts last (stable)
         v[i] = idx < n ? vals_in[b + idx] : 0;
     }
     BRS(tmp).Sort(k, v, 0, end_bit);
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
-        const int idx = threadIdx.x * kSortItems + i;
+    for (int i = 0; i < kSegItems; ++i) {
+        const int idx = threadIdx.x * kSegItems + i;
         if (idx < n) {
             keys_out[b + idx] = high | (K)k[i];
             vals_out[b + idx] = v[i];
@@ -87,7 +96,7 @@ __global__ void __launch_bounds__(kSortThreads) k_seg_sort(const K *keys_in, con
 template <typename K>
 static int seg_sort(const K *ki, const int32_t *vi, const int64_t *seg, int nseg, K *ko, int32_t *vo, int end_bit,
                     cudaStream_t st) {
-    using BRS = cub::BlockRadixSort<uint32_t, kSortThreads, kSortItems, int32_t>;
+    using BRS = SegSort;
     const size_t smem = sizeof(typename BRS::TempStorage);
     static bool configured = false;
     if (end_bit > 32) return -1;
@@ -96,7 +105,7 @@ static int seg_sort(const K *ki, const int32_t *vi, const int64_t *seg, int nseg
             return -1;
         configured = true;
     }
-    k_seg_sort<K><<<nseg, kSortThreads, smem, st>>>(ki, vi, seg, ko, vo, end_bit);
+    k_seg_sort<K><<<nseg, kSegThreads, smem, st>>>(ki, vi, seg, ko, vo, end_bit);
     return 0;
 }
 

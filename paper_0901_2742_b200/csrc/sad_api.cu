@@ -101,7 +101,9 @@ size_t cub_bytes_needed(int64_t n, int pl) {
     cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint32_t *)nullptr, (uint32_t *)nullptr, (const int32_t *)nullptr,
                                     (int32_t *)nullptr, (int)std::max<int64_t>(n, 1), 0, 32);
     cub::DeviceScan::InclusiveSum(nullptr, d, (const int64_t *)nullptr, (int64_t *)nullptr, (int)std::max<int64_t>(n, 1));
-    return std::max(std::max(a, b), std::max(c, d)) + 1024;
+    size_t f = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, f, (const uint32_t *)nullptr, (uint32_t *)nullptr, pl * kLenBinsMax);
+    return std::max(std::max(std::max(a, b), std::max(c, d)), f) + 1024;
 }
 
 // carve the workspace; with base == nullptr only the size is computed
@@ -119,6 +121,7 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_rinfo_s = b.take<RowInfo>((size_t)n);
     c->d_M = b.take<uint32_t>((size_t)pl * V);
     c->d_Mb = b.take<uint32_t>((size_t)pl * ((V + 31) / 32));
+    c->d_lcnt = b.take<uint32_t>((size_t)2 * pl * kLenBinsMax);
     c->d_col0 = b.take<uint32_t>((size_t)pl * V);
     c->d_err = b.take<unsigned long long>(4);
     c->d_kinfo = b.take<unsigned long long>((size_t)pl * kKinfo);
@@ -585,6 +588,10 @@ int sad_build_profiles(sad_ctx *ctx) {
         kmax = std::max(kmax, ctx->h_K[s]);
     }
     ctx->use_excess = any_excess;
+    ctx->len_bins = 1;
+    for (int s = 0; s < pl; ++s)
+        ctx->len_bins = (int)std::max<int64_t>(ctx->len_bins, (int64_t)hk[(size_t)kKinfo * s + 3] + 1);
+    ctx->len_bins = std::min(ctx->len_bins, kLenBinsMax);
     if (ctx->use_tc) {
         uint32_t *hc = reinterpret_cast<uint32_t *>(ctx->h_small + 12288);
         for (int s = 0; s < pl; ++s) {
@@ -689,18 +696,16 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
         // length order of every shard (sigma), then K3 under the layer caps; K6 list offsets and
         // lists; K4 beside K6 rows (side stream)
         {
-            uint32_t *k_in = reinterpret_cast<uint32_t *>(ctx->d_ckey), *k_out = reinterpret_cast<uint32_t *>(ctx->d_ckey_sorted);
-            launch_lenkeys(ctx->d_rowinfo, ctx->d_shard_base, pl, ctx->n, k_in, ctx->d_perm_in, ctx->st);
+            const int nb = ctx->len_bins;
+            uint32_t *cnt = ctx->d_lcnt, *pos = ctx->d_lcnt + (size_t)pl * kLenBinsMax;
+            CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)pl * nb, ctx->st));
+            launch_lenhist(ctx->d_rowinfo, ctx->d_shard_base, pl, ctx->n, nb, cnt, ctx->st);
             LAUNCHED();
-            int sbits = 0;
-            while ((1 << sbits) < pl) ++sbits;
-            if (!(pl > 1 && ctx->max_w <= kSmallSortMax &&
-                  seg_sort_pairs(k_in, ctx->d_perm_in, ctx->d_shard_base, pl, k_out, ctx->d_perm_sorted, 16,
-                                 ctx->st) == 0))
-                CK(sort_pairs(ctx, k_in, k_out, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n, 16 + sbits));
+            size_t tb = ctx->cub_bytes;
+            CK(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tb, cnt, pos, pl * nb, ctx->st));
             LAUNCHED();
-            launch_lenperm(k_out, ctx->d_perm_sorted, ctx->d_rowinfo, ctx->d_shard_base, ctx->n, ctx->d_sigma,
-                           ctx->d_sigma_inv, ctx->d_rinfo_s, ctx->st);
+            launch_lenscatter(ctx->d_rowinfo, ctx->d_shard_base, pl, ctx->n, nb, pos, ctx->d_sigma, ctx->d_sigma_inv,
+                              ctx->d_rinfo_s, ctx->st);
         }
         LAUNCHED();
         o.sigma = ctx->d_sigma;

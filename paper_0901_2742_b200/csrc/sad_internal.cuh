@@ -29,10 +29,11 @@ namespace sad {
 constexpr int kMaxLocalShards = 256;
 constexpr int kRowPad = 128;        // operand rows per shard padded to this (tensor-core M tile)
 constexpr int kColPad = 128;        // operand columns padded to this (one 128-byte K block)
-constexpr int kKinfo = 24;          // u64 per shard in kinfo: [0] windows, [1] distinct, [2] K (no cap),
+constexpr int kKinfo = 24;          // u64 per shard in kinfo: [0] windows, [1] distinct, [2] K (no cap), [3] max Tw,
                                     // [4 + j] max_i sum_tau (n_i - 2^j)+, [8 + j] K under cap 2^j,
                                     // [12 + j] sum_tau C(X_j(tau), 2), [16 + j] sum_tau X_j(tau) with
                                     // X_j(tau) = #{i : n_i(tau) > 2^j}   (j < kNumCaps)
+constexpr int kLenBinsMax = 65536; // Tw <= 65535 (checked by K1/K2)
 constexpr int kNumCaps = 4;         // candidate layer caps T = 1, 2, 4, 8
 constexpr int kXrSmem = 200 * 1024; // K6 row accumulators (u8 per shard column) per block
 constexpr int64_t kMaxExcessBytes = int64_t(32) << 30;   // K6 dense excess matrices above this: no layer cap
@@ -117,12 +118,11 @@ struct OperandArgs {
     const uint32_t *ident;           // device [pl] 1: the column of tau is tau (cap 1, all V k-mers present), or NULL
 };
 void launch_indicator(const OperandArgs &a, cudaStream_t st);
-void launch_lenkeys(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *keys,
-                    int32_t *vals, cudaStream_t st);
-void launch_lenperm(const uint32_t *keys_sorted, const int32_t *vals_sorted, const RowInfo *rowinfo,
-                    const int64_t *shard_base, int64_t n, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s,
+// length order by counting (K3): bins Tw = 0..nb-1 per shard; sigma within equal Tw is arbitrary
+void launch_lenhist(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, int nb, uint32_t *cnt,
                     cudaStream_t st);
-
+void launch_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, int nb, uint32_t *pos,
+                       int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s, cudaStream_t st);
 // K6: the sparse excess of the capped layers (k_excess.cu),
 //   e_ij = sum_tau min((n_i(tau) - T_s)+, (n_j(tau) - T_s)+)   for i < j in shard s,
 // as a dense u8 matrix E_s[r][c] over sorted positions (length order; row pitch rup(w_s, 16);
@@ -366,6 +366,8 @@ struct sad_ctx {
     int32_t *d_sigma = nullptr, *d_sigma_inv = nullptr;   // length order of every shard (TC path)
     sad::RowInfo *d_rinfo_s = nullptr;                    // RowInfo in length order, .shard = local index
     uint32_t *d_M = nullptr, *d_Mb = nullptr, *d_col0 = nullptr;
+    uint32_t *d_lcnt = nullptr;      // [pl][kLenBinsMax] length-order counts, then positions (scan)
+    int len_bins = 0;                // bins in use this step: max Tw + 1 (from K1/K2)
     unsigned long long *d_err = nullptr, *d_kinfo = nullptr;
     uint32_t *d_cap = nullptr, *d_xsel = nullptr;   // layer cap T_s and its index j_s per shard
     uint32_t *d_ident = nullptr;                    // per shard: identity column map (K4 skips col0)

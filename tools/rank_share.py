@@ -61,5 +61,5 @@ def main(G=8, steps=10):
 
 
 if __name__ == "__main__":
-    for g in (1, 2, 4, 8):
+    for g in ([int(x) for x in sys.argv[1:]] or (1, 2, 4, 8)):
         main(g)
