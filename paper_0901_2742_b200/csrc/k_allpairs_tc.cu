@@ -621,6 +621,22 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                         rowsum += q;
                         cv[j] = q;
                     }
+                } else if (!P.sim) {
+                    // diagonal / edge tile: in length order every real pair (col > row) still has
+                    // the row's denominator, so the interior arithmetic applies under a column mask;
+                    // the self term (col == row) is exactly 2^32 (reading A3) and goes to the row only
+                    const int64_t cb = col0 + ch * 16;
+                    const int64_t lo64 = row + 1 - cb, hi64 = w - cb;
+                    const int lo = lo64 < 0 ? 0 : (lo64 > 16 ? 16 : (int)lo64);
+                    const int hi = hi64 < 0 ? 0 : (hi64 > 16 ? 16 : (int)hi64);
+                    const uint32_t m = (vrow && hi > lo) ? (((1u << (hi - lo)) - 1u) << lo) : 0u;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const uint64_t q = ((m >> j) & 1u) ? fixed_q_nd(v[j], ri.tw, nd, ri.qd, ri.rp) : 0ull;
+                        rowsum += q;
+                        cv[j] = q;
+                    }
+                    if (vrow && row >= cb && row < cb + 16) rowsum += 1ull << 32;
                 } else {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
