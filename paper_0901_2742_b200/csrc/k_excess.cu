@@ -180,7 +180,10 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows(ExcessArgs a, int warps
 // L2-resident while the warp works on the row): the row's upper part is zeroed when its first
 // excess k-mer appears, then the partners' bytes are added with fire-and-forget 32-bit atomics
 // (no carry: every e_ij <= 255). No shared-memory accumulator, so occupancy is not bounded by w.
-__global__ void __launch_bounds__(kXrWarps * 32) k_xrows_g(ExcessArgs a) {
+#ifndef SAD_XR_MINB
+#define SAD_XR_MINB 6
+#endif
+__global__ void __launch_bounds__(kXrWarps * 32, SAD_XR_MINB) k_xrows_g(ExcessArgs a) {
     __shared__ unsigned long long lbase[kMaxLocalShards + 1];
     __shared__ uint32_t sg_end[kXrWarps][32], sg_src[kXrWarps][32], sg_xa[kXrWarps][32];   // per-batch list segments
     if (threadIdx.x == 0) {

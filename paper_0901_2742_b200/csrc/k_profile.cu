@@ -39,6 +39,10 @@ constexpr int kProfWarps = SAD_PROF_WARPS;
 constexpr int kBinBits = SAD_PROF_BINBITS, kBinsPerWord = 32 / kBinBits;
 constexpr uint32_t kBinMax = (1u << kBinBits) - 1u;
 constexpr int kWidePasses = 16 / kBinBits;   // overflow fallback: u16 bins over 1/kWidePasses of the k-mers
+#ifndef SAD_PROF_UNROLL
+#define SAD_PROF_UNROLL 2
+#endif
+constexpr int kCountUnroll = SAD_PROF_UNROLL;   // windows per lane per counting step
 constexpr int kCodeSeg = 2048;           // residue codes staged per warp
 constexpr int kCodeBuf = kCodeSeg + 32;  // staged bytes keep the residues' 16-byte alignment (shift <= 15)
 
@@ -202,26 +206,34 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
             for (int g = 0; g < nseg; ++g) {
                 stage(g);
                 const int w1 = (int)min((int64_t)SW, Tw - (int64_t)g * SW);
-                for (int t0 = 0; t0 < w1; t0 += 32) {
-                    const int t = t0 + lane;
-                    bool first = false;
-                    uint32_t tau = 0;
-                    if (t < w1) {
-                        tau = window_tau<KT>(cod + sh + t, k, A);
-                        if (tau >= lo && tau < hi) {
-                            const uint32_t idx = tau - lo;
-                            const bool nb = bits != 16;
-                            const uint32_t sh8 = nb ? kBinBits * (idx % kBinsPerWord) : 16u * (idx & 1u);
-                            const uint32_t old = atomicAdd(&hist[nb ? idx / kBinsPerWord : idx >> 1], 1u << sh8);
-                            const uint32_t ob = (old >> sh8) & (nb ? kBinMax : 0xFFFFu);
-                            if (nb && ob == kBinMax) ovf = true;
-                            first = ob == 0;
+                for (int t0 = 0; t0 < w1; t0 += 32 * kCountUnroll) {   // independent windows per lane in flight
+                    bool first[kCountUnroll];
+                    uint32_t tau[kCountUnroll];
+#pragma unroll
+                    for (int u = 0; u < kCountUnroll; ++u) {
+                        const int t = t0 + 32 * u + lane;
+                        first[u] = false;
+                        tau[u] = 0;
+                        if (t < w1) {
+                            tau[u] = window_tau<KT>(cod + sh + t, k, A);
+                            if (tau[u] >= lo && tau[u] < hi) {
+                                const uint32_t idx = tau[u] - lo;
+                                const bool nb = bits != 16;
+                                const uint32_t sh8 = nb ? kBinBits * (idx % kBinsPerWord) : 16u * (idx & 1u);
+                                const uint32_t old = atomicAdd(&hist[nb ? idx / kBinsPerWord : idx >> 1], 1u << sh8);
+                                const uint32_t ob = (old >> sh8) & (nb ? kBinMax : 0xFFFFu);
+                                if (nb && ob == kBinMax) ovf = true;
+                                first[u] = ob == 0;
+                            }
                         }
                     }
                     if (lst) {
-                        const uint32_t fm = __ballot_sync(0xffffffffu, first);
-                        if (first) lst[nl + __popc(fm & ((1u << lane) - 1u))] = (uint16_t)tau;
-                        nl += __popc(fm);
+#pragma unroll
+                        for (int u = 0; u < kCountUnroll; ++u) {
+                            const uint32_t fm = __ballot_sync(0xffffffffu, first[u]);
+                            if (first[u]) lst[nl + __popc(fm & ((1u << lane) - 1u))] = (uint16_t)tau[u];
+                            nl += __popc(fm);
+                        }
                     }
                 }
             }
@@ -286,14 +298,20 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         if (!count(kBinBits, 0u, (uint32_t)V, lst)) {
             if (lst) {
                 bk = nl;                               // d is known: the two groups meet exactly
-                for (int e0 = 0; e0 < nl; e0 += 32) {
-                    const int e = e0 + lane;
-                    uint32_t c = 0, tau = 0;
-                    if (e < nl) {
-                        tau = lst[e];
-                        c = (hist[tau / kBinsPerWord] >> (kBinBits * (tau % kBinsPerWord))) & kBinMax;
+                for (int e0 = 0; e0 < nl; e0 += 32 * kCountUnroll) {
+                    uint32_t c[kCountUnroll], tau[kCountUnroll];
+#pragma unroll
+                    for (int u = 0; u < kCountUnroll; ++u) {
+                        const int e = e0 + 32 * u + lane;
+                        c[u] = 0;
+                        tau[u] = 0;
+                        if (e < nl) {
+                            tau[u] = lst[e];
+                            c[u] = (hist[tau[u] / kBinsPerWord] >> (kBinBits * (tau[u] % kBinsPerWord))) & kBinMax;
+                        }
                     }
-                    emit(c, tau);
+#pragma unroll
+                    for (int u = 0; u < kCountUnroll; ++u) emit(c[u], tau[u]);
                 }
                 __syncwarp();
                 for (int t = lane; t < hw / 4; t += 32) reinterpret_cast<uint4 *>(hist)[t] = make_uint4(0, 0, 0, 0);
