@@ -389,22 +389,45 @@ void launch_profile(const ProfileArgs &a, cudaStream_t st) {
 // with .shard replaced by the local index. Rows of equal Tw land in arbitrary order: nothing
 // downstream depends on it (T and S are permutation invariant; K5 only needs Tw non-decreasing
 // along every shard, K6 only a consistent order).
-__global__ void k_lenhist(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, int nb,
-                          uint32_t *cnt) {
+__global__ void k_lenhist(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *cnt) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int s = 0;
         while (s + 1 < pl && i >= shard_base[s + 1]) ++s;
-        atomicAdd(&cnt[(size_t)s * nb + min((int)rowinfo[i].tw, nb - 1)], 1u);
+        atomicAdd(&cnt[(size_t)s * kLenBinsMax + rowinfo[i].tw], 1u);     // Tw <= 65535 (K1/K2)
     }
 }
 
-__global__ void k_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, int nb,
-                             uint32_t *pos, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s) {
+// one block per shard: exclusive scan of the shard's bins 0..max Tw (max Tw from K1/K2 in kinfo[3],
+// read on the device so that no host decision is needed), offset by the shard's first row
+__global__ void __launch_bounds__(1024) k_lenscan(const uint32_t *cnt, const unsigned long long *kinfo,
+                                                   const int64_t *shard_base, uint32_t *pos) {
+    using BS = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ uint32_t carry;
+    const int s = blockIdx.x;
+    const unsigned long long mt = kinfo[(size_t)s * kKinfo + 3];
+    const int nb = (int)(mt + 1 < (unsigned long long)kLenBinsMax ? mt + 1 : (unsigned long long)kLenBinsMax);
+    if (threadIdx.x == 0) carry = (uint32_t)shard_base[s];
+    __syncthreads();
+    for (int b0 = 0; b0 < nb; b0 += 1024) {
+        const int b = b0 + threadIdx.x;
+        const uint32_t v = b < nb ? cnt[(size_t)s * kLenBinsMax + b] : 0u;
+        uint32_t ex, tot;
+        BS(tmp).ExclusiveSum(v, ex, tot);
+        if (b < nb) pos[(size_t)s * kLenBinsMax + b] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+}
+
+__global__ void k_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *pos,
+                             int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int s = 0;
         while (s + 1 < pl && i >= shard_base[s + 1]) ++s;
         RowInfo r = rowinfo[i];
-        const int64_t p = atomicAdd(&pos[(size_t)s * nb + min((int)r.tw, nb - 1)], 1u);   // sorted position
+        const int64_t p = atomicAdd(&pos[(size_t)s * kLenBinsMax + r.tw], 1u);   // sorted position
         const int64_t b = shard_base[s];
         const int32_t local = (int32_t)(i - b);
         sigma[p] = local;
@@ -414,16 +437,15 @@ __global__ void k_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, 
     }
 }
 
-void launch_lenhist(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, int nb, uint32_t *cnt,
-                    cudaStream_t st) {
+void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, const unsigned long long *kinfo, int pl,
+                     int64_t n, uint32_t *cnt, uint32_t *pos, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s,
+                     cudaStream_t st) {
     const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
-    if (g > 0) k_lenhist<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, nb, cnt);
-}
-
-void launch_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, int nb, uint32_t *pos,
-                       int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s, cudaStream_t st) {
-    const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
-    if (g > 0) k_lenscatter<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, nb, pos, sigma, sigma_inv, rinfo_s);
+    if (g <= 0) return;
+    cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)pl * kLenBinsMax, st);
+    k_lenhist<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, cnt);
+    k_lenscan<<<pl, 1024, 0, st>>>(cnt, kinfo, shard_base, pos);
+    k_lenscatter<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, pos, sigma, sigma_inv, rinfo_s);
 }
 
 

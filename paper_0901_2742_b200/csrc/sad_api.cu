@@ -275,6 +275,7 @@ int sad_create(const sad_config *cfg, sad_ctx **out) {
     if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_stats, cudaEventDisableTiming) != cudaSuccess ||
         [&] {
             for (auto &e : ctx->ev_chunk)
                 if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return true;
@@ -306,6 +307,7 @@ void sad_destroy(sad_ctx *ctx) {
     }
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->ev_stats) cudaEventDestroy(ctx->ev_stats);
     for (auto &e : ctx->ev_chunk)
         if (e) cudaEventDestroy(e);
     if (ctx->h_small) cudaFreeHost(ctx->h_small);
@@ -538,7 +540,15 @@ int sad_build_profiles(sad_ctx *ctx) {
     unsigned long long *hk = ctx->h_small + 8192;
     CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaMemcpyAsync(hk, ctx->d_kinfo, sizeof(unsigned long long) * kKinfo * pl, cudaMemcpyDeviceToHost, ctx->st));
-    CK(cudaStreamSynchronize(ctx->st));
+    CK(cudaEventRecord(ctx->ev_stats, ctx->st));
+    if (ctx->use_tc) {
+        // the length order needs no host decision: it runs while the host reads the statistics
+        launch_lenorder(ctx->d_rowinfo, ctx->d_shard_base, ctx->d_kinfo, pl, ctx->n, ctx->d_lcnt,
+                        ctx->d_lcnt + (size_t)pl * kLenBinsMax, ctx->d_sigma, ctx->d_sigma_inv, ctx->d_rinfo_s,
+                        ctx->st);
+        ctx->launches_step += 3;
+    }
+    CK(cudaEventSynchronize(ctx->ev_stats));
     const unsigned long long NONE = ~0ull;
     if (ctx->h_small[0] != NONE) {
         ctx->err_idx = (int64_t)(ctx->h_small[0] >> 32);
@@ -588,10 +598,7 @@ int sad_build_profiles(sad_ctx *ctx) {
         kmax = std::max(kmax, ctx->h_K[s]);
     }
     ctx->use_excess = any_excess;
-    ctx->len_bins = 1;
-    for (int s = 0; s < pl; ++s)
-        ctx->len_bins = (int)std::max<int64_t>(ctx->len_bins, (int64_t)hk[(size_t)kKinfo * s + 3] + 1);
-    ctx->len_bins = std::min(ctx->len_bins, kLenBinsMax);
+
     if (ctx->use_tc) {
         uint32_t *hc = reinterpret_cast<uint32_t *>(ctx->h_small + 12288);
         for (int s = 0; s < pl; ++s) {
@@ -693,21 +700,8 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     xtot = reinterpret_cast<unsigned long long *>(rup(reinterpret_cast<int64_t>(xtot), 8));
     record_pair(ctx, ctx->ev_pairs_op, true);
     if (ctx->use_tc) {
-        // length order of every shard (sigma), then K3 under the layer caps; K6 list offsets and
-        // lists; K4 beside K6 rows (side stream)
-        {
-            const int nb = ctx->len_bins;
-            uint32_t *cnt = ctx->d_lcnt, *pos = ctx->d_lcnt + (size_t)pl * kLenBinsMax;
-            CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)pl * nb, ctx->st));
-            launch_lenhist(ctx->d_rowinfo, ctx->d_shard_base, pl, ctx->n, nb, cnt, ctx->st);
-            LAUNCHED();
-            size_t tb = ctx->cub_bytes;
-            CK(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tb, cnt, pos, pl * nb, ctx->st));
-            LAUNCHED();
-            launch_lenscatter(ctx->d_rowinfo, ctx->d_shard_base, pl, ctx->n, nb, pos, ctx->d_sigma, ctx->d_sigma_inv,
-                              ctx->d_rinfo_s, ctx->st);
-        }
-        LAUNCHED();
+        // K3 under the layer caps (the length order sigma was computed by sad_build_profiles);
+        // K6 list offsets and lists; K4 beside K6 rows (side stream)
         o.sigma = ctx->d_sigma;
         launch_capscan(ctx->d_M, ctx->V, nullptr, ctx->d_cap, ctx->d_col0, nullptr, 0, pl, ctx->V, ctx->st);
         LAUNCHED();

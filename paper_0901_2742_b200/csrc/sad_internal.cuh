@@ -118,11 +118,11 @@ struct OperandArgs {
     const uint32_t *ident;           // device [pl] 1: the column of tau is tau (cap 1, all V k-mers present), or NULL
 };
 void launch_indicator(const OperandArgs &a, cudaStream_t st);
-// length order by counting (K3): bins Tw = 0..nb-1 per shard; sigma within equal Tw is arbitrary
-void launch_lenhist(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, int nb, uint32_t *cnt,
-                    cudaStream_t st);
-void launch_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, int nb, uint32_t *pos,
-                       int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s, cudaStream_t st);
+// length order by counting (K3): Tw histogram per shard, per-shard scan up to the max Tw in kinfo[3],
+// slot scatter -> sigma, sigma_inv, rinfo_s (ties in arbitrary order); 3 launches + 1 memset
+void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, const unsigned long long *kinfo, int pl,
+                     int64_t n, uint32_t *cnt, uint32_t *pos, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s,
+                     cudaStream_t st);
 // K6: the sparse excess of the capped layers (k_excess.cu),
 //   e_ij = sum_tau min((n_i(tau) - T_s)+, (n_j(tau) - T_s)+)   for i < j in shard s,
 // as a dense u8 matrix E_s[r][c] over sorted positions (length order; row pitch rup(w_s, 16);
@@ -331,6 +331,7 @@ struct sad_ctx {
     cudaStream_t st = nullptr;
     cudaStream_t side = nullptr;     // internal stream: K6 rows run beside K4 (fork/join by events)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_stats = nullptr;  // K1/K2 statistics on the host side; the length order runs on meanwhile
     static constexpr int kLoadChunks = 16;     // host loads: chunked H2D copies on `side`, each chunk's
     cudaEvent_t ev_chunk[kLoadChunks] = {};    // k-mer counts launched on `st` as soon as it lands
     bool profiled = false;                     // K1/K2 already launched by sad_load
@@ -367,7 +368,6 @@ struct sad_ctx {
     sad::RowInfo *d_rinfo_s = nullptr;                    // RowInfo in length order, .shard = local index
     uint32_t *d_M = nullptr, *d_Mb = nullptr, *d_col0 = nullptr;
     uint32_t *d_lcnt = nullptr;      // [pl][kLenBinsMax] length-order counts, then positions (scan)
-    int len_bins = 0;                // bins in use this step: max Tw + 1 (from K1/K2)
     unsigned long long *d_err = nullptr, *d_kinfo = nullptr;
     uint32_t *d_cap = nullptr, *d_xsel = nullptr;   // layer cap T_s and its index j_s per shard
     uint32_t *d_ident = nullptr;                    // per shard: identity column map (K4 skips col0)
