@@ -197,11 +197,17 @@ def main():
         ctx.load(d_a, d_o, n, lo, residues=R_loc)
         ctx.run(sync=False)
 
+    h_keys = None
+
     def step_e2e():
+        nonlocal h_keys
         ctx.load(h_a.numpy(), h_o.numpy(), n, lo)                   # H2D from pinned host memory
         sizes = ctx.run()
-        keys = ctx.out_keys().cpu()                                  # D2H of the step's result
-        return keys, sizes
+        keys = ctx.out_keys()
+        if h_keys is None or h_keys.shape != keys.shape:
+            h_keys = torch.empty(keys.shape, dtype=keys.dtype, pin_memory=True)
+        h_keys.copy_(keys)                                           # D2H of the step's result (pinned)
+        return h_keys, sizes
 
     def timed(fn, steps):
         ev = []

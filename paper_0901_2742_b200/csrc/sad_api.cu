@@ -470,7 +470,7 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
         // the previous step's readers of d_ascii (on ctx->st) finish before the first chunk lands
         CK(cudaEventRecord(ctx->ev_fork, ctx->st));
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-        for (int c = 0; c < nch; ++c) {
+        for (int c = 0; c < nch; ++c) {      // even chunks (a small last chunk measured slower)
             const int64_t i0 = n_local * c / nch, i1 = n_local * (c + 1) / nch;
             const int64_t b0 = offsets[i0], b1 = offsets[i1];
             if (b1 > b0)
@@ -699,6 +699,12 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     unsigned long long *xtot = reinterpret_cast<unsigned long long *>(ctx->d_xoff + (size_t)pl * ctx->V + 1) ;
     xtot = reinterpret_cast<unsigned long long *>(rup(reinterpret_cast<int64_t>(xtot), 8));
     record_pair(ctx, ctx->ev_pairs_op, true);
+    // SAD_OP_TIMELINE=1 (experiments): events inside the operand stage, printed to stderr
+    static const bool op_tl = getenv("SAD_OP_TIMELINE") != nullptr;
+    static cudaEvent_t tl[6] = {};
+    if (op_tl && !tl[0])
+        for (auto &e : tl) cudaEventCreate(&e);
+    if (op_tl) cudaEventRecord(tl[0], ctx->st);
     if (ctx->use_tc) {
         // K3 under the layer caps (the length order sigma was computed by sad_build_profiles);
         // K6 list offsets and lists; K4 beside K6 rows (side stream)
@@ -732,18 +738,30 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
             x.ebase = ctx->d_ebase;
             x.sigma = ctx->d_sigma;
             x.sigma_inv = ctx->d_sigma_inv;
+            if (op_tl) cudaEventRecord(tl[1], ctx->st);
             launch_xfill(x, ctx->d_xcur, ctx->st);
             LAUNCHED();
+            if (op_tl) cudaEventRecord(tl[2], ctx->st);
             // K6 rows on the side stream, concurrently with K4 (both only read the CSR / lists)
             CK(cudaEventRecord(ctx->ev_fork, ctx->st));
             CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
             if (launch_excess(x, ctx->side)) return fail(ctx, SAD_E_ARG, "K6: shard too wide for the row accumulators");
             LAUNCHED();
             CK(cudaEventRecord(ctx->ev_join, ctx->side));
+            if (op_tl) cudaEventRecord(tl[3], ctx->side);
         }
         launch_indicator(o, ctx->st);
         LAUNCHED();
+        if (op_tl) cudaEventRecord(tl[4], ctx->st);
         if (lists) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_join, 0));
+        if (op_tl && lists) {
+            cudaEventRecord(tl[5], ctx->st);
+            cudaEventSynchronize(tl[5]);
+            float m[5];
+            for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&m[i], tl[0], tl[i + 1]);
+            fprintf(stderr, "optl capscans %.4f xfill %.4f K6-end %.4f K4-end %.4f join %.4f ms\n", m[0], m[1], m[2],
+                    m[3], m[4]);
+        }
     } else {
         launch_dense_counts(o, ctx->st);
         LAUNCHED();
