@@ -269,7 +269,12 @@ def main():
         except Exception:
             pass
         fp4 = args.kernel in ("tc", "tc1", "tcfull")
-        if fp4 and "fp4_tflops" in measured:
+        if fp4 and "fp4_mma_only_tops" in measured:
+            peak, src = measured["fp4_mma_only_tops"], (
+                "measured fp4 tensor peak on this B200: issue rate of tcgen05.mma.cta_group::2.kind::mxf4 "
+                "(the all-pairs kernel built MMA-only, tools/mma_peak.py, profiles/peaks_b200.json); no library "
+                "fp4 GEMM is reachable from torch here")
+        elif fp4 and "fp4_tflops" in measured:
             peak, src = measured["fp4_tflops"], ("measured fp4 (mxf4) dense peak, cuBLAS torch._scaled_mm 8192^3 "
                                                  "burst (profiles/peaks_b200.json, tools/peaks.py)")
         elif fp4 and "int8_tops" in measured:
@@ -317,6 +322,17 @@ def main():
             roof["peak_bf16x4"] = 4.0 * bf16
             roof["frac_bf16x4"] = roof["achieved"] / roof["peak_bf16x4"]
         roof["frac_nominal_fp4_9000"] = roof["achieved"] / 9000.0
+        if "int8_tops" in measured:
+            roof["frac_2x_int8"] = roof["achieved"] / (2.0 * measured["int8_tops"])
+        if args.kernel == "tc":
+            # dense ops the kernel actually issues (256 x 240 tiles over each shard's upper triangle,
+            # K padded to 256 columns), against the same peak: the MMA stream's own efficiency
+            def n_tiles(w, bm=256, bn=240):
+                nI, nJ = (w + bm - 1) // bm, (w + bn - 1) // bn
+                return sum(max(0, nJ - (0 if bm * I - (bn - 1) <= 0 else (bm * I - (bn - 1) + bn - 1) // bn))
+                           for I in range(nI))
+            hw = sum(n_tiles(w) * 256 * 240 * ((int(k) + 255) // 256 * 256) * 2 for w, k in zip(w_loc, kcols))
+            roof["issued_ops_frac"] = hw / (ap_ms / 1e3) / 1e12 / roof["peak"]
     roof["kernel_ms"] = ap_ms
     roof["operand_build_ms"] = op_ms
 
