@@ -289,7 +289,9 @@ def main():
         roof = {"bound": "tensor", "achieved": ops / (ap_ms / 1e3) / 1e12, "peak": peak, "unit": "TOPS",
                 "frac": None, "traffic": None, "peak_source": src,
                 "int8_sustained_peak": measured.get("int8_tops_sustained")}
-        tr = os.path.join(ROOT, "profiles", f"r01_ncu_syrk_{args.kernel}_summary.csv")
+        # the ncu capture of this kernel on this workload (config 4 keeps the plain name)
+        suffix = "" if args.config == 4 and (args.p or 8) == 8 else f"_cfg{args.config}" + ("" if args.p is None else f"_p{args.p}")
+        tr = os.path.join(ROOT, "profiles", f"r01_ncu_syrk_{args.kernel}{suffix}_summary.csv")
         if os.path.exists(tr):
             vals = {}
             for line in open(tr):
