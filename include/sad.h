@@ -138,7 +138,10 @@ int sad_workspace_size(const sad_ctx *ctx, int64_t n_local, int64_t residues_loc
  *   offsets  [n_local+1] int64, offsets[0] == 0, nondecreasing (host or device per mem)
  *   residues_local  offsets[n_local] if known, else -1 (device offsets are then read back,
  *            which costs a synchronization)
- *   mem      SAD_MEM_HOST (copied with cudaMemcpyAsync; synchronous w.r.t. the inputs),
+ *   mem      SAD_MEM_HOST (copied with cudaMemcpyAsync; synchronous w.r.t. the inputs; from
+ *            4 MB on, the residues are copied in 4 chunks on an internal stream and each chunk's
+ *            k-mer counts (the first part of sad_build_profiles) start as soon as it has landed,
+ *            so pinned inputs overlap the PCIe copy with the counting),
  *            SAD_MEM_DEVICE (copied device-to-device on the stream) or SAD_MEM_DEVICE_REBASE
  *            (device, offsets[0] may be nonzero: offsets are taken relative to it)
  *   d_ws     device workspace of at least sad_workspace_size(n_local, offsets[n_local]) bytes,
@@ -154,8 +157,10 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
 /*
  * sad_build_profiles — k-mer count profiles n_x(tau) of every local sequence,
  * tau = sum_m c_m A^(k-1-m) over residue codes c. Validates symbols and lengths, builds the
- * per-sequence sorted (tau, count) lists and each shard's column map for the all-pairs
- * stage. Syncs once (to report input errors and size the all-pairs operand).
+ * per-sequence (tau, count) lists (unordered in tau; entries with count >= 2 first) and each
+ * shard's statistics for the all-pairs stage, and the length order of every shard (rows sorted by
+ * L - k + 1, ties in arbitrary order: no result depends on it). Waits once for the statistics (to
+ * report input errors and size the all-pairs operand); the length order runs meanwhile.
  */
 int sad_build_profiles(sad_ctx *ctx);
 
