@@ -3,6 +3,8 @@
 // for the per-rank sorts of small shards (many GPUs, small p). Larger inputs use cub::DeviceRadixSort.
 #include <cub/block/block_radix_sort.cuh>
 
+#include <algorithm>
+
 #include "sad_internal.cuh"
 
 namespace sad {
@@ -62,15 +64,22 @@ static int block_sort(const K *ki, const int32_t *vi, int n, K *ko, int32_t *vo,
 constexpr int kSegThreads = SAD_SEG_THREADS, kSegItems = kSmallSortMax / SAD_SEG_THREADS;
 using SegSort = cub::BlockRadixSort<uint32_t, kSegThreads, kSegItems, int32_t, SAD_SEG_RADIX>;
 
+// Sub-segment runs: block x sorts run (x % nruns) of segment (x / nruns), the segment split into
+// nruns contiguous runs; with nruns = 1 it sorts the whole segment.
+__device__ __forceinline__ int64_t run_begin(const int64_t *seg, int s, int r, int nruns) {
+    return seg[s] + (seg[s + 1] - seg[s]) * r / nruns;
+}
+
 template <typename K>
 __global__ void __launch_bounds__(kSegThreads) k_seg_sort(const K *keys_in, const int32_t *vals_in,
                                                             const int64_t *seg, K *keys_out, int32_t *vals_out,
-                                                            int end_bit) {
+                                                            int end_bit, int nruns) {
     using BRS = SegSort;
     extern __shared__ __align__(16) uint8_t sort_smem[];
     typename BRS::TempStorage &tmp = *reinterpret_cast<typename BRS::TempStorage *>(sort_smem);
-    const int64_t b = seg[blockIdx.x];
-    const int n = (int)(seg[blockIdx.x + 1] - b);
+    const int sg = blockIdx.x / nruns, rn = blockIdx.x % nruns;
+    const int64_t b = run_begin(seg, sg, rn, nruns);
+    const int n = (int)(run_begin(seg, sg, rn + 1, nruns) - b);
     if (n <= 0) return;
     const K low = end_bit >= (int)(8 * sizeof(K)) ? ~K(0) : ((K(1) << end_bit) - 1);
     const K high = keys_in[b] & ~low;
@@ -105,8 +114,61 @@ static int seg_sort(const K *ki, const int32_t *vi, const int64_t *seg, int nseg
             return -1;
         configured = true;
     }
-    k_seg_sort<K><<<nseg, kSegThreads, smem, st>>>(ki, vi, seg, ko, vo, end_bit);
+    k_seg_sort<K><<<nseg, kSegThreads, smem, st>>>(ki, vi, seg, ko, vo, end_bit, 1);
     return 0;
+}
+
+// Merge of the nruns sorted runs of every segment: an element's output position is its index in
+// its own run plus, for every other run, the number of keys there that precede it -- keys <= it in
+// earlier runs, < it in later runs, so equal keys keep run (= input) order: the result is the
+// stable sort of the segment.
+template <typename K>
+__global__ void k_merge_runs(const K *keys, const int32_t *vals, const int64_t *seg, int nseg, int nruns, int64_t n,
+                             K *keys_out, int32_t *vals_out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int s = 0;
+        while (s + 1 < nseg && i >= seg[s + 1]) ++s;
+        int r = 0;
+        while (r + 1 < nruns && i >= run_begin(seg, s, r + 1, nruns)) ++r;
+        const K key = keys[i];
+        int64_t pos = i - run_begin(seg, s, r, nruns);
+        for (int q = 0; q < nruns; ++q) {
+            if (q == r) continue;
+            int64_t lo = run_begin(seg, s, q, nruns), hi = run_begin(seg, s, q + 1, nruns);
+            const int64_t b0 = lo;
+            while (lo < hi) {                  // first element > key (q < r) or >= key (q > r)
+                const int64_t m = (lo + hi) >> 1;
+                const K x = keys[m];
+                if (q < r ? x <= key : x < key) lo = m + 1; else hi = m;
+            }
+            pos += lo - b0;
+        }
+        keys_out[seg[s] + pos] = key;
+        vals_out[seg[s] + pos] = vals[i];
+    }
+}
+
+// runs sorted in place, then merged into (ko, vo): several blocks per segment
+template <typename K>
+static int seg_sort_runs(K *ki, int32_t *vi, const int64_t *seg, int nseg, int nruns, int64_t n, K *ko, int32_t *vo,
+                         int end_bit, cudaStream_t st) {
+    const size_t smem = sizeof(typename SegSort::TempStorage);
+    static bool configured = false;
+    if (end_bit > 32) return -1;
+    if (!configured) {
+        if (cudaFuncSetAttribute(k_seg_sort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return -1;
+        configured = true;
+    }
+    k_seg_sort<K><<<nseg * nruns, kSegThreads, smem, st>>>(ki, vi, seg, ki, vi, end_bit, nruns);
+    const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
+    if (g > 0) k_merge_runs<K><<<(unsigned)g, 256, 0, st>>>(ki, vi, seg, nseg, nruns, n, ko, vo);
+    return 0;
+}
+
+int seg_sort_pairs_runs(unsigned long long *ki, int32_t *vi, const int64_t *seg, int nseg, int nruns, int64_t n,
+                        unsigned long long *ko, int32_t *vo, int end_bit, cudaStream_t st) {
+    return seg_sort_runs<unsigned long long>(ki, vi, seg, nseg, nruns, n, ko, vo, end_bit, st);
 }
 
 int seg_sort_pairs(const uint32_t *ki, const int32_t *vi, const int64_t *seg, int nseg, uint32_t *ko, int32_t *vo,

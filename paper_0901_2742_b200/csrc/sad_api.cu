@@ -905,9 +905,12 @@ int sad_rank_global(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out
         launch_f1_gainfo(ctx->d_anc_local, ctx->pl, ctx->shard0, p, ctx->first_idx, ctx->d_ga_info, ctx->st);
         LAUNCHED();
     }
-    if (!(ctx->pl > 1 && qbits == 32 && ctx->max_w <= kSmallSortMax &&
-          seg_sort_pairs(ctx->d_ckey, ctx->d_perm_in, ctx->d_shard_base, ctx->pl, ctx->d_ckey_sorted, ctx->d_perm_sorted,
-                         32, ctx->st) == 0))
+#ifndef SAD_RANK_SORT_RUNS
+#define SAD_RANK_SORT_RUNS 4                 // blocks per shard of the local rank sort (then one merge)
+#endif
+    if (!(qbits == 32 && ctx->max_w <= kSmallSortMax * SAD_RANK_SORT_RUNS &&
+          seg_sort_pairs_runs(ctx->d_ckey, ctx->d_perm_in, ctx->d_shard_base, ctx->pl, SAD_RANK_SORT_RUNS, ctx->n,
+                              ctx->d_ckey_sorted, ctx->d_perm_sorted, 32, ctx->st) == 0))
         CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
                       qbits + sbits));
     LAUNCHED();

@@ -315,6 +315,10 @@ int seg_sort_pairs(const uint32_t *ki, const int32_t *vi, const int64_t *seg, in
                    int end_bit, cudaStream_t st);
 int seg_sort_pairs(const unsigned long long *ki, const int32_t *vi, const int64_t *seg, int nseg,
                    unsigned long long *ko, int32_t *vo, int end_bit, cudaStream_t st);
+// the same with every segment split into nruns runs sorted by separate blocks (in place in ki, vi),
+// then merged stably into (ko, vo); 0 or -1
+int seg_sort_pairs_runs(unsigned long long *ki, int32_t *vi, const int64_t *seg, int nseg, int nruns, int64_t n,
+                        unsigned long long *ko, int32_t *vo, int end_bit, cudaStream_t st);
 void launch_rebase(const int64_t *src, int64_t n1, int64_t *off, cudaStream_t st);
 void launch_distance(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, float *D, cudaStream_t st);
 void launch_distance64(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, double *D, cudaStream_t st);
