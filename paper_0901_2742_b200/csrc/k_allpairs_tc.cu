@@ -83,7 +83,8 @@ struct Traits {
 }  // namespace tc
 
 struct TcTile {
-    int32_t s, I, J, pad;
+    int32_t s, I, J, pad;            // pad: 0 full tile; n > 0: only the first n (multiple of 16) columns
+                                     // hold real rows (a shard's last column block); -1: no tile
 };
 
 struct TcParams {
@@ -313,7 +314,7 @@ __device__ __forceinline__ void epi_pre_rows(const TcParams &P, EpiPre &p, uint3
     const RowInfo none{1u, 0xFFFFFFFFu, 1u, 0u};
     p.ri = none;
     p.ci = none;
-    if (p.tl.pad != 0) return;
+    if (p.tl.pad < 0) return;
     const int64_t rbase = P.shard_base[p.tl.s];
     const int64_t w = P.shard_base[p.tl.s + 1] - rbase;
     const int64_t row = (int64_t)p.tl.I * BMT + (int64_t)crank * tc::BM + quarter * 32 + lane;
@@ -407,7 +408,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             for (int64_t t = t0; t < P.n_tiles; t += tstep) {
                 const TcTile tl = P.tiles[t];
                 const int rowA = (int)(P.shard_rowpad[tl.s] + (int64_t)tl.I * BMT + (int64_t)crank * BM);
-                const int rowB = (int)(P.shard_rowpad[tl.s] + (int64_t)tl.J * BN + (int64_t)crank * BNC);
+                // an edge tile with N = tl.pad columns: each CTA of the pair holds N/2 of its B rows
+                const int rowB = (int)(P.shard_rowpad[tl.s] + (int64_t)tl.J * BN +
+                                       (int64_t)crank * (CG == 2 && tl.pad > 0 ? tl.pad / 2 : BNC));
                 const int nkb = (int)P.kblocks[tl.s];
                 for (int kb = 0; kb < nkb; ++kb) {
                     TC_TW(pw0, mbar_wait(&empty[stage], phase ^ 1));
@@ -442,6 +445,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             for (int64_t t = t0; t < P.n_tiles; t += tstep) {
                 const TcTile tl = P.tiles[t];
                 const int nkb = (int)P.kblocks[tl.s];
+                // MMA N of this tile (edge tiles: only the columns that hold real rows)
+                const uint32_t idesc = tl.pad > 0 ? ((Tr::IDESC & ~(0x3Fu << 17)) | ((uint32_t)(tl.pad >> 3) << 17))
+                                                  : Tr::IDESC;
                 TC_TW(pw0, mbar_wait(&tempty[acc], acc_phase ^ 1));
                 tc_fence_after();
                 const uint32_t d = tmem_base + (uint32_t)(acc * ACC_COLS);
@@ -453,7 +459,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
 #ifdef SAD_TC_DBG_NOMMA
                         tc_commit_pair_elect(&empty[stage]);       // timing experiment: no MMAs (wrong results)
 #else
-                        mma_stage_pair<KIND>(d, sw128_desc(a0), sw128_desc(b0), Tr::IDESC, kb != 0,
+                        mma_stage_pair<KIND>(d, sw128_desc(a0), sw128_desc(b0), idesc, kb != 0,
                                              tmem_base + Tr::SF_COL, &empty[stage]);
 #endif
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -539,7 +545,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         for (int64_t t = t0; t < P.n_tiles; t += tstep) {
             const TcTile tl = cur.tl;
             const TcTile tl2 = t + 2 * tstep < P.n_tiles ? P.tiles[t + 2 * tstep] : tnone;
-            const bool has_next = nxt.tl.pad == 0;
+            const bool has_next = nxt.tl.pad >= 0;
             const int64_t rbase = P.shard_base[tl.s];
             const int64_t w = P.shard_base[tl.s + 1] - rbase;
             const int64_t col0 = (int64_t)tl.J * BN, row0 = (int64_t)tl.I * BMT + (int64_t)crank * BM;
@@ -580,6 +586,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             for (int ch = ch0; ch < ch1; ++ch) {
 #endif
                 uint32_t v[16];
+                if (tl.pad > 0 && ch * 16 >= tl.pad) {   // edge tile: no real column in this chunk
+                    if (has_next && ch == ch0) epi_pre_rows<BN, BMT>(P, nxt, crank, quarter, lane, e);
+                    continue;
+                }
 #ifdef SAD_TC_DBG_NOTLD
                 for (int j = 0; j < 16; ++j) v[j] = (uint32_t)(ch * 16 + j + lane);   // timing experiment: no TMEM loads
 #else
@@ -798,17 +808,22 @@ int tc_bn(int kind) { return kind == 0 ? tc::Traits<0>::BN : tc::Traits<1>::BN; 
 // tiles of the upper triangle of every shard: (I, J) such that the tile holds some j >= i, i.e.
 // BN*J + BN - 1 >= BM*I, in groups of kGroupJ column blocks so that the ~148 tiles in flight
 // share a few A_J blocks and walk the A_I blocks (L2 reuse).
-static void build_tiles(int pl, const int64_t *h_shard_base, int bn, int bm, std::vector<TcTile> &out) {
+static void build_tiles(int pl, const int64_t *h_shard_base, int bn, int bm, std::vector<TcTile> &out,
+                        bool edge_n = false) {
     constexpr int kGroupJ = 8;
     out.clear();
     for (int s = 0; s < pl; ++s) {
         const int64_t w = h_shard_base[s + 1] - h_shard_base[s];
         const int nI = (int)((w + bm - 1) / bm), nJ = (int)((w + bn - 1) / bn);
+        // CTA pairs: the shard's last column block runs with N = the real columns rounded up to 16
+        const int64_t rem = w - (int64_t)(nJ - 1) * bn;
+        const int nlast = (edge_n && rem < bn) ? (int)((rem + 15) / 16 * 16) : 0;
         for (int j0 = 0; j0 < nJ; j0 += kGroupJ)
             for (int I = 0; I < nI; ++I) {
                 const int64_t need = (int64_t)bm * I - (bn - 1);
                 const int jmin = need <= 0 ? 0 : (int)((need + bn - 1) / bn);
-                for (int J = std::max(j0, jmin); J < std::min(nJ, j0 + kGroupJ); ++J) out.push_back(TcTile{s, I, J, 0});
+                for (int J = std::max(j0, jmin); J < std::min(nJ, j0 + kGroupJ); ++J)
+                    out.push_back(TcTile{s, I, J, J == nJ - 1 ? nlast : 0});
             }
     }
 }
@@ -827,7 +842,7 @@ int64_t tc_tiles_bound(int64_t n, int pl) {
 // the tile table of a layout, written to host memory (16 bytes per tile); returns the count
 int64_t tc_build_tiles(int pl, const int64_t *h_shard_base, int kind, int cg, void *host_out, int64_t cap) {
     std::vector<TcTile> t;
-    build_tiles(pl, h_shard_base, tc_bn(kind), tc::BM * cg, t);
+    build_tiles(pl, h_shard_base, tc_bn(kind), tc::BM * cg, t, cg == 2);
     if ((int64_t)t.size() > cap) return -1;
     std::memcpy(host_out, t.data(), t.size() * sizeof(TcTile));
     return (int64_t)t.size();
