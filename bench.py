@@ -329,11 +329,20 @@ def main():
         if args.kernel == "tc":
             # dense ops the kernel actually issues (256 x 240 tiles over each shard's upper triangle,
             # K padded to 256 columns), against the same peak: the MMA stream's own efficiency
-            def n_tiles(w, bm=256, bn=240):
+            def tile_cols(w, bm=256, bn=240):
+                # summed MMA N over the shard's tiles (the last column block runs with N = its real
+                # columns rounded up to 16)
                 nI, nJ = (w + bm - 1) // bm, (w + bn - 1) // bn
-                return sum(max(0, nJ - (0 if bm * I - (bn - 1) <= 0 else (bm * I - (bn - 1) + bn - 1) // bn))
-                           for I in range(nI))
-            hw = sum(n_tiles(w) * 256 * 240 * ((int(k) + 255) // 256 * 256) * 2 for w, k in zip(w_loc, kcols))
+                rem = w - (nJ - 1) * bn
+                nlast = (rem + 15) // 16 * 16
+                tot = 0
+                for I in range(nI):
+                    need = bm * I - (bn - 1)
+                    jmin = 0 if need <= 0 else (need + bn - 1) // bn
+                    if jmin < nJ:
+                        tot += (nJ - 1 - jmin) * bn + nlast
+                return tot
+            hw = sum(tile_cols(w) * 256 * ((int(k) + 255) // 256 * 256) * 2 for w, k in zip(w_loc, kcols))
             roof["issued_ops_frac"] = hw / (ap_ms / 1e3) / 1e12 / roof["peak"]
     roof["kernel_ms"] = ap_ms
     roof["operand_build_ms"] = op_ms
