@@ -3,7 +3,7 @@
 No library fp4 GEMM is reachable from torch here, so the fp4 tensor peak is measured with the
 all-pairs kernel itself built MMA-only (-DSAD_TC_DBG_NOTMA -DSAD_TC_DBG_NOEPI: no operand loads,
 no epilogue; results are meaningless, only the MMA stream remains): dense ops actually issued
-(tiles x 256 x 240 x K padded to 256 x 2) / kernel time, on config 4 (p = 8; ~1.3 ms of MMAs
+(256 x summed tile N x K padded to 256 x 2) / kernel time, on config 4 (p = 8; ~1.3 ms of MMAs
 per launch). Prints one JSON object.
 
     SAD_LIB_PATH=ab/libsad_mma.so python tools/mma_peak.py
@@ -22,13 +22,17 @@ from synth import gen  # noqa: E402
 BM, BN = 256, 240
 
 
-def tiles(w):
+def tile_cols(w):
+    """Summed MMA N over a shard's tiles (the last column block runs with N = its real columns
+    rounded up to 16)."""
     nI, nJ = (w + BM - 1) // BM, (w + BN - 1) // BN
+    nlast = (w - (nJ - 1) * BN + 15) // 16 * 16
     t = 0
     for I in range(nI):
         need = BM * I - (BN - 1)
         jmin = 0 if need <= 0 else (need + BN - 1) // BN
-        t += max(0, nJ - jmin)
+        if jmin < nJ:
+            t += (nJ - 1 - jmin) * BN + nlast
     return t
 
 
@@ -48,7 +52,7 @@ def run(a, o, p, steps=5):
     ms = st["allpairs_ms_total"] / max(st["calls"], 1)
     _, _, kcols = ctx.profile_info()
     sb = gen.shard_bounds(n, p)
-    hw = sum(tiles(int(sb[s + 1] - sb[s])) * BM * BN * ((int(kcols[s]) + 255) // 256 * 256) * 2 for s in range(p))
+    hw = sum(tile_cols(int(sb[s + 1] - sb[s])) * BM * ((int(kcols[s]) + 255) // 256 * 256) * 2 for s in range(p))
     return ms, hw / (ms / 1e3) / 1e12
 
 
