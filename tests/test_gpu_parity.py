@@ -411,3 +411,22 @@ def test_host_load_pipelined():
     with pytest.raises(SadError) as e:
         ctx_e.run()
     assert e.value.name == "SAD_E_SYMBOL" and e.value.location == (n - 1, 5)
+
+
+@pytest.mark.parametrize("kernel", [k for k in KERNELS if k in ("tc", "tc8", "tc1")])
+def test_tile_edges(kernel):
+    """Shard widths around the 256 x 240 tile grid of the tensor-core path: a last column block
+    with 1, 16, 17, 239 or 240 real columns (the edge tiles run with N = the real columns rounded
+    up to 16), a single row block, and shards of unequal width (N mod p != 0)."""
+    rng = np.random.default_rng(23)
+    fam = gen.random_set(rng, 40, "protein", 60, 200)
+    for n, p in ((481, 1), (496, 1), (497, 1), (719, 1), (720, 1), (255, 1), (1443, 3)):
+        a, o = gen.random_set(rng, n, "protein", 30, 260)
+        if n > 600:                                    # shared families: S spans the fixed-point range
+            s_f = gen.to_strings(*fam)
+            s = gen.to_strings(a, o)
+            s = [s_f[i % len(s_f)] if i % 3 == 0 else x for i, x in enumerate(s)]
+            a, o = gen.from_strings(s)
+        ctx, sizes = _run_gpu(a, o, "protein", 3, p, kernel)
+        r = oracle.run(a, o, "protein", 3, p)
+        _compare_full(ctx, sizes, r, a, o, p)
