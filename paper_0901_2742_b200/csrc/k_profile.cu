@@ -558,9 +558,15 @@ __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl
 // HBM sees exactly one streaming write of the operand. The entry and column-map loads are
 // issued kOpBatch per lane at a time, and the next row's CSR position is fetched one row ahead.
 constexpr int kOpThreads = 256;
-constexpr int kOpWarps = 8;
+#ifndef SAD_OP_WARPS
+#define SAD_OP_WARPS 8
+#endif
+#ifndef SAD_OP_BATCH
+#define SAD_OP_BATCH 4
+#endif
+constexpr int kOpWarps = SAD_OP_WARPS;
 constexpr int kRowSlice = 16384;
-constexpr int kOpBatch = 4;
+constexpr int kOpBatch = SAD_OP_BATCH;
 __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int slice) {
     extern __shared__ __align__(16) uint8_t opsm[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
