@@ -232,8 +232,10 @@ __global__ void __launch_bounds__(kXrWarps * 32, SAD_XR_MINB) k_xrows_g(ExcessAr
                 const uint32_t mask = __ballot_sync(0xffffffffu, hit);
                 if (!mask) continue;
                 if (!zeroed) {                    // the row's upper part, once
+#ifndef SAD_XR_DBG_NOZERO
                     for (int c = (int)((local + 1) >> 4) + lane; c < nch; c += 32)
                         reinterpret_cast<uint4 *>(erow)[c] = make_uint4(0, 0, 0, 0);
+#endif
                     zeroed = true;
                     __syncwarp();                 // orders the zeros before every lane's atomics
                 }
@@ -278,9 +280,13 @@ __global__ void __launch_bounds__(kXrWarps * 32, SAD_XR_MINB) k_xrows_g(ExcessAr
 #pragma unroll
                     for (int u = 0; u < SAD_XR_BATCH; ++u) {
                         const uint32_t b = vb[u] >> 8;
+#ifdef SAD_XR_DBG_NORED
+                        if (xa[u] && b > local && (vb[u] & 0xFFu) == 0xFFu) erow[0] = 1;   // timing experiment
+#else
                         if (xa[u] && b > local)
                             atomicAdd(reinterpret_cast<uint32_t *>(erow + (b & ~3u)),
                                       min(xa[u], vb[u] & 0xFFu) << (8u * (b & 3u)));
+#endif
                     }
                 }
                 __syncwarp();
