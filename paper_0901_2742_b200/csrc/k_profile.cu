@@ -119,10 +119,14 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
     int64_t off_c = i0 < i1 ? a.off[i0] : 0, off_e = i0 < i1 ? a.off[i0 + 1] : 0;
     uint4 qpre = i0 < i1 ? *reinterpret_cast<const uint4 *>(a.ascii + ((off_c & ~int64_t(15)) + 16 * lane))
                          : make_uint4(0, 0, 0, 0);
+    int64_t s_end = a.shard_base[s + 1];                       // end of the current shard
+    uint32_t *xcs = a.Xc + (size_t)s * kNumCaps * V;           // the shard's per-cap excess counts
     for (int64_t i = i0; i < i1; ++i) {
-        if (i >= a.shard_base[s + 1]) {                        // shard change: flush the totals
+        if (i >= s_end) {                                      // shard change: flush the totals
             flush();
             while (s + 1 < a.pl && i >= a.shard_base[s + 1]) ++s;
+            s_end = a.shard_base[s + 1];
+            xcs = a.Xc + (size_t)s * kNumCaps * V;
         }
         const int64_t off0 = off_c;
         const int64_t L = off_e - off0;
@@ -244,12 +248,13 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         uint32_t *out = a.csr + (off0 - i * (int64_t)(k - 1));
         uint32_t *Ms = a.M + (size_t)s * V;
         uint32_t n_hi = 0, n_lo = 0, ex[kNumCaps] = {};
-        int64_t bk = Tw;                                  // count-1 entries fill [.., bk) from the back
+        uint32_t bk = (uint32_t)Tw;                       // count-1 entries fill [.., bk) from the back
         auto emit = [&](uint32_t c, uint32_t tau) {       // warp-uniform call; c = 0: nothing
             const uint32_t mh = __ballot_sync(0xffffffffu, c >= 2), ml = __ballot_sync(0xffffffffu, c == 1);
             const uint32_t lt = (1u << lane) - 1u;
+            // (32-bit slot arithmetic: a row holds at most Tw <= 65535 entries)
             if (c >= 2) out[n_hi + __popc(mh & lt)] = (tau << 16) | c;
-            else if (c == 1) out[bk - 1 - (n_lo + __popc(ml & lt))] = (tau << 16) | 1u;
+            else if (c == 1) out[bk - 1u - n_lo - __popc(ml & lt)] = (tau << 16) | 1u;
             n_hi += __popc(mh);
             n_lo += __popc(ml);
             if (c) {
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
                     for (int j = 0; j < kNumCaps; ++j)
                         if (c > (1u << j)) {
                             ex[j] += c - (1u << j);
-                            atomicAdd(&a.Xc[((size_t)s * kNumCaps + j) * V + tau], 1u);
+                            atomicAdd(&xcs[(uint32_t)j * (uint32_t)V + tau], 1u);
                         }
                 }
             }
@@ -307,15 +312,22 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
                         tau[u] = 0;
                         if (e < nl) {
                             tau[u] = lst[e];
-                            c[u] = (hist[tau[u] / kBinsPerWord] >> (kBinBits * (tau[u] % kBinsPerWord))) & kBinMax;
+                            if constexpr (kBinBits == 8) {       // byte bins: read the count and clear it
+                                c[u] = reinterpret_cast<uint8_t *>(hist)[tau[u]];
+                                reinterpret_cast<uint8_t *>(hist)[tau[u]] = 0;
+                            } else {
+                                c[u] = (hist[tau[u] / kBinsPerWord] >> (kBinBits * (tau[u] % kBinsPerWord))) & kBinMax;
+                            }
                         }
                     }
 #pragma unroll
                     for (int u = 0; u < kCountUnroll; ++u) emit(c[u], tau[u]);
                 }
                 __syncwarp();
-                for (int t = lane; t < hw / 4; t += 32) reinterpret_cast<uint4 *>(hist)[t] = make_uint4(0, 0, 0, 0);
-                __syncwarp();
+                if constexpr (kBinBits != 8) {
+                    for (int t = lane; t < hw / 4; t += 32) reinterpret_cast<uint4 *>(hist)[t] = make_uint4(0, 0, 0, 0);
+                    __syncwarp();
+                }
             } else {
                 claim(kBinBits, 0u, (uint32_t)V);
             }
