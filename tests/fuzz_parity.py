@@ -3,7 +3,9 @@ p, sequence count and length mix, repeats, identical and contained sequences —
 the full path on every kernel variant and compared with the oracle bit for bit (the same checks
 as tests/test_gpu_parity.py::_compare_full). Stops at the first mismatch and prints its seed.
 
-    python tools/fuzz_parity.py [seconds] [first_seed]
+    python tests/fuzz_parity.py [seconds] [first_seed]
+
+(A script, not a pytest module: it lives under tests/ because only tests/ may run the oracle.)
 """
 import os
 import sys
@@ -13,7 +15,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import oracle  # noqa: E402
 from synth import gen  # noqa: E402
 from test_gpu_parity import _compare_full, _run_gpu  # noqa: E402
