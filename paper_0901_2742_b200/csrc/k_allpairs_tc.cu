@@ -131,11 +131,23 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *ba
         : "memory");
 }
 // contiguous global -> shared bulk copy (16-byte aligned, size a multiple of 16) completing `bar`
+#ifndef SAD_TC_E_EVICT_FIRST
+#define SAD_TC_E_EVICT_FIRST 1   // K6 excess rows are read once: evict them first, keep the operand tiles in L2
+#endif
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+#if SAD_TC_E_EVICT_FIRST
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+#else
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
                  "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
+#endif
 }
 // 2-CTA (cta_group::2) variants. A shared::cta address with the peer bit (24) cleared names the
 // same offset in the leader CTA (rank 0) of the pair.

@@ -1,0 +1,6 @@
+out=gpurun_out/ab5.txt; : > $out
+for r in 1 2; do for lib in ab/libsad_base.so ab/libsad_new.so; do
+ for cfg in 4 5; do
+  res=$(SAD_LIB_PATH=$lib timeout 180 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('%.4f %.4f %.4f' % (d['ms_per_step'], d['roofline']['kernel_ms'], d['roofline']['frac']))")
+  echo "$lib cfg$cfg: $res" >> $out
+ done; done; done
