@@ -235,13 +235,25 @@ __device__ __forceinline__ void tc_commit_pair_elect(uint64_t *bar) {
 // posts the expect_tx of both CTAs' bytes on its full barrier
 __device__ __forceinline__ void tma_stage_pair(const CUtensorMap *mA, const CUtensorMap *mB, uint64_t *bar, void *dA,
                                                void *dB, int c0, int rA, int rB, uint32_t expect) {
+#ifndef SAD_TC_OP_POLICY
+#define SAD_TC_OP_POLICY 0   // 1: operand tiles loaded with an L2 evict-last policy (experiment)
+#endif
+#if SAD_TC_OP_POLICY
+#define SAD_TC_OP_HINT ".L2::cache_hint"
+#define SAD_TC_OP_POL ", pol"
+#define SAD_TC_OP_MKPOL "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+#else
+#define SAD_TC_OP_HINT ""
+#define SAD_TC_OP_POL ""
+#define SAD_TC_OP_MKPOL ""
+#endif
     asm volatile(
-        "{\n\t.reg .pred e, l;\n\t"
+        "{\n\t.reg .pred e, l;\n\t.reg .b64 pol;\n\t" SAD_TC_OP_MKPOL
         "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.and.b32 l, %7, 0, e;\n\t"
         "@l mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %7;\n\t"
-        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%3], [%0, {%5, %6}], [%9];\n\t"
-        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%4], [%1, {%5, %8}], [%9];\n}" ::"l"(
+        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes" SAD_TC_OP_HINT " [%3], [%0, {%5, %6}], [%9]" SAD_TC_OP_POL ";\n\t"
+        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes" SAD_TC_OP_HINT " [%4], [%1, {%5, %8}], [%9]" SAD_TC_OP_POL ";\n}" ::"l"(
             reinterpret_cast<uint64_t>(mA)),
         "l"(reinterpret_cast<uint64_t>(mB)), "r"(smem_u32(bar)), "r"(smem_u32(dA)), "r"(smem_u32(dB)), "r"(c0), "r"(rA),
         "r"(expect), "r"(rB), "r"(smem_u32(bar) & kPeerMask)
