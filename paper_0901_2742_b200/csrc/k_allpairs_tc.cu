@@ -45,7 +45,10 @@ constexpr int SF_COLS = 32;                       // TMEM columns of unit block 
 // KIND 1: packed e2m1 0/1 operands (two per byte), tcgen05.mma.kind::mxf4.block_scale with
 //         every UE8M0 scale = 2^0, fp32 accumulators (exact: S <= 65535 < 2^24), N = 240 so
 //         that two accumulators + the scale columns fit the 512 TMEM columns.
-template <int KIND, int CG = 1>
+// DEEP (CTA pairs, long K): five operand stages and one excess buffer instead of four and two --
+// more bytes in flight for shards whose operand rows miss L2 (config 5's long DNA rows); with
+// short K the single excess buffer stalls the epilogue, so the host picks it per launch.
+template <int KIND, int CG = 1, bool DEEP = false>
 struct Traits {
     static constexpr int BN = KIND == 0 ? 256 : SAD_FP4_BN;   // MMA N (tile columns)
     static constexpr int BNC = BN / CG;                 // B rows held by each CTA of the pair
@@ -59,8 +62,8 @@ struct Traits {
 #ifndef SAD_TC_NOBAR
 #define SAD_TC_NOBAR 0       // 1: epilogue warps add their row / column partials to T directly (no barriers)
 #endif
-    static constexpr int STAGES = CG == 1 ? (KIND == 0 ? 2 : 3) : SAD_TC_STAGES2;   // (one-CTA tiles: reference variants)
-    static constexpr int XBUFS = SAD_TC_XBUFS;          // K6 staging buffers
+    static constexpr int STAGES = CG == 1 ? (KIND == 0 ? 2 : 3) : (DEEP ? 5 : SAD_TC_STAGES2);   // (one-CTA tiles: reference variants)
+    static constexpr int XBUFS = DEEP ? 1 : SAD_TC_XBUFS;   // K6 staging buffers
     static constexpr int B_BYTES = BNC * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int ACC_COLS = BN;
@@ -347,11 +350,11 @@ __device__ __forceinline__ void epi_pre_rows(const TcParams &P, EpiPre &p, uint3
     if (row < w) p.ri = P.rowinfo[rbase + row];
 }
 
-template <int KIND, int CG>
+template <int KIND, int CG, bool DEEP = false>
 __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constant__ CUtensorMap tmapA,
                                                             const __grid_constant__ CUtensorMap tmapB, TcParams P) {
     using namespace tc;
-    using Tr = Traits<KIND, CG>;
+    using Tr = Traits<KIND, CG, DEEP>;
     constexpr int BN = Tr::BN, B_BYTES = Tr::B_BYTES, STAGE_BYTES = Tr::STAGE_BYTES, ACC_COLS = Tr::ACC_COLS;
     constexpr int STAGES = Tr::STAGES, BNC = Tr::BNC, BMT = Tr::BMT;
     constexpr int OFF_BAR = Tr::OFF_BAR, OFF_COLINFO = Tr::OFF_COLINFO, OFF_COLSUM = Tr::OFF_COLSUM;
@@ -817,7 +820,9 @@ bool tc_supported(std::string &why) {
             cudaFuncSetAttribute(k_syrk_tc<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  tc::Traits<0, 2>::SMEM_BYTES) != cudaSuccess ||
             cudaFuncSetAttribute(k_syrk_tc<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::Traits<1, 2>::SMEM_BYTES) != cudaSuccess) {
+                                 tc::Traits<1, 2>::SMEM_BYTES) != cudaSuccess ||
+            cudaFuncSetAttribute(k_syrk_tc<1, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::Traits<1, 2, true>::SMEM_BYTES) != cudaSuccess) {
             reason = "cannot reserve shared memory";
             return;
         }
@@ -883,6 +888,9 @@ static bool encode(CUtensorMap *map, const void *base, int64_t stride, int64_t r
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+#ifndef SAD_TC_DEEP_KB
+#define SAD_TC_DEEP_KB 64
+#endif
 int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err) {
     std::string why;
     if (!tc_supported(why)) {
@@ -923,7 +931,12 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(a.num_sms / 2, P.n_tiles)));
         cfg.blockDim = dim3(tc::THREADS);
-        cfg.dynamicSmemBytes = a.kind == 0 ? tc::Traits<0, 2>::SMEM_BYTES : tc::Traits<1, 2>::SMEM_BYTES;
+        // long K (64+ K blocks in some shard, i.e. rows of 16k+ fp4 columns): the deeper ring
+        int64_t max_kb = 0;
+        for (int s = 0; s < a.pl; ++s) max_kb = std::max<int64_t>(max_kb, a.h_kblocks[s]);
+        const bool deep = a.kind == 1 && max_kb >= SAD_TC_DEEP_KB;
+        cfg.dynamicSmemBytes = a.kind == 0 ? tc::Traits<0, 2>::SMEM_BYTES
+                                           : (deep ? tc::Traits<1, 2, true>::SMEM_BYTES : tc::Traits<1, 2>::SMEM_BYTES);
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -933,6 +946,7 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         cudaError_t e = a.kind == 0 ? cudaLaunchKernelEx(&cfg, k_syrk_tc<0, 2>, mapA, mapB, P)
+                        : deep      ? cudaLaunchKernelEx(&cfg, k_syrk_tc<1, 2, true>, mapA, mapB, P)
                                     : cudaLaunchKernelEx(&cfg, k_syrk_tc<1, 2>, mapA, mapB, P);
         if (e != cudaSuccess) {
             err = std::string("cluster launch failed: ") + cudaGetErrorString(e);
