@@ -839,7 +839,10 @@ int tc_bn(int kind) { return kind == 0 ? tc::Traits<0>::BN : tc::Traits<1>::BN; 
 // share a few A_J blocks and walk the A_I blocks (L2 reuse).
 static void build_tiles(int pl, const int64_t *h_shard_base, int bn, int bm, std::vector<TcTile> &out,
                         bool edge_n = false) {
-    constexpr int kGroupJ = 8;
+#ifndef SAD_TC_GROUPJ
+#define SAD_TC_GROUPJ 8
+#endif
+    constexpr int kGroupJ = SAD_TC_GROUPJ;   // column blocks swept together over all row blocks (L2 reuse)
     out.clear();
     for (int s = 0; s < pl; ++s) {
         const int64_t w = h_shard_base[s + 1] - h_shard_base[s];
