@@ -146,12 +146,30 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------------------
 
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` launched without torchrun: re-launch this command as N ranks (one per
+    GPU) through torch.distributed.run; fail loudly when fewer than N GPUs are visible."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"error": f"--gpus {n} needs {n} visible GPUs, found {have}"}), flush=True)
+        return 2
+    port = 29500 + os.getpid() % 2000
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     from synth import gen
     spec = gen.SPECS[args.config]
     p = args.p or (8 if args.config in (2, 3, 4) else spec.p)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
 
@@ -243,7 +261,10 @@ def main():
     for _ in range(max(1, args.warmup // 2)):
         step_e2e()
     e2e_h2d = int(h_a.numel() + h_o.numel() * 8)
-    keys, _ = step_e2e()
+    keys, sizes_all = step_e2e()
+    # a12: the library's load report (sad_get_load_report: largest bucket vs 2w + p, < 2w when p | w;
+    # PAPER.md:188, reading A23)
+    load = dict(ctx.load_report(), bucket_sizes=[int(x) for x in sizes_all])
     e2e_d2h = int(keys.numel() * 8 + p * 8)
     ms_e2e = timed(step_e2e, args.steps)
 
@@ -258,40 +279,52 @@ def main():
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
+    measured = {}
+    try:
+        measured = json.load(open(os.path.join(ROOT, "profiles", "peaks_b200.json")))
+    except Exception:
+        pass
     _, _, kcols = ctx.profile_info()
     w_loc = [sb[rank * pl + s + 1] - sb[rank * pl + s] for s in range(pl)]
+    fp4 = args.kernel in ("tc", "tc1", "tcfull")
     if args.kernel.startswith("tc"):
         # algorithmic dense work of the threshold-indicator SYRK: 2 * K_s ops per pair i <= j
+        # (SURVEY §8(d) f_tc numerator: sum_s w_s (w_s + 1) K_s)
         ops = sum(2 * (w * (w + 1) // 2) * int(k) for w, k in zip(w_loc, kcols))
-        measured = {}
-        try:
-            measured = json.load(open(os.path.join(ROOT, "profiles", "peaks_b200.json")))
-        except Exception:
-            pass
-        fp4 = args.kernel in ("tc", "tc1", "tcfull")
-        if fp4 and "fp4_mma_only_tops" in measured:
-            peak, src = measured["fp4_mma_only_tops"], (
-                "measured fp4 tensor peak on this B200: issue rate of tcgen05.mma.cta_group::2.kind::mxf4 "
-                "(the all-pairs kernel built MMA-only, tools/mma_peak.py, profiles/peaks_b200.json); no library "
-                "fp4 GEMM is reachable from torch here")
-        elif fp4 and "fp4_tflops" in measured:
-            peak, src = measured["fp4_tflops"], ("measured fp4 (mxf4) dense peak, cuBLAS torch._scaled_mm 8192^3 "
-                                                 "burst (profiles/peaks_b200.json, tools/peaks.py)")
-        elif fp4 and "int8_tops" in measured:
-            peak, src = 2.0 * measured["int8_tops"], ("2 x measured int8 dense peak (cuBLAS torch._int_mm 8192^3 "
-                                                      "burst, profiles/peaks_b200.json): nominal fp4:int8 = 9:4.5")
-        elif "int8_tops" in measured:
-            peak, src = measured["int8_tops"], ("measured int8 dense peak, cuBLAS torch._int_mm 8192^3 burst "
-                                                "(profiles/peaks_b200.json, tools/peaks.py)")
+        bf16 = peaks.get("bf16_tflops")
+        if bf16:
+            # primary: the driver-measured bf16 burst x the nominal dense ratio of the operand dtype
+            # (fp4 : bf16 = 9 : 2.25 = 4; int8 : bf16 = 4.5 : 2.25 = 2), B200_PROFILING.md
+            ratio = 4.0 if fp4 else 2.0
+            peak = ratio * bf16
+            src = (f"MEASURED_PEAKS.json bf16_tflops (burst, {bf16:.1f}) x nominal "
+                   f"{'fp4' if fp4 else 'int8'}:bf16 = {ratio:g}")
         else:
-            bf16 = peaks.get("bf16_tflops", 1590.0)
-            peak, src = 2.0 * bf16, "2 x measured bf16 burst (nominal int8:bf16 = 2)"
+            peak = 9000.0 if fp4 else 4500.0
+            src = "nominal dense B200 peak (MEASURED_PEAKS.json absent)"
         roof = {"bound": "tensor", "achieved": ops / (ap_ms / 1e3) / 1e12, "peak": peak, "unit": "TOPS",
-                "frac": None, "traffic": None, "peak_source": src,
-                "int8_sustained_peak": measured.get("int8_tops_sustained")}
-        # the ncu capture of this kernel on this workload (config 4 keeps the plain name)
+                "frac": None, "traffic": None, "peak_source": src}
+        # the all-pairs STAGE (a3 = K3 + K4 + K6 + K5: operand build and the contraction), SURVEY §8(d)
+        roof["stage_ms"] = ap_ms + op_ms
+        roof["stage_frac"] = ops / ((ap_ms + op_ms) / 1e3) / 1e12 / peak
+        # operand bytes the contraction streams (rows padded to 128, K padded to one 128-byte block)
+        bpc = 0.5 if fp4 else 1.0
+        roof["operand_bytes"] = int(sum(((w + 127) // 128) * 128 * ((int(k) + 255) // 256 * 256) * bpc
+                                        for w, k in zip(w_loc, kcols)))
+        # context: the same kernel against this B200's own measured ceilings
+        if fp4 and "fp4_mma_only_tops" in measured:
+            roof["frac_of_mma_issue_rate"] = roof["achieved"] / measured["fp4_mma_only_tops"]
+            roof["mma_issue_rate_tops"] = measured["fp4_mma_only_tops"]
+        if "int8_tops" in measured:
+            roof["frac_of_cublas_int8" + ("_x2" if fp4 else "")] = roof["achieved"] / (
+                (2.0 if fp4 else 1.0) * measured["int8_tops"])
+        roof["frac_of_nominal"] = roof["achieved"] / (9000.0 if fp4 else 4500.0)
+        # DRAM traffic of one launch: ncu --set full of the same kernel on this workload
         suffix = "" if args.config == 4 and (args.p or 8) == 8 else f"_cfg{args.config}" + ("" if args.p is None else f"_p{args.p}")
-        tr = os.path.join(ROOT, "profiles", f"r01_ncu_syrk_{args.kernel}{suffix}_summary.csv")
+        for tag in ("r02", "r01"):
+            tr = os.path.join(ROOT, "profiles", f"{tag}_ncu_syrk_{args.kernel}{suffix}_summary.csv")
+            if os.path.exists(tr):
+                break
         if os.path.exists(tr):
             vals = {}
             for line in open(tr):
@@ -304,8 +337,6 @@ def main():
                     return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}[u]
                 roof["traffic"] = gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum")
                 roof["traffic_source"] = f"ncu --set full, one k_syrk_tc launch ({os.path.relpath(tr, ROOT)})"
-                roof["operand_bytes"] = int(sum(((w + 127) // 128) * 128 for w in w_loc) * int(
-                    (max(int(k) for k in kcols) + 127) // 128 * 128))
             except Exception:
                 pass
     else:
@@ -316,34 +347,6 @@ def main():
                 "frac": None, "traffic": None,
                 "peak_source": "148 SMs x 128 int32 lanes x sm_max_mhz (DESIGN.md §5)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    if args.kernel in ("tc", "tc1", "tcfull"):
-        # the same fraction against the other admissible denominators, for context: MEASURED_PEAKS.json's
-        # bf16 burst x the nominal fp4:bf16 ratio (9 : 2.25), and the nominal dense fp4 figure
-        bf16 = peaks.get("bf16_tflops")
-        if bf16:
-            roof["peak_bf16x4"] = 4.0 * bf16
-            roof["frac_bf16x4"] = roof["achieved"] / roof["peak_bf16x4"]
-        roof["frac_nominal_fp4_9000"] = roof["achieved"] / 9000.0
-        if "int8_tops" in measured:
-            roof["frac_2x_int8"] = roof["achieved"] / (2.0 * measured["int8_tops"])
-        if args.kernel == "tc":
-            # dense ops the kernel actually issues (256 x 240 tiles over each shard's upper triangle,
-            # K padded to 256 columns), against the same peak: the MMA stream's own efficiency
-            def tile_cols(w, bm=256, bn=240):
-                # summed MMA N over the shard's tiles (the last column block runs with N = its real
-                # columns rounded up to 16)
-                nI, nJ = (w + bm - 1) // bm, (w + bn - 1) // bn
-                rem = w - (nJ - 1) * bn
-                nlast = (rem + 15) // 16 * 16
-                tot = 0
-                for I in range(nI):
-                    need = bm * I - (bn - 1)
-                    jmin = 0 if need <= 0 else (need + bn - 1) // bn
-                    if jmin < nJ:
-                        tot += (nJ - 1 - jmin) * bn + nlast
-                return tot
-            hw = sum(tile_cols(w) * 256 * ((int(k) + 255) // 256 * 256) * 2 for w, k in zip(w_loc, kcols))
-            roof["issued_ops_frac"] = hw / (ap_ms / 1e3) / 1e12 / roof["peak"]
     roof["kernel_ms"] = ap_ms
     roof["operand_build_ms"] = op_ms
 
@@ -368,6 +371,7 @@ def main():
                     "ms_per_step": ms_e2e / args.steps},
             "allpairs_pairs_per_s": pairs_job / world / (ap_ms / 1e3) * world if ap_ms > 0 else None,
             "roofline": roof,
+            "load_report": load,
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": int(launches) * args.steps,

@@ -267,6 +267,18 @@ int sad_finish(sad_ctx *ctx, const int64_t *h_counts_all, const uint64_t *d_recv
 /* Sizes of all p buckets (after sad_finish; P:188 load report). */
 int sad_get_bucket_sizes(sad_ctx *ctx, int64_t *h_sizes);
 
+/*
+ * sad_get_load_report — SURVEY §8(a) row a12, the load bound of the regular-sampling partition
+ * ("all the data to be aligned by processor 1 must be <= y1 ... the upper bound on the number of
+ * sequences that a processor will receive is less than 2w"
+ * check_load_bound). Under the sampling rule of readings A10/A11 the bound that always holds is
+ * max bucket <= 2w + p, and max bucket < 2w when p divides w (reading A23).
+ * After sad_finish; syncs like the other getters. h_report (int64 [6]):
+ *   [0] largest bucket  [1] w = largest shard (ceil(N/p))  [2] 2w + p
+ *   [3] 1 if [0] <= 2w + p   [4] 1 if p divides every shard size w   [5] 1 if [0] < 2w
+ */
+int sad_get_load_report(sad_ctx *ctx, int64_t *h_report);
+
 /* T_i (uint64) of every sequence of local shard s (0 <= s < p/world), in input order. */
 int sad_get_local_rank(sad_ctx *ctx, int shard, uint64_t *h_T, int64_t cap);
 
@@ -283,8 +295,10 @@ int sad_get_sorted(sad_ctx *ctx, int shard, int64_t *h_idx, int64_t cap);
 int sad_get_pivots(sad_ctx *ctx, uint64_t *h_pivots);
 
 /* One bucket owned by this rank (after sad_finish): source indices, keys, residues (ASCII)
- * and offsets[n+1] (relative to the bucket's first residue). Returns SAD_E_CAPACITY if a
- * cap is too small; *n_out / *res_out receive the sizes in any case. Any output may be NULL. */
+ * and offsets[n+1] (relative to the bucket's first residue). cap_seqs is the capacity of
+ * h_idx / h_key (>= n) and of h_offsets (>= n + 1 when h_offsets is given); cap_res that of
+ * h_res. Returns SAD_E_CAPACITY if a cap is too small; *n_out / *res_out receive the sizes in
+ * any case. Any output may be NULL. */
 int sad_get_bucket(sad_ctx *ctx, int bucket, int64_t *h_idx, uint64_t *h_key, uint8_t *h_res,
                    int64_t *h_offsets, int64_t cap_seqs, int64_t cap_res, int64_t *n_out, int64_t *res_out);
 

@@ -26,7 +26,7 @@ SYMBOLS = [
     "sad_output_layout", "sad_finish", "sad_get_local_rank", "sad_get_ancestors", "sad_get_ranks", "sad_get_sorted",
     "sad_get_pivots", "sad_get_bucket", "sad_get_bucket_sizes", "sad_get_similarity", "sad_get_profile_info", "sad_get_stats",
     "sad_reset_stats", "sad_selftest_fixed_point", "sad_get_bucket_view", "sad_get_distance", "sad_exchange_records", "sad_get_distance_f64",
-    "sad_upgma_workspace", "sad_upgma",
+    "sad_upgma_workspace", "sad_upgma", "sad_get_load_report",
 ]
 
 
@@ -82,6 +82,7 @@ def lib():
         "sad_get_pivots": (i32, [P, P]),
         "sad_get_bucket": (i32, [P, i32, P, P, P, P, i64, i64, P, P]),
         "sad_get_bucket_sizes": (i32, [P, P]),
+        "sad_get_load_report": (i32, [P, P]),
         "sad_get_similarity": (i32, [P, i32, P, i64]),
         "sad_get_profile_info": (i32, [P, P, P, P]),
         "sad_get_stats": (i32, [P, P, P]),

@@ -59,9 +59,6 @@ struct Traits {
 #ifndef SAD_TC_XBUFS
 #define SAD_TC_XBUFS 2
 #endif
-#ifndef SAD_TC_NOBAR
-#define SAD_TC_NOBAR 0       // 1: epilogue warps add their row / column partials to T directly (no barriers)
-#endif
     static constexpr int STAGES = CG == 1 ? (KIND == 0 ? 2 : 3) : (DEEP ? 5 : SAD_TC_STAGES2);   // (one-CTA tiles: reference variants)
     static constexpr int XBUFS = DEEP ? 1 : SAD_TC_XBUFS;   // K6 staging buffers
     static constexpr int B_BYTES = BNC * BK;
@@ -238,25 +235,13 @@ __device__ __forceinline__ void tc_commit_pair_elect(uint64_t *bar) {
 // posts the expect_tx of both CTAs' bytes on its full barrier
 __device__ __forceinline__ void tma_stage_pair(const CUtensorMap *mA, const CUtensorMap *mB, uint64_t *bar, void *dA,
                                                void *dB, int c0, int rA, int rB, uint32_t expect) {
-#ifndef SAD_TC_OP_POLICY
-#define SAD_TC_OP_POLICY 0   // 1: operand tiles loaded with an L2 evict-last policy (experiment)
-#endif
-#if SAD_TC_OP_POLICY
-#define SAD_TC_OP_HINT ".L2::cache_hint"
-#define SAD_TC_OP_POL ", pol"
-#define SAD_TC_OP_MKPOL "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-#else
-#define SAD_TC_OP_HINT ""
-#define SAD_TC_OP_POL ""
-#define SAD_TC_OP_MKPOL ""
-#endif
     asm volatile(
-        "{\n\t.reg .pred e, l;\n\t.reg .b64 pol;\n\t" SAD_TC_OP_MKPOL
+        "{\n\t.reg .pred e, l;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.and.b32 l, %7, 0, e;\n\t"
         "@l mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %7;\n\t"
-        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes" SAD_TC_OP_HINT " [%3], [%0, {%5, %6}], [%9]" SAD_TC_OP_POL ";\n\t"
-        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes" SAD_TC_OP_HINT " [%4], [%1, {%5, %8}], [%9]" SAD_TC_OP_POL ";\n}" ::"l"(
+        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%3], [%0, {%5, %6}], [%9];\n\t"
+        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%4], [%1, {%5, %8}], [%9];\n}" ::"l"(
             reinterpret_cast<uint64_t>(mA)),
         "l"(reinterpret_cast<uint64_t>(mB)), "r"(smem_u32(bar)), "r"(smem_u32(dA)), "r"(smem_u32(dB)), "r"(c0), "r"(rA),
         "r"(expect), "r"(rB), "r"(smem_u32(bar) & kPeerMask)
@@ -310,23 +295,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 384;" ::: "memory"); }
 
-// SAD_TC_DBG_PROF (timing experiment): clock64 cycles each role spends waiting, printed by two
-// CTA pairs at the end of the launch
-#ifdef SAD_TC_DBG_PROF
-#define TC_TW(acc, stmt)                  \
-    {                                     \
-        const long long _c0 = clock64();  \
-        stmt;                             \
-        acc += clock64() - _c0;           \
-    }
-#define TC_PROF_PRINT(role, a, b, c)                                                                          \
-    if (blockIdx.x < 2 || blockIdx.x == gridDim.x - 1)                                                      \
-        printf("tcprof blk %d %s total %lld waitA %lld waitB %lld\n", (int)blockIdx.x, role, (long long)(a), \
-               (long long)(b), (long long)(c));
-#else
-#define TC_TW(acc, stmt) stmt
-#define TC_PROF_PRINT(role, a, b, c)
-#endif
 
 // global inputs of one tile's epilogue for one thread (row = its TMEM lane, column e < BN for the
 // shared colinfo row)
@@ -430,8 +398,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             // ===== TMA producer (pairs: the whole warp runs the loop, one elected lane issues) =====
             int stage = 0;
             uint32_t phase = 0;
-            long long pw0 = 0, pw1 = 0;
-            const long long pst = clock64();
             for (int64_t t = t0; t < P.n_tiles; t += tstep) {
                 const TcTile tl = P.tiles[t];
                 const int rowA = (int)(P.shard_rowpad[tl.s] + (int64_t)tl.I * BMT + (int64_t)crank * BM);
@@ -440,17 +406,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                                        (int64_t)crank * (CG == 2 && tl.pad > 0 ? tl.pad / 2 : BNC));
                 const int nkb = (int)P.kblocks[tl.s];
                 for (int kb = 0; kb < nkb; ++kb) {
-                    TC_TW(pw0, mbar_wait(&empty[stage], phase ^ 1));
+                    mbar_wait(&empty[stage], phase ^ 1);
                     if constexpr (CG == 1) {
                         mbar_expect_tx(&full[stage], STAGE_BYTES);
                         tma_load_2d(&tmapA, &full[stage], sA + stage * A_BYTES, kb * BK, rowA);
                         tma_load_2d(&tmapB, &full[stage], sB + stage * B_BYTES, kb * BK, rowB);
                     } else {
-#ifdef SAD_TC_DBG_NOTMA
-                        if (leader && lane == 0) mbar_arrive(&full[stage]);   // timing experiment: no loads (wrong results)
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                        continue;
-#endif
                         // the leader's full barrier counts the bytes of both CTAs
                         tma_stage_pair(&tmapA, &tmapB, &full[stage], sA + stage * A_BYTES, sB + stage * B_BYTES, kb * BK,
                                        rowA, rowB, leader ? 2u * STAGE_BYTES : 0u);
@@ -458,7 +419,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
-            if (lane == 0) TC_PROF_PRINT("tma(empty)", clock64() - pst, pw0, pw1);
         }
     } else if (warp == 1) {
         if (leader && (CG == 2 || lane == 0)) {
@@ -467,28 +427,22 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            long long pw0 = 0, pw1 = 0;
-            const long long pst = clock64();
             for (int64_t t = t0; t < P.n_tiles; t += tstep) {
                 const TcTile tl = P.tiles[t];
                 const int nkb = (int)P.kblocks[tl.s];
                 // MMA N of this tile (edge tiles: only the columns that hold real rows)
                 const uint32_t idesc = tl.pad > 0 ? ((Tr::IDESC & ~(0x3Fu << 17)) | ((uint32_t)(tl.pad >> 3) << 17))
                                                   : Tr::IDESC;
-                TC_TW(pw0, mbar_wait(&tempty[acc], acc_phase ^ 1));
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + (uint32_t)(acc * ACC_COLS);
                 for (int kb = 0; kb < nkb; ++kb) {
-                    TC_TW(pw1, mbar_wait(&full[stage], phase));
+                    mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
                     if constexpr (CG == 2) {
-#ifdef SAD_TC_DBG_NOMMA
-                        tc_commit_pair_elect(&empty[stage]);       // timing experiment: no MMAs (wrong results)
-#else
                         mma_stage_pair<KIND>(d, sw128_desc(a0), sw128_desc(b0), idesc, kb != 0,
                                              tmem_base + Tr::SF_COL, &empty[stage]);
-#endif
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                         continue;
                     }
@@ -496,9 +450,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     for (int kk = 0; kk < BK / 32; ++kk) {
                         const uint64_t ad = sw128_desc(a0 + kk * 32), bd = sw128_desc(b0 + kk * 32);
                         const uint32_t accf = (kb | kk) != 0;
-#ifdef SAD_TC_DBG_NOMMA
-                        if (kb >= 0) continue;       // timing experiment: no MMAs (wrong results)
-#endif
                         if constexpr (CG == 1) {
                             if constexpr (KIND == 0) mma_i8(d, ad, bd, Tr::IDESC, accf);
                             else mma_mxf4(d, ad, bd, Tr::IDESC, accf, tmem_base + Tr::SF_COL, tmem_base + Tr::SF_COL);
@@ -513,7 +464,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                 if constexpr (CG == 1) tc_commit(&tfull[acc]); else tc_commit_pair_elect(&tfull[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
-            if (lane == 0) TC_PROF_PRINT("mma(tempty,full)", clock64() - pst, pw0, pw1);
         }
     } else if (warp == 3) {
         if (P.xrow) {
@@ -522,8 +472,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             // [row][XSTRIDE] buffer; the copies complete the buffer's mbarrier =====
             int xb = 0;
             uint32_t xph = 0;
-            long long pw0 = 0, pw1 = 0;
-            const long long pst = clock64();
             for (int64_t t = t0; t < P.n_tiles; t += tstep) {
                 const TcTile tl = P.tiles[t];
                 const int64_t rbase = P.shard_base[tl.s];
@@ -537,7 +485,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     const int64_t row = (int64_t)tl.I * BMT + (int64_t)crank * BM + u * 32 + lane;
                     src[u] = (row < w && P.xrow[rbase + row].x) ? P.E + P.ebase[tl.s] + row * wp + col0 : P.zero;
                 }
-                TC_TW(pw0, mbar_wait(&xempty[xb], xph ^ 1));
+                mbar_wait(&xempty[xb], xph ^ 1);
                 if (lane == 0) mbar_expect_tx(&xfull[xb], (uint32_t)BM * nbytes);
                 __syncwarp();
                 uint8_t *xd = xbuf + xb * Tr::XBUF_BYTES;
@@ -545,7 +493,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                 for (int u = 0; u < 4; ++u) bulk_g2s(xd + (u * 32 + lane) * Tr::XSTRIDE, src[u], nbytes, &xfull[xb]);
                 if (++xb == Tr::XBUFS) { xb = 0; xph ^= 1; }
             }
-            if (lane == 0) TC_PROF_PRINT("stage(xempty)", clock64() - pst, pw0, pw1);
         }
     } else if (warp >= 4) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REG_EPILOGUE));
@@ -567,8 +514,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
         cur.tl = t0 < P.n_tiles ? P.tiles[t0] : tnone;
         nxt.tl = t0 + tstep < P.n_tiles ? P.tiles[t0 + tstep] : tnone;
         epi_pre_rows<BN, BMT>(P, cur, crank, quarter, lane, e);
-        long long pw0 = 0, pw1 = 0, pw2 = 0;
-        const long long pst = clock64();
         for (int64_t t = t0; t < P.n_tiles; t += tstep) {
             const TcTile tl = cur.tl;
             const TcTile tl2 = t + 2 * tstep < P.n_tiles ? P.tiles[t + 2 * tstep] : tnone;
@@ -576,11 +521,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             const int64_t rbase = P.shard_base[tl.s];
             const int64_t w = P.shard_base[tl.s + 1] - rbase;
             const int64_t col0 = (int64_t)tl.J * BN, row0 = (int64_t)tl.I * BMT + (int64_t)crank * BM;
-#if !SAD_TC_NOBAR
-            TC_TW(pw1, epi_bar());                // previous tile's colinfo / colsum / rowpart consumed
+            epi_bar();                // previous tile's colinfo / colsum / rowpart consumed
             if (e < BN) colinfo[e] = cur.ci;
-            TC_TW(pw1, epi_bar());
-#endif
+            epi_bar();
             const int64_t row = row0 + quarter * 32 + lane;
             const bool vrow = row < w;
             const RowInfo ri = cur.ri;
@@ -590,42 +533,19 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             uint16_t *simr = (P.sim && vrow) ? P.sim + P.sim_base[tl.s] : nullptr;
             // K6: this tile's excess bytes of this row, staged by warp 3
             const uint8_t *xrow_s = xbuf + xb * Tr::XBUF_BYTES + (quarter * 32 + lane) * Tr::XSTRIDE;
-            if (P.xrow) TC_TW(pw2, mbar_wait(&xfull[xb], xph));
-            TC_TW(pw0, mbar_wait(&tfull[acc], acc_phase));
+            if (P.xrow) mbar_wait(&xfull[xb], xph);
+            mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             unsigned long long rowsum = 0;
             const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * ACC_COLS);
-#ifdef SAD_TC_DBG_SPIN
-            {   // timing experiment: SAD_TC_DBG_SPIN iterations of 4 independent integer chains per thread
-                uint32_t a0 = lane, a1 = lane + 1, a2 = lane + 2, a3 = lane + 3;
-#pragma unroll 4
-                for (int i = 0; i < SAD_TC_DBG_SPIN; ++i) {
-                    a0 = a0 * 0x9E3779B1u + 7u; a1 = a1 * 0x85EBCA77u + 5u;
-                    a2 = a2 * 0xC2B2AE3Du + 3u; a3 = a3 * 0x27D4EB2Fu + 1u;
-                }
-                if ((a0 ^ a1 ^ a2 ^ a3) == 0x12345u) rowsum += 1;
-            }
-#endif
 #pragma unroll 1
-#ifdef SAD_TC_DBG_NOEPI
-            for (int ch = ch0; ch < ch0; ++ch) {     // timing experiment: no epilogue work (wrong results)
-#else
             for (int ch = ch0; ch < ch1; ++ch) {
-#endif
                 uint32_t v[16];
                 if (tl.pad > 0 && ch * 16 >= tl.pad) {   // edge tile: no real column in this chunk
                     if (has_next && ch == ch0) epi_pre_rows<BN, BMT>(P, nxt, crank, quarter, lane, e);
                     continue;
                 }
-#ifdef SAD_TC_DBG_NOTLD
-                for (int j = 0; j < 16; ++j) v[j] = (uint32_t)(ch * 16 + j + lane);   // timing experiment: no TMEM loads
-#else
                 tmem_ld16(tbase + ch * 16, v);
-#endif
-#ifdef SAD_TC_DBG_TLDONLY
-                if (v[0] == 0xFFFFFFFFu && v[15] == 0xFFFFFFFEu) rowsum += v[3];        // timing experiment: TMEM loads only
-                continue;
-#endif
                 if (has_next && ch == ch0) epi_pre_rows<BN, BMT>(P, nxt, crank, quarter, lane, e);
                 if constexpr (KIND == 1) {
                     // fp32 accumulators hold exact integers < 2^23: adding 2^23 puts the value in the
@@ -634,7 +554,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + 8388608.0f) - 0x4B000000u;
                 }
                 // S = capped-layer contraction + excess e_ij, before the fixed point
-#ifndef SAD_TC_DBG_NOXADD
                 if (P.xrow) {
                     const uint4 ex = *reinterpret_cast<const uint4 *>(xrow_s + ch * 16);
                     if (ex.x | ex.y | ex.z | ex.w) {
@@ -643,18 +562,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                         for (int j = 0; j < 16; ++j) v[j] += (ew[j >> 2] >> (8 * (j & 3))) & 0xFFu;
                     }
                 }
-#endif
                 unsigned long long cv[16];
                 if (interior && !P.sim) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         // length order: every column of a tile strictly above the diagonal is at
                         // least as long as the row, so the pair's denominator is the row's
-#ifdef SAD_TC_DBG_NOFQ
-                        const uint64_t q = v[j];    // timing experiment: no fixed point (wrong results)
-#else
                         const uint64_t q = fixed_q_nd(v[j], ri.tw, nd, ri.qd, ri.rp);
-#endif
                         rowsum += q;
                         cv[j] = q;
                     }
@@ -681,11 +595,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                         const bool ok = vrow && col < w && col >= row;
                         // the self term is exactly 2^32 (reading A3: S_ii = den_ii = L_i - k + 1)
                         const uint32_t S = col == row ? ri.tw : v[j];
-#if SAD_TC_NOBAR
-                        const RowInfo cj = col < w ? P.rowinfo[rbase + col] : RowInfo{1u, 0xFFFFFFFFu, 1u, 0u};
-#else
                         const RowInfo cj = colinfo[ch * 16 + j];
-#endif
                         const uint64_t q = pair_q(ok ? S : 0u, ri, cj);
                         rowsum += q;
                         cv[j] = (col != row) ? q : 0ull;
@@ -696,10 +606,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                         }
                     }
                 }
-#ifdef SAD_TC_DBG_NOSHFL
-                if (!(lane & 1)) colsum[quarter * 256 + ch * 16 + ((lane >> 1) & 15)] = cv[lane & 15];
-                continue;                    // timing experiment: no column reduction (wrong results)
-#endif
                 // warp transpose-reduce: after offsets 16, 8, 4, 2 lane l holds column (l >> 1) & 15
                 // summed over the 16 lanes sharing bit 0; offset 1 completes the 32-lane sum.
 #pragma unroll
@@ -730,16 +636,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                     cv[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 2);
                 }
                 cv[0] += __shfl_xor_sync(0xffffffffu, cv[0], 1);
-#if SAD_TC_NOBAR
-                // this warp's 32-row partial of column (lane >> 1) & 15 straight into T (u64 RED; the
-                // four row quarters and the two CTAs add theirs independently: integer addition)
-                if (!(lane & 1)) {
-                    const int64_t col = col0 + ch * 16 + ((lane >> 1) & 15);
-                    if (col < w && cv[0]) atomicAdd(&P.T[rbase + P.rowinfo[rbase + col].shard], cv[0]);
-                }
-#else
                 if (!(lane & 1)) colsum[quarter * 256 + ch * 16 + ((lane >> 1) & 15)] = cv[0];
-#endif
             }
             tc_fence_before();
             __syncwarp();
@@ -749,11 +646,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
             }
             if (++xb == Tr::XBUFS) { xb = 0; xph ^= 1; }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-#if SAD_TC_NOBAR
-            if (vrow && rowsum) atomicAdd(&P.T[rbase + ri.shard], rowsum);       // .shard: local index
-#else
             if (grp) rowpart[(grp - 1) * 128 + quarter * 32 + lane] = rowsum;
-            TC_TW(pw1, epi_bar());
+            epi_bar();
             if (grp == 0) {
                 rowsum += rowpart[quarter * 32 + lane] + rowpart[128 + quarter * 32 + lane];
                 if (vrow && rowsum) atomicAdd(&P.T[rbase + ri.shard], rowsum);   // .shard: local index
@@ -763,13 +657,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
                 const unsigned long long cs = colsum[e] + colsum[256 + e] + colsum[512 + e] + colsum[768 + e];
                 if (col < w && cs) atomicAdd(&P.T[rbase + colinfo[e].shard], cs);
             }
-#endif
             cur = nxt;
             nxt.tl = tl2;
-        }
-        if (lane == 0 && (warp == 4 || warp == 15)) {
-            TC_PROF_PRINT(warp == 4 ? "epi4(tfull,bar)" : "epi15(tfull,bar)", clock64() - pst, pw0, pw1);
-            TC_PROF_PRINT(warp == 4 ? "epi4(xfull)" : "epi15(xfull)", 0, pw2, 0);
         }
     }
     tc_fence_before();
@@ -790,46 +679,41 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_syrk_tc(const __grid_constan
 // ---------------------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
+// Checked on the CURRENT device (every ABI call runs on its context's device): an sm_100 part, the
+// driver's tensor-map encoder (fetched once per process) and the kernels' shared memory opt-in
+// (per device, smem_optin).
 bool tc_supported(std::string &why) {
     static std::once_flag once;
-    static bool ok = false;
-    static std::string reason;
     std::call_once(once, [] {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceProp prop{};
-        if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
-            reason = "no CUDA device";
-            return;
-        }
-        if (prop.major != 10) {
-            reason = "needs sm_100 (B200)";
-            return;
-        }
         void *fn = nullptr;
         cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
-            reason = "cuTensorMapEncodeTiled unavailable";
-            return;
-        }
-        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-        if (cudaFuncSetAttribute(k_syrk_tc<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::Traits<0, 1>::SMEM_BYTES) != cudaSuccess ||
-            cudaFuncSetAttribute(k_syrk_tc<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::Traits<1, 1>::SMEM_BYTES) != cudaSuccess ||
-            cudaFuncSetAttribute(k_syrk_tc<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::Traits<0, 2>::SMEM_BYTES) != cudaSuccess ||
-            cudaFuncSetAttribute(k_syrk_tc<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::Traits<1, 2>::SMEM_BYTES) != cudaSuccess ||
-            cudaFuncSetAttribute(k_syrk_tc<1, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::Traits<1, 2, true>::SMEM_BYTES) != cudaSuccess) {
-            reason = "cannot reserve shared memory";
-            return;
-        }
-        ok = true;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess && fn)
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     });
-    why = reason;
-    return ok;
+    int dev = 0, major = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) {
+        why = "no CUDA device";
+        return false;
+    }
+    if (major != 10) {
+        why = "needs sm_100 (B200)";
+        return false;
+    }
+    if (!g_encode) {
+        why = "cuTensorMapEncodeTiled unavailable";
+        return false;
+    }
+    if (smem_optin(k_syrk_tc<0, 1>, tc::Traits<0, 1>::SMEM_BYTES) != cudaSuccess ||
+        smem_optin(k_syrk_tc<1, 1>, tc::Traits<1, 1>::SMEM_BYTES) != cudaSuccess ||
+        smem_optin(k_syrk_tc<0, 2>, tc::Traits<0, 2>::SMEM_BYTES) != cudaSuccess ||
+        smem_optin(k_syrk_tc<1, 2>, tc::Traits<1, 2>::SMEM_BYTES) != cudaSuccess ||
+        smem_optin(k_syrk_tc<1, 2, true>, tc::Traits<1, 2, true>::SMEM_BYTES) != cudaSuccess) {
+        why = "cannot reserve shared memory";
+        return false;
+    }
+    why.clear();
+    return true;
 }
 
 int tc_bn(int kind) { return kind == 0 ? tc::Traits<0>::BN : tc::Traits<1>::BN; }

@@ -232,10 +232,8 @@ __global__ void __launch_bounds__(kXrWarps * 32, SAD_XR_MINB) k_xrows_g(ExcessAr
                 const uint32_t mask = __ballot_sync(0xffffffffu, hit);
                 if (!mask) continue;
                 if (!zeroed) {                    // the row's upper part, once
-#ifndef SAD_XR_DBG_NOZERO
                     for (int c = (int)((local + 1) >> 4) + lane; c < nch; c += 32)
                         reinterpret_cast<uint4 *>(erow)[c] = make_uint4(0, 0, 0, 0);
-#endif
                     zeroed = true;
                     __syncwarp();                 // orders the zeros before every lane's atomics
                 }
@@ -280,13 +278,9 @@ __global__ void __launch_bounds__(kXrWarps * 32, SAD_XR_MINB) k_xrows_g(ExcessAr
 #pragma unroll
                     for (int u = 0; u < SAD_XR_BATCH; ++u) {
                         const uint32_t b = vb[u] >> 8;
-#ifdef SAD_XR_DBG_NORED
-                        if (xa[u] && b > local && (vb[u] & 0xFFu) == 0xFFu) erow[0] = 1;   // timing experiment
-#else
                         if (xa[u] && b > local)
                             atomicAdd(reinterpret_cast<uint32_t *>(erow + (b & ~3u)),
                                       min(xa[u], vb[u] & 0xFFu) << (8u * (b & 3u)));
-#endif
                     }
                 }
                 __syncwarp();
@@ -323,11 +317,7 @@ int launch_excess(const ExcessArgs &a, cudaStream_t st) {
     const int warps = (int)std::min<int64_t>(kXrWarps, (int64_t)kXrSmem / a.accb);
     if (warps < 1) return -1;
     const size_t smem = (size_t)warps * a.accb;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_xrows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kXrSmem);
-        configured = true;
-    }
+    smem_optin(k_xrows, (size_t)kXrSmem);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

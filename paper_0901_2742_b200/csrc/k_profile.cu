@@ -375,13 +375,7 @@ void launch_profile(const ProfileArgs &a, cudaStream_t st) {
     const int warps = (int)std::max<size_t>(1, std::min<size_t>(kProfWarps, (size_t)(220 * 1024 / SAD_PROF_MINB) / per_warp));
     const size_t smem = per_warp * warps;
     auto kern = a.k == 3 ? k_profile<3> : a.k == 6 ? k_profile<6> : k_profile<0>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_profile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_profile<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_profile<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = true;
-    }
+    smem_optin(kern, 200 * 1024);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -667,11 +661,7 @@ __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int 
 void launch_indicator(const OperandArgs &a, cudaStream_t st) {
     const int slice = (int)std::min<int64_t>(a.stride, kRowSlice);
     const size_t smem = (size_t)kOpWarps * slice;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(k_indicator, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
+    smem_optin(k_indicator, smem);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -711,11 +701,7 @@ __global__ void __launch_bounds__(kOpThreads) k_dense_counts(OperandArgs a) {
 
 void launch_dense_counts(const OperandArgs &a, cudaStream_t st) {
     const size_t smem = (size_t)a.stride;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(k_dense_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
+    smem_optin(k_dense_counts, smem);
     if (a.rows_pad > 0) k_dense_counts<<<(unsigned)a.rows_pad, kOpThreads, smem, st>>>(a);
 }
 

@@ -198,11 +198,7 @@ __global__ void __launch_bounds__(kRankThreads) k_rank_vs_ga(RankArgs a) {
 
 void launch_rank_vs_ga(const RankArgs &a, cudaStream_t st) {
     const size_t smem = (size_t)a.V * 2;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(k_rank_vs_ga, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
+    smem_optin(k_rank_vs_ga, smem);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -285,11 +281,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanArgs a) {
 
 void launch_plan(const PlanArgs &a, cudaStream_t st) {
     const size_t smem = (size_t)(a.p * (a.p - 1) + a.p) * 8;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
+    smem_optin(k_plan, smem);
     k_plan<<<a.pl, kPlanThreads, smem, st>>>(a);
 }
 
@@ -692,11 +684,7 @@ __global__ void __launch_bounds__(256) k_rank_vs_samples(RankArgs a, int m, unsi
 int launch_rank_vs_samples(const RankArgs &a, int m, unsigned long long *Tp, int num_sms, cudaStream_t st) {
     const size_t smem = (size_t)a.V * kSmpG;
     if (smem > 200 * 1024) return -1;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_rank_vs_samples, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = true;
-    }
+    smem_optin(k_rank_vs_samples, 200 * 1024);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rank_vs_samples, 256, smem);
     const int groups = (m + kSmpG - 1) / kSmpG;

@@ -42,12 +42,7 @@ template <typename K>
 static int block_sort(const K *ki, const int32_t *vi, int n, K *ko, int32_t *vo, int b0, int b1, cudaStream_t st) {
     using BRS = cub::BlockRadixSort<K, kSortThreads, kSortItems, int32_t>;
     const size_t smem = sizeof(typename BRS::TempStorage);
-    static bool configured = false;
-    if (!configured) {
-        if (cudaFuncSetAttribute(k_block_sort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return -1;
-        configured = true;
-    }
+    if (smem_optin(k_block_sort<K>, smem) != cudaSuccess) return -1;
     k_block_sort<K><<<1, kSortThreads, smem, st>>>(ki, vi, n, ko, vo, b0, b1);
     return 0;
 }
@@ -107,13 +102,8 @@ static int seg_sort(const K *ki, const int32_t *vi, const int64_t *seg, int nseg
                     cudaStream_t st) {
     using BRS = SegSort;
     const size_t smem = sizeof(typename BRS::TempStorage);
-    static bool configured = false;
     if (end_bit > 32) return -1;
-    if (!configured) {
-        if (cudaFuncSetAttribute(k_seg_sort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return -1;
-        configured = true;
-    }
+    if (smem_optin(k_seg_sort<K>, smem) != cudaSuccess) return -1;
     k_seg_sort<K><<<nseg, kSegThreads, smem, st>>>(ki, vi, seg, ko, vo, end_bit, 1);
     return 0;
 }
@@ -153,13 +143,8 @@ template <typename K>
 static int seg_sort_runs(K *ki, int32_t *vi, const int64_t *seg, int nseg, int nruns, int64_t n, K *ko, int32_t *vo,
                          int end_bit, cudaStream_t st) {
     const size_t smem = sizeof(typename SegSort::TempStorage);
-    static bool configured = false;
     if (end_bit > 32) return -1;
-    if (!configured) {
-        if (cudaFuncSetAttribute(k_seg_sort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return -1;
-        configured = true;
-    }
+    if (smem_optin(k_seg_sort<K>, smem) != cudaSuccess) return -1;
     k_seg_sort<K><<<nseg * nruns, kSegThreads, smem, st>>>(ki, vi, seg, ki, vi, end_bit, nruns);
     const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
     if (g > 0) k_merge_runs<K><<<(unsigned)g, 256, 0, st>>>(ki, vi, seg, nseg, nruns, n, ko, vo);

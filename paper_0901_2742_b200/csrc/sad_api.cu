@@ -60,12 +60,13 @@ int fail(sad_ctx *c, int code, const char *fmt, ...) {
                         __FILE__, __LINE__);                                                \
     } while (0)
 
+// argument / state checks of every context call, then the context's device made current for the
+// rest of the call (restored on return: the caller's current device is left as it was)
 #define GUARD(min_stage)                                                                    \
-    do {                                                                                    \
-        if (!ctx) return SAD_E_ARG;                                                         \
-        if (ctx->sticky) return SAD_E_STATE;                                                \
-        if (ctx->stage < (min_stage)) return fail(ctx, SAD_E_STATE, "call order: stage %d < %d", ctx->stage, (min_stage)); \
-    } while (0)
+    if (!ctx) return SAD_E_ARG;                                                             \
+    if (ctx->sticky) return SAD_E_STATE;                                                    \
+    if (ctx->stage < (min_stage)) return fail(ctx, SAD_E_STATE, "call order: stage %d < %d", ctx->stage, (min_stage)); \
+    DeviceScope dev_scope_(ctx->cfg.device)
 
 // shard bases of this rank under the block split of reading A15
 void shard_layout(const sad_ctx *c, int64_t n_global, std::vector<int64_t> &sb) {
@@ -263,10 +264,12 @@ int sad_create(const sad_config *cfg, sad_ctx **out) {
     ctx->use_tc = !(cfg->flags & SAD_F_KERNEL_ALU);
     ctx->tc_kind = (cfg->flags & SAD_F_TC_INT8) ? 0 : 1;
     ctx->tc_cg = (cfg->flags & SAD_F_TC_1SM) ? 1 : 2;
-    if (cudaSetDevice(cfg->device) != cudaSuccess) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) {
         delete ctx;
         return SAD_E_CUDA;
     }
+    DeviceScope dev_scope_(cfg->device);
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
     if (cudaMallocHost(&ctx->h_small, 65536 * sizeof(unsigned long long)) != cudaSuccess) {
         delete ctx;
@@ -298,6 +301,7 @@ int sad_create(const sad_config *cfg, sad_ctx **out) {
 
 void sad_destroy(sad_ctx *ctx) {
     if (!ctx) return;
+    DeviceScope dev_scope_(ctx->cfg.device);
     if (ctx->st) cudaStreamSynchronize(ctx->st); else cudaDeviceSynchronize();
     for (auto &v : {&ctx->ev_pairs_ap, &ctx->ev_pairs_op, &ctx->ev_free})
         for (auto &e : *v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
@@ -396,11 +400,7 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
     const cudaMemcpyKind kind = mem == SAD_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     // host inputs of a few MB or more: the residues are copied in chunks on the internal stream and
     // each chunk's k-mer counts (K1/K2) start on ctx->st as soon as it has landed (below)
-    static const int nch_env = [] {        // SAD_LOAD_CHUNKS=0 disables the pipeline (experiments)
-        const char *e = getenv("SAD_LOAD_CHUNKS");
-        return e ? std::max(0, std::min(atoi(e), (int)sad_ctx::kLoadChunks)) : 4;
-    }();
-    const int nch = nch_env;
+    const int nch = 4;                     // chunks of a pipelined host load (16 max; 4 measured best)
     const bool pipelined = nch > 0 && mem == SAD_MEM_HOST && R >= (int64_t(4) << 20) && n_local >= 64 * nch;
     ctx->profiled = false;
     if (R > 0 && !pipelined) CK(cudaMemcpyAsync(ctx->d_ascii, ascii, (size_t)R, kind, ctx->st));
@@ -411,8 +411,9 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
         CK(cudaMemcpyAsync(ctx->d_off, offsets, sizeof(int64_t) * (size_t)(n_local + 1), kind, ctx->st));
     }
     // small per-shard tables (uploaded only when the layout changes)
+    // (the carve places the tables behind the R-sized residue buffer, so R is part of the key)
     const bool same = ctx->tbl_ws == base && ctx->tbl_n == n_local && ctx->tbl_ng == n_global &&
-                      ctx->tbl_first == first_source_index;
+                      ctx->tbl_first == first_source_index && ctx->tbl_R == R;
     if (!same) {
         int64_t *tbl = reinterpret_cast<int64_t *>(ctx->h_small + 32768);
         int64_t simb = 0, tiles = 0;
@@ -462,6 +463,7 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
         ctx->tbl_n = n_local;
         ctx->tbl_ng = n_global;
         ctx->tbl_first = first_source_index;
+        ctx->tbl_R = R;
         need_sync = true;
     }
     ctx->launches_step = 0;
@@ -699,12 +701,6 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     unsigned long long *xtot = reinterpret_cast<unsigned long long *>(ctx->d_xoff + (size_t)pl * ctx->V + 1) ;
     xtot = reinterpret_cast<unsigned long long *>(rup(reinterpret_cast<int64_t>(xtot), 8));
     record_pair(ctx, ctx->ev_pairs_op, true);
-    // SAD_OP_TIMELINE=1 (experiments): events inside the operand stage, printed to stderr
-    static const bool op_tl = getenv("SAD_OP_TIMELINE") != nullptr;
-    static cudaEvent_t tl[6] = {};
-    if (op_tl && !tl[0])
-        for (auto &e : tl) cudaEventCreate(&e);
-    if (op_tl) cudaEventRecord(tl[0], ctx->st);
     if (ctx->use_tc) {
         // K3 under the layer caps (the length order sigma was computed by sad_build_profiles);
         // K6 list offsets and lists; K4 beside K6 rows (side stream)
@@ -738,30 +734,18 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
             x.ebase = ctx->d_ebase;
             x.sigma = ctx->d_sigma;
             x.sigma_inv = ctx->d_sigma_inv;
-            if (op_tl) cudaEventRecord(tl[1], ctx->st);
             launch_xfill(x, ctx->d_xcur, ctx->st);
             LAUNCHED();
-            if (op_tl) cudaEventRecord(tl[2], ctx->st);
             // K6 rows on the side stream, concurrently with K4 (both only read the CSR / lists)
             CK(cudaEventRecord(ctx->ev_fork, ctx->st));
             CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
             if (launch_excess(x, ctx->side)) return fail(ctx, SAD_E_ARG, "K6: shard too wide for the row accumulators");
             LAUNCHED();
             CK(cudaEventRecord(ctx->ev_join, ctx->side));
-            if (op_tl) cudaEventRecord(tl[3], ctx->side);
         }
         launch_indicator(o, ctx->st);
         LAUNCHED();
-        if (op_tl) cudaEventRecord(tl[4], ctx->st);
         if (lists) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_join, 0));
-        if (op_tl && lists) {
-            cudaEventRecord(tl[5], ctx->st);
-            cudaEventSynchronize(tl[5]);
-            float m[5];
-            for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&m[i], tl[0], tl[i + 1]);
-            fprintf(stderr, "optl capscans %.4f xfill %.4f K6-end %.4f K4-end %.4f join %.4f ms\n", m[0], m[1], m[2],
-                    m[3], m[4]);
-        }
     } else {
         launch_dense_counts(o, ctx->st);
         LAUNCHED();
@@ -807,7 +791,6 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     ap.n_tiles_tc = ctx->tc_tiles_n;
     ap.cg = ctx->tc_cg;
     ap.xrow = lists ? ctx->d_xrow : nullptr;
-    if (getenv("SAD_DEBUG_SKIP_EXCESS_EPI")) ap.xrow = nullptr;   // timing experiment only: wrong S
     ap.E = E;
     ap.ebase = ctx->d_ebase;
     ap.zero = E ? E + ctx->h_ebase[pl] : nullptr;
@@ -1184,6 +1167,23 @@ int sad_get_bucket_sizes(sad_ctx *ctx, int64_t *h_sizes) {
     return SAD_OK;
 }
 
+int sad_get_load_report(sad_ctx *ctx, int64_t *h_report) {
+    GUARD(6);
+    if (!h_report) return SAD_E_ARG;
+    if (int rc = resolve_counts(ctx)) return rc;
+    const int p = ctx->cfg.p;
+    int64_t mb = 0;
+    for (int b = 0; b < p; ++b) mb = std::max(mb, ctx->bucket_sizes[b]);
+    const int64_t w = (ctx->n_global + p - 1) / p;               // the largest shard (reading A15)
+    h_report[0] = mb;
+    h_report[1] = w;
+    h_report[2] = 2 * w + p;
+    h_report[3] = mb <= 2 * w + p;
+    h_report[4] = (ctx->n_global % p == 0) && (w % p == 0);
+    h_report[5] = mb < 2 * w;
+    return SAD_OK;
+}
+
 static int shard_check(sad_ctx *ctx, int shard, int64_t cap, int64_t &b0, int64_t &w) {
     if (shard < 0 || shard >= ctx->pl) return fail(ctx, SAD_E_ARG, "bad shard %d", shard);
     b0 = ctx->shard_base[shard];
@@ -1259,7 +1259,9 @@ int sad_get_bucket(sad_ctx *ctx, int bucket, int64_t *h_idx, uint64_t *h_key, ui
     CK(cudaStreamSynchronize(ctx->st));
     if (n_out) *n_out = n;
     if (res_out) *res_out = r1 - r0;
-    if ((h_idx || h_key || h_offsets) && cap_seqs < n) return fail(ctx, SAD_E_CAPACITY, "bucket has %lld sequences", (long long)n);
+    if ((h_idx || h_key) && cap_seqs < n) return fail(ctx, SAD_E_CAPACITY, "bucket has %lld sequences", (long long)n);
+    if (h_offsets && cap_seqs < n + 1)       // the offsets take n + 1 entries
+        return fail(ctx, SAD_E_CAPACITY, "bucket offsets need %lld entries", (long long)(n + 1));
     if (h_res && cap_res < r1 - r0) return fail(ctx, SAD_E_CAPACITY, "bucket has %lld residues", (long long)(r1 - r0));
     std::vector<uint64_t> keys(n);
     if (n) CK(cudaMemcpyAsync(keys.data(), o.key + first, 8 * n, cudaMemcpyDeviceToHost, ctx->st));
@@ -1368,6 +1370,7 @@ int sad_get_profile_info(sad_ctx *ctx, int64_t *h_windows, int64_t *h_distinct, 
 int sad_get_stats(sad_ctx *ctx, double *h_ms, int64_t *h_counts) {
     if (!ctx) return SAD_E_ARG;
     if (ctx->sticky) return SAD_E_STATE;
+    DeviceScope dev_scope_(ctx->cfg.device);
     CK(cudaStreamSynchronize(ctx->st));
     for (auto *v : {&ctx->ev_pairs_ap, &ctx->ev_pairs_op}) {
         double &acc = v == &ctx->ev_pairs_ap ? ctx->ms_ap : ctx->ms_op;

@@ -325,6 +325,30 @@ void launch_distance64(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, d
 size_t upgma_workspace(int64_t n);
 void launch_upgma(double *D, int64_t n, int64_t *merges, double *heights, int64_t *sizes, void *ws, cudaStream_t st);
 
+// Dynamic shared memory opt-in (> 48 KB) of kernel `func` on the CURRENT device. The attribute is
+// per device, so the opt-in is remembered per (device, kernel) and only raised; thread-safe
+// (sad_util.cu).
+cudaError_t smem_optin_raw(const void *func, size_t bytes);
+template <class F>
+inline cudaError_t smem_optin(F *func, size_t bytes) {
+    return smem_optin_raw(reinterpret_cast<const void *>(func), bytes);
+}
+
+// Makes a context's device current for the duration of an ABI call and restores the caller's
+// device afterwards (every entry point runs on ctx->cfg.device, whatever the caller made current).
+struct DeviceScope {
+    int prev = -1, dev = -1;
+    explicit DeviceScope(int d) : dev(d) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceScope() {
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+    DeviceScope(const DeviceScope &) = delete;
+    DeviceScope &operator=(const DeviceScope &) = delete;
+};
+
 }  // namespace sad
 
 // ------------------------------------------------------------------------------------
@@ -415,7 +439,7 @@ struct sad_ctx {
 
     // layout of the last uploaded per-shard tables
     uint8_t *tbl_ws = nullptr;
-    int64_t tbl_n = -1, tbl_ng = -1, tbl_first = -1;
+    int64_t tbl_n = -1, tbl_ng = -1, tbl_first = -1, tbl_R = -1;
 
     // pinned host staging
     unsigned long long *h_small = nullptr;              // pinned, 4096 u64

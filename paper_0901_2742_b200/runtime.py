@@ -277,6 +277,13 @@ class Context:
         self._call("sad_get_bucket_sizes", _vp(out))
         return out
 
+    def load_report(self) -> dict:
+        """the largest bucket against the PSRS bound (sad_get_load_report)."""
+        r = np.zeros(6, np.int64)
+        self._call("sad_get_load_report", _vp(r))
+        return {"max_bucket": int(r[0]), "w": int(r[1]), "bound_2w_plus_p": int(r[2]), "holds": bool(r[3]),
+                "p_divides_w": bool(r[4]), "below_2w": bool(r[5])}
+
     # -- results -------------------------------------------------------------------------
     def out_keys(self) -> torch.Tensor:
         """uint64 keys (as int64) of all owned buckets, back to back, each in key order (device view)."""
@@ -322,10 +329,10 @@ class Context:
     def bucket(self, b: int):
         n, r = ctypes.c_int64(), ctypes.c_int64()
         self._call("sad_get_bucket", b, None, None, None, None, 0, 0, ctypes.byref(n), ctypes.byref(r))
-        idx, key = np.zeros(max(n.value, 1), np.int64), np.zeros(max(n.value, 1), np.uint64)
+        idx, key = np.zeros(n.value + 1, np.int64), np.zeros(n.value + 1, np.uint64)
         res, off = np.zeros(max(r.value, 1), np.uint8), np.zeros(n.value + 1, np.int64)
-        self._call("sad_get_bucket", b, _vp(idx), _vp(key), _vp(res), _vp(off), n.value, r.value, ctypes.byref(n),
-                   ctypes.byref(r))
+        self._call("sad_get_bucket", b, _vp(idx), _vp(key), _vp(res), _vp(off), n.value + 1, r.value,
+                   ctypes.byref(n), ctypes.byref(r))
         return idx[: n.value], key[: n.value], res[: r.value], off
 
     def bucket_view(self, b: int):

@@ -1,0 +1,121 @@
+"""Full-size parity: the CUDA path (libsad.so through the C ABI) against oracle goldens of
+BASELINE.json's five configs at their full sizes (tests/golden/full/*.json, written by
+tests/make_goldens.py, which calls only oracle/).
+
+For every layout the golden holds (config 1 p=2, config 2 p=8, config 3 p=2/4/8, config 4 p=8,
+config 5 p=1/2/4/8) the GPU run is compared element by element through SHA-256 digests:
+T_i (u64) per shard, S_i and den_i vs the GA per shard, the local sort order per shard, every
+bucket's sequence order, and the small outputs in full (local ancestors, GA, pivots, bucket
+sizes). A digest mismatch is reported with the golden's sampled values beside the GPU's.
+Layouts with p > 1 also run with G = 2, 4, 8 emulated ranks (p % G == 0) on the one GPU: the
+world > 1 device path (per-rank shards, pack, receive-side merge) must give the same bits.
+"""
+import glob
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from synth import gen
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = sorted(glob.glob(os.path.join(HERE, "golden", "full", "*.json")))
+
+
+def _load(path):
+    with open(path) as f:
+        return json.load(f)
+
+
+def _sha(a, dtype):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=dtype).tobytes()).hexdigest()
+
+
+def _input_sha(a, o):
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(a, dtype=np.uint8).tobytes())
+    h.update(np.ascontiguousarray(o, dtype="<i8").tobytes())
+    return h.hexdigest()
+
+
+def _inputs(g):
+    a, o = gen.generate(g["config"])
+    assert _input_sha(a, o) == g["input_sha256"], "synth/gen.py no longer reproduces the golden's input"
+    return a, o
+
+
+def _expect(name, got, dtype, digest, pos, sample):
+    if _sha(got, dtype) != digest:
+        g = [int(got[i]) for i in pos]
+        bad = [(i, w, x) for i, w, x in zip(pos, sample, g) if w != x]
+        pytest.fail(f"{name}: digest differs; sampled (pos, golden, gpu) mismatches: {bad[:8]} of {len(pos)}")
+
+
+def _check(ctxs, g, G, sizes):
+    """ctxs[r] = the context of rank r (G ranks, p/G shards each)."""
+    p = g["p"]
+    pl = p // G
+    for r, c in enumerate(ctxs):
+        loc, ga = c.ancestors()
+        assert loc.tolist() == g["anc"], "local ancestors differ"
+        assert ga == g["ga"], "GA differs"
+        assert [int(x) & 0x7FFFFFFF for x in c.pivots()] == g["pivots"], "pivots differ"
+        for sl in range(pl):
+            s = r * pl + sl
+            sh = g["shards"][s]
+            pos = sh["sample_pos"]
+            _expect(f"T shard {s}", c.local_rank(sl), "<u8", sh["T"], pos, sh["T_sample"])
+            S, D, _ = c.ranks(sl)
+            _expect(f"S shard {s}", S.astype(np.int64), "<i8", sh["S"], pos, sh["S_sample"])
+            _expect(f"den shard {s}", D.astype(np.int64), "<i8", sh["den"], pos, sh["den_sample"])
+            _expect(f"sorted shard {s}", c.sorted(sl), "<i8", sh["sorted"], pos, sh["sorted_sample"])
+        for b in range(r * pl, (r + 1) * pl):
+            bk = g["buckets"][b]
+            idx = c.bucket(b)[0]
+            assert len(idx) == bk["n"], f"bucket {b} size"
+            _expect(f"bucket {b}", idx, "<i8", bk["order"], bk["sample_pos"], bk["order_sample"])
+    assert [int(x) for x in sizes] == g["bsize"], "bucket sizes differ"
+    # a12: the load report of the run (reading A23)
+    ld = g["load"]
+    assert max(int(x) for x in sizes) == ld["max_bucket"] and ld["holds"]
+
+
+def _ids():
+    return [os.path.basename(p)[:-5] for p in GOLDEN]
+
+
+@pytest.mark.parametrize("kernel", ["tc", "alu"])
+@pytest.mark.parametrize("path", GOLDEN, ids=_ids())
+def test_full_size_golden_one_gpu(path, kernel):
+    """All p shards on one GPU (the bench's launch configuration)."""
+    from paper_0901_2742_b200.runtime import Context
+    g = _load(path)
+    a, o = _inputs(g)
+    n = len(o) - 1
+    ctx = Context(g["alphabet"], g["k"], g["p"], kernel=kernel)
+    ctx.load(a, o, n, 0)
+    sizes = ctx.run()
+    _check([ctx], g, 1, sizes)
+    lr = ctx.load_report()
+    assert lr["max_bucket"] == g["load"]["max_bucket"] and lr["holds"]
+    assert lr["bound_2w_plus_p"] == g["load"]["bound_2w_plus_p"]
+    ctx.close()
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("path", GOLDEN, ids=_ids())
+def test_full_size_golden_emulated_ranks(path, G):
+    """G ranks emulated in one process (host-driven exchange, tests/test_gpu_multirank.py)."""
+    from tests.test_gpu_multirank import run_emulated
+    g = _load(path)
+    if g["p"] % G or g["p"] == 1:
+        pytest.skip("p % G != 0")
+    a, o = _inputs(g)
+    ctxs, sizes = run_emulated(a, o, g["alphabet"], g["k"], g["p"], G, "tc")
+    _check(ctxs, g, G, sizes)
+    for c in ctxs:
+        c.close()
