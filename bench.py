@@ -44,6 +44,8 @@ def parse():
                     help="ga: rank vs the global ancestor (north star); samples: SURVEY f1, vs the k*p samples")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time eager steps instead of one CUDA graph replay per step (world == 1)")
     return ap.parse_args()
 
 
@@ -194,15 +196,17 @@ def main():
     a_loc = np.ascontiguousarray(a[o[lo]: o[hi]])
     o_loc = np.ascontiguousarray(o[lo: hi + 1] - o[lo])
     dev = torch.device("cuda", local_rank)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)          # the context's own stream (graph capture needs a non-default one)
     d_a = torch.from_numpy(a_loc).to(dev)
     d_o = torch.from_numpy(o_loc).to(dev)
     h_a = torch.from_numpy(a_loc).pin_memory()
     h_o = torch.from_numpy(o_loc).pin_memory()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)       # 256 MB > 126 MB L2
 
+    # world > 1: the library's own NCCL communicator runs every exchange (collective API)
     ctx = Context(spec.alphabet, spec.k, p, world=world, rank=rank, device=local_rank, stream=stream,
-                  kernel=args.kernel, group=group, rank_mode=args.rank_mode)
+                  kernel=args.kernel, group=group, rank_mode=args.rank_mode, comm=world > 1)
+    R_glob = int(o[-1])
 
     def barrier():
         if world > 1:
@@ -213,21 +217,21 @@ def main():
 
     def step_device():
         ctx.load(d_a, d_o, n, lo, residues=R_loc)
-        ctx.run(sync=False)
+        ctx.run(sync=False, residues_global=R_glob)
 
     h_keys = None
 
     def step_e2e():
         nonlocal h_keys
         ctx.load(h_a.numpy(), h_o.numpy(), n, lo)                   # H2D from pinned host memory
-        sizes = ctx.run()
+        sizes = ctx.run(residues_global=R_glob)
         keys = ctx.out_keys()
         if h_keys is None or h_keys.shape != keys.shape:
             h_keys = torch.empty(keys.shape, dtype=keys.dtype, pin_memory=True)
         h_keys.copy_(keys)                                           # D2H of the step's result (pinned)
         return h_keys, sizes
 
-    def timed(fn, steps):
+    def timed(fn, steps, post=None):
         ev = []
         for _ in range(steps):
             barrier()
@@ -238,6 +242,9 @@ def main():
             fn()
             e.record(stream)
             ev.append((s, e))
+            if post is not None:                                    # after the step (untimed)
+                barrier()
+                post()
         barrier()
         ms = sum(s.elapsed_time(e) for s, e in ev)
         if world > 1:
@@ -248,10 +255,27 @@ def main():
 
     for _ in range(args.warmup):
         step_device()
+    graph = None
+    if world == 1 and not args.no_graph:
+        # the whole device-resident step (load .. partition) as ONE CUDA graph: no host
+        # synchronization and no launch gaps inside the step
+        barrier()
+        graph = ctx.capture_step(d_a, d_o, R_loc)
+        with torch.cuda.stream(stream):
+            graph.replay()
+        barrier()
+
+    def replay():
+        with torch.cuda.stream(stream):
+            graph.replay()
+
     ctx.reset_stats()
     clocks = ClockSampler(local_rank)
     clocks.start()
-    ms_dev = timed(step_device, args.steps)
+    if graph is not None:
+        ms_dev = timed(replay, args.steps, post=ctx.graph_account)
+    else:
+        ms_dev = timed(step_device, args.steps)
     clk = clocks.stop()
     st = ctx.stats()
     launches = st["launches"]
@@ -365,6 +389,9 @@ def main():
             "vs_baseline": None, "dtype": {"tc": "e2m1", "tc1": "e2m1", "tcfull": "e2m1", "tc8": "i8", "tc81": "i8", "tc8full": "i8",
                                                "alu": "u16"}[args.kernel], "data": "synthetic",
             "config": {"workload": workload_name(spec, p), "p": p, "kernel": args.kernel, "rank_mode": args.rank_mode,
+                       "step": ("one CUDA graph replay (sad_load .. sad_partition captured)" if graph is not None
+                                else "eager C-ABI calls (sad_load, sad_build_profiles, sad_rank, sad_partition)"),
+                       "exchange": "library NCCL communicator (collective API)" if world > 1 else "none (G = 1)",
                        "pairs_per_step": pairs_job,
                        "l2": "L2 flushed (256 MB write) before every timed step; operand working set > L2"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,

@@ -18,10 +18,25 @@
  *   "Sort all the p*(p-1) ranks ... p buckets",
  *   bucket boundaries                             -> sad_partition_plan
  *   "Redistributed sequences among processors"    -> sad_pack (send side) + sad_finish (receive side)
- * Between those calls the caller moves the small exchange buffers between ranks
- * (all-gather of ancestor records, of sample keys and of the count matrix, and
- * the variable all-to-all of sequences); every byte of arithmetic of the method
- * runs inside this library's CUDA kernels.
+ *
+ * TWO WAYS TO DRIVE ONE STEP
+ *  - The collective API (the product path): sad_create with an NCCL unique id
+ *    (sad_nccl_unique_id on rank 0, broadcast by the caller), then per step
+ *        sad_load -> sad_build_profiles -> sad_rank -> sad_partition
+ *    sad_rank and sad_partition are collective calls: the library owns an NCCL communicator and
+ *    runs every exchange on cfg.stream itself (ncclAllGather of the ancestor records, of
+ *    the regular samples and of the count matrix; grouped ncclSend/ncclRecv for the
+ *    all-to-all personalized redistribution). With world == 1 the context
+ *    needs no communicator (nccl_id == NULL: the exchanges are local); given one, the exchange
+ *    steps still run through NCCL (to a single rank).
+ *    For world == 1 the whole step runs without any host synchronization (it can be captured in
+ *    one CUDA graph); for world > 1 sad_partition waits once, for the all-gathered count matrix
+ *    that sizes the all-to-all.
+ *  - The split API (stage by stage: sad_rank_local, sad_rank_global, sad_partition_plan,
+ *    sad_pack, sad_finish): the caller moves the small exchange buffers between ranks itself
+ *    (all-gather of ancestor records, of sample keys and of the count matrix, and the variable
+ *    all-to-all of sequences), e.g. over torch.distributed; used for emulated ranks and tests.
+ * Every byte of arithmetic of the method runs inside this library's CUDA kernels either way.
  *
  * CONVENTIONS (all calls)
  *  - Return 0 on success or a negative SAD_E_* code. No exception crosses the ABI.
@@ -33,7 +48,17 @@
  *    until the stream has consumed them, and are never freed by the library. Host
  *    pointers ("h_" prefix) are read/written synchronously within the call.
  *  - Layouts are dense, row-major, little-endian; no padding unless stated.
- *  - The context is not thread-safe; one context per (process, GPU).
+ *  - The context is not thread-safe; one context per (process, GPU). Every call runs on
+ *    cfg.device and leaves the caller's current device unchanged.
+ *  - Device-detected input errors (SAD_E_SYMBOL, SAD_E_TOO_SHORT, SAD_E_TOO_LONG) and operand
+ *    overflow (SAD_E_REPLAN) are found by the step's kernels and reported by the first call that
+ *    synchronizes with the step: sad_partition (world > 1, or with h_bucket_sizes), a getter, or
+ *    sad_rank_local of the split API.
+ *  - SAD_E_REPLAN is not sticky: the all-pairs operand of this step was too small (its column
+ *    capacity is chosen before the k-mer statistics are known, SURVEY Appendix A.1 bounds it by
+ *    8 A^k for capped layers). The context has grown the capacity and returned to the "loaded"
+ *    state: query sad_operand_size again and rerun the step from sad_build_profiles (all ranks
+ *    receive the same code from a collective call).
  */
 #ifndef SAD_H_
 #define SAD_H_
@@ -45,7 +70,7 @@
 extern "C" {
 #endif
 
-#define SAD_ABI_VERSION 1u
+#define SAD_ABI_VERSION 2u
 
 /* alphabets ("sequences of amino acids"; DNA per BASELINE.json configs[4]).
  * Protein codes follow "ACDEFGHIKLMNPQRSTVWY", DNA "ACGT"; any other byte is an
@@ -92,7 +117,10 @@ extern "C" {
 #define SAD_E_EMPTY (-7)         /* n_global == 0 or a rank with no shard rows */
 #define SAD_E_CAPACITY (-8)      /* a caller buffer is too small */
 #define SAD_E_CUDA (-9)          /* CUDA runtime error (message in sad_last_error) */
+#define SAD_E_NCCL (-10)         /* NCCL error, a peer rank failed (it called sad_abort or reported an
+                                    input error in the count exchange), or the communicator was aborted */
 #define SAD_E_OOM (-11)          /* workspace too small / host allocation failed */
+#define SAD_E_REPLAN (-12)       /* the step's all-pairs operand capacity was exceeded: rerun (see above) */
 
 typedef struct sad_config {
     int32_t alphabet;   /* SAD_PROTEIN20 | SAD_DNA4 */
@@ -111,8 +139,21 @@ typedef struct sad_ctx sad_ctx;
 /* Version of this header the library was built from. */
 uint32_t sad_abi_version(void);
 
-/* Create a context. Does not allocate device memory. */
-int sad_create(const sad_config *cfg, sad_ctx **out);
+/* NCCL rendezvous id for sad_create (ncclGetUniqueId): call on rank 0 only and broadcast the 128
+ * bytes to every rank (e.g. with torch.distributed.broadcast_object_list). */
+int sad_nccl_unique_id(uint8_t *out128);
+
+/* Create a context. Does not allocate device memory.
+ *   nccl_id  NULL: no library communicator (world == 1 collective calls run locally; with
+ *            world > 1 only the split API can be used); else the 128-byte id of
+ *            sad_nccl_unique_id, and sad_create is COLLECTIVE over the world ranks
+ *            (ncclCommInitRank on cfg.device). */
+int sad_create(const sad_config *cfg, const uint8_t *nccl_id, sad_ctx **out);
+
+/* Abort the context's communicator (ncclCommAbort) after a local failure, so that peers blocked
+ * in a collective call return SAD_E_NCCL instead of hanging (replacing SPEC's
+ * PeerDisconnected). The context is then in the sticky SAD_E_NCCL state. */
+int sad_abort(sad_ctx *ctx);
 
 /* Destroy a context (waits for its stream). NULL is a no-op. */
 void sad_destroy(sad_ctx *ctx);
@@ -159,13 +200,60 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
  * tau = sum_m c_m A^(k-1-m) over residue codes c. Validates symbols and lengths, builds the
  * per-sequence (tau, count) lists (unordered in tau; entries with count >= 2 first) and each
  * shard's statistics for the all-pairs stage, and the length order of every shard (rows sorted by
- * L - k + 1, ties in arbitrary order: no result depends on it). Waits once for the statistics (to
- * report input errors and size the all-pairs operand); the length order runs meanwhile.
+ * L - k + 1, ties in arbitrary order: no result depends on it). The per-shard layer cap T_s and
+ * the operand width K_s are chosen on the device from those statistics;
+ * nothing is read back: input errors surface at the step's first synchronizing call.
  */
 int sad_build_profiles(sad_ctx *ctx);
 
-/* Bytes of the all-pairs operand buffer sad_rank_local needs (valid after sad_build_profiles). */
+/* Bytes of the all-pairs operand buffer sad_rank / sad_rank_local need (valid after
+ * sad_build_profiles): [binary indicator rows of the context's column capacity | K6 lists |
+ * K6 excess rows]. Host only. */
 int sad_operand_size(const sad_ctx *ctx, size_t *bytes);
+
+/*
+ * sad_rank — COLLECTIVE (collective API). "Locally compute k-mer rank of all the sequences in each
+ * processor", the local ancestors, "Send the k samples from each processor to all
+ * the processors" (here the p/world ancestor records, ncclAllGather), the global ancestor
+ * and "Compute the k-mer rank of each sequence against [it]", the local sort and the
+ * regular samples: sad_rank_local + all-gather + sad_rank_global in one call on
+ * cfg.stream (readings A5-A10). d_operand: >= sad_operand_size bytes, 1024-byte aligned,
+ * caller-owned scratch. No host synchronization.
+ */
+int sad_rank(sad_ctx *ctx, void *d_operand, size_t operand_bytes);
+
+/* Host logic of sad_partition's count exchange (pure host, no context; exposed for tests). From
+ * the all-gathered count blocks of every rank (h_gathered = world x (p/world*p*2 + 4) int64: the
+ * rank's [p/world][p][2] sequence/residue counts, then [operand overflow, first input-error kind
+ * (1 symbol, 2 too short, 3 too long), output bytes, 0]) it takes the decision every rank takes:
+ *   SAD_OK          exchange; h_counts_all ([p][p][2]) holds the count matrix
+ *   SAD_E_NCCL      some rank has an input error (*who = the first, *kind its kind): nothing moves
+ *   SAD_E_REPLAN    some rank's operand overflowed: every rank reruns the step
+ *   SAD_E_CAPACITY  rank *who announced fewer output bytes than its buckets need
+ * The inputs are identical on all ranks, so is the decision: no rank moves data alone. */
+int sad_exchange_verdict(int32_t p, int32_t world, const int64_t *h_gathered, int64_t *h_counts_all, int32_t *who,
+                         int32_t *kind);
+
+/* Output bytes of sad_partition on this rank for ANY outcome of the partition (the buckets it
+ * owns hold at most min(N, (p/world)(2w + p)) sequences, reading A23, and at most all
+ * residues_global residues of the job); world == 1: exact (residues_global is ignored). */
+int sad_output_bound(const sad_ctx *ctx, int64_t residues_global, size_t *bytes);
+
+/*
+ * sad_partition — COLLECTIVE (collective API). "Sort all the p*(p-1) ranks ... divide the range of
+ * ranks into p buckets" (ncclAllGather of the regular samples, pivots replicated on every
+ * rank, reading A14), bucket ranges (reading A13), the count exchange (ncclAllGather
+ * of the [p][p][2] sequence/residue counts plus every rank's status), and "Redistributed sequences
+ * among processors" (pack, grouped ncclSend/ncclRecv, receive-side merge): every
+ * rank ends with its buckets, each in key order, in d_out.
+ *   d_out / out_bytes  >= sad_output_bound bytes, 256-byte aligned; read with the getters
+ *   h_bucket_sizes     [p] int64 out, sizes of ALL buckets (may be NULL when world == 1, then
+ *                      nothing is read back and the call does not synchronize)
+ * world > 1: synchronizes once (the count matrix sizes the all-to-all); if any rank reported an
+ * input error, an operand overflow or a too small d_out, no data moves and every rank returns the
+ * same kind of code (the failing rank its own, the others SAD_E_NCCL; SAD_E_REPLAN everywhere).
+ */
+int sad_partition(sad_ctx *ctx, void *d_out, size_t out_bytes, int64_t *h_bucket_sizes);
 
 /* Bytes of one ancestor record: { int64 source_index; int32 L; int32 pad; uint16 counts[A^k] }
  * padded to 16 bytes. */
@@ -177,6 +265,8 @@ size_t sad_ancestor_record_bytes(const sad_ctx *ctx);
 int32_t sad_exchange_records(const sad_ctx *ctx);
 
 /*
+ * SPLIT API (the caller moves the exchange buffers; see the top of this file).
+ *
  * sad_rank_local — "Locally compute k-mer rank of all the sequences in each processor"
  * and the local ancestor (reading A6):
  *   S_ij = sum_tau min(n_i(tau), n_j(tau)),  den_ij = min(L_i, L_j) - k + 1   (reading A1)
@@ -184,6 +274,8 @@ int32_t sad_exchange_records(const sad_ctx *ctx);
  *   a_s  = argmax_{i in s} T_i, ties -> smaller source index                  (reading A6)
  *   d_operand  device buffer of >= sad_operand_size bytes (scratch, caller-owned)
  *   d_anc_out  device buffer of (p/world) ancestor records, this rank's shards in order
+ * Split API only: waits for the step's k-mer statistics first and returns the input error or
+ * SAD_E_REPLAN (operand capacity exceeded: query sad_operand_size again and call this again).
  */
 int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_anc_out);
 
@@ -352,6 +444,13 @@ int sad_get_profile_info(sad_ctx *ctx, int64_t *h_windows, int64_t *h_distinct, 
  * dense operand MACs per call (sum_s w_s(w_s+1)/2 * K_s), h_counts[3] = kernel launches of the
  * last full step (load..finish). Syncs. */
 int sad_get_stats(sad_ctx *ctx, double *h_ms, int64_t *h_counts);
+
+/* A step captured into a CUDA graph (stream capture of sad_load .. sad_partition on cfg.stream,
+ * world == 1 without a communicator) records its stage events as external event nodes; after
+ * each replay has completed, this adds that replay's operand-build and all-pairs kernel times to
+ * the sad_get_stats totals (and counts one call), and makes the getters read the replay's
+ * results. Syncs. */
+int sad_graph_account(sad_ctx *ctx);
 int sad_reset_stats(sad_ctx *ctx);
 
 /* Exhaustive self-test of the device fixed-point division q = floor(2^32 S / den)

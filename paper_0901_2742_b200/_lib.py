@@ -16,7 +16,9 @@ SAD_F_KEEP_SIM, SAD_F_KERNEL_ALU, SAD_F_KERNEL_TC, SAD_F_TC_INT8, SAD_F_TC_1SM, 
 SAD_F_RANK_SAMPLES = 64
 SAD_MEM_HOST, SAD_MEM_DEVICE, SAD_MEM_DEVICE_REBASE = 0, 1, 2
 ERRORS = {-1: "SAD_E_ARG", -2: "SAD_E_STATE", -3: "SAD_E_SYMBOL", -4: "SAD_E_TOO_SHORT", -5: "SAD_E_TOO_LONG",
-          -6: "SAD_E_INSUFFICIENT", -7: "SAD_E_EMPTY", -8: "SAD_E_CAPACITY", -9: "SAD_E_CUDA", -11: "SAD_E_OOM"}
+          -6: "SAD_E_INSUFFICIENT", -7: "SAD_E_EMPTY", -8: "SAD_E_CAPACITY", -9: "SAD_E_CUDA", -10: "SAD_E_NCCL",
+          -11: "SAD_E_OOM", -12: "SAD_E_REPLAN"}
+SAD_E_CAPACITY, SAD_E_NCCL, SAD_E_REPLAN = -8, -10, -12
 
 # every symbol include/sad.h declares (checked by tests/test_abi.py)
 SYMBOLS = [
@@ -26,7 +28,8 @@ SYMBOLS = [
     "sad_output_layout", "sad_finish", "sad_get_local_rank", "sad_get_ancestors", "sad_get_ranks", "sad_get_sorted",
     "sad_get_pivots", "sad_get_bucket", "sad_get_bucket_sizes", "sad_get_similarity", "sad_get_profile_info", "sad_get_stats",
     "sad_reset_stats", "sad_selftest_fixed_point", "sad_get_bucket_view", "sad_get_distance", "sad_exchange_records", "sad_get_distance_f64",
-    "sad_upgma_workspace", "sad_upgma", "sad_get_load_report",
+    "sad_upgma_workspace", "sad_upgma", "sad_get_load_report", "sad_nccl_unique_id", "sad_abort", "sad_rank",
+    "sad_partition", "sad_output_bound", "sad_graph_account", "sad_exchange_verdict",
 ]
 
 
@@ -57,7 +60,14 @@ def lib():
     P, i32, i64, u32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_size_t
     sig = {
         "sad_abi_version": (u32, []),
-        "sad_create": (i32, [ctypes.POINTER(SadConfig), ctypes.POINTER(P)]),
+        "sad_create": (i32, [ctypes.POINTER(SadConfig), P, ctypes.POINTER(P)]),
+        "sad_nccl_unique_id": (i32, [P]),
+        "sad_abort": (i32, [P]),
+        "sad_rank": (i32, [P, P, sz]),
+        "sad_partition": (i32, [P, P, sz, P]),
+        "sad_output_bound": (i32, [P, i64, ctypes.POINTER(sz)]),
+        "sad_graph_account": (i32, [P]),
+        "sad_exchange_verdict": (i32, [i32, i32, P, P, P, P]),
         "sad_destroy": (None, [P]),
         "sad_last_error": (ctypes.c_char_p, [P]),
         "sad_error_location": (i32, [P, P, P]),

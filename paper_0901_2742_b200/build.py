@@ -21,8 +21,22 @@ OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libsad.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dirs():
+    """NCCL headers and library of the pip wheel torch uses (nvidia-nccl-cu12); only libnccl.so.2
+    ships, so the link names it explicitly and the rpath points at it."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec is None or not spec.submodule_search_locations:
+        raise RuntimeError("nvidia.nccl (the NCCL wheel) is not importable")
+    base = list(spec.submodule_search_locations)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
+NCCL_INC, NCCL_LIB = _nccl_dirs()
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
-         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-Xptxas", "-v"]
+         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", NCCL_INC, "-Xptxas", "-v"]
 
 
 def _sources():
@@ -64,7 +78,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for obj, log in results:
             f.write(f"== {os.path.basename(obj)}\n{log}\n")
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[o for o, _ in results]]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[o for o, _ in results], "-L", NCCL_LIB, "-l:libnccl.so.2",
+           "-Xlinker", "-rpath=" + NCCL_LIB]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

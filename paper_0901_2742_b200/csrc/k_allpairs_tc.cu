@@ -819,9 +819,8 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
         cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(a.num_sms / 2, P.n_tiles)));
         cfg.blockDim = dim3(tc::THREADS);
         // long K (64+ K blocks in some shard, i.e. rows of 16k+ fp4 columns): the deeper ring
-        int64_t max_kb = 0;
-        for (int s = 0; s < a.pl; ++s) max_kb = std::max<int64_t>(max_kb, a.h_kblocks[s]);
-        const bool deep = a.kind == 1 && max_kb >= SAD_TC_DEEP_KB;
+        // (the K blocks themselves are read on the device; the hint only picks the instantiation)
+        const bool deep = a.kind == 1 && a.kblocks_hint >= SAD_TC_DEEP_KB;
         cfg.dynamicSmemBytes = a.kind == 0 ? tc::Traits<0, 2>::SMEM_BYTES
                                            : (deep ? tc::Traits<1, 2, true>::SMEM_BYTES : tc::Traits<1, 2>::SMEM_BYTES);
         cfg.stream = st;

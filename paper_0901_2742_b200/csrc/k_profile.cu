@@ -549,6 +549,47 @@ void launch_kstats(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned
     k_kstats<<<dim3(bx, pl), kScanThreads, 0, st>>>(M, Mb, Xc, kinfo, V);
 }
 
+// K3 decision (split identity): per shard the smallest layer cap T = 2^j whose
+// per-row excess max_i sum_tau (n_i(tau) - T)+ fits the K6 byte (<= 255), the operand width under
+// that cap and the shard's K blocks; taken on the device so that no host round trip sits between
+// the k-mer counts and the all-pairs stage. Mirrors, bit for bit, the rule the host applied before.
+__global__ void k_select(unsigned long long *kinfo, int pl, int V, int allow_cap, int64_t kcap_blocks, int kcpb,
+                         uint32_t *cap, uint32_t *xsel, uint32_t *ident, int64_t *kblocks,
+                         unsigned long long *status) {
+    for (int s = threadIdx.x; s < pl; s += blockDim.x) {
+        unsigned long long *ki = kinfo + (size_t)s * kKinfo;
+        unsigned long long K = ki[2];
+        uint32_t T = kNoCap, sel = (uint32_t)kNumCaps;
+        if (allow_cap)
+            for (int j = 0; j < kNumCaps; ++j)
+                if (ki[4 + j] <= 255ull) {
+                    T = 1u << j;
+                    K = ki[8 + j];
+                    if (ki[4 + j] > 0) sel = (uint32_t)j;    // the shard has entries above its cap
+                    break;
+                }
+        cap[s] = T;
+        xsel[s] = sel;
+        ident[s] = (T == 1u && K == (unsigned long long)V) ? 1u : 0u;   // col0(tau) = tau
+        int64_t kb = (int64_t)((K + (unsigned long long)kcpb - 1) / (unsigned long long)kcpb);
+        if (kb < 1) kb = 1;
+        if (kb > kcap_blocks) {                                          // operand too narrow: flagged
+            atomicOr(&status[0], 1ull);
+            kb = kcap_blocks;
+        }
+        kblocks[s] = kb;
+        ki[20] = K;
+        ki[21] = T;
+        atomicMax(&status[1], K);
+    }
+}
+
+void launch_select(unsigned long long *kinfo, int pl, int V, int allow_cap, int64_t kcap_blocks, int kcpb,
+                   uint32_t *cap, uint32_t *xsel, uint32_t *ident, int64_t *kblocks, unsigned long long *status,
+                   cudaStream_t st) {
+    k_select<<<1, 256, 0, st>>>(kinfo, pl, V, allow_cap, kcap_blocks, kcpb, cap, xsel, ident, kblocks, status);
+}
+
 __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl, int64_t r) {
     int s = 0;
     while (s + 1 < pl && r >= rowpad[s + 1]) ++s;
@@ -606,8 +647,10 @@ __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int 
         int64_t eon = 0;
         if (r + nw < a.rows_pad) locate(r + nw, sn, eon, dn);
         uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a.op) + r * a.stride);
-        for (uint32_t ch = 0; ch < stride; ch += (uint32_t)slice) {
-            const uint32_t len = min((uint32_t)slice, stride - ch);
+        // bytes of this row the contraction reads: the shard's K blocks (the stride is a capacity)
+        const uint32_t rowb = a.kblocks ? min(stride, (uint32_t)a.kblocks[s] * 128u) : stride;
+        for (uint32_t ch = 0; ch < rowb; ch += (uint32_t)slice) {
+            const uint32_t len = min((uint32_t)slice, rowb - ch);
             for (uint32_t t = lane; t < len / 16; t += 32) reinterpret_cast<uint4 *>(row)[t] = make_uint4(0, 0, 0, 0);
             __syncwarp();
             const uint32_t c_lo = ch * per_byte, c_hi = (ch + len) * per_byte;
@@ -640,7 +683,7 @@ __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int 
                 }
             }
             have_pre = false;
-            if (ch + (uint32_t)slice >= stride && r + nw < a.rows_pad) {   // the next row's first batch
+            if (ch + (uint32_t)slice >= rowb && r + nw < a.rows_pad) {     // the next row's first batch
 #pragma unroll
                 for (int b = 0; b < kOpBatch; ++b) {
                     const int e = b * 32 + lane;

@@ -732,3 +732,24 @@ void launch_f1_gainfo(const int64_t *anc_local, int pl, int shard0, int p, int64
 }
 
 }  // namespace sad
+
+namespace sad {
+
+// the count-exchange status of this rank (sad_partition): operand overflow and the first device-
+// detected input error, so that every rank learns from the one all-gather whether the step holds
+__global__ void k_status_tail(const unsigned long long *status, const unsigned long long *err, int64_t out_bytes,
+                              int64_t *tail) {
+    if (threadIdx.x != 0) return;
+    const unsigned long long NONE = ~0ull;
+    tail[0] = (int64_t)(status[0] & 1ull);
+    tail[1] = err[0] != NONE ? 1 : err[1] != NONE ? 2 : err[2] != NONE ? 3 : 0;
+    tail[2] = out_bytes;
+    tail[3] = 0;
+}
+
+void launch_status_tail(const unsigned long long *status, const unsigned long long *err, int64_t out_bytes,
+                        int64_t *tail, cudaStream_t st) {
+    k_status_tail<<<1, 32, 0, st>>>(status, err, out_bytes, tail);
+}
+
+}  // namespace sad

@@ -1,8 +1,10 @@
 // sad_api.cu — the C ABI of libsad.so (include/sad.h): argument checks, workspace carving,
-// stage orchestration on the caller's stream. All arithmetic of the method is in k_*.cu.
+// stage orchestration on the caller's stream, and the collective calls over the library's own
+// NCCL communicator. All arithmetic of the method is in k_*.cu.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_radix_sort.cuh>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -10,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <thread>
 
 #include "sad_internal.cuh"
 
@@ -43,11 +46,31 @@ int fail(sad_ctx *c, int code, const char *fmt, ...) {
     return code;
 }
 
+// a failure that leaves the context usable (SAD_E_REPLAN, a too small output buffer)
+int soft_fail(sad_ctx *c, int code, const char *fmt, ...) __attribute__((format(printf, 3, 4)));
+int soft_fail(sad_ctx *c, int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+    return code;
+}
+
 #define CK(call)                                                                            \
     do {                                                                                    \
         cudaError_t e_ = (call);                                                            \
         if (e_ != cudaSuccess)                                                              \
             return fail(ctx, SAD_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                \
+    } while (0)
+
+#define NK(call)                                                                            \
+    do {                                                                                    \
+        ncclResult_t r_ = (call);                                                           \
+        if (r_ != ncclSuccess)                                                              \
+            return fail(ctx, SAD_E_NCCL, "%s failed: %s (%s:%d)", #call, ncclGetErrorString(r_), \
                         __FILE__, __LINE__);                                                \
     } while (0)
 
@@ -68,15 +91,14 @@ int fail(sad_ctx *c, int code, const char *fmt, ...) {
     if (ctx->stage < (min_stage)) return fail(ctx, SAD_E_STATE, "call order: stage %d < %d", ctx->stage, (min_stage)); \
     DeviceScope dev_scope_(ctx->cfg.device)
 
+inline ncclComm_t comm_of(const sad_ctx *c) { return reinterpret_cast<ncclComm_t>(c->comm); }
+
 // shard bases of this rank under the block split of reading A15
 void shard_layout(const sad_ctx *c, int64_t n_global, std::vector<int64_t> &sb) {
     const int p = c->cfg.p;
     const int64_t base = n_global / p, extra = n_global % p;
     sb.assign(c->pl + 1, 0);
-    int64_t g0 = 0;
-    for (int s = 0; s < c->shard0; ++s) g0 += base + (s < extra ? 1 : 0);
     for (int s = 0; s < c->pl; ++s) sb[s + 1] = sb[s] + base + (c->shard0 + s < extra ? 1 : 0);
-    (void)g0;
 }
 
 int64_t first_index_of_rank(const sad_ctx *c, int64_t n_global) {
@@ -107,10 +129,16 @@ size_t cub_bytes_needed(int64_t n, int pl) {
     return std::max(std::max(std::max(a, b), std::max(c, d)), f) + 1024;
 }
 
+int exchange_records(const sad_ctx *c) {
+    return (c->cfg.flags & SAD_F_RANK_SAMPLES) ? c->pl * (c->cfg.p - 1) : c->pl;
+}
+size_t record_bytes(const sad_ctx *c) { return (size_t)rup(16 + 2 * (int64_t)c->V, 16); }
+int64_t count_block(const sad_ctx *c) { return (int64_t)c->pl * c->cfg.p * 2 + 4; }   // counts + status tail
+
 // carve the workspace; with base == nullptr only the size is computed
 size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     Bump b{base};
-    const int pl = c->pl, p = c->cfg.p, V = c->V;
+    const int pl = c->pl, p = c->cfg.p, V = c->V, G = c->cfg.world;
     c->d_ascii = b.take<uint8_t>((size_t)R + 528);     // + 512 + 16: vector reads past the last residue
     c->d_off = b.take<int64_t>((size_t)n + 1);
     c->d_rowinfo = b.take<RowInfo>((size_t)n);
@@ -124,8 +152,10 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_Mb = b.take<uint32_t>((size_t)pl * ((V + 31) / 32));
     c->d_lcnt = b.take<uint32_t>((size_t)2 * pl * kLenBinsMax);
     c->d_col0 = b.take<uint32_t>((size_t)pl * V);
-    c->d_err = b.take<unsigned long long>(4);
-    c->d_kinfo = b.take<unsigned long long>((size_t)pl * kKinfo);
+    // the step statistics block, copied to the host in one piece: err[4] | status[4] | kinfo
+    c->d_err = b.take<unsigned long long>(8 + (size_t)pl * kKinfo);
+    c->d_status = c->d_err ? c->d_err + 4 : nullptr;
+    c->d_kinfo = c->d_err ? c->d_err + 8 : nullptr;
     c->d_cap = b.take<uint32_t>((size_t)pl);
     c->d_ident = b.take<uint32_t>((size_t)pl);
     c->d_xsel = b.take<uint32_t>((size_t)pl);
@@ -162,6 +192,21 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_tc_tiles = b.take<uint8_t>((size_t)c->tc_tiles_cap * 16);
     c->cub_bytes = cub_bytes_needed(n, pl);
     c->d_cub = b.take<uint8_t>(c->cub_bytes);
+    // collective API: exchange records, samples and counts (this rank's and all ranks')
+    const int recs = exchange_records(c);
+    c->d_anc_mine = b.take<uint8_t>((size_t)recs * record_bytes(c));
+    c->d_anc_all = b.take<uint8_t>((size_t)G * recs * record_bytes(c));
+    c->d_smp_mine = b.take<unsigned long long>((size_t)std::max(pl * (p - 1), 1));
+    c->d_smp_all = b.take<unsigned long long>((size_t)std::max(p * (p - 1), 1));
+    c->d_cnt_send = b.take<int64_t>((size_t)count_block(c));
+    c->d_cnt_all = b.take<int64_t>((size_t)G * count_block(c));
+    if (c->comm) {                   // send buffers of the all-to-all
+        c->d_send_meta = b.take<unsigned long long>((size_t)2 * std::max<int64_t>(n, 1));
+        c->d_send_res = b.take<uint8_t>((size_t)R + 16);
+    } else {
+        c->d_send_meta = nullptr;
+        c->d_send_res = nullptr;
+    }
     if (c->cfg.flags & SAD_F_KEEP_SIM) {
         c->sim_elems = n * n;
         c->d_sim = b.take<uint16_t>((size_t)c->sim_elems);
@@ -173,14 +218,16 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
 }
 
 struct OutLayout {
-    unsigned long long *key, *keys_in;
+    unsigned long long *key, *keys_in, *recv_meta;
     int64_t *off, *len_in, *len_sorted, *src_off;
-    uint8_t *res, *cub;
+    uint8_t *res, *cub, *recv_res;
     int32_t *vals_in, *perm;
     size_t cub_bytes, total;
 };
 
-OutLayout out_layout(uint8_t *base, int64_t n, int64_t r) {
+// the output buffer: keys, offsets, residues of the owned buckets, merge scratch and (collective
+// API with an exchange) the all-to-all receive buffers
+OutLayout out_layout(uint8_t *base, int64_t n, int64_t r, bool recv) {
     Bump b{base};
     OutLayout o{};
     o.key = b.take<unsigned long long>((size_t)n);
@@ -200,9 +247,16 @@ OutLayout out_layout(uint8_t *base, int64_t n, int64_t r) {
     cub::DeviceScan::InclusiveSum(nullptr, s2, (const int64_t *)nullptr, (int64_t *)nullptr, nn);
     o.cub_bytes = std::max(a, std::max(s1, s2)) + 1024;
     o.cub = b.take<uint8_t>(o.cub_bytes);
+    if (recv) {
+        o.recv_meta = b.take<unsigned long long>((size_t)2 * std::max<int64_t>(n, 1));
+        o.recv_res = b.take<uint8_t>((size_t)r + 16);
+    }
     o.total = b.off + 256;
     return o;
 }
+
+// the collective path moves the buckets through NCCL (always when the context has a communicator)
+inline bool coll_exchange(const sad_ctx *c) { return c->comm != nullptr; }
 
 void sum_recv(const sad_ctx *c, const int64_t *h_counts_all, int64_t &n_out, int64_t &r_out) {
     const int p = c->cfg.p, bpr = c->pl;
@@ -219,8 +273,17 @@ void sum_recv(const sad_ctx *c, const int64_t *h_counts_all, int64_t &n_out, int
         }
 }
 
-}  // namespace
+// pinned host buffers of one context (sizes depend only on the configuration)
+bool alloc_host(sad_ctx *c) {
+    const int pl = c->pl, p = c->cfg.p, G = c->cfg.world;
+    return cudaMallocHost(&c->h_small, 65536 * sizeof(unsigned long long)) == cudaSuccess &&
+           cudaMallocHost(&c->h_stats, (8 + (size_t)pl * kKinfo) * sizeof(unsigned long long)) == cudaSuccess &&
+           cudaMallocHost(&c->h_cnt_all, (size_t)G * count_block(c) * sizeof(int64_t)) == cudaSuccess &&
+           cudaMallocHost(&c->h_seg, (size_t)pl * p * 2 * sizeof(int64_t)) == cudaSuccess &&
+           cudaMallocHost(&c->h_runs, ((size_t)p + 1) * sizeof(int64_t)) == cudaSuccess;
+}
 
+}  // namespace
 
 // stable (key, row) radix sort: one block for small inputs, else cub::DeviceRadixSort
 template <typename K>
@@ -232,13 +295,145 @@ static cudaError_t sort_pairs(sad_ctx *ctx, const K *ki, K *ko, const int32_t *v
     return cub::DeviceRadixSort::SortPairs(ctx->d_cub, tb, ki, ko, vi, vo, n, 0, end_bit, ctx->st);
 }
 
+// operand K capacity of a fresh layout: with capped layers K_s = sum_tau min(M(tau), T_s) <= 8 A^k
+// (T_s <= 8); uncapped shards that need more are flagged and replanned
+static int64_t initial_kcap_blocks(const sad_ctx *ctx) {
+    return std::max<int64_t>(1, (8 * (int64_t)ctx->V + ctx->kcols_per_block - 1) / ctx->kcols_per_block);
+}
+
+// Reads the step statistics sad_build_profiles copied to pinned memory (errors, operand status,
+// per-shard K and cap). wait: block until they have landed (a synchronizing call); else only if
+// they already have, and only to learn sizes (start of the next step: errors of an unobserved
+// step are dropped, the step's own validation reports them again).
+static int absorb(sad_ctx *ctx, bool wait) {
+    if (!ctx->stats_pending) return SAD_OK;
+    if (wait) {
+        CK(cudaEventSynchronize(ctx->ev_async));
+    } else if (cudaEventQuery(ctx->ev_async) != cudaSuccess) {
+        cudaGetLastError();          // cudaErrorNotReady is not an error
+        return SAD_OK;
+    }
+    ctx->stats_pending = false;
+    const int pl = ctx->pl;
+    const unsigned long long *h = ctx->h_stats, *st = h + 4, *ki = h + 8;
+    ctx->h_windows.assign(pl, 0);
+    ctx->h_distinct.assign(pl, 0);
+    ctx->h_K.assign(pl, 0);
+    ctx->h_cap.assign(pl, kNoCap);
+    int64_t macs = 0;
+    for (int s = 0; s < pl; ++s) {
+        const unsigned long long *k = ki + (size_t)s * kKinfo;
+        ctx->h_windows[s] = (int64_t)k[0];
+        ctx->h_distinct[s] = (int64_t)k[1];
+        ctx->h_K[s] = ctx->use_tc ? (int64_t)k[20] : (int64_t)k[2];
+        ctx->h_cap[s] = ctx->use_tc ? (uint32_t)k[21] : kNoCap;
+        const int64_t w = ctx->shard_base[s + 1] - ctx->shard_base[s];
+        macs += w * (w + 1) / 2 * ctx->h_K[s];
+    }
+    ctx->macs = macs;
+    const bool overflow = ctx->use_tc && (st[0] & 1ull);
+    if (ctx->use_tc) {
+        const int64_t kb = std::max<int64_t>(1, ((int64_t)st[1] + ctx->kcols_per_block - 1) / ctx->kcols_per_block);
+        ctx->kmax_blocks_seen = kb;
+        // the next step's capacity: the largest K seen plus 1/8 (and one block) of headroom
+        ctx->kcap_next = kb + std::max<int64_t>(1, kb / 8);
+    }
+    if (!wait) return SAD_OK;
+    const unsigned long long NONE = ~0ull;
+    if (h[0] != NONE) {
+        ctx->err_idx = (int64_t)(h[0] >> 32);
+        ctx->err_pos = (int64_t)(h[0] & 0xFFFFFFFFull);
+        return fail(ctx, SAD_E_SYMBOL, "IllegalSymbol(sequence %lld, position %lld)", (long long)ctx->err_idx,
+                    (long long)ctx->err_pos);
+    }
+    if (h[1] != NONE) {
+        ctx->err_idx = (int64_t)h[1];
+        return fail(ctx, SAD_E_TOO_SHORT, "SequenceTooShort(sequence %lld): L < k = %d", (long long)ctx->err_idx,
+                    ctx->cfg.k);
+    }
+    if (h[2] != NONE) {
+        ctx->err_idx = (int64_t)h[2];
+        return fail(ctx, SAD_E_TOO_LONG, "sequence %lld: L - k + 1 > 65535", (long long)ctx->err_idx);
+    }
+    if (overflow) {
+        ctx->kcap_blocks = std::max(ctx->kcap_blocks, ctx->kcap_next);
+        ctx->stage = 1;
+        return soft_fail(ctx, SAD_E_REPLAN, "all-pairs operand of %lld K blocks exceeded (needs %lld): rerun the step",
+                         (long long)ctx->kcap_blocks, (long long)ctx->kmax_blocks_seen);
+    }
+    return SAD_OK;
+}
+
+// stage timing events (CUDA events on the context stream; inside a CUDA graph capture they become
+// external event-record nodes that sad_graph_account reads after each replay)
+static void record_pair(sad_ctx *ctx, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, bool begin, int gslot) {
+    if (ctx->capturing) {
+        cudaEventRecordWithFlags(ctx->gev[gslot], ctx->st, cudaEventRecordExternal);
+        ctx->graph_events = true;
+        return;
+    }
+    if (begin) {
+        std::pair<cudaEvent_t, cudaEvent_t> e;
+        if (!ctx->ev_free.empty()) {
+            e = ctx->ev_free.back();
+            ctx->ev_free.pop_back();
+        } else {
+            cudaEventCreate(&e.first);
+            cudaEventCreate(&e.second);
+        }
+        cudaEventRecord(e.first, ctx->st);
+        v.push_back(e);
+    } else {
+        cudaEventRecord(v.back().second, ctx->st);
+    }
+}
+
+static bool stream_capturing(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return cs == cudaStreamCaptureStatusActive;
+}
+
+// waits for an event while polling the communicator for asynchronous errors (a failed or aborted
+// peer): the call then returns SAD_E_NCCL instead of blocking forever
+static int wait_collective(sad_ctx *ctx, cudaEvent_t ev) {
+    for (;;) {
+        const cudaError_t e = cudaEventQuery(ev);
+        if (e == cudaSuccess) return SAD_OK;
+        if (e != cudaErrorNotReady) return fail(ctx, SAD_E_CUDA, "waiting for the exchange: %s", cudaGetErrorString(e));
+        cudaGetLastError();
+        if (ctx->comm) {
+            ncclResult_t ae = ncclSuccess;
+            ncclCommGetAsyncError(comm_of(ctx), &ae);
+            if (ae != ncclSuccess && ae != ncclInProgress) {
+                ncclCommAbort(comm_of(ctx));
+                ctx->comm = nullptr;
+                return fail(ctx, SAD_E_NCCL, "collective failed: %s (a peer failed or aborted)", ncclGetErrorString(ae));
+            }
+        }
+        std::this_thread::yield();
+    }
+}
+
 extern "C" {
 
 static void bucket_sizes_from_counts(sad_ctx *ctx);
 
 uint32_t sad_abi_version(void) { return SAD_ABI_VERSION; }
 
-int sad_create(const sad_config *cfg, sad_ctx **out) {
+int sad_nccl_unique_id(uint8_t *out128) {
+    if (!out128) return SAD_E_ARG;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return SAD_E_NCCL;
+    std::memcpy(out128, &id, 128);
+    return SAD_OK;
+}
+
+int sad_create(const sad_config *cfg, const uint8_t *nccl_id, sad_ctx **out) {
     if (!cfg || !out) return SAD_E_ARG;
     *out = nullptr;
     if (cfg->alphabet != SAD_PROTEIN20 && cfg->alphabet != SAD_DNA4) return SAD_E_ARG;
@@ -253,6 +448,11 @@ int sad_create(const sad_config *cfg, sad_ctx **out) {
         if (V > 65536) return SAD_E_ARG;
     }
     if ((cfg->flags & SAD_F_RANK_SAMPLES) && V * 8 > 200 * 1024) return SAD_E_ARG;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) {
+        cudaGetLastError();
+        return SAD_E_CUDA;
+    }
     sad_ctx *ctx = new (std::nothrow) sad_ctx();
     if (!ctx) return SAD_E_OOM;
     ctx->cfg = *cfg;
@@ -264,28 +464,19 @@ int sad_create(const sad_config *cfg, sad_ctx **out) {
     ctx->use_tc = !(cfg->flags & SAD_F_KERNEL_ALU);
     ctx->tc_kind = (cfg->flags & SAD_F_TC_INT8) ? 0 : 1;
     ctx->tc_cg = (cfg->flags & SAD_F_TC_1SM) ? 1 : 2;
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) {
-        delete ctx;
-        return SAD_E_CUDA;
-    }
+    ctx->kcols_per_block = (ctx->use_tc && ctx->tc_kind == 1) ? 256 : 128;
     DeviceScope dev_scope_(cfg->device);
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
-    if (cudaMallocHost(&ctx->h_small, 65536 * sizeof(unsigned long long)) != cudaSuccess) {
-        delete ctx;
-        return SAD_E_CUDA;
-    }
-    if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_stats, cudaEventDisableTiming) != cudaSuccess ||
-        [&] {
-            for (auto &e : ctx->ev_chunk)
-                if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return true;
-            return false;
-        }()) {
-        cudaFreeHost(ctx->h_small);
-        delete ctx;
+    bool ok = alloc_host(ctx) && cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->ev_stats, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->ev_async, cudaEventDisableTiming) == cudaSuccess;
+    for (auto &e : ctx->ev_chunk) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    for (auto &e : ctx->gev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        sad_destroy(ctx);
         return SAD_E_CUDA;
     }
     if (ctx->use_tc) {
@@ -295,6 +486,16 @@ int sad_create(const sad_config *cfg, sad_ctx **out) {
             return SAD_E_ARG;
         }
     }
+    if (nccl_id) {                   // collective over the world ranks
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, 128);
+        ncclComm_t comm = nullptr;
+        if (ncclCommInitRank(&comm, cfg->world, id, cfg->rank) != ncclSuccess) {
+            sad_destroy(ctx);
+            return SAD_E_NCCL;
+        }
+        ctx->comm = comm;
+    }
     *out = ctx;
     return SAD_OK;
 }
@@ -303,20 +504,35 @@ void sad_destroy(sad_ctx *ctx) {
     if (!ctx) return;
     DeviceScope dev_scope_(ctx->cfg.device);
     if (ctx->st) cudaStreamSynchronize(ctx->st); else cudaDeviceSynchronize();
+    if (ctx->comm) ncclCommDestroy(comm_of(ctx));
     for (auto &v : {&ctx->ev_pairs_ap, &ctx->ev_pairs_op, &ctx->ev_free})
         for (auto &e : *v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
         cudaStreamDestroy(ctx->side);
     }
-    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
-    if (ctx->ev_stats) cudaEventDestroy(ctx->ev_stats);
+    for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_join, ctx->ev_stats, ctx->ev_async})
+        if (e) cudaEventDestroy(e);
     for (auto &e : ctx->ev_chunk)
         if (e) cudaEventDestroy(e);
-    if (ctx->h_small) cudaFreeHost(ctx->h_small);
-    if (ctx->h_tiles) cudaFreeHost(ctx->h_tiles);
+    for (auto &e : ctx->gev)
+        if (e) cudaEventDestroy(e);
+    for (void *h : {(void *)ctx->h_small, (void *)ctx->h_tiles, (void *)ctx->h_stats, (void *)ctx->h_cnt_all,
+                    (void *)ctx->h_seg, (void *)ctx->h_runs})
+        if (h) cudaFreeHost(h);
+    cudaGetLastError();
     delete ctx;
+}
+
+int sad_abort(sad_ctx *ctx) {
+    if (!ctx) return SAD_E_ARG;
+    DeviceScope dev_scope_(ctx->cfg.device);
+    if (ctx->comm) {
+        ncclCommAbort(comm_of(ctx));
+        ctx->comm = nullptr;
+    }
+    fail(ctx, SAD_E_NCCL, "aborted by sad_abort");
+    return SAD_OK;
 }
 
 const char *sad_last_error(const sad_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
@@ -335,7 +551,9 @@ int sad_workspace_size(const sad_ctx *cctx, int64_t n_local, int64_t residues_lo
     tmp.cfg = ctx->cfg;
     tmp.pl = ctx->pl;
     tmp.V = ctx->V;
+    tmp.comm = ctx->comm;
     *bytes = carve(&tmp, nullptr, n_local, residues_local);
+    tmp.comm = nullptr;
     return SAD_OK;
 }
 
@@ -362,6 +580,7 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
                     (long long)first_source_index);
     if (n_local == 0) return fail(ctx, SAD_E_EMPTY, "rank has no sequences");
     if (n_global / p + 1 >= (int64_t(1) << 24)) return fail(ctx, SAD_E_ARG, "shards of 2^24 or more sequences");
+    ctx->capturing = stream_capturing(ctx->st);
     int64_t R = residues_local;
     bool need_sync = mem == SAD_MEM_HOST;     // host inputs may be reused by the caller on return
     if (mem == SAD_MEM_HOST) {
@@ -371,10 +590,12 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
     } else if (R < 0 && mem == SAD_MEM_DEVICE_REBASE) {
         return fail(ctx, SAD_E_ARG, "SAD_MEM_DEVICE_REBASE needs residues_local");
     } else if (R < 0) {
+        if (ctx->capturing) return fail(ctx, SAD_E_ARG, "device inputs in a graph capture need residues_local");
         CK(cudaMemcpyAsync(ctx->h_small + 40000, offsets + n_local, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
         R = (int64_t)ctx->h_small[40000];
     }
+    if (ctx->capturing && mem == SAD_MEM_HOST) return fail(ctx, SAD_E_ARG, "host inputs cannot be graph-captured");
     if (R > 0 && !ascii) return fail(ctx, SAD_E_ARG, "ascii is NULL");
     const size_t need = carve(ctx, nullptr, n_local, R);
     if (ws_bytes < need) return fail(ctx, SAD_E_OOM, "workspace %zu < %zu bytes", ws_bytes, need);
@@ -391,17 +612,20 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
     ctx->shard_base = sb;
     ctx->max_w = 0;
     ctx->shard_rowpad.assign(ctx->pl + 1, 0);
+    int64_t pairs = 0;
     for (int s = 0; s < ctx->pl; ++s) {
         const int64_t w = sb[s + 1] - sb[s];
         ctx->max_w = std::max(ctx->max_w, w);
         ctx->shard_rowpad[s + 1] = ctx->shard_rowpad[s] + rup(w, kRowPad);
+        pairs += w * (w - 1) / 2;
     }
+    ctx->pairs = pairs;
     ctx->rows_pad = ctx->shard_rowpad[ctx->pl];
     const cudaMemcpyKind kind = mem == SAD_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     // host inputs of a few MB or more: the residues are copied in chunks on the internal stream and
     // each chunk's k-mer counts (K1/K2) start on ctx->st as soon as it has landed (below)
     const int nch = 4;                     // chunks of a pipelined host load (16 max; 4 measured best)
-    const bool pipelined = nch > 0 && mem == SAD_MEM_HOST && R >= (int64_t(4) << 20) && n_local >= 64 * nch;
+    const bool pipelined = mem == SAD_MEM_HOST && R >= (int64_t(4) << 20) && n_local >= 64 * nch;
     ctx->profiled = false;
     if (R > 0 && !pipelined) CK(cudaMemcpyAsync(ctx->d_ascii, ascii, (size_t)R, kind, ctx->st));
     if (mem == SAD_MEM_DEVICE_REBASE) {
@@ -415,6 +639,7 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
     const bool same = ctx->tbl_ws == base && ctx->tbl_n == n_local && ctx->tbl_ng == n_global &&
                       ctx->tbl_first == first_source_index && ctx->tbl_R == R;
     if (!same) {
+        if (ctx->capturing) return fail(ctx, SAD_E_STATE, "a graph capture needs the layout loaded once before");
         int64_t *tbl = reinterpret_cast<int64_t *>(ctx->h_small + 32768);
         int64_t simb = 0, tiles = 0;
         for (int s = 0; s <= ctx->pl; ++s) {
@@ -451,7 +676,6 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
             if (ctx->tc_tiles_n > 0)
                 CK(cudaMemcpyAsync(ctx->d_tc_tiles, ctx->h_tiles, (size_t)ctx->tc_tiles_n * 16, cudaMemcpyHostToDevice,
                                    ctx->st));
-
         }
         const size_t tb = sizeof(int64_t) * (ctx->pl + 1);
         CK(cudaMemcpyAsync(ctx->d_shard_base, tbl, tb, cudaMemcpyHostToDevice, ctx->st));
@@ -464,8 +688,18 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
         ctx->tbl_ng = n_global;
         ctx->tbl_first = first_source_index;
         ctx->tbl_R = R;
+        // capped layers + K6 excess are possible in this layout (the K6 row accumulators hold
+        // max_w bytes per warp; the dense excess matrices must fit their bound)
+        ctx->allow_cap = ctx->use_tc && !(ctx->cfg.flags & SAD_F_TC_ALL_LAYERS) && rup(ctx->max_w, 16) <= kXrSmem &&
+                         ctx->h_ebase[ctx->pl] <= kMaxExcessBytes;
+        // fresh layout: the operand capacity starts from the capped-layer bound
+        ctx->kcap_blocks = ctx->kcap_next = initial_kcap_blocks(ctx);
+        ctx->kmax_blocks_seen = -1;
+        ctx->stats_pending = false;
         need_sync = true;
     }
+    // K6 list entries: at most one per CSR entry (sum of the distinct counts <= windows <= R)
+    ctx->x_entries_bound = std::max<int64_t>(R, 1);
     ctx->launches_step = 0;
     if (pipelined) {
         if (int rc = profile_reset(ctx)) return rc;
@@ -494,7 +728,7 @@ static int profile_reset(sad_ctx *ctx) {
     CK(cudaMemsetAsync(ctx->d_M, 0, sizeof(uint32_t) * (size_t)pl * V, ctx->st));
     CK(cudaMemsetAsync(ctx->d_Mb, 0, sizeof(uint32_t) * (size_t)pl * ((V + 31) / 32), ctx->st));
     CK(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long) * 4, ctx->st));
-    CK(cudaMemsetAsync(ctx->d_kinfo, 0, sizeof(unsigned long long) * kKinfo * (size_t)pl, ctx->st));
+    CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(unsigned long long) * (4 + kKinfo * (size_t)pl), ctx->st));
     CK(cudaMemsetAsync(ctx->d_Xc, 0, sizeof(uint32_t) * kNumCaps * (size_t)pl * V, ctx->st));
     return SAD_OK;
 }
@@ -532,6 +766,11 @@ static int profile_launch(sad_ctx *ctx, int64_t i0, int64_t i1) {
 int sad_build_profiles(sad_ctx *ctx) {
     GUARD(1);
     const int pl = ctx->pl, V = ctx->V;
+    ctx->capturing = stream_capturing(ctx->st);
+    if (!ctx->capturing) {
+        absorb(ctx, false);          // sizes learnt from the previous step, if it has finished
+        ctx->kcap_blocks = ctx->kcap_next;
+    }
     if (!ctx->profiled) {
         if (int rc = profile_reset(ctx)) return rc;
         if (int rc = profile_launch(ctx, 0, ctx->n)) return rc;
@@ -539,82 +778,25 @@ int sad_build_profiles(sad_ctx *ctx) {
     ctx->profiled = false;
     launch_kstats(ctx->d_M, ctx->d_Mb, ctx->d_Xc, ctx->d_kinfo, pl, V, ctx->st);
     LAUNCHED();
-    unsigned long long *hk = ctx->h_small + 8192;
-    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, ctx->st));
-    CK(cudaMemcpyAsync(hk, ctx->d_kinfo, sizeof(unsigned long long) * kKinfo * pl, cudaMemcpyDeviceToHost, ctx->st));
-    CK(cudaEventRecord(ctx->ev_stats, ctx->st));
     if (ctx->use_tc) {
-        // the length order needs no host decision: it runs while the host reads the statistics
+        // the length order (rows by L - k + 1) and the cap / K decision, all on the device
         launch_lenorder(ctx->d_rowinfo, ctx->d_shard_base, ctx->d_kinfo, pl, ctx->n, ctx->d_lcnt,
                         ctx->d_lcnt + (size_t)pl * kLenBinsMax, ctx->d_sigma, ctx->d_sigma_inv, ctx->d_rinfo_s,
                         ctx->st);
         ctx->launches_step += 3;
+        launch_select(ctx->d_kinfo, pl, V, ctx->allow_cap ? 1 : 0, ctx->kcap_blocks, (int)ctx->kcols_per_block,
+                      ctx->d_cap, ctx->d_xsel, ctx->d_ident, ctx->d_kblocks, ctx->d_status, ctx->st);
+        LAUNCHED();
     }
-    CK(cudaEventSynchronize(ctx->ev_stats));
-    const unsigned long long NONE = ~0ull;
-    if (ctx->h_small[0] != NONE) {
-        ctx->err_idx = (int64_t)(ctx->h_small[0] >> 32);
-        ctx->err_pos = (int64_t)(ctx->h_small[0] & 0xFFFFFFFFull);
-        return fail(ctx, SAD_E_SYMBOL, "IllegalSymbol(sequence %lld, position %lld)", (long long)ctx->err_idx,
-                    (long long)ctx->err_pos);
+    // the statistics go to pinned host memory; read at the step's first synchronizing call
+    CK(cudaMemcpyAsync(ctx->h_stats, ctx->d_err, sizeof(unsigned long long) * (8 + (size_t)pl * kKinfo),
+                       cudaMemcpyDeviceToHost, ctx->st));
+    if (!ctx->capturing) {
+        CK(cudaEventRecord(ctx->ev_async, ctx->st));
+        ctx->stats_pending = true;
     }
-    if (ctx->h_small[1] != NONE) {
-        ctx->err_idx = (int64_t)ctx->h_small[1];
-        return fail(ctx, SAD_E_TOO_SHORT, "SequenceTooShort(sequence %lld): L < k = %d", (long long)ctx->err_idx,
-                    ctx->cfg.k);
-    }
-    if (ctx->h_small[2] != NONE) {
-        ctx->err_idx = (int64_t)ctx->h_small[2];
-        return fail(ctx, SAD_E_TOO_LONG, "sequence %lld: L - k + 1 > 65535", (long long)ctx->err_idx);
-    }
-    ctx->h_windows.assign(pl, 0);
-    ctx->h_distinct.assign(pl, 0);
-    ctx->h_K.assign(pl, 0);
-    ctx->h_cap.assign(pl, kNoCap);
-    std::vector<uint32_t> sel(pl, kNumCaps);
-    int64_t kmax = 0;
-    ctx->n_x = 0;
-    bool any_excess = false;
-    for (int s = 0; s < pl; ++s) {
-        const unsigned long long *ki = hk + (size_t)kKinfo * s;
-        ctx->h_windows[s] = (int64_t)ki[0];
-        ctx->h_distinct[s] = (int64_t)ki[1];
-        ctx->h_K[s] = (int64_t)ki[2];
-        // layer cap: the smallest T in {1, 2, 4, 8} whose per-row excess
-        // sum_tau (n_i - T)+ stays <= 255 for every row, so that every pair's excess fits one
-        // byte of the K6 matrix; otherwise all layers stay dense (no cap)
-        // (the K6 row accumulators hold max_w bytes per warp in shared memory)
-        if (ctx->use_tc && !(ctx->cfg.flags & SAD_F_TC_ALL_LAYERS) && rup(ctx->max_w, 16) <= kXrSmem &&
-            ctx->h_ebase[pl] <= kMaxExcessBytes)
-            for (int j = 0; j < kNumCaps; ++j)
-                if (ki[4 + j] <= 255) {
-                    ctx->h_cap[s] = 1u << j;
-                    ctx->h_K[s] = (int64_t)ki[8 + j];
-                    if (ki[4 + j] > 0) {
-                        any_excess = true;
-                        sel[s] = (uint32_t)j;
-                        ctx->n_x += (int64_t)ki[16 + j];
-                    }
-                    break;
-                }
-        kmax = std::max(kmax, ctx->h_K[s]);
-    }
-    ctx->use_excess = any_excess;
-
-    if (ctx->use_tc) {
-        uint32_t *hc = reinterpret_cast<uint32_t *>(ctx->h_small + 12288);
-        for (int s = 0; s < pl; ++s) {
-            hc[s] = ctx->h_cap[s];
-            hc[pl + s] = sel[s];
-            hc[2 * pl + s] = (ctx->h_cap[s] == 1u && ctx->h_K[s] == V) ? 1u : 0u;   // col0(tau) = tau
-        }
-        CK(cudaMemcpyAsync(ctx->d_ident, hc + 2 * pl, sizeof(uint32_t) * pl, cudaMemcpyHostToDevice, ctx->st));
-        CK(cudaMemcpyAsync(ctx->d_cap, hc, sizeof(uint32_t) * pl, cudaMemcpyHostToDevice, ctx->st));
-        CK(cudaMemcpyAsync(ctx->d_xsel, hc + pl, sizeof(uint32_t) * pl, cudaMemcpyHostToDevice, ctx->st));
-    }
-    // operand row: K columns padded to one 128-byte K block = 128 int8 or 256 packed fp4 entries
-    ctx->kcols_per_block = (ctx->use_tc && ctx->tc_kind == 1) ? 256 : 128;
-    ctx->K_stride = std::max<int64_t>(1, (kmax + ctx->kcols_per_block - 1) / ctx->kcols_per_block) * 128;
+    // operand row: the capacity in 128-byte K blocks (128 int8 or 256 packed fp4 entries each)
+    ctx->K_stride = ctx->kcap_blocks * 128;
     ctx->V_pad = rup(V, 64);
     ctx->stage = 2;
     return SAD_OK;
@@ -625,8 +807,8 @@ static void operand_parts(const sad_ctx *ctx, size_t &op, size_t &xl, size_t &xe
     op = ctx->use_tc ? (size_t)ctx->rows_pad * (size_t)ctx->K_stride : (size_t)ctx->rows_pad * (size_t)ctx->V_pad * 2;
     op = (size_t)rup((int64_t)op, 1024);
     xl = xe = 0;
-    if (ctx->use_tc && ctx->use_excess) {
-        xl = (size_t)rup(ctx->n_x * 4, 1024);
+    if (ctx->use_tc && ctx->allow_cap) {
+        xl = (size_t)rup(ctx->x_entries_bound * 4, 1024);
         xe = (size_t)rup(ctx->h_ebase[ctx->pl] + 256, 1024);
     }
 }
@@ -643,32 +825,13 @@ int sad_operand_size(const sad_ctx *cctx, size_t *bytes) {
 
 int32_t sad_exchange_records(const sad_ctx *ctx) {
     if (!ctx) return SAD_E_ARG;
-    return (ctx->cfg.flags & SAD_F_RANK_SAMPLES) ? ctx->pl * (ctx->cfg.p - 1) : ctx->pl;
+    return exchange_records(ctx);
 }
 
-size_t sad_ancestor_record_bytes(const sad_ctx *ctx) {
-    return ctx ? (size_t)rup(16 + 2 * (int64_t)ctx->V, 16) : 0;
-}
+size_t sad_ancestor_record_bytes(const sad_ctx *ctx) { return ctx ? record_bytes(ctx) : 0; }
 
-static void record_pair(sad_ctx *ctx, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, bool begin) {
-    if (begin) {
-        std::pair<cudaEvent_t, cudaEvent_t> e;
-        if (!ctx->ev_free.empty()) {
-            e = ctx->ev_free.back();
-            ctx->ev_free.pop_back();
-        } else {
-            cudaEventCreate(&e.first);
-            cudaEventCreate(&e.second);
-        }
-        cudaEventRecord(e.first, ctx->st);
-        v.push_back(e);
-    } else {
-        cudaEventRecord(v.back().second, ctx->st);
-    }
-}
-
-int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_anc_out) {
-    GUARD(2);
+// a3 + a4 (and the f1 sample records): operand, all-pairs, local ancestors; no host decisions
+static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_anc_out) {
     size_t need = 0;
     sad_operand_size(ctx, &need);
     if (!d_operand || operand_bytes < need || !d_anc_out)
@@ -698,13 +861,14 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     operand_parts(ctx, op_b, xl_b, xe_b);
     uint32_t *lists = xl_b ? reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_operand) + op_b) : nullptr;
     uint8_t *E = xl_b ? reinterpret_cast<uint8_t *>(d_operand) + op_b + xl_b : nullptr;
-    unsigned long long *xtot = reinterpret_cast<unsigned long long *>(ctx->d_xoff + (size_t)pl * ctx->V + 1) ;
+    unsigned long long *xtot = reinterpret_cast<unsigned long long *>(ctx->d_xoff + (size_t)pl * ctx->V + 1);
     xtot = reinterpret_cast<unsigned long long *>(rup(reinterpret_cast<int64_t>(xtot), 8));
-    record_pair(ctx, ctx->ev_pairs_op, true);
+    record_pair(ctx, ctx->ev_pairs_op, true, 0);
     if (ctx->use_tc) {
-        // K3 under the layer caps (the length order sigma was computed by sad_build_profiles);
-        // K6 list offsets and lists; K4 beside K6 rows (side stream)
+        // K3 under the layer caps k_select chose (the length order sigma was computed by
+        // sad_build_profiles); K6 list offsets and lists; K4 beside K6 rows (side stream)
         o.sigma = ctx->d_sigma;
+        o.kblocks = ctx->d_kblocks;
         launch_capscan(ctx->d_M, ctx->V, nullptr, ctx->d_cap, ctx->d_col0, nullptr, 0, pl, ctx->V, ctx->st);
         LAUNCHED();
         o.cap = ctx->d_cap;
@@ -750,22 +914,7 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
         launch_dense_counts(o, ctx->st);
         LAUNCHED();
     }
-    record_pair(ctx, ctx->ev_pairs_op, false);
-
-    // per shard K blocks (TC)
-    std::vector<int64_t> kb(pl + 1, 0);
-    int64_t pairs = 0, macs = 0;
-    for (int s = 0; s < pl; ++s) {
-        kb[s] = (ctx->h_K[s] + ctx->kcols_per_block - 1) / ctx->kcols_per_block;
-        const int64_t w = ctx->shard_base[s + 1] - ctx->shard_base[s];
-        pairs += w * (w - 1) / 2;
-        macs += w * (w + 1) / 2 * ctx->h_K[s];
-    }
-    ctx->pairs = pairs;
-    ctx->macs = macs;
-    std::memcpy(ctx->h_small + 1024, kb.data(), sizeof(int64_t) * (pl + 1));
-    CK(cudaMemcpyAsync(ctx->d_kblocks, ctx->h_small + 1024, sizeof(int64_t) * (pl + 1), cudaMemcpyHostToDevice,
-                       ctx->st));
+    record_pair(ctx, ctx->ev_pairs_op, false, 1);
 
     AllPairsArgs ap{};
     ap.op = d_operand;
@@ -785,7 +934,7 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     ap.n_tiles = ctx->alu_tiles;
     ap.h_shard_base = ctx->shard_base.data();
     ap.h_shard_rowpad = ctx->shard_rowpad.data();
-    ap.h_kblocks = kb.data();
+    ap.kblocks_hint = ctx->kmax_blocks_seen;
     ap.kind = ctx->tc_kind;
     ap.tiles = ctx->d_tc_tiles;
     ap.n_tiles_tc = ctx->tc_tiles_n;
@@ -794,7 +943,7 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     ap.E = E;
     ap.ebase = ctx->d_ebase;
     ap.zero = E ? E + ctx->h_ebase[pl] : nullptr;
-    record_pair(ctx, ctx->ev_pairs_ap, true);
+    record_pair(ctx, ctx->ev_pairs_ap, true, 2);
     if (ctx->use_tc) {
         std::string e;
         const int rc = launch_allpairs_tc(ap, ctx->st, e);
@@ -803,8 +952,8 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
         launch_allpairs_alu(ap, ctx->st);
     }
     LAUNCHED();
-    record_pair(ctx, ctx->ev_pairs_ap, false);
-    ctx->calls += 1;
+    record_pair(ctx, ctx->ev_pairs_ap, false, 3);
+    if (!ctx->capturing) ctx->calls += 1;
 
     AncArgs an{};
     an.T = ctx->d_T;
@@ -817,7 +966,7 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     an.k = ctx->cfg.k;
     an.V = ctx->V;
     an.pl = pl;
-    an.rec_bytes = sad_ancestor_record_bytes(ctx);
+    an.rec_bytes = record_bytes(ctx);
     an.anc_local = ctx->d_anc_local;
     const bool f1 = ctx->cfg.flags & SAD_F_RANK_SAMPLES;
     an.rec_out = f1 ? nullptr : reinterpret_cast<uint8_t *>(d_anc_out);
@@ -841,13 +990,21 @@ int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_
     return SAD_OK;
 }
 
-int sad_rank_global(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out) {
-    GUARD(3);
+int sad_rank_local(sad_ctx *ctx, void *d_operand, size_t operand_bytes, void *d_anc_out) {
+    GUARD(2);
+    // split API: the caller reads no step results before moving the exchange buffers, so the
+    // statistics are checked here (one wait) rather than at a later synchronizing call
+    if (int rc = absorb(ctx, true)) return rc;
+    return rank_local_impl(ctx, d_operand, operand_bytes, d_anc_out);
+}
+
+// a5-a8: GA, rank vs GA (or f1: vs the samples), local sort, regular samples
+static int rank_global_impl(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out) {
     const int p = ctx->cfg.p;
     if (!d_anc_all || (p > 1 && !d_samples_out)) return fail(ctx, SAD_E_ARG, "sad_rank_global: NULL buffer");
     RankArgs r{};
     r.anc_all = reinterpret_cast<const uint8_t *>(d_anc_all);
-    r.rec_bytes = sad_ancestor_record_bytes(ctx);
+    r.rec_bytes = record_bytes(ctx);
     r.p = p;
     r.k = ctx->cfg.k;
     r.V = ctx->V;
@@ -888,11 +1045,9 @@ int sad_rank_global(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out
         launch_f1_gainfo(ctx->d_anc_local, ctx->pl, ctx->shard0, p, ctx->first_idx, ctx->d_ga_info, ctx->st);
         LAUNCHED();
     }
-#ifndef SAD_RANK_SORT_RUNS
-#define SAD_RANK_SORT_RUNS 4                 // blocks per shard of the local rank sort (then one merge)
-#endif
-    if (!(qbits == 32 && ctx->max_w <= kSmallSortMax * SAD_RANK_SORT_RUNS &&
-          seg_sort_pairs_runs(ctx->d_ckey, ctx->d_perm_in, ctx->d_shard_base, ctx->pl, SAD_RANK_SORT_RUNS, ctx->n,
+    constexpr int kRankSortRuns = 4;       // blocks per shard of the local rank sort (then one merge)
+    if (!(qbits == 32 && ctx->max_w <= kSmallSortMax * kRankSortRuns &&
+          seg_sort_pairs_runs(ctx->d_ckey, ctx->d_perm_in, ctx->d_shard_base, ctx->pl, kRankSortRuns, ctx->n,
                               ctx->d_ckey_sorted, ctx->d_perm_sorted, 32, ctx->st) == 0))
         CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
                       qbits + sbits));
@@ -916,8 +1071,29 @@ int sad_rank_global(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out
     return SAD_OK;
 }
 
-int sad_partition_plan(sad_ctx *ctx, const uint64_t *d_samples_all, int64_t *d_counts_out) {
-    GUARD(4);
+int sad_rank_global(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_samples_out) {
+    GUARD(3);
+    return rank_global_impl(ctx, d_anc_all, d_samples_out);
+}
+
+int sad_rank(sad_ctx *ctx, void *d_operand, size_t operand_bytes) {
+    GUARD(2);
+    if (ctx->cfg.world > 1 && !ctx->comm)
+        return fail(ctx, SAD_E_STATE, "sad_rank with world > 1 needs a communicator (sad_create with an NCCL id)");
+    ctx->capturing = stream_capturing(ctx->st);
+    if (int rc = rank_local_impl(ctx, d_operand, operand_bytes, ctx->d_anc_mine)) return rc;
+    // "Send the k samples from each processor to all the processors": the ancestor records
+    const void *anc_all = ctx->d_anc_mine;
+    if (ctx->comm) {
+        const size_t bytes = (size_t)exchange_records(ctx) * record_bytes(ctx);
+        NK(ncclAllGather(ctx->d_anc_mine, ctx->d_anc_all, bytes, ncclUint8, comm_of(ctx), ctx->st));
+        anc_all = ctx->d_anc_all;
+    }
+    return rank_global_impl(ctx, anc_all, reinterpret_cast<uint64_t *>(ctx->d_smp_mine));
+}
+
+// a9 + a10: pivots and bucket ranges
+static int plan_impl(sad_ctx *ctx, const uint64_t *d_samples_all, int64_t *d_counts_out) {
     const int p = ctx->cfg.p;
     if ((p > 1 && !d_samples_all) || !d_counts_out) return fail(ctx, SAD_E_ARG, "sad_partition_plan: NULL buffer");
     PlanArgs a{};
@@ -935,10 +1111,16 @@ int sad_partition_plan(sad_ctx *ctx, const uint64_t *d_samples_all, int64_t *d_c
     a.counts = d_counts_out;
     launch_plan(a, ctx->st);
     LAUNCHED();
-    CK(cudaMemcpyAsync(ctx->d_counts, d_counts_out, sizeof(int64_t) * (size_t)ctx->pl * p * 2,
-                       cudaMemcpyDeviceToDevice, ctx->st));
+    if (d_counts_out != ctx->d_counts)
+        CK(cudaMemcpyAsync(ctx->d_counts, d_counts_out, sizeof(int64_t) * (size_t)ctx->pl * p * 2,
+                           cudaMemcpyDeviceToDevice, ctx->st));
     ctx->stage = 5;
     return SAD_OK;
+}
+
+int sad_partition_plan(sad_ctx *ctx, const uint64_t *d_samples_all, int64_t *d_counts_out) {
+    GUARD(4);
+    return plan_impl(ctx, d_samples_all, d_counts_out);
 }
 
 int sad_exchange_sizes(int32_t p, int32_t world, int32_t rank, const int64_t *h_counts_all, int64_t *h_send_seqs,
@@ -981,14 +1163,12 @@ int sad_pack_plan(int32_t p, int32_t world, int32_t rank, const int64_t *h_count
     return SAD_OK;
 }
 
-int sad_pack(sad_ctx *ctx, const int64_t *h_counts_all, uint64_t *d_send_meta, uint8_t *d_send_res) {
-    GUARD(5);
-    if (!h_counts_all || !d_send_meta || !d_send_res) return fail(ctx, SAD_E_ARG, "sad_pack: NULL buffer");
+// K13: this rank's sequences grouped by destination rank; seg = the pack plan (pinned host, valid
+// until the copy has run)
+static int pack_impl(sad_ctx *ctx, const int64_t *h_seg_pinned, uint64_t *d_send_meta, uint8_t *d_send_res) {
     const int p = ctx->cfg.p;
-    std::vector<int64_t> seg((size_t)ctx->pl * p * 2, 0);
-    sad_pack_plan(p, ctx->cfg.world, ctx->cfg.rank, h_counts_all, seg.data());
-    std::memcpy(ctx->h_small + 2048, seg.data(), seg.size() * sizeof(int64_t));
-    CK(cudaMemcpyAsync(ctx->d_seg, ctx->h_small + 2048, seg.size() * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ctx->d_seg, h_seg_pinned, sizeof(int64_t) * (size_t)ctx->pl * p * 2, cudaMemcpyHostToDevice,
+                       ctx->st));
     PackArgs a{};
     a.key_sorted = ctx->d_key_sorted;
     a.perm_sorted = ctx->d_perm_sorted;
@@ -1007,7 +1187,17 @@ int sad_pack(sad_ctx *ctx, const int64_t *h_counts_all, uint64_t *d_send_meta, u
     a.send_res = d_send_res;
     launch_pack(a, ctx->st);
     LAUNCHED();
-    // the staging buffer is reused by later calls: make sure the copy has been consumed
+    return SAD_OK;
+}
+
+int sad_pack(sad_ctx *ctx, const int64_t *h_counts_all, uint64_t *d_send_meta, uint8_t *d_send_res) {
+    GUARD(5);
+    if (!h_counts_all || !d_send_meta || !d_send_res) return fail(ctx, SAD_E_ARG, "sad_pack: NULL buffer");
+    const int p = ctx->cfg.p;
+    int64_t *seg = reinterpret_cast<int64_t *>(ctx->h_small + 2048);
+    sad_pack_plan(p, ctx->cfg.world, ctx->cfg.rank, h_counts_all, seg);
+    if (int rc = pack_impl(ctx, seg, d_send_meta, d_send_res)) return rc;
+    // split API: the pinned staging of the plan is reused by the next call
     CK(cudaStreamSynchronize(ctx->st));
     return SAD_OK;
 }
@@ -1018,17 +1208,44 @@ int sad_output_size(const sad_ctx *cctx, const int64_t *h_counts_all, size_t *by
     if ((!h_counts_all && ctx->cfg.world != 1) || !bytes) return SAD_E_ARG;
     int64_t n_out, r_out;
     sum_recv(ctx, h_counts_all, n_out, r_out);
-    *bytes = out_layout(nullptr, n_out, r_out).total;
+    *bytes = out_layout(nullptr, n_out, r_out, false).total;
+    return SAD_OK;
+}
+
+int sad_output_bound(const sad_ctx *cctx, int64_t residues_global, size_t *bytes) {
+    sad_ctx *ctx = const_cast<sad_ctx *>(cctx);
+    GUARD(1);
+    if (!bytes) return SAD_E_ARG;
+    const int p = ctx->cfg.p;
+    if (ctx->cfg.world == 1) {
+        *bytes = out_layout(nullptr, ctx->n, ctx->R, coll_exchange(ctx)).total;
+        return SAD_OK;
+    }
+    if (residues_global < ctx->R) return fail(ctx, SAD_E_ARG, "residues_global < this rank's residues");
+    const int64_t w = (ctx->n_global + p - 1) / p;
+    const int64_t n_b = std::min<int64_t>(ctx->n_global, (int64_t)ctx->pl * (2 * w + p));   // reading A23
+    *bytes = out_layout(nullptr, n_b, residues_global, true).total;
     return SAD_OK;
 }
 
 int sad_output_layout(const sad_ctx *cctx, const int64_t *h_counts_all, int64_t *h_layout) {
     sad_ctx *ctx = const_cast<sad_ctx *>(cctx);
     GUARD(5);
-    if ((!h_counts_all && ctx->cfg.world != 1) || !h_layout) return SAD_E_ARG;
+    if (!h_layout) return SAD_E_ARG;
     int64_t n_out, r_out;
-    sum_recv(ctx, h_counts_all, n_out, r_out);
-    OutLayout o = out_layout(nullptr, n_out, r_out);
+    bool recv = false;
+    if (h_counts_all) {
+        sum_recv(ctx, h_counts_all, n_out, r_out);
+    } else if (ctx->stage >= 6) {    // the last finished partition
+        n_out = ctx->out_n;
+        r_out = ctx->out_r;
+        recv = ctx->out_recv_layout;
+    } else if (ctx->cfg.world == 1) {
+        sum_recv(ctx, nullptr, n_out, r_out);
+    } else {
+        return SAD_E_ARG;
+    }
+    OutLayout o = out_layout(nullptr, n_out, r_out, recv);
     h_layout[0] = n_out;
     h_layout[1] = r_out;
     h_layout[2] = (int64_t)reinterpret_cast<uintptr_t>(o.key);
@@ -1038,19 +1255,18 @@ int sad_output_layout(const sad_ctx *cctx, const int64_t *h_counts_all, int64_t 
     return SAD_OK;
 }
 
-int sad_finish(sad_ctx *ctx, const int64_t *h_counts_all, const uint64_t *d_recv_meta, const uint8_t *d_recv_res,
-               void *d_out, size_t out_bytes, int64_t *h_bucket_sizes) {
-    GUARD(5);
+// K14 receive side: merge the runs (this rank's own sorted shards for a local finish, or the
+// received runs in source-shard order) into the owned buckets, each in key order
+static int finish_impl(sad_ctx *ctx, const int64_t *h_counts_all, const uint64_t *d_recv_meta,
+                       const uint8_t *d_recv_res, void *d_out, size_t out_bytes, bool recv_layout) {
     const int p = ctx->cfg.p;
-    if ((!h_counts_all && ctx->cfg.world != 1) || !d_out) return fail(ctx, SAD_E_ARG, "sad_finish: NULL buffer");
     if ((reinterpret_cast<uintptr_t>(d_out) & 255) != 0) return fail(ctx, SAD_E_ARG, "output must be 256-byte aligned");
     const bool local = d_recv_meta == nullptr;
-    if (local && ctx->cfg.world != 1) return fail(ctx, SAD_E_ARG, "NULL receive buffers need world == 1");
     int64_t n_out, r_out;
     sum_recv(ctx, h_counts_all, n_out, r_out);
     if (local && h_counts_all && (n_out != ctx->n || r_out != ctx->R))
         return fail(ctx, SAD_E_STATE, "counts do not cover the input");
-    OutLayout o = out_layout(reinterpret_cast<uint8_t *>(d_out), n_out, r_out);
+    OutLayout o = out_layout(reinterpret_cast<uint8_t *>(d_out), n_out, r_out, recv_layout);
     if (out_bytes < o.total) return fail(ctx, SAD_E_CAPACITY, "output %zu < %zu bytes", out_bytes, o.total);
     const int nn = (int)n_out;
     // K14: merge the sorted runs by ranking (every owned bucket is a key range, so the merged
@@ -1077,7 +1293,7 @@ int sad_finish(sad_ctx *ctx, const int64_t *h_counts_all, const uint64_t *d_recv
     } else {                              // runs = the source shards, in rank (= shard) order
         if (n_out > 0 && (!d_recv_meta || (r_out > 0 && !d_recv_res)))
             return fail(ctx, SAD_E_ARG, "sad_finish: NULL receive buffer");
-        int64_t *runs = reinterpret_cast<int64_t *>(ctx->h_small + 16384);
+        int64_t *runs = recv_layout ? ctx->h_runs : reinterpret_cast<int64_t *>(ctx->h_small + 16384);
         runs[0] = 0;
         for (int s = 0; s < p; ++s) {
             int64_t c = 0;
@@ -1116,8 +1332,20 @@ int sad_finish(sad_ctx *ctx, const int64_t *h_counts_all, const uint64_t *d_recv
     ctx->out_bytes = out_bytes;
     ctx->out_n = n_out;
     ctx->out_r = r_out;
+    ctx->out_recv_layout = recv_layout;
     ctx->stage = 6;
     ctx->launches_last = ctx->launches_step;
+    return SAD_OK;
+}
+
+int sad_finish(sad_ctx *ctx, const int64_t *h_counts_all, const uint64_t *d_recv_meta, const uint8_t *d_recv_res,
+               void *d_out, size_t out_bytes, int64_t *h_bucket_sizes) {
+    GUARD(5);
+    const int p = ctx->cfg.p;
+    if ((!h_counts_all && ctx->cfg.world != 1) || !d_out) return fail(ctx, SAD_E_ARG, "sad_finish: NULL buffer");
+    const bool local = d_recv_meta == nullptr;
+    if (local && ctx->cfg.world != 1) return fail(ctx, SAD_E_ARG, "NULL receive buffers need world == 1");
+    if (int rc = finish_impl(ctx, h_counts_all, d_recv_meta, d_recv_res, d_out, out_bytes, false)) return rc;
     if (h_counts_all) {
         ctx->h_counts_all.assign(h_counts_all, h_counts_all + (size_t)p * p * 2);
         ctx->counts_pending = false;
@@ -1132,8 +1360,134 @@ int sad_finish(sad_ctx *ctx, const int64_t *h_counts_all, const uint64_t *d_recv
             if (int rc = sad_get_bucket_sizes(ctx, h_bucket_sizes)) return rc;
         }
     }
-    ctx->stage = 6;
-    ctx->launches_last = ctx->launches_step;
+    return SAD_OK;
+}
+
+int sad_exchange_verdict(int32_t p, int32_t world, const int64_t *h_gathered, int64_t *h_counts_all, int32_t *who,
+                         int32_t *kind) {
+    if (!h_gathered || !h_counts_all || p < 1 || world < 1 || p % world) return SAD_E_ARG;
+    const int pl = p / world;
+    const int64_t B = (int64_t)pl * p * 2 + 4;
+    if (who) *who = -1;
+    if (kind) *kind = 0;
+    // an input error anywhere: no rank moves data (peers report the first failing rank)
+    for (int r = 0; r < world; ++r) {
+        const int64_t *tail = h_gathered + (size_t)r * B + (size_t)pl * p * 2;
+        if (tail[1]) {
+            if (who) *who = r;
+            if (kind) *kind = (int32_t)tail[1];
+            return SAD_E_NCCL;
+        }
+    }
+    for (int r = 0; r < world; ++r)
+        if (h_gathered[(size_t)r * B + (size_t)pl * p * 2]) return SAD_E_REPLAN;   // an operand overflowed
+    // counts_all [p][p][2]: rank r's block holds shards r*pl .. in order
+    for (int r = 0; r < world; ++r)
+        std::memcpy(h_counts_all + (size_t)r * pl * p * 2, h_gathered + (size_t)r * B, sizeof(int64_t) * (size_t)pl * p * 2);
+    // every rank's output need against the capacity it announced
+    for (int r = 0; r < world; ++r) {
+        int64_t n_r = 0, r_r = 0;
+        for (int s = 0; s < p; ++s)
+            for (int b = r * pl; b < (r + 1) * pl; ++b) {
+                n_r += h_counts_all[((size_t)s * p + b) * 2 + 0];
+                r_r += h_counts_all[((size_t)s * p + b) * 2 + 1];
+            }
+        const int64_t have = h_gathered[(size_t)r * B + (size_t)pl * p * 2 + 2];
+        if ((int64_t)out_layout(nullptr, n_r, r_r, true).total > have) {
+            if (who) *who = r;
+            return SAD_E_CAPACITY;
+        }
+    }
+    return SAD_OK;
+}
+
+int sad_partition(sad_ctx *ctx, void *d_out, size_t out_bytes, int64_t *h_bucket_sizes) {
+    GUARD(4);
+    const int p = ctx->cfg.p, G = ctx->cfg.world, pl = ctx->pl;
+    if (G > 1 && !ctx->comm)
+        return fail(ctx, SAD_E_STATE, "sad_partition with world > 1 needs a communicator (sad_create with an NCCL id)");
+    if (!d_out || (G > 1 && !h_bucket_sizes)) return fail(ctx, SAD_E_ARG, "sad_partition: NULL buffer");
+    ctx->capturing = stream_capturing(ctx->st);
+    // a9: "Sort all the p*(p-1) ranks ..." -- every rank's regular samples, replicated selection
+    const uint64_t *smp_all = reinterpret_cast<const uint64_t *>(ctx->d_smp_mine);
+    if (ctx->comm && p > 1) {
+        NK(ncclAllGather(ctx->d_smp_mine, ctx->d_smp_all, (size_t)pl * (p - 1), ncclUint64, comm_of(ctx), ctx->st));
+        smp_all = reinterpret_cast<const uint64_t *>(ctx->d_smp_all);
+    }
+    if (int rc = plan_impl(ctx, smp_all, ctx->d_cnt_send)) return rc;
+    if (!coll_exchange(ctx)) {
+        // world == 1 without a communicator: the buckets are this rank's own shards, merged locally
+        if (int rc = finish_impl(ctx, nullptr, nullptr, nullptr, d_out, out_bytes, false)) return rc;
+        CK(cudaMemcpyAsync(ctx->h_small + 45056, ctx->d_counts, sizeof(int64_t) * (size_t)p * p * 2,
+                           cudaMemcpyDeviceToHost, ctx->st));
+        ctx->counts_pending = true;
+        if (h_bucket_sizes) {
+            if (int rc = sad_get_bucket_sizes(ctx, h_bucket_sizes)) return rc;
+        }
+        return SAD_OK;
+    }
+    if (ctx->capturing) return fail(ctx, SAD_E_STATE, "the count exchange synchronizes: it cannot be graph-captured");
+    // the count exchange: every rank's [pl][p][2] counts plus its status (operand overflow, first
+    // input error, output capacity), so that all ranks take the same decision
+    const int64_t B = count_block(ctx);
+    launch_status_tail(ctx->d_status, ctx->d_err, (int64_t)out_bytes, ctx->d_cnt_send + (size_t)pl * p * 2, ctx->st);
+    LAUNCHED();
+    NK(ncclAllGather(ctx->d_cnt_send, ctx->d_cnt_all, (size_t)B, ncclInt64, comm_of(ctx), ctx->st));
+    CK(cudaMemcpyAsync(ctx->h_cnt_all, ctx->d_cnt_all, sizeof(int64_t) * (size_t)G * B, cudaMemcpyDeviceToHost,
+                       ctx->st));
+    CK(cudaEventRecord(ctx->ev_stats, ctx->st));
+    if (int rc = wait_collective(ctx, ctx->ev_stats)) return rc;
+    // the same decision on every rank, from the same gathered blocks
+    std::vector<int64_t> counts_all((size_t)p * p * 2);
+    int32_t who = -1, kind = 0;
+    const int verdict = sad_exchange_verdict(p, G, ctx->h_cnt_all, counts_all.data(), &who, &kind);
+    const int own = absorb(ctx, true);   // this rank's own error / overflow, with its message
+    if (verdict == SAD_E_NCCL) {
+        if (own && own != SAD_E_REPLAN) return own;
+        static const char *kinds[4] = {"", "an illegal symbol", "a sequence shorter than k", "a sequence too long"};
+        return fail(ctx, SAD_E_NCCL, "rank %d reported %s; no data moved", who, kinds[kind & 3]);
+    }
+    if (verdict == SAD_E_REPLAN) {
+        ctx->kcap_blocks = std::max(ctx->kcap_blocks, ctx->kcap_next);
+        ctx->stage = 1;
+        return soft_fail(ctx, SAD_E_REPLAN, "a rank's all-pairs operand overflowed: rerun the step on every rank");
+    }
+    if (own) return own;
+    if (verdict == SAD_E_CAPACITY) {
+        ctx->stage = 4;              // the partition can be called again with a larger buffer
+        return soft_fail(ctx, SAD_E_CAPACITY, "rank %d: output buffer below its need (sad_output_bound)", who);
+    }
+    // a11: pack, then the all-to-all personalized exchange (grouped send / receive)
+    sad_pack_plan(p, G, ctx->cfg.rank, counts_all.data(), ctx->h_seg);
+    if (int rc = pack_impl(ctx, ctx->h_seg, reinterpret_cast<uint64_t *>(ctx->d_send_meta), ctx->d_send_res)) return rc;
+    std::vector<int64_t> ss(G), sr(G), rs(G), rr(G);
+    sad_exchange_sizes(p, G, ctx->cfg.rank, counts_all.data(), ss.data(), sr.data(), rs.data(), rr.data());
+    int64_t n_out = 0, r_out = 0;
+    for (int r = 0; r < G; ++r) {
+        n_out += rs[r];
+        r_out += rr[r];
+    }
+    OutLayout o = out_layout(reinterpret_cast<uint8_t *>(d_out), n_out, r_out, true);
+    NK(ncclGroupStart());
+    int64_t so = 0, sro = 0, ro = 0, rro = 0;
+    for (int r = 0; r < G; ++r) {
+        if (ss[r]) NK(ncclSend(ctx->d_send_meta + 2 * so, (size_t)(2 * ss[r]), ncclUint64, r, comm_of(ctx), ctx->st));
+        if (rs[r]) NK(ncclRecv(o.recv_meta + 2 * ro, (size_t)(2 * rs[r]), ncclUint64, r, comm_of(ctx), ctx->st));
+        if (sr[r]) NK(ncclSend(ctx->d_send_res + sro, (size_t)sr[r], ncclUint8, r, comm_of(ctx), ctx->st));
+        if (rr[r]) NK(ncclRecv(o.recv_res + rro, (size_t)rr[r], ncclUint8, r, comm_of(ctx), ctx->st));
+        so += ss[r];
+        sro += sr[r];
+        ro += rs[r];
+        rro += rr[r];
+    }
+    NK(ncclGroupEnd());
+    if (int rc = finish_impl(ctx, counts_all.data(), reinterpret_cast<const uint64_t *>(o.recv_meta), o.recv_res, d_out,
+                             out_bytes, true))
+        return rc;
+    ctx->h_counts_all = counts_all;
+    ctx->counts_pending = false;
+    bucket_sizes_from_counts(ctx);
+    if (h_bucket_sizes) std::memcpy(h_bucket_sizes, ctx->bucket_sizes.data(), sizeof(int64_t) * p);
     return SAD_OK;
 }
 
@@ -1148,9 +1502,16 @@ static void bucket_sizes_from_counts(sad_ctx *ctx) {
     for (int b = 0; b < p; ++b) ctx->bucket_first[b + 1] = ctx->bucket_first[b] + ctx->bucket_sizes[b];
 }
 
-static int resolve_counts(sad_ctx *ctx) {
-    if (!ctx->counts_pending) return SAD_OK;
+// every synchronizing getter: wait for the step, report its device-detected errors
+static int sync_step(sad_ctx *ctx) {
+    if (int rc = absorb(ctx, true)) return rc;
     CK(cudaStreamSynchronize(ctx->st));
+    return SAD_OK;
+}
+
+static int resolve_counts(sad_ctx *ctx) {
+    if (int rc = sync_step(ctx)) return rc;
+    if (!ctx->counts_pending) return SAD_OK;
     const int p = ctx->cfg.p;
     const int64_t *c = reinterpret_cast<const int64_t *>(ctx->h_small + 45056);
     ctx->h_counts_all.assign(c, c + (size_t)p * p * 2);
@@ -1196,6 +1557,7 @@ int sad_get_local_rank(sad_ctx *ctx, int shard, uint64_t *h_T, int64_t cap) {
     GUARD(3);
     int64_t b0, w;
     if (int rc = shard_check(ctx, shard, cap, b0, w)) return rc;
+    if (int rc = sync_step(ctx)) return rc;
     CK(cudaMemcpyAsync(h_T, ctx->d_T + b0, sizeof(uint64_t) * w, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     return SAD_OK;
@@ -1204,6 +1566,7 @@ int sad_get_local_rank(sad_ctx *ctx, int shard, uint64_t *h_T, int64_t cap) {
 int sad_get_ancestors(sad_ctx *ctx, int64_t *h_local, int64_t *h_ga) {
     GUARD(4);
     const int p = ctx->cfg.p;
+    if (int rc = sync_step(ctx)) return rc;
     std::vector<long long> g(p + 2);
     CK(cudaMemcpyAsync(g.data(), ctx->d_ga_info, sizeof(long long) * (p + 2), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
@@ -1216,6 +1579,7 @@ int sad_get_ranks(sad_ctx *ctx, int shard, uint32_t *h_S, uint32_t *h_den, uint6
     GUARD(4);
     int64_t b0, w;
     if (int rc = shard_check(ctx, shard, cap, b0, w)) return rc;
+    if (int rc = sync_step(ctx)) return rc;
     if (h_S) CK(cudaMemcpyAsync(h_S, ctx->d_S_ga + b0, 4 * w, cudaMemcpyDeviceToHost, ctx->st));
     if (h_den) CK(cudaMemcpyAsync(h_den, ctx->d_den_ga + b0, 4 * w, cudaMemcpyDeviceToHost, ctx->st));
     if (h_key) CK(cudaMemcpyAsync(h_key, ctx->d_key + b0, 8 * w, cudaMemcpyDeviceToHost, ctx->st));
@@ -1227,6 +1591,7 @@ int sad_get_sorted(sad_ctx *ctx, int shard, int64_t *h_idx, int64_t cap) {
     GUARD(4);
     int64_t b0, w;
     if (int rc = shard_check(ctx, shard, cap, b0, w)) return rc;
+    if (int rc = sync_step(ctx)) return rc;
     std::vector<int32_t> t(w);
     CK(cudaMemcpyAsync(t.data(), ctx->d_perm_sorted + b0, 4 * w, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
@@ -1236,6 +1601,7 @@ int sad_get_sorted(sad_ctx *ctx, int shard, int64_t *h_idx, int64_t cap) {
 
 int sad_get_pivots(sad_ctx *ctx, uint64_t *h_pivots) {
     GUARD(5);
+    if (int rc = sync_step(ctx)) return rc;
     if (ctx->cfg.p > 1) {
         CK(cudaMemcpyAsync(h_pivots, ctx->d_pivots, 8 * (ctx->cfg.p - 1), cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
@@ -1252,7 +1618,7 @@ int sad_get_bucket(sad_ctx *ctx, int bucket, int64_t *h_idx, uint64_t *h_key, ui
     int64_t first = 0;
     for (int b = b0; b < bucket; ++b) first += ctx->bucket_sizes[b];
     const int64_t n = ctx->bucket_sizes[bucket];
-    OutLayout o = out_layout(ctx->d_out, ctx->out_n, ctx->out_r);
+    OutLayout o = out_layout(ctx->d_out, ctx->out_n, ctx->out_r, ctx->out_recv_layout);
     int64_t r0 = 0, r1 = 0;
     CK(cudaMemcpyAsync(&r0, o.off + first, 8, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaMemcpyAsync(&r1, o.off + first + n, 8, cudaMemcpyDeviceToHost, ctx->st));
@@ -1282,6 +1648,7 @@ int sad_get_similarity(sad_ctx *ctx, int shard, uint16_t *h_S, int64_t cap) {
     int64_t b0, w;
     if (int rc = shard_check(ctx, shard, INT64_MAX, b0, w)) return rc;
     if (cap < w * w) return fail(ctx, SAD_E_CAPACITY, "capacity %lld < %lld", (long long)cap, (long long)(w * w));
+    if (int rc = sync_step(ctx)) return rc;
     int64_t sb = 0;
     for (int s = 0; s < shard; ++s) {
         const int64_t ws = ctx->shard_base[s + 1] - ctx->shard_base[s];
@@ -1301,7 +1668,7 @@ int sad_get_bucket_view(sad_ctx *ctx, int bucket, const uint8_t **d_res, const i
     int64_t first = 0;
     for (int b = b0; b < bucket; ++b) first += ctx->bucket_sizes[b];
     const int64_t nb = ctx->bucket_sizes[bucket];
-    OutLayout o = out_layout(ctx->d_out, ctx->out_n, ctx->out_r);
+    OutLayout o = out_layout(ctx->d_out, ctx->out_n, ctx->out_r, ctx->out_recv_layout);
     int64_t r[2] = {0, 0};
     CK(cudaMemcpyAsync(r, o.off + first, 8, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaMemcpyAsync(r + 1, o.off + first + nb, 8, cudaMemcpyDeviceToHost, ctx->st));
@@ -1359,10 +1726,11 @@ int sad_upgma(double *d_D, int64_t n, int64_t *d_merges, double *d_heights, int6
 
 int sad_get_profile_info(sad_ctx *ctx, int64_t *h_windows, int64_t *h_distinct, int64_t *h_kcols) {
     GUARD(2);
+    if (int rc = absorb(ctx, true)) return rc;
     for (int s = 0; s < ctx->pl; ++s) {
-        if (h_windows) h_windows[s] = ctx->h_windows[s];
-        if (h_distinct) h_distinct[s] = ctx->h_distinct[s];
-        if (h_kcols) h_kcols[s] = ctx->h_K[s];
+        if (h_windows) h_windows[s] = s < (int)ctx->h_windows.size() ? ctx->h_windows[s] : 0;
+        if (h_distinct) h_distinct[s] = s < (int)ctx->h_distinct.size() ? ctx->h_distinct[s] : 0;
+        if (h_kcols) h_kcols[s] = s < (int)ctx->h_K.size() ? ctx->h_K[s] : 0;
     }
     return SAD_OK;
 }
@@ -1389,6 +1757,22 @@ int sad_get_stats(sad_ctx *ctx, double *h_ms, int64_t *h_counts) {
         h_counts[2] = ctx->macs;
         h_counts[3] = ctx->launches_last;
     }
+    return SAD_OK;
+}
+
+int sad_graph_account(sad_ctx *ctx) {
+    if (!ctx) return SAD_E_ARG;
+    if (ctx->sticky) return SAD_E_STATE;
+    if (!ctx->graph_events) return fail(ctx, SAD_E_STATE, "no captured step");
+    DeviceScope dev_scope_(ctx->cfg.device);
+    CK(cudaStreamSynchronize(ctx->st));
+    float op = 0, ap = 0;
+    CK(cudaEventElapsedTime(&op, ctx->gev[0], ctx->gev[1]));
+    CK(cudaEventElapsedTime(&ap, ctx->gev[2], ctx->gev[3]));
+    ctx->ms_op += op;
+    ctx->ms_ap += ap;
+    ctx->calls += 1;
+    if (ctx->stage >= 6) ctx->counts_pending = true;   // the replay rewrote the counts: getters reread them
     return SAD_OK;
 }
 

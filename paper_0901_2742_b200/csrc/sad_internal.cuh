@@ -32,7 +32,8 @@ constexpr int kColPad = 128;        // operand columns padded to this (one 128-b
 constexpr int kKinfo = 24;          // u64 per shard in kinfo: [0] windows, [1] distinct, [2] K (no cap), [3] max Tw,
                                     // [4 + j] max_i sum_tau (n_i - 2^j)+, [8 + j] K under cap 2^j,
                                     // [12 + j] sum_tau C(X_j(tau), 2), [16 + j] sum_tau X_j(tau) with
-                                    // X_j(tau) = #{i : n_i(tau) > 2^j}   (j < kNumCaps)
+                                    // X_j(tau) = #{i : n_i(tau) > 2^j}   (j < kNumCaps);
+                                    // [20] operand columns K_s and [21] layer cap T_s chosen by k_select
 constexpr int kLenBinsMax = 65536; // Tw <= 65535 (checked by K1/K2)
 constexpr int kNumCaps = 4;         // candidate layer caps T = 1, 2, 4, 8
 constexpr int kXrSmem = 200 * 1024; // K6 row accumulators (u8 per shard column) per block
@@ -100,6 +101,18 @@ void launch_capscan(const uint32_t *in, int64_t in_stride, const uint32_t *sel, 
                     unsigned long long *total_out, int total_stride, int pl, int V, cudaStream_t st);
 void launch_kstats(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,
                    cudaStream_t st);
+// K3 decision on the device (no host round trip): per shard the layer cap T_s = the smallest
+// 2^j (j < kNumCaps) with max_i sum_tau (n_i(tau) - T)+ <= 255 when capping is allowed (else none),
+// the operand width K_s = sum_tau min(M(tau), T_s) and its K blocks (kcpb columns each, clipped
+// to the operand's capacity kcap_blocks). status[0] |= 1 when some K_s exceeds the capacity,
+// status[1] = max_s K_s (status zeroed by the caller). Writes kinfo[s][20] = K_s, [21] = T_s.
+void launch_select(unsigned long long *kinfo, int pl, int V, int allow_cap, int64_t kcap_blocks, int kcpb,
+                   uint32_t *cap, uint32_t *xsel, uint32_t *ident, int64_t *kblocks, unsigned long long *status,
+                   cudaStream_t st);
+// the count-exchange status of this rank appended to its count block: [0] operand overflow,
+// [1] first input error kind (0 none, 1 symbol, 2 too short, 3 too long), [2] out_bytes, [3] 0
+void launch_status_tail(const unsigned long long *status, const unsigned long long *err, int64_t out_bytes,
+                        int64_t *tail, cudaStream_t st);
 
 struct OperandArgs {
     const uint32_t *csr;
@@ -116,6 +129,8 @@ struct OperandArgs {
     const uint32_t *cap;             // device [pl] layer cap T_s per shard (kNoCap: none), or NULL
     const int32_t *sigma;            // device [n] length order (sorted position -> local index), or NULL
     const uint32_t *ident;           // device [pl] 1: the column of tau is tau (cap 1, all V k-mers present), or NULL
+    const int64_t *kblocks;          // device [pl] 128-byte K blocks of each shard's rows (only those are
+                                     // written; the row stride is the capacity), or NULL: the whole stride
 };
 void launch_indicator(const OperandArgs &a, cudaStream_t st);
 // length order by counting (K3): Tw histogram per shard, per-shard scan up to the max Tw in kinfo[3],
@@ -168,7 +183,7 @@ struct AllPairsArgs {
     const void *tmap;                // TC: CUtensorMap (64 B, host copy passed as __grid_constant__)
     const int64_t *h_shard_base;     // host copies (launch configuration)
     const int64_t *h_shard_rowpad;
-    const int64_t *h_kblocks;
+    int64_t kblocks_hint;            // TC: largest K block count expected (picks the deep ring; any value is exact)
     int kind;                        // TC: 0 = int8 operands (kind::i8), 1 = packed fp4 (kind::mxf4)
     const void *tiles;               // TC: device tile table (16 B per tile) and its length
     int64_t n_tiles_tc;
@@ -376,8 +391,6 @@ struct sad_ctx {
     int64_t rows_pad = 0, max_w = 0;
     std::vector<int64_t> h_windows, h_distinct, h_K; // [pl]
     std::vector<uint32_t> h_cap;                      // [pl] layer cap T_s (kNoCap: all layers dense)
-    bool use_excess = false;                          // some shard has entries above its cap (K6 runs)
-    int64_t n_x = 0;                                  // K6 list entries
     int64_t K_stride = 0, V_pad = 0;
     bool use_tc = false;
     int tc_kind = 1;                 // 0 = int8, 1 = fp4
@@ -436,6 +449,33 @@ struct sad_ctx {
     int64_t out_n = 0, out_r = 0;
     std::vector<int64_t> bucket_sizes, bucket_first;  // [p] sizes, first row of owned buckets in out
     std::vector<int64_t> h_counts_all;                  // [p][p][2]
+
+    // asynchronous step statistics: k-mer statistics, errors and the operand status are copied to
+    // pinned host memory at the end of sad_build_profiles and read at the next synchronizing call
+    unsigned long long *h_stats = nullptr;           // [8 + pl * kKinfo]: err[4], status[4], kinfo
+    cudaEvent_t ev_async = nullptr;
+    bool stats_pending = false;
+    unsigned long long *d_status = nullptr;         // [4] device: operand overflow, max K_s, -, -
+    int64_t kcap_blocks = 0;                         // operand K capacity (128-byte blocks per row)
+    int64_t kcap_next = 0;                           // the capacity the next step starts with
+    int64_t kmax_blocks_seen = -1;                   // largest K blocks of the last absorbed step (-1: none)
+    bool allow_cap = false;                          // capped layers + K6 excess possible in this layout
+    int64_t x_entries_bound = 0;                     // K6 list entries bound (all CSR entries)
+
+    // collective API
+    void *comm = nullptr;                            // ncclComm_t (NULL: none)
+    void *d_anc_mine = nullptr, *d_anc_all = nullptr;
+    unsigned long long *d_smp_mine = nullptr, *d_smp_all = nullptr;
+    int64_t *d_cnt_send = nullptr, *d_cnt_all = nullptr;   // [pl*p*2 + 4] / [world][pl*p*2 + 4]
+    int64_t *h_cnt_all = nullptr;                    // pinned copy of d_cnt_all
+    int64_t *h_seg = nullptr;                        // pinned pack plan of the collective path
+    int64_t *h_runs = nullptr;                       // pinned receive runs
+    unsigned long long *d_send_meta = nullptr;
+    uint8_t *d_send_res = nullptr;
+    bool capturing = false;                          // the stream is being captured into a CUDA graph
+    cudaEvent_t gev[4] = {};                         // stage events recorded inside a captured step
+    bool graph_events = false;
+    bool out_recv_layout = false;                    // the output buffer holds the receive buffers too
 
     // layout of the last uploaded per-shard tables
     uint8_t *tbl_ws = nullptr;

@@ -110,7 +110,11 @@ class Context:
 
     def __init__(self, alphabet: str, k: int, p: int, *, world: int = 1, rank: int = 0, device: int | None = None,
                  stream: torch.cuda.Stream | None = None, kernel: str = "tc", keep_sim: bool = False, group=None,
-                 rank_mode: str = "ga"):
+                 rank_mode: str = "ga", comm: bool = False):
+        """comm: give the library its own NCCL communicator (sad_create with an id that rank 0 draws
+        and torch.distributed broadcasts over `group`): the collective calls sad_rank / sad_partition
+        then run every exchange themselves. Needed by run() when world > 1; with world == 1 it makes
+        the exchange steps run through NCCL anyway (a single-rank communicator)."""
         if not torch.cuda.is_available():
             raise RuntimeError("the k-mer-rank path needs a CUDA device (no CPU fallback)")
         if device is None:
@@ -129,7 +133,18 @@ class Context:
         self.kernel = kernel
         cfg = L.SadConfig(ALPHABETS[alphabet], k, p, world, rank, device, self.stream.cuda_stream, flags)
         h = ctypes.c_void_p()
-        L.call("sad_create", ctypes.byref(cfg), ctypes.byref(h))
+        nid = None
+        if comm:
+            uid = (ctypes.c_uint8 * 128)()
+            if rank == 0:
+                L.call("sad_nccl_unique_id", uid)
+            if world > 1:                      # rank 0's id to every rank (the only torch exchange)
+                box = [bytes(uid)]
+                dist.broadcast_object_list(box, src=0, group=group)
+                ctypes.memmove(uid, box[0], 128)
+            nid = uid
+        self.comm = comm
+        L.call("sad_create", ctypes.byref(cfg), nid, ctypes.byref(h))
         self._h = h
         self._bufs: dict[str, torch.Tensor] = {}
         self.rec_bytes = int(L.lib().sad_ancestor_record_bytes(h))
@@ -257,20 +272,90 @@ class Context:
         recv_res = all_to_all_v(send_res, sr, rr, self.group)
         return self.finish(counts_all, recv_meta, recv_res)
 
-    def run(self, sync: bool = True):
-        """One full step: profiles -> local rank -> GA rank -> plan -> redistribution.
-        Returns the sizes of all p buckets (host); with world == 1 and sync=False nothing is
-        read back (the step is left enqueued on the stream) and None is returned."""
-        self.build_profiles()
-        anc = self.rank_local()
+    def run(self, sync: bool = True, residues_global: int | None = None):
+        """One full step through the collective API (include/sad.h): sad_build_profiles ->
+        sad_rank -> sad_partition. Returns the sizes of all p buckets (host); with world == 1 and
+        sync=False nothing is read back (the step stays enqueued on the stream; no host
+        synchronization at all) and None is returned. world > 1 needs comm=True; residues_global
+        (all ranks' residues) sizes the output by the partition bound (sad_output_bound).
+        SAD_E_REPLAN (the operand capacity grew) reruns the step."""
+        if self.world > 1 and not self.comm:
+            return self.run_split()
+        for attempt in range(4):
+            try:
+                return self._step(sync, residues_global)
+            except L.SadError as e:
+                if e.code != L.SAD_E_REPLAN or attempt == 3:
+                    raise
+
+    def _step(self, sync, residues_global):
+        self._call("sad_build_profiles")
+        ob = ctypes.c_size_t()
+        self._call("sad_operand_size", ctypes.byref(ob))
+        p_op = self._buf("operand", ob.value, align=1024)
+        self._call("sad_rank", ctypes.c_void_p(p_op), ob.value)
+        if self.world > 1 and residues_global is None:
+            residues_global = self._residues_global()
+        obytes = ctypes.c_size_t()
+        self._call("sad_output_bound", int(residues_global or self.R), ctypes.byref(obytes))
+        p_out = self._buf("out", obytes.value, align=256)
+        want = sync or self.world > 1
+        sizes = np.zeros(self.p, np.int64) if want else None
+        self._call("sad_partition", ctypes.c_void_p(p_out), obytes.value, _vp(sizes))
+        self._out_ptr = p_out
+        lay = np.zeros(6, np.int64)
+        self._call("sad_output_layout", None, _vp(lay))
+        self.layout = lay
+        self.bucket_sizes = sizes
+        return sizes
+
+    def _residues_global(self) -> int:
+        """Sum of every rank's residues (once per layout; torch.distributed over `group`)."""
+        key = (self.n_local, self.R)
+        if getattr(self, "_rg_key", None) != key:
+            t = torch.tensor([self.R], dtype=torch.int64,
+                             device=self.device if dist.get_backend(self.group) == "nccl" else "cpu")
+            dist.all_reduce(t, group=self.group)
+            self._rg, self._rg_key = int(t.item()), key
+        return self._rg
+
+    def run_split(self):
+        """One full step through the split API, the exchanges done here over torch.distributed
+        (gloo on CPU tests, NCCL on GPUs): used for world > 1 contexts without a library
+        communicator."""
+        for attempt in range(4):
+            self.build_profiles()
+            try:
+                anc = self.rank_local()
+                break
+            except L.SadError as e:
+                if e.code != L.SAD_E_REPLAN or attempt == 3:
+                    raise
         anc_all = all_gather_rows(anc, self.world, self.group)
         samples = self.rank_global(anc_all)
         samples_all = all_gather_rows(samples, self.world, self.group) if self.p > 1 else samples
         counts = self.partition_plan(samples_all)
         if self.world == 1:
-            return self.finish(None, sync=sync)
+            return self.finish(None)
         counts_all = all_gather_rows(counts, self.world, self.group).cpu().numpy()   # the one D2H of the plan
         return self.redistribute(counts_all.reshape(self.p, self.p, 2))
+
+    # -- CUDA graph of one device-resident step (world == 1, no communicator) --------------
+    def capture_step(self, d_ascii: torch.Tensor, d_offsets: torch.Tensor, residues: int):
+        """Capture load (device inputs) + one whole step into a CUDA graph on this context's stream
+        (which must not be the legacy default stream). Run one eager step on the same inputs first
+        (it sizes every buffer and the operand capacity). Returns the torch.cuda.CUDAGraph; after
+        each replay() has completed, call graph_account() to add the replay's stage times."""
+        if self.world != 1 or self.comm:
+            raise ValueError("graph capture needs world == 1 without a communicator")
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream, capture_error_mode="relaxed"):
+            self.load(d_ascii, d_offsets, self.n_global, self.first_index, residues=residues)
+            self._step(False, None)
+        return g
+
+    def graph_account(self):
+        self._call("sad_graph_account")
 
     def bucket_sizes_now(self) -> np.ndarray:
         out = np.zeros(self.p, np.int64)

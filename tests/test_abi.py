@@ -25,7 +25,7 @@ def test_exports_every_declared_symbol(L):
     for name in declared:
         assert hasattr(lib, name), f"libsad.so does not export {name}"
     assert sorted(declared) == sorted(L.SYMBOLS)
-    assert lib.sad_abi_version() == 1
+    assert lib.sad_abi_version() == 2
 
 
 def _model_sizes(p, G, rank, c):
