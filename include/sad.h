@@ -90,8 +90,10 @@ extern "C" {
 #define SAD_F_RANK_SAMPLES 64u /* SURVEY §8(f) row f1, the paper's literal listing: rank every
                                  sequence by its mean fixed-point similarity to the k*p gathered samples
                                  (k = p-1 per shard, evenly spaced in the local order by T) instead of by
-                                 its similarity to the global ancestor; key = (floor(sum_s q / (p(p-1)))
-                                 << 31) + index. Needs p >= 2 and A^k <= 25600. sad_rank_local then
+                                 its similarity to the global ancestor: by the exact sum T' = sum_s q
+                                 (the mean's 1/(p(p-1)) is a common factor, reading A27), ties by index;
+                                 key = (T' << sad_key_index_bits) + index (needs p(p-1) 2^32 N < 2^64).
+                                 Needs p >= 2 and A^k <= 25600. sad_rank_local then
                                  writes p/world*(p-1) sample records instead of p/world ancestor records
                                  (sad_exchange_records) and sad_rank_global takes all p(p-1) of them. */
 #define SAD_F_TC_ALL_LAYERS 32u /* tensor-core path with every threshold layer t <= max n(tau) dense in the
@@ -259,6 +261,12 @@ int sad_partition(sad_ctx *ctx, void *d_out, size_t out_bytes, int64_t *h_bucket
  * padded to 16 bytes. */
 size_t sad_ancestor_record_bytes(const sad_ctx *ctx);
 
+/* Index bits of the uint64 rank keys: key = (rank value << bits) + source index. 31 when ranking
+ * against the GA (value floor(2^32 S/den) <= 2^32); with SAD_F_RANK_SAMPLES the bit
+ * length of N - 1 (value = the exact fixed-point sum T' < p(p-1) 2^32, reading A27). Valid after
+ * sad_load. */
+int32_t sad_key_index_bits(const sad_ctx *ctx);
+
 /* Records this rank contributes to the exchange after sad_rank_local (and that sad_rank_global
  * expects world times): p/world ancestor records, or p/world*(p-1) rank-sample records with
  * SAD_F_RANK_SAMPLES. Each record is sad_ancestor_record_bytes long. */
@@ -377,7 +385,8 @@ int sad_get_local_rank(sad_ctx *ctx, int shard, uint64_t *h_T, int64_t cap);
 /* Local ancestors of ALL p shards and the GA, as global source indices (after sad_rank_global). */
 int sad_get_ancestors(sad_ctx *ctx, int64_t *h_local, int64_t *h_ga);
 
-/* S_i, den_i and key_i of every sequence of local shard s, in input order (after sad_rank_global). */
+/* S_i, den_i and key_i of every sequence of local shard s, in input order (after sad_rank_global).
+ * With SAD_F_RANK_SAMPLES: S_i = T'_i mod 2^32 and den_i = T'_i >> 32 (T' the rank sum, A27). */
 int sad_get_ranks(sad_ctx *ctx, int shard, uint32_t *h_S, uint32_t *h_den, uint64_t *h_key, int64_t cap);
 
 /* Source indices of local shard s in its local sort order (after sad_rank_global). */

@@ -58,6 +58,8 @@ def lib():
         L.or_run2.argtypes = [P, P, i64, i32, i32, i32, i32, i32] + [P] * 15
         L.or_rows_T.restype = i32
         L.or_rows_T.argtypes = [P, P, i64, i32, i32, P, i64, i32, P]
+        L.or_rank_vs_set.restype = i32
+        L.or_rank_vs_set.argtypes = [P, P, i64, i32, P, i64, i32, P]
         L.or_pairs_S.restype = i32
         L.or_pairs_S.argtypes = [P, P, i32, P, P, i64, i32, P, P]
         L.or_rank_R.restype = ctypes.c_double
@@ -141,7 +143,8 @@ class Result:
 def run(ascii_, offsets, alphabet: str, k: int, p: int, nthreads: int = 0, mode: str = "ga") -> Result:
     """The whole oracle pipeline on one process. mode "ga": rank against
     the global ancestor (readings A7, A8); "samples": the paper's literal rank against the k*p
-    gathered samples (S and den then hold (Dbar, 1))."""
+    gathered samples (reading A27; S and den then hold (T', 1), T' the exact
+    fixed-point sum of q over the samples)."""
     a = np.ascontiguousarray(ascii_, dtype=np.uint8)
     if a.size == 0:
         a = np.zeros(1, np.uint8)
@@ -171,6 +174,19 @@ def rows_T(ascii_, offsets, k: int, p: int, rows, nthreads: int = 0) -> np.ndarr
     if rc:
         raise OracleError(rc)
     return out[: len(r)]
+
+
+def rank_vs_set(ascii_, offsets, k: int, ref, nthreads: int = 0) -> np.ndarray:
+    """T'_i = sum over the reference set `ref` (source indices) of q(x_i, s), for every sequence."""
+    a = np.ascontiguousarray(ascii_, dtype=np.uint8)
+    o = np.ascontiguousarray(offsets, dtype=np.int64)
+    r = np.ascontiguousarray(ref, dtype=np.int64)
+    n = len(o) - 1
+    out = np.zeros(max(n, 1), np.uint64)
+    rc = lib().or_rank_vs_set(_p(a), _p(o), n, k, _p(r), len(r), nthreads, _p(out))
+    if rc:
+        raise OracleError(rc)
+    return out[:n]
 
 
 def pairs_S(ascii_, offsets, k: int, pi, pj, nthreads: int = 0):

@@ -36,7 +36,7 @@
 #define OR_E_EMPTY (-7)
 #define OR_E_OOM (-11)
 
-int or_abi(void) { return 4; }
+int or_abi(void) { return 5; }
 
 /* ---------------------------------------------------------------------------
  * Input alphabet ("Input <- N sequences of amino acids x1 ... xN";
@@ -241,8 +241,10 @@ int or_run(const uint8_t *ascii, const int64_t *offsets, int64_t n, int alphabet
  * mode 1: the paper's literal listing: the
  *   k = p-1 rank samples of every shard are the sequences at the evenly spaced positions of its
  *   local order, and every sequence is ranked by its mean fixed-point similarity to the
- *   m = p(p-1) gathered samples, Dbar_i = floor(sum_s q(x_i, s) / m) (reading A5 for the sum);
- *   the rank order is (Dbar, index); Sg/dg report (Dbar, 1), ga = -1, and rsamples[m] the
+ *   m = p(p-1) gathered samples, D_i = (1/m) sum_s r(x_i, s) (PAPER.md:46 with the samples as
+ *   the reference set), carried as the exact fixed-point sum T'_i = sum_s q(x_i, s) (reading A5;
+ *   the common factor 1/m is dropped exactly as A5 drops 1/N, reading A27); the rank order is
+ *   (T', index); Sg/dg report (T', 1), ga = -1, and rsamples[m] the
  *   rank samples (source indices). Needs p >= 2. */
 int or_run2(const uint8_t *ascii, const int64_t *offsets, int64_t n, int alphabet, int k, int p, int mode,
             int nthreads, uint64_t *T, int64_t *anc, int64_t *ga, int64_t *Sg, int64_t *dg, int64_t *sorted,
@@ -352,7 +354,7 @@ int or_run2(const uint8_t *ascii, const int64_t *offsets, int64_t n, int alphabe
          * :69 "Choose a sample set of k sequences in each processor" (k = p-1 at the evenly
          * spaced 1-based positions floor(j*w/p), readings A10, A20), :70 "Send the k samples
          * from each processor to all the processors", :72 "Compute the k-mer rank of each
-         * sequence against the k*p samples": Dbar_i = floor(sum_s q(x_i, s) / m). */
+         * sequence against the k*p samples": T'_i = sum_s q(x_i, s), ordered exactly (A27). */
         int64_t m = (int64_t)p * (p - 1);
         int64_t *rs = (int64_t *)malloc(sizeof(int64_t) * (size_t)m);
         tkey *tk = (tkey *)malloc(sizeof(tkey) * (size_t)n);
@@ -370,7 +372,7 @@ int or_run2(const uint8_t *ascii, const int64_t *offsets, int64_t n, int alphabe
                 int64_t j = rs[t], Lj = offsets[j + 1] - offsets[j];
                 acc += or_q((uint64_t)min_sum(&kc[i], &kc[j], k), (uint64_t)den_of(Li, Lj, k));
             }
-            rk[i].S = (int64_t)(acc / (uint64_t)m);
+            rk[i].S = (int64_t)acc;      /* T'_i < m 2^32 + 1: the cross products below stay < 2^63 */
             rk[i].den = 1;
             rk[i].idx = i;
         }
@@ -486,6 +488,42 @@ int or_rows_T(const uint8_t *ascii, const int64_t *offsets, int64_t n, int k, in
         T_out[r] = acc;
     }
     free(sb);
+    return fail ? OR_E_OOM : OR_OK;
+}
+
+/*
+ * or_rank_vs_set — T'_i = sum over a reference set of q(x_i, s) for every sequence i (PAPER.md:46,
+ * D_i = (1/m) sum_s r(x_i, s) in the fixed point of reading A5; the rank of SURVEY §8(f) f1 with
+ * the set = the gathered samples, and of f2 with the set = all N sequences, "sample
+ * degeneracy"). set[m] are source indices (repeats allowed).
+ */
+int or_rank_vs_set(const uint8_t *ascii, const int64_t *offsets, int64_t n, int k, const int64_t *set, int64_t m,
+                   int nthreads, uint64_t *T_out) {
+    if (n <= 0 || m < 0) return OR_E_ARG;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    kcounts *kc = (kcounts *)calloc((size_t)n, sizeof(kcounts));
+    int fail = 0;
+#pragma omp parallel for schedule(dynamic, 64) reduction(| : fail)
+    for (int64_t i = 0; i < n; ++i)
+        fail |= count_kmers(ascii + offsets[i], offsets[i + 1] - offsets[i], k, &kc[i]) != 0;
+    if (!fail) {
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int64_t i = 0; i < n; ++i) {
+            uint64_t acc = 0;
+            int64_t Li = offsets[i + 1] - offsets[i];
+            for (int64_t t = 0; t < m; ++t) {
+                int64_t j = set[t], Lj = offsets[j + 1] - offsets[j];
+                acc += or_q((uint64_t)min_sum(&kc[i], &kc[j], k), (uint64_t)den_of(Li, Lj, k));
+            }
+            T_out[i] = acc;
+        }
+    }
+    for (int64_t i = 0; i < n; ++i) free_counts(&kc[i]);
+    free(kc);
     return fail ? OR_E_OOM : OR_OK;
 }
 

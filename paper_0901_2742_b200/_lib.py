@@ -29,7 +29,7 @@ SYMBOLS = [
     "sad_get_pivots", "sad_get_bucket", "sad_get_bucket_sizes", "sad_get_similarity", "sad_get_profile_info", "sad_get_stats",
     "sad_reset_stats", "sad_selftest_fixed_point", "sad_get_bucket_view", "sad_get_distance", "sad_exchange_records", "sad_get_distance_f64",
     "sad_upgma_workspace", "sad_upgma", "sad_get_load_report", "sad_nccl_unique_id", "sad_abort", "sad_rank",
-    "sad_partition", "sad_output_bound", "sad_graph_account", "sad_exchange_verdict",
+    "sad_partition", "sad_output_bound", "sad_graph_account", "sad_exchange_verdict", "sad_key_index_bits",
 ]
 
 
@@ -68,6 +68,7 @@ def lib():
         "sad_output_bound": (i32, [P, i64, ctypes.POINTER(sz)]),
         "sad_graph_account": (i32, [P]),
         "sad_exchange_verdict": (i32, [i32, i32, P, P, P, P]),
+        "sad_key_index_bits": (i32, [P]),
         "sad_destroy": (None, [P]),
         "sad_last_error": (ctypes.c_char_p, [P]),
         "sad_error_location": (i32, [P, P, P]),

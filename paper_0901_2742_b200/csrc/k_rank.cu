@@ -384,25 +384,27 @@ void launch_gather_out(const int32_t *perm, int64_t n, const int64_t *src_off, c
 }
 
 
-// unpack the sorted composite keys (shard | q | row) into the real keys and rows
+// unpack the sorted composite keys (shard | q | row) into the real keys (q << ibits) + source
+// index and rows. GA mode (qbits 32): the sort key holds min(q, 2^32 - 1); q = 2^32 (S = den) is
+// restored from the all-ones value, which no other q reaches.
 __global__ void k_unpack_sorted(const unsigned long long *ck, const int32_t *perm_sorted, int64_t n, int64_t first_idx,
                                 unsigned long long *key_sorted, const RowInfo *rowinfo, int k, int64_t *len_sorted,
-                                unsigned long long qmask) {
+                                unsigned long long qmask, int ibits) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long q32 = ck[t] & qmask;
         const unsigned long long q = (qmask == 0xFFFFFFFFull && q32 == 0xFFFFFFFFull) ? (1ull << 32) : q32;
         const int32_t row = perm_sorted[t];
-        key_sorted[t] = (q << 31) + (unsigned long long)(first_idx + row);
+        key_sorted[t] = (q << ibits) + (unsigned long long)(first_idx + row);
         len_sorted[t] = (int64_t)rowinfo[row].tw + k - 1;
     }
 }
 
 void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, int64_t n,
                           int64_t first_idx, unsigned long long *key_sorted, const RowInfo *rowinfo, int k,
-                          int64_t *len_sorted, int qbits, cudaStream_t st) {
+                          int64_t *len_sorted, int qbits, int ibits, cudaStream_t st) {
     if (n > 0)
         k_unpack_sorted<<<grid1d(n), 256, 0, st>>>(ckey_sorted, perm_sorted, n, first_idx, key_sorted, rowinfo, k,
-                                                   len_sorted, (1ull << qbits) - 1ull);
+                                                   len_sorted, (1ull << qbits) - 1ull, ibits);
 }
 
 // K14: merge by ranking. Keys are unique, every run is sorted, so the output slot of an element is
@@ -696,25 +698,29 @@ int launch_rank_vs_samples(const RankArgs &a, int m, unsigned long long *Tp, int
     return 0;
 }
 
-// Dbar_i = floor(T'_i / m); key_i = (Dbar_i << 31) + source index; the a7 sort key (shard, Dbar)
-// takes 33 bits of Dbar (Dbar <= 2^32). S_ga reports the low 32 bits of Dbar, den_ga 0.
-__global__ void k_f1_keys(const unsigned long long *Tp, int64_t n, int m, int64_t first_idx, const RowInfo *rowinfo,
-                          unsigned long long *key, unsigned long long *ckey, int32_t *perm_in, uint32_t *S_ga,
-                          uint32_t *den_ga) {
+// f1 rank (reading A27): the exact fixed-point sum T'_i = sum_s q(x_i, s) over the m samples
+// (T' < 2^tbits, tbits = 32 + bit length of m) orders the sequences, ties by source index:
+// key_i = (T'_i << ibits) + source index (ibits = bit length of N - 1; tbits + ibits <= 64 is
+// checked by sad_load); the a7 sort key is (shard << tbits) | T'. S_ga / den_ga report T' mod 2^32
+// and T' >> 32.
+__global__ void k_f1_keys(const unsigned long long *Tp, int64_t n, int tbits, int ibits, int64_t first_idx,
+                          const RowInfo *rowinfo, unsigned long long *key, unsigned long long *ckey, int32_t *perm_in,
+                          uint32_t *S_ga, uint32_t *den_ga) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long db = Tp[i] / (unsigned long long)m;
-        key[i] = (db << 31) + (unsigned long long)(first_idx + i);
-        ckey[i] = ((unsigned long long)rowinfo[i].shard << 33) | db;
+        const unsigned long long t = Tp[i];
+        key[i] = (t << ibits) + (unsigned long long)(first_idx + i);
+        ckey[i] = ((unsigned long long)rowinfo[i].shard << tbits) | t;
         perm_in[i] = (int32_t)i;
-        S_ga[i] = (uint32_t)db;
-        den_ga[i] = 0u;
+        S_ga[i] = (uint32_t)t;
+        den_ga[i] = (uint32_t)(t >> 32);
     }
 }
 
-void launch_f1_keys(const unsigned long long *Tp, int64_t n, int m, int64_t first_idx, const RowInfo *rowinfo,
-                    unsigned long long *key, unsigned long long *ckey, int32_t *perm_in, uint32_t *S_ga,
-                    uint32_t *den_ga, cudaStream_t st) {
-    if (n > 0) k_f1_keys<<<grid1d(n), 256, 0, st>>>(Tp, n, m, first_idx, rowinfo, key, ckey, perm_in, S_ga, den_ga);
+void launch_f1_keys(const unsigned long long *Tp, int64_t n, int tbits, int ibits, int64_t first_idx,
+                    const RowInfo *rowinfo, unsigned long long *key, unsigned long long *ckey, int32_t *perm_in,
+                    uint32_t *S_ga, uint32_t *den_ga, cudaStream_t st) {
+    if (n > 0)
+        k_f1_keys<<<grid1d(n), 256, 0, st>>>(Tp, n, tbits, ibits, first_idx, rowinfo, key, ckey, perm_in, S_ga, den_ga);
 }
 
 // f1 has no global ancestor: ga_info = {-1, -1, local ancestors of this rank's shards, -1 elsewhere}

@@ -579,6 +579,15 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
                     (long long)(first_index_of_rank(ctx, n_global) + sb[ctx->pl]), (long long)n_local,
                     (long long)first_source_index);
     if (n_local == 0) return fail(ctx, SAD_E_EMPTY, "rank has no sequences");
+    if (ctx->cfg.flags & SAD_F_RANK_SAMPLES) {
+        // f1 keys (reading A27): (T' << ibits) + index with T' < m 2^32, m = p(p-1)
+        auto bitlen = [](uint64_t v) { int b = 0; while (v) { ++b; v >>= 1; } return b; };
+        ctx->tbits = 32 + bitlen((uint64_t)p * (p - 1));
+        ctx->ibits = std::max(1, bitlen((uint64_t)(n_global - 1)));
+        if (ctx->tbits + ctx->ibits > 64)
+            return fail(ctx, SAD_E_ARG, "rank vs samples: p(p-1) 2^32 N >= 2^64 (the exact key needs %d bits)",
+                        ctx->tbits + ctx->ibits);
+    }
     if (n_global / p + 1 >= (int64_t(1) << 24)) return fail(ctx, SAD_E_ARG, "shards of 2^24 or more sequences");
     ctx->capturing = stream_capturing(ctx->st);
     int64_t R = residues_local;
@@ -823,6 +832,8 @@ int sad_operand_size(const sad_ctx *cctx, size_t *bytes) {
     return SAD_OK;
 }
 
+int32_t sad_key_index_bits(const sad_ctx *ctx) { return ctx ? ctx->ibits : SAD_E_ARG; }
+
 int32_t sad_exchange_records(const sad_ctx *ctx) {
     if (!ctx) return SAD_E_ARG;
     return exchange_records(ctx);
@@ -1025,22 +1036,22 @@ static int rank_global_impl(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_sam
     while ((1 << sbits) < ctx->pl) ++sbits;
     r.ckey = ctx->d_ckey;
     const bool f1 = ctx->cfg.flags & SAD_F_RANK_SAMPLES;
-    const int qbits = f1 ? 33 : 32;
+    const int qbits = ctx->tbits;
     if (!f1) {
         launch_ga_pairs(r, ctx->st);
         LAUNCHED();
         launch_rank_vs_ga(r, ctx->st);
         LAUNCHED();
     } else {
-        // f1: T'_i = sum of q(x_i, s) over the m = p(p-1) gathered samples, then
-        // Dbar_i = floor(T'_i / m) and the keys (d_key doubles as the T' accumulator)
+        // f1 (reading A27): T'_i = sum of q(x_i, s) over the m = p(p-1) gathered
+        // samples, ordered exactly, and the keys (d_key doubles as the T' accumulator)
         const int m = p * (p - 1);
         CK(cudaMemsetAsync(ctx->d_key, 0, sizeof(unsigned long long) * (size_t)ctx->n, ctx->st));
         if (launch_rank_vs_samples(r, m, ctx->d_key, ctx->num_sms, ctx->st))
             return fail(ctx, SAD_E_ARG, "rank vs samples: V too large");
         LAUNCHED();
-        launch_f1_keys(ctx->d_key, ctx->n, m, ctx->first_idx, ctx->d_rowinfo, ctx->d_key, ctx->d_ckey, ctx->d_perm_in,
-                       ctx->d_S_ga, ctx->d_den_ga, ctx->st);
+        launch_f1_keys(ctx->d_key, ctx->n, ctx->tbits, ctx->ibits, ctx->first_idx, ctx->d_rowinfo, ctx->d_key,
+                       ctx->d_ckey, ctx->d_perm_in, ctx->d_S_ga, ctx->d_den_ga, ctx->st);
         LAUNCHED();
         launch_f1_gainfo(ctx->d_anc_local, ctx->pl, ctx->shard0, p, ctx->first_idx, ctx->d_ga_info, ctx->st);
         LAUNCHED();
@@ -1053,7 +1064,7 @@ static int rank_global_impl(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_sam
                       qbits + sbits));
     LAUNCHED();
     launch_unpack_sorted(ctx->d_ckey_sorted, ctx->d_perm_sorted, ctx->n, ctx->first_idx, ctx->d_key_sorted,
-                         ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, qbits, ctx->st);
+                         ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, qbits, ctx->ibits, ctx->st);
     LAUNCHED();
     // exclusive prefix of L in sorted order (the residue offsets of every bucket slice, K12/K13)
     CK(cudaMemsetAsync(ctx->d_lpre, 0, sizeof(int64_t), ctx->st));
@@ -1636,7 +1647,7 @@ int sad_get_bucket(sad_ctx *ctx, int bucket, int64_t *h_idx, uint64_t *h_key, ui
     CK(cudaStreamSynchronize(ctx->st));
     for (int64_t i = 0; i < n; ++i) {
         if (h_key) h_key[i] = keys[i];
-        if (h_idx) h_idx[i] = (int64_t)(keys[i] & 0x7FFFFFFFull);
+        if (h_idx) h_idx[i] = (int64_t)(keys[i] & ((1ull << ctx->ibits) - 1ull));
     }
     if (h_offsets) for (int64_t i = 0; i <= n; ++i) h_offsets[i] -= r0;
     return SAD_OK;

@@ -239,7 +239,7 @@ void launch_samples(const unsigned long long *key_sorted, const int64_t *shard_b
                     unsigned long long *samples_out, cudaStream_t st);
 void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, int64_t n,
                           int64_t first_idx, unsigned long long *key_sorted, const RowInfo *rowinfo, int k,
-                          int64_t *len_sorted, int qbits, cudaStream_t st);
+                          int64_t *len_sorted, int qbits, int ibits, cudaStream_t st);
 // f1: rank against the k*p gathered samples
 void launch_tkeys(const unsigned long long *T, const RowInfo *rowinfo, int64_t n, unsigned long long *keys,
                   int32_t *rows, cudaStream_t st);
@@ -247,9 +247,9 @@ void launch_sample_records(const int32_t *rows_sorted, const int64_t *shard_base
                            const int64_t *off, const int32_t *dcnt, const RowInfo *rowinfo, int64_t first_idx, int k,
                            size_t rec_bytes, uint8_t *rec_out, cudaStream_t st);
 int launch_rank_vs_samples(const RankArgs &a, int m, unsigned long long *Tp, int num_sms, cudaStream_t st);
-void launch_f1_keys(const unsigned long long *Tp, int64_t n, int m, int64_t first_idx, const RowInfo *rowinfo,
-                    unsigned long long *key, unsigned long long *ckey, int32_t *perm_in, uint32_t *S_ga,
-                    uint32_t *den_ga, cudaStream_t st);
+void launch_f1_keys(const unsigned long long *Tp, int64_t n, int tbits, int ibits, int64_t first_idx,
+                    const RowInfo *rowinfo, unsigned long long *key, unsigned long long *ckey, int32_t *perm_in,
+                    uint32_t *S_ga, uint32_t *den_ga, cudaStream_t st);
 void launch_f1_gainfo(const int64_t *anc_local, int pl, int shard0, int p, int64_t first_idx, long long *ga_info,
                       cudaStream_t st);
 
@@ -461,6 +461,8 @@ struct sad_ctx {
     int64_t kmax_blocks_seen = -1;                   // largest K blocks of the last absorbed step (-1: none)
     bool allow_cap = false;                          // capped layers + K6 excess possible in this layout
     int64_t x_entries_bound = 0;                     // K6 list entries bound (all CSR entries)
+    int ibits = 31;                                  // key = (rank << ibits) + source index
+    int tbits = 32;                                  // bits of the rank value in the a7 sort key
 
     // collective API
     void *comm = nullptr;                            // ncclComm_t (NULL: none)

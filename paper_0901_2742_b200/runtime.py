@@ -362,6 +362,15 @@ class Context:
         self._call("sad_get_bucket_sizes", _vp(out))
         return out
 
+    @property
+    def key_index_bits(self) -> int:
+        """Index bits of the rank keys: key = (rank value << bits) + source index (sad_key_index_bits)."""
+        return int(L.lib().sad_key_index_bits(self._h))
+
+    def key_index(self, keys) -> np.ndarray:
+        """Source indices of uint64 rank keys (pivots, bucket keys)."""
+        return (np.asarray(keys, dtype=np.uint64) & np.uint64((1 << self.key_index_bits) - 1)).astype(np.int64)
+
     def load_report(self) -> dict:
         """the largest bucket against the PSRS bound (sad_get_load_report)."""
         r = np.zeros(6, np.int64)

@@ -42,7 +42,8 @@ def pipeline(seqs, k: int, p: int, mode: str = "ga") -> dict:
     """mode "ga": rank against the global ancestor (readings A7, A8); "samples": the paper's
     listing PAPER.md:67-72 literally: local order by T (ties by index), the
     p-1 sequences at positions floor(j w/p) of every shard as rank samples, and the rank
-    Dbar_i = floor(sum_s floor(2^32 F(x_i, s)) / (p(p-1))) with index tie-break."""
+    T'_i = sum_s floor(2^32 F(x_i, s)) (the mean's common 1/(p(p-1)) dropped, reading A27) with
+    index tie-break."""
     n = len(seqs)
     sh = shards(n, p)
     T = [0] * n
@@ -59,8 +60,7 @@ def pipeline(seqs, k: int, p: int, mode: str = "ga") -> dict:
             loc = sorted(s, key=lambda i: (T[i], i))
             w = len(loc)
             rsamples += [loc[(j * w) // p - 1] for j in range(1, p)]
-        m = len(rsamples)
-        f = [Fraction(sum(fixed(F(seqs[i], seqs[t], k)) for t in rsamples) // m) for i in range(n)]
+        f = [Fraction(sum(fixed(F(seqs[i], seqs[t], k)) for t in rsamples)) for i in range(n)]
         ga = -1
     else:
         f = [F(seqs[i], seqs[ga], k) for i in range(n)]

@@ -275,10 +275,16 @@ def _compare_f1(ctx, sizes, r, a, o, p):
     assert np.array_equal(T, r.T)
     loc, ga = ctx.ancestors()
     assert ga == -1 and loc.tolist() == r.anc.tolist()
+    # reading A27: key = (T' << index bits) + index, T' the exact sum of q over the samples
+    ib = ctx.key_index_bits
+    assert ib == max(1, int(n - 1).bit_length())
     K = np.concatenate([ctx.ranks(s)[2] for s in range(p)])
-    assert [int(x) for x in K] == [(int(d) << 31) + i for i, d in enumerate(r.S)]
+    assert [int(x) for x in K] == [(int(t) << ib) + i for i, t in enumerate(r.S)]
+    S_lo = np.concatenate([ctx.ranks(s)[0] for s in range(p)]).astype(np.int64)
+    S_hi = np.concatenate([ctx.ranks(s)[1] for s in range(p)]).astype(np.int64)
+    assert ((S_hi << 32) + S_lo).tolist() == [int(t) for t in r.S]
     assert np.array_equal(np.concatenate([ctx.sorted(s) for s in range(p)]), r.sorted)
-    assert [int(x) & 0x7FFFFFFF for x in ctx.pivots()] == r.pivots.tolist()
+    assert ctx.key_index(ctx.pivots()).tolist() == r.pivots.tolist()
     assert sizes.tolist() == r.bsize.tolist()
     for b, ref in enumerate(r.buckets()):
         assert ctx.bucket(b)[0].tolist() == ref

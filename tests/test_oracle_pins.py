@@ -204,7 +204,8 @@ def test_pipeline_samples_mode_vs_bruteforce(alpha, k, p):
 def test_samples_mode_hand_case():
     """f1 by hand (PAPER.md:67-72): p = 2, four DNA sequences, k = 2. Shards {0,1}, {2,3};
     T within each shard, one rank sample per shard at position floor(1*2/2) = 1 of its local order
-    (the smaller T), Dbar = floor((q(x, s0) + q(x, s1)) / 2)."""
+    (the smaller T), rank T' = q(x, s0) + q(x, s1) (reading A27: the exact fixed-point sum; the
+    mean's common factor 1/2 is dropped like A5's 1/N)."""
     seqs = ["ACGT", "ACGA", "TTTT", "TTTA"]
     a, o = gen.from_strings(seqs)
     r = oracle.run(a, o, "dna", 2, 2, mode="samples")
@@ -213,14 +214,44 @@ def test_samples_mode_hand_case():
     assert r.rsamples.tolist() == [0, 2]
     q23 = (2 << 32) // 3
     assert [int(t) for t in r.T] == [(1 << 32) + q23] * 4
-    # Dbar_0 = floor((2^32 + q(S(0,2)=0)) / 2), S(ACGT, TTTT) = 0
-    assert int(r.S[0]) == (1 << 32) // 2
-    # Dbar_1: F(ACGA, ACGT) = 2/3, F(ACGA, TTTT) = 0
-    assert int(r.S[1]) == q23 // 2
-    # Dbar_2: F(TTTT, ACGT) = 0, self = 2^32
-    assert int(r.S[2]) == (1 << 32) // 2
-    # Dbar_3: F(TTTA, ACGT) = 0 (TT, TA vs AC, CG, GT), F(TTTA, TTTT) = 2/3
-    assert int(r.S[3]) == q23 // 2
+    # T'_0 = q(ACGT, ACGT) + q(ACGT, TTTT) = 2^32 + 0 (S(ACGT, TTTT) = 0)
+    assert int(r.S[0]) == 1 << 32
+    # T'_1: F(ACGA, ACGT) = 2/3, F(ACGA, TTTT) = 0
+    assert int(r.S[1]) == q23
+    # T'_2: F(TTTT, ACGT) = 0, self = 2^32
+    assert int(r.S[2]) == 1 << 32
+    # T'_3: F(TTTA, ACGT) = 0 (TT, TA vs AC, CG, GT), F(TTTA, TTTT) = 2/3
+    assert int(r.S[3]) == q23
+    # order (T', index): 1 < 3 < 0 < 2; the rank samples' own T' via the reference-set routine
+    assert oracle.rank_vs_set(a, o, 2, [0, 2]).tolist() == [int(x) for x in r.S]
+
+
+@pytest.mark.parametrize("alpha,k", [("protein", 3), ("dna", 2), ("dna", 6)])
+def test_sample_degeneracy(alpha, k):
+    """SPEC S:208 / acceptance #3: ranking against samples = the FULL set equals
+    the centralized rank exactly. The reference-set sum (or_rank_vs_set, the f1 rank path) over all
+    N sequences must equal T_i of the centralized run (p = 1, the O4 all-pairs loop, a different
+    code path), and the reported R = ln(0.1 + D) with D = T'/(N 2^32) and
+    D = T/(N 2^32) are the same doubles; pinned to the Counter + Fraction brute force too."""
+    rng = np.random.default_rng(900 + k)
+    for trial in range(4):
+        n = int(rng.integers(8, 50))
+        a, o = gen.random_set(rng, n, alpha, k, 60)
+        if trial == 3:                                  # repeats, so ties exist
+            seqs = gen.to_strings(a, o)
+            seqs = seqs[: n // 2] + seqs[: n - n // 2]
+            a, o = gen.from_strings(seqs)
+        seqs = gen.to_strings(a, o)
+        cen = oracle.run(a, o, alpha, k, 1)
+        deg = oracle.rank_vs_set(a, o, k, np.arange(n))
+        assert deg.tolist() == cen.T.tolist()
+        assert deg.tolist() == bf.pipeline(seqs, k, 1)["T"]
+        D = lambda t: float(t) / (n * 2.0 ** 32)
+        assert [oracle.rank_R(D(x)) for x in deg] == [oracle.rank_R(D(x)) for x in cen.T]
+        # and the f1 mode's own sums equal the reference-set routine on its rank samples
+        if n >= 9:
+            r = oracle.run(a, o, alpha, k, 3, mode="samples")
+            assert oracle.rank_vs_set(a, o, k, r.rsamples).tolist() == [int(x) for x in r.S]
 
 
 # ---------------------------------------------------------------- invariants (SPEC.md:297-300, north star)
