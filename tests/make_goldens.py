@@ -38,8 +38,12 @@ from synth import gen  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden", "full")
 
-LAYOUTS = [("cfg1", 1, 2), ("cfg2", 2, 8), ("cfg3", 3, 2), ("cfg3", 3, 4), ("cfg3", 3, 8),
-           ("cfg5", 5, 1), ("cfg5", 5, 2), ("cfg5", 5, 4), ("cfg5", 5, 8), ("cfg4", 4, 8)]
+LAYOUTS = [("cfg1", 1, 2, "ga"), ("cfg2", 2, 8, "ga"), ("cfg3", 3, 2, "ga"), ("cfg3", 3, 4, "ga"),
+           ("cfg3", 3, 8, "ga"), ("cfg5", 5, 1, "ga"), ("cfg5", 5, 2, "ga"), ("cfg5", 5, 4, "ga"),
+           ("cfg5", 5, 8, "ga"), ("cfg4", 4, 8, "ga"),
+           # the rank against the k*p gathered samples (reading A27)
+           ("cfg1", 1, 2, "samples"), ("cfg2", 2, 8, "samples"), ("cfg3", 3, 8, "samples"),
+           ("cfg5", 5, 8, "samples"), ("cfg4", 4, 8, "samples")]
 
 
 def sha(a, dtype) -> str:
@@ -58,12 +62,12 @@ def sample_positions(n: int, m: int = 32, seed: int = 7):
     return sorted(set(int(x) for x in rng.integers(0, n, size=min(m, n))))
 
 
-def make(name: str, cfg: int, p: int, threads: int) -> dict:
+def make(name: str, cfg: int, p: int, threads: int, mode: str = "ga") -> dict:
     spec = gen.SPECS[cfg]
     a, o = gen.generate(spec)
     n = len(o) - 1
     t0 = time.perf_counter()
-    r = oracle.run(a, o, spec.alphabet, spec.k, p, nthreads=threads)
+    r = oracle.run(a, o, spec.alphabet, spec.k, p, nthreads=threads, mode=mode)
     dt = time.perf_counter() - t0
     sb = gen.shard_bounds(n, p)
     shards = []
@@ -93,10 +97,12 @@ def make(name: str, cfg: int, p: int, threads: int) -> dict:
     w = n // p
     mb = int(max(r.bsize))
     return {
-        "name": f"{name}_p{p}", "config": cfg, "p": p, "n": n, "alphabet": spec.alphabet, "k": spec.k,
+        "name": f"{name}_p{p}" + ("" if mode == "ga" else f"_{mode}"), "mode": mode, "config": cfg, "p": p, "n": n,
+        "alphabet": spec.alphabet, "k": spec.k,
         "seed": spec.seed, "residues": int(o[-1]), "input_sha256": input_digest(a, o),
         "anc": [int(x) for x in r.anc], "ga": int(r.ga),
         "samples": [int(x) for x in r.samples], "pivots": [int(x) for x in r.pivots],
+        "rank_samples": None if r.rsamples is None else [int(x) for x in r.rsamples],
         "bsize": [int(x) for x in r.bsize],
         "load": {"max_bucket": mb, "w": w, "w_max": w_max, "bound_2w_plus_p": 2 * w_max + p,
                  "holds": mb <= 2 * w_max + p, "p_divides_w": (n % p == 0 and w % p == 0),
@@ -115,11 +121,11 @@ def main():
     args = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     want = set(x for x in args.only.split(",") if x)
-    for name, cfg, p in LAYOUTS:
-        tag = f"{name}_p{p}"
+    for name, cfg, p, mode in LAYOUTS:
+        tag = f"{name}_p{p}" + ("" if mode == "ga" else f"_{mode}")
         if want and tag not in want:
             continue
-        g = make(name, cfg, p, args.threads)
+        g = make(name, cfg, p, args.threads, mode)
         path = os.path.join(OUT, f"{tag}.json")
         with open(path, "w") as f:
             json.dump(g, f, indent=1)

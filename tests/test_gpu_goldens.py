@@ -61,15 +61,22 @@ def _check(ctxs, g, G, sizes):
     pl = p // G
     for r, c in enumerate(ctxs):
         loc, ga = c.ancestors()
-        assert loc.tolist() == g["anc"], "local ancestors differ"
+        if g.get("mode", "ga") == "samples":     # f1: each rank reports its own shards' ancestors
+            mine = list(range(r * pl, (r + 1) * pl))
+            assert [int(loc[s]) for s in mine] == [g["anc"][s] for s in mine], "local ancestors differ"
+        else:
+            assert loc.tolist() == g["anc"], "local ancestors differ"
         assert ga == g["ga"], "GA differs"
-        assert [int(x) & 0x7FFFFFFF for x in c.pivots()] == g["pivots"], "pivots differ"
+        assert c.key_index(c.pivots()).tolist() == g["pivots"], "pivots differ"
         for sl in range(pl):
             s = r * pl + sl
             sh = g["shards"][s]
             pos = sh["sample_pos"]
             _expect(f"T shard {s}", c.local_rank(sl), "<u8", sh["T"], pos, sh["T_sample"])
             S, D, _ = c.ranks(sl)
+            if g.get("mode", "ga") == "samples":     # f1 (reading A27): S = T' mod 2^32, den = T' >> 32
+                S = (D.astype(np.int64) << 32) + S.astype(np.int64)
+                D = np.ones(len(S), np.int64)
             _expect(f"S shard {s}", S.astype(np.int64), "<i8", sh["S"], pos, sh["S_sample"])
             _expect(f"den shard {s}", D.astype(np.int64), "<i8", sh["den"], pos, sh["den_sample"])
             _expect(f"sorted shard {s}", c.sorted(sl), "<i8", sh["sorted"], pos, sh["sorted_sample"])
@@ -96,7 +103,7 @@ def test_full_size_golden_one_gpu(path, kernel):
     g = _load(path)
     a, o = _inputs(g)
     n = len(o) - 1
-    ctx = Context(g["alphabet"], g["k"], g["p"], kernel=kernel)
+    ctx = Context(g["alphabet"], g["k"], g["p"], kernel=kernel, rank_mode=g.get("mode", "ga"))
     ctx.load(a, o, n, 0)
     sizes = ctx.run()
     _check([ctx], g, 1, sizes)
@@ -115,7 +122,7 @@ def test_full_size_golden_emulated_ranks(path, G):
     if g["p"] % G or g["p"] == 1:
         pytest.skip("p % G != 0")
     a, o = _inputs(g)
-    ctxs, sizes = run_emulated(a, o, g["alphabet"], g["k"], g["p"], G, "tc")
+    ctxs, sizes = run_emulated(a, o, g["alphabet"], g["k"], g["p"], G, "tc", rank_mode=g.get("mode", "ga"))
     _check(ctxs, g, G, sizes)
     for c in ctxs:
         c.close()
