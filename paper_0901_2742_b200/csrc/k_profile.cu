@@ -40,7 +40,7 @@ constexpr int kBinBits = SAD_PROF_BINBITS, kBinsPerWord = 32 / kBinBits;
 constexpr uint32_t kBinMax = (1u << kBinBits) - 1u;
 constexpr int kWidePasses = 16 / kBinBits;   // overflow fallback: u16 bins over 1/kWidePasses of the k-mers
 #ifndef SAD_PROF_UNROLL
-#define SAD_PROF_UNROLL 2
+#define SAD_PROF_UNROLL 4
 #endif
 constexpr int kCountUnroll = SAD_PROF_UNROLL;   // windows per lane per counting step
 constexpr int kCodeSeg = 2048;           // residue codes staged per warp
@@ -619,85 +619,93 @@ __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int 
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t *row = opsm + (size_t)wid * slice;
     uint32_t *row32 = reinterpret_cast<uint32_t *>(row);
-    const int64_t nw = (int64_t)gridDim.x * kOpWarps;
     const uint32_t stride = (uint32_t)a.stride;
     const uint32_t per_byte = a.fp4 ? 2u : 1u;               // operand columns per byte
-    // CSR position (entry offset, entry count) of padded row r; count 0 for padding rows
-    auto locate = [&](int64_t r, int &s, int64_t &eo, int &d) {
-        s = shard_of_padded_row(a.shard_rowpad, a.pl, r);
-        const int64_t local = r - a.shard_rowpad[s];
-        const bool real = local < a.shard_base[s + 1] - a.shard_base[s];
-        const int64_t i = a.shard_base[s] + (real && a.sigma ? a.sigma[a.shard_base[s] + local] : local);
-        eo = real ? a.off[i] - i * (int64_t)(a.k - 1) : 0;
-        d = real ? a.dcnt[i] : 0;
-    };
-    int64_t r = (int64_t)blockIdx.x * kOpWarps + wid;
-    int s = 0, d = 0;
-    int64_t eo = 0;
-    if (r < a.rows_pad) locate(r, s, eo, d);
-    uint32_t vpre[kOpBatch];                 // the row's first entry batch, loaded during the previous row
-    bool have_pre = false;
-    for (; r < a.rows_pad; r += nw) {
-        const uint32_t *ent = a.csr + eo;
-        const uint32_t *c0 = a.col0 + (size_t)s * a.V;
-        const uint32_t T = a.cap ? a.cap[s] : 0xFFFFFFFFu;
-        const bool ident = a.ident && a.ident[s];   // column of tau is tau itself (cap 1, every k-mer present)
-        const int dcur = d;
-        int sn = 0, dn = 0;                  // next row of this warp, fetched ahead
-        int64_t eon = 0;
-        if (r + nw < a.rows_pad) locate(r + nw, sn, eon, dn);
-        uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a.op) + r * a.stride);
-        // bytes of this row the contraction reads: the shard's K blocks (the stride is a capacity)
-        const uint32_t rowb = a.kblocks ? min(stride, (uint32_t)a.kblocks[s] * 128u) : stride;
-        for (uint32_t ch = 0; ch < rowb; ch += (uint32_t)slice) {
-            const uint32_t len = min((uint32_t)slice, rowb - ch);
-            for (uint32_t t = lane; t < len / 16; t += 32) reinterpret_cast<uint4 *>(row)[t] = make_uint4(0, 0, 0, 0);
-            __syncwarp();
-            const uint32_t c_lo = ch * per_byte, c_hi = (ch + len) * per_byte;
-            for (int e0 = 0; e0 < dcur; e0 += 32 * kOpBatch) {
-                uint32_t v[kOpBatch], cb[kOpBatch];
-                if (e0 == 0 && ch == 0 && have_pre) {
+    // Sequences in input order, 32 per warp-group: their CSR positions, shards and operand rows
+    // (sigma^-1: length-order slots) come from one coalesced load each, so no load chain precedes
+    // a row's entries; each row lands at its slot. Padding rows are never written: the all-pairs
+    // epilogue masks every product that involves one.
+    const int64_t ngroups = (a.n + 31) / 32;
+    for (int64_t g = (int64_t)blockIdx.x * kOpWarps + wid; g < ngroups; g += (int64_t)gridDim.x * kOpWarps) {
+        const int64_t il = g * 32 + lane;
+        int64_t eo_l = 0, slot_l = 0;
+        int d_l = 0, s_l = 0;
+        if (il < a.n) {
+            s_l = (int)a.rowinfo[il].shard;
+            eo_l = a.off[il] - il * (int64_t)(a.k - 1);
+            d_l = a.dcnt[il];
+            slot_l = a.shard_rowpad[s_l] + (a.sigma_inv ? a.sigma_inv[il] : il - a.shard_base[s_l]);
+        }
+        const int nrows = (int)min((int64_t)32, a.n - g * 32);
+        uint32_t vpre[kOpBatch];             // the row's first entry batch, loaded during the previous row
 #pragma unroll
-                    for (int b = 0; b < kOpBatch; ++b) v[b] = vpre[b];
-                } else {
+        for (int b = 0; b < kOpBatch; ++b) {
+            const int e = b * 32 + lane;
+            const int d0 = __shfl_sync(0xffffffffu, d_l, 0);
+            const int64_t eo0 = __shfl_sync(0xffffffffu, eo_l, 0);
+            vpre[b] = e < d0 ? a.csr[eo0 + e] : 0u;
+        }
+        for (int j = 0; j < nrows; ++j) {
+            const int s = __shfl_sync(0xffffffffu, s_l, j);
+            const int dcur = __shfl_sync(0xffffffffu, d_l, j);
+            const int64_t eo = __shfl_sync(0xffffffffu, eo_l, j);
+            const int64_t slot = __shfl_sync(0xffffffffu, slot_l, j);
+            const int dn = __shfl_sync(0xffffffffu, d_l, (j + 1) & 31);
+            const int64_t eon = __shfl_sync(0xffffffffu, eo_l, (j + 1) & 31);
+            const uint32_t *ent = a.csr + eo;
+            const uint32_t *c0 = a.col0 + (size_t)s * a.V;
+            const uint32_t T = a.cap ? a.cap[s] : 0xFFFFFFFFu;
+            const bool ident = a.ident && a.ident[s];   // column of tau is tau itself (cap 1, every k-mer present)
+            uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a.op) + slot * a.stride);
+            // bytes of this row the contraction reads: the shard's K blocks (the stride is a capacity)
+            const uint32_t rowb = a.kblocks ? min(stride, (uint32_t)a.kblocks[s] * 128u) : stride;
+            bool have_pre = true;
+            for (uint32_t ch = 0; ch < rowb; ch += (uint32_t)slice) {
+                const uint32_t len = min((uint32_t)slice, rowb - ch);
+                for (uint32_t t = lane; t < len / 16; t += 32) reinterpret_cast<uint4 *>(row)[t] = make_uint4(0, 0, 0, 0);
+                __syncwarp();
+                const uint32_t c_lo = ch * per_byte, c_hi = (ch + len) * per_byte;
+                for (int e0 = 0; e0 < dcur; e0 += 32 * kOpBatch) {
+                    uint32_t v[kOpBatch], cb[kOpBatch];
+                    if (e0 == 0 && have_pre) {
+#pragma unroll
+                        for (int b = 0; b < kOpBatch; ++b) v[b] = vpre[b];
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < kOpBatch; ++b) {
+                            const int e = e0 + b * 32 + lane;
+                            v[b] = e < dcur ? ent[e] : 0u;
+                        }
+                    }
+#pragma unroll
+                    for (int b = 0; b < kOpBatch; ++b)
+                        cb[b] = ident ? (v[b] >> 16) : ((v[b] & 0xFFFFu) ? c0[v[b] >> 16] : 0u);
 #pragma unroll
                     for (int b = 0; b < kOpBatch; ++b) {
-                        const int e = e0 + b * 32 + lane;
-                        v[b] = e < dcur ? ent[e] : 0u;
+                        const uint32_t n = v[b] & 0xFFFFu;     // 0 for lanes past the row's entries
+                        const uint32_t lo = max(cb[b], c_lo), hi = min(cb[b] + min(n, T), c_hi);
+                        for (uint32_t c = lo; c < hi; ++c) {
+                            const uint32_t cc = c - c_lo;
+                            if (a.fp4)        // e2m1 1.0 = 0b0010; neighbouring k-mers may share a word
+                                atomicOr(&row32[cc >> 3], 2u << (4 * (cc & 7)));
+                            else
+                                row[cc] = 1;
+                        }
                     }
                 }
+                if (ch + (uint32_t)slice >= rowb && j + 1 < nrows) {   // the next row's first batch
 #pragma unroll
-                for (int b = 0; b < kOpBatch; ++b)
-                    cb[b] = ident ? (v[b] >> 16) : ((v[b] & 0xFFFFu) ? c0[v[b] >> 16] : 0u);
-#pragma unroll
-                for (int b = 0; b < kOpBatch; ++b) {
-                    const uint32_t n = v[b] & 0xFFFFu;     // 0 for lanes past the row's entries
-                    const uint32_t lo = max(cb[b], c_lo), hi = min(cb[b] + min(n, T), c_hi);
-                    for (uint32_t c = lo; c < hi; ++c) {
-                        const uint32_t cc = c - c_lo;
-                        if (a.fp4)        // e2m1 1.0 = 0b0010; neighbouring k-mers may share a word
-                            atomicOr(&row32[cc >> 3], 2u << (4 * (cc & 7)));
-                        else
-                            row[cc] = 1;
+                    for (int b = 0; b < kOpBatch; ++b) {
+                        const int e = b * 32 + lane;
+                        vpre[b] = e < dn ? a.csr[eon + e] : 0u;
                     }
                 }
+                have_pre = false;
+                __syncwarp();
+                for (uint32_t t = lane; t < len / 16; t += 32) dst[ch / 16 + t] = reinterpret_cast<const uint4 *>(row)[t];
+                __syncwarp();
             }
-            have_pre = false;
-            if (ch + (uint32_t)slice >= rowb && r + nw < a.rows_pad) {     // the next row's first batch
-#pragma unroll
-                for (int b = 0; b < kOpBatch; ++b) {
-                    const int e = b * 32 + lane;
-                    vpre[b] = e < dn ? a.csr[eon + e] : 0u;
-                }
-                have_pre = true;
-            }
-            __syncwarp();
-            for (uint32_t t = lane; t < len / 16; t += 32) dst[ch / 16 + t] = reinterpret_cast<const uint4 *>(row)[t];
-            __syncwarp();
         }
-        s = sn;
-        eo = eon;
-        d = dn;
     }
 }
 
@@ -714,7 +722,7 @@ void launch_indicator(const OperandArgs &a, cudaStream_t st) {
 #define SAD_K4_DIV 1
 #endif
     int64_t grid = (int64_t)sms * std::max(per_sm / SAD_K4_DIV, 1);
-    const int64_t need = (a.rows_pad + kOpWarps - 1) / kOpWarps;
+    const int64_t need = ((a.n + 31) / 32 + kOpWarps - 1) / kOpWarps;
     if (grid > need) grid = need;
     if (grid > 0) k_indicator<<<(unsigned)grid, kOpWarps * 32, smem, st>>>(a, slice);
 }

@@ -879,6 +879,9 @@ static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, 
         // K3 under the layer caps k_select chose (the length order sigma was computed by
         // sad_build_profiles); K6 list offsets and lists; K4 beside K6 rows (side stream)
         o.sigma = ctx->d_sigma;
+        o.sigma_inv = ctx->d_sigma_inv;
+        o.rowinfo = ctx->d_rowinfo;
+        o.n = ctx->n;
         o.kblocks = ctx->d_kblocks;
         launch_capscan(ctx->d_M, ctx->V, nullptr, ctx->d_cap, ctx->d_col0, nullptr, 0, pl, ctx->V, ctx->st);
         LAUNCHED();

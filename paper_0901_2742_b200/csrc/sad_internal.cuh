@@ -131,6 +131,9 @@ struct OperandArgs {
     const uint32_t *ident;           // device [pl] 1: the column of tau is tau (cap 1, all V k-mers present), or NULL
     const int64_t *kblocks;          // device [pl] 128-byte K blocks of each shard's rows (only those are
                                      // written; the row stride is the capacity), or NULL: the whole stride
+    const RowInfo *rowinfo;          // [n] input order (.shard = local shard)  (K4)
+    const int32_t *sigma_inv;        // [n] local index -> length-order slot in its shard, or NULL (K4)
+    int64_t n;                       // local sequences (K4)
 };
 void launch_indicator(const OperandArgs &a, cudaStream_t st);
 // length order by counting (K3): Tw histogram per shard, per-shard scan up to the max Tw in kinfo[3],
