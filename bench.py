@@ -44,6 +44,8 @@ def parse():
                     help="ga: rank vs the global ancestor (north star); samples: SURVEY f1, vs the k*p samples")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--oracle-threads", type=int, default=0,
+                    help="reference arm / cpu_baseline: oracle threads (0 = all host cores)")
     ap.add_argument("--no-graph", action="store_true",
                     help="time eager steps instead of one CUDA graph replay per step (world == 1)")
     return ap.parse_args()
@@ -64,17 +66,17 @@ def total_pairs(n, p):
 # CPU oracle timing (cpu_baseline leg and --impl reference)
 # ----------------------------------------------------------------------------------------
 
-def oracle_sample(a, o, spec, p, seconds):
+def oracle_sample(a, o, spec, p, seconds, threads=0):
     """Size a prefix of the workload (same p) so that one oracle run takes about `seconds` on
     all host threads: grow the prefix until a probe run takes >= seconds/4, then scale by the
     pairs' n^2 growth."""
     import oracle
-    cores = oracle.threads(0)
+    cores = oracle.threads(threads)
     N = len(o) - 1
     n_sub = min(N, max(p * p, 800))
     while True:
         t0 = time.perf_counter()
-        oracle.run(a[: o[n_sub]], o[: n_sub + 1], spec.alphabet, spec.k, p)
+        oracle.run(a[: o[n_sub]], o[: n_sub + 1], spec.alphabet, spec.k, p, nthreads=threads)
         dt = time.perf_counter() - t0
         if dt >= seconds / 4 or n_sub >= N:
             break
@@ -83,10 +85,10 @@ def oracle_sample(a, o, spec, p, seconds):
     return n_sub, cores
 
 
-def run_oracle(a, o, spec, p, n_sub):
+def run_oracle(a, o, spec, p, n_sub, threads=0):
     import oracle
     t0 = time.perf_counter()
-    oracle.run(a[: o[n_sub]], o[: n_sub + 1], spec.alphabet, spec.k, p)
+    oracle.run(a[: o[n_sub]], o[: n_sub + 1], spec.alphabet, spec.k, p, nthreads=threads)
     return time.perf_counter() - t0
 
 
@@ -419,10 +421,11 @@ def reference_arm(args, spec, p, world, rank):
     from synth import gen
     a, o = gen.generate(spec)
     per_step = max(2.0, min(8.0, 120.0 / max(args.steps + args.warmup, 1)))
-    n_sub, cores = oracle_sample(a, o, spec, p, per_step)
+    th = args.oracle_threads
+    n_sub, cores = oracle_sample(a, o, spec, p, per_step, th)
     for _ in range(args.warmup):
-        run_oracle(a, o, spec, p, n_sub)
-    t = sum(run_oracle(a, o, spec, p, n_sub) for _ in range(args.steps))
+        run_oracle(a, o, spec, p, n_sub, th)
+    t = sum(run_oracle(a, o, spec, p, n_sub, th) for _ in range(args.steps))
     value = total_pairs(n_sub, p) / (t / args.steps)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,

@@ -82,15 +82,34 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
     const int V = a.V;
     const uint32_t Vh = (uint32_t)(V + kWidePasses - 1) / kWidePasses;   // u16 fallback: k-mers per sub-pass
     const int64_t W = (int64_t)gridDim.x * warps, gw = (int64_t)blockIdx.x * warps + wid;
-    const int64_t nr = a.i_end - a.i_begin;
-    const int64_t i0 = a.i_begin + gw * nr / W, i1 = a.i_begin + (gw + 1) * nr / W;
+    // contiguous ranges of sequences balanced by residues (the offsets are the residue prefix), so
+    // that a warp with a few long sequences does not trail: the first sequence starting at or after
+    // residue r0 + (r1 - r0) gw / W, found by a 32-way warp search over the offsets
+    const int64_t r0 = a.off[a.i_begin], rr = a.off[a.i_end] - r0;
+    auto first_at = [&](int64_t wq) -> int64_t {
+        if (wq <= 0) return a.i_begin;
+        if (wq >= W) return a.i_end;
+        const int64_t target = r0 + (int64_t)(((__int128)rr * wq) / W);
+        int64_t lo = a.i_begin, hi = a.i_end;              // answer in (lo, hi]: off[lo] < target <= off[hi]
+        if (a.off[lo] >= target) return lo;
+        while (hi - lo > 1) {
+            const int64_t step = (hi - lo + 31) / 32;
+            const int64_t probe = min(hi, lo + (int64_t)(lane + 1) * step);
+            const uint32_t ge = __ballot_sync(0xffffffffu, a.off[probe] >= target);
+            const int f = __ffs(ge) - 1;                   // first probe at or past the target (>= 0: off[hi] >= target)
+            hi = min(hi, lo + (int64_t)(f + 1) * step);
+            lo = f > 0 ? lo + (int64_t)f * step : lo;
+        }
+        return hi;
+    };
+    const int64_t i0 = first_at(gw), i1 = first_at(gw + 1);
     int s = 0;
     while (s + 1 < a.pl && i0 >= a.shard_base[s + 1]) ++s;
     unsigned long long acc_w = 0, acc_d = 0, max_tw = 0;
     uint32_t exm[kNumCaps] = {};
     auto flush = [&]() {
         // M(tau) >= 1 for every k-mer present: the warp's presence bits, OR-ed once per word
-        // (counts >= 2 update M itself); k_kstats folds the bits into M
+        // (counts >= 2 update M itself); k_shard_plan folds the bits into M
         __syncwarp();
         for (int t = lane; t < VW; t += 32) {
             const uint32_t b = pres[t];
@@ -455,64 +474,48 @@ void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, const un
 }
 
 
-// K3: per shard, col0(tau) = exclusive scan over tau of min(M(tau), T_s) and
-// K_s = sum_tau min(M(tau), T_s). Column block [col0(tau), col0(tau) + min(M(tau), T_s)) holds
-// the threshold layers t = 1..min(M(tau), T_s) of k-mer tau (SURVEY Appendix A.1:
-// min(a,b) = min(min(a,T), min(b,T)) + min((a-T)+, (b-T)+), the first term being
-// sum_{t<=T} [a>=t][b>=t]); the second term is the sparse excess of K6 (k_excess.cu).
-// The same kernel (cap = NULL, sel = the chosen cap index per shard) scans the K6 list lengths
-// X_T(tau) = #{i : n_i(tau) > T_s} into per-shard list offsets.
+// K3, one block per shard, everything between the k-mer counts and the operand in one launch
+// (no host round trip):
+//  (1) statistics for every candidate cap T = 2^j (and no cap), after folding the presence bits
+//      into M (a k-mer present at most once per sequence has M = 1):
+//        K_s(T) = sum_tau min(M(tau), T)                        -> kinfo[s][2] (no cap), [8 + j]
+//        sum_tau C(X_T(tau), 2), X_T(tau) = #{i : n_i(tau) > T}  -> kinfo[s][12 + j] (bound of K6 pairs)
+//        sum_tau X_T(tau)                                       -> kinfo[s][16 + j] (K6 list entries)
+//  (2) the decision: the smallest layer cap T_s = 2^j whose per-row excess
+//      max_i sum_tau (n_i(tau) - T)+ (kinfo[s][4 + j], from K1/K2) fits the K6 byte (<= 255), when
+//      capping is allowed, else none; the operand width K_s = K_s(T_s) and its K blocks (kcpb
+//      columns each, clipped to the operand's capacity kcap_blocks: status[0] |= 1 flags an
+//      overflow, status[1] = max_s K_s); kinfo[s][20] = K_s, [21] = T_s;
+//  (3) the column map col0(tau) = exclusive scan over tau of min(M(tau), T_s): column block
+//      [col0(tau), col0(tau) + min(M(tau), T_s)) holds the threshold layers t = 1..min(M, T_s) of
+//      tau (min(a,b) = min(min(a,T),min(b,T)) + min((a-T)+,(b-T)+)); the second term
+//      is the sparse excess of K6 (k_excess.cu), whose list offsets are (4) the exclusive scan of
+//      X_{T_s}(tau) (shards without entries above their cap get empty lists).
 constexpr int kScanThreads = 1024;
-__global__ void __launch_bounds__(kScanThreads) k_capscan(const uint32_t *in, int64_t in_stride, const uint32_t *sel,
-                                                          const uint32_t *cap, uint32_t *out,
-                                                          unsigned long long *total_out, int total_stride, int V) {
+__global__ void __launch_bounds__(kScanThreads) k_shard_plan(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc,
+                                                             unsigned long long *kinfo, int V, int allow_cap,
+                                                             int64_t kcap_blocks, int kcpb, uint32_t *cap,
+                                                             uint32_t *xsel, uint32_t *ident, int64_t *kblocks,
+                                                             unsigned long long *status, uint32_t *col0,
+                                                             uint32_t *xoff, unsigned long long *xtot) {
     typedef cub::BlockScan<unsigned long long, kScanThreads> Scan;
-    __shared__ typename Scan::TempStorage tmp;
-    const int s = blockIdx.x;
-    const uint32_t T = cap ? cap[s] : 0xFFFFFFFFu;
-    if (sel && sel[s] >= (uint32_t)kNumCaps) {       // shard without excess lists
-        for (int t = threadIdx.x; t < V; t += kScanThreads) out[(size_t)s * V + t] = 0;
-        if (threadIdx.x == 0 && total_out) total_out[(size_t)s * total_stride] = 0;
-        return;
-    }
-    const uint32_t *m = in + (size_t)s * in_stride + (sel ? (size_t)sel[s] * V : 0);
-    uint32_t *c = out + (size_t)s * V;
-    const int per = (V + kScanThreads - 1) / kScanThreads;
-    const int t0 = min(V, (int)threadIdx.x * per), t1 = min(V, t0 + per);
-    unsigned long long sum = 0;
-    for (int t = t0; t < t1; ++t) sum += min(m[t], T);
-    unsigned long long base, total;
-    Scan(tmp).ExclusiveSum(sum, base, total);
-    for (int t = t0; t < t1; ++t) {
-        c[t] = (uint32_t)base;
-        base += min(m[t], T);
-    }
-    if (threadIdx.x == 0 && total_out) total_out[(size_t)s * total_stride] = total;
-}
-
-void launch_capscan(const uint32_t *in, int64_t in_stride, const uint32_t *sel, const uint32_t *cap, uint32_t *out,
-                    unsigned long long *total_out, int total_stride, int pl, int V, cudaStream_t st) {
-    k_capscan<<<pl, kScanThreads, 0, st>>>(in, in_stride, sel, cap, out, total_out, total_stride, V);
-}
-
-// K3 statistics per shard, for every candidate cap T = 2^j (and no cap):
-//   K_s(T) = sum_tau min(M(tau), T)                        -> kinfo[s][2] (no cap), [8 + j]
-//   sum_tau C(X_T(tau), 2), X_T(tau) = #{i : n_i(tau) > T}  -> kinfo[s][12 + j] (bound of K6 pairs)
-//   sum_tau X_T(tau)                                       -> kinfo[s][16 + j] (K6 list entries)
-__global__ void __launch_bounds__(kScanThreads) k_kstats(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc,
-                                                         unsigned long long *kinfo, int V) {
     constexpr int NV = 3 * kNumCaps + 1;
+    __shared__ typename Scan::TempStorage tmp;
     __shared__ unsigned long long red[NV];
-    const int s = blockIdx.y;                 // blocks of k-mers x shards (kinfo zeroed by the caller)
-    if (threadIdx.x < NV) red[threadIdx.x] = 0;
-    __syncthreads();
+    __shared__ uint32_t s_T, s_sel;
+    const int s = blockIdx.x;
     uint32_t *m = M + (size_t)s * V;
     const uint32_t *xc = Xc + (size_t)s * kNumCaps * V;
-    unsigned long long acc[NV] = {};
     const uint32_t *mb = Mb + (size_t)s * ((V + 31) / 32);
-    for (int t = blockIdx.x * kScanThreads + threadIdx.x; t < V; t += gridDim.x * kScanThreads) {
+    unsigned long long *ki = kinfo + (size_t)s * kKinfo;
+    const int per = (V + kScanThreads - 1) / kScanThreads;
+    const int t0 = min(V, (int)threadIdx.x * per), t1 = min(V, t0 + per);
+    if (threadIdx.x < NV) red[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long acc[NV] = {};
+    for (int t = t0; t < t1; ++t) {                       // (1)
         uint32_t x = m[t];
-        if (x == 0 && ((mb[t >> 5] >> (t & 31)) & 1u)) {   // present once at most per sequence: M = 1
+        if (x == 0 && ((mb[t >> 5] >> (t & 31)) & 1u)) {
             x = 1;
             m[t] = 1;
         }
@@ -532,32 +535,13 @@ __global__ void __launch_bounds__(kScanThreads) k_kstats(uint32_t *M, const uint
         if ((threadIdx.x & 31) == 0 && v) atomicAdd(&red[j], v);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long *ki = kinfo + (size_t)s * kKinfo;
-        atomicAdd(&ki[2], red[kNumCaps]);
+    if (threadIdx.x == 0) {                               // (2)
+        ki[2] = red[kNumCaps];
         for (int j = 0; j < kNumCaps; ++j) {
-            atomicAdd(&ki[8 + j], red[j]);
-            atomicAdd(&ki[12 + j], red[kNumCaps + 1 + j]);
-            atomicAdd(&ki[16 + j], red[2 * kNumCaps + 1 + j]);
+            ki[8 + j] = red[j];
+            ki[12 + j] = red[kNumCaps + 1 + j];
+            ki[16 + j] = red[2 * kNumCaps + 1 + j];
         }
-    }
-}
-
-void launch_kstats(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,
-                   cudaStream_t st) {
-    const int bx = std::max(1, std::min(16, V / 512));
-    k_kstats<<<dim3(bx, pl), kScanThreads, 0, st>>>(M, Mb, Xc, kinfo, V);
-}
-
-// K3 decision (split identity): per shard the smallest layer cap T = 2^j whose
-// per-row excess max_i sum_tau (n_i(tau) - T)+ fits the K6 byte (<= 255), the operand width under
-// that cap and the shard's K blocks; taken on the device so that no host round trip sits between
-// the k-mer counts and the all-pairs stage. Mirrors, bit for bit, the rule the host applied before.
-__global__ void k_select(unsigned long long *kinfo, int pl, int V, int allow_cap, int64_t kcap_blocks, int kcpb,
-                         uint32_t *cap, uint32_t *xsel, uint32_t *ident, int64_t *kblocks,
-                         unsigned long long *status) {
-    for (int s = threadIdx.x; s < pl; s += blockDim.x) {
-        unsigned long long *ki = kinfo + (size_t)s * kKinfo;
         unsigned long long K = ki[2];
         uint32_t T = kNoCap, sel = (uint32_t)kNumCaps;
         if (allow_cap)
@@ -581,13 +565,45 @@ __global__ void k_select(unsigned long long *kinfo, int pl, int V, int allow_cap
         ki[20] = K;
         ki[21] = T;
         atomicMax(&status[1], K);
+        s_T = T;
+        s_sel = sel;
     }
+    __syncthreads();
+    const uint32_t T = s_T, sel = s_sel;
+    {                                                     // (3)
+        unsigned long long sum = 0, base, total;
+        for (int t = t0; t < t1; ++t) sum += min(m[t], T);
+        Scan(tmp).ExclusiveSum(sum, base, total);
+        uint32_t *c = col0 + (size_t)s * V;
+        for (int t = t0; t < t1; ++t) {
+            c[t] = (uint32_t)base;
+            base += min(m[t], T);
+        }
+    }
+    __syncthreads();
+    uint32_t *xo = xoff + (size_t)s * V;                  // (4)
+    if (sel >= (uint32_t)kNumCaps) {
+        for (int t = threadIdx.x; t < V; t += kScanThreads) xo[t] = 0;
+        if (threadIdx.x == 0) xtot[s] = 0;
+        return;
+    }
+    const uint32_t *x = xc + (size_t)sel * V;
+    unsigned long long sum = 0, base, total;
+    for (int t = t0; t < t1; ++t) sum += x[t];
+    Scan(tmp).ExclusiveSum(sum, base, total);
+    for (int t = t0; t < t1; ++t) {
+        xo[t] = (uint32_t)base;
+        base += x[t];
+    }
+    if (threadIdx.x == 0) xtot[s] = total;
 }
 
-void launch_select(unsigned long long *kinfo, int pl, int V, int allow_cap, int64_t kcap_blocks, int kcpb,
-                   uint32_t *cap, uint32_t *xsel, uint32_t *ident, int64_t *kblocks, unsigned long long *status,
-                   cudaStream_t st) {
-    k_select<<<1, 256, 0, st>>>(kinfo, pl, V, allow_cap, kcap_blocks, kcpb, cap, xsel, ident, kblocks, status);
+void launch_shard_plan(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,
+                       int allow_cap, int64_t kcap_blocks, int kcpb, uint32_t *cap, uint32_t *xsel, uint32_t *ident,
+                       int64_t *kblocks, unsigned long long *status, uint32_t *col0, uint32_t *xoff,
+                       unsigned long long *xtot, cudaStream_t st) {
+    k_shard_plan<<<pl, kScanThreads, 0, st>>>(M, Mb, Xc, kinfo, V, allow_cap, kcap_blocks, kcpb, cap, xsel, ident,
+                                              kblocks, status, col0, xoff, xtot);
 }
 
 __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl, int64_t r) {
@@ -614,29 +630,29 @@ constexpr int kOpThreads = 256;
 constexpr int kOpWarps = SAD_OP_WARPS;
 constexpr int kRowSlice = 16384;
 constexpr int kOpBatch = SAD_OP_BATCH;
-__global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int slice) {
+__global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int slice, int rpg) {
     extern __shared__ __align__(16) uint8_t opsm[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t *row = opsm + (size_t)wid * slice;
     uint32_t *row32 = reinterpret_cast<uint32_t *>(row);
     const uint32_t stride = (uint32_t)a.stride;
     const uint32_t per_byte = a.fp4 ? 2u : 1u;               // operand columns per byte
-    // Sequences in input order, 32 per warp-group: their CSR positions, shards and operand rows
-    // (sigma^-1: length-order slots) come from one coalesced load each, so no load chain precedes
-    // a row's entries; each row lands at its slot. Padding rows are never written: the all-pairs
-    // epilogue masks every product that involves one.
-    const int64_t ngroups = (a.n + 31) / 32;
+    // Sequences in input order, rpg (<= 32, sized so that every resident warp has a group) per
+    // warp-group: their CSR positions, shards and operand rows (sigma^-1: length-order slots) come
+    // from one coalesced load each, so no load chain precedes a row's entries; each row lands at its
+    // slot. Padding rows are never written: the all-pairs epilogue masks every product with one.
+    const int64_t ngroups = (a.n + rpg - 1) / rpg;
     for (int64_t g = (int64_t)blockIdx.x * kOpWarps + wid; g < ngroups; g += (int64_t)gridDim.x * kOpWarps) {
-        const int64_t il = g * 32 + lane;
+        const int64_t il = g * rpg + lane;
         int64_t eo_l = 0, slot_l = 0;
         int d_l = 0, s_l = 0;
-        if (il < a.n) {
+        if (lane < rpg && il < a.n) {
             s_l = (int)a.rowinfo[il].shard;
             eo_l = a.off[il] - il * (int64_t)(a.k - 1);
             d_l = a.dcnt[il];
             slot_l = a.shard_rowpad[s_l] + (a.sigma_inv ? a.sigma_inv[il] : il - a.shard_base[s_l]);
         }
-        const int nrows = (int)min((int64_t)32, a.n - g * 32);
+        const int nrows = (int)min((int64_t)rpg, a.n - g * rpg);
         uint32_t vpre[kOpBatch];             // the row's first entry batch, loaded during the previous row
 #pragma unroll
         for (int b = 0; b < kOpBatch; ++b) {
@@ -722,9 +738,12 @@ void launch_indicator(const OperandArgs &a, cudaStream_t st) {
 #define SAD_K4_DIV 1
 #endif
     int64_t grid = (int64_t)sms * std::max(per_sm / SAD_K4_DIV, 1);
-    const int64_t need = ((a.n + 31) / 32 + kOpWarps - 1) / kOpWarps;
+    // rows per warp-group: enough groups for every resident warp, at most 32 (one per lane)
+    const int64_t warps = grid * kOpWarps;
+    const int rpg = (int)std::max<int64_t>(1, std::min<int64_t>(32, (a.n + warps - 1) / warps));
+    const int64_t need = ((a.n + rpg - 1) / rpg + kOpWarps - 1) / kOpWarps;
     if (grid > need) grid = need;
-    if (grid > 0) k_indicator<<<(unsigned)grid, kOpWarps * 32, smem, st>>>(a, slice);
+    if (grid > 0) k_indicator<<<(unsigned)grid, kOpWarps * 32, smem, st>>>(a, slice, rpg);
 }
 
 // K4': dense uint16 count rows n_i(tau), tau = 0..V_pad-1, for the CUDA-core min-sum.

@@ -295,6 +295,12 @@ static cudaError_t sort_pairs(sad_ctx *ctx, const K *ki, K *ko, const int32_t *v
     return cub::DeviceRadixSort::SortPairs(ctx->d_cub, tb, ki, ko, vi, vo, n, 0, end_bit, ctx->st);
 }
 
+// the K6 list totals, behind the per-(shard, tau) list offsets
+static unsigned long long *xtot_of(const sad_ctx *ctx) {
+    unsigned long long *x = reinterpret_cast<unsigned long long *>(ctx->d_xoff + (size_t)ctx->pl * ctx->V + 1);
+    return reinterpret_cast<unsigned long long *>(rup(reinterpret_cast<int64_t>(x), 8));
+}
+
 // operand K capacity of a fresh layout: with capped layers K_s = sum_tau min(M(tau), T_s) <= 8 A^k
 // (T_s <= 8); uncapped shards that need more are flagged and replanned
 static int64_t initial_kcap_blocks(const sad_ctx *ctx) {
@@ -785,17 +791,17 @@ int sad_build_profiles(sad_ctx *ctx) {
         if (int rc = profile_launch(ctx, 0, ctx->n)) return rc;
     }
     ctx->profiled = false;
-    launch_kstats(ctx->d_M, ctx->d_Mb, ctx->d_Xc, ctx->d_kinfo, pl, V, ctx->st);
+    // K3 (statistics, the cap / K decision, column map, K6 list offsets) in one launch, all on the
+    // device, then the length order (rows by L - k + 1)
+    launch_shard_plan(ctx->d_M, ctx->d_Mb, ctx->d_Xc, ctx->d_kinfo, pl, V, ctx->allow_cap ? 1 : 0, ctx->kcap_blocks,
+                      (int)ctx->kcols_per_block, ctx->d_cap, ctx->d_xsel, ctx->d_ident, ctx->d_kblocks, ctx->d_status,
+                      ctx->d_col0, ctx->d_xoff, xtot_of(ctx), ctx->st);
     LAUNCHED();
     if (ctx->use_tc) {
-        // the length order (rows by L - k + 1) and the cap / K decision, all on the device
         launch_lenorder(ctx->d_rowinfo, ctx->d_shard_base, ctx->d_kinfo, pl, ctx->n, ctx->d_lcnt,
                         ctx->d_lcnt + (size_t)pl * kLenBinsMax, ctx->d_sigma, ctx->d_sigma_inv, ctx->d_rinfo_s,
                         ctx->st);
         ctx->launches_step += 3;
-        launch_select(ctx->d_kinfo, pl, V, ctx->allow_cap ? 1 : 0, ctx->kcap_blocks, (int)ctx->kcols_per_block,
-                      ctx->d_cap, ctx->d_xsel, ctx->d_ident, ctx->d_kblocks, ctx->d_status, ctx->st);
-        LAUNCHED();
     }
     // the statistics go to pinned host memory; read at the step's first synchronizing call
     CK(cudaMemcpyAsync(ctx->h_stats, ctx->d_err, sizeof(unsigned long long) * (8 + (size_t)pl * kKinfo),
@@ -872,25 +878,19 @@ static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, 
     operand_parts(ctx, op_b, xl_b, xe_b);
     uint32_t *lists = xl_b ? reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_operand) + op_b) : nullptr;
     uint8_t *E = xl_b ? reinterpret_cast<uint8_t *>(d_operand) + op_b + xl_b : nullptr;
-    unsigned long long *xtot = reinterpret_cast<unsigned long long *>(ctx->d_xoff + (size_t)pl * ctx->V + 1);
-    xtot = reinterpret_cast<unsigned long long *>(rup(reinterpret_cast<int64_t>(xtot), 8));
+    unsigned long long *xtot = xtot_of(ctx);
     record_pair(ctx, ctx->ev_pairs_op, true, 0);
     if (ctx->use_tc) {
-        // K3 under the layer caps k_select chose (the length order sigma was computed by
-        // sad_build_profiles); K6 list offsets and lists; K4 beside K6 rows (side stream)
+        // K3 ran in sad_build_profiles (layer caps, column maps, K6 list offsets); the K6 lists,
+        // then K6 rows on the side stream beside K4
         o.sigma = ctx->d_sigma;
         o.sigma_inv = ctx->d_sigma_inv;
         o.rowinfo = ctx->d_rowinfo;
         o.n = ctx->n;
         o.kblocks = ctx->d_kblocks;
-        launch_capscan(ctx->d_M, ctx->V, nullptr, ctx->d_cap, ctx->d_col0, nullptr, 0, pl, ctx->V, ctx->st);
-        LAUNCHED();
         o.cap = ctx->d_cap;
         o.ident = ctx->d_ident;
         if (lists) {
-            launch_capscan(ctx->d_Xc, (int64_t)kNumCaps * ctx->V, ctx->d_xsel, nullptr, ctx->d_xoff, xtot, 1, pl,
-                           ctx->V, ctx->st);
-            LAUNCHED();
             CK(cudaMemsetAsync(ctx->d_xcur, 0, sizeof(uint32_t) * (size_t)pl * ctx->V, ctx->st));
             CK(cudaMemsetAsync(E + ctx->h_ebase[pl], 0, 256, ctx->st));   // the zero row segment
             ExcessArgs x{};
@@ -1059,9 +1059,11 @@ static int rank_global_impl(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_sam
         launch_f1_gainfo(ctx->d_anc_local, ctx->pl, ctx->shard0, p, ctx->first_idx, ctx->d_ga_info, ctx->st);
         LAUNCHED();
     }
-    constexpr int kRankSortRuns = 4;       // blocks per shard of the local rank sort (then one merge)
-    if (!(qbits == 32 && ctx->max_w <= kSmallSortMax * kRankSortRuns &&
-          seg_sort_pairs_runs(ctx->d_ckey, ctx->d_perm_in, ctx->d_shard_base, ctx->pl, kRankSortRuns, ctx->n,
+    // blocks per shard of the local rank sort (then one merge by ranking): 4 with 8+ shards on the
+    // rank, more with fewer shards so that a one-shard rank still sorts with 32 blocks
+    const int runs = std::max(4, 32 / ctx->pl);
+    if (!(qbits == 32 && ctx->max_w <= (int64_t)kSmallSortMax * runs &&
+          seg_sort_pairs_runs(ctx->d_ckey, ctx->d_perm_in, ctx->d_shard_base, ctx->pl, runs, ctx->n,
                               ctx->d_ckey_sorted, ctx->d_perm_sorted, 32, ctx->st) == 0))
         CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
                       qbits + sbits));

@@ -33,7 +33,7 @@ constexpr int kKinfo = 24;          // u64 per shard in kinfo: [0] windows, [1] 
                                     // [4 + j] max_i sum_tau (n_i - 2^j)+, [8 + j] K under cap 2^j,
                                     // [12 + j] sum_tau C(X_j(tau), 2), [16 + j] sum_tau X_j(tau) with
                                     // X_j(tau) = #{i : n_i(tau) > 2^j}   (j < kNumCaps);
-                                    // [20] operand columns K_s and [21] layer cap T_s chosen by k_select
+                                    // [20] operand columns K_s and [21] layer cap T_s chosen by k_shard_plan
 constexpr int kLenBinsMax = 65536; // Tw <= 65535 (checked by K1/K2)
 constexpr int kNumCaps = 4;         // candidate layer caps T = 1, 2, 4, 8
 constexpr int kXrSmem = 200 * 1024; // K6 row accumulators (u8 per shard column) per block
@@ -97,18 +97,13 @@ struct ProfileArgs {
     int32_t *nhi;                    // [n] entries with count >= 2 (they lead each CSR row)
 };
 void launch_profile(const ProfileArgs &a, cudaStream_t st);
-void launch_capscan(const uint32_t *in, int64_t in_stride, const uint32_t *sel, const uint32_t *cap, uint32_t *out,
-                    unsigned long long *total_out, int total_stride, int pl, int V, cudaStream_t st);
-void launch_kstats(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,
-                   cudaStream_t st);
-// K3 decision on the device (no host round trip): per shard the layer cap T_s = the smallest
-// 2^j (j < kNumCaps) with max_i sum_tau (n_i(tau) - T)+ <= 255 when capping is allowed (else none),
-// the operand width K_s = sum_tau min(M(tau), T_s) and its K blocks (kcpb columns each, clipped
-// to the operand's capacity kcap_blocks). status[0] |= 1 when some K_s exceeds the capacity,
-// status[1] = max_s K_s (status zeroed by the caller). Writes kinfo[s][20] = K_s, [21] = T_s.
-void launch_select(unsigned long long *kinfo, int pl, int V, int allow_cap, int64_t kcap_blocks, int kcpb,
-                   uint32_t *cap, uint32_t *xsel, uint32_t *ident, int64_t *kblocks, unsigned long long *status,
-                   cudaStream_t st);
+// K3 in one launch, one block per shard (k_profile.cu): statistics per candidate cap, the layer cap
+// T_s and operand width K_s (clipped to kcap_blocks; status[0] |= 1 on overflow, status[1] = max K_s;
+// kinfo[s][20] = K_s, [21] = T_s), the column map col0 and the K6 list offsets (xtot[s] totals)
+void launch_shard_plan(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,
+                       int allow_cap, int64_t kcap_blocks, int kcpb, uint32_t *cap, uint32_t *xsel, uint32_t *ident,
+                       int64_t *kblocks, unsigned long long *status, uint32_t *col0, uint32_t *xoff,
+                       unsigned long long *xtot, cudaStream_t st);
 // the count-exchange status of this rank appended to its count block: [0] operand overflow,
 // [1] first input error kind (0 none, 1 symbol, 2 too short, 3 too long), [2] out_bytes, [3] 0
 void launch_status_tail(const unsigned long long *status, const unsigned long long *err, int64_t out_bytes,
