@@ -39,6 +39,8 @@ constexpr int kXrWarps = 8;
 // per row over the row's leading count >= 2 entries (positions from per-(shard, tau) cursors)
 __global__ void __launch_bounds__(256) k_xfill(ExcessArgs a, uint32_t *xcur) {
     __shared__ unsigned long long lbase[kMaxLocalShards + 1];
+    if (blockIdx.x == 0 && threadIdx.x < 16 && a.zero_seg)
+        reinterpret_cast<uint4 *>(a.zero_seg)[threadIdx.x] = make_uint4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
         unsigned long long acc = 0;
         for (int s = 0; s < a.pl; ++s) {

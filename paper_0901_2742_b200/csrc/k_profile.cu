@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
             if (lane == 0) {
                 atomicMin(&a.err[L < k ? 1 : 2], gidx);
                 a.rowinfo[i] = RowInfo{1u, 0xFFFFFFFFu, 1u, (uint32_t)s};
+                a.T[i] = 0ull;
                 a.dcnt[i] = 0;
                 a.nhi[i] = 0;
             }
@@ -376,6 +377,7 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
             a.dcnt[i] = (int32_t)(n_hi + n_lo);
             const uint32_t tw = (uint32_t)Tw;
             a.rowinfo[i] = RowInfo{tw, 0xFFFFFFFFu / tw, 0xFFFFFFFFu % tw + 1u, (uint32_t)s};
+            a.T[i] = 0ull;                              // the all-pairs kernel accumulates T_i atomically
         }
         acc_w += (unsigned long long)Tw;
         max_tw = max(max_tw, (unsigned long long)Tw);
@@ -383,6 +385,23 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         __syncwarp();
     }
     flush();
+}
+
+__global__ void k_profile_reset(uint32_t *M, size_t nM, uint32_t *Mb, size_t nMb, uint32_t *Xc, size_t nXc,
+                                unsigned long long *err4, unsigned long long *statkinfo, size_t nsk) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x, t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (size_t t = t0; t < nM; t += stride) M[t] = 0u;
+    for (size_t t = t0; t < nMb; t += stride) Mb[t] = 0u;
+    for (size_t t = t0; t < nXc; t += stride) Xc[t] = 0u;
+    for (size_t t = t0; t < nsk; t += stride) statkinfo[t] = 0ull;
+    if (t0 < 4) err4[t0] = ~0ull;
+}
+
+void launch_profile_reset(uint32_t *M, size_t nM, uint32_t *Mb, size_t nMb, uint32_t *Xc, size_t nXc,
+                          unsigned long long *err4, unsigned long long *statkinfo, size_t nsk, cudaStream_t st) {
+    const size_t big = std::max(std::max(nM, nXc), std::max(nMb, nsk));
+    const int64_t g = std::max<int64_t>(1, std::min<int64_t>(1024, (int64_t)((big + 255) / 256)));
+    k_profile_reset<<<(unsigned)g, 256, 0, st>>>(M, nM, Mb, nMb, Xc, nXc, err4, statkinfo, nsk);
 }
 
 void launch_profile(const ProfileArgs &a, cudaStream_t st) {
@@ -414,46 +433,41 @@ void launch_profile(const ProfileArgs &a, cudaStream_t st) {
 // with .shard replaced by the local index. Rows of equal Tw land in arbitrary order: nothing
 // downstream depends on it (T and S are permutation invariant; K5 only needs Tw non-decreasing
 // along every shard, K6 only a consistent order).
-__global__ void k_lenhist(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *cnt) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        int s = 0;
-        while (s + 1 < pl && i >= shard_base[s + 1]) ++s;
-        atomicAdd(&cnt[(size_t)s * kLenBinsMax + rowinfo[i].tw], 1u);     // Tw <= 65535 (K1/K2)
-    }
-}
-
-// one block per shard: exclusive scan of the shard's bins 0..max Tw (max Tw from K1/K2 in kinfo[3],
-// read on the device so that no host decision is needed), offset by the shard's first row
-__global__ void __launch_bounds__(1024) k_lenscan(const uint32_t *cnt, const unsigned long long *kinfo,
-                                                   const int64_t *shard_base, uint32_t *pos) {
+// In one launch, one block per shard: histogram, scan and slot scatter with
+// the bins in shared memory when the shard's max Tw (kinfo[3], from K1/K2) is below kLenSmemBins,
+// else in the shard's global bins. Used for every layout (launch count matters on small shards).
+constexpr int kLenSmemBins = 16384;
+__global__ void __launch_bounds__(1024) k_lenorder(const RowInfo *rowinfo, const int64_t *shard_base,
+                                                   const unsigned long long *kinfo, uint32_t *gbins, int32_t *sigma,
+                                                   int32_t *sigma_inv, RowInfo *rinfo_s) {
     using BS = cub::BlockScan<uint32_t, 1024>;
     __shared__ typename BS::TempStorage tmp;
     __shared__ uint32_t carry;
+    extern __shared__ __align__(16) uint32_t lbins[];
     const int s = blockIdx.x;
+    const int64_t b = shard_base[s], e = shard_base[s + 1];
     const unsigned long long mt = kinfo[(size_t)s * kKinfo + 3];
     const int nb = (int)(mt + 1 < (unsigned long long)kLenBinsMax ? mt + 1 : (unsigned long long)kLenBinsMax);
-    if (threadIdx.x == 0) carry = (uint32_t)shard_base[s];
+    uint32_t *bins = nb <= kLenSmemBins ? lbins : gbins + (size_t)s * kLenBinsMax;
+    for (int t = threadIdx.x; t < nb; t += 1024) bins[t] = 0;
+    __syncthreads();
+    for (int64_t i = b + threadIdx.x; i < e; i += 1024) atomicAdd(&bins[min(rowinfo[i].tw, (uint32_t)(nb - 1))], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) carry = (uint32_t)b;
     __syncthreads();
     for (int b0 = 0; b0 < nb; b0 += 1024) {
-        const int b = b0 + threadIdx.x;
-        const uint32_t v = b < nb ? cnt[(size_t)s * kLenBinsMax + b] : 0u;
+        const int t = b0 + threadIdx.x;
+        const uint32_t v = t < nb ? bins[t] : 0u;
         uint32_t ex, tot;
         BS(tmp).ExclusiveSum(v, ex, tot);
-        if (b < nb) pos[(size_t)s * kLenBinsMax + b] = carry + ex;
+        if (t < nb) bins[t] = carry + ex;
         __syncthreads();
         if (threadIdx.x == 0) carry += tot;
         __syncthreads();
     }
-}
-
-__global__ void k_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *pos,
-                             int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        int s = 0;
-        while (s + 1 < pl && i >= shard_base[s + 1]) ++s;
+    for (int64_t i = b + threadIdx.x; i < e; i += 1024) {
         RowInfo r = rowinfo[i];
-        const int64_t p = atomicAdd(&pos[(size_t)s * kLenBinsMax + r.tw], 1u);   // sorted position
-        const int64_t b = shard_base[s];
+        const int64_t p = atomicAdd(&bins[min(r.tw, (uint32_t)(nb - 1))], 1u);   // sorted position
         const int32_t local = (int32_t)(i - b);
         sigma[p] = local;
         sigma_inv[i] = (int32_t)(p - b);
@@ -465,12 +479,11 @@ __global__ void k_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, 
 void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, const unsigned long long *kinfo, int pl,
                      int64_t n, uint32_t *cnt, uint32_t *pos, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s,
                      cudaStream_t st) {
-    const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
-    if (g <= 0) return;
-    cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)pl * kLenBinsMax, st);
-    k_lenhist<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, cnt);
-    k_lenscan<<<pl, 1024, 0, st>>>(cnt, kinfo, shard_base, pos);
-    k_lenscatter<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, pos, sigma, sigma_inv, rinfo_s);
+    (void)pos;
+    if (n <= 0) return;
+    const size_t smem = (size_t)kLenSmemBins * sizeof(uint32_t);
+    smem_optin(k_lenorder, smem);
+    k_lenorder<<<pl, 1024, smem, st>>>(rowinfo, shard_base, kinfo, cnt, sigma, sigma_inv, rinfo_s);
 }
 
 
@@ -497,7 +510,8 @@ __global__ void __launch_bounds__(kScanThreads) k_shard_plan(uint32_t *M, const 
                                                              int64_t kcap_blocks, int kcpb, uint32_t *cap,
                                                              uint32_t *xsel, uint32_t *ident, int64_t *kblocks,
                                                              unsigned long long *status, uint32_t *col0,
-                                                             uint32_t *xoff, unsigned long long *xtot) {
+                                                             uint32_t *xoff, unsigned long long *xtot,
+                                                             uint32_t *xcur) {
     typedef cub::BlockScan<unsigned long long, kScanThreads> Scan;
     constexpr int NV = 3 * kNumCaps + 1;
     __shared__ typename Scan::TempStorage tmp;
@@ -581,6 +595,7 @@ __global__ void __launch_bounds__(kScanThreads) k_shard_plan(uint32_t *M, const 
         }
     }
     __syncthreads();
+    for (int t = threadIdx.x; t < V; t += kScanThreads) xcur[(size_t)s * V + t] = 0u;   // K6 list cursors
     uint32_t *xo = xoff + (size_t)s * V;                  // (4)
     if (sel >= (uint32_t)kNumCaps) {
         for (int t = threadIdx.x; t < V; t += kScanThreads) xo[t] = 0;
@@ -601,9 +616,9 @@ __global__ void __launch_bounds__(kScanThreads) k_shard_plan(uint32_t *M, const 
 void launch_shard_plan(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,
                        int allow_cap, int64_t kcap_blocks, int kcpb, uint32_t *cap, uint32_t *xsel, uint32_t *ident,
                        int64_t *kblocks, unsigned long long *status, uint32_t *col0, uint32_t *xoff,
-                       unsigned long long *xtot, cudaStream_t st) {
+                       unsigned long long *xtot, uint32_t *xcur, cudaStream_t st) {
     k_shard_plan<<<pl, kScanThreads, 0, st>>>(M, Mb, Xc, kinfo, V, allow_cap, kcap_blocks, kcpb, cap, xsel, ident,
-                                              kblocks, status, col0, xoff, xtot);
+                                              kblocks, status, col0, xoff, xtot, xcur);
 }
 
 __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl, int64_t r) {

@@ -57,7 +57,11 @@ static int block_sort(const K *ki, const int32_t *vi, int n, K *ko, int32_t *vo,
 #define SAD_SEG_RADIX 4
 #endif
 constexpr int kSegThreads = SAD_SEG_THREADS, kSegItems = kSmallSortMax / SAD_SEG_THREADS;
-using SegSort = cub::BlockRadixSort<uint32_t, kSegThreads, kSegItems, int32_t, SAD_SEG_RADIX>;
+template <int ITEMS>
+using SegSortT = cub::BlockRadixSort<uint32_t, kSegThreads, ITEMS, int32_t, SAD_SEG_RADIX>;
+using SegSort = SegSortT<kSegItems>;
+constexpr int kRunItems = 4;                      // run blocks of the rank sort: 512 x 4 = 2048 keys
+constexpr int kRunMax = kSegThreads * kRunItems;
 
 // Sub-segment runs: block x sorts run (x % nruns) of segment (x / nruns), the segment split into
 // nruns contiguous runs; with nruns = 1 it sorts the whole segment.
@@ -65,11 +69,11 @@ __device__ __forceinline__ int64_t run_begin(const int64_t *seg, int s, int r, i
     return seg[s] + (seg[s + 1] - seg[s]) * r / nruns;
 }
 
-template <typename K>
+template <typename K, int ITEMS = kSegItems>
 __global__ void __launch_bounds__(kSegThreads) k_seg_sort(const K *keys_in, const int32_t *vals_in,
                                                             const int64_t *seg, K *keys_out, int32_t *vals_out,
                                                             int end_bit, int nruns) {
-    using BRS = SegSort;
+    using BRS = SegSortT<ITEMS>;
     extern __shared__ __align__(16) uint8_t sort_smem[];
     typename BRS::TempStorage &tmp = *reinterpret_cast<typename BRS::TempStorage *>(sort_smem);
     const int sg = blockIdx.x / nruns, rn = blockIdx.x % nruns;
@@ -78,18 +82,18 @@ __global__ void __launch_bounds__(kSegThreads) k_seg_sort(const K *keys_in, cons
     if (n <= 0) return;
     const K low = end_bit >= (int)(8 * sizeof(K)) ? ~K(0) : ((K(1) << end_bit) - 1);
     const K high = keys_in[b] & ~low;
-    uint32_t k[kSegItems];
-    int32_t v[kSegItems];
+    uint32_t k[ITEMS];
+    int32_t v[ITEMS];
 #pragma unroll
-    for (int i = 0; i < kSegItems; ++i) {
-        const int idx = threadIdx.x * kSegItems + i;
+    for (int i = 0; i < ITEMS; ++i) {
+        const int idx = threadIdx.x * ITEMS + i;
         k[i] = idx < n ? (uint32_t)(keys_in[b + idx] & low) : 0xFFFFFFFFu;   // padding sorts last (stable)
         v[i] = idx < n ? vals_in[b + idx] : 0;
     }
     BRS(tmp).Sort(k, v, 0, end_bit);
 #pragma unroll
-    for (int i = 0; i < kSegItems; ++i) {
-        const int idx = threadIdx.x * kSegItems + i;
+    for (int i = 0; i < ITEMS; ++i) {
+        const int idx = threadIdx.x * ITEMS + i;
         if (idx < n) {
             keys_out[b + idx] = high | (K)k[i];
             vals_out[b + idx] = v[i];
@@ -138,22 +142,72 @@ __global__ void k_merge_runs(const K *keys, const int32_t *vals, const int64_t *
     }
 }
 
-// runs sorted in place, then merged into (ko, vo): several blocks per segment
+// The same merge with the whole segment's keys staged in shared memory (one block per segment of
+// at most kMergeSmemMax keys): the binary searches run on shared memory instead of L2 latency.
+constexpr int kMergeThreads = 1024, kMergeSmemMax = 16384;
 template <typename K>
-static int seg_sort_runs(K *ki, int32_t *vi, const int64_t *seg, int nseg, int nruns, int64_t n, K *ko, int32_t *vo,
-                         int end_bit, cudaStream_t st) {
-    const size_t smem = sizeof(typename SegSort::TempStorage);
+__global__ void __launch_bounds__(kMergeThreads) k_merge_runs_smem(const K *keys, const int32_t *vals,
+                                                                   const int64_t *seg, int nruns, K *keys_out,
+                                                                   int32_t *vals_out) {
+    extern __shared__ __align__(16) uint8_t merge_smem[];
+    K *sk = reinterpret_cast<K *>(merge_smem);
+    const int s = blockIdx.x;
+    const int64_t b = seg[s];
+    const int n = (int)(seg[s + 1] - b);
+    for (int t = threadIdx.x; t < n; t += kMergeThreads) sk[t] = keys[b + t];
+    __syncthreads();
+    for (int t = threadIdx.x; t < n; t += kMergeThreads) {
+        int r = 0;
+        while (r + 1 < nruns && t >= (int)((int64_t)n * (r + 1) / nruns)) ++r;
+        const K key = sk[t];
+        int pos = t - (int)((int64_t)n * r / nruns);
+        for (int q = 0; q < nruns; ++q) {
+            if (q == r) continue;
+            int lo = (int)((int64_t)n * q / nruns), hi = (int)((int64_t)n * (q + 1) / nruns);
+            const int b0 = lo;
+            while (lo < hi) {                  // first element > key (q < r) or >= key (q > r)
+                const int m = (lo + hi) >> 1;
+                const K x = sk[m];
+                if (q < r ? x <= key : x < key) lo = m + 1; else hi = m;
+            }
+            pos += lo - b0;
+        }
+        keys_out[b + pos] = key;
+        vals_out[b + pos] = vals[b + t];
+    }
+}
+
+// the stable sort of every segment: runs of at most kRunMax keys sorted in place by separate blocks
+// (512 x 4 items: the block sort's cost follows its capacity, not the run), then merged into
+// (ko, vo) by ranking; a segment that fits one run is sorted straight into (ko, vo)
+template <typename K>
+static int seg_sort_runs(K *ki, int32_t *vi, const int64_t *seg, int nseg, int64_t max_seg, int64_t n, K *ko,
+                         int32_t *vo, int end_bit, cudaStream_t st) {
     if (end_bit > 32) return -1;
-    if (smem_optin(k_seg_sort<K>, smem) != cudaSuccess) return -1;
-    k_seg_sort<K><<<nseg * nruns, kSegThreads, smem, st>>>(ki, vi, seg, ki, vi, end_bit, nruns);
-    const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
-    if (g > 0) k_merge_runs<K><<<(unsigned)g, 256, 0, st>>>(ki, vi, seg, nseg, nruns, n, ko, vo);
+    const int nruns = (int)std::max<int64_t>(1, (max_seg + kRunMax - 1) / kRunMax);
+    if (nruns == 1) {
+        const size_t smem = sizeof(typename SegSortT<kRunItems>::TempStorage);
+        if (smem_optin(k_seg_sort<K, kRunItems>, smem) != cudaSuccess) return -1;
+        k_seg_sort<K, kRunItems><<<nseg, kSegThreads, smem, st>>>(ki, vi, seg, ko, vo, end_bit, 1);
+        return 0;
+    }
+    const size_t smem = sizeof(typename SegSortT<kRunItems>::TempStorage);
+    if (smem_optin(k_seg_sort<K, kRunItems>, smem) != cudaSuccess) return -1;
+    k_seg_sort<K, kRunItems><<<nseg * nruns, kSegThreads, smem, st>>>(ki, vi, seg, ki, vi, end_bit, nruns);
+    if (max_seg <= kMergeSmemMax) {
+        const size_t ms = (size_t)max_seg * sizeof(K);
+        if (smem_optin(k_merge_runs_smem<K>, ms) != cudaSuccess) return -1;
+        k_merge_runs_smem<K><<<nseg, kMergeThreads, ms, st>>>(ki, vi, seg, nruns, ko, vo);
+    } else {
+        const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
+        if (g > 0) k_merge_runs<K><<<(unsigned)g, 256, 0, st>>>(ki, vi, seg, nseg, nruns, n, ko, vo);
+    }
     return 0;
 }
 
-int seg_sort_pairs_runs(unsigned long long *ki, int32_t *vi, const int64_t *seg, int nseg, int nruns, int64_t n,
+int seg_sort_pairs_runs(unsigned long long *ki, int32_t *vi, const int64_t *seg, int nseg, int64_t max_seg, int64_t n,
                         unsigned long long *ko, int32_t *vo, int end_bit, cudaStream_t st) {
-    return seg_sort_runs<unsigned long long>(ki, vi, seg, nseg, nruns, n, ko, vo, end_bit, st);
+    return seg_sort_runs<unsigned long long>(ki, vi, seg, nseg, max_seg, n, ko, vo, end_bit, st);
 }
 
 int seg_sort_pairs(const uint32_t *ki, const int32_t *vi, const int64_t *seg, int nseg, uint32_t *ko, int32_t *vo,

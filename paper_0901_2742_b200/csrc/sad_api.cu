@@ -185,7 +185,6 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_pivots = b.take<unsigned long long>((size_t)p);
     c->d_bnd = b.take<int64_t>((size_t)pl * p);
     c->d_lpre = b.take<int64_t>((size_t)n + pl + 1);
-    c->d_len_sorted = b.take<int64_t>((size_t)n);
     c->d_seg = b.take<int64_t>((size_t)pl * p * 2);
     c->d_counts = b.take<int64_t>((size_t)pl * p * 2);
     c->tc_tiles_cap = tc_tiles_bound(n, pl);
@@ -740,11 +739,9 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
 // K1/K2 accumulators cleared, on ctx->st
 static int profile_reset(sad_ctx *ctx) {
     const int pl = ctx->pl, V = ctx->V;
-    CK(cudaMemsetAsync(ctx->d_M, 0, sizeof(uint32_t) * (size_t)pl * V, ctx->st));
-    CK(cudaMemsetAsync(ctx->d_Mb, 0, sizeof(uint32_t) * (size_t)pl * ((V + 31) / 32), ctx->st));
-    CK(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long) * 4, ctx->st));
-    CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(unsigned long long) * (4 + kKinfo * (size_t)pl), ctx->st));
-    CK(cudaMemsetAsync(ctx->d_Xc, 0, sizeof(uint32_t) * kNumCaps * (size_t)pl * V, ctx->st));
+    launch_profile_reset(ctx->d_M, (size_t)pl * V, ctx->d_Mb, (size_t)pl * ((V + 31) / 32), ctx->d_Xc,
+                         (size_t)kNumCaps * pl * V, ctx->d_err, ctx->d_status, 4 + kKinfo * (size_t)pl, ctx->st);
+    LAUNCHED();
     return SAD_OK;
 }
 
@@ -771,6 +768,7 @@ static int profile_launch(sad_ctx *ctx, int64_t i0, int64_t i1) {
     a.Xc = ctx->d_Xc;
     a.Mb = ctx->d_Mb;
     a.nhi = ctx->d_nhi;
+    a.T = ctx->d_T;
     a.i_begin = i0;
     a.i_end = i1;
     launch_profile(a, ctx->st);
@@ -791,11 +789,12 @@ int sad_build_profiles(sad_ctx *ctx) {
         if (int rc = profile_launch(ctx, 0, ctx->n)) return rc;
     }
     ctx->profiled = false;
+    ctx->t_used = false;
     // K3 (statistics, the cap / K decision, column map, K6 list offsets) in one launch, all on the
     // device, then the length order (rows by L - k + 1)
     launch_shard_plan(ctx->d_M, ctx->d_Mb, ctx->d_Xc, ctx->d_kinfo, pl, V, ctx->allow_cap ? 1 : 0, ctx->kcap_blocks,
                       (int)ctx->kcols_per_block, ctx->d_cap, ctx->d_xsel, ctx->d_ident, ctx->d_kblocks, ctx->d_status,
-                      ctx->d_col0, ctx->d_xoff, xtot_of(ctx), ctx->st);
+                      ctx->d_col0, ctx->d_xoff, xtot_of(ctx), ctx->d_xcur, ctx->st);
     LAUNCHED();
     if (ctx->use_tc) {
         launch_lenorder(ctx->d_rowinfo, ctx->d_shard_base, ctx->d_kinfo, pl, ctx->n, ctx->d_lcnt,
@@ -857,7 +856,9 @@ static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, 
         return fail(ctx, SAD_E_ARG, "operand must be 1024-byte aligned");
     ctx->d_operand = d_operand;
     const int pl = ctx->pl;
-    CK(cudaMemsetAsync(ctx->d_T, 0, sizeof(unsigned long long) * (size_t)ctx->n, ctx->st));
+    // K1/K2 zeroed T; a second all-pairs pass over the same profiles starts from zero again
+    if (ctx->t_used) CK(cudaMemsetAsync(ctx->d_T, 0, sizeof(unsigned long long) * (size_t)ctx->n, ctx->st));
+    ctx->t_used = true;
     if (ctx->d_sim) CK(cudaMemsetAsync(ctx->d_sim, 0, sizeof(uint16_t) * (size_t)ctx->sim_elems, ctx->st));
 
     OperandArgs o{};
@@ -891,9 +892,8 @@ static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, 
         o.cap = ctx->d_cap;
         o.ident = ctx->d_ident;
         if (lists) {
-            CK(cudaMemsetAsync(ctx->d_xcur, 0, sizeof(uint32_t) * (size_t)pl * ctx->V, ctx->st));
-            CK(cudaMemsetAsync(E + ctx->h_ebase[pl], 0, 256, ctx->st));   // the zero row segment
             ExcessArgs x{};
+            x.zero_seg = E + ctx->h_ebase[pl];   // the zero row segment (cleared by k_xfill)
             x.csr = ctx->d_csr;
             x.off = ctx->d_off;
             x.nhi = ctx->d_nhi;
@@ -1059,25 +1059,17 @@ static int rank_global_impl(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_sam
         launch_f1_gainfo(ctx->d_anc_local, ctx->pl, ctx->shard0, p, ctx->first_idx, ctx->d_ga_info, ctx->st);
         LAUNCHED();
     }
-    // blocks per shard of the local rank sort (then one merge by ranking): 4 with 8+ shards on the
-    // rank, more with fewer shards so that a one-shard rank still sorts with 32 blocks
-    const int runs = std::max(4, 32 / ctx->pl);
-    if (!(qbits == 32 && ctx->max_w <= (int64_t)kSmallSortMax * runs &&
-          seg_sort_pairs_runs(ctx->d_ckey, ctx->d_perm_in, ctx->d_shard_base, ctx->pl, runs, ctx->n,
+    // the local rank sort: runs of <= 2048 keys per block, merged by ranking in shared memory
+    if (!(qbits == 32 && ctx->max_w <= (int64_t)16384 &&
+          seg_sort_pairs_runs(ctx->d_ckey, ctx->d_perm_in, ctx->d_shard_base, ctx->pl, ctx->max_w, ctx->n,
                               ctx->d_ckey_sorted, ctx->d_perm_sorted, 32, ctx->st) == 0))
         CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
                       qbits + sbits));
     LAUNCHED();
-    launch_unpack_sorted(ctx->d_ckey_sorted, ctx->d_perm_sorted, ctx->n, ctx->first_idx, ctx->d_key_sorted,
-                         ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, qbits, ctx->ibits, ctx->st);
+    launch_unpack_sorted(ctx->d_ckey_sorted, ctx->d_perm_sorted, ctx->d_shard_base, ctx->pl, ctx->d_off, ctx->n,
+                         ctx->first_idx, ctx->d_key_sorted, ctx->d_rowinfo, ctx->cfg.k, ctx->d_lpre, qbits, ctx->ibits,
+                         ctx->st);
     LAUNCHED();
-    // exclusive prefix of L in sorted order (the residue offsets of every bucket slice, K12/K13)
-    CK(cudaMemsetAsync(ctx->d_lpre, 0, sizeof(int64_t), ctx->st));
-    {
-        size_t tb2 = ctx->cub_bytes;
-        CK(cub::DeviceScan::InclusiveSum(ctx->d_cub, tb2, ctx->d_len_sorted, ctx->d_lpre + 1, (int)ctx->n, ctx->st));
-        LAUNCHED();
-    }
     if (p > 1) {
         launch_samples(ctx->d_key_sorted, ctx->d_shard_base, ctx->pl, p,
                        reinterpret_cast<unsigned long long *>(d_samples_out), ctx->st);

@@ -95,15 +95,20 @@ struct ProfileArgs {
     uint32_t *Xc;                    // [pl][kNumCaps][V]: #{i : n_i(tau) > 2^j} (zeroed)
     uint32_t *Mb;                    // [pl][ceil(V/32)]: k-mers present in the shard (zeroed; M >= 2 goes to M)
     int32_t *nhi;                    // [n] entries with count >= 2 (they lead each CSR row)
+    unsigned long long *T;           // [n] within-shard rank sums, zeroed here for the all-pairs kernel
 };
 void launch_profile(const ProfileArgs &a, cudaStream_t st);
+// the per-step accumulators of K1/K2 and K3 cleared in one launch: M, Mb, Xc = 0; err = all ones;
+// status + kinfo = 0
+void launch_profile_reset(uint32_t *M, size_t nM, uint32_t *Mb, size_t nMb, uint32_t *Xc, size_t nXc,
+                          unsigned long long *err4, unsigned long long *statkinfo, size_t nsk, cudaStream_t st);
 // K3 in one launch, one block per shard (k_profile.cu): statistics per candidate cap, the layer cap
 // T_s and operand width K_s (clipped to kcap_blocks; status[0] |= 1 on overflow, status[1] = max K_s;
 // kinfo[s][20] = K_s, [21] = T_s), the column map col0 and the K6 list offsets (xtot[s] totals)
 void launch_shard_plan(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,
                        int allow_cap, int64_t kcap_blocks, int kcpb, uint32_t *cap, uint32_t *xsel, uint32_t *ident,
                        int64_t *kblocks, unsigned long long *status, uint32_t *col0, uint32_t *xoff,
-                       unsigned long long *xtot, cudaStream_t st);
+                       unsigned long long *xtot, uint32_t *xcur, cudaStream_t st);
 // the count-exchange status of this rank appended to its count block: [0] operand overflow,
 // [1] first input error kind (0 none, 1 symbol, 2 too short, 3 too long), [2] out_bytes, [3] 0
 void launch_status_tail(const unsigned long long *status, const unsigned long long *err, int64_t out_bytes,
@@ -156,6 +161,7 @@ struct ExcessArgs {
     const int32_t *sigma_inv;        // [n] local index -> sorted position
     uint2 *xrow;                     // [n] .x = 1 if the row (sorted position) has excess
     uint8_t *E;                      // dense excess rows
+    uint8_t *zero_seg;               // 256 bytes zeroed by k_xfill (the staging source of rows without excess)
     const int64_t *ebase;            // device [pl+1] per shard byte offset of E_s
 };
 int launch_excess(const ExcessArgs &a, cudaStream_t st);
@@ -235,9 +241,11 @@ void launch_rank_vs_ga(const RankArgs &a, cudaStream_t st);
 
 void launch_samples(const unsigned long long *key_sorted, const int64_t *shard_base, int pl, int p,
                     unsigned long long *samples_out, cudaStream_t st);
-void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, int64_t n,
-                          int64_t first_idx, unsigned long long *key_sorted, const RowInfo *rowinfo, int k,
-                          int64_t *len_sorted, int qbits, int ibits, cudaStream_t st);
+// unpack the sorted composite keys into keys (q << ibits) + index and the exclusive prefix of L in
+// sorted order over all local shards (lpre [n + 1]); one block per shard
+void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, const int64_t *shard_base,
+                          int pl, const int64_t *off, int64_t n, int64_t first_idx, unsigned long long *key_sorted,
+                          const RowInfo *rowinfo, int k, int64_t *lpre, int qbits, int ibits, cudaStream_t st);
 // f1: rank against the k*p gathered samples
 void launch_tkeys(const unsigned long long *T, const RowInfo *rowinfo, int64_t n, unsigned long long *keys,
                   int32_t *rows, cudaStream_t st);
@@ -328,9 +336,9 @@ int seg_sort_pairs(const uint32_t *ki, const int32_t *vi, const int64_t *seg, in
                    int end_bit, cudaStream_t st);
 int seg_sort_pairs(const unsigned long long *ki, const int32_t *vi, const int64_t *seg, int nseg,
                    unsigned long long *ko, int32_t *vo, int end_bit, cudaStream_t st);
-// the same with every segment split into nruns runs sorted by separate blocks (in place in ki, vi),
-// then merged stably into (ko, vo); 0 or -1
-int seg_sort_pairs_runs(unsigned long long *ki, int32_t *vi, const int64_t *seg, int nseg, int nruns, int64_t n,
+// the same with every segment (at most max_seg pairs) split into runs of at most 2048 pairs sorted by
+// separate blocks (in place in ki, vi), then merged stably into (ko, vo); 0 or -1
+int seg_sort_pairs_runs(unsigned long long *ki, int32_t *vi, const int64_t *seg, int nseg, int64_t max_seg, int64_t n,
                         unsigned long long *ko, int32_t *vo, int end_bit, cudaStream_t st);
 void launch_rebase(const int64_t *src, int64_t n1, int64_t *off, cudaStream_t st);
 void launch_distance(const uint16_t *sim, const RowInfo *rowinfo, int64_t w, float *D, cudaStream_t st);
@@ -432,7 +440,6 @@ struct sad_ctx {
     int32_t *d_perm_in = nullptr, *d_perm_sorted = nullptr;
     unsigned long long *d_pivots = nullptr;
     int64_t *d_bnd = nullptr, *d_lpre = nullptr, *d_seg = nullptr, *d_counts = nullptr;
-    int64_t *d_len_sorted = nullptr;  // [n] L of each sequence in sorted order (scanned into d_lpre)
     bool counts_pending = false;
     void *d_tmap = nullptr;
     void *d_cub = nullptr;
@@ -473,6 +480,7 @@ struct sad_ctx {
     unsigned long long *d_send_meta = nullptr;
     uint8_t *d_send_res = nullptr;
     bool capturing = false;                          // the stream is being captured into a CUDA graph
+    bool t_used = false;                             // T accumulated since K1/K2 last zeroed it
     cudaEvent_t gev[4] = {};                         // stage events recorded inside a captured step
     bool graph_events = false;
     bool out_recv_layout = false;                    // the output buffer holds the receive buffers too
