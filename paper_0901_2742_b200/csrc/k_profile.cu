@@ -433,41 +433,46 @@ void launch_profile(const ProfileArgs &a, cudaStream_t st) {
 // with .shard replaced by the local index. Rows of equal Tw land in arbitrary order: nothing
 // downstream depends on it (T and S are permutation invariant; K5 only needs Tw non-decreasing
 // along every shard, K6 only a consistent order).
-// In one launch, one block per shard: histogram, scan and slot scatter with
-// the bins in shared memory when the shard's max Tw (kinfo[3], from K1/K2) is below kLenSmemBins,
-// else in the shard's global bins. Used for every layout (launch count matters on small shards).
-constexpr int kLenSmemBins = 16384;
-__global__ void __launch_bounds__(1024) k_lenorder(const RowInfo *rowinfo, const int64_t *shard_base,
-                                                   const unsigned long long *kinfo, uint32_t *gbins, int32_t *sigma,
-                                                   int32_t *sigma_inv, RowInfo *rinfo_s) {
+__global__ void k_lenhist(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *cnt) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int s = 0;
+        while (s + 1 < pl && i >= shard_base[s + 1]) ++s;
+        atomicAdd(&cnt[(size_t)s * kLenBinsMax + rowinfo[i].tw], 1u);     // Tw <= 65535 (K1/K2)
+    }
+}
+
+// one block per shard: exclusive scan of the shard's bins 0..max Tw (max Tw from K1/K2 in kinfo[3],
+// read on the device so that no host decision is needed), offset by the shard's first row
+__global__ void __launch_bounds__(1024) k_lenscan(const uint32_t *cnt, const unsigned long long *kinfo,
+                                                   const int64_t *shard_base, uint32_t *pos) {
     using BS = cub::BlockScan<uint32_t, 1024>;
     __shared__ typename BS::TempStorage tmp;
     __shared__ uint32_t carry;
-    extern __shared__ __align__(16) uint32_t lbins[];
     const int s = blockIdx.x;
-    const int64_t b = shard_base[s], e = shard_base[s + 1];
     const unsigned long long mt = kinfo[(size_t)s * kKinfo + 3];
     const int nb = (int)(mt + 1 < (unsigned long long)kLenBinsMax ? mt + 1 : (unsigned long long)kLenBinsMax);
-    uint32_t *bins = nb <= kLenSmemBins ? lbins : gbins + (size_t)s * kLenBinsMax;
-    for (int t = threadIdx.x; t < nb; t += 1024) bins[t] = 0;
-    __syncthreads();
-    for (int64_t i = b + threadIdx.x; i < e; i += 1024) atomicAdd(&bins[min(rowinfo[i].tw, (uint32_t)(nb - 1))], 1u);
-    __syncthreads();
-    if (threadIdx.x == 0) carry = (uint32_t)b;
+    if (threadIdx.x == 0) carry = (uint32_t)shard_base[s];
     __syncthreads();
     for (int b0 = 0; b0 < nb; b0 += 1024) {
-        const int t = b0 + threadIdx.x;
-        const uint32_t v = t < nb ? bins[t] : 0u;
+        const int b = b0 + threadIdx.x;
+        const uint32_t v = b < nb ? cnt[(size_t)s * kLenBinsMax + b] : 0u;
         uint32_t ex, tot;
         BS(tmp).ExclusiveSum(v, ex, tot);
-        if (t < nb) bins[t] = carry + ex;
+        if (b < nb) pos[(size_t)s * kLenBinsMax + b] = carry + ex;
         __syncthreads();
         if (threadIdx.x == 0) carry += tot;
         __syncthreads();
     }
-    for (int64_t i = b + threadIdx.x; i < e; i += 1024) {
+}
+
+__global__ void k_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *pos,
+                             int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int s = 0;
+        while (s + 1 < pl && i >= shard_base[s + 1]) ++s;
         RowInfo r = rowinfo[i];
-        const int64_t p = atomicAdd(&bins[min(r.tw, (uint32_t)(nb - 1))], 1u);   // sorted position
+        const int64_t p = atomicAdd(&pos[(size_t)s * kLenBinsMax + r.tw], 1u);   // sorted position
+        const int64_t b = shard_base[s];
         const int32_t local = (int32_t)(i - b);
         sigma[p] = local;
         sigma_inv[i] = (int32_t)(p - b);
@@ -479,11 +484,12 @@ __global__ void __launch_bounds__(1024) k_lenorder(const RowInfo *rowinfo, const
 void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, const unsigned long long *kinfo, int pl,
                      int64_t n, uint32_t *cnt, uint32_t *pos, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s,
                      cudaStream_t st) {
-    (void)pos;
-    if (n <= 0) return;
-    const size_t smem = (size_t)kLenSmemBins * sizeof(uint32_t);
-    smem_optin(k_lenorder, smem);
-    k_lenorder<<<pl, 1024, smem, st>>>(rowinfo, shard_base, kinfo, cnt, sigma, sigma_inv, rinfo_s);
+    const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
+    if (g <= 0) return;
+    cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)pl * kLenBinsMax, st);
+    k_lenhist<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, cnt);
+    k_lenscan<<<pl, 1024, 0, st>>>(cnt, kinfo, shard_base, pos);
+    k_lenscatter<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, pos, sigma, sigma_inv, rinfo_s);
 }
 
 
@@ -517,17 +523,16 @@ __global__ void __launch_bounds__(kScanThreads) k_shard_plan(uint32_t *M, const 
     __shared__ typename Scan::TempStorage tmp;
     __shared__ unsigned long long red[NV];
     __shared__ uint32_t s_T, s_sel;
+    __shared__ unsigned long long s_carry;
     const int s = blockIdx.x;
     uint32_t *m = M + (size_t)s * V;
     const uint32_t *xc = Xc + (size_t)s * kNumCaps * V;
     const uint32_t *mb = Mb + (size_t)s * ((V + 31) / 32);
     unsigned long long *ki = kinfo + (size_t)s * kKinfo;
-    const int per = (V + kScanThreads - 1) / kScanThreads;
-    const int t0 = min(V, (int)threadIdx.x * per), t1 = min(V, t0 + per);
     if (threadIdx.x < NV) red[threadIdx.x] = 0;
     __syncthreads();
     unsigned long long acc[NV] = {};
-    for (int t = t0; t < t1; ++t) {                       // (1)
+    for (int t = threadIdx.x; t < V; t += kScanThreads) {   // (1), coalesced
         uint32_t x = m[t];
         if (x == 0 && ((mb[t >> 5] >> (t & 31)) & 1u)) {
             x = 1;
@@ -581,36 +586,43 @@ __global__ void __launch_bounds__(kScanThreads) k_shard_plan(uint32_t *M, const 
         atomicMax(&status[1], K);
         s_T = T;
         s_sel = sel;
+        s_carry = 0;
     }
     __syncthreads();
     const uint32_t T = s_T, sel = s_sel;
-    {                                                     // (3)
-        unsigned long long sum = 0, base, total;
-        for (int t = t0; t < t1; ++t) sum += min(m[t], T);
-        Scan(tmp).ExclusiveSum(sum, base, total);
-        uint32_t *c = col0 + (size_t)s * V;
-        for (int t = t0; t < t1; ++t) {
-            c[t] = (uint32_t)base;
-            base += min(m[t], T);
-        }
-    }
-    __syncthreads();
     for (int t = threadIdx.x; t < V; t += kScanThreads) xcur[(size_t)s * V + t] = 0u;   // K6 list cursors
-    uint32_t *xo = xoff + (size_t)s * V;                  // (4)
+    // (3) and (4): exclusive scans in chunks of kScanThreads consecutive k-mers (coalesced), with a carry
+    uint32_t *c = col0 + (size_t)s * V;
+    for (int c0 = 0; c0 < V; c0 += kScanThreads) {
+        const int t = c0 + threadIdx.x;
+        const unsigned long long v = t < V ? min(m[t], T) : 0u;
+        unsigned long long ex, tot;
+        Scan(tmp).ExclusiveSum(v, ex, tot);
+        if (t < V) c[t] = (uint32_t)(s_carry + ex);
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += tot;
+        __syncthreads();
+    }
+    uint32_t *xo = xoff + (size_t)s * V;
     if (sel >= (uint32_t)kNumCaps) {
         for (int t = threadIdx.x; t < V; t += kScanThreads) xo[t] = 0;
         if (threadIdx.x == 0) xtot[s] = 0;
         return;
     }
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
     const uint32_t *x = xc + (size_t)sel * V;
-    unsigned long long sum = 0, base, total;
-    for (int t = t0; t < t1; ++t) sum += x[t];
-    Scan(tmp).ExclusiveSum(sum, base, total);
-    for (int t = t0; t < t1; ++t) {
-        xo[t] = (uint32_t)base;
-        base += x[t];
+    for (int c0 = 0; c0 < V; c0 += kScanThreads) {
+        const int t = c0 + threadIdx.x;
+        const unsigned long long v = t < V ? x[t] : 0u;
+        unsigned long long ex, tot;
+        Scan(tmp).ExclusiveSum(v, ex, tot);
+        if (t < V) xo[t] = (uint32_t)(s_carry + ex);
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += tot;
+        __syncthreads();
     }
-    if (threadIdx.x == 0) xtot[s] = total;
+    if (threadIdx.x == 0) xtot[s] = s_carry;
 }
 
 void launch_shard_plan(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,

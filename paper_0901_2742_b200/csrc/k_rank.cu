@@ -384,66 +384,27 @@ void launch_gather_out(const int32_t *perm, int64_t n, const int64_t *src_off, c
 }
 
 
-// Unpack the sorted composite keys (shard | q | row) into the real keys (q << ibits) + source index
-// (GA mode, qbits 32: the sort key holds min(q, 2^32 - 1); q = 2^32 (S = den) is restored from the
-// all-ones value, which no other q reaches), fused with the exclusive prefix of L in
-// sorted order over all local shards
-// (lpre[0] = 0, lpre[t + 1] = lpre[t] + L of sorted row t: the residue offsets of every bucket
-// slice, K12/K13), one block per shard: a shard's prefix starts at its residues' offset
-// off[shard_base[s]] (a shard holds the same residues in any order).
-constexpr int kUnpackThreads = 1024;
-__global__ void __launch_bounds__(kUnpackThreads) k_unpack_scan(const unsigned long long *ck, const int32_t *perm_sorted,
-                                                                const int64_t *shard_base, const int64_t *off,
-                                                                int64_t first_idx, unsigned long long *key_sorted,
-                                                                const RowInfo *rowinfo, int k, int64_t *lpre,
-                                                                unsigned long long qmask, int ibits) {
-    using BS = cub::BlockScan<long long, kUnpackThreads>;
-    __shared__ typename BS::TempStorage tmp;
-    __shared__ long long carry;
-    const int s = blockIdx.x;
-    const int64_t b = shard_base[s], e = shard_base[s + 1];
-    if (threadIdx.x == 0) {
-        carry = off[b] - off[0];
-        if (s == 0) lpre[0] = 0;
-    }
-    __syncthreads();
-    constexpr int IT = 8;                                  // items per thread per chunk
-    for (int64_t c0 = b; c0 < e; c0 += (int64_t)kUnpackThreads * IT) {
-        long long len[IT], sum = 0;
-#pragma unroll
-        for (int u = 0; u < IT; ++u) {
-            const int64_t t = c0 + (int64_t)threadIdx.x * IT + u;
-            len[u] = 0;
-            if (t < e) {
-                const unsigned long long q32 = ck[t] & qmask;
-                const unsigned long long q = (qmask == 0xFFFFFFFFull && q32 == 0xFFFFFFFFull) ? (1ull << 32) : q32;
-                const int32_t row = perm_sorted[t];
-                key_sorted[t] = (q << ibits) + (unsigned long long)(first_idx + row);
-                len[u] = (long long)rowinfo[row].tw + k - 1;
-            }
-            sum += len[u];
-        }
-        long long ex, tot;
-        BS(tmp).ExclusiveSum(sum, ex, tot);
-        long long run = carry + ex;
-#pragma unroll
-        for (int u = 0; u < IT; ++u) {
-            const int64_t t = c0 + (int64_t)threadIdx.x * IT + u;
-            run += len[u];
-            if (t < e) lpre[t + 1] = run;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) carry += tot;
-        __syncthreads();
+// unpack the sorted composite keys (shard | q | row) into the real keys (q << ibits) + source
+// index and rows. GA mode (qbits 32): the sort key holds min(q, 2^32 - 1); q = 2^32 (S = den) is
+// restored from the all-ones value, which no other q reaches.
+__global__ void k_unpack_sorted(const unsigned long long *ck, const int32_t *perm_sorted, int64_t n, int64_t first_idx,
+                                unsigned long long *key_sorted, const RowInfo *rowinfo, int k, int64_t *len_sorted,
+                                unsigned long long qmask, int ibits) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long q32 = ck[t] & qmask;
+        const unsigned long long q = (qmask == 0xFFFFFFFFull && q32 == 0xFFFFFFFFull) ? (1ull << 32) : q32;
+        const int32_t row = perm_sorted[t];
+        key_sorted[t] = (q << ibits) + (unsigned long long)(first_idx + row);
+        len_sorted[t] = (int64_t)rowinfo[row].tw + k - 1;
     }
 }
 
-void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, const int64_t *shard_base,
-                          int pl, const int64_t *off, int64_t n, int64_t first_idx, unsigned long long *key_sorted,
-                          const RowInfo *rowinfo, int k, int64_t *lpre, int qbits, int ibits, cudaStream_t st) {
+void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, int64_t n,
+                          int64_t first_idx, unsigned long long *key_sorted, const RowInfo *rowinfo, int k,
+                          int64_t *len_sorted, int qbits, int ibits, cudaStream_t st) {
     if (n > 0)
-        k_unpack_scan<<<pl, kUnpackThreads, 0, st>>>(ckey_sorted, perm_sorted, shard_base, off, first_idx, key_sorted,
-                                                     rowinfo, k, lpre, (1ull << qbits) - 1ull, ibits);
+        k_unpack_sorted<<<grid1d(n), 256, 0, st>>>(ckey_sorted, perm_sorted, n, first_idx, key_sorted, rowinfo, k,
+                                                   len_sorted, (1ull << qbits) - 1ull, ibits);
 }
 
 // K14: merge by ranking. Keys are unique, every run is sorted, so the output slot of an element is

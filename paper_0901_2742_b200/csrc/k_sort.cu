@@ -144,26 +144,28 @@ __global__ void k_merge_runs(const K *keys, const int32_t *vals, const int64_t *
 
 // The same merge with the whole segment's keys staged in shared memory (one block per segment of
 // at most kMergeSmemMax keys): the binary searches run on shared memory instead of L2 latency.
-constexpr int kMergeThreads = 1024, kMergeSmemMax = 16384;
+constexpr int kMergeThreads = 1024, kMergeSmemMax = 16384, kMergeMaxRuns = 64;
 template <typename K>
 __global__ void __launch_bounds__(kMergeThreads) k_merge_runs_smem(const K *keys, const int32_t *vals,
-                                                                   const int64_t *seg, int nruns, K *keys_out,
-                                                                   int32_t *vals_out) {
+                                                                   const int64_t *seg, int nruns, int bps,
+                                                                   K *keys_out, int32_t *vals_out) {
     extern __shared__ __align__(16) uint8_t merge_smem[];
+    __shared__ int rb[kMergeMaxRuns + 1];                  // run bounds (the same split as the run sorts)
     K *sk = reinterpret_cast<K *>(merge_smem);
-    const int s = blockIdx.x;
+    const int s = blockIdx.x / bps, part = blockIdx.x % bps;   // bps blocks share a segment's elements
     const int64_t b = seg[s];
     const int n = (int)(seg[s + 1] - b);
+    if (threadIdx.x <= nruns) rb[threadIdx.x] = (int)((int64_t)n * threadIdx.x / nruns);
     for (int t = threadIdx.x; t < n; t += kMergeThreads) sk[t] = keys[b + t];
     __syncthreads();
-    for (int t = threadIdx.x; t < n; t += kMergeThreads) {
+    for (int t = part * kMergeThreads + threadIdx.x; t < n; t += bps * kMergeThreads) {
         int r = 0;
-        while (r + 1 < nruns && t >= (int)((int64_t)n * (r + 1) / nruns)) ++r;
+        while (r + 1 < nruns && t >= rb[r + 1]) ++r;
         const K key = sk[t];
-        int pos = t - (int)((int64_t)n * r / nruns);
+        int pos = t - rb[r];
         for (int q = 0; q < nruns; ++q) {
             if (q == r) continue;
-            int lo = (int)((int64_t)n * q / nruns), hi = (int)((int64_t)n * (q + 1) / nruns);
+            int lo = rb[q], hi = rb[q + 1];
             const int b0 = lo;
             while (lo < hi) {                  // first element > key (q < r) or >= key (q > r)
                 const int m = (lo + hi) >> 1;
@@ -197,7 +199,8 @@ static int seg_sort_runs(K *ki, int32_t *vi, const int64_t *seg, int nseg, int64
     if (max_seg <= kMergeSmemMax) {
         const size_t ms = (size_t)max_seg * sizeof(K);
         if (smem_optin(k_merge_runs_smem<K>, ms) != cudaSuccess) return -1;
-        k_merge_runs_smem<K><<<nseg, kMergeThreads, ms, st>>>(ki, vi, seg, nruns, ko, vo);
+        const int bps = std::max(1, 64 / nseg);      // blocks per segment: ~64 blocks in all
+        k_merge_runs_smem<K><<<nseg * bps, kMergeThreads, ms, st>>>(ki, vi, seg, nruns, bps, ko, vo);
     } else {
         const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
         if (g > 0) k_merge_runs<K><<<(unsigned)g, 256, 0, st>>>(ki, vi, seg, nseg, nruns, n, ko, vo);

@@ -185,6 +185,7 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_pivots = b.take<unsigned long long>((size_t)p);
     c->d_bnd = b.take<int64_t>((size_t)pl * p);
     c->d_lpre = b.take<int64_t>((size_t)n + pl + 1);
+    c->d_len_sorted = b.take<int64_t>((size_t)n);
     c->d_seg = b.take<int64_t>((size_t)pl * p * 2);
     c->d_counts = b.take<int64_t>((size_t)pl * p * 2);
     c->tc_tiles_cap = tc_tiles_bound(n, pl);
@@ -1066,10 +1067,16 @@ static int rank_global_impl(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_sam
         CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
                       qbits + sbits));
     LAUNCHED();
-    launch_unpack_sorted(ctx->d_ckey_sorted, ctx->d_perm_sorted, ctx->d_shard_base, ctx->pl, ctx->d_off, ctx->n,
-                         ctx->first_idx, ctx->d_key_sorted, ctx->d_rowinfo, ctx->cfg.k, ctx->d_lpre, qbits, ctx->ibits,
-                         ctx->st);
+    launch_unpack_sorted(ctx->d_ckey_sorted, ctx->d_perm_sorted, ctx->n, ctx->first_idx, ctx->d_key_sorted,
+                         ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, qbits, ctx->ibits, ctx->st);
     LAUNCHED();
+    // exclusive prefix of L in sorted order (the residue offsets of every bucket slice, K12/K13)
+    CK(cudaMemsetAsync(ctx->d_lpre, 0, sizeof(int64_t), ctx->st));
+    {
+        size_t tb2 = ctx->cub_bytes;
+        CK(cub::DeviceScan::InclusiveSum(ctx->d_cub, tb2, ctx->d_len_sorted, ctx->d_lpre + 1, (int)ctx->n, ctx->st));
+        LAUNCHED();
+    }
     if (p > 1) {
         launch_samples(ctx->d_key_sorted, ctx->d_shard_base, ctx->pl, p,
                        reinterpret_cast<unsigned long long *>(d_samples_out), ctx->st);

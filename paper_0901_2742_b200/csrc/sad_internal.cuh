@@ -241,11 +241,9 @@ void launch_rank_vs_ga(const RankArgs &a, cudaStream_t st);
 
 void launch_samples(const unsigned long long *key_sorted, const int64_t *shard_base, int pl, int p,
                     unsigned long long *samples_out, cudaStream_t st);
-// unpack the sorted composite keys into keys (q << ibits) + index and the exclusive prefix of L in
-// sorted order over all local shards (lpre [n + 1]); one block per shard
-void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, const int64_t *shard_base,
-                          int pl, const int64_t *off, int64_t n, int64_t first_idx, unsigned long long *key_sorted,
-                          const RowInfo *rowinfo, int k, int64_t *lpre, int qbits, int ibits, cudaStream_t st);
+void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, int64_t n,
+                          int64_t first_idx, unsigned long long *key_sorted, const RowInfo *rowinfo, int k,
+                          int64_t *len_sorted, int qbits, int ibits, cudaStream_t st);
 // f1: rank against the k*p gathered samples
 void launch_tkeys(const unsigned long long *T, const RowInfo *rowinfo, int64_t n, unsigned long long *keys,
                   int32_t *rows, cudaStream_t st);
@@ -440,6 +438,7 @@ struct sad_ctx {
     int32_t *d_perm_in = nullptr, *d_perm_sorted = nullptr;
     unsigned long long *d_pivots = nullptr;
     int64_t *d_bnd = nullptr, *d_lpre = nullptr, *d_seg = nullptr, *d_counts = nullptr;
+    int64_t *d_len_sorted = nullptr;  // [n] L of each sequence in sorted order (scanned into d_lpre)
     bool counts_pending = false;
     void *d_tmap = nullptr;
     void *d_cub = nullptr;
