@@ -10,6 +10,7 @@ import os
 
 import numpy as np
 import pytest
+from fractions import Fraction
 
 import oracle
 from synth import gen
@@ -386,3 +387,55 @@ def test_upgma_vs_scipy_average_linkage():
         assert [sorted(r) for r in m.tolist()] == [sorted(map(int, r)) for r in Z[:, :2]]
         assert s.tolist() == Z[:, 3].astype(int).tolist()
         assert np.all(np.diff(h) >= -1e-15)                       # ultrametric: heights never decrease
+
+
+# ---------------------------------------------------------------- the oracle's sampled checkers
+
+@pytest.mark.parametrize("alpha,k", [("protein", 3), ("dna", 2), ("dna", 6)])
+@pytest.mark.parametrize("p", [1, 2, 3, 8])
+def test_sampled_checkers_vs_bruteforce(alpha, k, p):
+    """or_rows_T (T_i of selected rows, O4 for one row, PAPER.md:44-46 with reading A5),
+    or_rank_vs_set (f1's T' against an arbitrary reference set, reading A27) and or_pairs_S
+    (S, den of arbitrary pairs, PAPER.md:42) are the checkers of the full-size sampled GPU tests;
+    pinned here to the Counter + Fraction brute force, not to oracle.run."""
+    rng = np.random.default_rng(31000 + 100 * p + 10 * k + len(alpha))
+    for trial in range(2):
+        n = int(rng.integers(max(p, 2) * 3, 40))
+        if trial == 0:
+            a, o = gen.random_set(rng, n, alpha, k, 50)
+        else:
+            spec = gen.Spec("t", n, alpha, k, p, 2, "equal", 0.0, ("normal", 30, 10, max(k, 8), 60),
+                            (0.05, 0.3), 0.05, int(rng.integers(1 << 30)))
+            a, o = gen.generate(spec)
+        seqs = gen.to_strings(a, o)
+        sh = bf.shards(n, p)
+        T = [0] * n
+        for s in sh:
+            for i in s:
+                T[i] = sum(bf.fixed(bf.F(seqs[i], seqs[j], k)) for j in s)
+        rows = sorted(set(rng.integers(0, n, 7).tolist()) | {0, n - 1})
+        assert [int(t) for t in oracle.rows_T(a, o, k, p, rows)] == [T[r] for r in rows]
+        ref = rng.integers(0, n, 5).tolist()
+        want = [sum(bf.fixed(bf.F(seqs[i], seqs[t], k)) for t in ref) for i in range(n)]
+        assert [int(t) for t in oracle.rank_vs_set(a, o, k, ref)] == want
+        pi, pj = rng.integers(0, n, 25), rng.integers(0, n, 25)
+        S, d = oracle.pairs_S(a, o, k, pi, pj)
+        for x, y, s_, d_ in zip(pi, pj, S, d):
+            f = bf.F(seqs[x], seqs[y], k)
+            assert int(s_) == bf.S(seqs[x], seqs[y], k)
+            assert int(d_) == min(len(seqs[x]), len(seqs[y])) - k + 1
+            assert Fraction(int(s_), int(d_)) == f
+
+
+def test_long_sequences_near_the_key_bound():
+    """Sequences with L - k + 1 up to 65 535 (the ABI's SAD_E_TOO_LONG bound, DESIGN A.3): S near
+    2^16, checked against closed forms. All-'A' DNA of length L has one k-mer of count L - k + 1,
+    so S(x, y) = min(L_x, L_y) - k + 1 and F = 1; a periodic sequence (ACGT)^m has
+    four k-mers (k = 3), none of them AAA."""
+    k = 3
+    Ls = [65537, 65537, 60000, 40001]
+    seqs = ["A" * L for L in Ls] + ["ACGT" * 16384 + "A"]
+    a, o = gen.from_strings(seqs)
+    S, d = oracle.pairs_S(a, o, k, [0, 0, 1, 2, 3, 4, 4], [1, 2, 2, 3, 0, 4, 0])
+    assert S.tolist() == [65535, 59998, 59998, 39999, 39999, 65535, 0]
+    assert d.tolist() == [65535, 59998, 59998, 39999, 39999, 65535, 65535]
