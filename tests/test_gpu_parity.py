@@ -436,3 +436,67 @@ def test_tile_edges(kernel):
         ctx, sizes = _run_gpu(a, o, "protein", 3, p, kernel)
         r = oracle.run(a, o, "protein", 3, p)
         _compare_full(ctx, sizes, r, a, o, p)
+
+
+@pytest.mark.parametrize("kernel", [k for k in KERNELS if k != "alu"])
+def test_long_k_deep_ring(kernel):
+    """Operand rows of 64+ K blocks (16 384+ fp4 columns) in a shard: the all-pairs launch of the
+    CTA-pair fp4 kernel then takes the 5-stage / 1-excess-buffer ring (k_allpairs_tc.cu,
+    SAD_TC_DEEP_KB), chosen from the K of the previous step of the same context. DNA k = 7
+    (V = 16 384, every k-mer present), random and family sequences of ~1.5-3.5 kb, p = 1 and 2.
+    Two steps per context, each compared element-wise with the oracle."""
+    rng = np.random.default_rng(77)
+    seqs = ["".join(rng.choice(list("ACGT"), int(rng.integers(1500, 3500)))) for _ in range(420)]
+    for _ in range(30):                                          # families: near-identical pairs
+        base = seqs[int(rng.integers(0, len(seqs)))]
+        x = list(base)
+        for j in rng.integers(0, len(x), len(x) // 20):
+            x[j] = "ACGT"[int(rng.integers(0, 4))]
+        seqs.append("".join(x))
+    seqs = [seqs[i] for i in rng.permutation(len(seqs))]
+    a, o = gen.from_strings(seqs)
+    for p in (1, 2):
+        r = oracle.run(a, o, "dna", 7, p)
+        ctx = _ctx("dna", 7, p, kernel)
+        ctx.load(a, o, len(o) - 1, 0)
+        for step in range(2):
+            sizes = ctx.run()
+            _compare_full(ctx, sizes, r, a, o, p)
+        K = ctx.profile_info()[2]
+        assert int(K.max()) >= 64 * 256, K
+        ctx.close()
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_similarity_near_the_fp32_bound(kernel):
+    """S up to 65 535 = the ABI's L - k + 1 bound (SAD_E_TOO_LONG), where the fp32 accumulators
+    of the fp4 kernel must still be exact (S < 2^24) and the u16 lanes of the ALU kernel do not
+    wrap: all-'A' sequences (one k-mer of count L - k + 1, no layer cap possible, K grows past the
+    initial operand capacity -> SAD_E_REPLAN and a rerun), random DNA of 65 537 residues and
+    mutated copies of it (S ~ 6e4 over 64 k-mers), next to short sequences."""
+    rng = np.random.default_rng(65535)
+    big = "".join(rng.choice(list("ACGT"), 65537))
+    seqs = ["A" * 65537, "A" * 65537, "A" * 65000, big, big]
+    for rate in (0.01, 0.05, 0.2):
+        x = list(big)
+        for j in rng.integers(0, len(x), int(rate * len(x))):
+            x[j] = "ACGT"[int(rng.integers(0, 4))]
+        seqs.append("".join(x))
+    seqs += ["".join(rng.choice(list("ACGT"), int(rng.integers(3, 3000)))) for _ in range(40)]
+    seqs = [seqs[i] for i in rng.permutation(len(seqs))]
+    a, o = gen.from_strings(seqs)
+    for p in (1, 2):
+        ctx, sizes = _run_gpu(a, o, "dna", 3, p, kernel, keep_sim=True)
+        r = oracle.run(a, o, "dna", 3, p)
+        _compare_full(ctx, sizes, r, a, o, p)
+        n = len(o) - 1
+        sb = gen.shard_bounds(n, p)
+        smax = 0
+        for s in range(p):
+            Sm = ctx.similarity(s)
+            ii, jj = np.meshgrid(np.arange(sb[s], sb[s + 1]), np.arange(sb[s], sb[s + 1]), indexing="ij")
+            Sref, _ = oracle.pairs_S(a, o, 3, ii.ravel(), jj.ravel())
+            assert np.array_equal(Sm.ravel().astype(np.int64), Sref)
+            smax = max(smax, int(Sref.max()))
+        assert smax == 65535
+        ctx.close()
