@@ -3,6 +3,7 @@
 // PAPER.md:40-44 (§2 "k-mer Rank"): "A k-mer is a contiguous subsequence of length k ...
 // nx_i(tau) ... the number of times tau occurs in x_i". A window of residue codes
 // c_0..c_{k-1} is numbered tau = sum_m c_m A^(k-1-m), so tau order is lexicographic order.
+#include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
@@ -195,14 +196,18 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
                     const uint32_t c2 = lut[(qw[i] >> 16) & 0xFFu], c3 = lut[qw[i] >> 24];
                     cw[i] = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
                 }
-                // bytes [lo, hi) of this vector belong to the segment
+                // bytes [lo, hi) of this vector belong to the segment; the masks are only needed when
+                // some byte of the vector is outside the alphabet (bit 7 of its LUT entry)
                 const int lo = max(0, sh - u), hi = min(16, nb - u);
-                uint32_t bad = 0;
+                uint32_t bad = (cw[0] | cw[1] | cw[2] | cw[3]) & 0x80808080u;
+                if (bad) {
+                    bad = 0;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int l = min(max(lo - 4 * i, 0), 4), h = min(max(hi - 4 * i, 0), 4);
-                    const uint32_t m = h > l ? ((0xFFFFFFFFu >> (32 - 8 * (h - l))) << (8 * l)) : 0u;
-                    bad |= cw[i] & m & 0x80808080u;
+                    for (int i = 0; i < 4; ++i) {
+                        const int l = min(max(lo - 4 * i, 0), 4), h = min(max(hi - 4 * i, 0), 4);
+                        const uint32_t m = h > l ? ((0xFFFFFFFFu >> (32 - 8 * (h - l))) << (8 * l)) : 0u;
+                        bad |= cw[i] & m & 0x80808080u;
+                    }
                 }
                 if (bad) {                                   // rare: report the first bad residue, code it 0
 #pragma unroll
@@ -320,9 +325,46 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         stage(0);
         const int lofs = (sh + (int)min(L, (int64_t)kCodeSeg) + 15) & ~15;
         uint16_t *lst = (nseg == 1 && (kCodeBuf - lofs) / 2 >= Tw) ? reinterpret_cast<uint16_t *>(cod + lofs) : nullptr;
-        if (!count(kBinBits, 0u, (uint32_t)V, lst)) {
-            if (lst) {
-                bk = nl;                               // d is known: the two groups meet exactly
+        bool narrow_ovf;
+        bool fast = false;
+        if constexpr (kBinBits == 8) fast = lst != nullptr;
+        if (fast) {
+            // The common case, specialised: one segment, byte bins over all V k-mers, the owner list.
+            // Counting: one shared-memory atomic per window; a bin's first window (old count 0) appends
+            // its k-mer to the owner list. Emission: every owner once (its count c >= 1 read and its
+            // bin cleared), one ballot per 32 owners: count >= 2 entries from the front, count-1
+            // entries from the back of the row's d slots (d = nl), meeting exactly.
+            uint8_t *hb = reinterpret_cast<uint8_t *>(hist);
+            const int w1 = (int)Tw;
+            const uint32_t lt = (1u << lane) - 1u;
+            bool ovf = false;
+            for (int t0 = 0; t0 < w1; t0 += 32 * kCountUnroll) {
+                bool first[kCountUnroll];
+                uint32_t tau[kCountUnroll];
+#pragma unroll
+                for (int u = 0; u < kCountUnroll; ++u) {
+                    const int t = t0 + 32 * u + lane;
+                    first[u] = false;
+                    tau[u] = 0;
+                    if (t < w1) {
+                        tau[u] = window_tau<KT>(cod + sh + t, k, A);
+                        const uint32_t sh8 = (tau[u] & 3u) << 3;
+                        const uint32_t ob = (atomicAdd(&hist[tau[u] >> 2], 1u << sh8) >> sh8) & 0xFFu;
+                        ovf |= ob == 0xFFu;
+                        first[u] = ob == 0u;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kCountUnroll; ++u) {
+                    const uint32_t fm = __ballot_sync(0xffffffffu, first[u]);
+                    if (first[u]) lst[nl + __popc(fm & lt)] = (uint16_t)tau[u];
+                    nl += __popc(fm);
+                }
+            }
+            __syncwarp();
+            narrow_ovf = __any_sync(0xffffffffu, ovf);
+            if (!narrow_ovf) {
+                bk = nl;
                 for (int e0 = 0; e0 < nl; e0 += 32 * kCountUnroll) {
                     uint32_t c[kCountUnroll], tau[kCountUnroll];
 #pragma unroll
@@ -332,26 +374,66 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
                         tau[u] = 0;
                         if (e < nl) {
                             tau[u] = lst[e];
-                            if constexpr (kBinBits == 8) {       // byte bins: read the count and clear it
-                                c[u] = reinterpret_cast<uint8_t *>(hist)[tau[u]];
-                                reinterpret_cast<uint8_t *>(hist)[tau[u]] = 0;
-                            } else {
-                                c[u] = (hist[tau[u] / kBinsPerWord] >> (kBinBits * (tau[u] % kBinsPerWord))) & kBinMax;
-                            }
+                            c[u] = hb[tau[u]];
+                            hb[tau[u]] = 0;
                         }
                     }
 #pragma unroll
-                    for (int u = 0; u < kCountUnroll; ++u) emit(c[u], tau[u]);
+                    for (int u = 0; u < kCountUnroll; ++u) {
+                        const int nv = min(32, nl - (e0 + 32 * u));   // valid lanes: a prefix of the warp
+                        if (nv <= 0) break;
+                        const uint32_t mh = __ballot_sync(0xffffffffu, c[u] >= 2u);
+                        const uint32_t hr = __popc(mh & lt);
+                        if (c[u]) {
+                            const uint32_t slot = c[u] >= 2u ? n_hi + hr : bk - 1u - n_lo - ((uint32_t)lane - hr);
+                            out[slot] = (tau[u] << 16) | c[u];
+                            atomicOr(&pres[tau[u] >> 5], 1u << (tau[u] & 31));
+                        }
+                        const uint32_t nh = __popc(mh);
+                        n_hi += nh;
+                        n_lo += (uint32_t)nv - nh;
+                        if (mh && c[u] >= 2u) {                 // excess beyond the layer caps 1, 2, 4, 8
+                            atomicMax(&Ms[tau[u]], c[u]);
+#pragma unroll
+                            for (int j = 0; j < kNumCaps; ++j)
+                                if (c[u] > (1u << j)) {
+                                    ex[j] += c[u] - (1u << j);
+                                    atomicAdd(&xcs[(uint32_t)j * (uint32_t)V + tau[u]], 1u);
+                                }
+                        }
+                    }
                 }
                 __syncwarp();
-                if constexpr (kBinBits != 8) {
-                    for (int t = lane; t < hw / 4; t += 32) reinterpret_cast<uint4 *>(hist)[t] = make_uint4(0, 0, 0, 0);
-                    __syncwarp();
-                }
-            } else {
-                claim(kBinBits, 0u, (uint32_t)V);
             }
         } else {
+            narrow_ovf = count(kBinBits, 0u, (uint32_t)V, lst);
+            if (!narrow_ovf) {
+                if (lst) {
+                    bk = nl;                               // d is known: the two groups meet exactly
+                    for (int e0 = 0; e0 < nl; e0 += 32 * kCountUnroll) {
+                        uint32_t c[kCountUnroll], tau[kCountUnroll];
+#pragma unroll
+                        for (int u = 0; u < kCountUnroll; ++u) {
+                            const int e = e0 + 32 * u + lane;
+                            c[u] = 0;
+                            tau[u] = 0;
+                            if (e < nl) {
+                                tau[u] = lst[e];
+                                c[u] = (hist[tau[u] / kBinsPerWord] >> (kBinBits * (tau[u] % kBinsPerWord))) & kBinMax;
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kCountUnroll; ++u) emit(c[u], tau[u]);
+                    }
+                    __syncwarp();
+                    for (int t = lane; t < hw / 4; t += 32) reinterpret_cast<uint4 *>(hist)[t] = make_uint4(0, 0, 0, 0);
+                    __syncwarp();
+                } else {
+                    claim(kBinBits, 0u, (uint32_t)V);
+                }
+            }
+        }
+        if (narrow_ovf) {
             for (int t = lane; t < hw; t += 32) hist[t] = 0;
             __syncwarp();
             for (uint32_t h = 0; h < (uint32_t)kWidePasses; ++h) {
@@ -366,11 +448,16 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
             const int64_t d = (int64_t)n_hi + n_lo, src0 = d > bk - n_lo ? d : bk - n_lo;
             for (int64_t t = lane; t < bk - src0; t += 32) out[n_hi + t] = out[src0 + t];
         }
-#pragma unroll
-        for (int j = 0; j < kNumCaps; ++j) {
-            uint32_t v = ex[j];
-            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            exm[j] = max(exm[j], v);
+        if (n_hi) {                                     // per-cap excess sums (each <= Tw <= 65535: two per word)
+            uint32_t v0 = ex[0] | (ex[1] << 16), v1 = ex[2] | (ex[3] << 16);
+            for (int o = 16; o; o >>= 1) {
+                v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+                v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+            }
+            exm[0] = max(exm[0], v0 & 0xFFFFu);
+            exm[1] = max(exm[1], v0 >> 16);
+            exm[2] = max(exm[2], v1 & 0xFFFFu);
+            exm[3] = max(exm[3], v1 >> 16);
         }
         if (lane == 0) {
             a.nhi[i] = (int32_t)n_hi;
@@ -510,21 +597,26 @@ void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, const un
 //      tau (min(a,b) = min(min(a,T),min(b,T)) + min((a-T)+,(b-T)+)); the second term
 //      is the sparse excess of K6 (k_excess.cu), whose list offsets are (4) the exclusive scan of
 //      X_{T_s}(tau) (shards without entries above their cap get empty lists).
-constexpr int kScanThreads = 1024;
-__global__ void __launch_bounds__(kScanThreads) k_shard_plan(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc,
-                                                             unsigned long long *kinfo, int V, int allow_cap,
-                                                             int64_t kcap_blocks, int kcpb, uint32_t *cap,
-                                                             uint32_t *xsel, uint32_t *ident, int64_t *kblocks,
-                                                             unsigned long long *status, uint32_t *col0,
-                                                             uint32_t *xoff, unsigned long long *xtot,
-                                                             uint32_t *xcur) {
+// One cluster of kPlanCtas CTAs per shard (distributed shared memory): CTA c owns the k-mers
+// [c V / C, (c + 1) V / C); partial statistics and chunk totals meet in the leader CTA's shared
+// memory, so the whole plan is one launch with every k-mer touched by its own thread.
+constexpr int kScanThreads = 512, kPlanCtas = 8;
+__global__ void __cluster_dims__(kPlanCtas, 1, 1) __launch_bounds__(kScanThreads)
+    k_shard_plan(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int V, int allow_cap,
+                 int64_t kcap_blocks, int kcpb, uint32_t *cap, uint32_t *xsel, uint32_t *ident, int64_t *kblocks,
+                 unsigned long long *status, uint32_t *col0, uint32_t *xoff, unsigned long long *xtot,
+                 uint32_t *xcur) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
     typedef cub::BlockScan<unsigned long long, kScanThreads> Scan;
     constexpr int NV = 3 * kNumCaps + 1;
     __shared__ typename Scan::TempStorage tmp;
-    __shared__ unsigned long long red[NV];
-    __shared__ uint32_t s_T, s_sel;
-    __shared__ unsigned long long s_carry;
-    const int s = blockIdx.x;
+    __shared__ unsigned long long red[NV];          // this CTA's partial statistics
+    __shared__ unsigned long long ctot;             // this CTA's packed chunk total
+    __shared__ uint32_t s_T, s_sel;                 // the decision (leader CTA)
+    const unsigned c = cluster.block_rank();
+    const int s = blockIdx.x / kPlanCtas;
+    const int t0 = (int)(((int64_t)V * c) / kPlanCtas), t1 = (int)(((int64_t)V * (c + 1)) / kPlanCtas);
     uint32_t *m = M + (size_t)s * V;
     const uint32_t *xc = Xc + (size_t)s * kNumCaps * V;
     const uint32_t *mb = Mb + (size_t)s * ((V + 31) / 32);
@@ -532,7 +624,7 @@ __global__ void __launch_bounds__(kScanThreads) k_shard_plan(uint32_t *M, const 
     if (threadIdx.x < NV) red[threadIdx.x] = 0;
     __syncthreads();
     unsigned long long acc[NV] = {};
-    for (int t = threadIdx.x; t < V; t += kScanThreads) {   // (1), coalesced
+    for (int t = t0 + (int)threadIdx.x; t < t1; t += kScanThreads) {   // (1), coalesced
         uint32_t x = m[t];
         if (x == 0 && ((mb[t >> 5] >> (t & 31)) & 1u)) {
             x = 1;
@@ -542,10 +634,11 @@ __global__ void __launch_bounds__(kScanThreads) k_shard_plan(uint32_t *M, const 
 #pragma unroll
         for (int j = 0; j < kNumCaps; ++j) {
             acc[j] += min(x, 1u << j);
-            const unsigned long long c = xc[(size_t)j * V + t];
-            acc[kNumCaps + 1 + j] += c * (c - (c ? 1 : 0)) / 2;
-            acc[2 * kNumCaps + 1 + j] += c;
+            const unsigned long long cc = xc[(size_t)j * V + t];
+            acc[kNumCaps + 1 + j] += cc * (cc - (cc ? 1 : 0)) / 2;
+            acc[2 * kNumCaps + 1 + j] += cc;
         }
+        xcur[(size_t)s * V + t] = 0u;                                 // K6 list cursors
     }
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
@@ -553,13 +646,19 @@ __global__ void __launch_bounds__(kScanThreads) k_shard_plan(uint32_t *M, const 
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if ((threadIdx.x & 31) == 0 && v) atomicAdd(&red[j], v);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {                               // (2)
-        ki[2] = red[kNumCaps];
+    cluster.sync();                                   // every CTA's partials (and M folds) are in place
+    if (c == 0 && threadIdx.x == 0) {                 // (2) in the leader
+        unsigned long long tot[NV] = {};
+        for (unsigned r = 0; r < kPlanCtas; ++r) {
+            const unsigned long long *rr = cluster.map_shared_rank(red, r);
+#pragma unroll
+            for (int j = 0; j < NV; ++j) tot[j] += rr[j];
+        }
+        ki[2] = tot[kNumCaps];
         for (int j = 0; j < kNumCaps; ++j) {
-            ki[8 + j] = red[j];
-            ki[12 + j] = red[kNumCaps + 1 + j];
-            ki[16 + j] = red[2 * kNumCaps + 1 + j];
+            ki[8 + j] = tot[j];
+            ki[12 + j] = tot[kNumCaps + 1 + j];
+            ki[16 + j] = tot[2 * kNumCaps + 1 + j];
         }
         unsigned long long K = ki[2];
         uint32_t T = kNoCap, sel = (uint32_t)kNumCaps;
@@ -586,51 +685,46 @@ __global__ void __launch_bounds__(kScanThreads) k_shard_plan(uint32_t *M, const 
         atomicMax(&status[1], K);
         s_T = T;
         s_sel = sel;
-        s_carry = 0;
     }
-    __syncthreads();
-    const uint32_t T = s_T, sel = s_sel;
-    for (int t = threadIdx.x; t < V; t += kScanThreads) xcur[(size_t)s * V + t] = 0u;   // K6 list cursors
-    // (3) and (4): exclusive scans in chunks of kScanThreads consecutive k-mers (coalesced), with a carry
-    uint32_t *c = col0 + (size_t)s * V;
-    for (int c0 = 0; c0 < V; c0 += kScanThreads) {
-        const int t = c0 + threadIdx.x;
-        const unsigned long long v = t < V ? min(m[t], T) : 0u;
-        unsigned long long ex, tot;
-        Scan(tmp).ExclusiveSum(v, ex, tot);
-        if (t < V) c[t] = (uint32_t)(s_carry + ex);
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry += tot;
-        __syncthreads();
+    cluster.sync();
+    const uint32_t T = *cluster.map_shared_rank(&s_T, 0), sel = *cluster.map_shared_rank(&s_sel, 0);
+    // (3) and (4) in one scan: every thread owns a contiguous chunk of its CTA's k-mers and scans
+    // the pair (min(M, T_s), X_{T_s}) packed in one u64 (col0 high, list offsets low: a shard's list
+    // entries are < 2^32, the u32 offsets' own bound); CTA totals are carried across the cluster
+    const int C = (t1 - t0 + kScanThreads - 1) / kScanThreads;
+    const int a0 = min(t1, t0 + (int)threadIdx.x * C), a1 = min(t1, a0 + C);
+    const uint32_t *x = sel < (uint32_t)kNumCaps ? xc + (size_t)sel * V : nullptr;
+    unsigned long long loc = 0;
+    for (int t = a0; t < a1; ++t) loc += ((unsigned long long)min(m[t], T) << 32) + (x ? x[t] : 0u);
+    unsigned long long ex, agg;
+    Scan(tmp).ExclusiveSum(loc, ex, agg);
+    if (threadIdx.x == 0) ctot = agg;
+    cluster.sync();
+    unsigned long long carry = 0, all = 0;
+    for (unsigned r = 0; r < kPlanCtas; ++r) {
+        const unsigned long long v = *cluster.map_shared_rank(&ctot, r);
+        if (r < c) carry += v;
+        all += v;
     }
+    uint32_t *cp = col0 + (size_t)s * V;
     uint32_t *xo = xoff + (size_t)s * V;
-    if (sel >= (uint32_t)kNumCaps) {
-        for (int t = threadIdx.x; t < V; t += kScanThreads) xo[t] = 0;
-        if (threadIdx.x == 0) xtot[s] = 0;
-        return;
+    uint32_t ch = (uint32_t)((carry + ex) >> 32), cl = (uint32_t)(carry + ex);
+    for (int t = a0; t < a1; ++t) {
+        cp[t] = ch;
+        xo[t] = cl;
+        ch += min(m[t], T);
+        cl += x ? x[t] : 0u;
     }
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    const uint32_t *x = xc + (size_t)sel * V;
-    for (int c0 = 0; c0 < V; c0 += kScanThreads) {
-        const int t = c0 + threadIdx.x;
-        const unsigned long long v = t < V ? x[t] : 0u;
-        unsigned long long ex, tot;
-        Scan(tmp).ExclusiveSum(v, ex, tot);
-        if (t < V) xo[t] = (uint32_t)(s_carry + ex);
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry += tot;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) xtot[s] = s_carry;
+    if (c == 0 && threadIdx.x == 0) xtot[s] = x ? (unsigned long long)(uint32_t)all : 0ull;
+    cluster.sync();                                   // no CTA leaves while its shared memory is read
 }
 
 void launch_shard_plan(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,
                        int allow_cap, int64_t kcap_blocks, int kcpb, uint32_t *cap, uint32_t *xsel, uint32_t *ident,
                        int64_t *kblocks, unsigned long long *status, uint32_t *col0, uint32_t *xoff,
                        unsigned long long *xtot, uint32_t *xcur, cudaStream_t st) {
-    k_shard_plan<<<pl, kScanThreads, 0, st>>>(M, Mb, Xc, kinfo, V, allow_cap, kcap_blocks, kcpb, cap, xsel, ident,
-                                              kblocks, status, col0, xoff, xtot, xcur);
+    k_shard_plan<<<pl * kPlanCtas, kScanThreads, 0, st>>>(M, Mb, Xc, kinfo, V, allow_cap, kcap_blocks, kcpb, cap,
+                                                          xsel, ident, kblocks, status, col0, xoff, xtot, xcur);
 }
 
 __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl, int64_t r) {
