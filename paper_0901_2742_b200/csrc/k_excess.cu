@@ -36,7 +36,7 @@ constexpr int kXrWarps = 8;
 #endif
 
 // K6 lists: every entry above its shard's cap goes to L_tau as (row << 8) | (n - T_s), one warp
-// per row over the row's leading count >= 2 entries (positions from per-(shard, tau) cursors)
+// per row over the row's count >= 2 entries (its CSR tail; positions from per-(shard, tau) cursors)
 __global__ void __launch_bounds__(256) k_xfill(ExcessArgs a, uint32_t *xcur) {
     __shared__ unsigned long long lbase[kMaxLocalShards + 1];
     if (blockIdx.x == 0 && threadIdx.x < 16 && a.zero_seg)
@@ -56,8 +56,8 @@ __global__ void __launch_bounds__(256) k_xfill(ExcessArgs a, uint32_t *xcur) {
         while (s + 1 < a.pl && r >= a.shard_base[s + 1]) ++s;
         const uint32_t T = a.cap[s];
         if (T == kNoCap) continue;
-        const int dh = a.nhi[r];
-        const uint32_t *ent = a.csr + (a.off[r] - r * (int64_t)(a.k - 1));
+        const int dh = a.nhi[r];                  // the count >= 2 entries: the row's CSR tail
+        const uint32_t *ent = a.csr + (a.off[r + 1] - (r + 1) * (int64_t)(a.k - 1)) - dh;
         const uint32_t local = (uint32_t)a.sigma_inv[r];      // the row's position in length order
         for (int e = lane; e < dh; e += 32) {
             const uint32_t v = ent[e], n = v & 0xFFFFu;
@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows(ExcessArgs a, int warps
         const int64_t w = a.shard_base[s + 1] - a.shard_base[s];
         uint32_t distinct = 0;
         if (T != kNoCap) {
-            const uint32_t *ent = a.csr + (a.off[i] - i * (int64_t)(a.k - 1));
-            const int d = a.nhi[i];               // the row's count >= 2 entries lead its CSR
+            const int d = a.nhi[i];               // the row's count >= 2 entries: its CSR tail
+            const uint32_t *ent = a.csr + (a.off[i + 1] - (i + 1) * (int64_t)(a.k - 1)) - d;
             for (int e0 = 0; e0 < d; e0 += 32) {
                 // the batch's excess k-mers: lane-parallel list lookups, then one flattened walk
                 // over the concatenated lists (4 independent loads in flight per lane)
@@ -208,8 +208,8 @@ __global__ void __launch_bounds__(kXrWarps * 32, SAD_XR_MINB) k_xrows_g(ExcessAr
         return a.shard_base[s] + a.sigma[rr];
     };
     i_c = r < a.n ? seq_of(r) : 0;
-    int64_t eo_c = r < a.n ? a.off[i_c] - i_c * (int64_t)(a.k - 1) : 0;
     int d_c = r < a.n ? a.nhi[i_c] : 0;
+    int64_t eo_c = r < a.n ? a.off[i_c + 1] - (i_c + 1) * (int64_t)(a.k - 1) - d_c : 0;   // the CSR tail
     uint32_t v_c = lane < d_c ? a.csr[eo_c + lane] : 0u;
     for (; r < a.n; r += nw) {
         int s = 0;
@@ -259,8 +259,8 @@ __global__ void __launch_bounds__(kXrWarps * 32, SAD_XR_MINB) k_xrows_g(ExcessAr
                 const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
                 __syncwarp();
                 if (e0 == 0 && rn < a.n) {        // step 2 of the next row
-                    eo_n = a.off[i_n] - i_n * (int64_t)(a.k - 1);
                     d_n = a.nhi[i_n];
+                    eo_n = a.off[i_n + 1] - (i_n + 1) * (int64_t)(a.k - 1) - d_n;
                 }
                 int g = 0;
                 for (uint32_t t0 = 0; t0 < tot; t0 += 32 * SAD_XR_BATCH) {
@@ -291,8 +291,8 @@ __global__ void __launch_bounds__(kXrWarps * 32, SAD_XR_MINB) k_xrows_g(ExcessAr
         if (lane == 0) a.xrow[r] = make_uint2(zeroed ? 1u : 0u, 0u);
         if (rn < a.n) {
             if (!d_n && !eo_n) {                  // step 2 not issued above (no hit batch in this row)
-                eo_n = a.off[i_n] - i_n * (int64_t)(a.k - 1);
                 d_n = a.nhi[i_n];
+                eo_n = a.off[i_n + 1] - (i_n + 1) * (int64_t)(a.k - 1) - d_n;
             }
             v_c = lane < d_n ? a.csr[eo_n + lane] : 0u;                  // step 3
         }

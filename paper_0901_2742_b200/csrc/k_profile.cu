@@ -14,19 +14,19 @@ namespace sad {
 
 __constant__ char c_alpha[2][24] = {"ACDEFGHIKLMNPQRSTVWY", "ACGT"};
 
-// K1+K2. One warp per sequence (persistent warps over contiguous runs of sequences, no block
-// barriers), each with its own shared-memory histogram of narrow bins (kBinBits = 4: eight per u32
-// word, so that 32 warps fit an SM; a sequence with a k-mer seen 2^kBinBits - 1 or more times is
-// recounted with u16 bins over 1/kWidePasses of the k-mers at a time, which cannot carry since
-// L-k+1 <= 65535) and a staging buffer of residue codes.
-// Pass 1 validates every residue (K1) and counts every window tau = sum_m c_m A^(k-1-m) (K2).
-// Pass 2 revisits the windows: the first lane to clear a bin with atomicAnd receives its count
-// and emits the distinct entry (tau << 16 | count), so the histogram is left zeroed for the next
-// sequence. The entry list is unordered in tau (no consumer needs tau order: operand rows, GA
-// rank and ancestor records are all sums or scatters over the entries) but grouped: the nhi[i]
-// entries with count >= 2 come first (warp-aggregated appends from the front, count-1 entries
-// from the back, then the gap is closed), so the K6 consumers read only those. Sequences longer
-// than the staging buffer are processed in segments of windows.
+// K1+K2. One warp per sequence (persistent warps over contiguous runs of sequences balanced by
+// residues, no block barriers), each with its own shared-memory histogram of byte bins and a staging
+// buffer of residue codes (a sequence with a k-mer seen 255 or more times is recounted with u16 bins
+// over 1/kWidePasses of the k-mers at a time, which cannot carry since L-k+1 <= 65535).
+// Pass 1 validates every residue (K1) and counts every window tau = sum_m c_m A^(k-1-m) (K2); the
+// first window of every k-mer (its bin was 0) appends it to an owner list.
+// Pass 2 walks the owners: each reads and clears its bin and emits the distinct entry
+// (tau << 16 | count) at its list slot, so the histogram is left zeroed for the next sequence.
+// The entries are unordered in tau (no consumer needs tau order: operand rows, GA rank and
+// ancestor records are all sums or scatters over the entries); the nhi[i] entries with count >= 2
+// are repeated in the row's last slots (free: Tw - d = sum (count - 1) >= nhi), so the K6
+// consumers read only those. Sequences longer than the staging buffer (or whose owner list does
+// not fit beside it) are processed in segments of windows, the bins claimed by atomicAnd.
 #ifndef SAD_PROF_BINBITS
 #define SAD_PROF_BINBITS 8               // bin width of the k-mer histogram (4 or 8 bits)
 #endif
@@ -272,16 +272,16 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         // pass 2: every k-mer once, emit (tau, count), update the shard's column maxima
         uint32_t *out = a.csr + (off0 - i * (int64_t)(k - 1));
         uint32_t *Ms = a.M + (size_t)s * V;
-        uint32_t n_hi = 0, n_lo = 0, ex[kNumCaps] = {};
-        uint32_t bk = (uint32_t)Tw;                       // count-1 entries fill [.., bk) from the back
+        uint32_t n_hi = 0, n_d = 0, ex[kNumCaps] = {};
+        // every distinct entry goes to [0, d); the count >= 2 ones are repeated in the row's tail
+        // [Tw - nhi, Tw), which is free: Tw - d = sum (count - 1) >= nhi
+        const uint32_t lt = (1u << lane) - 1u;
         auto emit = [&](uint32_t c, uint32_t tau) {       // warp-uniform call; c = 0: nothing
-            const uint32_t mh = __ballot_sync(0xffffffffu, c >= 2), ml = __ballot_sync(0xffffffffu, c == 1);
-            const uint32_t lt = (1u << lane) - 1u;
-            // (32-bit slot arithmetic: a row holds at most Tw <= 65535 entries)
-            if (c >= 2) out[n_hi + __popc(mh & lt)] = (tau << 16) | c;
-            else if (c == 1) out[bk - 1u - n_lo - __popc(ml & lt)] = (tau << 16) | 1u;
+            const uint32_t md = __ballot_sync(0xffffffffu, c != 0u), mh = __ballot_sync(0xffffffffu, c >= 2);
+            if (c) out[n_d + __popc(md & lt)] = (tau << 16) | c;
+            if (c >= 2) out[(uint32_t)Tw - 1u - n_hi - __popc(mh & lt)] = (tau << 16) | c;
+            n_d += __popc(md);
             n_hi += __popc(mh);
-            n_lo += __popc(ml);
             if (c) {
                 atomicOr(&pres[tau >> 5], 1u << (tau & 31));
                 if (c >= 2) {                          // excess beyond the layer caps 1, 2, 4, 8
@@ -364,7 +364,6 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
             __syncwarp();
             narrow_ovf = __any_sync(0xffffffffu, ovf);
             if (!narrow_ovf) {
-                bk = nl;
                 for (int e0 = 0; e0 < nl; e0 += 32 * kCountUnroll) {
                     uint32_t c[kCountUnroll], tau[kCountUnroll];
 #pragma unroll
@@ -376,40 +375,35 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
                             tau[u] = lst[e];
                             c[u] = hb[tau[u]];
                             hb[tau[u]] = 0;
+                            out[e] = (tau[u] << 16) | c[u];        // list order: slot = owner index
+                            atomicOr(&pres[tau[u] >> 5], 1u << (tau[u] & 31));
                         }
                     }
 #pragma unroll
                     for (int u = 0; u < kCountUnroll; ++u) {
-                        const int nv = min(32, nl - (e0 + 32 * u));   // valid lanes: a prefix of the warp
-                        if (nv <= 0) break;
                         const uint32_t mh = __ballot_sync(0xffffffffu, c[u] >= 2u);
-                        const uint32_t hr = __popc(mh & lt);
-                        if (c[u]) {
-                            const uint32_t slot = c[u] >= 2u ? n_hi + hr : bk - 1u - n_lo - ((uint32_t)lane - hr);
-                            out[slot] = (tau[u] << 16) | c[u];
-                            atomicOr(&pres[tau[u] >> 5], 1u << (tau[u] & 31));
-                        }
-                        const uint32_t nh = __popc(mh);
-                        n_hi += nh;
-                        n_lo += (uint32_t)nv - nh;
-                        if (mh && c[u] >= 2u) {                 // excess beyond the layer caps 1, 2, 4, 8
-                            atomicMax(&Ms[tau[u]], c[u]);
+                        if (mh) {                                  // rare: the tail copy and the excess statistics
+                            if (c[u] >= 2u) {
+                                out[(uint32_t)Tw - 1u - n_hi - __popc(mh & lt)] = (tau[u] << 16) | c[u];
+                                atomicMax(&Ms[tau[u]], c[u]);
 #pragma unroll
-                            for (int j = 0; j < kNumCaps; ++j)
-                                if (c[u] > (1u << j)) {
-                                    ex[j] += c[u] - (1u << j);
-                                    atomicAdd(&xcs[(uint32_t)j * (uint32_t)V + tau[u]], 1u);
-                                }
+                                for (int j = 0; j < kNumCaps; ++j)
+                                    if (c[u] > (1u << j)) {
+                                        ex[j] += c[u] - (1u << j);
+                                        atomicAdd(&xcs[(uint32_t)j * (uint32_t)V + tau[u]], 1u);
+                                    }
+                            }
+                            n_hi += __popc(mh);
                         }
                     }
                 }
+                n_d = (uint32_t)nl;
                 __syncwarp();
             }
         } else {
             narrow_ovf = count(kBinBits, 0u, (uint32_t)V, lst);
             if (!narrow_ovf) {
                 if (lst) {
-                    bk = nl;                               // d is known: the two groups meet exactly
                     for (int e0 = 0; e0 < nl; e0 += 32 * kCountUnroll) {
                         uint32_t c[kCountUnroll], tau[kCountUnroll];
 #pragma unroll
@@ -442,12 +436,6 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
                 claim(16, lo, hi);
             }
         }
-        // close the gap: [0, n_hi) count >= 2 (the K6 candidates), then [n_hi, d) count 1. Only the
-        // count-1 entries at [max(d, Tw - n_lo), Tw) move, into the gap [n_hi, Tw - n_lo) (disjoint).
-        {
-            const int64_t d = (int64_t)n_hi + n_lo, src0 = d > bk - n_lo ? d : bk - n_lo;
-            for (int64_t t = lane; t < bk - src0; t += 32) out[n_hi + t] = out[src0 + t];
-        }
         if (n_hi) {                                     // per-cap excess sums (each <= Tw <= 65535: two per word)
             uint32_t v0 = ex[0] | (ex[1] << 16), v1 = ex[2] | (ex[3] << 16);
             for (int o = 16; o; o >>= 1) {
@@ -461,14 +449,14 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         }
         if (lane == 0) {
             a.nhi[i] = (int32_t)n_hi;
-            a.dcnt[i] = (int32_t)(n_hi + n_lo);
+            a.dcnt[i] = (int32_t)n_d;
             const uint32_t tw = (uint32_t)Tw;
             a.rowinfo[i] = RowInfo{tw, 0xFFFFFFFFu / tw, 0xFFFFFFFFu % tw + 1u, (uint32_t)s};
             a.T[i] = 0ull;                              // the all-pairs kernel accumulates T_i atomically
         }
         acc_w += (unsigned long long)Tw;
         max_tw = max(max_tw, (unsigned long long)Tw);
-        acc_d += n_hi + n_lo;
+        acc_d += n_d;
         __syncwarp();
     }
     flush();

@@ -5,10 +5,11 @@
 //   ascii   u8  [R]          residues as loaded (the redistribution payload)
 //   off     i64 [n+1]        residue offsets
 //   rowinfo u32x4 [n]        {Tw = L-k+1, Qd = floor((2^32-1)/Tw), Rp = (2^32-1) mod Tw + 1, shard}
-//   csr     u32 [sum Tw]     per sequence, distinct k-mers sorted by tau: (tau << 16) | count;
-//                            sequence i starts at off[i] - i*(k-1)
-//   dcnt    i32 [n]          distinct k-mers per sequence
-//   nhi     i32 [n]          of which count >= 2; those lead the row's CSR entries
+//   csr     u32 [sum Tw]     per sequence i, Tw slots at off[i] - i*(k-1): its d distinct k-mers
+//                            (tau << 16) | count in slots [0, d) (any order), the nhi of them with
+//                            count >= 2 repeated in the last nhi slots (d + nhi <= Tw)
+//   dcnt    i32 [n]          distinct k-mers per sequence (d)
+//   nhi     i32 [n]          of which count >= 2
 //   M/col0  u32 [pl][V]      per shard max count of tau / first operand column of tau
 //   T       u64 [n]          within-shard fixed-point rank sums (reading A5)
 //   key     u64 [n]          (floor(2^32 S/den) << 31) + source_index
@@ -94,7 +95,7 @@ struct ProfileArgs {
     unsigned long long *kinfo;       // [pl][kKinfo] (see kKinfo)
     uint32_t *Xc;                    // [pl][kNumCaps][V]: #{i : n_i(tau) > 2^j} (zeroed)
     uint32_t *Mb;                    // [pl][ceil(V/32)]: k-mers present in the shard (zeroed; M >= 2 goes to M)
-    int32_t *nhi;                    // [n] entries with count >= 2 (they lead each CSR row)
+    int32_t *nhi;                    // [n] entries with count >= 2 (repeated in each CSR row's tail)
     unsigned long long *T;           // [n] within-shard rank sums, zeroed here for the all-pairs kernel
 };
 void launch_profile(const ProfileArgs &a, cudaStream_t st);
@@ -148,7 +149,7 @@ void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, const un
 struct ExcessArgs {
     const uint32_t *csr;
     const int64_t *off;
-    const int32_t *nhi;              // [n] leading count >= 2 entries of each CSR row
+    const int32_t *nhi;              // [n] count >= 2 entries of each CSR row (its last nhi slots)
     const int64_t *shard_base;       // device [pl+1]
     int64_t n;
     int pl, V, k;
