@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
             if (lane == 0) {
                 atomicMin(&a.err[L < k ? 1 : 2], gidx);
                 a.rowinfo[i] = RowInfo{1u, 0xFFFFFFFFu, 1u, (uint32_t)s};
+                if (a.lcnt) atomicAdd(&a.lcnt[(size_t)s * kLenBinsMax + 1], 1u);
                 a.T[i] = 0ull;
                 a.dcnt[i] = 0;
                 a.nhi[i] = 0;
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         // list is at most Tw entries); the emission then walks d owners instead of Tw windows
         stage(0);
         const int lofs = (sh + (int)min(L, (int64_t)kCodeSeg) + 15) & ~15;
-        uint16_t *lst = (nseg == 1 && (kCodeBuf - lofs) / 2 >= Tw) ? reinterpret_cast<uint16_t *>(cod + lofs) : nullptr;
+        uint16_t *lst = (nseg == 1 && (kCodeBuf - lofs) / 2 >= Tw + 1) ? reinterpret_cast<uint16_t *>(cod + lofs) : nullptr;
         bool narrow_ovf;
         bool fast = false;
         if constexpr (kBinBits == 8) fast = lst != nullptr;
@@ -357,7 +358,7 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
 #pragma unroll
                 for (int u = 0; u < kCountUnroll; ++u) {
                     const uint32_t fm = __ballot_sync(0xffffffffu, first[u]);
-                    if (first[u]) lst[nl + __popc(fm & lt)] = (uint16_t)tau[u];
+                    lst[first[u] ? nl + __popc(fm & lt) : (uint32_t)w1] = (uint16_t)tau[u];   // slot Tw: a dummy
                     nl += __popc(fm);
                 }
             }
@@ -380,22 +381,23 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
                         }
                     }
 #pragma unroll
-                    for (int u = 0; u < kCountUnroll; ++u) {
+                    for (int u = 0; u < kCountUnroll; ++u) {   // the count >= 2 entries: the row's tail
                         const uint32_t mh = __ballot_sync(0xffffffffu, c[u] >= 2u);
-                        if (mh) {                                  // rare: the tail copy and the excess statistics
-                            if (c[u] >= 2u) {
-                                out[(uint32_t)Tw - 1u - n_hi - __popc(mh & lt)] = (tau[u] << 16) | c[u];
-                                atomicMax(&Ms[tau[u]], c[u]);
-#pragma unroll
-                                for (int j = 0; j < kNumCaps; ++j)
-                                    if (c[u] > (1u << j)) {
-                                        ex[j] += c[u] - (1u << j);
-                                        atomicAdd(&xcs[(uint32_t)j * (uint32_t)V + tau[u]], 1u);
-                                    }
-                            }
-                            n_hi += __popc(mh);
-                        }
+                        if (c[u] >= 2u) out[(uint32_t)Tw - 1u - n_hi - __popc(mh & lt)] = (tau[u] << 16) | c[u];
+                        n_hi += __popc(mh);
                     }
+                }
+                __syncwarp();
+                // their statistics, all lanes busy: shard maxima, per-cap excess counts and sums
+                for (uint32_t e = lane; e < n_hi; e += 32) {
+                    const uint32_t v = out[(uint32_t)Tw - 1u - e], c = v & 0xFFFFu, tau = v >> 16;
+                    atomicMax(&Ms[tau], c);
+#pragma unroll
+                    for (int j = 0; j < kNumCaps; ++j)
+                        if (c > (1u << j)) {
+                            ex[j] += c - (1u << j);
+                            atomicAdd(&xcs[(uint32_t)j * (uint32_t)V + tau], 1u);
+                        }
                 }
                 n_d = (uint32_t)nl;
                 __syncwarp();
@@ -452,6 +454,7 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
             a.dcnt[i] = (int32_t)n_d;
             const uint32_t tw = (uint32_t)Tw;
             a.rowinfo[i] = RowInfo{tw, 0xFFFFFFFFu / tw, 0xFFFFFFFFu % tw + 1u, (uint32_t)s};
+            if (a.lcnt) atomicAdd(&a.lcnt[(size_t)s * kLenBinsMax + tw], 1u);    // the length order's histogram
             a.T[i] = 0ull;                              // the all-pairs kernel accumulates T_i atomically
         }
         acc_w += (unsigned long long)Tw;
@@ -463,8 +466,10 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
 }
 
 __global__ void k_profile_reset(uint32_t *M, size_t nM, uint32_t *Mb, size_t nMb, uint32_t *Xc, size_t nXc,
-                                unsigned long long *err4, unsigned long long *statkinfo, size_t nsk) {
+                                unsigned long long *err4, unsigned long long *statkinfo, size_t nsk, uint32_t *lcnt,
+                                size_t nl) {
     const size_t stride = (size_t)gridDim.x * blockDim.x, t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (size_t t = t0; t < nl / 4; t += stride) reinterpret_cast<uint4 *>(lcnt)[t] = make_uint4(0, 0, 0, 0);
     for (size_t t = t0; t < nM; t += stride) M[t] = 0u;
     for (size_t t = t0; t < nMb; t += stride) Mb[t] = 0u;
     for (size_t t = t0; t < nXc; t += stride) Xc[t] = 0u;
@@ -473,10 +478,11 @@ __global__ void k_profile_reset(uint32_t *M, size_t nM, uint32_t *Mb, size_t nMb
 }
 
 void launch_profile_reset(uint32_t *M, size_t nM, uint32_t *Mb, size_t nMb, uint32_t *Xc, size_t nXc,
-                          unsigned long long *err4, unsigned long long *statkinfo, size_t nsk, cudaStream_t st) {
-    const size_t big = std::max(std::max(nM, nXc), std::max(nMb, nsk));
+                          unsigned long long *err4, unsigned long long *statkinfo, size_t nsk, uint32_t *lcnt,
+                          size_t nl, cudaStream_t st) {
+    const size_t big = std::max(std::max(std::max(nM, nXc), std::max(nMb, nsk)), nl / 4);
     const int64_t g = std::max<int64_t>(1, std::min<int64_t>(1024, (int64_t)((big + 255) / 256)));
-    k_profile_reset<<<(unsigned)g, 256, 0, st>>>(M, nM, Mb, nMb, Xc, nXc, err4, statkinfo, nsk);
+    k_profile_reset<<<(unsigned)g, 256, 0, st>>>(M, nM, Mb, nMb, Xc, nXc, err4, statkinfo, nsk, lcnt, lcnt ? nl : 0);
 }
 
 void launch_profile(const ProfileArgs &a, cudaStream_t st) {
@@ -502,44 +508,12 @@ void launch_profile(const ProfileArgs &a, cudaStream_t st) {
 
 // Length order of every shard (the all-pairs kernel works on rows sorted by L - k + 1, so that
 // in a tile strictly above the diagonal every pair's denominator min(L_i, L_j) - k + 1 is the
-// row's own), by counting: per-shard histogram of Tw, one exclusive scan over [shard][Tw] (which
-// gives global sorted positions directly: shards are contiguous), then every sequence takes the next
-// slot of its bin -> sigma (sorted position -> local index), its inverse, and the sorted RowInfo
-// with .shard replaced by the local index. Rows of equal Tw land in arbitrary order: nothing
-// downstream depends on it (T and S are permutation invariant; K5 only needs Tw non-decreasing
-// along every shard, K6 only a consistent order).
-__global__ void k_lenhist(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *cnt) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        int s = 0;
-        while (s + 1 < pl && i >= shard_base[s + 1]) ++s;
-        atomicAdd(&cnt[(size_t)s * kLenBinsMax + rowinfo[i].tw], 1u);     // Tw <= 65535 (K1/K2)
-    }
-}
-
-// one block per shard: exclusive scan of the shard's bins 0..max Tw (max Tw from K1/K2 in kinfo[3],
-// read on the device so that no host decision is needed), offset by the shard's first row
-__global__ void __launch_bounds__(1024) k_lenscan(const uint32_t *cnt, const unsigned long long *kinfo,
-                                                   const int64_t *shard_base, uint32_t *pos) {
-    using BS = cub::BlockScan<uint32_t, 1024>;
-    __shared__ typename BS::TempStorage tmp;
-    __shared__ uint32_t carry;
-    const int s = blockIdx.x;
-    const unsigned long long mt = kinfo[(size_t)s * kKinfo + 3];
-    const int nb = (int)(mt + 1 < (unsigned long long)kLenBinsMax ? mt + 1 : (unsigned long long)kLenBinsMax);
-    if (threadIdx.x == 0) carry = (uint32_t)shard_base[s];
-    __syncthreads();
-    for (int b0 = 0; b0 < nb; b0 += 1024) {
-        const int b = b0 + threadIdx.x;
-        const uint32_t v = b < nb ? cnt[(size_t)s * kLenBinsMax + b] : 0u;
-        uint32_t ex, tot;
-        BS(tmp).ExclusiveSum(v, ex, tot);
-        if (b < nb) pos[(size_t)s * kLenBinsMax + b] = carry + ex;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += tot;
-        __syncthreads();
-    }
-}
-
+// row's own), by counting: per-shard histogram of Tw (K1/K2), one exclusive scan over [shard][Tw]
+// (k_shard_plan; it gives global sorted positions directly: shards are contiguous), then every
+// sequence takes the next slot of its bin -> sigma (sorted position -> local index), its inverse,
+// and the sorted RowInfo with .shard replaced by the local index. Rows of equal Tw land in
+// arbitrary order: nothing downstream depends on it (T and S are permutation invariant; K5 only
+// needs Tw non-decreasing along every shard, K6 only a consistent order).
 __global__ void k_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *pos,
                              int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -556,17 +530,12 @@ __global__ void k_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, 
     }
 }
 
-void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, const unsigned long long *kinfo, int pl,
-                     int64_t n, uint32_t *cnt, uint32_t *pos, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s,
-                     cudaStream_t st) {
+void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *pos,
+                     int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s, cudaStream_t st) {
     const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
     if (g <= 0) return;
-    cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)pl * kLenBinsMax, st);
-    k_lenhist<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, cnt);
-    k_lenscan<<<pl, 1024, 0, st>>>(cnt, kinfo, shard_base, pos);
     k_lenscatter<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, pos, sigma, sigma_inv, rinfo_s);
 }
-
 
 // K3, one block per shard, everything between the k-mer counts and the operand in one launch
 // (no host round trip):
@@ -593,7 +562,7 @@ __global__ void __cluster_dims__(kPlanCtas, 1, 1) __launch_bounds__(kScanThreads
     k_shard_plan(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int V, int allow_cap,
                  int64_t kcap_blocks, int kcpb, uint32_t *cap, uint32_t *xsel, uint32_t *ident, int64_t *kblocks,
                  unsigned long long *status, uint32_t *col0, uint32_t *xoff, unsigned long long *xtot,
-                 uint32_t *xcur) {
+                 uint32_t *xcur, const uint32_t *lcnt, uint32_t *lpos, const int64_t *shard_base) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     typedef cub::BlockScan<unsigned long long, kScanThreads> Scan;
@@ -704,15 +673,36 @@ __global__ void __cluster_dims__(kPlanCtas, 1, 1) __launch_bounds__(kScanThreads
         cl += x ? x[t] : 0u;
     }
     if (c == 0 && threadIdx.x == 0) xtot[s] = x ? (unsigned long long)(uint32_t)all : 0ull;
+    if (lcnt && c == kPlanCtas - 1) {
+        // the length order's bin offsets: exclusive scan of the shard's Tw histogram over bins
+        // 0..max Tw (kinfo[3], from K1/K2), offset by the shard's first row
+        __syncthreads();                              // tmp of the scan above is reused
+        const unsigned long long mt = ki[3];
+        const int nb = (int)(mt + 1 < (unsigned long long)kLenBinsMax ? mt + 1 : (unsigned long long)kLenBinsMax);
+        const uint32_t *lc = lcnt + (size_t)s * kLenBinsMax;
+        uint32_t *lp = lpos + (size_t)s * kLenBinsMax;
+        unsigned long long lcarry = (unsigned long long)shard_base[s];
+        for (int b0 = 0; b0 < nb; b0 += kScanThreads) {
+            const int b = b0 + (int)threadIdx.x;
+            const unsigned long long v = b < nb ? lc[b] : 0u;
+            unsigned long long e2, a2;
+            Scan(tmp).ExclusiveSum(v, e2, a2);
+            if (b < nb) lp[b] = (uint32_t)(lcarry + e2);
+            lcarry += a2;
+            __syncthreads();
+        }
+    }
     cluster.sync();                                   // no CTA leaves while its shared memory is read
 }
 
 void launch_shard_plan(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,
                        int allow_cap, int64_t kcap_blocks, int kcpb, uint32_t *cap, uint32_t *xsel, uint32_t *ident,
                        int64_t *kblocks, unsigned long long *status, uint32_t *col0, uint32_t *xoff,
-                       unsigned long long *xtot, uint32_t *xcur, cudaStream_t st) {
+                       unsigned long long *xtot, uint32_t *xcur, const uint32_t *lcnt, uint32_t *lpos,
+                       const int64_t *shard_base, cudaStream_t st) {
     k_shard_plan<<<pl * kPlanCtas, kScanThreads, 0, st>>>(M, Mb, Xc, kinfo, V, allow_cap, kcap_blocks, kcpb, cap,
-                                                          xsel, ident, kblocks, status, col0, xoff, xtot, xcur);
+                                                          xsel, ident, kblocks, status, col0, xoff, xtot, xcur,
+                                                          lcnt, lpos, shard_base);
 }
 
 __device__ __forceinline__ int shard_of_padded_row(const int64_t *rowpad, int pl, int64_t r) {

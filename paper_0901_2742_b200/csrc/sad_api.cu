@@ -741,7 +741,8 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
 static int profile_reset(sad_ctx *ctx) {
     const int pl = ctx->pl, V = ctx->V;
     launch_profile_reset(ctx->d_M, (size_t)pl * V, ctx->d_Mb, (size_t)pl * ((V + 31) / 32), ctx->d_Xc,
-                         (size_t)kNumCaps * pl * V, ctx->d_err, ctx->d_status, 4 + kKinfo * (size_t)pl, ctx->st);
+                         (size_t)kNumCaps * pl * V, ctx->d_err, ctx->d_status, 4 + kKinfo * (size_t)pl,
+                         ctx->use_tc ? ctx->d_lcnt : nullptr, (size_t)pl * kLenBinsMax, ctx->st);
     LAUNCHED();
     return SAD_OK;
 }
@@ -770,6 +771,7 @@ static int profile_launch(sad_ctx *ctx, int64_t i0, int64_t i1) {
     a.Mb = ctx->d_Mb;
     a.nhi = ctx->d_nhi;
     a.T = ctx->d_T;
+    a.lcnt = ctx->use_tc ? ctx->d_lcnt : nullptr;
     a.i_begin = i0;
     a.i_end = i1;
     launch_profile(a, ctx->st);
@@ -791,17 +793,17 @@ int sad_build_profiles(sad_ctx *ctx) {
     }
     ctx->profiled = false;
     ctx->t_used = false;
-    // K3 (statistics, the cap / K decision, column map, K6 list offsets) in one launch, all on the
-    // device, then the length order (rows by L - k + 1)
+    // K3 (statistics, the cap / K decision, column map, K6 list offsets, the length order's bin
+    // offsets) in one launch, all on the device, then the length order's scatter (rows by L - k + 1)
     launch_shard_plan(ctx->d_M, ctx->d_Mb, ctx->d_Xc, ctx->d_kinfo, pl, V, ctx->allow_cap ? 1 : 0, ctx->kcap_blocks,
                       (int)ctx->kcols_per_block, ctx->d_cap, ctx->d_xsel, ctx->d_ident, ctx->d_kblocks, ctx->d_status,
-                      ctx->d_col0, ctx->d_xoff, xtot_of(ctx), ctx->d_xcur, ctx->st);
+                      ctx->d_col0, ctx->d_xoff, xtot_of(ctx), ctx->d_xcur, ctx->use_tc ? ctx->d_lcnt : nullptr,
+                      ctx->d_lcnt + (size_t)pl * kLenBinsMax, ctx->d_shard_base, ctx->st);
     LAUNCHED();
-    if (ctx->use_tc) {
-        launch_lenorder(ctx->d_rowinfo, ctx->d_shard_base, ctx->d_kinfo, pl, ctx->n, ctx->d_lcnt,
-                        ctx->d_lcnt + (size_t)pl * kLenBinsMax, ctx->d_sigma, ctx->d_sigma_inv, ctx->d_rinfo_s,
-                        ctx->st);
-        ctx->launches_step += 3;
+    if (ctx->use_tc) {     // the length order's slot scatter (histogram: K1/K2, bin offsets: K3)
+        launch_lenorder(ctx->d_rowinfo, ctx->d_shard_base, pl, ctx->n, ctx->d_lcnt + (size_t)pl * kLenBinsMax,
+                        ctx->d_sigma, ctx->d_sigma_inv, ctx->d_rinfo_s, ctx->st);
+        LAUNCHED();
     }
     // the statistics go to pinned host memory; read at the step's first synchronizing call
     CK(cudaMemcpyAsync(ctx->h_stats, ctx->d_err, sizeof(unsigned long long) * (8 + (size_t)pl * kKinfo),

@@ -97,19 +97,22 @@ struct ProfileArgs {
     uint32_t *Mb;                    // [pl][ceil(V/32)]: k-mers present in the shard (zeroed; M >= 2 goes to M)
     int32_t *nhi;                    // [n] entries with count >= 2 (repeated in each CSR row's tail)
     unsigned long long *T;           // [n] within-shard rank sums, zeroed here for the all-pairs kernel
+    uint32_t *lcnt;                  // [pl][kLenBinsMax] Tw histogram of the length order (zeroed), or NULL
 };
 void launch_profile(const ProfileArgs &a, cudaStream_t st);
 // the per-step accumulators of K1/K2 and K3 cleared in one launch: M, Mb, Xc = 0; err = all ones;
 // status + kinfo = 0
 void launch_profile_reset(uint32_t *M, size_t nM, uint32_t *Mb, size_t nMb, uint32_t *Xc, size_t nXc,
-                          unsigned long long *err4, unsigned long long *statkinfo, size_t nsk, cudaStream_t st);
+                          unsigned long long *err4, unsigned long long *statkinfo, size_t nsk, uint32_t *lcnt,
+                          size_t nl, cudaStream_t st);
 // K3 in one launch, one block per shard (k_profile.cu): statistics per candidate cap, the layer cap
 // T_s and operand width K_s (clipped to kcap_blocks; status[0] |= 1 on overflow, status[1] = max K_s;
 // kinfo[s][20] = K_s, [21] = T_s), the column map col0 and the K6 list offsets (xtot[s] totals)
 void launch_shard_plan(uint32_t *M, const uint32_t *Mb, const uint32_t *Xc, unsigned long long *kinfo, int pl, int V,
                        int allow_cap, int64_t kcap_blocks, int kcpb, uint32_t *cap, uint32_t *xsel, uint32_t *ident,
                        int64_t *kblocks, unsigned long long *status, uint32_t *col0, uint32_t *xoff,
-                       unsigned long long *xtot, uint32_t *xcur, cudaStream_t st);
+                       unsigned long long *xtot, uint32_t *xcur, const uint32_t *lcnt, uint32_t *lpos,
+                       const int64_t *shard_base, cudaStream_t st);
 // the count-exchange status of this rank appended to its count block: [0] operand overflow,
 // [1] first input error kind (0 none, 1 symbol, 2 too short, 3 too long), [2] out_bytes, [3] 0
 void launch_status_tail(const unsigned long long *status, const unsigned long long *err, int64_t out_bytes,
@@ -139,9 +142,8 @@ struct OperandArgs {
 void launch_indicator(const OperandArgs &a, cudaStream_t st);
 // length order by counting (K3): Tw histogram per shard, per-shard scan up to the max Tw in kinfo[3],
 // slot scatter -> sigma, sigma_inv, rinfo_s (ties in arbitrary order); 3 launches + 1 memset
-void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, const unsigned long long *kinfo, int pl,
-                     int64_t n, uint32_t *cnt, uint32_t *pos, int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s,
-                     cudaStream_t st);
+void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *pos,
+                     int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s, cudaStream_t st);
 // K6: the sparse excess of the capped layers (k_excess.cu),
 //   e_ij = sum_tau min((n_i(tau) - T_s)+, (n_j(tau) - T_s)+)   for i < j in shard s,
 // as a dense u8 matrix E_s[r][c] over sorted positions (length order; row pitch rup(w_s, 16);
