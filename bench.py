@@ -378,8 +378,8 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_sub, cores = oracle_sample(a, o, spec, p, args.cpu_seconds)
-        dt = run_oracle(a, o, spec, p, n_sub)
+        n_sub, cores = oracle_sample(a, o, spec, p, args.cpu_seconds, threads=args.oracle_threads)
+        dt = run_oracle(a, o, spec, p, n_sub, threads=args.oracle_threads)
         cpu = {"value": total_pairs(n_sub, p) / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"oracle.run (full pipeline, p={p}) on the first {n_sub} sequences of the workload, "
                          f"{dt:.1f} s; value = that subset's within-shard pairs / time"}
