@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rank-mode", default="ga", choices=["ga", "samples"],
                     help="ga: rank vs the global ancestor (north star); samples: SURVEY f1, vs the k*p samples")
+    ap.add_argument("--f1-cuda-cores", action="store_true",
+                    help="with --rank-mode samples: the rank against the samples on the CUDA cores")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--oracle-threads", type=int, default=0,
@@ -207,7 +209,8 @@ def main():
 
     # world > 1: the library's own NCCL communicator runs every exchange (collective API)
     ctx = Context(spec.alphabet, spec.k, p, world=world, rank=rank, device=local_rank, stream=stream,
-                  kernel=args.kernel, group=group, rank_mode=args.rank_mode, comm=world > 1)
+                  kernel=args.kernel, group=group, rank_mode=args.rank_mode, comm=world > 1,
+                  f1_cuda_cores=args.f1_cuda_cores)
     R_glob = int(o[-1])
 
     def barrier():

@@ -96,6 +96,11 @@ extern "C" {
                                  Needs p >= 2 and A^k <= 25600. sad_rank_local then
                                  writes p/world*(p-1) sample records instead of p/world ancestor records
                                  (sad_exchange_records) and sad_rank_global takes all p(p-1) of them. */
+#define SAD_F_F1_CUDA_CORES 128u /* with SAD_F_RANK_SAMPLES: the rank against the samples on the CUDA cores
+                                 (byte-SIMD min-sums over each row's CSR entries). Default with the fp4
+                                 tensor-core kernel: the w x p(p-1) contraction of the shard's all-pairs
+                                 operand with the samples' indicator rows on tcgen05 (the excess above
+                                 the layer cap on the CUDA cores); both are exact. */
 #define SAD_F_TC_ALL_LAYERS 32u /* tensor-core path with every threshold layer t <= max n(tau) dense in the
                                  contraction. Default: the layers are capped per shard at the smallest
                                  T in {1,2,4,8} with max_i sum_tau (n_i(tau) - T)+ <= 255, and the

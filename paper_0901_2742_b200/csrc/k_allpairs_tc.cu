@@ -842,4 +842,285 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
     return 0;
 }
 
+
+// =========================================================================================
+// f1 on the tensor cores ("rank ... against the k*p samples",
+// reading A27): T'_i = sum_j q(x_i, s_j) over the m gathered rank samples, q = floor(2^32 S / den)
+// with den = min(L_i, L_j) - k + 1 (reading A5). For shard s with layer cap T_s and column map
+// col0_s (K3), by the split identity
+//   S(x_i, s_j) = (A_s B_s^T)_ij + e_ij,
+// A_s the shard's capped threshold-indicator operand (K4: rows in length order, packed e2m1),
+// B_s the samples' rows in the same column space (layers t <= min(c_j(tau), M_s(tau), T_s): the
+// shard has no column above M_s, and n_i <= M_s), and e_ij = sum_tau min((n_i - T_s)+, (c_j - T_s)+)
+// the excess above the cap (CUDA cores: k_f1_excess, from the rows' count >= 2 CSR tails).
+// =========================================================================================
+
+// the samples' counts transposed to [tau][mrows] (rows j >= m are zero)
+__global__ void k_f1_ctrans(const uint8_t *rec, size_t rec_bytes, int m, int mrows, int V, uint16_t *cT) {
+    const int64_t tot = (int64_t)V * mrows;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int tau = (int)(t / mrows), j = (int)(t % mrows);
+        cT[t] = j < m ? reinterpret_cast<const uint16_t *>(rec + (size_t)j * rec_bytes + 16)[tau] : (uint16_t)0;
+    }
+}
+
+// B_s: one block per (shard, sample row); the row (the shard's K blocks) zeroed, then every k-mer of
+// the sample sets its layers 1..min(c, M_s(tau), T_s) at col0_s(tau) (e2m1 1.0 = 0b0010, packed
+// two per byte, low nibble first, as K4 packs A)
+__global__ void __launch_bounds__(256) k_f1_bop(const uint8_t *rec, size_t rec_bytes, int m, int mrows, int V,
+                                                const uint32_t *M, const uint32_t *col0, const uint32_t *cap,
+                                                const uint32_t *ident, const int64_t *kblocks, int64_t stride,
+                                                uint8_t *bop) {
+    const int s = blockIdx.x / mrows, j = blockIdx.x % mrows;
+    uint8_t *row = bop + ((int64_t)s * mrows + j) * stride;
+    const int64_t rowb = min(stride, kblocks[s] * 128);
+    for (int64_t t = threadIdx.x; t < rowb / 16; t += blockDim.x) reinterpret_cast<uint4 *>(row)[t] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    if (j >= m) return;
+    const uint16_t *cnt = reinterpret_cast<const uint16_t *>(rec + (size_t)j * rec_bytes + 16);
+    const uint32_t T = cap[s];
+    const bool id = ident[s] != 0u;
+    uint32_t *row32 = reinterpret_cast<uint32_t *>(row);
+    for (int tau = threadIdx.x; tau < V; tau += blockDim.x) {
+        const uint32_t c = cnt[tau];
+        if (!c) continue;
+        const uint32_t L = min(min(c, M[(size_t)s * V + tau]), T);
+        const uint32_t c0 = id ? (uint32_t)tau : col0[(size_t)s * V + tau];
+        for (uint32_t t = 0; t < L; ++t) {
+            const uint32_t cc = c0 + t;
+            atomicOr(&row32[cc >> 3], 2u << (4 * (cc & 7)));
+        }
+    }
+}
+
+// e_ij for every row: one thread per sorted position p, the samples 64 at a time as bytes in 16
+// registers. For each of the row's count >= 2 entries (its CSR tail) above the shard's cap,
+// x = n - T_s and the samples' y_j = min((c_j - T_s)+, 255) (byte-SIMD from the transposed counts)
+// give acc_j += min(x, y_j); every partial sum is <= sum_tau (n_i - T_s)+ <= 255 (K3's cap rule),
+// so no byte carries and the clamp of y is exact.
+__global__ void __launch_bounds__(128) k_f1_excess(const int64_t *shard_base, const int64_t *shard_rowpad, int pl,
+                                                   int64_t n, const int32_t *sigma, const uint32_t *csr,
+                                                   const int64_t *off, const int32_t *nhi, int k, const uint32_t *cap,
+                                                   const uint16_t *cT, int mrows, uint8_t *ex) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int s = 0;
+    while (s + 1 < pl && p >= shard_base[s + 1]) ++s;
+    const int64_t local = p - shard_base[s];
+    uint4 *out = reinterpret_cast<uint4 *>(ex + (shard_rowpad[s] + local) * mrows);
+    const uint32_t T = cap[s];
+    const int64_t i = shard_base[s] + sigma[p];
+    const int d = T == kNoCap ? 0 : nhi[i];
+    const uint32_t *tail = csr + (off[i + 1] - (i + 1) * (int64_t)(k - 1)) - d;
+    const uint32_t T2 = T == kNoCap ? 0u : (T | (T << 16));
+    for (int j0 = 0; j0 < mrows; j0 += 64) {
+        uint32_t acc[16] = {};
+        const int nj = min(64, mrows - j0);                     // a multiple of 16
+        for (int e = 0; e < d; ++e) {
+            const uint32_t v = tail[e], nx = v & 0xFFFFu;
+            if (nx <= T) continue;
+            const uint32_t x4 = (nx - T) * 0x01010101u;         // x <= 255
+            const uint4 *crow = reinterpret_cast<const uint4 *>(cT + (size_t)(v >> 16) * mrows + j0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {                        // 8 samples per 16-byte load
+                if (q * 8 >= nj) break;
+                const uint4 c = crow[q];
+                const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {                    // 4 samples -> 4 bytes
+                    const uint32_t lo = __vminu2(__vsubus2(cw[2 * h], T2), 0x00FF00FFu);
+                    const uint32_t hi = __vminu2(__vsubus2(cw[2 * h + 1], T2), 0x00FF00FFu);
+                    const uint32_t y4 = __byte_perm(lo, hi, 0x6420);
+                    acc[2 * q + h] = __vadd4(acc[2 * q + h], __vminu4(y4, x4));
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q * 16 < nj) out[j0 / 16 + q] = make_uint4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+    }
+}
+
+struct F1Params {
+    const int64_t *shard_base, *shard_rowpad, *kblocks;
+    const RowInfo *rinfo_s;          // [n] length order (.shard = local index in the shard)
+    const uint8_t *ex;               // [rows_pad][mrows] e_ij
+    const uint8_t *rec;              // the samples' records (Tw at byte 12)
+    size_t rec_bytes;
+    int pl, m, mrows, ntile;
+    unsigned long long *Tp;          // [n] T' by local index
+};
+
+namespace f1 {
+constexpr int STAGES = 4, THREADS = 256;
+__host__ __device__ constexpr int smem_bytes(int ntile) { return STAGES * (tc::A_BYTES + ntile * tc::BK) + 1024 + 256 + 256 * 16; }
+}
+
+// one CTA per (128-row block of the length-ordered operand, tile of <= 256 samples): warp 0 TMA
+// producer, warp 1 MMA issuer (tcgen05.mma.cta_group::1.kind::mxf4, M = 128, N = ntile, unit block
+// scales), warp 2 TMEM allocator, warps 4-7 the epilogue (TMEM lane = row): S = acc + e_ij, exact
+// q with the pair's denominator, the tile's samples summed into T'_i (one u64 atomic per row and tile)
+__global__ void __launch_bounds__(f1::THREADS, 1) k_f1_tc(const __grid_constant__ CUtensorMap tmapA,
+                                                           const __grid_constant__ CUtensorMap tmapB, F1Params P) {
+    using namespace tc;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int ntile = P.ntile;
+    const int B_BYTES = ntile * BK;
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + f1::STAGES * A_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + f1::STAGES * (A_BYTES + B_BYTES));
+    uint64_t *empty = full + f1::STAGES;
+    uint64_t *accf = empty + f1::STAGES;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accf + 1);
+    int *s_shard = reinterpret_cast<int *>(tmem_slot + 1);
+    RowInfo *sri = reinterpret_cast<RowInfo *>(smem + f1::STAGES * (A_BYTES + B_BYTES) + 256);   // [ntile]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row0 = (int64_t)blockIdx.x * BM;          // in the padded operand rows
+    const int J = blockIdx.y;
+    uint32_t tcols = 32;
+    while (tcols < (uint32_t)ntile + 32u) tcols <<= 1;      // accumulator + the scale column
+    if (threadIdx.x == 0) {
+        int s = 0;
+        while (s + 1 < P.pl && row0 >= P.shard_rowpad[s + 1]) ++s;
+        *s_shard = s;
+        for (int i = 0; i < f1::STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(accf, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmapA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmapB)) : "memory");
+    }
+    for (int t = threadIdx.x; t < ntile; t += f1::THREADS) {
+        const int j = J * ntile + t;
+        const uint32_t tw = j < P.m ? *reinterpret_cast<const uint32_t *>(P.rec + (size_t)j * P.rec_bytes + 12) : 1u;
+        sri[t] = RowInfo{tw, 0xFFFFFFFFu / tw, 0xFFFFFFFFu % tw + 1u, 0u};
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(tcols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int s = *s_shard;
+    const uint32_t sf = tmem_base + (uint32_t)ntile;          // unit UE8M0 scales (127 = 2^0)
+    if (warp >= 4) tmem_st32_const(tmem_base + ((uint32_t)((warp - 4) * 32) << 16) + (uint32_t)ntile, 0x7F7F7F7Fu);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const int nkb = (int)P.kblocks[s];
+    if (warp == 0 && lane == 0) {
+        int stage = 0;
+        uint32_t phase = 0;
+        const int rowB = (int)((int64_t)s * P.mrows + (int64_t)J * ntile);
+        for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], (uint32_t)(A_BYTES + B_BYTES));
+            tma_load_2d(&tmapA, &full[stage], sA + stage * A_BYTES, kb * BK, (int)row0);
+            tma_load_2d(&tmapB, &full[stage], sB + stage * B_BYTES, kb * BK, rowB);
+            if (++stage == f1::STAGES) { stage = 0; phase ^= 1; }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // mxf4, M = 128: A = B = E2M1, UE8M0 scales, N >> 3 at bit 17, M >> 4 at bit 24
+        const uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(ntile >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < BK / 32; ++kk)
+                mma_mxf4(tmem_base, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, (kb | kk) != 0, sf, sf);
+            tc_commit(&empty[stage]);
+            if (++stage == f1::STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(accf);
+    } else if (warp >= 4) {
+        const int q4 = warp - 4;
+        const int64_t local = row0 + q4 * 32 + lane - P.shard_rowpad[s];   // length-order position in the shard
+        const int64_t w = P.shard_base[s + 1] - P.shard_base[s];
+        const bool valid = local < w;
+        RowInfo ri{1u, 0xFFFFFFFFu, 1u, 0u};
+        if (valid) ri = P.rinfo_s[P.shard_base[s] + local];
+        const uint8_t *exr = P.ex + (row0 + q4 * 32 + lane) * (int64_t)P.mrows + (int64_t)J * ntile;
+        mbar_wait(accf, 0);
+        tc_fence_after();
+        unsigned long long sum = 0;
+        for (int ch = 0; ch < ntile / 16; ++ch) {
+            uint32_t v[16];
+            tmem_ld16(tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ch * 16), v);
+            if (!valid) continue;
+            const uint4 e4 = *reinterpret_cast<const uint4 *>(exr + ch * 16);
+            const uint32_t ew[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int jt = ch * 16 + u;
+                if (J * ntile + jt >= P.m) break;
+                // exact integers < 2^23 in fp32: adding 2^23 leaves the value in the mantissa
+                const uint32_t S0 = __float_as_uint(__uint_as_float(v[u]) + 8388608.0f) - 0x4B000000u;
+                const uint32_t S = S0 + ((ew[u >> 2] >> (8 * (u & 3))) & 0xFFu);
+                sum += pair_q(S, ri, sri[jt]);
+            }
+        }
+        if (valid) atomicAdd(&P.Tp[P.shard_base[s] + ri.shard], sum);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tcols) : "memory");
+}
+
+int f1_tc_rows(int m) { return m <= 256 ? (m + 15) / 16 * 16 : (m + 255) / 256 * 256; }
+
+int launch_f1_tc(const F1Args &a, cudaStream_t st, std::string &err) {
+    std::string why;
+    if (!tc_supported(why)) {
+        err = why;
+        return -1;
+    }
+    const int mrows = f1_tc_rows(a.m), ntile = std::min(mrows, 256);
+    {
+        const int64_t tot = (int64_t)a.V * mrows;
+        k_f1_ctrans<<<(unsigned)std::min<int64_t>(4096, (tot + 255) / 256), 256, 0, st>>>(a.rec, a.rec_bytes, a.m,
+                                                                                          mrows, a.V, a.cT);
+    }
+    k_f1_bop<<<(unsigned)(a.pl * mrows), 256, 0, st>>>(a.rec, a.rec_bytes, a.m, mrows, a.V, a.M, a.col0, a.cap,
+                                                       a.ident, a.kblocks, a.stride, a.bop);
+    if (a.n > 0)
+        k_f1_excess<<<(unsigned)((a.n + 127) / 128), 128, 0, st>>>(a.shard_base, a.shard_rowpad, a.pl, a.n, a.sigma,
+                                                                    a.csr, a.off, a.nhi, a.k, a.cap, a.cT, mrows, a.ex);
+    CUtensorMap mapA, mapB;
+    if (!encode(&mapA, a.op, a.stride, a.rows_pad, tc::BM) || !encode(&mapB, a.bop, a.stride, (int64_t)a.pl * mrows, ntile)) {
+        err = "cuTensorMapEncodeTiled failed";
+        return -1;
+    }
+    F1Params P{};
+    P.shard_base = a.shard_base;
+    P.shard_rowpad = a.shard_rowpad;
+    P.kblocks = a.kblocks;
+    P.rinfo_s = a.rinfo_s;
+    P.ex = a.ex;
+    P.rec = a.rec;
+    P.rec_bytes = a.rec_bytes;
+    P.pl = a.pl;
+    P.m = a.m;
+    P.mrows = mrows;
+    P.ntile = ntile;
+    P.Tp = a.Tp;
+    const size_t smem = (size_t)f1::smem_bytes(ntile);
+    if (smem_optin(k_f1_tc, smem) != cudaSuccess) {
+        err = "shared memory opt-in failed";
+        return -1;
+    }
+    dim3 grid((unsigned)(a.rows_pad / tc::BM), (unsigned)(mrows / ntile));
+    k_f1_tc<<<grid, f1::THREADS, smem, st>>>(mapA, mapB, P);
+    return 0;
+}
+
 }  // namespace sad

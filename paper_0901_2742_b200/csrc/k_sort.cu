@@ -57,8 +57,8 @@ static int block_sort(const K *ki, const int32_t *vi, int n, K *ko, int32_t *vo,
 #define SAD_SEG_RADIX 4
 #endif
 constexpr int kSegThreads = SAD_SEG_THREADS, kSegItems = kSmallSortMax / SAD_SEG_THREADS;
-template <int ITEMS>
-using SegSortT = cub::BlockRadixSort<uint32_t, kSegThreads, ITEMS, int32_t, SAD_SEG_RADIX>;
+template <int ITEMS, typename KI = uint32_t>
+using SegSortT = cub::BlockRadixSort<KI, kSegThreads, ITEMS, int32_t, SAD_SEG_RADIX>;
 using SegSort = SegSortT<kSegItems>;
 constexpr int kRunItems = 4;                      // run blocks of the rank sort: 512 x 4 = 2048 keys
 constexpr int kRunMax = kSegThreads * kRunItems;
@@ -69,11 +69,12 @@ __device__ __forceinline__ int64_t run_begin(const int64_t *seg, int s, int r, i
     return seg[s] + (seg[s + 1] - seg[s]) * r / nruns;
 }
 
-template <typename K, int ITEMS = kSegItems>
+// KI: the key type the block sorts (the bits below end_bit; uint64_t when end_bit > 32)
+template <typename K, int ITEMS = kSegItems, typename KI = uint32_t>
 __global__ void __launch_bounds__(kSegThreads) k_seg_sort(const K *keys_in, const int32_t *vals_in,
                                                             const int64_t *seg, K *keys_out, int32_t *vals_out,
                                                             int end_bit, int nruns) {
-    using BRS = SegSortT<ITEMS>;
+    using BRS = SegSortT<ITEMS, KI>;
     extern __shared__ __align__(16) uint8_t sort_smem[];
     typename BRS::TempStorage &tmp = *reinterpret_cast<typename BRS::TempStorage *>(sort_smem);
     const int sg = blockIdx.x / nruns, rn = blockIdx.x % nruns;
@@ -82,12 +83,12 @@ __global__ void __launch_bounds__(kSegThreads) k_seg_sort(const K *keys_in, cons
     if (n <= 0) return;
     const K low = end_bit >= (int)(8 * sizeof(K)) ? ~K(0) : ((K(1) << end_bit) - 1);
     const K high = keys_in[b] & ~low;
-    uint32_t k[ITEMS];
+    KI k[ITEMS];
     int32_t v[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const int idx = threadIdx.x * ITEMS + i;
-        k[i] = idx < n ? (uint32_t)(keys_in[b + idx] & low) : 0xFFFFFFFFu;   // padding sorts last (stable)
+        k[i] = idx < n ? (KI)(keys_in[b + idx] & low) : ~KI(0);             // padding sorts last (stable)
         v[i] = idx < n ? vals_in[b + idx] : 0;
     }
     BRS(tmp).Sort(k, v, 0, end_bit);
@@ -182,20 +183,18 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_runs_smem(const K *keys
 // the stable sort of every segment: runs of at most kRunMax keys sorted in place by separate blocks
 // (512 x 4 items: the block sort's cost follows its capacity, not the run), then merged into
 // (ko, vo) by ranking; a segment that fits one run is sorted straight into (ko, vo)
-template <typename K>
-static int seg_sort_runs(K *ki, int32_t *vi, const int64_t *seg, int nseg, int64_t max_seg, int64_t n, K *ko,
-                         int32_t *vo, int end_bit, cudaStream_t st) {
-    if (end_bit > 32) return -1;
+template <typename K, typename KI>
+static int seg_sort_runs_t(K *ki, int32_t *vi, const int64_t *seg, int nseg, int64_t max_seg, int64_t n, K *ko,
+                           int32_t *vo, int end_bit, cudaStream_t st) {
     const int nruns = (int)std::max<int64_t>(1, (max_seg + kRunMax - 1) / kRunMax);
+    const size_t smem = sizeof(typename SegSortT<kRunItems, KI>::TempStorage);
+    auto kern = k_seg_sort<K, kRunItems, KI>;
+    if (smem_optin(kern, smem) != cudaSuccess) return -1;
     if (nruns == 1) {
-        const size_t smem = sizeof(typename SegSortT<kRunItems>::TempStorage);
-        if (smem_optin(k_seg_sort<K, kRunItems>, smem) != cudaSuccess) return -1;
-        k_seg_sort<K, kRunItems><<<nseg, kSegThreads, smem, st>>>(ki, vi, seg, ko, vo, end_bit, 1);
+        kern<<<nseg, kSegThreads, smem, st>>>(ki, vi, seg, ko, vo, end_bit, 1);
         return 0;
     }
-    const size_t smem = sizeof(typename SegSortT<kRunItems>::TempStorage);
-    if (smem_optin(k_seg_sort<K, kRunItems>, smem) != cudaSuccess) return -1;
-    k_seg_sort<K, kRunItems><<<nseg * nruns, kSegThreads, smem, st>>>(ki, vi, seg, ki, vi, end_bit, nruns);
+    kern<<<nseg * nruns, kSegThreads, smem, st>>>(ki, vi, seg, ki, vi, end_bit, nruns);
     if (max_seg <= kMergeSmemMax) {
         const size_t ms = (size_t)max_seg * sizeof(K);
         if (smem_optin(k_merge_runs_smem<K>, ms) != cudaSuccess) return -1;
@@ -206,6 +205,16 @@ static int seg_sort_runs(K *ki, int32_t *vi, const int64_t *seg, int nseg, int64
         if (g > 0) k_merge_runs<K><<<(unsigned)g, 256, 0, st>>>(ki, vi, seg, nseg, nruns, n, ko, vo);
     }
     return 0;
+}
+
+// end_bit <= 32: the blocks sort 32-bit keys; up to 64: 64-bit keys (more radix passes)
+template <typename K>
+static int seg_sort_runs(K *ki, int32_t *vi, const int64_t *seg, int nseg, int64_t max_seg, int64_t n, K *ko,
+                         int32_t *vo, int end_bit, cudaStream_t st) {
+    if (end_bit <= 32) return seg_sort_runs_t<K, uint32_t>(ki, vi, seg, nseg, max_seg, n, ko, vo, end_bit, st);
+    if (sizeof(K) == 8 && end_bit <= 64)
+        return seg_sort_runs_t<K, unsigned long long>(ki, vi, seg, nseg, max_seg, n, ko, vo, end_bit, st);
+    return -1;
 }
 
 int seg_sort_pairs_runs(unsigned long long *ki, int32_t *vi, const int64_t *seg, int nseg, int64_t max_seg, int64_t n,

@@ -469,6 +469,8 @@ int sad_create(const sad_config *cfg, const uint8_t *nccl_id, sad_ctx **out) {
     ctx->shard0 = cfg->rank * ctx->pl;
     ctx->use_tc = !(cfg->flags & SAD_F_KERNEL_ALU);
     ctx->tc_kind = (cfg->flags & SAD_F_TC_INT8) ? 0 : 1;
+    ctx->f1_tc = ctx->use_tc && ctx->tc_kind == 1 && (cfg->flags & SAD_F_RANK_SAMPLES) &&
+                 !(cfg->flags & SAD_F_F1_CUDA_CORES);
     ctx->tc_cg = (cfg->flags & SAD_F_TC_1SM) ? 1 : 2;
     ctx->kcols_per_block = (ctx->use_tc && ctx->tc_kind == 1) ? 256 : 128;
     DeviceScope dev_scope_(cfg->device);
@@ -820,13 +822,19 @@ int sad_build_profiles(sad_ctx *ctx) {
 }
 
 // the operand buffer: [indicator | counts operand][K6 lists L_tau u32][K6 dense excess E u8 + 256 zero bytes]
-static void operand_parts(const sad_ctx *ctx, size_t &op, size_t &xl, size_t &xe) {
+// [f1 on the tensor cores: the samples' operand rows | e_ij | the samples' counts transposed]
+static void operand_parts(const sad_ctx *ctx, size_t &op, size_t &xl, size_t &xe, size_t &f1b) {
     op = ctx->use_tc ? (size_t)ctx->rows_pad * (size_t)ctx->K_stride : (size_t)ctx->rows_pad * (size_t)ctx->V_pad * 2;
     op = (size_t)rup((int64_t)op, 1024);
-    xl = xe = 0;
+    xl = xe = f1b = 0;
     if (ctx->use_tc && ctx->allow_cap) {
         xl = (size_t)rup(ctx->x_entries_bound * 4, 1024);
         xe = (size_t)rup(ctx->h_ebase[ctx->pl] + 256, 1024);
+    }
+    if (ctx->f1_tc) {
+        const int64_t mr = f1_tc_rows(ctx->cfg.p * (ctx->cfg.p - 1));
+        f1b = (size_t)rup((int64_t)ctx->pl * mr * ctx->K_stride, 1024) + (size_t)rup(ctx->rows_pad * mr, 1024) +
+              (size_t)rup((int64_t)ctx->V * mr * 2, 1024);
     }
 }
 
@@ -834,9 +842,9 @@ int sad_operand_size(const sad_ctx *cctx, size_t *bytes) {
     sad_ctx *ctx = const_cast<sad_ctx *>(cctx);
     GUARD(2);
     if (!bytes) return SAD_E_ARG;
-    size_t op = 0, xl = 0, xe = 0;
-    operand_parts(ctx, op, xl, xe);
-    *bytes = op + xl + xe;
+    size_t op = 0, xl = 0, xe = 0, f1b = 0;
+    operand_parts(ctx, op, xl, xe, f1b);
+    *bytes = op + xl + xe + f1b;
     return SAD_OK;
 }
 
@@ -878,8 +886,8 @@ static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, 
     o.pl = pl;
     o.fp4 = ctx->use_tc && ctx->tc_kind == 1;
     o.op = d_operand;
-    size_t op_b = 0, xl_b = 0, xe_b = 0;
-    operand_parts(ctx, op_b, xl_b, xe_b);
+    size_t op_b = 0, xl_b = 0, xe_b = 0, f1_b = 0;
+    operand_parts(ctx, op_b, xl_b, xe_b, f1_b);
     uint32_t *lists = xl_b ? reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_operand) + op_b) : nullptr;
     uint8_t *E = xl_b ? reinterpret_cast<uint8_t *>(d_operand) + op_b + xl_b : nullptr;
     unsigned long long *xtot = xtot_of(ctx);
@@ -995,8 +1003,15 @@ static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, 
         LAUNCHED();
         int sbits = 0;
         while ((1 << sbits) < pl) ++sbits;
-        CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
-                      56 + sbits));
+        // within a shard T <= w 2^32: the segmented run sort on those bits (64-bit block keys), else
+        // one device radix sort of (shard, T)
+        int tb = 32;
+        while (tb < 56 && (int64_t(1) << (tb - 32)) <= ctx->max_w) ++tb;
+        if (!(ctx->max_w <= (int64_t)16384 &&
+              seg_sort_pairs_runs(ctx->d_ckey, ctx->d_perm_in, ctx->d_shard_base, ctx->pl, ctx->max_w, ctx->n,
+                                  ctx->d_ckey_sorted, ctx->d_perm_sorted, tb, ctx->st) == 0))
+            CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
+                          56 + sbits));
         LAUNCHED();
         launch_sample_records(ctx->d_perm_sorted, ctx->d_shard_base, pl, ctx->cfg.p, ctx->d_csr, ctx->d_off,
                               ctx->d_dcnt, ctx->d_rowinfo, ctx->first_idx, ctx->cfg.k, an.rec_bytes,
@@ -1053,9 +1068,48 @@ static int rank_global_impl(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_sam
         // samples, ordered exactly, and the keys (d_key doubles as the T' accumulator)
         const int m = p * (p - 1);
         CK(cudaMemsetAsync(ctx->d_key, 0, sizeof(unsigned long long) * (size_t)ctx->n, ctx->st));
-        if (launch_rank_vs_samples(r, m, ctx->d_key, ctx->num_sms, ctx->st))
-            return fail(ctx, SAD_E_ARG, "rank vs samples: V too large");
-        LAUNCHED();
+        if (ctx->f1_tc) {
+            // the w x m contraction on the tensor cores against the all-pairs operand of this step
+            size_t op_b = 0, xl_b = 0, xe_b = 0, f1_b = 0;
+            operand_parts(ctx, op_b, xl_b, xe_b, f1_b);
+            const int64_t mr = f1_tc_rows(m);
+            uint8_t *f1base = reinterpret_cast<uint8_t *>(ctx->d_operand) + op_b + xl_b + xe_b;
+            F1Args fa{};
+            fa.rec = r.anc_all;
+            fa.rec_bytes = r.rec_bytes;
+            fa.m = m;
+            fa.V = ctx->V;
+            fa.k = ctx->cfg.k;
+            fa.pl = ctx->pl;
+            fa.num_sms = ctx->num_sms;
+            fa.n = ctx->n;
+            fa.rows_pad = ctx->rows_pad;
+            fa.stride = ctx->K_stride;
+            fa.op = ctx->d_operand;
+            fa.shard_base = ctx->d_shard_base;
+            fa.shard_rowpad = ctx->d_shard_rowpad;
+            fa.kblocks = ctx->d_kblocks;
+            fa.M = ctx->d_M;
+            fa.col0 = ctx->d_col0;
+            fa.cap = ctx->d_cap;
+            fa.ident = ctx->d_ident;
+            fa.sigma = ctx->d_sigma;
+            fa.nhi = ctx->d_nhi;
+            fa.csr = ctx->d_csr;
+            fa.off = ctx->d_off;
+            fa.rinfo_s = ctx->d_rinfo_s;
+            fa.bop = f1base;
+            fa.ex = f1base + rup((int64_t)ctx->pl * mr * ctx->K_stride, 1024);
+            fa.cT = reinterpret_cast<uint16_t *>(fa.ex + rup(ctx->rows_pad * mr, 1024));
+            fa.Tp = ctx->d_key;
+            std::string e;
+            if (launch_f1_tc(fa, ctx->st, e)) return fail(ctx, SAD_E_CUDA, "f1 on the tensor cores: %s", e.c_str());
+            ctx->launches_step += 4;
+        } else {
+            if (launch_rank_vs_samples(r, m, ctx->d_key, ctx->num_sms, ctx->st))
+                return fail(ctx, SAD_E_ARG, "rank vs samples: V too large");
+            LAUNCHED();
+        }
         launch_f1_keys(ctx->d_key, ctx->n, ctx->tbits, ctx->ibits, ctx->first_idx, ctx->d_rowinfo, ctx->d_key,
                        ctx->d_ckey, ctx->d_perm_in, ctx->d_S_ga, ctx->d_den_ga, ctx->st);
         LAUNCHED();
@@ -1063,9 +1117,9 @@ static int rank_global_impl(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_sam
         LAUNCHED();
     }
     // the local rank sort: runs of <= 2048 keys per block, merged by ranking in shared memory
-    if (!(qbits == 32 && ctx->max_w <= (int64_t)16384 &&
+    if (!(ctx->max_w <= (int64_t)16384 &&
           seg_sort_pairs_runs(ctx->d_ckey, ctx->d_perm_in, ctx->d_shard_base, ctx->pl, ctx->max_w, ctx->n,
-                              ctx->d_ckey_sorted, ctx->d_perm_sorted, 32, ctx->st) == 0))
+                              ctx->d_ckey_sorted, ctx->d_perm_sorted, qbits, ctx->st) == 0))
         CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
                       qbits + sbits));
     LAUNCHED();

@@ -254,6 +254,26 @@ void launch_sample_records(const int32_t *rows_sorted, const int64_t *shard_base
                            const int64_t *off, const int32_t *dcnt, const RowInfo *rowinfo, int64_t first_idx, int k,
                            size_t rec_bytes, uint8_t *rec_out, cudaStream_t st);
 int launch_rank_vs_samples(const RankArgs &a, int m, unsigned long long *Tp, int num_sms, cudaStream_t st);
+// f1 on the tensor cores (k_allpairs_tc.cu; packed-fp4 operand only): T'_i += sum_j q(x_i, s_j)
+struct F1Args {
+    const uint8_t *rec;              // [m] gathered sample records
+    size_t rec_bytes;
+    int m, V, k, pl, num_sms;
+    int64_t n, rows_pad, stride;     // local rows, operand rows (padded), operand row bytes
+    const void *op;                  // the all-pairs operand A (K4, length order)
+    const int64_t *shard_base, *shard_rowpad, *kblocks;
+    const uint32_t *M, *col0, *cap, *ident;
+    const int32_t *sigma, *nhi;
+    const uint32_t *csr;
+    const int64_t *off;
+    const RowInfo *rinfo_s;
+    uint8_t *bop;                    // scratch: [pl][f1_tc_rows(m)][stride] the samples' operand rows
+    uint8_t *ex;                     // scratch: [rows_pad][f1_tc_rows(m)] e_ij
+    uint16_t *cT;                    // scratch: [V][f1_tc_rows(m)] the samples' counts, transposed
+    unsigned long long *Tp;          // [n] T' (accumulated; zeroed by the caller)
+};
+int f1_tc_rows(int m);
+int launch_f1_tc(const F1Args &a, cudaStream_t st, std::string &err);
 void launch_f1_keys(const unsigned long long *Tp, int64_t n, int tbits, int ibits, int64_t first_idx,
                     const RowInfo *rowinfo, unsigned long long *key, unsigned long long *ckey, int32_t *perm_in,
                     uint32_t *S_ga, uint32_t *den_ga, cudaStream_t st);
@@ -465,6 +485,7 @@ struct sad_ctx {
     unsigned long long *d_status = nullptr;         // [4] device: operand overflow, max K_s, -, -
     int64_t kcap_blocks = 0;                         // operand K capacity (128-byte blocks per row)
     int64_t kcap_next = 0;                           // the capacity the next step starts with
+    bool f1_tc = false;              // f1 rank vs samples as a tensor-core contraction (F1Args)
     int64_t kmax_blocks_seen = -1;                   // largest K blocks of the last absorbed step (-1: none)
     bool allow_cap = false;                          // capped layers + K6 excess possible in this layout
     int64_t x_entries_bound = 0;                     // K6 list entries bound (all CSR entries)

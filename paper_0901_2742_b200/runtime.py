@@ -110,7 +110,7 @@ class Context:
 
     def __init__(self, alphabet: str, k: int, p: int, *, world: int = 1, rank: int = 0, device: int | None = None,
                  stream: torch.cuda.Stream | None = None, kernel: str = "tc", keep_sim: bool = False, group=None,
-                 rank_mode: str = "ga", comm: bool = False):
+                 rank_mode: str = "ga", comm: bool = False, f1_cuda_cores: bool = False):
         """comm: give the library its own NCCL communicator (sad_create with an id that rank 0 draws
         and torch.distributed broadcasts over `group`): the collective calls sad_rank / sad_partition
         then run every exchange themselves. Needed by run() when world > 1; with world == 1 it makes
@@ -128,7 +128,7 @@ class Context:
         if rank_mode not in ("ga", "samples"):
             raise ValueError(f"rank_mode must be 'ga' or 'samples', not {rank_mode!r}")
         flags = (L.SAD_F_KEEP_SIM if keep_sim else 0) | KERNELS[kernel] | (
-            L.SAD_F_RANK_SAMPLES if rank_mode == "samples" else 0)
+            L.SAD_F_RANK_SAMPLES if rank_mode == "samples" else 0) | (L.SAD_F_F1_CUDA_CORES if f1_cuda_cores else 0)
         self.rank_mode = rank_mode
         self.kernel = kernel
         cfg = L.SadConfig(ALPHABETS[alphabet], k, p, world, rank, device, self.stream.cuda_stream, flags)

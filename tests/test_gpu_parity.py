@@ -291,11 +291,13 @@ def _compare_f1(ctx, sizes, r, a, o, p):
     assert int(sizes.sum()) == n
 
 
-@pytest.mark.parametrize("kernel", ["tc", "tc8", "alu"])
-@pytest.mark.parametrize("case", ["cfg1", "cfg2", "cfg3_small_p4", "dna_p3", "adv"])
+@pytest.mark.parametrize("kernel", ["tc", "tc1", "tc+cc", "tc8", "alu"])
+@pytest.mark.parametrize("case", ["cfg1", "cfg2", "cfg3_small_p4", "dna_p3", "adv", "p12"])
 def test_samples_mode(kernel, case):
     """the GPU path in rank-against-samples mode is bit-identical
-    to the oracle's mode "samples"."""
+    to the oracle's mode "samples" -- the fp4 kernels with the rank on the tensor cores (tc, tc1),
+    or on the CUDA cores (tc+cc, and the int8 / ALU kernels). p = 12: 132 samples (the f1 tile's
+    N = 144), shards with and without layer caps."""
     from paper_0901_2742_b200.runtime import Context
     if case in ("cfg1", "cfg2"):
         spec = gen.SPECS[int(case[3])]
@@ -316,8 +318,13 @@ def test_samples_mode(kernel, case):
         seqs = [seqs[i] for i in rng.permutation(len(seqs))]
         a, o = gen.from_strings(seqs)
         alpha, k, p = "protein", 3, 3
+    if case == "p12":
+        spec = gen.SPECS[3]
+        a, o = gen.generate(spec, n=2000, seed=29)
+        alpha, k, p = spec.alphabet, spec.k, 12
     n = len(o) - 1
-    ctx = Context(alpha, k, p, kernel=kernel, rank_mode="samples")
+    cc = kernel == "tc+cc"
+    ctx = Context(alpha, k, p, kernel="tc" if cc else kernel, rank_mode="samples", f1_cuda_cores=cc)
     ctx.load(a, o, n, 0)
     sizes = ctx.run()
     r = oracle.run(a, o, alpha, k, p, mode="samples")
