@@ -505,3 +505,52 @@ class Context:
         bad = ctypes.c_int64()
         self._call("sad_selftest_fixed_point", max_den, ctypes.byref(bad))
         return bad.value
+
+
+class Pipeline:
+    """End-to-end steps over host inputs, double-buffered (world == 1): `depth` contexts, each on its
+    own stream, take the steps in turn, so that the pinned host-to-device copy and k-mer counts of
+    step k+1 (sad_load, copy engine + K1/K2) run while the device works on step k, and the keys of
+    step k are read back (device-to-host into pinned memory) while step k+1 runs. Every step is a
+    complete sad_load .. sad_partition over its own inputs; submit() returns once the step's inputs
+    have been copied (the host buffers may then be reused), collect() returns the oldest step's keys
+    (pinned host tensor, every owned bucket back to back in key order) and bucket sizes."""
+
+    def __init__(self, alphabet: str, k: int, p: int, *, depth: int = 2, device: int | None = None, **kw):
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        if kw.get("world", 1) != 1:
+            raise ValueError("Pipeline overlaps whole steps of one rank (world == 1)")
+        dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+        self.ctx = [Context(alphabet, k, p, device=dev.index, stream=torch.cuda.Stream(dev), **kw) for _ in range(depth)]
+        self._next = 0
+        self._pending = []
+        self._host = {}
+
+    def submit(self, ascii_, offsets, n_global: int | None = None, first_index: int = 0):
+        if len(self._pending) == len(self.ctx):
+            raise RuntimeError("every context holds an uncollected step: collect() first")
+        c = self.ctx[self._next]
+        self._next = (self._next + 1) % len(self.ctx)
+        n = len(offsets) - 1
+        c.load(ascii_, offsets, n if n_global is None else n_global, first_index)
+        c.run(sync=False)                     # world == 1: the step is enqueued, nothing read back
+        keys = c.out_keys()
+        h = self._host.get(id(c))
+        if h is None or h.shape != keys.shape:
+            h = torch.empty(keys.shape, dtype=keys.dtype, pin_memory=True)
+            self._host[id(c)] = h
+        with torch.cuda.stream(c.stream):
+            h.copy_(keys, non_blocking=True)  # D2H of the step's result, ordered after the step
+            ev = torch.cuda.Event()
+            ev.record(c.stream)
+        self._pending.append((c, h, ev))
+
+    def collect(self):
+        c, h, ev = self._pending.pop(0)
+        ev.synchronize()
+        return h, c.bucket_sizes_now()
+
+    def close(self):
+        for c in self.ctx:
+            c.close()

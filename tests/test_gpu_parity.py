@@ -507,3 +507,28 @@ def test_similarity_near_the_fp32_bound(kernel):
             smax = max(smax, int(Sref.max()))
         assert smax == 65535
         ctx.close()
+
+
+def test_pipeline_double_buffered():
+    """runtime.Pipeline (the e2e path of bench.py): steps over different host inputs taken in turn by
+    two contexts on two streams, each step's keys and bucket sizes equal to the oracle's."""
+    from paper_0901_2742_b200.runtime import Pipeline
+    spec = gen.SPECS[2]
+    sets = [gen.generate(spec, n=1200 + 97 * j, seed=300 + j) for j in range(5)]
+    pipe = Pipeline(spec.alphabet, spec.k, spec.p, depth=2)
+    got = []
+    for j, (a, o) in enumerate(sets):
+        pipe.submit(a, o)
+        if j >= 1:
+            h, sz = pipe.collect()
+            got.append((h.clone().numpy(), sz))
+    h, sz = pipe.collect()
+    got.append((h.clone().numpy(), sz))
+    pipe.close()
+    for (a, o), (keys, sizes) in zip(sets, got):
+        r = oracle.run(a, o, spec.alphabet, spec.k, spec.p)
+        assert sizes.tolist() == r.bsize.tolist()
+        idx = np.concatenate([np.asarray(b, np.int64) for b in r.buckets()])
+        q = np.array([oracle.q(int(r.S[i]), int(r.den[i])) for i in idx], dtype=object)
+        want = [(int(qq) << 31) + int(i) for qq, i in zip(q, idx)]     # GA mode: key = (q << 31) + index
+        assert [int(x) & ((1 << 64) - 1) for x in keys.tolist()] == want
