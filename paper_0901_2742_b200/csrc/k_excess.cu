@@ -52,8 +52,7 @@ __global__ void __launch_bounds__(256) k_xfill(ExcessArgs a, uint32_t *xcur) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * 8;
     for (int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); r < a.n; r += nw) {
-        int s = 0;
-        while (s + 1 < a.pl && r >= a.shard_base[s + 1]) ++s;
+        const int s = (int)a.rowinfo[r].shard;    // input order: K1/K2 recorded the row's shard
         const uint32_t T = a.cap[s];
         if (T == kNoCap) continue;
         const int dh = a.nhi[r];                  // the count >= 2 entries: the row's CSR tail

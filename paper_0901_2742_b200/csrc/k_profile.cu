@@ -517,9 +517,8 @@ void launch_profile(const ProfileArgs &a, cudaStream_t st) {
 __global__ void k_lenscatter(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *pos,
                              int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        int s = 0;
-        while (s + 1 < pl && i >= shard_base[s + 1]) ++s;
         RowInfo r = rowinfo[i];
+        const int s = (int)r.shard;                // K1/K2 recorded every row's shard
         const int64_t p = atomicAdd(&pos[(size_t)s * kLenBinsMax + r.tw], 1u);   // sorted position
         const int64_t b = shard_base[s];
         const int32_t local = (int32_t)(i - b);

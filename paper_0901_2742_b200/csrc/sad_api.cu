@@ -923,6 +923,7 @@ static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, 
             x.ebase = ctx->d_ebase;
             x.sigma = ctx->d_sigma;
             x.sigma_inv = ctx->d_sigma_inv;
+            x.rowinfo = ctx->d_rowinfo;
             launch_xfill(x, ctx->d_xcur, ctx->st);
             LAUNCHED();
             // K6 rows on the side stream, concurrently with K4 (both only read the CSR / lists)

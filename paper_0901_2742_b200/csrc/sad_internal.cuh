@@ -162,6 +162,7 @@ struct ExcessArgs {
     int accb;                        // bytes of one row accumulator (max_w rounded up to 16)
     const int32_t *sigma;            // [n] length order: sorted position -> local index
     const int32_t *sigma_inv;        // [n] local index -> sorted position
+    const RowInfo *rowinfo;          // [n] input order (.shard)
     uint2 *xrow;                     // [n] .x = 1 if the row (sorted position) has excess
     uint8_t *E;                      // dense excess rows
     uint8_t *zero_seg;               // 256 bytes zeroed by k_xfill (the staging source of rows without excess)
