@@ -29,7 +29,7 @@ namespace sad {
 
 constexpr int kXrWarps = 8;
 #ifndef SAD_XR_BATCH
-#define SAD_XR_BATCH 4                  // list entries per lane in flight (one round trip per 32 * batch)
+#define SAD_XR_BATCH 8                  // list entries per lane in flight (one round trip per 32 * batch)
 #endif
 #ifndef SAD_XROWS_GLOBAL
 #define SAD_XROWS_GLOBAL 1   // 1: accumulate each row's excess in place in E (global); 0: shared-memory rows
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kXrWarps * 32) k_xrows(ExcessArgs a, int warps
 // excess k-mer appears, then the partners' bytes are added with fire-and-forget 32-bit atomics
 // (no carry: every e_ij <= 255). No shared-memory accumulator, so occupancy is not bounded by w.
 #ifndef SAD_XR_MINB
-#define SAD_XR_MINB 6
+#define SAD_XR_MINB 5
 #endif
 __global__ void __launch_bounds__(kXrWarps * 32, SAD_XR_MINB) k_xrows_g(ExcessArgs a) {
     __shared__ unsigned long long lbase[kMaxLocalShards + 1];
