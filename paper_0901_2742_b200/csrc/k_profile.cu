@@ -328,38 +328,51 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         uint16_t *lst = (nseg == 1 && (kCodeBuf - lofs) / 2 >= Tw + 1) ? reinterpret_cast<uint16_t *>(cod + lofs) : nullptr;
         bool narrow_ovf;
         bool fast = false;
-        if constexpr (kBinBits == 8) fast = lst != nullptr;
+        if constexpr (kBinBits == 8) fast = true;
         if (fast) {
-            // The common case, specialised: one segment, byte bins over all V k-mers, the owner list.
-            // Counting: one shared-memory atomic per window; a bin's first window (old count 0) appends
-            // its k-mer to the owner list. Emission: every owner once (its count c >= 1 read and its
-            // bin cleared), one ballot per 32 owners: count >= 2 entries from the front, count-1
-            // entries from the back of the row's d slots (d = nl), meeting exactly.
+            // Byte bins over all V k-mers and an owner list: in shared memory beside the staged codes
+            // (one-segment sequences), else in the row's own CSR slots (a row has d <= Tw distinct
+            // k-mers: the list becomes the entries in place). Counting: one shared-memory atomic per
+            // window; a bin's first window (old count 0) appends its k-mer to the list. Emission:
+            // every owner once (its count read and its bin cleared), entry slot = owner index; the
+            // count >= 2 entries copied to the row's tail (free: Tw - d >= nhi).
             uint8_t *hb = reinterpret_cast<uint8_t *>(hist);
-            const int w1 = (int)Tw;
             const uint32_t lt = (1u << lane) - 1u;
             bool ovf = false;
-            for (int t0 = 0; t0 < w1; t0 += 32 * kCountUnroll) {
-                bool first[kCountUnroll];
-                uint32_t tau[kCountUnroll];
+            for (int g = 0; g < nseg; ++g) {
+                stage(g);
+                const int w1 = (int)min((int64_t)SW, Tw - (int64_t)g * SW);
+                for (int t0 = 0; t0 < w1; t0 += 32 * kCountUnroll) {
+                    bool first[kCountUnroll];
+                    uint32_t tau[kCountUnroll];
 #pragma unroll
-                for (int u = 0; u < kCountUnroll; ++u) {
-                    const int t = t0 + 32 * u + lane;
-                    first[u] = false;
-                    tau[u] = 0;
-                    if (t < w1) {
-                        tau[u] = window_tau<KT>(cod + sh + t, k, A);
-                        const uint32_t sh8 = (tau[u] & 3u) << 3;
-                        const uint32_t ob = (atomicAdd(&hist[tau[u] >> 2], 1u << sh8) >> sh8) & 0xFFu;
-                        ovf |= ob == 0xFFu;
-                        first[u] = ob == 0u;
+                    for (int u = 0; u < kCountUnroll; ++u) {
+                        const int t = t0 + 32 * u + lane;
+                        first[u] = false;
+                        tau[u] = 0;
+                        if (t < w1) {
+                            tau[u] = window_tau<KT>(cod + sh + t, k, A);
+                            const uint32_t sh8 = (tau[u] & 3u) << 3;
+                            const uint32_t ob = (atomicAdd(&hist[tau[u] >> 2], 1u << sh8) >> sh8) & 0xFFu;
+                            ovf |= ob == 0xFFu;
+                            first[u] = ob == 0u;
+                        }
                     }
-                }
+                    if (lst) {
 #pragma unroll
-                for (int u = 0; u < kCountUnroll; ++u) {
-                    const uint32_t fm = __ballot_sync(0xffffffffu, first[u]);
-                    lst[first[u] ? nl + __popc(fm & lt) : (uint32_t)w1] = (uint16_t)tau[u];   // slot Tw: a dummy
-                    nl += __popc(fm);
+                        for (int u = 0; u < kCountUnroll; ++u) {
+                            const uint32_t fm = __ballot_sync(0xffffffffu, first[u]);
+                            lst[first[u] ? nl + __popc(fm & lt) : (uint32_t)Tw] = (uint16_t)tau[u];   // slot Tw: a dummy
+                            nl += __popc(fm);
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < kCountUnroll; ++u) {
+                            const uint32_t fm = __ballot_sync(0xffffffffu, first[u]);
+                            if (first[u]) out[nl + __popc(fm & lt)] = tau[u] << 16;
+                            nl += __popc(fm);
+                        }
+                    }
                 }
             }
             __syncwarp();
@@ -373,7 +386,7 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
                         c[u] = 0;
                         tau[u] = 0;
                         if (e < nl) {
-                            tau[u] = lst[e];
+                            tau[u] = lst ? (uint32_t)lst[e] : out[e] >> 16;
                             c[u] = hb[tau[u]];
                             hb[tau[u]] = 0;
                             out[e] = (tau[u] << 16) | c[u];        // list order: slot = owner index
