@@ -10,7 +10,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 echo "ncu launches rc=$?"
 python tools/launches.py gpurun_out/launches_$tag.csv 0 > gpurun_out/launches_${tag}_summary.txt 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k "regex:k_profile|k_xrows_g|k_xfill|k_indicator|k_rank_vs_ga|k_seg_sort|k_merge_runs|k_syrk_tc|k_kstats|k_capscan|k_plan|k_rank_merge|k_gather_res|k_local_anc|k_lenscatter" \
+    -k "regex:k_profile<|k_xrows_g|k_xfill|k_indicator|k_rank_vs_ga|k_seg_sort|k_merge_runs|k_syrk_tc|k_shard_plan|k_plan|k_rank_merge|k_gather_res|k_local_anc|k_lenscatter|k_f1_" \
     -s 40 -c 16 -f -o gpurun_out/prof_$tag \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-graph "$@" > gpurun_out/ncu_full_$tag.log 2>&1
 echo "ncu full rc=$?"
