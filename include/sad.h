@@ -101,6 +101,17 @@ extern "C" {
                                  tensor-core kernel: the w x p(p-1) contraction of the shard's all-pairs
                                  operand with the samples' indicator rows on tcgen05 (the excess above
                                  the layer cap on the CUDA cores); both are exact. */
+#define SAD_F_TILE_SPLIT 512u /* SURVEY §8(f) row f2 across GPUs (PAPER.md:103 centralized rank, "rows sharded
+                                 over G"): every rank loads the SAME input (all N sequences, the profiles
+                                 recomputed on every rank) and the p shards stay whole on every rank (p may
+                                 be 1: the N x N all-pairs); the all-pairs tiles are split over the world
+                                 ranks by row blocks (longest-processing-time greedy on tile counts, the
+                                 same on every rank), K6 builds only the owned rows' excess, and T is summed
+                                 over the ranks with one ncclAllReduce on the library's communicator right
+                                 after the all-pairs kernel; everything after it is replicated (no exchange).
+                                 Needs the tensor-core kernel, not SAD_F_KEEP_SIM. Without an NCCL id the
+                                 reduction is skipped: T then holds this rank's partial sums only (the
+                                 emulation used by the tests). */
 #define SAD_F_TC_ALL_LAYERS 32u /* tensor-core path with every threshold layer t <= max n(tau) dense in the
                                  contraction. Default: the layers are capped per shard at the smallest
                                  T in {1,2,4,8} with max_i sum_tau (n_i(tau) - T)+ <= 255, and the

@@ -15,6 +15,7 @@ SAD_PROTEIN20, SAD_DNA4 = 0, 1
 SAD_F_KEEP_SIM, SAD_F_KERNEL_ALU, SAD_F_KERNEL_TC, SAD_F_TC_INT8, SAD_F_TC_1SM, SAD_F_TC_ALL_LAYERS = 1, 2, 4, 8, 16, 32
 SAD_F_RANK_SAMPLES = 64
 SAD_F_F1_CUDA_CORES = 128
+SAD_F_TILE_SPLIT = 512
 SAD_MEM_HOST, SAD_MEM_DEVICE, SAD_MEM_DEVICE_REBASE = 0, 1, 2
 ERRORS = {-1: "SAD_E_ARG", -2: "SAD_E_STATE", -3: "SAD_E_SYMBOL", -4: "SAD_E_TOO_SHORT", -5: "SAD_E_TOO_LONG",
           -6: "SAD_E_INSUFFICIENT", -7: "SAD_E_EMPTY", -8: "SAD_E_CAPACITY", -9: "SAD_E_CUDA", -10: "SAD_E_NCCL",

@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -755,10 +756,39 @@ int64_t tc_tiles_bound(int64_t n, int pl) {
     return (n / tc::BM + pl + 1) * (n / tc::Traits<1>::BN + pl + 1) + 1;
 }
 
-// the tile table of a layout, written to host memory (16 bytes per tile); returns the count
-int64_t tc_build_tiles(int pl, const int64_t *h_shard_base, int kind, int cg, void *host_out, int64_t cap) {
+// the tile table of a layout, written to host memory (16 bytes per tile); returns the count.
+// Tile split (split_world > 1): only the tiles of the row blocks that rank split_rank owns; the row
+// blocks (all shards, numbered consecutively) go to the ranks by longest-processing-time greedy on
+// their tile counts (the same deterministic assignment on every rank); own_out[rb] = 1 marks them.
+int64_t tc_build_tiles(int pl, const int64_t *h_shard_base, int kind, int cg, void *host_out, int64_t cap,
+                       int split_world, int split_rank, uint8_t *own_out) {
     std::vector<TcTile> t;
     build_tiles(pl, h_shard_base, tc_bn(kind), tc::BM * cg, t, cg == 2);
+    if (split_world > 1) {
+        const int bm = tc::BM * cg;
+        std::vector<int64_t> rb0(pl + 1, 0);
+        for (int s = 0; s < pl; ++s) rb0[s + 1] = rb0[s] + (h_shard_base[s + 1] - h_shard_base[s] + bm - 1) / bm;
+        std::vector<int64_t> work(rb0[pl], 0);
+        for (const TcTile &x : t) work[rb0[x.s] + x.I] += 1;
+        std::vector<int64_t> order(rb0[pl]);
+        for (int64_t i = 0; i < rb0[pl]; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return work[a] > work[b]; });
+        std::vector<int64_t> load(split_world, 0);
+        std::vector<int> owner(rb0[pl], 0);
+        for (int64_t rb : order) {
+            int r = 0;
+            for (int q = 1; q < split_world; ++q)
+                if (load[q] < load[r]) r = q;
+            owner[rb] = r;
+            load[r] += work[rb];
+        }
+        std::vector<TcTile> mine;
+        for (const TcTile &x : t)
+            if (owner[rb0[x.s] + x.I] == split_rank) mine.push_back(x);
+        t.swap(mine);
+        if (own_out)
+            for (int64_t rb = 0; rb < rb0[pl]; ++rb) own_out[rb] = owner[rb] == split_rank ? 1 : 0;
+    }
     if ((int64_t)t.size() > cap) return -1;
     std::memcpy(host_out, t.data(), t.size() * sizeof(TcTile));
     return (int64_t)t.size();

@@ -213,8 +213,9 @@ __global__ void __launch_bounds__(kXrWarps * 32, SAD_XR_MINB) k_xrows_g(ExcessAr
     for (; r < a.n; r += nw) {
         int s = 0;
         while (s + 1 < a.pl && r >= a.shard_base[s + 1]) ++s;
-        const uint32_t T = a.cap[s];
         const uint32_t local = (uint32_t)(r - a.shard_base[s]);          // sorted position (length order)
+        // tile split: rows of row blocks another rank computes need no excess here
+        const uint32_t T = (a.rb_own && !a.rb_own[(a.shard_rowpad[s] + local) / a.rb_rows]) ? kNoCap : a.cap[s];
         const int64_t w = a.shard_base[s + 1] - a.shard_base[s];
         const int nch = (int)((w + 15) >> 4);
         uint8_t *erow = a.E + a.ebase[s] + (int64_t)local * (nch * 16);

@@ -549,6 +549,41 @@ void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, int pl, 
     k_lenscatter<<<(unsigned)g, 256, 0, st>>>(rowinfo, shard_base, pl, n, pos, sigma, sigma_inv, rinfo_s);
 }
 
+// The deterministic length order (tile split: every rank must place the same sequences in the same
+// row blocks): keys (shard << 32) | Tw with the row as value for a stable sort (ties by index), then
+// sigma, sigma_inv and the sorted RowInfo from the sorted rows.
+__global__ void k_lenkeys(const RowInfo *rowinfo, int64_t n, unsigned long long *keys, int32_t *rows) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const RowInfo r = rowinfo[i];
+        keys[i] = ((unsigned long long)r.shard << 32) | r.tw;
+        rows[i] = (int32_t)i;
+    }
+}
+
+__global__ void k_lenapply(const int32_t *rows_sorted, const RowInfo *rowinfo, const int64_t *shard_base, int64_t n,
+                           int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = rows_sorted[p];
+        RowInfo r = rowinfo[i];
+        const int64_t b = shard_base[r.shard];
+        sigma[p] = (int32_t)(i - b);
+        sigma_inv[i] = (int32_t)(p - b);
+        r.shard = (uint32_t)(i - b);
+        rinfo_s[p] = r;
+    }
+}
+
+void launch_lenkeys(const RowInfo *rowinfo, int64_t n, unsigned long long *keys, int32_t *rows, cudaStream_t st) {
+    const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
+    if (g > 0) k_lenkeys<<<(unsigned)g, 256, 0, st>>>(rowinfo, n, keys, rows);
+}
+
+void launch_lenapply(const int32_t *rows_sorted, const RowInfo *rowinfo, const int64_t *shard_base, int64_t n,
+                     int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s, cudaStream_t st) {
+    const int64_t g = std::min<int64_t>(4096, (n + 255) / 256);
+    if (g > 0) k_lenapply<<<(unsigned)g, 256, 0, st>>>(rows_sorted, rowinfo, shard_base, n, sigma, sigma_inv, rinfo_s);
+}
+
 // K3, one block per shard, everything between the k-mer counts and the operand in one launch
 // (no host round trip):
 //  (1) statistics for every candidate cap T = 2^j (and no cap), after folding the presence bits

@@ -136,6 +136,9 @@ size_t record_bytes(const sad_ctx *c) { return (size_t)rup(16 + 2 * (int64_t)c->
 int64_t count_block(const sad_ctx *c) { return (int64_t)c->pl * c->cfg.p * 2 + 4; }   // counts + status tail
 
 // carve the workspace; with base == nullptr only the size is computed
+// rows per all-pairs row block (the tile height: 128, or 256 for CTA pairs)
+static inline int64_t tc_row_block(const sad_ctx *c) { return 128 * (int64_t)c->tc_cg; }
+
 size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     Bump b{base};
     const int pl = c->pl, p = c->cfg.p, V = c->V, G = c->cfg.world;
@@ -190,6 +193,7 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_counts = b.take<int64_t>((size_t)pl * p * 2);
     c->tc_tiles_cap = tc_tiles_bound(n, pl);
     c->d_tc_tiles = b.take<uint8_t>((size_t)c->tc_tiles_cap * 16);
+    c->d_rb_own = b.take<uint8_t>((size_t)(n / 128 + pl + 2));   // per 128 padded operand rows
     c->cub_bytes = cub_bytes_needed(n, pl);
     c->d_cub = b.take<uint8_t>(c->cub_bytes);
     // collective API: exchange records, samples and counts (this rank's and all ranks')
@@ -256,7 +260,8 @@ OutLayout out_layout(uint8_t *base, int64_t n, int64_t r, bool recv) {
 }
 
 // the collective path moves the buckets through NCCL (always when the context has a communicator)
-inline bool coll_exchange(const sad_ctx *c) { return c->comm != nullptr; }
+// the data-path exchanges run on the communicator (a tile-split context uses it for T only)
+inline bool coll_exchange(const sad_ctx *c) { return c->comm != nullptr && c->tile_world == 1; }
 
 void sum_recv(const sad_ctx *c, const int64_t *h_counts_all, int64_t &n_out, int64_t &r_out) {
     const int p = c->cfg.p, bpr = c->pl;
@@ -445,7 +450,9 @@ int sad_create(const sad_config *cfg, const uint8_t *nccl_id, sad_ctx **out) {
     if (cfg->alphabet != SAD_PROTEIN20 && cfg->alphabet != SAD_DNA4) return SAD_E_ARG;
     if (cfg->k < 1 || cfg->p < 1 || cfg->p > 64 || cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world)
         return SAD_E_ARG;
-    if (cfg->p % cfg->world != 0) return SAD_E_ARG;
+    const bool split = (cfg->flags & SAD_F_TILE_SPLIT) != 0;
+    if (split && ((cfg->flags & SAD_F_KERNEL_ALU) || (cfg->flags & SAD_F_KEEP_SIM))) return SAD_E_ARG;
+    if (!split && cfg->p % cfg->world != 0) return SAD_E_ARG;
     if ((cfg->flags & SAD_F_RANK_SAMPLES) && cfg->p < 2) return SAD_E_ARG;   // f1 needs k = p-1 >= 1 samples
     const int A = cfg->alphabet == SAD_PROTEIN20 ? 20 : 4;
     int64_t V = 1;
@@ -462,11 +469,19 @@ int sad_create(const sad_config *cfg, const uint8_t *nccl_id, sad_ctx **out) {
     sad_ctx *ctx = new (std::nothrow) sad_ctx();
     if (!ctx) return SAD_E_OOM;
     ctx->cfg = *cfg;
+    if (split) {
+        // the data path is a world-1 path on the whole input; world / rank only split the all-pairs tiles
+        ctx->tile_world = cfg->world;
+        ctx->tile_rank = cfg->rank;
+        ctx->tile_reduce = nccl_id != nullptr && cfg->world > 1;
+        ctx->cfg.world = 1;
+        ctx->cfg.rank = 0;
+    }
     ctx->st = reinterpret_cast<cudaStream_t>(cfg->stream);
     ctx->A = A;
     ctx->V = (int)V;
-    ctx->pl = cfg->p / cfg->world;
-    ctx->shard0 = cfg->rank * ctx->pl;
+    ctx->pl = ctx->cfg.p / ctx->cfg.world;
+    ctx->shard0 = ctx->cfg.rank * ctx->pl;
     ctx->use_tc = !(cfg->flags & SAD_F_KERNEL_ALU);
     ctx->tc_kind = (cfg->flags & SAD_F_TC_INT8) ? 0 : 1;
     ctx->f1_tc = ctx->use_tc && ctx->tc_kind == 1 && (cfg->flags & SAD_F_RANK_SAMPLES) &&
@@ -688,7 +703,26 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
                 CK(cudaMallocHost(&ctx->h_tiles, need_b));
                 ctx->h_tiles_bytes = need_b;
             }
-            ctx->tc_tiles_n = tc_build_tiles(ctx->pl, sb.data(), ctx->tc_kind, ctx->tc_cg, ctx->h_tiles, ctx->tc_tiles_cap);
+            // tile split: the owned row blocks (of tile height), re-indexed per 128 padded operand rows
+            // (shards are padded to 128 rows, so every 128-row block lies in one shard and one row block)
+            std::vector<uint8_t> own_rb;
+            if (ctx->tile_world > 1) own_rb.assign((size_t)(ctx->n / tc_row_block(ctx) + ctx->pl + 2), 0);
+            ctx->tc_tiles_n = tc_build_tiles(ctx->pl, sb.data(), ctx->tc_kind, ctx->tc_cg, ctx->h_tiles,
+                                             ctx->tc_tiles_cap, ctx->tile_world, ctx->tile_rank,
+                                             own_rb.empty() ? nullptr : own_rb.data());
+            if (!own_rb.empty()) {
+                const int64_t nb128 = ctx->rows_pad / 128;
+                if (nb128 > 16384 * 8) return fail(ctx, SAD_E_ARG, "tile split: too many row blocks");
+                uint8_t *own = reinterpret_cast<uint8_t *>(ctx->h_small + 48000);   // staging, <= 128 KB
+                int64_t rb0 = 0;
+                for (int s = 0; s < ctx->pl; ++s) {
+                    const int64_t w = sb[s + 1] - sb[s], bm = tc_row_block(ctx);
+                    for (int64_t b = 0; b < (w + 127) / 128; ++b)
+                        own[ctx->shard_rowpad[s] / 128 + b] = own_rb[(size_t)(rb0 + (128 * b) / bm)];
+                    rb0 += (w + bm - 1) / bm;
+                }
+                CK(cudaMemcpyAsync(ctx->d_rb_own, own, (size_t)nb128, cudaMemcpyHostToDevice, ctx->st));
+            }
             if (ctx->tc_tiles_n < 0) return fail(ctx, SAD_E_OOM, "tile table exceeds its bound");
             if (ctx->tc_tiles_n > 0)
                 CK(cudaMemcpyAsync(ctx->d_tc_tiles, ctx->h_tiles, (size_t)ctx->tc_tiles_n * 16, cudaMemcpyHostToDevice,
@@ -802,7 +836,25 @@ int sad_build_profiles(sad_ctx *ctx) {
                       ctx->d_col0, ctx->d_xoff, xtot_of(ctx), ctx->d_xcur, ctx->use_tc ? ctx->d_lcnt : nullptr,
                       ctx->d_lcnt + (size_t)pl * kLenBinsMax, ctx->d_shard_base, ctx->st);
     LAUNCHED();
-    if (ctx->use_tc) {     // the length order's slot scatter (histogram: K1/K2, bin offsets: K3)
+    if (ctx->use_tc && ctx->tile_world > 1) {
+        // tile split: every rank must hold the same rows in the same row blocks -- the length order by
+        // a stable sort (ties by index) instead of the scatter's arbitrary order within a length
+        launch_lenkeys(ctx->d_rowinfo, ctx->n, ctx->d_ckey, ctx->d_perm_in, ctx->st);
+        LAUNCHED();
+        int sbits = 0;
+        while ((1 << sbits) < pl) ++sbits;
+        if (!(ctx->max_w <= (int64_t)16384 &&
+              seg_sort_pairs_runs(ctx->d_ckey, ctx->d_perm_in, ctx->d_shard_base, pl, ctx->max_w, ctx->n,
+                                  ctx->d_ckey_sorted, ctx->d_perm_sorted, 16, ctx->st) == 0)) {
+            // one stable device radix sort of (shard << 32 | Tw)
+            CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
+                          32 + sbits));
+        }
+        LAUNCHED();
+        launch_lenapply(ctx->d_perm_sorted, ctx->d_rowinfo, ctx->d_shard_base, ctx->n, ctx->d_sigma, ctx->d_sigma_inv,
+                        ctx->d_rinfo_s, ctx->st);
+        LAUNCHED();
+    } else if (ctx->use_tc) {     // the length order's slot scatter (histogram: K1/K2, bin offsets: K3)
         launch_lenorder(ctx->d_rowinfo, ctx->d_shard_base, pl, ctx->n, ctx->d_lcnt + (size_t)pl * kLenBinsMax,
                         ctx->d_sigma, ctx->d_sigma_inv, ctx->d_rinfo_s, ctx->st);
         LAUNCHED();
@@ -924,6 +976,9 @@ static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, 
             x.sigma = ctx->d_sigma;
             x.sigma_inv = ctx->d_sigma_inv;
             x.rowinfo = ctx->d_rowinfo;
+            x.rb_own = ctx->tile_world > 1 ? ctx->d_rb_own : nullptr;
+            x.shard_rowpad = ctx->d_shard_rowpad;
+            x.rb_rows = 128;
             launch_xfill(x, ctx->d_xcur, ctx->st);
             LAUNCHED();
             // K6 rows on the side stream, concurrently with K4 (both only read the CSR / lists)
@@ -978,6 +1033,8 @@ static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, 
         launch_allpairs_alu(ap, ctx->st);
     }
     LAUNCHED();
+    if (ctx->tile_reduce)        // tile split: T_i = the sum of every rank's tiles (integer sums, exact)
+        NK(ncclAllReduce(ctx->d_T, ctx->d_T, (size_t)ctx->n, ncclUint64, ncclSum, comm_of(ctx), ctx->st));
     record_pair(ctx, ctx->ev_pairs_ap, false, 3);
     if (!ctx->capturing) ctx->calls += 1;
 
@@ -1156,7 +1213,7 @@ int sad_rank(sad_ctx *ctx, void *d_operand, size_t operand_bytes) {
     if (int rc = rank_local_impl(ctx, d_operand, operand_bytes, ctx->d_anc_mine)) return rc;
     // "Send the k samples from each processor to all the processors": the ancestor records
     const void *anc_all = ctx->d_anc_mine;
-    if (ctx->comm) {
+    if (coll_exchange(ctx)) {
         const size_t bytes = (size_t)exchange_records(ctx) * record_bytes(ctx);
         NK(ncclAllGather(ctx->d_anc_mine, ctx->d_anc_all, bytes, ncclUint8, comm_of(ctx), ctx->st));
         anc_all = ctx->d_anc_all;
@@ -1482,7 +1539,7 @@ int sad_partition(sad_ctx *ctx, void *d_out, size_t out_bytes, int64_t *h_bucket
     ctx->capturing = stream_capturing(ctx->st);
     // a9: "Sort all the p*(p-1) ranks ..." -- every rank's regular samples, replicated selection
     const uint64_t *smp_all = reinterpret_cast<const uint64_t *>(ctx->d_smp_mine);
-    if (ctx->comm && p > 1) {
+    if (coll_exchange(ctx) && p > 1) {
         NK(ncclAllGather(ctx->d_smp_mine, ctx->d_smp_all, (size_t)pl * (p - 1), ncclUint64, comm_of(ctx), ctx->st));
         smp_all = reinterpret_cast<const uint64_t *>(ctx->d_smp_all);
     }

@@ -144,6 +144,10 @@ void launch_indicator(const OperandArgs &a, cudaStream_t st);
 // slot scatter -> sigma, sigma_inv, rinfo_s (ties in arbitrary order); 3 launches + 1 memset
 void launch_lenorder(const RowInfo *rowinfo, const int64_t *shard_base, int pl, int64_t n, uint32_t *pos,
                      int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s, cudaStream_t st);
+// the same order made deterministic (ties by index; tile split): keys, a stable sort, then apply
+void launch_lenkeys(const RowInfo *rowinfo, int64_t n, unsigned long long *keys, int32_t *rows, cudaStream_t st);
+void launch_lenapply(const int32_t *rows_sorted, const RowInfo *rowinfo, const int64_t *shard_base, int64_t n,
+                     int32_t *sigma, int32_t *sigma_inv, RowInfo *rinfo_s, cudaStream_t st);
 // K6: the sparse excess of the capped layers (k_excess.cu),
 //   e_ij = sum_tau min((n_i(tau) - T_s)+, (n_j(tau) - T_s)+)   for i < j in shard s,
 // as a dense u8 matrix E_s[r][c] over sorted positions (length order; row pitch rup(w_s, 16);
@@ -163,6 +167,9 @@ struct ExcessArgs {
     const int32_t *sigma;            // [n] length order: sorted position -> local index
     const int32_t *sigma_inv;        // [n] local index -> sorted position
     const RowInfo *rowinfo;          // [n] input order (.shard)
+    const uint8_t *rb_own;           // tile split: [row blocks] 1 = this rank computes the row block's tiles, or NULL
+    const int64_t *shard_rowpad;     // device [pl+1] (row block of a row: (rowpad[s] + local) / rb_rows)
+    int rb_rows;                     // rows per row block (the all-pairs tile height)
     uint2 *xrow;                     // [n] .x = 1 if the row (sorted position) has excess
     uint8_t *E;                      // dense excess rows
     uint8_t *zero_seg;               // 256 bytes zeroed by k_xfill (the staging source of rows without excess)
@@ -206,7 +213,8 @@ int launch_allpairs_tc(const AllPairsArgs &a, cudaStream_t st, std::string &err)
 bool tc_supported(std::string &why);
 int64_t tc_tiles_bytes(int pl, const int64_t *h_shard_base, int kind, int cg);
 int64_t tc_tiles_bound(int64_t n, int pl);
-int64_t tc_build_tiles(int pl, const int64_t *h_shard_base, int kind, int cg, void *host_out, int64_t cap);
+int64_t tc_build_tiles(int pl, const int64_t *h_shard_base, int kind, int cg, void *host_out, int64_t cap,
+                       int split_world = 1, int split_rank = 0, uint8_t *own_out = nullptr);
 int tc_bn(int kind);
 
 struct AncArgs {
@@ -487,6 +495,9 @@ struct sad_ctx {
     int64_t kcap_blocks = 0;                         // operand K capacity (128-byte blocks per row)
     int64_t kcap_next = 0;                           // the capacity the next step starts with
     bool f1_tc = false;              // f1 rank vs samples as a tensor-core contraction (F1Args)
+    int tile_world = 1, tile_rank = 0;   // SAD_F_TILE_SPLIT: the all-pairs tiles split over tile_world ranks
+    bool tile_reduce = false;        // ... and T summed over them on the communicator (else: the caller's job)
+    uint8_t *d_rb_own = nullptr;     // [row blocks] tiles owned by this rank (K6 skips the other rows)
     int64_t kmax_blocks_seen = -1;                   // largest K blocks of the last absorbed step (-1: none)
     bool allow_cap = false;                          // capped layers + K6 excess possible in this layout
     int64_t x_entries_bound = 0;                     // K6 list entries bound (all CSR entries)

@@ -110,11 +110,15 @@ class Context:
 
     def __init__(self, alphabet: str, k: int, p: int, *, world: int = 1, rank: int = 0, device: int | None = None,
                  stream: torch.cuda.Stream | None = None, kernel: str = "tc", keep_sim: bool = False, group=None,
-                 rank_mode: str = "ga", comm: bool = False, f1_cuda_cores: bool = False):
+                 rank_mode: str = "ga", comm: bool = False, f1_cuda_cores: bool = False,
+                 tile_split: bool = False):
         """comm: give the library its own NCCL communicator (sad_create with an id that rank 0 draws
         and torch.distributed broadcasts over `group`): the collective calls sad_rank / sad_partition
         then run every exchange themselves. Needed by run() when world > 1; with world == 1 it makes
-        the exchange steps run through NCCL anyway (a single-rank communicator)."""
+        the exchange steps run through NCCL anyway (a single-rank communicator).
+        tile_split (SAD_F_TILE_SPLIT, SURVEY §8(f) f2 across GPUs): every rank loads the whole input
+        and keeps all p shards; only the all-pairs tiles are split over the world ranks and T summed
+        over them on the communicator (comm=True; without it T holds the rank's partial sums)."""
         if not torch.cuda.is_available():
             raise RuntimeError("the k-mer-rank path needs a CUDA device (no CPU fallback)")
         if device is None:
@@ -122,13 +126,18 @@ class Context:
         self.device = torch.device("cuda", device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.alphabet, self.k, self.p, self.world, self.rank, self.group = alphabet, k, p, world, rank, group
-        self.pl = p // world
+        self.tile_world = world if tile_split else 1
+        if tile_split:                      # the data path is world 1 on the whole input
+            self.world, self.rank, self.pl = 1, 0, p
+        else:
+            self.pl = p // world
         if kernel not in KERNELS:
             raise ValueError(f"kernel must be one of {sorted(KERNELS)}, not {kernel!r}")
         if rank_mode not in ("ga", "samples"):
             raise ValueError(f"rank_mode must be 'ga' or 'samples', not {rank_mode!r}")
         flags = (L.SAD_F_KEEP_SIM if keep_sim else 0) | KERNELS[kernel] | (
-            L.SAD_F_RANK_SAMPLES if rank_mode == "samples" else 0) | (L.SAD_F_F1_CUDA_CORES if f1_cuda_cores else 0)
+            L.SAD_F_RANK_SAMPLES if rank_mode == "samples" else 0) | (L.SAD_F_F1_CUDA_CORES if f1_cuda_cores else 0) | (
+            L.SAD_F_TILE_SPLIT if tile_split else 0)
         self.rank_mode = rank_mode
         self.kernel = kernel
         cfg = L.SadConfig(ALPHABETS[alphabet], k, p, world, rank, device, self.stream.cuda_stream, flags)

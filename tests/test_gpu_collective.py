@@ -157,3 +157,56 @@ def test_abort_and_errors():
     with pytest.raises(SadError) as e:
         ctx.run()
     assert e.value.name == "SAD_E_SYMBOL" and e.value.location == (37, 10)
+
+
+@pytest.mark.parametrize("kernel", ["tc", "tc1", "tc8"])
+@pytest.mark.parametrize("case", [("cfg2", 1, 3), ("cfg2", 8, 4), ("cfg3s", 1, 8), ("excess", 2, 3)])
+def test_tile_split_emulated(kernel, case):
+    """SAD_F_TILE_SPLIT (SURVEY §8(f) f2 across GPUs): G contexts, each with the whole input, every
+    one computing only its row blocks' tiles (and their K6 excess rows), no communicator: their
+    partial T summed on the host equals the oracle's T element by element (every tile exactly once,
+    the excess of every computed pair present)."""
+    from paper_0901_2742_b200.runtime import Context
+    name, p, G = case
+    if name == "cfg2":
+        spec = gen.SPECS[2]
+        a, o = gen.generate(spec)
+        alpha, k = spec.alphabet, spec.k
+    elif name == "cfg3s":
+        spec = gen.SPECS[3]
+        a, o = gen.generate(spec, n=3000, seed=41)
+        alpha, k = spec.alphabet, spec.k
+    else:                                   # repeats: shards with layer caps and K6 excess rows
+        rng = np.random.default_rng(43)
+        al = list("ACDEFGHIKLMNPQRSTVWY")
+        seqs = ["".join(rng.choice(al, int(rng.integers(40, 400)))) + "".join(rng.choice(al, 4)) * int(rng.integers(1, 9))
+                for _ in range(1500)]
+        a, o = gen.from_strings(seqs)
+        alpha, k = "protein", 3
+    n = len(o) - 1
+    r = oracle.run(a, o, alpha, k, p)
+    T = np.zeros(n, np.uint64)
+    for rank in range(G):
+        ctx = Context(alpha, k, p, world=G, rank=rank, kernel=kernel, tile_split=True)
+        ctx.load(a, o, n, 0)
+        ctx.run()
+        T += np.concatenate([ctx.local_rank(s) for s in range(p)])
+        ctx.close()
+    assert np.array_equal(T, r.T)
+
+
+@pytest.mark.parametrize("p", [1, 8])
+def test_tile_split_single_rank_reduce(p):
+    """Tile split with a (single-rank) NCCL communicator: the ncclAllReduce of T runs inside
+    sad_rank right after the all-pairs kernel; the whole step then matches the oracle."""
+    from paper_0901_2742_b200.runtime import Context
+    spec = gen.SPECS[2]
+    a, o = gen.generate(spec)
+    n = len(o) - 1
+    ctx = Context(spec.alphabet, spec.k, p, world=1, rank=0, tile_split=True, comm=True)
+    ctx.load(a, o, n, 0)
+    sizes = ctx.run()
+    r = oracle.run(a, o, spec.alphabet, spec.k, p)
+    assert sizes.tolist() == r.bsize.tolist()
+    _full_compare(ctx, a, o, p, r)
+    ctx.close()
