@@ -46,6 +46,9 @@ def parse():
                     help="with --rank-mode samples: the rank against the samples on the CUDA cores")
     ap.add_argument("--e2e-sequential", action="store_true",
                     help="e2e as separately timed sequential steps (default at N=1: the double-buffered Pipeline)")
+    ap.add_argument("--tile-split", action="store_true",
+                    help="f2 across GPUs (SAD_F_TILE_SPLIT): every rank holds the whole input, the all-pairs tiles "
+                         "are split over the ranks, T all-reduced (use with --p 1 for the centralized rank)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--oracle-threads", type=int, default=0,
@@ -194,11 +197,11 @@ def main():
 
     a, o = gen.generate(spec)
     n = len(o) - 1
-    if p % world:
+    if p % world and not args.tile_split:
         raise SystemExit(f"p={p} must be a multiple of the GPU count {world}")
-    pl = p // world
+    pl = p if args.tile_split else p // world
     sb = gen.shard_bounds(n, p)
-    lo, hi = sb[rank * pl], sb[(rank + 1) * pl]
+    lo, hi = (0, n) if args.tile_split else (sb[rank * pl], sb[(rank + 1) * pl])
     a_loc = np.ascontiguousarray(a[o[lo]: o[hi]])
     o_loc = np.ascontiguousarray(o[lo: hi + 1] - o[lo])
     dev = torch.device("cuda", local_rank)
@@ -212,7 +215,7 @@ def main():
     # world > 1: the library's own NCCL communicator runs every exchange (collective API)
     ctx = Context(spec.alphabet, spec.k, p, world=world, rank=rank, device=local_rank, stream=stream,
                   kernel=args.kernel, group=group, rank_mode=args.rank_mode, comm=world > 1,
-                  f1_cuda_cores=args.f1_cuda_cores)
+                  f1_cuda_cores=args.f1_cuda_cores, tile_split=args.tile_split)
     R_glob = int(o[-1])
 
     def barrier():
@@ -348,12 +351,15 @@ def main():
     except Exception:
         pass
     _, _, kcols = ctx.profile_info()
-    w_loc = [sb[rank * pl + s + 1] - sb[rank * pl + s] for s in range(pl)]
+    s0 = 0 if args.tile_split else rank * pl
+    w_loc = [sb[s0 + s + 1] - sb[s0 + s] for s in range(pl)]
     fp4 = args.kernel in ("tc", "tc1", "tcfull")
     if args.kernel.startswith("tc"):
         # algorithmic dense work of the threshold-indicator SYRK: 2 * K_s ops per pair i <= j
         # (SURVEY §8(d) f_tc numerator: sum_s w_s (w_s + 1) K_s)
         ops = sum(2 * (w * (w + 1) // 2) * int(k) for w, k in zip(w_loc, kcols))
+        if args.tile_split:                # this rank's share of the tiles (LPT-balanced row blocks)
+            ops //= world
         bf16 = peaks.get("bf16_tflops")
         if bf16:
             # primary: the driver-measured bf16 burst x the nominal dense ratio of the operand dtype
@@ -430,7 +436,8 @@ def main():
             "config": {"workload": workload_name(spec, p), "p": p, "kernel": args.kernel, "rank_mode": args.rank_mode,
                        "step": ("one CUDA graph replay (sad_load .. sad_partition captured)" if graph is not None
                                 else "eager C-ABI calls (sad_load, sad_build_profiles, sad_rank, sad_partition)"),
-                       "exchange": "library NCCL communicator (collective API)" if world > 1 else "none (G = 1)",
+                       "exchange": ("ncclAllReduce of T (tile split, f2)" if args.tile_split and world > 1 else
+                                    "library NCCL communicator (collective API)" if world > 1 else "none (G = 1)"),
                        "pairs_per_step": pairs_job,
                        "l2": "L2 flushed (256 MB write) before every timed step; operand working set > L2"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,
