@@ -735,13 +735,17 @@ static void build_tiles(int pl, const int64_t *h_shard_base, int bn, int bm, std
         // CTA pairs: the shard's last column block runs with N = the real columns rounded up to 16
         const int64_t rem = w - (int64_t)(nJ - 1) * bn;
         const int nlast = (edge_n && rem < bn) ? (int)((rem + 15) / 16 * 16) : 0;
+        // the narrow last-column tiles (about half a full tile's time: bound by their A loads) go
+        // after the shard's full tiles, so that they fill the last round of the persistent schedule
+        std::vector<TcTile> edge;
         for (int j0 = 0; j0 < nJ; j0 += kGroupJ)
             for (int I = 0; I < nI; ++I) {
                 const int64_t need = (int64_t)bm * I - (bn - 1);
                 const int jmin = need <= 0 ? 0 : (int)((need + bn - 1) / bn);
                 for (int J = std::max(j0, jmin); J < std::min(nJ, j0 + kGroupJ); ++J)
-                    out.push_back(TcTile{s, I, J, J == nJ - 1 ? nlast : 0});
+                    (J == nJ - 1 && nlast ? edge : out).push_back(TcTile{s, I, J, J == nJ - 1 ? nlast : 0});
             }
+        out.insert(out.end(), edge.begin(), edge.end());
     }
 }
 

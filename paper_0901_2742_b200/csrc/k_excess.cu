@@ -36,8 +36,12 @@ constexpr int kXrWarps = 8;
 #endif
 
 // K6 lists: every entry above its shard's cap goes to L_tau as (row << 8) | (n - T_s), one warp
-// per row over the row's count >= 2 entries (its CSR tail; positions from per-(shard, tau) cursors)
-__global__ void __launch_bounds__(256) k_xfill(ExcessArgs a, uint32_t *xcur) {
+// per row over the row's count >= 2 entries (its CSR tail; positions from per-(shard, tau) cursors).
+// lpos != NULL: the length order's slot scatter (k_lenscatter) fused in: lane 0 takes the row's
+// sorted position from its Tw bin and writes sigma, sigma_inv and the sorted RowInfo (one launch
+// and one grid-wide pass fewer per step).
+__global__ void __launch_bounds__(256) k_xfill(ExcessArgs a, uint32_t *xcur, uint32_t *lpos, int32_t *sigma,
+                                               int32_t *sigma_inv, RowInfo *rinfo_s) {
     __shared__ unsigned long long lbase[kMaxLocalShards + 1];
     if (blockIdx.x == 0 && threadIdx.x < 16 && a.zero_seg)
         reinterpret_cast<uint4 *>(a.zero_seg)[threadIdx.x] = make_uint4(0, 0, 0, 0);
@@ -52,12 +56,28 @@ __global__ void __launch_bounds__(256) k_xfill(ExcessArgs a, uint32_t *xcur) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * 8;
     for (int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); r < a.n; r += nw) {
-        const int s = (int)a.rowinfo[r].shard;    // input order: K1/K2 recorded the row's shard
+        RowInfo ri = a.rowinfo[r];
+        const int s = (int)ri.shard;              // input order: K1/K2 recorded the row's shard
+        uint32_t local;                           // the row's position in length order
+        if (lpos) {
+            uint32_t p = 0;
+            if (lane == 0) {
+                const int64_t b = a.shard_base[s];
+                p = atomicAdd(&lpos[(size_t)s * kLenBinsMax + ri.tw], 1u);   // global sorted position
+                sigma[p] = (int32_t)(r - b);
+                sigma_inv[r] = (int32_t)(p - b);
+                ri.shard = (uint32_t)(r - b);
+                rinfo_s[p] = ri;
+                p -= (uint32_t)b;
+            }
+            local = __shfl_sync(0xffffffffu, p, 0);
+        } else {
+            local = (uint32_t)a.sigma_inv[r];
+        }
         const uint32_t T = a.cap[s];
         if (T == kNoCap) continue;
         const int dh = a.nhi[r];                  // the count >= 2 entries: the row's CSR tail
         const uint32_t *ent = a.csr + (a.off[r + 1] - (r + 1) * (int64_t)(a.k - 1)) - dh;
-        const uint32_t local = (uint32_t)a.sigma_inv[r];      // the row's position in length order
         for (int e = lane; e < dh; e += 32) {
             const uint32_t v = ent[e], n = v & 0xFFFFu;
             if (n > T) {
@@ -69,12 +89,13 @@ __global__ void __launch_bounds__(256) k_xfill(ExcessArgs a, uint32_t *xcur) {
     }
 }
 
-void launch_xfill(const ExcessArgs &a, uint32_t *xcur, cudaStream_t st) {
+void launch_xfill(const ExcessArgs &a, uint32_t *xcur, uint32_t *lpos, int32_t *sigma, int32_t *sigma_inv,
+                  RowInfo *rinfo_s, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t grid = std::min<int64_t>((int64_t)sms * 8, (a.n + 7) / 8);
-    if (grid > 0) k_xfill<<<(unsigned)grid, 256, 0, st>>>(a, xcur);
+    if (grid > 0) k_xfill<<<(unsigned)grid, 256, 0, st>>>(a, xcur, lpos, sigma, sigma_inv, rinfo_s);
 }
 
 __global__ void __launch_bounds__(kXrWarps * 32) k_xrows(ExcessArgs a, int warps) {

@@ -63,6 +63,9 @@ template <int KT>
 __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(ProfileArgs a, int warps, int hbytes) {
     extern __shared__ __align__(16) uint32_t psm[];
     __shared__ uint8_t lut[256];
+    __shared__ int fin_s[kProfWarps];                    // each warp's shard at the end
+    __shared__ unsigned long long bk_w, bk_d, bk_tw;     // the block's totals for the first warp's final shard
+    __shared__ uint32_t bk_ex[kNumCaps];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int t = threadIdx.x; t < 256; t += blockDim.x) lut[t] = 255;
     __syncthreads();
@@ -76,6 +79,13 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
     uint32_t *pres = hist + hw + kCodeBuf / 4;  // k-mers seen by this warp in the current shard
     for (int t = lane; t < hw; t += 32) hist[t] = 0;
     for (int t = lane; t < VW; t += 32) pres[t] = 0;
+    // block presence bits (after the warps' slices): zeroed here, written only after the end barrier
+    uint32_t *bpres = psm + (size_t)warps * (hw + kCodeBuf / 4 + ((VW + 3) & ~3));
+    if (wid == 0) {
+        for (int t = lane; t < VW; t += 32) bpres[t] = 0;
+        if (lane == 0) bk_w = bk_d = bk_tw = 0;
+        if (lane < kNumCaps) bk_ex[lane] = 0;
+    }
     __syncwarp();
 
     const int k = KT > 0 ? KT : a.k;
@@ -135,8 +145,18 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         for (int j = 0; j < kNumCaps; ++j) exm[j] = 0;
     };
     const int SW = kCodeSeg - (k - 1);   // windows per segment
-    // the next sequence's offsets and first 512 residue bytes are loaded during the current one
-    int64_t off_c = i0 < i1 ? a.off[i0] : 0, off_e = i0 < i1 ? a.off[i0 + 1] : 0;
+    // the warp's offsets, 32 sequences at a time in the lanes' registers with the next 32 already
+    // loaded (off[ob + d] = lane d of ochunk, d < 32, else of onext): no offset load on the
+    // per-sequence path; the next sequence's first 512 residue bytes are loaded during the current one
+    int64_t ob = i0;
+    int64_t ochunk = i0 + lane <= i1 ? a.off[i0 + lane] : 0;
+    int64_t onext = i0 + 32 + lane <= i1 ? a.off[i0 + 32 + lane] : 0;
+    auto offat = [&](int64_t q) -> int64_t {             // q in [ob, ob + 64); warp-uniform
+        const int d = (int)(q - ob);
+        const int64_t v0 = __shfl_sync(0xffffffffu, ochunk, d & 31), v1 = __shfl_sync(0xffffffffu, onext, d & 31);
+        return d < 32 ? v0 : v1;
+    };
+    int64_t off_c = i0 < i1 ? offat(i0) : 0, off_e = i0 < i1 ? offat(i0 + 1) : 0;
     uint4 qpre = i0 < i1 ? *reinterpret_cast<const uint4 *>(a.ascii + ((off_c & ~int64_t(15)) + 16 * lane))
                          : make_uint4(0, 0, 0, 0);
     int64_t s_end = a.shard_base[s + 1];                       // end of the current shard
@@ -151,9 +171,14 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         const int64_t off0 = off_c;
         const int64_t L = off_e - off0;
         const uint4 qfirst = qpre;                             // residues [off0 & ~15, +512) of this lane
+        if (i + 2 - ob >= 32) {                              // slide the offset window by 32
+            ob += 32;
+            ochunk = onext;
+            onext = ob + 32 + lane <= i1 ? a.off[ob + 32 + lane] : 0;
+        }
         if (i + 1 < i1) {
             off_c = off_e;
-            off_e = a.off[i + 2];
+            off_e = offat(i + 2);
             qpre = *reinterpret_cast<const uint4 *>(a.ascii + ((off_c & ~int64_t(15)) + 16 * lane));
         }
         const uint8_t *x = a.ascii + off0;
@@ -475,7 +500,49 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         acc_d += n_d;
         __syncwarp();
     }
-    flush();
+    // the final flush, merged per block: the warps that end in the same shard as warp 0 OR their
+    // presence bits and add their totals in shared memory, then the block updates global memory once
+    // (at G = 8 every warp ends in the one shard: ~10x fewer contended global atomics); the others
+    // flush on their own
+    if (lane == 0) fin_s[wid] = s;
+    asm volatile("bar.sync 1, %0;" ::"r"(warps * 32) : "memory");
+    const int s0 = fin_s[0];
+    if (s == s0) {
+        for (int t = lane; t < VW; t += 32) {
+            const uint32_t b = pres[t];
+            if (b) {
+                atomicOr(&bpres[t], b);
+                pres[t] = 0;
+            }
+        }
+        if (lane == 0) {
+            if (acc_w | acc_d) {
+                atomicAdd(&bk_w, acc_w);
+                atomicAdd(&bk_d, acc_d);
+                atomicMax(&bk_tw, max_tw);
+            }
+#pragma unroll
+            for (int j = 0; j < kNumCaps; ++j)
+                if (exm[j]) atomicMax(&bk_ex[j], exm[j]);
+        }
+    } else {
+        flush();
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(warps * 32) : "memory");
+    for (int t = threadIdx.x; t < VW; t += warps * 32) {
+        const uint32_t b = bpres[t];
+        if (b) atomicOr(&a.Mb[(size_t)s0 * VW + t], b);
+    }
+    if (threadIdx.x == 0) {
+        if (bk_w | bk_d) {
+            atomicAdd(&a.kinfo[s0 * kKinfo + 0], bk_w);
+            atomicAdd(&a.kinfo[s0 * kKinfo + 1], bk_d);
+            atomicMax(&a.kinfo[s0 * kKinfo + 3], bk_tw);
+        }
+#pragma unroll
+        for (int j = 0; j < kNumCaps; ++j)
+            if (bk_ex[j]) atomicMax(&a.kinfo[s0 * kKinfo + 4 + j], (unsigned long long)bk_ex[j]);
+    }
 }
 
 __global__ void k_profile_reset(uint32_t *M, size_t nM, uint32_t *Mb, size_t nMb, uint32_t *Xc, size_t nXc,
@@ -504,8 +571,9 @@ void launch_profile(const ProfileArgs &a, cudaStream_t st) {
     const int wide = 2 * ((a.V + kWidePasses - 1) / kWidePasses);
     const int hbytes = (std::max(narrow, wide) + 15) / 16 * 16;
     const size_t per_warp = (size_t)hbytes + kCodeBuf + 4 * (size_t)((((a.V + 31) / 32) + 3) & ~3);
-    const int warps = (int)std::max<size_t>(1, std::min<size_t>(kProfWarps, (size_t)(220 * 1024 / SAD_PROF_MINB) / per_warp));
-    const size_t smem = per_warp * warps;
+    const size_t bbits = 4 * (size_t)((((a.V + 31) / 32) + 3) & ~3);
+    const int warps = (int)std::max<size_t>(1, std::min<size_t>(kProfWarps, ((size_t)(220 * 1024 / SAD_PROF_MINB) - bbits) / per_warp));
+    const size_t smem = per_warp * warps + 4 * (size_t)((((a.V + 31) / 32) + 3) & ~3);   // + the block's presence bits
     auto kern = a.k == 3 ? k_profile<3> : a.k == 6 ? k_profile<6> : k_profile<0>;
     smem_optin(kern, 200 * 1024);
     int dev = 0, sms = 148;
@@ -651,47 +719,54 @@ __global__ void __cluster_dims__(kPlanCtas, 1, 1) __launch_bounds__(kScanThreads
         if ((threadIdx.x & 31) == 0 && v) atomicAdd(&red[j], v);
     }
     cluster.sync();                                   // every CTA's partials (and M folds) are in place
-    if (c == 0 && threadIdx.x == 0) {                 // (2) in the leader
-        unsigned long long tot[NV] = {};
-        for (unsigned r = 0; r < kPlanCtas; ++r) {
-            const unsigned long long *rr = cluster.map_shared_rank(red, r);
+    // (2) in every CTA (the same decision everywhere; no broadcast): thread j < NV sums partial j
+    // over the cluster, thread 0 decides; only the leader writes the results
+    __shared__ unsigned long long tot[NV];
+    if (threadIdx.x < NV) {
+        unsigned long long v = 0;
 #pragma unroll
-            for (int j = 0; j < NV; ++j) tot[j] += rr[j];
-        }
-        ki[2] = tot[kNumCaps];
-        for (int j = 0; j < kNumCaps; ++j) {
-            ki[8 + j] = tot[j];
-            ki[12 + j] = tot[kNumCaps + 1 + j];
-            ki[16 + j] = tot[2 * kNumCaps + 1 + j];
-        }
-        unsigned long long K = ki[2];
+        for (unsigned r = 0; r < kPlanCtas; ++r) v += cluster.map_shared_rank(red, r)[threadIdx.x];
+        tot[threadIdx.x] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long Knc = tot[kNumCaps];
+        unsigned long long K = Knc;
         uint32_t T = kNoCap, sel = (uint32_t)kNumCaps;
         if (allow_cap)
             for (int j = 0; j < kNumCaps; ++j)
                 if (ki[4 + j] <= 255ull) {
                     T = 1u << j;
-                    K = ki[8 + j];
+                    K = tot[j];
                     if (ki[4 + j] > 0) sel = (uint32_t)j;    // the shard has entries above its cap
                     break;
                 }
-        cap[s] = T;
-        xsel[s] = sel;
-        ident[s] = (T == 1u && K == (unsigned long long)V) ? 1u : 0u;   // col0(tau) = tau
-        int64_t kb = (int64_t)((K + (unsigned long long)kcpb - 1) / (unsigned long long)kcpb);
-        if (kb < 1) kb = 1;
-        if (kb > kcap_blocks) {                                          // operand too narrow: flagged
-            atomicOr(&status[0], 1ull);
-            kb = kcap_blocks;
-        }
-        kblocks[s] = kb;
-        ki[20] = K;
-        ki[21] = T;
-        atomicMax(&status[1], K);
         s_T = T;
         s_sel = sel;
+        if (c == 0) {
+            ki[2] = Knc;
+            for (int j = 0; j < kNumCaps; ++j) {
+                ki[8 + j] = tot[j];
+                ki[12 + j] = tot[kNumCaps + 1 + j];
+                ki[16 + j] = tot[2 * kNumCaps + 1 + j];
+            }
+            cap[s] = T;
+            xsel[s] = sel;
+            ident[s] = (T == 1u && K == (unsigned long long)V) ? 1u : 0u;   // col0(tau) = tau
+            int64_t kb = (int64_t)((K + (unsigned long long)kcpb - 1) / (unsigned long long)kcpb);
+            if (kb < 1) kb = 1;
+            if (kb > kcap_blocks) {                                          // operand too narrow: flagged
+                atomicOr(&status[0], 1ull);
+                kb = kcap_blocks;
+            }
+            kblocks[s] = kb;
+            ki[20] = K;
+            ki[21] = T;
+            atomicMax(&status[1], K);
+        }
     }
-    cluster.sync();
-    const uint32_t T = *cluster.map_shared_rank(&s_T, 0), sel = *cluster.map_shared_rank(&s_sel, 0);
+    __syncthreads();
+    const uint32_t T = s_T, sel = s_sel;
     // (3) and (4) in one scan: every thread owns a contiguous chunk of its CTA's k-mers and scans
     // the pair (min(M, T_s), X_{T_s}) packed in one u64 (col0 high, list offsets low: a shard's list
     // entries are < 2^32, the u32 offsets' own bound); CTA totals are carried across the cluster
@@ -722,19 +797,28 @@ __global__ void __cluster_dims__(kPlanCtas, 1, 1) __launch_bounds__(kScanThreads
     if (c == 0 && threadIdx.x == 0) xtot[s] = x ? (unsigned long long)(uint32_t)all : 0ull;
     if (lcnt && c == kPlanCtas - 1) {
         // the length order's bin offsets: exclusive scan of the shard's Tw histogram over bins
-        // 0..max Tw (kinfo[3], from K1/K2), offset by the shard's first row
+        // 0..max Tw (kinfo[3], from K1/K2), offset by the shard's first row; kLenItems bins per
+        // thread per block scan (one scan for max Tw < 2048)
         __syncthreads();                              // tmp of the scan above is reused
         const unsigned long long mt = ki[3];
         const int nb = (int)(mt + 1 < (unsigned long long)kLenBinsMax ? mt + 1 : (unsigned long long)kLenBinsMax);
         const uint32_t *lc = lcnt + (size_t)s * kLenBinsMax;
         uint32_t *lp = lpos + (size_t)s * kLenBinsMax;
         unsigned long long lcarry = (unsigned long long)shard_base[s];
-        for (int b0 = 0; b0 < nb; b0 += kScanThreads) {
-            const int b = b0 + (int)threadIdx.x;
-            const unsigned long long v = b < nb ? lc[b] : 0u;
-            unsigned long long e2, a2;
+        constexpr int kLenItems = 4;
+        for (int b0 = 0; b0 < nb; b0 += kScanThreads * kLenItems) {
+            unsigned long long v[kLenItems], e2[kLenItems], a2;
+#pragma unroll
+            for (int u = 0; u < kLenItems; ++u) {
+                const int b = b0 + (int)threadIdx.x * kLenItems + u;
+                v[u] = b < nb ? lc[b] : 0u;
+            }
             Scan(tmp).ExclusiveSum(v, e2, a2);
-            if (b < nb) lp[b] = (uint32_t)(lcarry + e2);
+#pragma unroll
+            for (int u = 0; u < kLenItems; ++u) {
+                const int b = b0 + (int)threadIdx.x * kLenItems + u;
+                if (b < nb) lp[b] = (uint32_t)(lcarry + e2[u]);
+            }
             lcarry += a2;
             __syncthreads();
         }

@@ -118,6 +118,7 @@ void launch_ga_pairs(const RankArgs &a, cudaStream_t st) {
 // exact rational order with index tie-break, reading A9).
 // ---------------------------------------------------------------------------------------
 constexpr int kRankThreads = 256;
+constexpr int kR9 = 12;                 // K9 entry loads per lane in flight
 __global__ void __launch_bounds__(kRankThreads) k_rank_vs_ga(RankArgs a) {
     extern __shared__ uint16_t ga_cnt[];
     __shared__ unsigned long long U[256];
@@ -156,7 +157,8 @@ __global__ void __launch_bounds__(kRankThreads) k_rank_vs_ga(RankArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)gridDim.x * (kRankThreads / 32);
     // the next sequence's CSR position and entry count are loaded during the current one, and
-    // each lane issues its entry loads four at a time (one round trip per 128 entries)
+    // each lane issues its entry loads kR9 at a time (one round trip per 32 kR9 entries: a
+    // config-4 row, d ~ 290, in one)
     int64_t i = (int64_t)blockIdx.x * (kRankThreads / 32) + (threadIdx.x >> 5);
     int64_t off_n = i < a.n ? a.off[i] : 0;
     int d_n = i < a.n ? a.dcnt[i] : 0;
@@ -170,15 +172,15 @@ __global__ void __launch_bounds__(kRankThreads) k_rank_vs_ga(RankArgs a) {
         }
         const RowInfo ri = a.rowinfo[i];
         uint32_t s = 0;
-        for (int e0 = 0; e0 < d; e0 += 128) {
-            uint32_t v[4];
+        for (int e0 = 0; e0 < d; e0 += 32 * kR9) {
+            uint32_t v[kR9];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kR9; ++u) {
                 const int e = e0 + u * 32 + lane;
                 v[u] = e < d ? ent[e] : 0u;        // (tau 0, count 0) adds nothing
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) s += min(v[u] & 0xFFFFu, (uint32_t)ga_cnt[v[u] >> 16]);
+            for (int u = 0; u < kR9; ++u) s += min(v[u] & 0xFFFFu, (uint32_t)ga_cnt[v[u] >> 16]);
         }
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) {
@@ -411,16 +413,22 @@ void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *
 // the number of keys smaller than it: its position in its own run plus a lower_bound in every
 // other run.
 __global__ void __launch_bounds__(256) k_rank_merge(MergeArgs a) {
-    __shared__ int64_t rs[65];
-    for (int r = threadIdx.x; r <= a.nr; r += blockDim.x) rs[r] = a.run_start[r];
+    __shared__ int64_t rs[65], cs[65];
+    for (int r = threadIdx.x; r <= a.nr; r += blockDim.x) {
+        rs[r] = a.run_start[r];
+        cs[r] = a.cpre[a.run_start[r]];
+    }
     __syncthreads();
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < a.n; t += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long kt = a.keys[t * a.kstride];
-        int64_t pos = 0;
+        // output slot = sum over the runs of the element's rank in each (its own run: its index
+        // there); its residue offset = the lengths of those preceding elements (run-local prefixes)
+        int64_t pos = 0, res = 0;
         for (int r = 0; r < a.nr; ++r) {
             int64_t lo = rs[r], hi = rs[r + 1];
             if (t >= lo && t < hi) {
                 pos += t - lo;
+                res += a.cpre[t] - cs[r];
                 continue;
             }
             const int64_t base = lo;
@@ -429,11 +437,14 @@ __global__ void __launch_bounds__(256) k_rank_merge(MergeArgs a) {
                 if (a.keys[mid * a.kstride] < kt) lo = mid + 1; else hi = mid;
             }
             pos += lo - base;
+            res += a.cpre[lo] - cs[r];
         }
         const int64_t L = a.lens ? (int64_t)a.lens[t * a.lstride] : (int64_t)a.rowinfo[a.perm[t]].tw + a.k - 1;
         a.out_key[pos] = kt;
         a.out_len[pos] = L;
         a.out_src[pos] = (int32_t)t;
+        a.out_off[pos] = res;
+        if (pos == a.n - 1) a.out_off[a.n] = res + L;
     }
 }
 

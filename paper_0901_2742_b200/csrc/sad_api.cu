@@ -855,9 +855,13 @@ int sad_build_profiles(sad_ctx *ctx) {
                         ctx->d_rinfo_s, ctx->st);
         LAUNCHED();
     } else if (ctx->use_tc) {     // the length order's slot scatter (histogram: K1/K2, bin offsets: K3)
-        launch_lenorder(ctx->d_rowinfo, ctx->d_shard_base, pl, ctx->n, ctx->d_lcnt + (size_t)pl * kLenBinsMax,
-                        ctx->d_sigma, ctx->d_sigma_inv, ctx->d_rinfo_s, ctx->st);
-        LAUNCHED();
+        if (ctx->allow_cap) {     // fused with the K6 list fill in sad_rank (or alone there if no shard is capped)
+            ctx->lenorder_deferred = true;
+        } else {
+            launch_lenorder(ctx->d_rowinfo, ctx->d_shard_base, pl, ctx->n, ctx->d_lcnt + (size_t)pl * kLenBinsMax,
+                            ctx->d_sigma, ctx->d_sigma_inv, ctx->d_rinfo_s, ctx->st);
+            LAUNCHED();
+        }
     }
     // the statistics go to pinned host memory; read at the step's first synchronizing call
     CK(cudaMemcpyAsync(ctx->h_stats, ctx->d_err, sizeof(unsigned long long) * (8 + (size_t)pl * kKinfo),
@@ -944,6 +948,17 @@ static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, 
     uint8_t *E = xl_b ? reinterpret_cast<uint8_t *>(d_operand) + op_b + xl_b : nullptr;
     unsigned long long *xtot = xtot_of(ctx);
     record_pair(ctx, ctx->ev_pairs_op, true, 0);
+    uint32_t *lpos = nullptr;     // the deferred length order (fused into k_xfill when it runs)
+    if (ctx->lenorder_deferred) {
+        ctx->lenorder_deferred = false;
+        lpos = ctx->d_lcnt + (size_t)pl * kLenBinsMax;
+        if (!lists) {
+            launch_lenorder(ctx->d_rowinfo, ctx->d_shard_base, pl, ctx->n, lpos, ctx->d_sigma, ctx->d_sigma_inv,
+                            ctx->d_rinfo_s, ctx->st);
+            LAUNCHED();
+            lpos = nullptr;
+        }
+    }
     if (ctx->use_tc) {
         // K3 ran in sad_build_profiles (layer caps, column maps, K6 list offsets); the K6 lists,
         // then K6 rows on the side stream beside K4
@@ -979,7 +994,7 @@ static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, 
             x.rb_own = ctx->tile_world > 1 ? ctx->d_rb_own : nullptr;
             x.shard_rowpad = ctx->d_shard_rowpad;
             x.rb_rows = 128;
-            launch_xfill(x, ctx->d_xcur, ctx->st);
+            launch_xfill(x, ctx->d_xcur, lpos, ctx->d_sigma, ctx->d_sigma_inv, ctx->d_rinfo_s, ctx->st);
             LAUNCHED();
             // K6 rows on the side stream, concurrently with K4 (both only read the CSR / lists)
             CK(cudaEventRecord(ctx->ev_fork, ctx->st));
@@ -1416,6 +1431,7 @@ static int finish_impl(sad_ctx *ctx, const int64_t *h_counts_all, const uint64_t
         m.nr = ctx->pl;
         m.perm = ctx->d_perm_sorted;
         m.rowinfo = ctx->d_rowinfo;
+        m.cpre = ctx->d_lpre;                     // exclusive prefix of L in sorted order (rank_global)
         src_off = ctx->d_off;
         src_perm = ctx->d_perm_sorted;
         src_res = ctx->d_ascii;
@@ -1438,21 +1454,21 @@ static int finish_impl(sad_ctx *ctx, const int64_t *h_counts_all, const uint64_t
         m.nr = p;
         launch_lens_recv(reinterpret_cast<const unsigned long long *>(d_recv_meta), n_out, o.len_sorted, ctx->st);
         LAUNCHED();
-        if (n_out > 0) {
+        CK(cudaMemsetAsync(o.src_off, 0, sizeof(int64_t), ctx->st));
+        if (n_out > 0) {                          // [n + 1] exclusive prefix of the received lengths
             size_t tb = o.cub_bytes;
-            CK(cub::DeviceScan::ExclusiveSum(o.cub, tb, o.len_sorted, o.src_off, nn, ctx->st));
+            CK(cub::DeviceScan::InclusiveSum(o.cub, tb, o.len_sorted, o.src_off + 1, nn, ctx->st));
             LAUNCHED();
         }
+        m.cpre = o.src_off;
         src_off = o.src_off;
         src_perm = nullptr;
         src_res = d_recv_res;
     }
-    CK(cudaMemsetAsync(o.off, 0, sizeof(int64_t), ctx->st));
+    m.out_off = o.off;
+    if (n_out == 0) CK(cudaMemsetAsync(o.off, 0, sizeof(int64_t), ctx->st));
     if (n_out > 0) {
-        launch_rank_merge(m, ctx->st);
-        LAUNCHED();
-        size_t tb = o.cub_bytes;
-        CK(cub::DeviceScan::InclusiveSum(o.cub, tb, o.len_in, o.off + 1, nn, ctx->st));
+        launch_rank_merge(m, ctx->st);         // keys, lengths, sources and residue offsets
         LAUNCHED();
         launch_gather_res(o.perm, src_perm, n_out, src_off, src_res, o.off, o.res, ctx->st);
         LAUNCHED();

@@ -176,7 +176,9 @@ struct ExcessArgs {
     const int64_t *ebase;            // device [pl+1] per shard byte offset of E_s
 };
 int launch_excess(const ExcessArgs &a, cudaStream_t st);
-void launch_xfill(const ExcessArgs &a, uint32_t *xcur, cudaStream_t st);   // K6 lists (before launch_excess)
+// K6 lists (before launch_excess); lpos != NULL: the length order's scatter fused in (see k_excess.cu)
+void launch_xfill(const ExcessArgs &a, uint32_t *xcur, uint32_t *lpos, int32_t *sigma, int32_t *sigma_inv,
+                  RowInfo *rinfo_s, cudaStream_t st);
 void launch_dense_counts(const OperandArgs &a, cudaStream_t st);
 
 struct AllPairsArgs {
@@ -306,6 +308,10 @@ struct MergeArgs {
     unsigned long long *out_key;     // [n]
     int64_t *out_len;                // [n]
     int32_t *out_src;                // [n] element index t of each output slot
+    // [n + 1] exclusive prefix of the element lengths over the concatenated runs: the output
+    // residue offsets out_off[n + 1] follow from every element's rank in every run (no scan)
+    const int64_t *cpre;
+    int64_t *out_off;
 };
 void launch_rank_merge(const MergeArgs &a, cudaStream_t st);
 // residues: dst_res[dst_off[r] ...] = src_res[src_off(out_src[r]) ...]; src_off(t) = src_off[perm ? perm[t] : t]
@@ -515,7 +521,8 @@ struct sad_ctx {
     unsigned long long *d_send_meta = nullptr;
     uint8_t *d_send_res = nullptr;
     bool capturing = false;                          // the stream is being captured into a CUDA graph
-    bool t_used = false;                             // T accumulated since K1/K2 last zeroed it
+    bool t_used = false;
+    bool lenorder_deferred = false;                  // the length order's scatter runs fused with K6's lists                             // T accumulated since K1/K2 last zeroed it
     cudaEvent_t gev[4] = {};                         // stage events recorded inside a captured step
     bool graph_events = false;
     bool out_recv_layout = false;                    // the output buffer holds the receive buffers too
