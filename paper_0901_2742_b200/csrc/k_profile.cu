@@ -145,18 +145,8 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         for (int j = 0; j < kNumCaps; ++j) exm[j] = 0;
     };
     const int SW = kCodeSeg - (k - 1);   // windows per segment
-    // the warp's offsets, 32 sequences at a time in the lanes' registers with the next 32 already
-    // loaded (off[ob + d] = lane d of ochunk, d < 32, else of onext): no offset load on the
-    // per-sequence path; the next sequence's first 512 residue bytes are loaded during the current one
-    int64_t ob = i0;
-    int64_t ochunk = i0 + lane <= i1 ? a.off[i0 + lane] : 0;
-    int64_t onext = i0 + 32 + lane <= i1 ? a.off[i0 + 32 + lane] : 0;
-    auto offat = [&](int64_t q) -> int64_t {             // q in [ob, ob + 64); warp-uniform
-        const int d = (int)(q - ob);
-        const int64_t v0 = __shfl_sync(0xffffffffu, ochunk, d & 31), v1 = __shfl_sync(0xffffffffu, onext, d & 31);
-        return d < 32 ? v0 : v1;
-    };
-    int64_t off_c = i0 < i1 ? offat(i0) : 0, off_e = i0 < i1 ? offat(i0 + 1) : 0;
+    // the next sequence's offsets and first 512 residue bytes are loaded during the current one
+    int64_t off_c = i0 < i1 ? a.off[i0] : 0, off_e = i0 < i1 ? a.off[i0 + 1] : 0;
     uint4 qpre = i0 < i1 ? *reinterpret_cast<const uint4 *>(a.ascii + ((off_c & ~int64_t(15)) + 16 * lane))
                          : make_uint4(0, 0, 0, 0);
     int64_t s_end = a.shard_base[s + 1];                       // end of the current shard
@@ -171,14 +161,9 @@ __global__ void __launch_bounds__(kProfWarps * 32, SAD_PROF_MINB) k_profile(Prof
         const int64_t off0 = off_c;
         const int64_t L = off_e - off0;
         const uint4 qfirst = qpre;                             // residues [off0 & ~15, +512) of this lane
-        if (i + 2 - ob >= 32) {                              // slide the offset window by 32
-            ob += 32;
-            ochunk = onext;
-            onext = ob + 32 + lane <= i1 ? a.off[ob + 32 + lane] : 0;
-        }
         if (i + 1 < i1) {
             off_c = off_e;
-            off_e = offat(i + 2);
+            off_e = a.off[i + 2];
             qpre = *reinterpret_cast<const uint4 *>(a.ascii + ((off_c & ~int64_t(15)) + 16 * lane));
         }
         const uint8_t *x = a.ascii + off0;

@@ -6,7 +6,10 @@ G-GPU job this runs the same profile, operand and all-pairs work; its partition 
 instead of p (a smaller plan, a merge of p/G local runs instead of p received runs). The exchange
 steps the real rank adds (not measurable with one GPU) are added as a stated estimate.
 
-    python tools/rank_share.py [G ...]     (GPU box) -> one line per G
+    python tools/rank_share.py [G ...]     (GPU box) -> one line per G (config 4, p = 8)
+    python tools/rank_share.py --cfg C [--p P | --p-eq-g] [G ...]
+        another config; --p-eq-g: p = G buckets at every G (config 3's layout: one shard per GPU),
+        projected throughput = the whole job's within-shard pairs / rank 0's step
 """
 import os
 import sys
@@ -25,10 +28,15 @@ from synth import gen  # noqa: E402
 EXCHANGE_EST_MS = 0.072
 
 
-def one(G: int, steps: int = 20, warmup: int = 3):
-    spec = gen.SPECS[4]
-    a, o = gen.generate(spec)
-    n, p = len(o) - 1, 8
+_DATA = {}
+
+
+def one(G: int, steps: int = 20, warmup: int = 3, cfg: int = 4, p: int = 8):
+    spec = gen.SPECS[cfg]
+    if cfg not in _DATA:
+        _DATA[cfg] = gen.generate(spec)
+    a, o = _DATA[cfg]
+    n = len(o) - 1
     pl = p // G
     sb = gen.shard_bounds(n, p)
     lo, hi = sb[0], sb[pl]
@@ -57,21 +65,37 @@ def one(G: int, steps: int = 20, warmup: int = 3):
     ap = stt["allpairs_ms_total"] / max(stt["calls"], 1)
     op = stt["operand_ms_total"] / max(stt["calls"], 1)
     ctx.close()
-    return float(np.median(ms)), ap, op, hi - lo
+    pairs = sum((sb[s + 1] - sb[s]) * (sb[s + 1] - sb[s] - 1) // 2 for s in range(p))   # the whole job's
+    return float(np.median(ms)), ap, op, hi - lo, pairs
 
 
 def main():
-    Gs = [int(x) for x in sys.argv[1:]] or [1, 2, 4, 8]
+    args = sys.argv[1:]
+    cfg, p, p_eq_g = 4, 8, False
+    if "--cfg" in args:
+        i = args.index("--cfg")
+        cfg = int(args[i + 1])
+        del args[i: i + 2]
+    if "--p" in args:
+        i = args.index("--p")
+        p = int(args[i + 1])
+        del args[i: i + 2]
+    if "--p-eq-g" in args:
+        args.remove("--p-eq-g")
+        p_eq_g = True
+    Gs = [int(x) for x in args] or [1, 2, 4, 8]
     base = None
     for G in Gs:
-        dev_ms, ap, op, w = one(G)
+        pG = G if p_eq_g else p
+        dev_ms, ap, op, w, pairs = one(G, cfg=cfg, p=pG)
         if G == 1:
             base = dev_ms
         proj = dev_ms + (EXCHANGE_EST_MS if G > 1 else 0.0)
-        eff = f" projected E({G}) = {base / (G * proj):.2f}" if base and G > 1 else ""
-        print(f"G={G}: virtual rank 0 ({w} sequences, {8 // G} shard(s)) graph-replayed step {dev_ms:.3f} ms"
-              f" (all-pairs kernel {ap:.3f}, operand stage {op:.3f}; rest {dev_ms - ap - op:.3f})"
-              f" + {EXCHANGE_EST_MS if G > 1 else 0:.3f} ms exchange estimate = {proj:.3f} ms{eff}", flush=True)
+        eff = f" projected E({G}) = {base / (G * proj):.2f}" if base and G > 1 and not p_eq_g else ""
+        print(f"cfg{cfg} G={G} p={pG}: virtual rank 0 ({w} sequences, {pG // G} shard(s)) graph-replayed step"
+              f" {dev_ms:.3f} ms (all-pairs kernel {ap:.3f}, operand stage {op:.3f}; rest {dev_ms - ap - op:.3f})"
+              f" + {EXCHANGE_EST_MS if G > 1 else 0:.3f} ms exchange estimate = {proj:.3f} ms;"
+              f" projected {pairs / (proj * 1e-3):.3e} pairs/s{eff}", flush=True)
 
 
 if __name__ == "__main__":
