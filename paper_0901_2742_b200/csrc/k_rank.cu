@@ -409,6 +409,98 @@ void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *
                                                    len_sorted, (1ull << qbits) - 1ull, ibits);
 }
 
+// The same unpack with the exclusive prefix of L in sorted order (lpre[0..n], the residue offsets
+// of every bucket slice) in the same pass: one tile of kUnpTile keys per block and a single-pass
+// scan with decoupled look-back (each tile publishes its aggregate, then its inclusive prefix,
+// in a status word tagged with the call's epoch, so no reset launch is needed between calls; the
+// last block to finish advances the epoch). Replaces the unpack + the two-kernel device scan.
+constexpr int kUnpThreads = 256, kUnpItems = 2, kUnpTile = kUnpThreads * kUnpItems;
+constexpr unsigned long long kStVal = (1ull << 46) - 1ull;
+__global__ void __launch_bounds__(kUnpThreads) k_unpack_scan(const unsigned long long *ck, const int32_t *perm_sorted,
+                                                             int64_t n, int64_t first_idx, unsigned long long *key_sorted,
+                                                             const RowInfo *rowinfo, int k, int64_t *len_sorted,
+                                                             unsigned long long qmask, int ibits, int64_t *lpre,
+                                                             uint32_t *sstate, unsigned long long *status) {
+    typedef cub::BlockScan<long long, kUnpThreads> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ long long s_before;
+    __shared__ uint32_t s_epoch;
+    const int tile = blockIdx.x;
+    if (threadIdx.x == 0) s_epoch = __ldcg(&sstate[0]);
+    const int64_t t0 = (int64_t)tile * kUnpTile + (int64_t)threadIdx.x * kUnpItems;
+    long long Ls[kUnpItems];
+    long long tsum = 0;
+#pragma unroll
+    for (int u = 0; u < kUnpItems; ++u) {
+        const int64_t t = t0 + u;
+        Ls[u] = 0;
+        if (t < n) {
+            const unsigned long long q32 = ck[t] & qmask;
+            const unsigned long long q = (qmask == 0xFFFFFFFFull && q32 == 0xFFFFFFFFull) ? (1ull << 32) : q32;
+            const int32_t row = perm_sorted[t];
+            key_sorted[t] = (q << ibits) + (unsigned long long)(first_idx + row);
+            Ls[u] = (long long)rowinfo[row].tw + k - 1;
+            len_sorted[t] = Ls[u];
+        }
+        tsum += Ls[u];
+    }
+    long long excl, agg;
+    Scan(tmp).ExclusiveSum(tsum, excl, agg);
+    if (threadIdx.x == 0) {
+        const unsigned long long tag = (unsigned long long)((s_epoch & 0x7FFFu) | 0x8000u) << 48;
+        volatile unsigned long long *vs = status;
+        long long before = 0;
+        if (tile == 0) {
+            vs[0] = tag | (2ull << 46) | (unsigned long long)agg;                  // inclusive prefix
+        } else {
+            vs[tile] = tag | (1ull << 46) | (unsigned long long)agg;               // aggregate only
+            __threadfence();
+            for (int pr = tile - 1; pr >= 0; --pr) {
+                unsigned long long st;
+                do {
+                    st = vs[pr];
+                } while ((st & ~((3ull << 46) | kStVal)) != tag);
+                before += (long long)(st & kStVal);
+                if (((st >> 46) & 3ull) == 2ull) break;                            // a prefix: done
+            }
+            __threadfence();
+            vs[tile] = tag | (2ull << 46) | (unsigned long long)(before + agg);
+        }
+        s_before = before;
+        if (tile == 0) lpre[0] = 0;
+    }
+    __syncthreads();
+    long long run = s_before + excl;
+#pragma unroll
+    for (int u = 0; u < kUnpItems; ++u) {
+        const int64_t t = t0 + u;
+        run += Ls[u];
+        if (t < n) lpre[t + 1] = run;
+    }
+    if (threadIdx.x == 0) {                  // the last block to finish advances the epoch
+        __threadfence();
+        if (atomicAdd(&sstate[1], 1u) == gridDim.x - 1) {
+            sstate[1] = 0u;
+            sstate[0] = s_epoch + 1u;
+        }
+    }
+}
+
+void launch_unpack_scan(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, int64_t n, int64_t first_idx,
+                        unsigned long long *key_sorted, const RowInfo *rowinfo, int k, int64_t *len_sorted, int qbits,
+                        int ibits, int64_t *lpre, uint32_t *sstate, unsigned long long *status, cudaStream_t st) {
+    const int64_t tiles = (n + kUnpTile - 1) / kUnpTile;
+    if (tiles <= 0) {
+        cudaMemsetAsync(lpre, 0, sizeof(int64_t), st);
+        return;
+    }
+    k_unpack_scan<<<(unsigned)tiles, kUnpThreads, 0, st>>>(ckey_sorted, perm_sorted, n, first_idx, key_sorted, rowinfo,
+                                                           k, len_sorted, (1ull << qbits) - 1ull, ibits, lpre, sstate,
+                                                           status);
+}
+
+int64_t unpack_scan_tiles(int64_t n) { return (n + kUnpTile - 1) / kUnpTile; }
+
 // K14: merge by ranking. Keys are unique, every run is sorted, so the output slot of an element is
 // the number of keys smaller than it: its position in its own run plus a lower_bound in every
 // other run.

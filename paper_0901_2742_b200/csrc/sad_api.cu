@@ -189,6 +189,8 @@ size_t carve(sad_ctx *c, uint8_t *base, int64_t n, int64_t R) {
     c->d_bnd = b.take<int64_t>((size_t)pl * p);
     c->d_lpre = b.take<int64_t>((size_t)n + pl + 1);
     c->d_len_sorted = b.take<int64_t>((size_t)n);
+    c->d_scan_state = b.take<uint32_t>(4);
+    c->d_scan_status = b.take<unsigned long long>((size_t)unpack_scan_tiles(n) + 1);
     c->d_seg = b.take<int64_t>((size_t)pl * p * 2);
     c->d_counts = b.take<int64_t>((size_t)pl * p * 2);
     c->tc_tiles_cap = tc_tiles_bound(n, pl);
@@ -734,6 +736,10 @@ int sad_load(sad_ctx *ctx, const uint8_t *ascii, const int64_t *offsets, int64_t
         CK(cudaMemcpyAsync(ctx->d_sim_base, tbl + 2 * (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_tile_base, tbl + 3 * (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_ebase, tbl + 4 * (ctx->pl + 1), tb, cudaMemcpyHostToDevice, ctx->st));
+        // the single-pass scan's epoch and tile status words start from zero in a fresh layout
+        CK(cudaMemsetAsync(ctx->d_scan_state, 0, 16, ctx->st));
+        CK(cudaMemsetAsync(ctx->d_scan_status, 0, sizeof(unsigned long long) * (size_t)(unpack_scan_tiles(n_local) + 1),
+                           ctx->st));
         ctx->tbl_ws = base;
         ctx->tbl_n = n_local;
         ctx->tbl_ng = n_global;
@@ -1196,16 +1202,12 @@ static int rank_global_impl(sad_ctx *ctx, const void *d_anc_all, uint64_t *d_sam
         CK(sort_pairs(ctx, ctx->d_ckey, ctx->d_ckey_sorted, ctx->d_perm_in, ctx->d_perm_sorted, (int)ctx->n,
                       qbits + sbits));
     LAUNCHED();
-    launch_unpack_sorted(ctx->d_ckey_sorted, ctx->d_perm_sorted, ctx->n, ctx->first_idx, ctx->d_key_sorted,
-                         ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, qbits, ctx->ibits, ctx->st);
+    // the real keys, and the exclusive prefix of L in sorted order (the residue offsets of every
+    // bucket slice, K12/K13/K14) in the same single-pass launch
+    launch_unpack_scan(ctx->d_ckey_sorted, ctx->d_perm_sorted, ctx->n, ctx->first_idx, ctx->d_key_sorted,
+                       ctx->d_rowinfo, ctx->cfg.k, ctx->d_len_sorted, qbits, ctx->ibits, ctx->d_lpre,
+                       ctx->d_scan_state, ctx->d_scan_status, ctx->st);
     LAUNCHED();
-    // exclusive prefix of L in sorted order (the residue offsets of every bucket slice, K12/K13)
-    CK(cudaMemsetAsync(ctx->d_lpre, 0, sizeof(int64_t), ctx->st));
-    {
-        size_t tb2 = ctx->cub_bytes;
-        CK(cub::DeviceScan::InclusiveSum(ctx->d_cub, tb2, ctx->d_len_sorted, ctx->d_lpre + 1, (int)ctx->n, ctx->st));
-        LAUNCHED();
-    }
     if (p > 1) {
         launch_samples(ctx->d_key_sorted, ctx->d_shard_base, ctx->pl, p,
                        reinterpret_cast<unsigned long long *>(d_samples_out), ctx->st);

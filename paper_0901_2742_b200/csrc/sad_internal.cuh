@@ -255,6 +255,12 @@ void launch_rank_vs_ga(const RankArgs &a, cudaStream_t st);
 
 void launch_samples(const unsigned long long *key_sorted, const int64_t *shard_base, int pl, int p,
                     unsigned long long *samples_out, cudaStream_t st);
+// unpack + the exclusive prefix of L in sorted order in one single-pass launch (lpre[0..n]);
+// sstate[2] (epoch, done counter) and status[unpack_scan_tiles(n)] zeroed when the layout is new
+void launch_unpack_scan(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, int64_t n, int64_t first_idx,
+                        unsigned long long *key_sorted, const RowInfo *rowinfo, int k, int64_t *len_sorted, int qbits,
+                        int ibits, int64_t *lpre, uint32_t *sstate, unsigned long long *status, cudaStream_t st);
+int64_t unpack_scan_tiles(int64_t n);
 void launch_unpack_sorted(const unsigned long long *ckey_sorted, const int32_t *perm_sorted, int64_t n,
                           int64_t first_idx, unsigned long long *key_sorted, const RowInfo *rowinfo, int k,
                           int64_t *len_sorted, int qbits, int ibits, cudaStream_t st);
@@ -477,6 +483,8 @@ struct sad_ctx {
     unsigned long long *d_pivots = nullptr;
     int64_t *d_bnd = nullptr, *d_lpre = nullptr, *d_seg = nullptr, *d_counts = nullptr;
     int64_t *d_len_sorted = nullptr;  // [n] L of each sequence in sorted order (scanned into d_lpre)
+    uint32_t *d_scan_state = nullptr;            // k_unpack_scan: epoch, done counter
+    unsigned long long *d_scan_status = nullptr; // k_unpack_scan: per-tile look-back status
     bool counts_pending = false;
     void *d_tmap = nullptr;
     void *d_cub = nullptr;
