@@ -940,13 +940,116 @@ __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int 
     }
 }
 
+// K4 for long rows (average Tw >= kWideTw, e.g. config 5's ~1.3k entries and 13 KB per row): one
+// block per row instead of one warp, so a row's entries are one or two loads per thread and the
+// block holds a single row slice in shared memory (up to 8 blocks per SM instead of 8 warps): the
+// warp-per-row kernel left config 5 latency-bound at 10 % occupancy (0.20 ms for 130 MB). The next
+// row's metadata and first entries are fetched during the current row.
+constexpr int kWideTw = 1024;
+__global__ void __launch_bounds__(kOpThreads) k_indicator_blk(OperandArgs a, int slice) {
+    extern __shared__ __align__(16) uint8_t opsm[];
+    uint32_t *row32 = reinterpret_cast<uint32_t *>(opsm);
+    uint4 *row4 = reinterpret_cast<uint4 *>(opsm);
+    const int tid = threadIdx.x;
+    const uint32_t stride = (uint32_t)a.stride;
+    const uint32_t per_byte = a.fp4 ? 2u : 1u;
+    int s_n = 0, d_n = 0;
+    int64_t eo_n = 0, slot_n = 0;
+    auto meta = [&](int64_t il) {
+        s_n = (int)a.rowinfo[il].shard;
+        eo_n = a.off[il] - il * (int64_t)(a.k - 1);
+        d_n = a.dcnt[il];
+        slot_n = a.shard_rowpad[s_n] + (a.sigma_inv ? a.sigma_inv[il] : il - a.shard_base[s_n]);
+    };
+    int64_t il = blockIdx.x;
+    uint32_t vpre[kOpBatch];
+#pragma unroll
+    for (int b = 0; b < kOpBatch; ++b) vpre[b] = 0u;
+    if (il < a.n) {
+        meta(il);
+#pragma unroll
+        for (int b = 0; b < kOpBatch; ++b) {
+            const int e = b * kOpThreads + tid;
+            vpre[b] = e < d_n ? a.csr[eo_n + e] : 0u;
+        }
+    }
+    for (; il < a.n; il += gridDim.x) {
+        const int s = s_n, dcur = d_n;
+        const int64_t eo = eo_n, slot = slot_n;
+        const int64_t iln = il + gridDim.x;
+        if (iln < a.n) meta(iln);                    // consumed after this row's last slice
+        const uint32_t *ent = a.csr + eo;
+        const uint32_t *c0 = a.col0 + (size_t)s * a.V;
+        const uint32_t T = a.cap ? a.cap[s] : 0xFFFFFFFFu;
+        const bool ident = a.ident && a.ident[s];
+        uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a.op) + slot * a.stride);
+        const uint32_t rowb = a.kblocks ? min(stride, (uint32_t)a.kblocks[s] * 128u) : stride;
+        bool have_pre = true;
+        for (uint32_t ch = 0; ch < rowb; ch += (uint32_t)slice) {
+            const uint32_t len = min((uint32_t)slice, rowb - ch);
+            // every thread zeroes the vectors it stored for the previous slice (or row): no barrier
+            // is needed between that store and this zeroing
+            for (uint32_t t = tid; t < len / 16; t += kOpThreads) row4[t] = make_uint4(0, 0, 0, 0);
+            __syncthreads();
+            const uint32_t c_lo = ch * per_byte, c_hi = (ch + len) * per_byte;
+            for (int e0 = 0; e0 < dcur; e0 += kOpThreads * kOpBatch) {
+                uint32_t v[kOpBatch], cb[kOpBatch];
+                if (e0 == 0 && have_pre) {
+#pragma unroll
+                    for (int b = 0; b < kOpBatch; ++b) v[b] = vpre[b];
+                } else {
+#pragma unroll
+                    for (int b = 0; b < kOpBatch; ++b) {
+                        const int e = e0 + b * kOpThreads + tid;
+                        v[b] = e < dcur ? ent[e] : 0u;
+                    }
+                }
+#pragma unroll
+                for (int b = 0; b < kOpBatch; ++b)
+                    cb[b] = ident ? (v[b] >> 16) : ((v[b] & 0xFFFFu) ? c0[v[b] >> 16] : 0u);
+#pragma unroll
+                for (int b = 0; b < kOpBatch; ++b) {
+                    const uint32_t n = v[b] & 0xFFFFu;     // 0 for threads past the row's entries
+                    const uint32_t lo = max(cb[b], c_lo), hi = min(cb[b] + min(n, T), c_hi);
+                    for (uint32_t c = lo; c < hi; ++c) {
+                        const uint32_t cc = c - c_lo;
+                        if (a.fp4)
+                            atomicOr(&row32[cc >> 3], 2u << (4 * (cc & 7)));
+                        else
+                            opsm[cc] = 1;
+                    }
+                }
+            }
+            if (ch + (uint32_t)slice >= rowb && iln < a.n) {           // the next row's first batch
+#pragma unroll
+                for (int b = 0; b < kOpBatch; ++b) {
+                    const int e = b * kOpThreads + tid;
+                    vpre[b] = e < d_n ? a.csr[eo_n + e] : 0u;
+                }
+            }
+            have_pre = false;
+            __syncthreads();
+            for (uint32_t t = tid; t < len / 16; t += kOpThreads) dst[ch / 16 + t] = row4[t];
+        }
+    }
+}
+
 void launch_indicator(const OperandArgs &a, cudaStream_t st) {
     const int slice = (int)std::min<int64_t>(a.stride, kRowSlice);
-    const size_t smem = (size_t)kOpWarps * slice;
-    smem_optin(k_indicator, smem);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (a.wide) {
+        const size_t smem = (size_t)slice;
+        smem_optin(k_indicator_blk, (size_t)kRowSlice);
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_indicator_blk, kOpThreads, smem);
+        const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), a.n);
+        if (grid > 0) k_indicator_blk<<<(unsigned)grid, kOpThreads, smem, st>>>(a, slice);
+        return;
+    }
+    const size_t smem = (size_t)kOpWarps * slice;
+    smem_optin(k_indicator, smem);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_indicator, kOpWarps * 32, smem);
 #ifndef SAD_K4_DIV

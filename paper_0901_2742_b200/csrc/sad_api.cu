@@ -948,6 +948,7 @@ static int rank_local_impl(sad_ctx *ctx, void *d_operand, size_t operand_bytes, 
     o.pl = pl;
     o.fp4 = ctx->use_tc && ctx->tc_kind == 1;
     o.op = d_operand;
+    o.wide = ctx->R >= (int64_t)1024 * ctx->n;   // host-known (no read-back): long rows, one block per row
     size_t op_b = 0, xl_b = 0, xe_b = 0, f1_b = 0;
     operand_parts(ctx, op_b, xl_b, xe_b, f1_b);
     uint32_t *lists = xl_b ? reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_operand) + op_b) : nullptr;

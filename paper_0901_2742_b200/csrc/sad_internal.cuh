@@ -138,6 +138,7 @@ struct OperandArgs {
     const RowInfo *rowinfo;          // [n] input order (.shard = local shard)  (K4)
     const int32_t *sigma_inv;        // [n] local index -> length-order slot in its shard, or NULL (K4)
     int64_t n;                       // local sequences (K4)
+    int wide;                        // 1: long rows (average Tw >= 1024): one block per row (k_indicator_blk)
 };
 void launch_indicator(const OperandArgs &a, cudaStream_t st);
 // length order by counting (K3): Tw histogram per shard, per-shard scan up to the max Tw in kinfo[3],
