@@ -915,12 +915,14 @@ __global__ void __launch_bounds__(kOpWarps * 32) k_indicator(OperandArgs a, int 
                     for (int b = 0; b < kOpBatch; ++b) {
                         const uint32_t n = v[b] & 0xFFFFu;     // 0 for lanes past the row's entries
                         const uint32_t lo = max(cb[b], c_lo), hi = min(cb[b] + min(n, T), c_hi);
-                        for (uint32_t c = lo; c < hi; ++c) {
-                            const uint32_t cc = c - c_lo;
-                            if (a.fp4)        // e2m1 1.0 = 0b0010; neighbouring k-mers may share a word
-                                atomicOr(&row32[cc >> 3], 2u << (4 * (cc & 7)));
-                            else
-                                row[cc] = 1;
+                        if (a.fp4) {      // e2m1 1.0 = 0b0010; the run of min(n, T) nibbles one word at a time
+                            for (uint32_t c = lo; c < hi;) {      // (neighbouring k-mers may share a word)
+                                const uint32_t cc = c - c_lo, o = cc & 7u, m = min(hi - c, 8u - o);
+                                atomicOr(&row32[cc >> 3], (0x22222222u >> (4u * (8u - m))) << (4u * o));
+                                c += m;
+                            }
+                        } else {
+                            for (uint32_t c = lo; c < hi; ++c) row[c - c_lo] = 1;
                         }
                     }
                 }
@@ -1011,12 +1013,14 @@ __global__ void __launch_bounds__(kOpThreads) k_indicator_blk(OperandArgs a, int
                 for (int b = 0; b < kOpBatch; ++b) {
                     const uint32_t n = v[b] & 0xFFFFu;     // 0 for threads past the row's entries
                     const uint32_t lo = max(cb[b], c_lo), hi = min(cb[b] + min(n, T), c_hi);
-                    for (uint32_t c = lo; c < hi; ++c) {
-                        const uint32_t cc = c - c_lo;
-                        if (a.fp4)
-                            atomicOr(&row32[cc >> 3], 2u << (4 * (cc & 7)));
-                        else
-                            opsm[cc] = 1;
+                    if (a.fp4) {          // the run of min(n, T) nibbles one word at a time
+                        for (uint32_t c = lo; c < hi;) {
+                            const uint32_t cc = c - c_lo, o = cc & 7u, m = min(hi - c, 8u - o);
+                            atomicOr(&row32[cc >> 3], (0x22222222u >> (4u * (8u - m))) << (4u * o));
+                            c += m;
+                        }
+                    } else {
+                        for (uint32_t c = lo; c < hi; ++c) opsm[c - c_lo] = 1;
                     }
                 }
             }
