@@ -474,6 +474,34 @@ def test_long_k_deep_ring(kernel):
         ctx.close()
 
 
+@pytest.mark.parametrize("kernel", [k for k in KERNELS if k != "alu"])
+def test_wide_rows_several_slices(kernel):
+    """Long rows through the block-per-row K4 (k_indicator_blk: average L - k + 1 >= 1024) with
+    operand rows wider than one 16 KB shared-memory slice: DNA k = 8 (V = 65 536), random and
+    near-duplicate sequences of 2.5-5 kb, so a shard has > 32 768 fp4 columns (two or more slices
+    per row, the row's entries re-read per slice). p = 1 and 2, two steps per context, every
+    output compared element-wise with the oracle."""
+    rng = np.random.default_rng(91)
+    seqs = ["".join(rng.choice(list("ACGT"), int(rng.integers(2500, 5000)))) for _ in range(150)]
+    for _ in range(14):
+        x = list(seqs[int(rng.integers(0, len(seqs)))])
+        for j in rng.integers(0, len(x), len(x) // 25):
+            x[j] = "ACGT"[int(rng.integers(0, 4))]
+        seqs.append("".join(x))
+    seqs = [seqs[i] for i in rng.permutation(len(seqs))]
+    a, o = gen.from_strings(seqs)
+    for p in (1, 2):
+        r = oracle.run(a, o, "dna", 8, p)
+        ctx = _ctx("dna", 8, p, kernel)
+        ctx.load(a, o, len(o) - 1, 0)
+        for step in range(2):
+            sizes = ctx.run()
+            _compare_full(ctx, sizes, r, a, o, p)
+        K = ctx.profile_info()[2]
+        assert int(K.max()) > 32768, K
+        ctx.close()
+
+
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_similarity_near_the_fp32_bound(kernel):
     """S up to 65 535 = the ABI's L - k + 1 bound (SAD_E_TOO_LONG), where the fp32 accumulators
