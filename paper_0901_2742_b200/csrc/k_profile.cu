@@ -550,7 +550,232 @@ void launch_profile_reset(uint32_t *M, size_t nM, uint32_t *Mb, size_t nMb, uint
     k_profile_reset<<<(unsigned)g, 256, 0, st>>>(M, nM, Mb, nMb, Xc, nXc, err4, statkinfo, nsk, lcnt, lcnt ? nl : 0);
 }
 
+// K1/K2 for long sequences (host-known average L >= 1024, e.g. config 5: ~1.7 kb, up to 8.5 kb):
+// one BLOCK per sequence instead of one warp. With a warp per sequence the longest sequence's
+// single-warp time is a floor under the kernel (config 5: 8.5 k windows ~ 170 us of the 227 us, 15 %
+// of the stall samples at the end barrier); here the block's threads share one u16 histogram (no
+// overflow: a count is at most Tw <= 65 535), the owner list is the row's own CSR slots (appended
+// per warp: one ballot and one shared-memory atomic), and the emission, the count >= 2 tail and the
+// statistics are strided over the block. Blocks take contiguous ranges of sequences balanced by
+// residues; totals and presence bits are flushed per block at a shard change and at the end.
+// Same outputs as k_profile (entries unordered within a row).
+constexpr int kBlkThreads = 256;
+constexpr int kBlkSeg = 8192;            // residue codes staged per block
+template <int KT>
+__global__ void __launch_bounds__(kBlkThreads, 4) k_profile_blk(ProfileArgs a) {
+    extern __shared__ __align__(16) uint32_t bsm[];
+    __shared__ uint8_t lut[256];
+    __shared__ uint32_t nl_s, nhi_s, ex_s[kNumCaps];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int t = tid; t < 256; t += kBlkThreads) lut[t] = 255;
+    __syncthreads();
+    if (tid < a.A) lut[(uint8_t)c_alpha[a.alphabet][tid]] = (uint8_t)tid;
+    const int k = KT > 0 ? KT : a.k;
+    const uint32_t A = (uint32_t)a.A;
+    const int V = a.V, VW = (V + 31) / 32;
+    const int hw = (V + 1) / 2;                               // u16 bins, two per word
+    uint32_t *hist = bsm;
+    uint16_t *h16 = reinterpret_cast<uint16_t *>(bsm);
+    uint32_t *bpres = bsm + ((hw + 3) & ~3);
+    uint8_t *cod = reinterpret_cast<uint8_t *>(bpres + ((VW + 3) & ~3));
+    for (int t = tid; t < hw; t += kBlkThreads) hist[t] = 0;
+    for (int t = tid; t < VW; t += kBlkThreads) bpres[t] = 0;
+    __syncthreads();
+    // contiguous ranges of sequences balanced by residues (every warp runs the same search)
+    const int64_t W = gridDim.x, gw = blockIdx.x;
+    const int64_t r0 = a.off[a.i_begin], rr = a.off[a.i_end] - r0;
+    auto first_at = [&](int64_t wq) -> int64_t {
+        if (wq <= 0) return a.i_begin;
+        if (wq >= W) return a.i_end;
+        const int64_t target = r0 + (int64_t)(((__int128)rr * wq) / W);
+        int64_t lo = a.i_begin, hi = a.i_end;
+        if (a.off[lo] >= target) return lo;
+        while (hi - lo > 1) {
+            const int64_t step = (hi - lo + 31) / 32;
+            const int64_t probe = min(hi, lo + (int64_t)(lane + 1) * step);
+            const uint32_t ge = __ballot_sync(0xffffffffu, a.off[probe] >= target);
+            const int f = __ffs(ge) - 1;
+            hi = min(hi, lo + (int64_t)(f + 1) * step);
+            lo = f > 0 ? lo + (int64_t)f * step : lo;
+        }
+        return hi;
+    };
+    const int64_t i0 = first_at(gw), i1 = first_at(gw + 1);
+    int s = 0;
+    while (s + 1 < a.pl && i0 >= a.shard_base[s + 1]) ++s;
+    unsigned long long acc_w = 0, acc_d = 0, max_tw = 0;     // thread 0's totals for shard s
+    uint32_t exm[kNumCaps] = {};
+    auto flush = [&]() {                                      // block-uniform call
+        __syncthreads();
+        for (int t = tid; t < VW; t += kBlkThreads) {
+            const uint32_t b = bpres[t];
+            if (b) {
+                atomicOr(&a.Mb[(size_t)s * VW + t], b);
+                bpres[t] = 0;
+            }
+        }
+        if (tid == 0) {
+            if (acc_w | acc_d) {
+                atomicAdd(&a.kinfo[s * kKinfo + 0], acc_w);
+                atomicAdd(&a.kinfo[s * kKinfo + 1], acc_d);
+                atomicMax(&a.kinfo[s * kKinfo + 3], max_tw);
+            }
+#pragma unroll
+            for (int j = 0; j < kNumCaps; ++j)
+                if (exm[j]) atomicMax(&a.kinfo[s * kKinfo + 4 + j], (unsigned long long)exm[j]);
+        }
+        acc_w = acc_d = max_tw = 0;
+#pragma unroll
+        for (int j = 0; j < kNumCaps; ++j) exm[j] = 0;
+        __syncthreads();
+    };
+    const int SW = kBlkSeg - (k - 1);                         // windows per segment
+    const uint32_t lt = (1u << lane) - 1u;
+    int64_t s_end = a.shard_base[s + 1];
+    for (int64_t i = i0; i < i1; ++i) {
+        if (i >= s_end) {
+            flush();
+            while (s + 1 < a.pl && i >= a.shard_base[s + 1]) ++s;
+            s_end = a.shard_base[s + 1];
+        }
+        const int64_t off0 = a.off[i], L = a.off[i + 1] - off0;
+        const uint8_t *x = a.ascii + off0;
+        const unsigned long long gidx = (unsigned long long)(a.first_idx + i);
+        const int64_t Tw = L - k + 1;
+        if (L < k || Tw > 65535) {                             // readings A19 / SURVEY A.3 precondition
+            for (int64_t t = tid; t < L; t += kBlkThreads)
+                if (lut[x[t]] == 255) atomicMin(&a.err[0], (gidx << 32) | (unsigned long long)t);
+            if (tid == 0) {
+                atomicMin(&a.err[L < k ? 1 : 2], gidx);
+                a.rowinfo[i] = RowInfo{1u, 0xFFFFFFFFu, 1u, (uint32_t)s};
+                if (a.lcnt) atomicAdd(&a.lcnt[(size_t)s * kLenBinsMax + 1], 1u);
+                a.T[i] = 0ull;
+                a.dcnt[i] = 0;
+                a.nhi[i] = 0;
+            }
+            continue;
+        }
+        uint32_t *out = a.csr + (off0 - i * (int64_t)(k - 1));
+        uint32_t *Ms = a.M + (size_t)s * V;
+        uint32_t *xcs = a.Xc + (size_t)s * kNumCaps * V;
+        if (tid == 0) {
+            nl_s = 0;
+            nhi_s = 0;
+        }
+        if (tid < kNumCaps) ex_s[tid] = 0;
+        const int nseg = (int)((Tw + SW - 1) / SW);
+        // pass 1: count every window; a bin's first window appends its k-mer to the owner list
+        for (int g = 0; g < nseg; ++g) {
+            const int64_t q0 = (int64_t)g * SW, q1 = min(L, q0 + SW + k - 1);
+            __syncthreads();                                   // the previous segment's windows are done
+            for (int64_t t = q0 + tid; t < q1; t += kBlkThreads) {
+                uint8_t c = lut[x[t]];
+                if (c == 255) {                                // K1: first bad residue, coded 0
+                    atomicMin(&a.err[0], (gidx << 32) | (unsigned long long)t);
+                    c = 0;
+                }
+                cod[t - q0] = c;
+            }
+            __syncthreads();
+            const int w1 = (int)min((int64_t)SW, Tw - q0);
+            for (int t0 = 0; t0 < w1; t0 += kBlkThreads) {
+                const int t = t0 + tid;
+                bool first = false;
+                uint32_t tau = 0;
+                if (t < w1) {
+                    tau = window_tau<KT>(cod + t, k, A);
+                    const uint32_t sh16 = (tau & 1u) << 4;
+                    first = ((atomicAdd(&hist[tau >> 1], 1u << sh16) >> sh16) & 0xFFFFu) == 0u;
+                }
+                const uint32_t fm = __ballot_sync(0xffffffffu, first);
+                if (fm) {
+                    uint32_t base = 0;
+                    if (lane == __ffs(fm) - 1) base = atomicAdd(&nl_s, (uint32_t)__popc(fm));
+                    base = __shfl_sync(0xffffffffu, base, __ffs(fm) - 1);
+                    if (first) out[base + __popc(fm & lt)] = tau << 16;
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t nl = nl_s;
+        // pass 2: every owner once: its count read and its bin cleared, entry slot = owner index; the
+        // count >= 2 entries repeated in the row's tail [Tw - nhi, Tw) (free: Tw - d >= nhi) with
+        // their statistics (shard maxima, per-cap excess counts and sums)
+        uint32_t ex[kNumCaps] = {};
+        for (uint32_t e0 = 0; e0 < nl; e0 += kBlkThreads) {
+            const uint32_t e = e0 + tid;
+            uint32_t c = 0, tau = 0;
+            if (e < nl) {
+                tau = out[e] >> 16;
+                c = h16[tau];
+                h16[tau] = 0;
+                out[e] = (tau << 16) | c;
+                atomicOr(&bpres[tau >> 5], 1u << (tau & 31));
+            }
+            const uint32_t mh = __ballot_sync(0xffffffffu, c >= 2u);
+            if (mh) {
+                uint32_t base = 0;
+                if (lane == __ffs(mh) - 1) base = atomicAdd(&nhi_s, (uint32_t)__popc(mh));
+                base = __shfl_sync(0xffffffffu, base, __ffs(mh) - 1);
+                if (c >= 2u) {
+                    out[(uint32_t)Tw - 1u - base - __popc(mh & lt)] = (tau << 16) | c;
+                    atomicMax(&Ms[tau], c);
+#pragma unroll
+                    for (int j = 0; j < kNumCaps; ++j)
+                        if (c > (1u << j)) {
+                            ex[j] += c - (1u << j);
+                            atomicAdd(&xcs[(uint32_t)j * (uint32_t)V + tau], 1u);
+                        }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kNumCaps; ++j) {
+            uint32_t v = ex[j];
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0 && v) atomicAdd(&ex_s[j], v);
+        }
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int j = 0; j < kNumCaps; ++j) exm[j] = max(exm[j], ex_s[j]);
+            a.nhi[i] = (int32_t)nhi_s;
+            a.dcnt[i] = (int32_t)nl;
+            const uint32_t tw = (uint32_t)Tw;
+            a.rowinfo[i] = RowInfo{tw, 0xFFFFFFFFu / tw, 0xFFFFFFFFu % tw + 1u, (uint32_t)s};
+            if (a.lcnt) atomicAdd(&a.lcnt[(size_t)s * kLenBinsMax + tw], 1u);
+            a.T[i] = 0ull;
+            acc_w += (unsigned long long)Tw;
+            max_tw = max(max_tw, (unsigned long long)Tw);
+            acc_d += nl;
+        }
+        __syncthreads();                                       // nl_s / nhi_s / ex_s are reset next
+    }
+    flush();
+}
+
+template <int KT>
+static void launch_profile_blk_t(const ProfileArgs &a, cudaStream_t st) {
+    const int VW = (a.V + 31) / 32, hw = (a.V + 1) / 2;
+    const size_t smem = 4 * (size_t)(((hw + 3) & ~3) + ((VW + 3) & ~3)) + kBlkSeg + 16;
+    smem_optin(k_profile_blk<KT>, smem);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_profile_blk<KT>, kBlkThreads, smem);
+    int64_t grid = std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), a.i_end - a.i_begin);
+    if (grid < 1) grid = 1;
+    k_profile_blk<KT><<<(unsigned)grid, kBlkThreads, smem, st>>>(a);
+}
+
 void launch_profile(const ProfileArgs &a, cudaStream_t st) {
+    if (a.blk) {
+        if (a.k == 3) launch_profile_blk_t<3>(a, st);
+        else if (a.k == 6) launch_profile_blk_t<6>(a, st);
+        else launch_profile_blk_t<0>(a, st);
+        return;
+    }
     // V narrow bins, or u16 bins over 1/kWidePasses of the k-mers (the overflow fallback)
     const int narrow = (int)(((int64_t)a.V * kBinBits + 7) / 8);
     const int wide = 2 * ((a.V + kWidePasses - 1) / kWidePasses);

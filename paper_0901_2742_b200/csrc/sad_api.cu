@@ -816,6 +816,7 @@ static int profile_launch(sad_ctx *ctx, int64_t i0, int64_t i1) {
     a.lcnt = ctx->use_tc ? ctx->d_lcnt : nullptr;
     a.i_begin = i0;
     a.i_end = i1;
+    a.blk = ctx->R >= (int64_t)1024 * ctx->n;   // host-known (no read-back): long sequences, one block each
     launch_profile(a, ctx->st);
     LAUNCHED();
     return SAD_OK;

@@ -98,6 +98,7 @@ struct ProfileArgs {
     int32_t *nhi;                    // [n] entries with count >= 2 (repeated in each CSR row's tail)
     unsigned long long *T;           // [n] within-shard rank sums, zeroed here for the all-pairs kernel
     uint32_t *lcnt;                  // [pl][kLenBinsMax] Tw histogram of the length order (zeroed), or NULL
+    int blk;                         // 1: long sequences (average L >= 1024): one block per sequence (k_profile_blk)
 };
 void launch_profile(const ProfileArgs &a, cudaStream_t st);
 // the per-step accumulators of K1/K2 and K3 cleared in one launch: M, Mb, Xc = 0; err = all ones;
