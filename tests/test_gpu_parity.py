@@ -198,6 +198,43 @@ def test_errors():
     assert e.value.name == "SAD_E_INSUFFICIENT"
 
 
+def test_errors_long_sequences():
+    """The same locations through the block-per-sequence K1/K2 (average L >= 1024): the first bad
+    symbol (smallest index, then smallest position, also in a later staged segment), a too-short
+    sequence among long ones, and L - k + 1 > 65 535."""
+    from paper_0901_2742_b200 import SadError
+    rng = np.random.default_rng(5)
+    seqs = ["".join(rng.choice(list("ACGT"), int(rng.integers(3000, 12000)))) for _ in range(12)]
+    bad = list(seqs)
+    x = list(bad[7]); x[9000 % len(x)] = "N"; x[100] = "A"; bad[7] = "".join(x)
+    y = list(bad[3]); pos = len(y) - 2; y[pos] = "J"; bad[3] = "".join(y)       # smaller index wins
+    a, o = gen.from_strings(bad)
+    ctx = _ctx("dna", 6, 2, "tc")
+    ctx.load(a, o, len(bad), 0)
+    with pytest.raises(SadError) as e:
+        ctx.run()
+    assert e.value.name == "SAD_E_SYMBOL" and e.value.location == (3, pos)
+    short = list(seqs); short[5] = "ACG"
+    a, o = gen.from_strings(short)
+    ctx = _ctx("dna", 6, 2, "tc")
+    ctx.load(a, o, len(short), 0)
+    with pytest.raises(SadError) as e:
+        ctx.run()
+    assert e.value.name == "SAD_E_TOO_SHORT" and e.value.location[0] == 5
+    longs = list(seqs); longs[9] = "".join(rng.choice(list("ACGT"), 65535 + 6))  # Tw = 65 536
+    a, o = gen.from_strings(longs)
+    ctx = _ctx("dna", 6, 2, "tc")
+    ctx.load(a, o, len(longs), 0)
+    with pytest.raises(SadError) as e:
+        ctx.run()
+    assert e.value.name == "SAD_E_TOO_LONG" and e.value.location[0] == 9
+    # and the largest legal length (Tw = 65 535: eight staged segments) against the oracle
+    ok = list(seqs); ok[9] = longs[9][:-1]
+    a, o = gen.from_strings(ok)
+    ctx, sizes = _run_gpu(a, o, "dna", 6, 2, "tc")
+    _compare_full(ctx, sizes, oracle.run(a, o, "dna", 6, 2), a, o, 2)
+
+
 @pytest.mark.parametrize("kernel", KERNELS[:1])
 @pytest.mark.parametrize("cfg", [4, 5])
 def test_full_size_sampled(kernel, cfg):
